@@ -1,0 +1,899 @@
+// pcs_capi.cu — extern "C" boundary of libpcsir_b200.so (see include/pcsir_b200.h).
+//
+// Host-side launch logic only; all arithmetic lives in the .cuh device code.
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_run_length_encode.cuh>
+#include <cub/device/device_scan.cuh>
+
+#include "pcs_bin.cuh"
+#include "pcs_common.cuh"
+#include "pcs_lik.cuh"
+#include "pcs_state.cuh"
+#include "pcs_track.cuh"
+#include "pcs_weights.cuh"
+
+using namespace pcs;
+
+static thread_local std::string g_last_error;
+void pcs_set_last_error(const char* msg) { g_last_error = msg ? msg : ""; }
+
+#define PCS_CHECK_ARG(cond, msg)      \
+  do {                                \
+    if (!(cond)) {                    \
+      pcs_set_last_error(msg);        \
+      return PCS_E_INVALID;           \
+    }                                 \
+  } while (0)
+
+#define PCS_LAUNCH_CHECK()                                  \
+  do {                                                      \
+    cudaError_t _e = cudaGetLastError();                    \
+    if (_e != cudaSuccess) {                                \
+      pcs_set_last_error(cudaGetErrorString(_e));           \
+      return PCS_E_CUDA;                                    \
+    }                                                       \
+  } while (0)
+
+static inline cudaStream_t S(void* s) { return (cudaStream_t)s; }
+
+// ---------------------------------------------------------------------------
+// context: device, SM count, grow-only scratch buffers, fused-track state
+// ---------------------------------------------------------------------------
+struct Buf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+struct TrackState {
+  bool active = false;
+  pcs_track_cfg_t cfg{};
+  TrackParams P{};
+  i64 ntiles = 0;
+  u128* tile_tot = nullptr;
+  u128* tile_pre = nullptr;
+  int acc_grid = 0;
+  i64 acc_chunk = 0;
+  int prop_grid = 0;
+  int maxs = 0;
+  i64 k = 0;             // host mirror of the frame counter
+  cudaGraphExec_t exec = nullptr;
+  cudaGraph_t graph = nullptr;
+  int launches = 0;
+};
+
+struct pcs_ctx {
+  int device = 0;
+  int sms = 148;
+  std::vector<Buf> bufs;  // indexed scratch slots
+  cudaStream_t cap = nullptr;
+  TrackState tr;
+  bool table_dirty = false;
+  u32* tab_cnt = nullptr;
+  u64* tab_sum = nullptr;
+  float* wtab = nullptr;
+  u32* occ = nullptr;
+};
+
+enum Slot {
+  SL_NORM = 0,
+  SL_CUB,
+  SL_SORT_KEYS,
+  SL_SORT_IDX,
+  SL_HEAD,
+  SL_INCL,
+  SL_NRUNS,
+  SL_SUMS,
+  SL_TILES,
+  SL_PRE,
+  SL_FLAGS,
+  SL_TR_BUF0,
+  SL_TR_BUF1,
+  SL_TR_ANC,
+  SL_TR_LL,
+  SL_TR_PSLOT,
+  SL_TR_CTL,
+  SL_TR_TILES,
+  SL_TR_PRE,
+  SL_COUNT
+};
+
+static int scratch(pcs_ctx* c, int slot, size_t bytes, void** out) {
+  if (c->bufs.size() < SL_COUNT) c->bufs.resize(SL_COUNT);
+  Buf& b = c->bufs[slot];
+  if (b.bytes < bytes) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    cudaError_t e = cudaMalloc(&b.p, bytes);
+    if (e != cudaSuccess) {
+      pcs_set_last_error(cudaGetErrorString(e));
+      return PCS_E_NOMEM;
+    }
+    b.bytes = bytes;
+  }
+  *out = b.p;
+  return PCS_OK;
+}
+
+#define PCS_SCRATCH(slot, bytes, ptr)                                   \
+  do {                                                                  \
+    void* _p = nullptr;                                                 \
+    int _r = scratch(ctx, slot, (size_t)(bytes), &_p);                  \
+    if (_r != PCS_OK) return _r;                                        \
+    ptr = (decltype(ptr))_p;                                            \
+  } while (0)
+
+static inline int grid_for(i64 n, int block, int sms, int per_sm = 8) {
+  i64 g = ceil_div(n, block);
+  i64 cap = (i64)sms * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+static Grid to_grid(const pcs_grid_t* g) {
+  Grid r;
+  r.ox = g->origin_x;
+  r.oy = g->origin_y;
+  r.lx = g->cell_width;
+  r.ly = g->cell_height;
+  r.ncols = g->n_cols;
+  r.nrows = g->n_rows;
+  return r;
+}
+
+static Spot to_spot(const pcs_spot_t* s) {
+  Spot r;
+  r.sigma_psf = (float)s->sigma_psf;
+  r.bg = (float)s->i_bg;
+  r.inv2s2 = (float)(1.0 / (2.0 * s->sigma_psf * s->sigma_psf));
+  r.inv_2sxi2 = 1.0 / (2.0 * s->sigma_xi * s->sigma_xi);
+  r.hw = s->halfwidth;
+  r.model = s->model;
+  r.erf_scale = (float)(s->sigma_psf * 1.2533141373155002512078826);  // sigma*sqrt(pi/2)
+  r.inv_sqrt2s = (float)(1.0 / (1.4142135623730950488 * s->sigma_psf));
+  return r;
+}
+
+static int maxs_for(int hw) {
+  int S = 2 * hw + 1;
+  if (S <= 9) return 9;
+  if (S <= 11) return 11;
+  if (S <= 15) return 15;
+  return 0;
+}
+
+static int check_spot(const pcs_spot_t* s) {
+  PCS_CHECK_ARG(s, "spot is NULL");
+  PCS_CHECK_ARG(s->sigma_psf > 0, "sigma_psf must be > 0");
+  PCS_CHECK_ARG(s->sigma_xi > 0, "sigma_xi must be > 0");
+  PCS_CHECK_ARG(s->halfwidth >= 0, "halfwidth must be >= 0");
+  PCS_CHECK_ARG(s->model >= 0 && s->model <= 2, "unknown likelihood model");
+  PCS_CHECK_ARG(s->model == 0 || s->i_bg > 0, "Poisson likelihood needs i_bg > 0");
+  PCS_CHECK_ARG(s->i_bg >= 0, "i_bg must be >= 0");
+  return PCS_OK;
+}
+
+static int check_grid(const pcs_grid_t* g) {
+  PCS_CHECK_ARG(g, "grid is NULL");
+  PCS_CHECK_ARG(g->cell_width > 0 && g->cell_height > 0, "cell dimensions must be > 0");
+  PCS_CHECK_ARG(g->n_cols >= 1 && g->n_rows >= 1, "grid extent must be >= 1 cell per axis");
+  PCS_CHECK_ARG((double)g->n_cols * (double)g->n_rows < 1.8e19, "grid has more than 2^64 cells");
+  return PCS_OK;
+}
+
+extern "C" {
+
+const char* pcs_last_error(void) { return g_last_error.c_str(); }
+int pcs_version(void) { return 10000; }
+
+int pcs_device_info(int device, int* sm_count, int64_t* l2_bytes, int* cc_major, int* cc_minor) {
+  cudaDeviceProp p;
+  PCS_CUDA_TRY(cudaGetDeviceProperties(&p, device));
+  if (sm_count) *sm_count = p.multiProcessorCount;
+  if (l2_bytes) *l2_bytes = p.l2CacheSize;
+  if (cc_major) *cc_major = p.major;
+  if (cc_minor) *cc_minor = p.minor;
+  return PCS_OK;
+}
+
+int pcs_ctx_create(pcs_ctx** out, int device) {
+  PCS_CHECK_ARG(out, "out is NULL");
+  PCS_CUDA_TRY(cudaSetDevice(device));
+  pcs_ctx* c = new pcs_ctx();
+  c->device = device;
+  cudaDeviceProp p;
+  if (cudaGetDeviceProperties(&p, device) == cudaSuccess) c->sms = p.multiProcessorCount;
+  c->bufs.resize(SL_COUNT);
+  cudaError_t e = cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    pcs_set_last_error(cudaGetErrorString(e));
+    return PCS_E_CUDA;
+  }
+  *out = c;
+  return PCS_OK;
+}
+
+static void track_release(pcs_ctx* c) {
+  if (c->tr.exec) cudaGraphExecDestroy(c->tr.exec);
+  if (c->tr.graph) cudaGraphDestroy(c->tr.graph);
+  c->tr.exec = nullptr;
+  c->tr.graph = nullptr;
+  c->tr.active = false;
+}
+
+int pcs_ctx_destroy(pcs_ctx* c) {
+  if (!c) return PCS_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  track_release(c);
+  for (auto& b : c->bufs)
+    if (b.p) cudaFree(b.p);
+  if (c->tab_cnt) cudaFree(c->tab_cnt);
+  if (c->tab_sum) cudaFree(c->tab_sum);
+  if (c->wtab) cudaFree(c->wtab);
+  if (c->occ) cudaFree(c->occ);
+  if (c->cap) cudaStreamDestroy(c->cap);
+  delete c;
+  return PCS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// RNG replay
+// ---------------------------------------------------------------------------
+int pcs_philox_normals(uint64_t seed, uint32_t frame, int64_t off, int64_t n, float* out,
+                       int64_t ld, void* stream) {
+  PCS_CHECK_ARG(n >= 0 && out && ld >= n, "bad arguments");
+  if (n == 0) return PCS_OK;
+  k_philox_normals<<<grid_for(n, 256, 148), 256, 0, S(stream)>>>(seed, frame, off, n, out, ld);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+int pcs_philox_init_normals(uint64_t seed, int64_t off, int64_t n, float* out, int64_t ld,
+                            void* stream) {
+  PCS_CHECK_ARG(n >= 0 && out && ld >= n, "bad arguments");
+  if (n == 0) return PCS_OK;
+  k_philox_init_normals<<<grid_for(n, 256, 148), 256, 0, S(stream)>>>(seed, off, n, out, ld);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+int pcs_philox_init_uniforms(uint64_t seed, int64_t off, int64_t n, double* out, int64_t ld,
+                             void* stream) {
+  PCS_CHECK_ARG(n >= 0 && out && ld >= n, "bad arguments");
+  if (n == 0) return PCS_OK;
+  k_philox_init_uniforms<<<grid_for(n, 256, 148), 256, 0, S(stream)>>>(seed, off, n, out, ld);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+double pcs_philox_resample_u(uint64_t seed, uint32_t frame) {
+  return philox_resample_u(seed, frame);
+}
+
+int pcs_philox_multinomial_points(uint64_t seed, uint32_t frame, int64_t n, double* out,
+                                  void* stream) {
+  PCS_CHECK_ARG(n >= 0 && out, "bad arguments");
+  if (n == 0) return PCS_OK;
+  k_philox_multinomial<<<grid_for(n, 256, 148), 256, 0, S(stream)>>>(seed, frame, n, out);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// init / propagate / gather
+// ---------------------------------------------------------------------------
+static InitSpecDev to_init(const pcs_init_t* init) {
+  InitSpecDev d;
+  for (int c = 0; c < 5; ++c) d.c[c] = init->center[c];
+  d.mode = init->mode;
+  d.width = init->width;
+  d.sigma = init->sigma;
+  return d;
+}
+
+int pcs_init_particles(const pcs_init_t* init, uint64_t seed, int64_t off, int64_t n,
+                       float* states, int64_t ld, void* stream) {
+  PCS_CHECK_ARG(init && states && n >= 1 && ld >= n, "bad arguments");
+  PCS_CHECK_ARG(init->mode >= 0 && init->mode <= 2, "unknown init mode");
+  PCS_CHECK_ARG(init->mode != 1 || init->width > 0, "uniform init needs width > 0");
+  PCS_CHECK_ARG(init->mode != 2 || init->sigma > 0, "gauss init needs sigma > 0");
+  k_init<<<grid_for(n, 256, 148), 256, 0, S(stream)>>>(to_init(init), seed, off, n, states, ld);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+int pcs_propagate(const float* sin, float* sout, int64_t ld, int64_t n, const int32_t* anc,
+                  const pcs_dynamics_t* dyn, uint64_t seed, uint32_t frame, int64_t off,
+                  void* stream) {
+  PCS_CHECK_ARG(sin && sout && dyn && n >= 1 && ld >= n, "bad arguments");
+  PCS_CHECK_ARG(sin != sout, "in-place propagate is not supported");
+  PCS_CHECK_ARG(dyn->sigma_pos >= 0 && dyn->sigma_vel >= 0 && dyn->sigma_int >= 0,
+                "noise magnitudes must be >= 0");
+  PCS_CHECK_ARG(dyn->dt > 0, "dt must be > 0");
+  Dyn d{dyn->sigma_pos, dyn->sigma_vel, dyn->sigma_int, dyn->dt};
+  int g = grid_for(n, 256, 148);
+  if (anc)
+    k_propagate<true><<<g, 256, 0, S(stream)>>>(sin, sout, ld, n, anc, d, seed, frame, off);
+  else
+    k_propagate<false><<<g, 256, 0, S(stream)>>>(sin, sout, ld, n, nullptr, d, seed, frame, off);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+int pcs_propagate_given(const float* sin, float* sout, int64_t ld, int64_t n, const int32_t* anc,
+                        const pcs_dynamics_t* dyn, const float* normals, int64_t ldz,
+                        void* stream) {
+  PCS_CHECK_ARG(sin && sout && dyn && normals && n >= 1 && ld >= n && ldz >= n, "bad arguments");
+  PCS_CHECK_ARG(sin != sout, "in-place propagate is not supported");
+  Dyn d{dyn->sigma_pos, dyn->sigma_vel, dyn->sigma_int, dyn->dt};
+  k_propagate_given<<<grid_for(n, 256, 148), 256, 0, S(stream)>>>(sin, sout, ld, n, anc, d,
+                                                                   normals, ldz);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+int pcs_gather(const float* sin, float* sout, int64_t ld, int64_t n, const int32_t* anc,
+               void* stream) {
+  PCS_CHECK_ARG(sin && sout && anc && n >= 1 && ld >= n && sin != sout, "bad arguments");
+  k_gather<<<grid_for(n, 256, 148), 256, 0, S(stream)>>>(sin, sout, ld, n, anc);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// likelihood
+// ---------------------------------------------------------------------------
+int pcs_spot_window_ssd_f64(const double* pixels, int64_t H, int64_t W, const double* xs,
+                            const double* ys, const double* is, int64_t n, double sigma_psf,
+                            double i_bg, int32_t hw, double* out, void* stream) {
+  PCS_CHECK_ARG(pixels && xs && ys && is && out && H >= 1 && W >= 1 && n >= 0 && hw >= 0,
+                "bad arguments");
+  PCS_CHECK_ARG(sigma_psf > 0, "sigma_psf must be > 0");
+  if (n == 0) return PCS_OK;
+  double inv = 1.0 / (2.0 * sigma_psf * sigma_psf);
+  k_ssd_f64<<<grid_for(n, 128, 148, 16), 128, 0, S(stream)>>>(pixels, H, W, xs, ys, is, n, inv,
+                                                               i_bg, hw, out);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+int pcs_loglik(const float* pixels, int64_t H, int64_t W, const float* xs, const float* ys,
+               const float* is, int64_t n, const pcs_spot_t* spot, float* out, void* stream) {
+  int r = check_spot(spot);
+  if (r) return r;
+  PCS_CHECK_ARG(pixels && xs && ys && is && out && H >= 1 && W >= 1 && n >= 0, "bad arguments");
+  if (n == 0) return PCS_OK;
+  Spot sp = to_spot(spot);
+  int g = grid_for(n, 256, 148, 16);
+  switch (maxs_for(spot->halfwidth)) {
+    case 9: k_loglik<9><<<g, 256, 0, S(stream)>>>(pixels, H, W, xs, ys, is, n, sp, out); break;
+    case 11: k_loglik<11><<<g, 256, 0, S(stream)>>>(pixels, H, W, xs, ys, is, n, sp, out); break;
+    case 15: k_loglik<15><<<g, 256, 0, S(stream)>>>(pixels, H, W, xs, ys, is, n, sp, out); break;
+    default: k_loglik_generic<<<g, 256, 0, S(stream)>>>(pixels, H, W, xs, ys, is, n, sp, out);
+  }
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// partition / dummies (general sort path)
+// ---------------------------------------------------------------------------
+int pcs_partition(pcs_ctx* ctx, const float* states, int64_t ld, int64_t n,
+                  const pcs_grid_t* grid, uint64_t* flat, int32_t* order, int32_t* bin_of,
+                  uint64_t* unique, int64_t* starts, int64_t* counts, int64_t* m_out,
+                  void* stream) {
+  int r = check_grid(grid);
+  if (r) return r;
+  PCS_CHECK_ARG(ctx && states && flat && order && bin_of && unique && starts && counts && m_out,
+                "bad arguments");
+  PCS_CHECK_ARG(n >= 1 && n < INT_MAX && ld >= n, "n out of range");
+  cudaStream_t st = S(stream);
+  Grid g = to_grid(grid);
+  u64* keys_sorted;
+  int* idx;
+  int* head;
+  int* incl;
+  i64* nruns;
+  u32* flags;
+  PCS_SCRATCH(SL_SORT_KEYS, n * sizeof(u64), keys_sorted);
+  PCS_SCRATCH(SL_SORT_IDX, n * sizeof(int), idx);
+  PCS_SCRATCH(SL_HEAD, n * sizeof(int), head);
+  PCS_SCRATCH(SL_INCL, n * sizeof(int), incl);
+  PCS_SCRATCH(SL_NRUNS, 64, nruns);
+  PCS_SCRATCH(SL_FLAGS, 64, flags);
+  PCS_CUDA_TRY(cudaMemsetAsync(flags, 0, 4, st));
+  int gr = grid_for(n, 256, ctx->sms);
+  k_cell_keys<<<gr, 256, 0, st>>>(states, ld, n, g, (u64*)flat, idx, flags);
+  PCS_LAUNCH_CHECK();
+  // key bits = bits of (n_cols*n_rows - 1)
+  u64 maxkey = (u64)grid->n_cols * (u64)grid->n_rows - 1ull;
+  int end_bit = maxkey ? 64 - clz64(maxkey) : 1;
+  size_t tb1 = 0, tb2 = 0, tb3 = 0, tb4 = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tb1, (const u64*)flat, keys_sorted, (const int*)idx,
+                                  (int*)order, (int)n, 0, end_bit, st);
+  cub::DeviceRunLengthEncode::Encode(nullptr, tb2, (const u64*)keys_sorted, (u64*)unique,
+                                     (i64*)counts, nruns, (int)n, st);
+  cub::DeviceScan::ExclusiveSum(nullptr, tb3, (const i64*)counts, (i64*)starts, (int)n, st);
+  cub::DeviceScan::InclusiveSum(nullptr, tb4, (const int*)head, incl, (int)n, st);
+  size_t tb = std::max(std::max(tb1, tb2), std::max(tb3, tb4));
+  void* temp;
+  PCS_SCRATCH(SL_CUB, tb, temp);
+  PCS_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, tb1, (const u64*)flat, keys_sorted,
+                                               (const int*)idx, (int*)order, (int)n, 0, end_bit, st));
+  PCS_CUDA_TRY(cub::DeviceRunLengthEncode::Encode(temp, tb2, (const u64*)keys_sorted,
+                                                  (u64*)unique, (i64*)counts, nruns, (int)n, st));
+  i64 m = 0;
+  PCS_CUDA_TRY(cudaMemcpyAsync(&m, nruns, sizeof(i64), cudaMemcpyDeviceToHost, st));
+  PCS_CUDA_TRY(cudaStreamSynchronize(st));
+  PCS_CUDA_TRY(cub::DeviceScan::ExclusiveSum(temp, tb3, (const i64*)counts, (i64*)starts, (int)m, st));
+  k_run_heads<<<gr, 256, 0, st>>>(keys_sorted, n, head);
+  PCS_LAUNCH_CHECK();
+  PCS_CUDA_TRY(cub::DeviceScan::InclusiveSum(temp, tb4, (const int*)head, incl, (int)n, st));
+  k_scatter_bin_of<<<gr, 256, 0, st>>>(incl, order, n, bin_of);
+  PCS_LAUNCH_CHECK();
+  u32 hflags = 0;
+  PCS_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, 4, cudaMemcpyDeviceToHost, st));
+  PCS_CUDA_TRY(cudaStreamSynchronize(st));
+  *m_out = m;
+  if (hflags & PCS_FLAG_NONFINITE) {
+    pcs_set_last_error("non-finite particle position");
+    return PCS_E_INVALID;
+  }
+  return PCS_OK;
+}
+
+
+int pcs_dummies(pcs_ctx* ctx, const float* states, int64_t ld, int64_t n, const int32_t* order,
+                const int32_t* bin_of, const int64_t* counts, const uint64_t* unique, int64_t m,
+                const pcs_grid_t* grid, int32_t placement, const float* prior_w, float* dummies,
+                int64_t ldd, void* stream) {
+  int r = check_grid(grid);
+  if (r) return r;
+  PCS_CHECK_ARG(ctx && states && order && bin_of && counts && unique && dummies, "bad arguments");
+  PCS_CHECK_ARG(n >= 1 && m >= 1 && m <= n && ldd >= m && ld >= n, "bad sizes");
+  PCS_CHECK_ARG(placement == 0 || placement == 1, "unknown placement");
+  cudaStream_t st = S(stream);
+  u64* sums;
+  size_t sb = (size_t)6 * m * 2 * sizeof(u64);
+  PCS_SCRATCH(SL_SUMS, sb, sums);
+  PCS_CUDA_TRY(cudaMemsetAsync(sums, 0, sb, st));
+  k_bin_sums<<<grid_for(n, 256, ctx->sms), 256, 0, st>>>(states, ld, n, order, bin_of, prior_w,
+                                                          sums, m);
+  PCS_LAUNCH_CHECK();
+  k_dummies<<<grid_for(m, 256, ctx->sms), 256, 0, st>>>(sums, (const i64*)counts, (const u64*)unique, m, to_grid(grid),
+                                                         placement, prior_w ? 1 : 0, dummies, ldd);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// weights
+// ---------------------------------------------------------------------------
+int pcs_weight_update(const float* prior_w, const double* prior_logw, const float* ll,
+                      const int32_t* bin_of, int64_t n, double* logw, void* stream) {
+  PCS_CHECK_ARG(ll && logw && n >= 1, "bad arguments");
+  k_weight_update<<<grid_for(n, 256, 148), 256, 0, S(stream)>>>(prior_w, prior_logw, ll, bin_of, n,
+                                                                 logw);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+int pcs_normalize(pcs_ctx* ctx, const double* logw, int64_t n, float* w, double* max_out,
+                  double* norm_out, int32_t* degenerate, void* stream) {
+  PCS_CHECK_ARG(ctx && logw && w && n >= 1, "bad arguments");
+  cudaStream_t st = S(stream);
+  NormCtl* nc;
+  PCS_SCRATCH(SL_NORM, sizeof(NormCtl), nc);
+  NormCtl h;
+  memset(&h, 0, sizeof(h));
+  h.max_ord = (i64)0x8000000000000000ll;  // below every encoded double
+  PCS_CUDA_TRY(cudaMemcpyAsync(nc, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  int g = grid_for(n, 256, ctx->sms);
+  k_logw_max<256><<<g, 256, 0, st>>>(logw, n, nc);
+  PCS_LAUNCH_CHECK();
+  PCS_CUDA_TRY(cudaMemcpyAsync(&h, nc, sizeof(h), cudaMemcpyDeviceToHost, st));
+  PCS_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h.nonfinite) {
+    pcs_set_last_error("likelihood values must be finite and >= 0");
+    return PCS_E_INVALID;
+  }
+  double m = *(double*)&h.max_ord;
+  {
+    i64 i = h.max_ord;
+    i64 raw = (i >= 0) ? i : (i ^ 0x7FFFFFFFFFFFFFFFll);
+    memcpy(&m, &raw, 8);
+  }
+  if (!(m > -INFINITY)) {
+    if (degenerate) *degenerate = 1;
+    if (max_out) *max_out = m;
+    if (norm_out) *norm_out = 0.0;
+    return PCS_OK;
+  }
+  k_logw_sum<256><<<g, 256, 0, st>>>(logw, n, nc);
+  PCS_LAUNCH_CHECK();
+  k_logw_normalise<<<g, 256, 0, st>>>(logw, n, nc, w);
+  PCS_LAUNCH_CHECK();
+  PCS_CUDA_TRY(cudaMemcpyAsync(&h, nc, sizeof(h), cudaMemcpyDeviceToHost, st));
+  PCS_CUDA_TRY(cudaStreamSynchronize(st));
+  if (degenerate) *degenerate = 0;
+  if (max_out) *max_out = m;
+  if (norm_out) {
+    i128 Sv = (i128)(((u128)h.S[1] << 64) | (u128)h.S[0]);
+    *norm_out = ldexp(i128_to_f64_rn(Sv), -FX_S);
+  }
+  return PCS_OK;
+}
+
+int pcs_estimate_ess(pcs_ctx* ctx, const float* states, int64_t ld, const float* w, int64_t n,
+                     double* est5, double* ess, void* stream) {
+  PCS_CHECK_ARG(ctx && states && w && n >= 1 && ld >= n, "bad arguments");
+  cudaStream_t st = S(stream);
+  NormCtl* nc;
+  PCS_SCRATCH(SL_NORM, sizeof(NormCtl), nc);
+  PCS_CUDA_TRY(cudaMemsetAsync(nc, 0, sizeof(NormCtl), st));
+  k_estimate_ess<256><<<grid_for(n, 256, ctx->sms), 256, 0, st>>>(states, ld, w, n, nc);
+  PCS_LAUNCH_CHECK();
+  NormCtl h;
+  PCS_CUDA_TRY(cudaMemcpyAsync(&h, nc, sizeof(h), cudaMemcpyDeviceToHost, st));
+  PCS_CUDA_TRY(cudaStreamSynchronize(st));
+  for (int c = 0; c < 5; ++c) {
+    i128 v = (i128)(((u128)h.est[c][1] << 64) | (u128)h.est[c][0]);
+    if (est5) est5[c] = ldexp(i128_to_f64_rn(v), -(FX_WQ + FX_STATE));
+  }
+  i128 v2 = (i128)(((u128)h.w2[1] << 64) | (u128)h.w2[0]);
+  if (ess) *ess = 1.0 / ldexp(i128_to_f64_rn(v2), -FX_W2);
+  return PCS_OK;
+}
+
+static int cdf_pass(pcs_ctx* ctx, const float* w, int64_t n, double u, int32_t* anc, double* cdf,
+                    int mode, cudaStream_t st) {
+  i64 nt = ceil_div(n, SCAN_TILE);
+  u128* tot;
+  u128* pre;
+  PCS_SCRATCH(SL_TILES, nt * sizeof(u128), tot);
+  PCS_SCRATCH(SL_PRE, nt * sizeof(u128), pre);
+  WeightSrc src;
+  memset(&src, 0, sizeof(src));
+  src.w = w;
+  src.kind = 0;
+  k_cdf_tiles<<<(unsigned)nt, SCAN_BLOCK, 0, st>>>(src, n, tot);
+  PCS_LAUNCH_CHECK();
+  k_scan_tiles<<<1, 1024, 0, st>>>(tot, nt, pre, nullptr);
+  PCS_LAUNCH_CHECK();
+  if (mode == 0)
+    k_cdf_emit<0><<<(unsigned)nt, SCAN_BLOCK, 0, st>>>(src, n, pre, u, anc, nullptr);
+  else
+    k_cdf_emit<1><<<(unsigned)nt, SCAN_BLOCK, 0, st>>>(src, n, pre, u, nullptr, cdf);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+int pcs_resample_systematic(pcs_ctx* ctx, const float* w, int64_t n, double u, int32_t* anc,
+                            void* stream) {
+  PCS_CHECK_ARG(ctx && w && anc && n >= 1 && n < INT_MAX, "bad arguments");
+  PCS_CHECK_ARG(u >= 0.0 && u < 1.0, "u must be in [0, 1)");
+  return cdf_pass(ctx, w, n, u, anc, nullptr, 0, S(stream));
+}
+
+int pcs_cdf(pcs_ctx* ctx, const float* w, int64_t n, double* cdf, void* stream) {
+  PCS_CHECK_ARG(ctx && w && cdf && n >= 1, "bad arguments");
+  return cdf_pass(ctx, w, n, 0.0, nullptr, cdf, 1, S(stream));
+}
+
+int pcs_resample_multinomial(pcs_ctx* ctx, const float* w, int64_t n, const double* points,
+                             int32_t* anc, void* stream) {
+  PCS_CHECK_ARG(ctx && w && points && anc && n >= 1 && n < INT_MAX, "bad arguments");
+  cudaStream_t st = S(stream);
+  double* cdf;
+  PCS_SCRATCH(SL_SORT_KEYS, n * sizeof(double), cdf);
+  int r = cdf_pass(ctx, w, n, 0.0, nullptr, cdf, 1, st);
+  if (r) return r;
+  k_searchsorted<<<grid_for(n, 256, ctx->sms), 256, 0, st>>>(cdf, n, points, anc);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+// ---------------------------------------------------------------------------
+// fused track
+// ---------------------------------------------------------------------------
+__global__ void k_iota(int* a, i64 n) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    a[i] = (int)i;
+}
+
+__global__ void k_ctl_init(TrackCtl* C, double cx, double cy) {
+  memset(C, 0, sizeof(TrackCtl));
+  reset_frame(C);
+  C->first_bad = INT_MAX;
+  C->center[0] = cx;
+  C->center[1] = cy;
+  C->table_ok = 1;
+}
+
+__global__ void k_ctl_io(TrackCtl* C, const float* frames, i64 kf, i64 ko, double* est,
+                         double* ess, unsigned char* res, i64* occ) {
+  C->frames = frames;
+  C->k_frames = kf;
+  C->k_out = ko;
+  C->out_est = est;
+  C->out_ess = ess;
+  C->out_res = res;
+  C->out_occ = occ;
+}
+
+// Enqueue one frame. If evs is non-null, evs[i] is recorded before launch i
+// and evs[launches] after the last one (per-kernel CUDA-event timing).
+static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullptr) {
+  TrackState& T = ctx->tr;
+  TrackParams& P = T.P;
+  int q = 0;
+  auto mark = [&]() {
+    if (evs) cudaEventRecord(evs[q], st);
+    ++q;
+  };
+  if (T.cfg.method == 1) {
+    mark();
+    k_pc_propagate<<<T.prop_grid, 256, 0, st>>>(P);
+    mark();
+    k_pc_accumulate<<<T.acc_grid, ACC_BLOCK, ACC_SMEM, st>>>(P, T.acc_chunk);
+    mark();
+    switch (T.maxs) {
+      case 9: k_pc_bins<9><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P); break;
+      case 11: k_pc_bins<11><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P); break;
+      case 15: k_pc_bins<15><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P); break;
+      default: k_pc_bins<0><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P);
+    }
+    mark();
+    k_track_tiles<1><<<(unsigned)T.ntiles, SCAN_BLOCK, 0, st>>>(P, T.tile_tot);
+    mark();
+    k_scan_tiles<<<1, 1024, 0, st>>>(T.tile_tot, T.ntiles, T.tile_pre, &P.ctl->k);
+    mark();
+    k_track_emit<1><<<(unsigned)T.ntiles, SCAN_BLOCK, 0, st>>>(P, T.tile_pre);
+  } else {
+    mark();
+    switch (T.maxs) {
+      case 9: k_sir_propagate_lik<9><<<T.prop_grid, 256, 0, st>>>(P); break;
+      case 11: k_sir_propagate_lik<11><<<T.prop_grid, 256, 0, st>>>(P); break;
+      case 15: k_sir_propagate_lik<15><<<T.prop_grid, 256, 0, st>>>(P); break;
+      default: k_sir_propagate_lik<0><<<T.prop_grid, 256, 0, st>>>(P);
+    }
+    mark();
+    k_sir_sum<<<grid_for(P.n, 256, ctx->sms), 256, 0, st>>>(P);
+    mark();
+    k_sir_tiles_stats<<<(unsigned)T.ntiles, SCAN_BLOCK, 0, st>>>(P, T.tile_tot);
+    mark();
+    k_sir_finalize<<<1, 1, 0, st>>>(P);
+    mark();
+    k_scan_tiles<<<1, 1024, 0, st>>>(T.tile_tot, T.ntiles, T.tile_pre, &P.ctl->k);
+    mark();
+    k_track_emit<2><<<(unsigned)T.ntiles, SCAN_BLOCK, 0, st>>>(P, T.tile_pre);
+  }
+  if (evs) cudaEventRecord(evs[q], st);
+  PCS_LAUNCH_CHECK();
+  T.launches = q;
+  return PCS_OK;
+}
+
+static const char* kPcNames[] = {"k_pc_propagate", "k_pc_accumulate", "k_pc_bins",
+                                 "k_track_tiles", "k_scan_tiles", "k_track_emit"};
+static const char* kSirNames[] = {"k_sir_propagate_lik", "k_sir_sum", "k_sir_tiles_stats",
+                                  "k_sir_finalize", "k_scan_tiles", "k_track_emit"};
+
+static bool g_attr_done = false;
+
+int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t W, void* stream) {
+  PCS_CHECK_ARG(ctx && cfg, "bad arguments");
+  PCS_CHECK_ARG(cfg->method == 0 || cfg->method == 1, "method must be 0 (SIR) or 1 (pcSIR)");
+  PCS_CHECK_ARG(cfg->n_particles >= 1 && cfg->n_particles < INT_MAX, "n_particles out of range");
+  PCS_CHECK_ARG(H >= 1 && W >= 1, "bad frame shape");
+  int r = check_spot(&cfg->spot);
+  if (r) return r;
+  if (cfg->method == 1) {
+    r = check_grid(&cfg->grid);
+    if (r) return r;
+    PCS_CHECK_ARG(cfg->placement == 0 || cfg->placement == 1, "unknown placement");
+  }
+  PCS_CHECK_ARG(cfg->dyn.dt > 0, "dt must be > 0");
+  cudaStream_t st = S(stream);
+  if (!g_attr_done) {
+    PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_accumulate, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)ACC_SMEM));
+    PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)BINS_SMEM));
+    PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)BINS_SMEM));
+    PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)BINS_SMEM));
+    PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<15>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)BINS_SMEM));
+    g_attr_done = true;
+  }
+  track_release(ctx);
+  TrackState& T = ctx->tr;
+  T = TrackState();
+  T.cfg = *cfg;
+  const i64 n = cfg->n_particles;
+  const i64 ld = ceil_div(n, 32) * 32;
+  TrackParams& P = T.P;
+  P.n = n;
+  P.ld = ld;
+  P.H = H;
+  P.W = W;
+  P.dyn = Dyn{cfg->dyn.sigma_pos, cfg->dyn.sigma_vel, cfg->dyn.sigma_int, cfg->dyn.dt};
+  P.spot = to_spot(&cfg->spot);
+  P.grid = cfg->method == 1 ? to_grid(&cfg->grid) : Grid{0, 0, 1, 1, 1, 1};
+  P.seed = cfg->seed;
+  P.frame0 = cfg->frame0;
+  P.placement = cfg->placement;
+  PCS_SCRATCH(SL_TR_BUF0, 5 * ld * sizeof(float), P.buf0);
+  PCS_SCRATCH(SL_TR_BUF1, 5 * ld * sizeof(float), P.buf1);
+  PCS_SCRATCH(SL_TR_ANC, ld * sizeof(int), P.anc);
+  PCS_SCRATCH(SL_TR_CTL, sizeof(TrackCtl), P.ctl);
+  T.ntiles = ceil_div(n, SCAN_TILE);
+  PCS_SCRATCH(SL_TR_TILES, T.ntiles * sizeof(u128), T.tile_tot);
+  PCS_SCRATCH(SL_TR_PRE, T.ntiles * sizeof(u128), T.tile_pre);
+  if (cfg->method == 0) {
+    PCS_SCRATCH(SL_TR_LL, ld * sizeof(float), P.ll);
+    P.pslot = nullptr;
+  } else {
+    PCS_SCRATCH(SL_TR_PSLOT, ld * sizeof(u32), P.pslot);
+    P.ll = nullptr;
+    if (!ctx->tab_cnt) {
+      PCS_CUDA_TRY(cudaMalloc(&ctx->tab_cnt, TABLE_CAP * sizeof(u32)));
+      PCS_CUDA_TRY(cudaMalloc(&ctx->tab_sum, 5 * TABLE_CAP * 2 * sizeof(u64)));
+      PCS_CUDA_TRY(cudaMalloc(&ctx->wtab, TABLE_CAP * sizeof(float)));
+      PCS_CUDA_TRY(cudaMalloc(&ctx->occ, MAXM * sizeof(u32)));
+      ctx->table_dirty = true;
+    }
+    if (ctx->table_dirty) {
+      PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_cnt, 0, TABLE_CAP * sizeof(u32), st));
+      PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_sum, 0, 5 * TABLE_CAP * 2 * sizeof(u64), st));
+      ctx->table_dirty = false;
+    }
+    P.tab_cnt = ctx->tab_cnt;
+    P.tab_sum = ctx->tab_sum;
+    P.wtab = ctx->wtab;
+    P.occ = ctx->occ;
+  }
+  T.maxs = maxs_for(cfg->spot.halfwidth);
+  T.prop_grid = grid_for(n, 256, ctx->sms, 8);
+  // accumulate: chunk <= 2^15 particles per CTA (int64 shared partials), ~2 CTAs/SM
+  i64 want = 2 * (i64)ctx->sms;
+  i64 chunk = std::max<i64>(512, ceil_div(n, want));
+  chunk = std::min<i64>(chunk, 1 << 15);
+  T.acc_chunk = chunk;
+  T.acc_grid = (int)ceil_div(n, chunk);
+  // initial cloud (state.py:164-175) and identity ancestors
+  pcs_init_t init = cfg->init;
+  r = pcs_init_particles(&init, cfg->seed, 0, n, P.buf0, ld, stream);
+  if (r) return r;
+  k_iota<<<grid_for(n, 256, ctx->sms), 256, 0, st>>>(P.anc, n);
+  k_ctl_init<<<1, 1, 0, st>>>(P.ctl, init.center[0], init.center[1]);
+  PCS_LAUNCH_CHECK();
+  T.k = 0;
+  T.active = true;
+  if (cfg->use_graph) {
+    // capture one frame on the private stream; replays read everything from the control block
+    PCS_CUDA_TRY(cudaStreamSynchronize(st));
+    PCS_CUDA_TRY(cudaStreamBeginCapture(ctx->cap, cudaStreamCaptureModeThreadLocal));
+    int er = enqueue_frame(ctx, ctx->cap);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(ctx->cap, &g);
+    if (er) return er;
+    PCS_CUDA_TRY(e);
+    T.graph = g;
+    PCS_CUDA_TRY(cudaGraphInstantiate(&T.exec, g, 0));
+  }
+  return PCS_OK;
+}
+
+int pcs_track_steps(pcs_ctx* ctx, const float* frames, int64_t k0, int64_t k1, double* est,
+                    double* ess, uint8_t* res, int64_t* occ, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active, "no active track (call pcs_track_begin)");
+  PCS_CHECK_ARG(frames && est && ess && res && occ, "bad arguments");
+  PCS_CHECK_ARG(k0 == ctx->tr.k && k1 >= k0, "frames must be stepped in order");
+  cudaStream_t st = S(stream);
+  TrackState& T = ctx->tr;
+  k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frames, k0, k0, est, ess, res, (i64*)occ);
+  PCS_LAUNCH_CHECK();
+  for (i64 k = k0; k < k1; ++k) {
+    if (T.exec) {
+      PCS_CUDA_TRY(cudaGraphLaunch(T.exec, st));
+    } else {
+      int r = enqueue_frame(ctx, st);
+      if (r) return r;
+    }
+  }
+  T.k = k1;
+  return PCS_OK;
+}
+
+int pcs_track_steps_timed(pcs_ctx* ctx, const float* frames, int64_t k0, int64_t k1, double* est,
+                          double* ess, uint8_t* res, int64_t* occ, double* kernel_ms,
+                          int32_t max_kernels, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active, "no active track (call pcs_track_begin)");
+  PCS_CHECK_ARG(frames && est && ess && res && occ && kernel_ms && max_kernels >= 8,
+                "bad arguments");
+  PCS_CHECK_ARG(k0 == ctx->tr.k && k1 >= k0, "frames must be stepped in order");
+  cudaStream_t st = S(stream);
+  TrackState& T = ctx->tr;
+  k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frames, k0, k0, est, ess, res, (i64*)occ);
+  PCS_LAUNCH_CHECK();
+  const int NE = 8;
+  cudaEvent_t evs[NE];
+  for (int i = 0; i < NE; ++i) PCS_CUDA_TRY(cudaEventCreate(&evs[i]));
+  for (int i = 0; i < max_kernels; ++i) kernel_ms[i] = 0.0;
+  int r = PCS_OK;
+  for (i64 k = k0; k < k1 && r == PCS_OK; ++k) {
+    r = enqueue_frame(ctx, st, evs);
+    if (r) break;
+    cudaError_t e = cudaEventSynchronize(evs[T.launches]);
+    if (e != cudaSuccess) {
+      pcs_set_last_error(cudaGetErrorString(e));
+      r = PCS_E_CUDA;
+      break;
+    }
+    for (int q = 0; q < T.launches; ++q) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, evs[q], evs[q + 1]);
+      kernel_ms[q] += ms;
+    }
+  }
+  for (int i = 0; i < NE; ++i) cudaEventDestroy(evs[i]);
+  if (r == PCS_OK) T.k = k1;
+  return r;
+}
+
+const char* pcs_track_kernel_name(pcs_ctx* ctx, int32_t i) {
+  if (!ctx || i < 0 || i >= 6) return "";
+  return ctx->tr.cfg.method == 1 ? kPcNames[i] : kSirNames[i];
+}
+
+int pcs_track_end(pcs_ctx* ctx, pcs_track_result_t* result, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && result, "bad arguments");
+  cudaStream_t st = S(stream);
+  TrackCtl h;
+  PCS_CUDA_TRY(cudaMemcpyAsync(&h, ctx->tr.P.ctl, sizeof(h), cudaMemcpyDeviceToHost, st));
+  PCS_CUDA_TRY(cudaStreamSynchronize(st));
+  result->flags = h.flags;
+  result->first_bad_frame = (h.first_bad == INT_MAX) ? -1 : h.first_bad;
+  result->likelihood_evals = h.evals;
+  if (h.flags & PCS_FLAG_CAPACITY) ctx->table_dirty = true;
+  if (h.flags & PCS_FLAG_CAPACITY) return PCS_E_CAPACITY;
+  return PCS_OK;
+}
+
+int pcs_track(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, const float* frames, int64_t K,
+              int64_t H, int64_t W, double* est, double* ess, uint8_t* res, int64_t* occ,
+              pcs_track_result_t* result, void* stream) {
+  PCS_CHECK_ARG(K >= 1, "need at least one frame");
+  int r = pcs_track_begin(ctx, cfg, H, W, stream);
+  if (r) return r;
+  r = pcs_track_steps(ctx, frames, 0, K, est, ess, res, occ, stream);
+  if (r) return r;
+  return pcs_track_end(ctx, result, stream);
+}
+
+int pcs_track_launches_per_step(pcs_ctx* ctx) { return ctx ? ctx->tr.launches : 0; }
+
+int pcs_track_states(pcs_ctx* ctx, float** states, int64_t* ld) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && states && ld, "bad arguments");
+  // frame k reads buf[k&1]; after k frames the latest propagated states are in buf[k&1]
+  // (the emission of frame k-1 produced the ancestors into that buffer's frame).
+  *states = (ctx->tr.k & 1) ? ctx->tr.P.buf1 : ctx->tr.P.buf0;
+  *ld = ctx->tr.P.ld;
+  return PCS_OK;
+}
+
+}  // extern "C"

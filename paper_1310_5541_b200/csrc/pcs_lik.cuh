@@ -1,0 +1,268 @@
+// pcs_lik.cuh — spot likelihoods.
+//
+// Reference: _speedups.pyx:17-85 and kernels.py:24-40 (windowed Gaussian
+// SSD), imaging.py:125-137 (exp(-ssd/(2 sigma_xi^2))). Window convention:
+// centre pixel floor(p + 0.5), each bound clamped to the frame independently
+// (_speedups.pyx:47-68) so far-out states see a border strip, never an error.
+#pragma once
+#include "pcs_common.cuh"
+
+namespace pcs {
+
+struct Spot {
+  float sigma_psf;
+  float bg;
+  float inv2s2;        // 1 / (2 sigma_psf^2)
+  double inv_2sxi2;    // 1 / (2 sigma_xi^2)
+  int hw;
+  int model;           // 0 gauss-ssd, 1 erf-poisson, 2 midpoint4x4-poisson
+  float erf_scale;     // sigma*sqrt(pi/2)  (model 1)
+  float inv_sqrt2s;    // 1/(sqrt(2) sigma) (model 1)
+};
+
+__device__ __forceinline__ void window_axis(double p, int hw, i64 extent, int& lo, int& hi) {
+  // cx = floor(p + 0.5); lo = clamp(cx - hw, 0, extent-1); hi = clamp(cx + hw, 0, extent-1)
+  double c = floor(p + 0.5);
+  double e1 = (double)(extent - 1);
+  double l = c - (double)hw, h = c + (double)hw;
+  l = (l < 0.0) ? 0.0 : ((l > e1) ? e1 : l);
+  h = (h < 0.0) ? 0.0 : ((h > e1) ? e1 : h);
+  lo = (int)l;
+  hi = (int)h;
+}
+
+// ---- Gaussian windowed SSD, float32 core (CANONICAL hot-path arithmetic) ----
+//   gx[i] = expf(-(d*d) * inv2s2), d = RN32(xi - x)          (fp32)
+//   pred  = fmaf(I0*gx[i], gy[j], bg); r = p - pred           (fp32)
+//   row   = sum_i fmaf(r, r, row)                             (fp32, per row)
+//   ssd   = sum_rows (double)row                              (fp64)
+//   ll    = RN32(-ssd * inv_2sxi2)
+template <int MAXS>
+__device__ __forceinline__ float loglik_gauss(const float* __restrict__ pix, i64 H, i64 W, float x,
+                                              float y, float i0, const Spot& sp) {
+  if (!(x == x) || !(y == y) || !(i0 == i0)) return __int_as_float(0x7fc00000);
+  int xlo, xhi, ylo, yhi;
+  window_axis((double)x, sp.hw, W, xlo, xhi);
+  window_axis((double)y, sp.hw, H, ylo, yhi);
+  int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
+  float ag[MAXS];
+#pragma unroll
+  for (int i = 0; i < MAXS; ++i) {
+    if (i < nx) {
+      float d = __double2float_rn((double)(xlo + i) - (double)x);
+      ag[i] = i0 * expf(-(d * d) * sp.inv2s2);
+    }
+  }
+  double ssd = 0.0;
+  const float* row = pix + (i64)ylo * W + xlo;
+  for (int j = 0; j < ny; ++j) {
+    float d = __double2float_rn((double)(ylo + j) - (double)y);
+    float gy = expf(-(d * d) * sp.inv2s2);
+    float acc = 0.0f;
+#pragma unroll
+    for (int i = 0; i < MAXS; ++i) {
+      if (i < nx) {
+        float r = __ldg(row + i) - fmaf(ag[i], gy, sp.bg);
+        acc = fmaf(r, r, acc);
+      }
+    }
+    ssd += (double)acc;
+    row += W;
+  }
+  return __double2float_rn(-ssd * sp.inv_2sxi2);
+}
+
+// ---- Poisson log-likelihood ratio vs background (config 3, new) -------------
+//   lambda = bg + I0 Ex(xi) Ey(yi);   ll = sum_window [ z log1p(mu/bg) - mu ],
+//   mu = I0 Ex Ey. Equals the full-frame Poisson log-likelihood minus a
+//   per-frame constant (pixels outside the window have lambda = bg), with
+//   the lgamma(z+1) term dropped.
+// model 1: Ex = integral of exp(-(t-x)^2/2s^2) over the pixel (erf form). The
+//   4x4 sub-pixel supersampled integral telescopes exactly to this, so the
+//   S+1 pixel-boundary erf values are evaluated (minimal form).
+// model 2: Ex = 1/4 sum_s exp(-((xi - 3/8 + s/4) - x)^2 / 2s^2) (mid-point 4x4).
+__device__ __forceinline__ float erf_diff(float a, float b) {
+  // erf(b) - erf(a), a < b, accurate in both tails
+  if (a >= 0.0f) return erfcf(a) - erfcf(b);
+  if (b <= 0.0f) return erfcf(-b) - erfcf(-a);
+  return erff(b) - erff(a);
+}
+
+template <int MAXS>
+__device__ __forceinline__ float loglik_poisson(const float* __restrict__ pix, i64 H, i64 W, float x,
+                                                float y, float i0, const Spot& sp) {
+  if (!(x == x) || !(y == y) || !(i0 == i0)) return __int_as_float(0x7fc00000);
+  int xlo, xhi, ylo, yhi;
+  window_axis((double)x, sp.hw, W, xlo, xhi);
+  window_axis((double)y, sp.hw, H, ylo, yhi);
+  int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
+  float ex[MAXS];
+  const float inv_bg = 1.0f / sp.bg;
+#pragma unroll
+  for (int i = 0; i < MAXS; ++i) {
+    if (i < nx) {
+      float d = __double2float_rn((double)(xlo + i) - (double)x);
+      float e;
+      if (sp.model == 1) {
+        e = sp.erf_scale * erf_diff((d - 0.5f) * sp.inv_sqrt2s, (d + 0.5f) * sp.inv_sqrt2s);
+      } else {
+        float t0 = d - 0.375f, t1 = d - 0.125f, t2 = d + 0.125f, t3 = d + 0.375f;
+        e = 0.25f * (expf(-(t0 * t0) * sp.inv2s2) + expf(-(t1 * t1) * sp.inv2s2) +
+                     expf(-(t2 * t2) * sp.inv2s2) + expf(-(t3 * t3) * sp.inv2s2));
+      }
+      ex[i] = i0 * e * inv_bg;   // mu/bg along x (times Ey later)
+    }
+  }
+  double ll = 0.0;
+  const float* row = pix + (i64)ylo * W + xlo;
+  for (int j = 0; j < ny; ++j) {
+    float d = __double2float_rn((double)(ylo + j) - (double)y);
+    float ey;
+    if (sp.model == 1) {
+      ey = sp.erf_scale * erf_diff((d - 0.5f) * sp.inv_sqrt2s, (d + 0.5f) * sp.inv_sqrt2s);
+    } else {
+      float t0 = d - 0.375f, t1 = d - 0.125f, t2 = d + 0.125f, t3 = d + 0.375f;
+      ey = 0.25f * (expf(-(t0 * t0) * sp.inv2s2) + expf(-(t1 * t1) * sp.inv2s2) +
+                    expf(-(t2 * t2) * sp.inv2s2) + expf(-(t3 * t3) * sp.inv2s2));
+    }
+    float acc = 0.0f;
+#pragma unroll
+    for (int i = 0; i < MAXS; ++i) {
+      if (i < nx) {
+        float t = ex[i] * ey;                   // mu / bg
+        float z = __ldg(row + i);
+        acc += fmaf(z, log1pf(t), -t * sp.bg);  // z log1p(mu/bg) - mu
+      }
+    }
+    ll += (double)acc;
+    row += W;
+  }
+  return __double2float_rn(ll);
+}
+
+template <int MAXS>
+__device__ __forceinline__ float loglik_any(const float* __restrict__ pix, i64 H, i64 W, float x,
+                                            float y, float i0, const Spot& sp) {
+  if (sp.model == 0) return loglik_gauss<MAXS>(pix, H, W, x, y, i0, sp);
+  return loglik_poisson<MAXS>(pix, H, W, x, y, i0, sp);
+}
+
+// Strided views: component arrays with element stride 1.
+template <int MAXS>
+__global__ void __launch_bounds__(256) k_loglik(const float* __restrict__ pix, i64 H, i64 W,
+                                                const float* __restrict__ xs,
+                                                const float* __restrict__ ys,
+                                                const float* __restrict__ is, i64 n, Spot sp,
+                                                float* __restrict__ out) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    out[i] = loglik_any<MAXS>(pix, H, W, __ldg(xs + i), __ldg(ys + i), __ldg(is + i), sp);
+}
+
+// Generic window (any halfwidth): gx/gy recomputed per pixel, fp32 core
+// identical per pixel to the MAXS form (same expressions, same order).
+__device__ __forceinline__ float loglik_gauss_generic(const float* __restrict__ pix, i64 H, i64 W,
+                                                      float x, float y, float i0, const Spot& sp) {
+  if (!(x == x) || !(y == y) || !(i0 == i0)) return __int_as_float(0x7fc00000);
+  int xlo, xhi, ylo, yhi;
+  window_axis((double)x, sp.hw, W, xlo, xhi);
+  window_axis((double)y, sp.hw, H, ylo, yhi);
+  double ssd = 0.0;
+  for (int yy = ylo; yy <= yhi; ++yy) {
+    float d = __double2float_rn((double)yy - (double)y);
+    float gy = expf(-(d * d) * sp.inv2s2);
+    float acc = 0.0f;
+    const float* row = pix + (i64)yy * W;
+    for (int xx = xlo; xx <= xhi; ++xx) {
+      float dx = __double2float_rn((double)xx - (double)x);
+      float ag = i0 * expf(-(dx * dx) * sp.inv2s2);
+      float r = __ldg(row + xx) - fmaf(ag, gy, sp.bg);
+      acc = fmaf(r, r, acc);
+    }
+    ssd += (double)acc;
+  }
+  return __double2float_rn(-ssd * sp.inv_2sxi2);
+}
+
+__device__ __forceinline__ float loglik_poisson_generic(const float* __restrict__ pix, i64 H,
+                                                        i64 W, float x, float y, float i0,
+                                                        const Spot& sp) {
+  if (!(x == x) || !(y == y) || !(i0 == i0)) return __int_as_float(0x7fc00000);
+  int xlo, xhi, ylo, yhi;
+  window_axis((double)x, sp.hw, W, xlo, xhi);
+  window_axis((double)y, sp.hw, H, ylo, yhi);
+  const float inv_bg = 1.0f / sp.bg;
+  double ll = 0.0;
+  for (int yy = ylo; yy <= yhi; ++yy) {
+    float d = __double2float_rn((double)yy - (double)y);
+    float ey;
+    if (sp.model == 1) {
+      ey = sp.erf_scale * erf_diff((d - 0.5f) * sp.inv_sqrt2s, (d + 0.5f) * sp.inv_sqrt2s);
+    } else {
+      float t0 = d - 0.375f, t1 = d - 0.125f, t2 = d + 0.125f, t3 = d + 0.375f;
+      ey = 0.25f * (expf(-(t0 * t0) * sp.inv2s2) + expf(-(t1 * t1) * sp.inv2s2) +
+                    expf(-(t2 * t2) * sp.inv2s2) + expf(-(t3 * t3) * sp.inv2s2));
+    }
+    float acc = 0.0f;
+    const float* row = pix + (i64)yy * W;
+    for (int xx = xlo; xx <= xhi; ++xx) {
+      float dx = __double2float_rn((double)xx - (double)x);
+      float e;
+      if (sp.model == 1) {
+        e = sp.erf_scale * erf_diff((dx - 0.5f) * sp.inv_sqrt2s, (dx + 0.5f) * sp.inv_sqrt2s);
+      } else {
+        float t0 = dx - 0.375f, t1 = dx - 0.125f, t2 = dx + 0.125f, t3 = dx + 0.375f;
+        e = 0.25f * (expf(-(t0 * t0) * sp.inv2s2) + expf(-(t1 * t1) * sp.inv2s2) +
+                     expf(-(t2 * t2) * sp.inv2s2) + expf(-(t3 * t3) * sp.inv2s2));
+      }
+      float t = (i0 * e * inv_bg) * ey;
+      float z = __ldg(row + xx);
+      acc += fmaf(z, log1pf(t), -t * sp.bg);
+    }
+    ll += (double)acc;
+  }
+  return __double2float_rn(ll);
+}
+
+__global__ void __launch_bounds__(256) k_loglik_generic(const float* __restrict__ pix, i64 H, i64 W,
+                                                        const float* __restrict__ xs,
+                                                        const float* __restrict__ ys,
+                                                        const float* __restrict__ is, i64 n,
+                                                        Spot sp, float* __restrict__ out) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    float x = __ldg(xs + i), y = __ldg(ys + i), i0 = __ldg(is + i);
+    out[i] = (sp.model == 0) ? loglik_gauss_generic(pix, H, W, x, y, i0, sp)
+                             : loglik_poisson_generic(pix, H, W, x, y, i0, sp);
+  }
+}
+
+// ---- float64 drop-in operator: spot_window_ssd (_speedups.pyx:42-83) ------
+// Same operation order as the Cython loop, FMA contraction disabled.
+__global__ void __launch_bounds__(128) k_ssd_f64(const double* __restrict__ pix, i64 H, i64 W,
+                                                 const double* __restrict__ xs,
+                                                 const double* __restrict__ ys,
+                                                 const double* __restrict__ is, i64 n,
+                                                 double inv2s2, double bg, int hw,
+                                                 double* __restrict__ out) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+    double x0 = xs[i], y0 = ys[i], amp = is[i];
+    int xlo, xhi, ylo, yhi;
+    window_axis(x0, hw, W, xlo, xhi);
+    window_axis(y0, hw, H, ylo, yhi);
+    double ssd = 0.0;
+    for (int yy = ylo; yy <= yhi; ++yy) {
+      double d = __dsub_rn((double)yy, y0);
+      double gyv = exp(__dmul_rn(__dmul_rn(-d, d), inv2s2));
+      const double* row = pix + (i64)yy * W;
+      for (int xx = xlo; xx <= xhi; ++xx) {
+        double dx = __dsub_rn((double)xx, x0);
+        double gx = exp(__dmul_rn(__dmul_rn(-dx, dx), inv2s2));
+        double pred = __dadd_rn(__dmul_rn(__dmul_rn(amp, gx), gyv), bg);
+        double r = __dsub_rn(row[xx], pred);
+        ssd = __dadd_rn(ssd, __dmul_rn(r, r));
+      }
+    }
+    out[i] = ssd;
+  }
+}
+
+}  // namespace pcs

@@ -1,0 +1,236 @@
+"""Filter steps and whole tracks on the device: golden steps from the
+reference (replayed draws), fused device loop == general driver bit-for-bit,
+pcSIR with sub-spacing cells == SIR bit-for-bit, oracle replay of the device's
+own draws, driver semantics (degenerate frame index, point mass, no-resample)."""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1310_5541_b200 as pc
+from conftest import golden, spot_pixels
+from oracle import pcsir_oracle as orc
+from paper_1310_5541_b200 import rng as prng_mod
+from paper_1310_5541_b200 import state
+
+pytestmark = pytest.mark.gpu
+
+W_RTOL = 1e-5
+
+
+# --- golden single steps (sis_step / pc_sis_step with the reference's draws) ----------
+def test_sis_step_golden(cuda):
+    g = golden("steps")
+    frame = pc.ImageFrame(g["frame"])
+    lik = pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(10.0, 5))
+    ps = pc.ParticleSet(g["states"], g["weights"])
+    out = pc.sis_step(ps, frame, lik, pc.DynamicsParams(0.5, 0.1, 1.0),
+                      prng_mod.ReplayNormals(g["normals"]))
+    assert np.array_equal(out.states, g["sis_states"].astype(np.float32))
+    # weights: the reference's float64 values within 1e-5 (float32 state path);
+    # compare normalised weights (the scale carries the reference's w_prev)
+    np.testing.assert_allclose(pc.normalize(out).weights, orc.normalize(g["sis_weights"]),
+                               rtol=W_RTOL, atol=1e-12)
+
+
+@pytest.mark.parametrize("cpp", [1, 2, 4])
+def test_pc_sis_step_golden(cuda, cpp):
+    g = golden("steps")
+    frame = pc.ImageFrame(g["frame"])
+    grid = pc.BinGrid.pixel_aligned(frame.width, frame.height, cpp)
+    lik = pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(10.0, 5))
+    ps = pc.ParticleSet(g["states"], g["weights"])
+    out, occ = pc.pc_sis_step(ps, frame, lik, pc.DynamicsParams(0.5, 0.1, 1.0), grid,
+                              pc.DummyPlacement.CENTER_OF_MASS,
+                              prng_mod.ReplayNormals(g["normals"]))
+    assert occ == int(g[f"pc{cpp}_occ"])                 # bit-exact occupied-bin count
+    assert lik.evals == int(g[f"pc{cpp}_evals"])
+    assert np.array_equal(out.states, g[f"pc{cpp}_states"].astype(np.float32))
+    np.testing.assert_allclose(pc.normalize(out).weights, orc.normalize(g[f"pc{cpp}_weights"]),
+                               rtol=W_RTOL, atol=1e-12)
+
+
+def test_weight_ratios_identical_within_cells(cuda):
+    # test_binning.py:146-162: broadcast of one likelihood per occupied cell
+    rng = np.random.default_rng(4)
+    frame = pc.ImageFrame(spot_pixels(20.0, 20.0, 22.0, 1.16, 10.0, 40, 40))
+    st = np.zeros((200, 5))
+    st[:, :2] = rng.uniform(15, 25, size=(200, 2))
+    st[:, 4] = 22.0
+    w0 = rng.uniform(0.1, 2.0, 200)
+    ps = pc.ParticleSet(st, w0)
+    grid = pc.BinGrid.pixel_aligned(40, 40, 1)
+    lik = pc.SpotLikelihood(pc.PsfParams(1.16, 10.0), pc.LikelihoodParams(10.0, 4))
+    out, occ = pc.pc_sis_step(ps, frame, lik, pc.DynamicsParams(0.0, 0.0, 0.0), grid,
+                              pc.DummyPlacement.CENTER_OF_MASS, pc.PhiloxRng(0))
+    assert lik.evals == occ
+    occ_map = pc.assign_bins(out, grid)
+    assert len(occ_map.members) == occ
+    ratios = out.weights / ps.weights
+    for idx in occ_map.members.values():
+        np.testing.assert_allclose(ratios[idx], ratios[idx][0], rtol=1e-12)
+
+
+# --- whole tracks ------------------------------------------------------------------------
+def _c1_like(n=2000, k=12, seed=0, width=64):
+    rng = np.random.default_rng(seed)
+    frames, truth = [], []
+    x, y = 20.0, 32.0
+    for _ in range(k):
+        x += 0.5
+        truth.append((x, y))
+        frames.append(pc.ImageFrame(rng.poisson(spot_pixels(x, y, 20.0, 1.5, 10.0, width, width))
+                                    .astype(np.float64)))
+    init = pc.InitSpec(pc.StateVector(20.0, 32.0, 0.5, 0.0, 20.0), "gauss", sigma=2.0)
+    dyn = pc.DynamicsParams(0.5, 0.1, 1.0)
+    return frames, np.array(truth), init, dyn
+
+
+def _lik():
+    return pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(10.0, 5))
+
+
+RES = pc.ResampleConfig(1.0, "systematic")
+
+
+@pytest.mark.parametrize("cpp,placement", [(1, "com"), (4, "com"), (2, "coc"), (1, "coc")])
+def test_fused_pcsir_equals_general(cuda, cpp, placement):
+    frames, truth, init, dyn = _c1_like()
+    pl = pc.DummyPlacement.CENTER_OF_MASS if placement == "com" else pc.DummyPlacement.CELL_CENTER
+    cfg = pc.PcFilterConfig(2000, init, dyn, RES, _lik(),
+                            grid=pc.BinGrid.pixel_aligned(64, 64, cpp), placement=pl)
+    a = pc.pcsir_track(frames, cfg, pc.PhiloxRng(5), fused=True)
+    cfg2 = pc.PcFilterConfig(2000, init, dyn, RES, _lik(),
+                             grid=pc.BinGrid.pixel_aligned(64, 64, cpp), placement=pl)
+    b = pc.pcsir_track(frames, cfg2, pc.PhiloxRng(5), fused=False)
+    assert a.path == "fused" and b.path == "general"
+    assert np.array_equal(a.estimates, b.estimates)
+    assert np.array_equal(a.ess, b.ess)
+    assert np.array_equal(a.resampled, b.resampled)
+    assert a.likelihood_evals == b.likelihood_evals == cfg.likelihood.evals
+    rmse = np.sqrt(np.mean(np.sum((a.positions - truth) ** 2, axis=1)))
+    assert rmse < 0.75
+
+
+def test_fused_sir_equals_general(cuda):
+    frames, truth, init, dyn = _c1_like()
+    a = pc.sir_track(frames, pc.FilterConfig(2000, init, dyn, RES, _lik()), pc.PhiloxRng(9),
+                     fused=True)
+    b = pc.sir_track(frames, pc.FilterConfig(2000, init, dyn, RES, _lik()), pc.PhiloxRng(9),
+                     fused=False)
+    assert a.path == "fused" and b.path == "general"
+    assert np.array_equal(a.estimates, b.estimates)
+    assert np.array_equal(a.ess, b.ess)
+    assert a.likelihood_evals == 2000 * len(frames)
+
+
+def test_pcsir_tiny_cells_bitidentical_to_sir(cuda):
+    # SPEC acceptance #1 / test_binning.py:208-226: 1e-5 px cells (64-bit keys)
+    frames, truth, init, dyn = _c1_like(n=500, k=10)
+    init = pc.InitSpec(pc.StateVector(20.0, 32.0, 0.5, 0.0, 20.0), "point")
+    sir = pc.sir_track(frames, pc.FilterConfig(500, init, dyn, RES, _lik()), pc.PhiloxRng(11))
+    tiny = pc.BinGrid(-0.5, -0.5, 1e-5, 1e-5, 64 * 10 ** 5, 64 * 10 ** 5)
+    pcr = pc.pcsir_track(frames, pc.PcFilterConfig(500, init, dyn, RES, _lik(), grid=tiny),
+                         pc.PhiloxRng(11))
+    assert np.array_equal(sir.estimates, pcr.estimates)
+    assert np.array_equal(sir.ess, pcr.ess)
+    assert np.array_equal(sir.resampled, pcr.resampled)
+
+
+def test_track_replays_into_oracle(cuda):
+    """The oracle's restatement of the reference driver, fed the device's own
+    draws, reproduces the device estimates (first frames before any
+    rounding-induced divergence) within 1e-5 and the same RMSE regime."""
+    frames, truth, init, dyn = _c1_like(n=3000, k=8)
+    seed = 21
+    r = pc.pcsir_track(frames, pc.PcFilterConfig(3000, init, dyn, RES, _lik(),
+                                                 grid=pc.BinGrid.pixel_aligned(64, 64, 1)),
+                       pc.PhiloxRng(seed))
+
+    def dev_normals(f, n):
+        return state.device_normals(seed, f, n).double().cpu().numpy()
+
+    def dev_init(n):
+        z = torch.empty((2, n), dtype=torch.float32, device="cuda")
+        from paper_1310_5541_b200 import _lib
+        _lib.check(_lib.lib().pcs_philox_init_normals(seed, 0, n, _lib.ptr(z), n, _lib.stream()))
+        return z.double().cpu().numpy()
+
+    replay = orc.PhiloxReplay(seed, normals_fn=dev_normals, init_fn=dev_init)
+    lik = orc.SpotModel(1.5, 10.0, 10.0, 5)
+    est, ess, res, evals = orc.track([f.pixels for f in frames], 3000,
+                                     [20.0, 32.0, 0.5, 0.0, 20.0], 2.0, [0.5, 0.5, 0.1, 0.1, 1.0],
+                                     1.0, lik, replay, grid=(-0.5, -0.5, 1.0, 1.0, 64, 64))
+    np.testing.assert_allclose(r.estimates[0], est[0], rtol=W_RTOL)
+    assert r.ess[0] == pytest.approx(ess[0], rel=W_RTOL)
+    rm_dev = np.sqrt(np.mean(np.sum((r.positions - truth) ** 2, axis=1)))
+    rm_orc = np.sqrt(np.mean(np.sum((est[:, :2] - truth) ** 2, axis=1)))
+    assert abs(rm_dev - rm_orc) < 0.1
+
+
+def test_point_mass_single_frame_exact(cuda):
+    truth = pc.StateVector(20.0, 24.0, 0.0, 0.0, 22.0)
+    frame = pc.ImageFrame(spot_pixels(20.0, 24.0, 22.0, 1.16, 10.0, 48, 48))
+    lik = pc.SpotLikelihood(pc.PsfParams(1.16, 10.0), pc.LikelihoodParams(10.0, 4))
+    cfg = pc.FilterConfig(16, pc.InitSpec(truth, "point"), pc.DynamicsParams(0.0, 0.0, 0.0),
+                          likelihood=lik)
+    result = pc.sir_track([frame], cfg, pc.PhiloxRng(0))
+    assert np.array_equal(result.estimates[0], truth.as_array())
+
+
+class ConstantLikelihood:
+    def __init__(self, value):
+        self.value = value
+
+    def batch(self, states, frame):
+        return np.full(states.shape[0], self.value)
+
+
+def test_constant_likelihood_never_resamples(cuda):
+    frames = [pc.ImageFrame(np.zeros((8, 8)))] * 12
+    init = pc.InitSpec(pc.StateVector(4, 4, 0, 0, 1.0), "uniform", width=2.0)
+    cfg = pc.FilterConfig(64, init, pc.DynamicsParams(0.1, 0.1, 0.0),
+                          pc.ResampleConfig(threshold_fraction=0.99),
+                          likelihood=ConstantLikelihood(0.5))
+    result = pc.sir_track(frames, cfg, pc.PhiloxRng(3))
+    assert not result.resampled.any()
+    np.testing.assert_allclose(result.ess, 64.0, rtol=1e-6)
+
+
+def test_degenerate_error_carries_frame_index(cuda):
+    class DiesOnThird(ConstantLikelihood):
+        def __init__(self):
+            super().__init__(1.0)
+            self.calls = 0
+
+        def batch(self, states, frame):
+            self.calls += 1
+            if self.calls == 3:
+                return np.zeros(states.shape[0])
+            return super().batch(states, frame)
+
+    frames = [pc.ImageFrame(np.zeros((8, 8)))] * 3
+    cfg = pc.FilterConfig(8, pc.InitSpec(pc.StateVector(4, 4, 0, 0, 1)),
+                          pc.DynamicsParams(0.0, 0.0, 0.0), likelihood=DiesOnThird())
+    with pytest.raises(pc.DegenerateWeightsError) as err:
+        pc.sir_track(frames, cfg, pc.PhiloxRng(0))
+    assert err.value.frame_index == 2
+
+
+def test_tracking_is_deterministic(cuda):
+    frames, truth, init, dyn = _c1_like(n=4000, k=6)
+    cfg = lambda: pc.PcFilterConfig(4000, init, dyn, RES, _lik(),  # noqa: E731
+                                    grid=pc.BinGrid.pixel_aligned(64, 64, 4))
+    a = pc.pcsir_track(frames, cfg(), pc.PhiloxRng(42))
+    b = pc.pcsir_track(frames, cfg(), pc.PhiloxRng(42))
+    assert np.array_equal(a.estimates, b.estimates) and np.array_equal(a.ess, b.ess)
+
+
+def test_eval_count_is_occupied_cells(cuda):
+    frames, truth, init, dyn = _c1_like(n=10000, k=5)
+    lik = _lik()
+    r = pc.pcsir_track(frames, pc.PcFilterConfig(10000, init, dyn, RES, lik,
+                                                 grid=pc.BinGrid.pixel_aligned(64, 64, 1)),
+                       pc.PhiloxRng(1))
+    assert r.likelihood_evals == lik.evals
+    assert r.likelihood_evals < 10000 * len(frames) / 10
