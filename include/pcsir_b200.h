@@ -122,7 +122,7 @@ int pcs_spot_window_ssd_f64(const double* pixels, int64_t height, int64_t width,
  * (e.g. rows of a SoA state block). */
 int pcs_loglik(const float* pixels, int64_t height, int64_t width, const float* xs,
                const float* ys, const float* i0s, int64_t n, const pcs_spot_t* spot,
-               float* out_loglik, void* stream);
+               double* out_loglik, void* stream);
 
 /* ---- _partition + _dummy_states (binning.py:97-112,157-172), general
  * sort path (any grid size, 64-bit keys).
@@ -146,7 +146,7 @@ int pcs_dummies(pcs_ctx* ctx, const float* states, int64_t ld, int64_t n, const 
  * broadcast) or identity (bin_of NULL). The prior is prior_logw (float64
  * log-weights) if given, else prior_w (float32 linear weights) if given,
  * else uniform (constant dropped). */
-int pcs_weight_update(const float* prior_w, const double* prior_logw, const float* loglik,
+int pcs_weight_update(const float* prior_w, const double* prior_logw, const double* loglik,
                       const int32_t* bin_of, int64_t n, double* logw, void* stream);
 /* normalize (filtering.py:75-85) in the log domain; writes float32
  * normalised weights and returns max/normaliser. *degenerate set when every

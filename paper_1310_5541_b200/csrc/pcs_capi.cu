@@ -369,7 +369,7 @@ int pcs_spot_window_ssd_f64(const double* pixels, int64_t H, int64_t W, const do
 }
 
 int pcs_loglik(const float* pixels, int64_t H, int64_t W, const float* xs, const float* ys,
-               const float* is, int64_t n, const pcs_spot_t* spot, float* out, void* stream) {
+               const float* is, int64_t n, const pcs_spot_t* spot, double* out, void* stream) {
   int r = check_spot(spot);
   if (r) return r;
   PCS_CHECK_ARG(pixels && xs && ys && is && out && H >= 1 && W >= 1 && n >= 0, "bad arguments");
@@ -380,7 +380,7 @@ int pcs_loglik(const float* pixels, int64_t H, int64_t W, const float* xs, const
     case 9: k_loglik<9><<<g, 256, 0, S(stream)>>>(pixels, H, W, xs, ys, is, n, sp, out); break;
     case 11: k_loglik<11><<<g, 256, 0, S(stream)>>>(pixels, H, W, xs, ys, is, n, sp, out); break;
     case 15: k_loglik<15><<<g, 256, 0, S(stream)>>>(pixels, H, W, xs, ys, is, n, sp, out); break;
-    default: k_loglik_generic<<<g, 256, 0, S(stream)>>>(pixels, H, W, xs, ys, is, n, sp, out);
+    default: k_loglik<0><<<g, 256, 0, S(stream)>>>(pixels, H, W, xs, ys, is, n, sp, out);
   }
   PCS_LAUNCH_CHECK();
   return PCS_OK;
@@ -480,7 +480,7 @@ int pcs_dummies(pcs_ctx* ctx, const float* states, int64_t ld, int64_t n, const 
 // ---------------------------------------------------------------------------
 // weights
 // ---------------------------------------------------------------------------
-int pcs_weight_update(const float* prior_w, const double* prior_logw, const float* ll,
+int pcs_weight_update(const float* prior_w, const double* prior_logw, const double* ll,
                       const int32_t* bin_of, int64_t n, double* logw, void* stream) {
   PCS_CHECK_ARG(ll && logw && n >= 1, "bad arguments");
   k_weight_update<<<grid_for(n, 256, 148), 256, 0, S(stream)>>>(prior_w, prior_logw, ll, bin_of, n,
@@ -744,7 +744,7 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   PCS_SCRATCH(SL_TR_TILES, T.ntiles * sizeof(u128), T.tile_tot);
   PCS_SCRATCH(SL_TR_PRE, T.ntiles * sizeof(u128), T.tile_pre);
   if (cfg->method == 0) {
-    PCS_SCRATCH(SL_TR_LL, ld * sizeof(float), P.ll);
+    PCS_SCRATCH(SL_TR_LL, ld * sizeof(double), P.ll);
     P.pslot = nullptr;
   } else {
     PCS_SCRATCH(SL_TR_PSLOT, ld * sizeof(u32), P.pslot);

@@ -4,6 +4,11 @@
 // SSD), imaging.py:125-137 (exp(-ssd/(2 sigma_xi^2))). Window convention:
 // centre pixel floor(p + 0.5), each bound clamped to the frame independently
 // (_speedups.pyx:47-68) so far-out states see a border strip, never an error.
+//
+// Precision contract: per-pixel prediction in float32, each
+// squared residual r*r added EXACTLY into a float64 accumulator (r is float32,
+// so r*r is exact in float64), log-likelihood returned in float64. The
+// remaining error is the float32 rounding of the predicted pixel value.
 #pragma once
 #include "pcs_common.cuh"
 
@@ -31,16 +36,17 @@ __device__ __forceinline__ void window_axis(double p, int hw, i64 extent, int& l
   hi = (int)h;
 }
 
-// ---- Gaussian windowed SSD, float32 core (CANONICAL hot-path arithmetic) ----
-//   gx[i] = expf(-(d*d) * inv2s2), d = RN32(xi - x)          (fp32)
-//   pred  = fmaf(I0*gx[i], gy[j], bg); r = p - pred           (fp32)
-//   row   = sum_i fmaf(r, r, row)                             (fp32, per row)
-//   ssd   = sum_rows (double)row                              (fp64)
-//   ll    = RN32(-ssd * inv_2sxi2)
+__device__ __forceinline__ double nan_ll() { return __longlong_as_double(0x7ff8000000000000ll); }
+
+// ---- Gaussian windowed SSD (CANONICAL hot-path arithmetic) ----------------
+//   gx[i] = expf(-(d*d) * inv2s2), d = RN32(xi - x)        (fp32)
+//   pred  = fmaf(I0*gx[i], gy[j], bg); r = p - pred         (fp32)
+//   ssd   = sum fma((double)r, (double)r, ssd)              (fp64, exact terms)
+//   ll    = -ssd * inv_2sxi2                                (fp64)
 template <int MAXS>
-__device__ __forceinline__ float loglik_gauss(const float* __restrict__ pix, i64 H, i64 W, float x,
-                                              float y, float i0, const Spot& sp) {
-  if (!(x == x) || !(y == y) || !(i0 == i0)) return __int_as_float(0x7fc00000);
+__device__ __forceinline__ double loglik_gauss(const float* __restrict__ pix, i64 H, i64 W, float x,
+                                               float y, float i0, const Spot& sp) {
+  if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
   int xlo, xhi, ylo, yhi;
   window_axis((double)x, sp.hw, W, xlo, xhi);
   window_axis((double)y, sp.hw, H, ylo, yhi);
@@ -58,18 +64,16 @@ __device__ __forceinline__ float loglik_gauss(const float* __restrict__ pix, i64
   for (int j = 0; j < ny; ++j) {
     float d = __double2float_rn((double)(ylo + j) - (double)y);
     float gy = expf(-(d * d) * sp.inv2s2);
-    float acc = 0.0f;
 #pragma unroll
     for (int i = 0; i < MAXS; ++i) {
       if (i < nx) {
         float r = __ldg(row + i) - fmaf(ag[i], gy, sp.bg);
-        acc = fmaf(r, r, acc);
+        ssd = fma((double)r, (double)r, ssd);
       }
     }
-    ssd += (double)acc;
     row += W;
   }
-  return __double2float_rn(-ssd * sp.inv_2sxi2);
+  return -ssd * sp.inv_2sxi2;
 }
 
 // ---- Poisson log-likelihood ratio vs background (config 3, new) -------------
@@ -88,10 +92,23 @@ __device__ __forceinline__ float erf_diff(float a, float b) {
   return erff(b) - erff(a);
 }
 
+__device__ __forceinline__ float psf_axis(float d, const Spot& sp) {
+  if (sp.model == 1)
+    return sp.erf_scale * erf_diff((d - 0.5f) * sp.inv_sqrt2s, (d + 0.5f) * sp.inv_sqrt2s);
+  float t0 = d - 0.375f, t1 = d - 0.125f, t2 = d + 0.125f, t3 = d + 0.375f;
+  return 0.25f * (expf(-(t0 * t0) * sp.inv2s2) + expf(-(t1 * t1) * sp.inv2s2) +
+                  expf(-(t2 * t2) * sp.inv2s2) + expf(-(t3 * t3) * sp.inv2s2));
+}
+
+__device__ __forceinline__ double poisson_term(float z, float t, float bg) {
+  // z log1p(mu/bg) - mu with t = mu/bg, accumulated in float64
+  return (double)fmaf(z, log1pf(t), -t * bg);
+}
+
 template <int MAXS>
-__device__ __forceinline__ float loglik_poisson(const float* __restrict__ pix, i64 H, i64 W, float x,
-                                                float y, float i0, const Spot& sp) {
-  if (!(x == x) || !(y == y) || !(i0 == i0)) return __int_as_float(0x7fc00000);
+__device__ __forceinline__ double loglik_poisson(const float* __restrict__ pix, i64 H, i64 W,
+                                                 float x, float y, float i0, const Spot& sp) {
+  if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
   int xlo, xhi, ylo, yhi;
   window_axis((double)x, sp.hw, W, xlo, xhi);
   window_axis((double)y, sp.hw, H, ylo, yhi);
@@ -102,67 +119,35 @@ __device__ __forceinline__ float loglik_poisson(const float* __restrict__ pix, i
   for (int i = 0; i < MAXS; ++i) {
     if (i < nx) {
       float d = __double2float_rn((double)(xlo + i) - (double)x);
-      float e;
-      if (sp.model == 1) {
-        e = sp.erf_scale * erf_diff((d - 0.5f) * sp.inv_sqrt2s, (d + 0.5f) * sp.inv_sqrt2s);
-      } else {
-        float t0 = d - 0.375f, t1 = d - 0.125f, t2 = d + 0.125f, t3 = d + 0.375f;
-        e = 0.25f * (expf(-(t0 * t0) * sp.inv2s2) + expf(-(t1 * t1) * sp.inv2s2) +
-                     expf(-(t2 * t2) * sp.inv2s2) + expf(-(t3 * t3) * sp.inv2s2));
-      }
-      ex[i] = i0 * e * inv_bg;   // mu/bg along x (times Ey later)
+      ex[i] = i0 * psf_axis(d, sp) * inv_bg;   // mu/bg along x (times Ey later)
     }
   }
   double ll = 0.0;
   const float* row = pix + (i64)ylo * W + xlo;
   for (int j = 0; j < ny; ++j) {
-    float d = __double2float_rn((double)(ylo + j) - (double)y);
-    float ey;
-    if (sp.model == 1) {
-      ey = sp.erf_scale * erf_diff((d - 0.5f) * sp.inv_sqrt2s, (d + 0.5f) * sp.inv_sqrt2s);
-    } else {
-      float t0 = d - 0.375f, t1 = d - 0.125f, t2 = d + 0.125f, t3 = d + 0.375f;
-      ey = 0.25f * (expf(-(t0 * t0) * sp.inv2s2) + expf(-(t1 * t1) * sp.inv2s2) +
-                    expf(-(t2 * t2) * sp.inv2s2) + expf(-(t3 * t3) * sp.inv2s2));
-    }
-    float acc = 0.0f;
+    float ey = psf_axis(__double2float_rn((double)(ylo + j) - (double)y), sp);
 #pragma unroll
-    for (int i = 0; i < MAXS; ++i) {
-      if (i < nx) {
-        float t = ex[i] * ey;                   // mu / bg
-        float z = __ldg(row + i);
-        acc += fmaf(z, log1pf(t), -t * sp.bg);  // z log1p(mu/bg) - mu
-      }
-    }
-    ll += (double)acc;
+    for (int i = 0; i < MAXS; ++i)
+      if (i < nx) ll += poisson_term(__ldg(row + i), ex[i] * ey, sp.bg);
     row += W;
   }
-  return __double2float_rn(ll);
+  return ll;
 }
 
 template <int MAXS>
-__device__ __forceinline__ float loglik_any(const float* __restrict__ pix, i64 H, i64 W, float x,
-                                            float y, float i0, const Spot& sp) {
+__device__ __forceinline__ double loglik_any(const float* __restrict__ pix, i64 H, i64 W, float x,
+                                             float y, float i0, const Spot& sp) {
   if (sp.model == 0) return loglik_gauss<MAXS>(pix, H, W, x, y, i0, sp);
   return loglik_poisson<MAXS>(pix, H, W, x, y, i0, sp);
 }
 
-// Strided views: component arrays with element stride 1.
-template <int MAXS>
-__global__ void __launch_bounds__(256) k_loglik(const float* __restrict__ pix, i64 H, i64 W,
-                                                const float* __restrict__ xs,
-                                                const float* __restrict__ ys,
-                                                const float* __restrict__ is, i64 n, Spot sp,
-                                                float* __restrict__ out) {
-  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
-    out[i] = loglik_any<MAXS>(pix, H, W, __ldg(xs + i), __ldg(ys + i), __ldg(is + i), sp);
-}
-
-// Generic window (any halfwidth): gx/gy recomputed per pixel, fp32 core
-// identical per pixel to the MAXS form (same expressions, same order).
-__device__ __forceinline__ float loglik_gauss_generic(const float* __restrict__ pix, i64 H, i64 W,
-                                                      float x, float y, float i0, const Spot& sp) {
-  if (!(x == x) || !(y == y) || !(i0 == i0)) return __int_as_float(0x7fc00000);
+// Generic window (any halfwidth): gx/gy recomputed per pixel; the per-pixel
+// expressions and the accumulation order are identical to the MAXS forms, so
+// results are bit-identical for any window size.
+__device__ __forceinline__ double loglik_gauss_generic(const float* __restrict__ pix, i64 H, i64 W,
+                                                       float x, float y, float i0,
+                                                       const Spot& sp) {
+  if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
   int xlo, xhi, ylo, yhi;
   window_axis((double)x, sp.hw, W, xlo, xhi);
   window_axis((double)y, sp.hw, H, ylo, yhi);
@@ -170,69 +155,59 @@ __device__ __forceinline__ float loglik_gauss_generic(const float* __restrict__ 
   for (int yy = ylo; yy <= yhi; ++yy) {
     float d = __double2float_rn((double)yy - (double)y);
     float gy = expf(-(d * d) * sp.inv2s2);
-    float acc = 0.0f;
     const float* row = pix + (i64)yy * W;
     for (int xx = xlo; xx <= xhi; ++xx) {
       float dx = __double2float_rn((double)xx - (double)x);
       float ag = i0 * expf(-(dx * dx) * sp.inv2s2);
       float r = __ldg(row + xx) - fmaf(ag, gy, sp.bg);
-      acc = fmaf(r, r, acc);
+      ssd = fma((double)r, (double)r, ssd);
     }
-    ssd += (double)acc;
   }
-  return __double2float_rn(-ssd * sp.inv_2sxi2);
+  return -ssd * sp.inv_2sxi2;
 }
 
-__device__ __forceinline__ float loglik_poisson_generic(const float* __restrict__ pix, i64 H,
-                                                        i64 W, float x, float y, float i0,
-                                                        const Spot& sp) {
-  if (!(x == x) || !(y == y) || !(i0 == i0)) return __int_as_float(0x7fc00000);
+__device__ __forceinline__ double loglik_poisson_generic(const float* __restrict__ pix, i64 H,
+                                                         i64 W, float x, float y, float i0,
+                                                         const Spot& sp) {
+  if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
   int xlo, xhi, ylo, yhi;
   window_axis((double)x, sp.hw, W, xlo, xhi);
   window_axis((double)y, sp.hw, H, ylo, yhi);
   const float inv_bg = 1.0f / sp.bg;
   double ll = 0.0;
   for (int yy = ylo; yy <= yhi; ++yy) {
-    float d = __double2float_rn((double)yy - (double)y);
-    float ey;
-    if (sp.model == 1) {
-      ey = sp.erf_scale * erf_diff((d - 0.5f) * sp.inv_sqrt2s, (d + 0.5f) * sp.inv_sqrt2s);
-    } else {
-      float t0 = d - 0.375f, t1 = d - 0.125f, t2 = d + 0.125f, t3 = d + 0.375f;
-      ey = 0.25f * (expf(-(t0 * t0) * sp.inv2s2) + expf(-(t1 * t1) * sp.inv2s2) +
-                    expf(-(t2 * t2) * sp.inv2s2) + expf(-(t3 * t3) * sp.inv2s2));
-    }
-    float acc = 0.0f;
+    float ey = psf_axis(__double2float_rn((double)yy - (double)y), sp);
     const float* row = pix + (i64)yy * W;
     for (int xx = xlo; xx <= xhi; ++xx) {
-      float dx = __double2float_rn((double)xx - (double)x);
-      float e;
-      if (sp.model == 1) {
-        e = sp.erf_scale * erf_diff((dx - 0.5f) * sp.inv_sqrt2s, (dx + 0.5f) * sp.inv_sqrt2s);
-      } else {
-        float t0 = dx - 0.375f, t1 = dx - 0.125f, t2 = dx + 0.125f, t3 = dx + 0.375f;
-        e = 0.25f * (expf(-(t0 * t0) * sp.inv2s2) + expf(-(t1 * t1) * sp.inv2s2) +
-                     expf(-(t2 * t2) * sp.inv2s2) + expf(-(t3 * t3) * sp.inv2s2));
-      }
-      float t = (i0 * e * inv_bg) * ey;
-      float z = __ldg(row + xx);
-      acc += fmaf(z, log1pf(t), -t * sp.bg);
+      float exi = i0 * psf_axis(__double2float_rn((double)xx - (double)x), sp) * inv_bg;
+      ll += poisson_term(__ldg(row + xx), exi * ey, sp.bg);
     }
-    ll += (double)acc;
   }
-  return __double2float_rn(ll);
+  return ll;
 }
 
-__global__ void __launch_bounds__(256) k_loglik_generic(const float* __restrict__ pix, i64 H, i64 W,
-                                                        const float* __restrict__ xs,
-                                                        const float* __restrict__ ys,
-                                                        const float* __restrict__ is, i64 n,
-                                                        Spot sp, float* __restrict__ out) {
-  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-    float x = __ldg(xs + i), y = __ldg(ys + i), i0 = __ldg(is + i);
-    out[i] = (sp.model == 0) ? loglik_gauss_generic(pix, H, W, x, y, i0, sp)
-                             : loglik_poisson_generic(pix, H, W, x, y, i0, sp);
-  }
+__device__ __forceinline__ double loglik_generic(const float* __restrict__ pix, i64 H, i64 W,
+                                                 float x, float y, float i0, const Spot& sp) {
+  return (sp.model == 0) ? loglik_gauss_generic(pix, H, W, x, y, i0, sp)
+                         : loglik_poisson_generic(pix, H, W, x, y, i0, sp);
+}
+
+// dispatch: MAXS > 0 -> register-resident window, MAXS == 0 -> generic
+template <int MAXS>
+__device__ __forceinline__ double loglik_dispatch(const float* __restrict__ pix, i64 H, i64 W,
+                                                  float x, float y, float i0, const Spot& sp) {
+  if constexpr (MAXS > 0) return loglik_any<MAXS>(pix, H, W, x, y, i0, sp);
+  else return loglik_generic(pix, H, W, x, y, i0, sp);
+}
+
+template <int MAXS>
+__global__ void __launch_bounds__(256) k_loglik(const float* __restrict__ pix, i64 H, i64 W,
+                                                const float* __restrict__ xs,
+                                                const float* __restrict__ ys,
+                                                const float* __restrict__ is, i64 n, Spot sp,
+                                                double* __restrict__ out) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    out[i] = loglik_dispatch<MAXS>(pix, H, W, __ldg(xs + i), __ldg(ys + i), __ldg(is + i), sp);
 }
 
 // ---- float64 drop-in operator: spot_window_ssd (_speedups.pyx:42-83) ------

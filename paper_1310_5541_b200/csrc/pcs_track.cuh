@@ -28,8 +28,9 @@ constexpr int BINS_BLOCK = 1024;
 struct TrackCtl {
   // ---- per frame (reset at the end of the frame for the next one)
   i64 bbox[4];          // ix_min, ix_max, iy_min, iy_max
-  int max_ll_ord;       // SIR: ordered-int max loglik
+  i64 max_ll_ord;       // SIR: ordered-int64 max loglik (float64)
   u32 n_occ;            // pcSIR: first-touch occupied list length
+  u32 wmin_bits, wmax_bits;  // SIR: min/max normalised weight (non-negative float bits)
   u64 S[2];             // SIR: normaliser
   u64 est[5][2];        // SIR: estimate numerators
   u64 w2[2];            // SIR: ESS denominator
@@ -69,7 +70,7 @@ struct TrackParams {
   float* buf0;
   float* buf1;
   int* anc;
-  float* ll;            // SIR
+  double* ll;           // SIR: per-particle log-likelihood (float64)
   u32* pslot;           // pcSIR
   u32* tab_cnt;
   u64* tab_sum;         // [5][TABLE_CAP][2]
@@ -88,8 +89,10 @@ __device__ __forceinline__ void reset_frame(TrackCtl* c) {
   c->bbox[1] = LLONG_MIN;
   c->bbox[2] = LLONG_MAX;
   c->bbox[3] = LLONG_MIN;
-  c->max_ll_ord = (int)0x80000000;
+  c->max_ll_ord = LLONG_MIN;
   c->n_occ = 0;
+  c->wmin_bits = 0xFFFFFFFFu;
+  c->wmax_bits = 0u;
   c->S[0] = c->S[1] = 0;
   for (int q = 0; q < 5; ++q) c->est[q][0] = c->est[q][1] = 0;
   c->w2[0] = c->w2[1] = 0;
@@ -285,9 +288,10 @@ __global__ void __launch_bounds__(ACC_BLOCK) k_pc_accumulate(TrackParams P, i64 
 template <int MAXS>
 __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P) {
   TrackCtl* C = P.ctl;
-  extern __shared__ __align__(16) float s_ll[];  // [MAXM]
+  extern __shared__ __align__(16) double s_ll[];  // [MAXM]
   __shared__ i128 s_red[BINS_BLOCK / 32];
-  __shared__ int s_max;
+  __shared__ long long s_max;
+  __shared__ unsigned s_wmin, s_wmax;
   const int t = threadIdx.x;
   const i64 k = C->k;
   const i64 ko = k - C->k_out;
@@ -303,10 +307,14 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P) {
   }
   const int M = (int)C->n_occ;
   const float* frame = C->frames + (k - C->k_frames) * P.H * P.W;
-  if (t == 0) s_max = (int)0x80000000;
+  if (t == 0) {
+    s_max = LLONG_MIN;
+    s_wmin = 0xFFFFFFFFu;
+    s_wmax = 0u;
+  }
   __syncthreads();
   // 1) dummies + likelihood
-  int lmax = (int)0x80000000;
+  long long lmax = LLONG_MIN;
   for (int b = t; b < M; b += BINS_BLOCK) {
     u32 cell = P.occ[b];
     u32 cnt = P.tab_cnt[cell];
@@ -321,23 +329,20 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P) {
       d[0] = __double2float_rn(__dadd_rn(P.grid.ox, __dmul_rn((double)ix + 0.5, P.grid.lx)));
       d[1] = __double2float_rn(__dadd_rn(P.grid.oy, __dmul_rn((double)iy + 0.5, P.grid.ly)));
     }
-    float ll = (MAXS > 0) ? loglik_any<(MAXS > 0 ? MAXS : 1)>(frame, P.H, P.W, d[0], d[1], d[4], P.spot)
-                          : ((P.spot.model == 0) ? loglik_gauss_generic(frame, P.H, P.W, d[0], d[1], d[4], P.spot)
-                                                 : loglik_poisson_generic(frame, P.H, P.W, d[0], d[1], d[4], P.spot));
+    double ll = loglik_dispatch<MAXS>(frame, P.H, P.W, d[0], d[1], d[4], P.spot);
     s_ll[b] = ll;
-    lmax = max(lmax, float_to_ordered(ll));
+    lmax = max(lmax, (long long)f64_to_ordered(ll));
   }
   atomicMax(&s_max, lmax);
   __syncthreads();
-  const float mf = ordered_to_float(s_max);
-  const double m = (double)mf;
-  const bool bad_m = !(mf == mf) || mf == INFINITY;
-  const bool degenerate = (mf == -INFINITY);
+  const double m = ordered_to_f64((i64)s_max);
+  const bool bad_m = !(m == m) || m == INFINITY;
+  const bool degenerate = (m == -INFINITY);
   // 2) normaliser S = sum_b cnt_b * round(exp(ll_b - m) * 2^95)
   i128 acc = 0;
   for (int b = t; b < M; b += BINS_BLOCK) {
     u32 cnt = P.tab_cnt[P.occ[b]];
-    acc += (i128)cnt * f64_to_fixed(exp(__dsub_rn((double)s_ll[b], m)), FX_S);
+    acc += (i128)cnt * f64_to_fixed(exp(__dsub_rn(s_ll[b], m)), FX_S);
   }
   i128 Sfix = block_sum_i128<BINS_BLOCK>(acc, s_red);
   __shared__ double s_Sf;
@@ -349,8 +354,10 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P) {
   for (int b = t; b < M; b += BINS_BLOCK) {
     u32 cell = P.occ[b];
     u32 cnt = P.tab_cnt[cell];
-    float w = __double2float_rn(__ddiv_rn(exp(__dsub_rn((double)s_ll[b], m)), Sf));
+    float w = normalised_weight(s_ll[b], m, Sf);
     P.wtab[cell] = w;
+    atomicMin(&s_wmin, __float_as_uint(w));
+    atomicMax(&s_wmax, __float_as_uint(w));
     i128 wq = f32_to_fixed(w, FX_WQ);
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
@@ -380,6 +387,9 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P) {
     for (int c = 0; c < 5; ++c) C->out_est[ko * 5 + c] = est[c];
     C->out_ess[ko] = ess;
     int res = (!flag_bad && ess < (double)P.n) ? 1 : 0;   // threshold_fraction = 1.0
+    // no resampling with unequal weights -> non-uniform prior next frame:
+    // only the general path carries per-particle prior weights
+    if (!res && !flag_bad && s_wmin != s_wmax) set_flag(C, PCS_FLAG_CAPACITY);
     C->out_res[ko] = (unsigned char)res;
     C->out_occ[ko] = M;
     C->evals += M;
@@ -405,7 +415,7 @@ __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
   const float* sin = (k & 1) ? P.buf1 : P.buf0;
   float* sout = (k & 1) ? P.buf0 : P.buf1;
   const float* frame = C->frames + (k - C->k_frames) * P.H * P.W;
-  int lmax = (int)0x80000000;
+  long long lmax = LLONG_MIN;
   bool bad = false;
   const i64 n = P.n, ld = P.ld;
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < n; j += (i64)gridDim.x * blockDim.x) {
@@ -417,16 +427,14 @@ __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
     propagate_one(s, z, P.dyn, o);
 #pragma unroll
     for (int c = 0; c < 5; ++c) sout[c * ld + j] = o[c];
-    float ll = (MAXS > 0) ? loglik_any<(MAXS > 0 ? MAXS : 1)>(frame, P.H, P.W, o[0], o[1], o[4], P.spot)
-                          : ((P.spot.model == 0) ? loglik_gauss_generic(frame, P.H, P.W, o[0], o[1], o[4], P.spot)
-                                                 : loglik_poisson_generic(frame, P.H, P.W, o[0], o[1], o[4], P.spot));
+    double ll = loglik_dispatch<MAXS>(frame, P.H, P.W, o[0], o[1], o[4], P.spot);
     P.ll[j] = ll;
     if (!(ll == ll) || ll == INFINITY) bad = true;
-    lmax = max(lmax, float_to_ordered(ll));
+    lmax = max(lmax, (long long)f64_to_ordered(ll));
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
-  if ((threadIdx.x & 31) == 0) atomicMax(&C->max_ll_ord, lmax);
+  if ((threadIdx.x & 31) == 0) atomicMax((long long*)&C->max_ll_ord, lmax);
   if (bad) set_flag(C, PCS_FLAG_NONFINITE);
 }
 
@@ -434,10 +442,10 @@ __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
 __global__ void __launch_bounds__(256) k_sir_sum(TrackParams P) {
   __shared__ i128 sh[8];
   TrackCtl* C = P.ctl;
-  const double m = (double)ordered_to_float(C->max_ll_ord);
+  const double m = ordered_to_f64(C->max_ll_ord);
   i128 acc = 0;
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < P.n; j += (i64)gridDim.x * blockDim.x)
-    acc += f64_to_fixed(exp(__dsub_rn((double)P.ll[j], m)), FX_S);
+    acc += f64_to_fixed(exp(__dsub_rn(P.ll[j], m)), FX_S);
   i128 t = block_sum_i128<256>(acc, sh);
   if (threadIdx.x == 0) atomic_add_i128(C->S, t);
 }
@@ -449,18 +457,20 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_sir_tiles_stats(TrackParams P,
   TrackCtl* C = P.ctl;
   const i64 k = C->k;
   const float* st = (k & 1) ? P.buf0 : P.buf1;
-  const float mf = ordered_to_float(C->max_ll_ord);
-  const double m = (double)mf;
+  const double m = ordered_to_f64(C->max_ll_ord);
   const double Sf = scalbn(i128_to_f64_rn(load_i128(C->S)), -FX_S);
   const i64 n = P.n, ld = P.ld;
   i64 base = (i64)blockIdx.x * SCAN_TILE;
   u128 acc = 0;
   i128 e[6] = {0, 0, 0, 0, 0, 0};
   bool range = false;
+  unsigned wmin = 0xFFFFFFFFu, wmax = 0u;
   for (int q = 0; q < SCAN_ITEMS; ++q) {
     i64 i = base + (i64)q * SCAN_BLOCK + threadIdx.x;
     if (i < n) {
-      float w = normalised_weight((double)P.ll[i], m, Sf);
+      float w = normalised_weight(P.ll[i], m, Sf);
+      wmin = min(wmin, __float_as_uint(w));
+      wmax = max(wmax, __float_as_uint(w));
       acc += cdf_fixed(w);
       i128 wq = f32_to_fixed(w, FX_WQ);
 #pragma unroll
@@ -480,13 +490,22 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_sir_tiles_stats(TrackParams P,
     if (threadIdx.x == 0) atomic_add_i128(c < 5 ? C->est[c] : C->w2, tt);
   }
   if (range) atomicOr(&C->flags, (u32)PCS_FLAG_RANGE);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    wmin = min(wmin, __shfl_xor_sync(0xffffffffu, wmin, o));
+    wmax = max(wmax, __shfl_xor_sync(0xffffffffu, wmax, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&C->wmin_bits, wmin);
+    atomicMax(&C->wmax_bits, wmax);
+  }
 }
 
 // SIR K4 (one thread): frame outputs and resampling decision
 __global__ void k_sir_finalize(TrackParams P) {
   TrackCtl* C = P.ctl;
   const i64 k = C->k, ko = k - C->k_out;
-  const float mf = ordered_to_float(C->max_ll_ord);
+  const double mf = ordered_to_f64(C->max_ll_ord);
   const bool degenerate = (mf == -INFINITY);
   const bool bad_m = !(mf == mf) || mf == INFINITY;
   double est[5];
@@ -500,11 +519,12 @@ __global__ void k_sir_finalize(TrackParams P) {
   if (degenerate) set_flag(C, PCS_FLAG_DEGENERATE);
   if (bad_m) set_flag(C, PCS_FLAG_NONFINITE);
   int res = (!flag_bad && ess < (double)P.n) ? 1 : 0;
+  if (!res && !flag_bad && C->wmin_bits != C->wmax_bits) set_flag(C, PCS_FLAG_CAPACITY);
   C->out_res[ko] = (unsigned char)res;
   C->out_occ[ko] = P.n;
   C->evals += P.n;
   C->do_resample = res;
-  C->m = (double)mf;
+  C->m = mf;
   C->Sf = scalbn(i128_to_f64_rn(load_i128(C->S)), -FX_S);
   C->u = philox_resample_u(P.seed, P.frame0 + (u32)k);
   reset_frame(C);
@@ -546,6 +566,6 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_track_emit(TrackParams P, const 
 }
 
 constexpr size_t ACC_SMEM = SUB_CELLS * (sizeof(u32) + 5 * sizeof(long long));
-constexpr size_t BINS_SMEM = MAXM * sizeof(float);
+constexpr size_t BINS_SMEM = MAXM * sizeof(double);
 
 }  // namespace pcs

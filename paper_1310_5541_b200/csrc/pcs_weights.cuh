@@ -62,10 +62,10 @@ struct NormCtl {
 // logw[i] = log(prior_w[i]) + ll[idx]  (float64; uniform prior drops log(1/N))
 __global__ void k_weight_update(const float* __restrict__ prior_w,
                                 const double* __restrict__ prior_logw,
-                                const float* __restrict__ ll, const int* __restrict__ bin_of,
+                                const double* __restrict__ ll, const int* __restrict__ bin_of,
                                 i64 n, double* __restrict__ logw) {
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-    double l = (double)ll[bin_of ? (i64)bin_of[i] : i];
+    double l = ll[bin_of ? (i64)bin_of[i] : i];
     double p = prior_logw ? prior_logw[i] : (prior_w ? log((double)prior_w[i]) : 0.0);
     logw[i] = __dadd_rn(p, l);
   }
@@ -151,13 +151,13 @@ struct WeightSrc {
   const float* w;
   const u32* slot;
   const float* wtab;
-  const float* ll;
+  const double* ll;
   double m, Sf;
   int kind;  // 0 direct, 1 table, 2 loglik
   __device__ __forceinline__ float get(i64 i) const {
     if (kind == 0) return w[i];
     if (kind == 1) return wtab[slot[i]];
-    return normalised_weight((double)ll[i], m, Sf);
+    return normalised_weight(ll[i], m, Sf);
   }
 };
 

@@ -79,14 +79,7 @@ def _weight_update(pset, ll, bin_of=None):
     """log w_new = log(w_prev) + ll[bin_of] in float64 (filtering.py:69, binning.py:190-192)."""
     n = pset.n
     dev = pset.soa.device
-    if ll.dtype == torch.float64:
-        # float64 values from a duck-typed host likelihood (conformance path only)
-        l64 = ll if bin_of is None else ll[bin_of.long()]
-        if pset.uniform:
-            return l64.clone()
-        if pset.w is not None:
-            return torch.log(pset.w.double()) + l64
-        return pset.logw + l64
+    ll = ll.to(dtype=torch.float64).contiguous()
     logw = torch.empty(n, dtype=torch.float64, device=dev)
     _lib.check(_lib.lib().pcs_weight_update(
         _lib.ptr(pset.w), _lib.ptr(pset.logw), _lib.ptr(ll), _lib.ptr(bin_of), n,

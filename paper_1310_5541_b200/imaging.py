@@ -125,9 +125,9 @@ class _DeviceLikelihood:
                             int(self.model))
 
     def loglik(self, soa, frame: ImageFrame, count=True):
-        """Log-likelihood of each state column of ``soa`` (5,M) float32 device."""
+        """Log-likelihood (float64) of each state column of ``soa`` (5,M) float32 device."""
         m = soa.shape[1]
-        out = torch.empty(m, dtype=torch.float32, device=soa.device)
+        out = torch.empty(m, dtype=torch.float64, device=soa.device)
         if m:
             pix = frame.device()
             spot = self.spot_c()

@@ -102,7 +102,7 @@ class ParticleSet:
     @classmethod
     def from_device(cls, soa, *, w=None, logw=None, uniform=False, timestep=0):
         obj = cls.__new__(cls)
-        obj.soa = soa
+        obj.soa = soa.contiguous()
         obj.timestep = int(timestep)
         obj.w = w
         obj.logw = logw
