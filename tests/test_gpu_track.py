@@ -16,6 +16,26 @@ from paper_1310_5541_b200 import state
 pytestmark = pytest.mark.gpu
 
 W_RTOL = 1e-5
+# The reference propagates in float64 and weights the UNROUNDED states; the
+# device state is float32 (bit-exact to float32(reference)). Position rounding
+# (<= 1e-6 px) moves log L by up to ~|dlogL/dx| * 1e-6, i.e. a few 1e-5 for
+# particles with large residuals — hence the looser tolerance when comparing
+# with the reference's float64-state weights. Stage-wise (oracle on the
+# device's own float32 states) the north-star 1e-5 holds.
+W_RTOL_F64_STATES = 2e-4
+
+
+def _oracle_weights(out_states32, prior, frame_pixels, lik_args, bin_map=None):
+    """Reference weighting (imaging.py:137, filtering.py:69 / binning.py:189-192)
+    on the device's float32 states; normalised (filtering.py:75-85)."""
+    st = out_states32.astype(np.float64)
+    if bin_map is None:
+        ll = orc.loglik_gauss(frame_pixels, st[:, 0], st[:, 1], st[:, 4], *lik_args)
+    else:
+        d, bin_of = bin_map
+        ll = orc.loglik_gauss(frame_pixels, d[0], d[1], d[4], *lik_args)[bin_of]
+    lw = np.log(prior) + ll
+    return orc.normalize(np.exp(lw - lw.max()))
 
 
 # --- golden single steps (sis_step / pc_sis_step with the reference's draws) ----------
@@ -27,10 +47,14 @@ def test_sis_step_golden(cuda):
     out = pc.sis_step(ps, frame, lik, pc.DynamicsParams(0.5, 0.1, 1.0),
                       prng_mod.ReplayNormals(g["normals"]))
     assert np.array_equal(out.states, g["sis_states"].astype(np.float32))
-    # weights: the reference's float64 values within 1e-5 (float32 state path);
-    # compare normalised weights (the scale carries the reference's w_prev)
-    np.testing.assert_allclose(pc.normalize(out).weights, orc.normalize(g["sis_weights"]),
-                               rtol=W_RTOL, atol=1e-12)
+    w = pc.normalize(out).weights
+    # stage-wise: oracle weighting of the device's float32 states
+    want = _oracle_weights(out.states, g["weights"], g["frame"].astype(np.float32).astype(float),
+                           (1.5, 10.0, 5, 10.0))
+    np.testing.assert_allclose(w, want, rtol=W_RTOL, atol=1e-12)
+    # against the reference's own float64-state weights
+    np.testing.assert_allclose(w, orc.normalize(g["sis_weights"]), rtol=W_RTOL_F64_STATES,
+                               atol=1e-12)
 
 
 @pytest.mark.parametrize("cpp", [1, 2, 4])
@@ -46,8 +70,19 @@ def test_pc_sis_step_golden(cuda, cpp):
     assert occ == int(g[f"pc{cpp}_occ"])                 # bit-exact occupied-bin count
     assert lik.evals == int(g[f"pc{cpp}_evals"])
     assert np.array_equal(out.states, g[f"pc{cpp}_states"].astype(np.float32))
-    np.testing.assert_allclose(pc.normalize(out).weights, orc.normalize(g[f"pc{cpp}_weights"]),
-                               rtol=W_RTOL, atol=1e-12)
+    w = pc.normalize(out).weights
+    # stage-wise: canonical dummies of the device states, oracle likelihood per bin
+    st32 = out.states.astype(np.float32)
+    gt = (grid.origin_x, grid.origin_y, grid.cell_width, grid.cell_height, grid.n_cols,
+          grid.n_rows)
+    _, order, unique, starts, counts = orc.partition(st32.astype(np.float64), gt)
+    bin_of = orc.bin_of_from_partition(len(st32), order, counts)
+    d = orc.dummies_exact(np.ascontiguousarray(st32.T), bin_of, counts).astype(np.float64)
+    want = _oracle_weights(st32, g["weights"], g["frame"].astype(np.float32).astype(float),
+                           (1.5, 10.0, 5, 10.0), (d, bin_of))
+    np.testing.assert_allclose(w, want, rtol=W_RTOL, atol=1e-12)
+    np.testing.assert_allclose(w, orc.normalize(g[f"pc{cpp}_weights"]),
+                               rtol=W_RTOL_F64_STATES, atol=1e-12)
 
 
 def test_weight_ratios_identical_within_cells(cuda):
