@@ -36,8 +36,10 @@ WORKLOADS = {
 VARIANTS = {"pcSIR-1px": 1.0, "pcSIR-0.5px": 0.5, "pcSIR-0.25px": 0.25, "pcSIR-2px": 2.0,
             "SIR": None}
 ALGO_BYTES = {  # algorithmic bytes per particle per launch
-    "k_pc_propagate": 44, "k_pc_accumulate": 24, "k_track_tiles": 8, "k_track_emit": 12,
-    "k_sir_propagate_lik": 48, "k_sir_sum": 4, "k_sir_tiles_stats": 24,
+    # pcSIR: R anc 4 + R state 20 + W state 20 + W cell 4; scan: R cell 4 + W ancestor 4
+    "k_pc_step1": 48, "k_scan_emit:pc": 8,
+    # SIR: + W loglik 8; sum: R 8; stats: R 8 + R 20; scan: R 8 + W 4
+    "k_sir_propagate_lik": 52, "k_sir_sum": 8, "k_sir_stats": 28, "k_scan_emit:sir": 12,
 }
 STEP_BYTES = 60  # canonical fused minimum per particle-update
 
@@ -335,7 +337,8 @@ def main():
                            min(args.steps, 20), args.seed, flush)
     dom = max(kprof, key=kprof.get)
     peak, peak_kind = peaks()
-    dom_bytes = ALGO_BYTES.get(dom, 0) * n
+    key = dom if dom != "k_scan_emit" else ("k_scan_emit:pc" if cpp_main else "k_scan_emit:sir")
+    dom_bytes = ALGO_BYTES.get(key, 0) * n
     achieved = dom_bytes / (kprof[dom] * 1e-3) / 1e9 if kprof[dom] > 0 else 0.0
     step_ms = total_ms / args.steps
     l2 = info["l2_bytes"]

@@ -56,11 +56,8 @@ struct TrackState {
   bool active = false;
   pcs_track_cfg_t cfg{};
   TrackParams P{};
-  i64 ntiles = 0;
-  u128* tile_tot = nullptr;
-  u128* tile_pre = nullptr;
-  int acc_grid = 0;
-  i64 acc_chunk = 0;
+  BinsScratch bins{};
+  int s1_grid = 0;
   int prop_grid = 0;
   int maxs = 0;
   i64 k = 0;             // host mirror of the frame counter
@@ -76,6 +73,7 @@ struct pcs_ctx {
   cudaStream_t cap = nullptr;
   TrackState tr;
   bool table_dirty = false;
+  i64 table_cells = 0;
   u32* tab_cnt = nullptr;
   u64* tab_sum = nullptr;
   float* wtab = nullptr;
@@ -604,8 +602,9 @@ int pcs_resample_multinomial(pcs_ctx* ctx, const float* w, int64_t n, const doub
   return PCS_OK;
 }
 
+
 // ---------------------------------------------------------------------------
-// fused track
+// fused track (device-resident loop, one CUDA graph per frame)
 // ---------------------------------------------------------------------------
 __global__ void k_iota(int* a, i64 n) {
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
@@ -618,7 +617,6 @@ __global__ void k_ctl_init(TrackCtl* C, double cx, double cy) {
   C->first_bad = INT_MAX;
   C->center[0] = cx;
   C->center[1] = cy;
-  C->table_ok = 1;
 }
 
 __global__ void k_ctl_io(TrackCtl* C, const float* frames, i64 kf, i64 ko, double* est,
@@ -632,6 +630,10 @@ __global__ void k_ctl_io(TrackCtl* C, const float* frames, i64 kf, i64 ko, doubl
   C->out_occ = occ;
 }
 
+static const char* kPcNames[] = {"k_pc_step1", "k_pc_bins", "k_scan_emit"};
+static const char* kSirNames[] = {"k_sir_propagate_lik", "k_sir_sum", "k_sir_stats",
+                                  "k_sir_finalize", "k_scan_emit"};
+
 // Enqueue one frame. If evs is non-null, evs[i] is recorded before launch i
 // and evs[launches] after the last one (per-kernel CUDA-event timing).
 static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullptr) {
@@ -644,22 +646,16 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
   };
   if (T.cfg.method == 1) {
     mark();
-    k_pc_propagate<<<T.prop_grid, 256, 0, st>>>(P);
-    mark();
-    k_pc_accumulate<<<T.acc_grid, ACC_BLOCK, ACC_SMEM, st>>>(P, T.acc_chunk);
+    k_pc_step1<<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(P);
     mark();
     switch (T.maxs) {
-      case 9: k_pc_bins<9><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P); break;
-      case 11: k_pc_bins<11><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P); break;
-      case 15: k_pc_bins<15><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P); break;
-      default: k_pc_bins<0><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P);
+      case 9: k_pc_bins<9><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P, T.bins); break;
+      case 11: k_pc_bins<11><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P, T.bins); break;
+      case 15: k_pc_bins<15><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P, T.bins); break;
+      default: k_pc_bins<0><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P, T.bins);
     }
     mark();
-    k_track_tiles<1><<<(unsigned)T.ntiles, SCAN_BLOCK, 0, st>>>(P, T.tile_tot);
-    mark();
-    k_scan_tiles<<<1, 1024, 0, st>>>(T.tile_tot, T.ntiles, T.tile_pre, &P.ctl->k);
-    mark();
-    k_track_emit<1><<<(unsigned)T.ntiles, SCAN_BLOCK, 0, st>>>(P, T.tile_pre);
+    k_scan_emit<1><<<(unsigned)P.ntiles, SCAN_BLOCK, 0, st>>>(P);
   } else {
     mark();
     switch (T.maxs) {
@@ -671,13 +667,11 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
     mark();
     k_sir_sum<<<grid_for(P.n, 256, ctx->sms), 256, 0, st>>>(P);
     mark();
-    k_sir_tiles_stats<<<(unsigned)T.ntiles, SCAN_BLOCK, 0, st>>>(P, T.tile_tot);
+    k_sir_stats<<<grid_for(P.n, 256, ctx->sms), 256, 0, st>>>(P);
     mark();
     k_sir_finalize<<<1, 1, 0, st>>>(P);
     mark();
-    k_scan_tiles<<<1, 1024, 0, st>>>(T.tile_tot, T.ntiles, T.tile_pre, &P.ctl->k);
-    mark();
-    k_track_emit<2><<<(unsigned)T.ntiles, SCAN_BLOCK, 0, st>>>(P, T.tile_pre);
+    k_scan_emit<2><<<(unsigned)P.ntiles, SCAN_BLOCK, 0, st>>>(P);
   }
   if (evs) cudaEventRecord(evs[q], st);
   PCS_LAUNCH_CHECK();
@@ -685,12 +679,23 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
   return PCS_OK;
 }
 
-static const char* kPcNames[] = {"k_pc_propagate", "k_pc_accumulate", "k_pc_bins",
-                                 "k_track_tiles", "k_scan_tiles", "k_track_emit"};
-static const char* kSirNames[] = {"k_sir_propagate_lik", "k_sir_sum", "k_sir_tiles_stats",
-                                  "k_sir_finalize", "k_scan_tiles", "k_track_emit"};
-
 static bool g_attr_done = false;
+
+static int set_attrs() {
+  if (g_attr_done) return PCS_OK;
+  PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_step1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)S1_SMEM));
+  PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)BINS_SMEM));
+  PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)BINS_SMEM));
+  PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)BINS_SMEM));
+  PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<15>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)BINS_SMEM));
+  g_attr_done = true;
+  return PCS_OK;
+}
 
 int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t W, void* stream) {
   PCS_CHECK_ARG(ctx && cfg, "bad arguments");
@@ -703,22 +708,15 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
     r = check_grid(&cfg->grid);
     if (r) return r;
     PCS_CHECK_ARG(cfg->placement == 0 || cfg->placement == 1, "unknown placement");
+    if ((double)cfg->grid.n_cols * (double)cfg->grid.n_rows > (double)TABLE_MAX) {
+      pcs_set_last_error("grid exceeds the fused dense-table capacity (2^28 cells)");
+      return PCS_E_CAPACITY;
+    }
   }
   PCS_CHECK_ARG(cfg->dyn.dt > 0, "dt must be > 0");
   cudaStream_t st = S(stream);
-  if (!g_attr_done) {
-    PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_accumulate, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)ACC_SMEM));
-    PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)BINS_SMEM));
-    PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)BINS_SMEM));
-    PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)BINS_SMEM));
-    PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<15>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)BINS_SMEM));
-    g_attr_done = true;
-  }
+  r = set_attrs();
+  if (r) return r;
   track_release(ctx);
   TrackState& T = ctx->tr;
   T = TrackState();
@@ -733,6 +731,8 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   P.dyn = Dyn{cfg->dyn.sigma_pos, cfg->dyn.sigma_vel, cfg->dyn.sigma_int, cfg->dyn.dt};
   P.spot = to_spot(&cfg->spot);
   P.grid = cfg->method == 1 ? to_grid(&cfg->grid) : Grid{0, 0, 1, 1, 1, 1};
+  P.inv_lx = 1.0 / P.grid.lx;
+  P.inv_ly = 1.0 / P.grid.ly;
   P.seed = cfg->seed;
   P.frame0 = cfg->frame0;
   P.placement = cfg->placement;
@@ -740,40 +740,50 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   PCS_SCRATCH(SL_TR_BUF1, 5 * ld * sizeof(float), P.buf1);
   PCS_SCRATCH(SL_TR_ANC, ld * sizeof(int), P.anc);
   PCS_SCRATCH(SL_TR_CTL, sizeof(TrackCtl), P.ctl);
-  T.ntiles = ceil_div(n, SCAN_TILE);
-  PCS_SCRATCH(SL_TR_TILES, T.ntiles * sizeof(u128), T.tile_tot);
-  PCS_SCRATCH(SL_TR_PRE, T.ntiles * sizeof(u128), T.tile_pre);
+  P.ntiles = ceil_div(n, SCAN_TILE);
+  PCS_SCRATCH(SL_TR_TILES, P.ntiles * (2 * sizeof(u128) + sizeof(u32)) + 64, P.tile_agg);
+  P.tile_inc = P.tile_agg + P.ntiles;
+  P.tile_status = (u32*)(P.tile_inc + P.ntiles);
+  PCS_CUDA_TRY(cudaMemsetAsync(P.tile_status, 0, P.ntiles * sizeof(u32), st));
   if (cfg->method == 0) {
     PCS_SCRATCH(SL_TR_LL, ld * sizeof(double), P.ll);
     P.pslot = nullptr;
   } else {
     PCS_SCRATCH(SL_TR_PSLOT, ld * sizeof(u32), P.pslot);
     P.ll = nullptr;
-    if (!ctx->tab_cnt) {
-      PCS_CUDA_TRY(cudaMalloc(&ctx->tab_cnt, TABLE_CAP * sizeof(u32)));
-      PCS_CUDA_TRY(cudaMalloc(&ctx->tab_sum, 5 * TABLE_CAP * 2 * sizeof(u64)));
-      PCS_CUDA_TRY(cudaMalloc(&ctx->wtab, TABLE_CAP * sizeof(float)));
-      PCS_CUDA_TRY(cudaMalloc(&ctx->occ, MAXM * sizeof(u32)));
+    P.G = cfg->grid.n_cols * cfg->grid.n_rows;
+    if (ctx->table_cells < P.G) {
+      if (ctx->tab_cnt) cudaFree(ctx->tab_cnt);
+      if (ctx->tab_sum) cudaFree(ctx->tab_sum);
+      if (ctx->wtab) cudaFree(ctx->wtab);
+      ctx->tab_cnt = nullptr;
+      ctx->tab_sum = nullptr;
+      ctx->wtab = nullptr;
+      ctx->table_cells = 0;
+      PCS_CUDA_TRY(cudaMalloc(&ctx->tab_cnt, P.G * sizeof(u32)));
+      PCS_CUDA_TRY(cudaMalloc(&ctx->tab_sum, 5 * P.G * 2 * sizeof(u64)));
+      PCS_CUDA_TRY(cudaMalloc(&ctx->wtab, P.G * sizeof(float)));
+      ctx->table_cells = P.G;
       ctx->table_dirty = true;
     }
+    if (!ctx->occ) PCS_CUDA_TRY(cudaMalloc(&ctx->occ, MAXM * sizeof(u32) + 3 * BINS_MAXM * sizeof(float)));
     if (ctx->table_dirty) {
-      PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_cnt, 0, TABLE_CAP * sizeof(u32), st));
-      PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_sum, 0, 5 * TABLE_CAP * 2 * sizeof(u64), st));
+      PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_cnt, 0, ctx->table_cells * sizeof(u32), st));
+      PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_sum, 0, 5 * ctx->table_cells * 2 * sizeof(u64), st));
       ctx->table_dirty = false;
     }
     P.tab_cnt = ctx->tab_cnt;
     P.tab_sum = ctx->tab_sum;
     P.wtab = ctx->wtab;
     P.occ = ctx->occ;
+    float* sd = (float*)(ctx->occ + MAXM);
+    T.bins.dx = sd;
+    T.bins.dy = sd + BINS_MAXM;
+    T.bins.di = sd + 2 * BINS_MAXM;
   }
   T.maxs = maxs_for(cfg->spot.halfwidth);
   T.prop_grid = grid_for(n, 256, ctx->sms, 8);
-  // accumulate: chunk <= 2^15 particles per CTA (int64 shared partials), ~2 CTAs/SM
-  i64 want = 2 * (i64)ctx->sms;
-  i64 chunk = std::max<i64>(512, ceil_div(n, want));
-  chunk = std::min<i64>(chunk, 1 << 15);
-  T.acc_chunk = chunk;
-  T.acc_grid = (int)ceil_div(n, chunk);
+  T.s1_grid = (int)std::min<i64>(ctx->sms, ceil_div(n, S1_TILE));
   // initial cloud (state.py:164-175) and identity ancestors
   pcs_init_t init = cfg->init;
   r = pcs_init_particles(&init, cfg->seed, 0, n, P.buf0, ld, stream);
@@ -856,8 +866,9 @@ int pcs_track_steps_timed(pcs_ctx* ctx, const float* frames, int64_t k0, int64_t
 }
 
 const char* pcs_track_kernel_name(pcs_ctx* ctx, int32_t i) {
-  if (!ctx || i < 0 || i >= 6) return "";
-  return ctx->tr.cfg.method == 1 ? kPcNames[i] : kSirNames[i];
+  if (!ctx) return "";
+  if (ctx->tr.cfg.method == 1) return (i >= 0 && i < 3) ? kPcNames[i] : "";
+  return (i >= 0 && i < 5) ? kSirNames[i] : "";
 }
 
 int pcs_track_end(pcs_ctx* ctx, pcs_track_result_t* result, void* stream) {
@@ -889,8 +900,7 @@ int pcs_track_launches_per_step(pcs_ctx* ctx) { return ctx ? ctx->tr.launches : 
 
 int pcs_track_states(pcs_ctx* ctx, float** states, int64_t* ld) {
   PCS_CHECK_ARG(ctx && ctx->tr.active && states && ld, "bad arguments");
-  // frame k reads buf[k&1]; after k frames the latest propagated states are in buf[k&1]
-  // (the emission of frame k-1 produced the ancestors into that buffer's frame).
+  // frame k reads buf[k&1] and writes buf[(k+1)&1]
   *states = (ctx->tr.k & 1) ? ctx->tr.P.buf1 : ctx->tr.P.buf0;
   *ld = ctx->tr.P.ld;
   return PCS_OK;

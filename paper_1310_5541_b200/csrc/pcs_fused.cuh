@@ -1,0 +1,649 @@
+// pcs_fused.cuh — fused per-frame kernels of the device-resident filter loop.
+//
+//   k_pc_step1      gather (resampling, filtering.py:107) + propagate
+//                   (state.py:115-127) + cell index (binning.py:61-67,105) +
+//                   exact per-cell sums for the dummies (binning.py:157-172)
+//                   in ONE pass over the particle states.
+//   k_scan_emit     single-pass exact-prefix systematic resampling
+//                   (filtering.py:93-100): decoupled look-back scan of the
+//                   fixed-point weights + ancestor emission.
+//
+// Per-cell accumulation without 64-bit shared-memory atomics in the hot loop:
+// each CTA counting-sorts a tile of 2048 particles by cell inside shared
+// memory (one native 32-bit shared atomic per particle gives the rank), then
+// every warp runs a segmented scan over 32 sorted particles at a time and one
+// lane per run adds the run total into the CTA's int128 sub-window
+// accumulators (a handful of uncontended atomics per run instead of one per
+// particle). Integer sums are order-free, so the result is exactly the
+// canonical sum of round(s * 2^40).
+#pragma once
+#include "pcs_common.cuh"
+#include "pcs_lik.cuh"
+#include "pcs_state.cuh"
+#include "pcs_weights.cuh"
+
+namespace pcs {
+
+constexpr int S1_THREADS = 512;
+constexpr int S1_IPT = 4;
+constexpr int S1_TILE = S1_THREADS * S1_IPT;   // 2048 particles per tile
+constexpr int S1_WARPS = S1_THREADS / 32;
+constexpr int SUBW = 1536;                     // shared-memory sub-window cells
+constexpr i64 TABLE_MAX = 1ll << 28;           // dense full-grid table (cells)
+constexpr int MAXM = 16384;                    // occupied cells per frame (fused)
+
+struct S1Smem {
+  unsigned long long acc_lo[5][SUBW];
+  unsigned long long acc_hi[5][SUBW];
+  u32 acc_cnt[SUBW];
+  u32 tile_cnt[SUBW];
+  u32 tile_start[SUBW];
+  float pay[5][S1_TILE];
+  unsigned short pay_q[S1_TILE];
+  unsigned short list[S1_TILE];
+  u32 n_list;
+  u32 n_in;
+  int scan_tmp[S1_WARPS];
+};
+
+struct TrackCtl {
+  // ---- per frame (reset at the end of the frame for the next one)
+  i64 max_ll_ord;            // SIR: ordered-int64 max loglik (float64)
+  u32 n_occ;                 // pcSIR: first-touch occupied list length
+  u32 wmin_bits, wmax_bits;  // SIR: min/max normalised weight (non-negative float bits)
+  u32 pad_a;
+  u64 S[2];                  // SIR: normaliser
+  u64 est[5][2];             // SIR: estimate numerators
+  u64 w2[2];                 // SIR: ESS denominator
+  // ---- sub-window of the current frame
+  i64 sx0, sy0, snx, sny;
+  // ---- scalars consumed by the scan / emission kernel
+  double m, Sf, u;
+  int do_resample;
+  int pad1;
+  // ---- persistent
+  i64 k;                     // absolute frame index (since begin)
+  i64 k_frames;              // frame index of frames[0]
+  i64 k_out;                 // frame index of out[0]
+  const float* frames;
+  double* out_est;
+  double* out_ess;
+  unsigned char* out_res;
+  i64* out_occ;
+  u32 flags;
+  int first_bad;
+  i64 evals;
+  double center[2];          // previous estimate (shared-memory sub-window centre)
+  unsigned long long tile_ctr;  // decoupled look-back: monotone tile ticket counter
+};
+
+struct TrackParams {
+  i64 n, ld;
+  i64 H, W;
+  Dyn dyn;
+  Spot spot;
+  Grid grid;
+  double inv_lx, inv_ly;
+  u64 seed;
+  u32 frame0;
+  int placement;
+  float* buf0;
+  float* buf1;
+  int* anc;
+  double* ll;                // SIR: per-particle log-likelihood (float64)
+  u32* pslot;                // pcSIR: flat cell id per particle
+  u32* tab_cnt;              // [G]
+  u64* tab_sum;              // [5][G][2]
+  float* wtab;               // [G]
+  u32* occ;                  // [MAXM]
+  i64 G;                     // table cells (= n_cols * n_rows)
+  i64 ntiles;                // scan tiles
+  u32* tile_status;          // [ntiles] (frame tag << 2 | state)
+  u128* tile_agg;            // [ntiles]
+  u128* tile_inc;            // [ntiles]
+  TrackCtl* ctl;
+};
+
+__device__ __forceinline__ void set_flag(TrackCtl* c, u32 f) {
+  atomicOr(&c->flags, f);
+  atomicMin(&c->first_bad, (int)c->k);
+}
+
+__device__ __forceinline__ void reset_frame(TrackCtl* c) {
+  c->max_ll_ord = LLONG_MIN;
+  c->n_occ = 0;
+  c->wmin_bits = 0xFFFFFFFFu;
+  c->wmax_bits = 0u;
+  c->S[0] = c->S[1] = 0;
+  for (int q = 0; q < 5; ++q) c->est[q][0] = c->est[q][1] = 0;
+  c->w2[0] = c->w2[1] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// fast exact cell index: floor(RN((p - o)/l)) without a division unless the
+// multiplied quotient is within a few ulps of an integer (CANONICAL result is
+// identical to cell_axis in pcs_common.cuh)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ i64 cell_axis_fast(float p, double origin, double cell, double inv,
+                                              i64 n) {
+  double d = __dsub_rn((double)p, origin);
+  double t = __dmul_rn(d, inv);
+  double f = floor(t);
+  double fr = t - f;
+  double margin = fabs(t) * 3.552713678800501e-15 + 1e-300;  // |t| * 2^-48
+  double q = (fr > margin && fr < 1.0 - margin) ? f : floor(__ddiv_rn(d, cell));
+  if (!(q >= 0.0)) return 0;
+  double hi = (double)(n - 1);
+  if (q > hi) return n - 1;
+  return (i64)q;
+}
+
+// cell lower edge as float32 and whether it is an integer multiple of 2^-40
+__device__ __forceinline__ float cell_ref32(double origin, double cell, i64 i, bool& ok) {
+  float r = __double2float_rn(__dadd_rn(origin, __dmul_rn((double)i, cell)));
+  ok = (r == 0.0f) || (fabsf(r) >= 7.62939453125e-06f);  // |r| >= 2^-17 -> lsb >= 2^-40
+  return r;
+}
+
+// D = round(v * 2^40) - round(ref * 2^40) via an exact float32 difference
+// (TwoSum check). Returns false if v - ref is not exact (caller falls back).
+__device__ __forceinline__ bool delta_fixed(float v, float ref, long long& D) {
+  float s = __fsub_rn(v, ref);
+  float bp = __fsub_rn(s, v);
+  float ap = __fsub_rn(s, bp);
+  float err = __fadd_rn(__fsub_rn(v, ap), __fsub_rn(-ref, bp));
+  if (err != 0.0f || !(fabsf(s) < 128.0f)) return false;
+  D = __float2ll_rn(__fmul_rn(s, 1099511627776.0f));  // exact scale by 2^40, RN-even
+  return true;
+}
+
+__device__ __forceinline__ void touch_cell(const TrackParams& P, TrackCtl* C, u32 cell, u32 cnt) {
+  u32 old = atomicAdd(P.tab_cnt + cell, cnt);
+  if (old == 0) {
+    u32 idx = atomicAdd(&C->n_occ, 1u);
+    if (idx < (u32)MAXM) P.occ[idx] = cell;
+  }
+}
+
+// shared-memory int128 accumulate (lo/hi words with carry); deterministic sum
+__device__ __forceinline__ void smem_add_i128(unsigned long long* lo, unsigned long long* hi,
+                                              long long v) {
+  unsigned long long vlo = (unsigned long long)v;
+  unsigned long long vhi = (v < 0) ? ~0ull : 0ull;
+  unsigned long long old = atomicAdd(lo, vlo);
+  if (old + vlo < old) vhi += 1ull;
+  if (vhi) atomicAdd(hi, vhi);
+}
+
+// ===========================================================================
+// pcSIR step 1
+// ===========================================================================
+__global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
+  extern __shared__ __align__(16) unsigned char s1_raw[];
+  S1Smem& sm = *reinterpret_cast<S1Smem*>(s1_raw);
+  TrackCtl* C = P.ctl;
+  if (C->flags & PCS_FLAG_CAPACITY) return;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const i64 k = C->k;
+  const float* sin = (k & 1) ? P.buf1 : P.buf0;
+  float* sout = (k & 1) ? P.buf0 : P.buf1;
+  const Grid g = P.grid;
+  const i64 n = P.n, ld = P.ld;
+
+  // sub-window (identical in every CTA): centred on the previous estimate
+  i64 snx = min((i64)39, g.ncols), sny = min((i64)39, g.nrows);
+  if (snx < 39) sny = min(g.nrows, (i64)(SUBW / snx));
+  if (sny < 39) snx = min(g.ncols, (i64)(SUBW / sny));
+  i64 cx = cell_axis_fast((float)C->center[0], g.ox, g.lx, P.inv_lx, g.ncols);
+  i64 cy = cell_axis_fast((float)C->center[1], g.oy, g.ly, P.inv_ly, g.nrows);
+  const i64 sx0 = min(max(cx - snx / 2, (i64)0), g.ncols - snx);
+  const i64 sy0 = min(max(cy - sny / 2, (i64)0), g.nrows - sny);
+  if (blockIdx.x == 0 && t == 0) {
+    C->sx0 = sx0; C->sy0 = sy0; C->snx = snx; C->sny = sny;
+  }
+  const int subn = (int)(snx * sny);
+  for (int q = t; q < SUBW; q += S1_THREADS) {
+    sm.acc_cnt[q] = 0;
+    sm.tile_cnt[q] = 0;
+#pragma unroll
+    for (int c = 0; c < 5; ++c) sm.acc_lo[c][q] = sm.acc_hi[c][q] = 0ull;
+  }
+  if (t == 0) sm.n_list = 0;
+  __syncthreads();
+
+  bool bad = false;
+  const i64 ntile = ceil_div(n, S1_TILE);
+  for (i64 tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+    // ---- phase 1: gather + propagate + cell; rank within the tile's cell ----
+    int q_k[S1_IPT], r_k[S1_IPT];
+    float o_k[S1_IPT][5];
+#pragma unroll
+    for (int it = 0; it < S1_IPT; ++it) {
+      q_k[it] = -1;
+      i64 j = tile * S1_TILE + (i64)it * S1_THREADS + t;
+      if (j >= n) continue;
+      i64 src = (i64)__ldg(P.anc + j);
+      float s[5], z[5];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) s[c] = __ldg(sin + c * ld + src);
+      philox_normals5(P.seed, P.frame0 + (u32)k, (u64)j, z);
+      propagate_one(s, z, P.dyn, o_k[it]);
+#pragma unroll
+      for (int c = 0; c < 5; ++c) sout[c * ld + j] = o_k[it][c];
+      const float* o = o_k[it];
+      if (!(o[0] == o[0]) || !(o[1] == o[1])) bad = true;
+      i64 ix = cell_axis_fast(o[0], g.ox, g.lx, P.inv_lx, g.ncols);
+      i64 iy = cell_axis_fast(o[1], g.oy, g.ly, P.inv_ly, g.nrows);
+      u32 flat = (u32)(iy * g.ncols + ix);
+      P.pslot[j] = flat;
+      i64 lx = ix - sx0, ly = iy - sy0;
+      bool in_sub = (lx >= 0 && lx < snx && ly >= 0 && ly < sny);
+      if (in_sub) {
+        bool okx, oky;
+        float rx = cell_ref32(g.ox, g.lx, ix, okx), ry = cell_ref32(g.oy, g.ly, iy, oky);
+        long long D;
+        in_sub = okx && oky && delta_fixed(o[0], rx, D) && delta_fixed(o[1], ry, D) &&
+                 fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f && fabsf(o[4]) < 128.0f;
+      }
+      if (in_sub) {
+        int q = (int)(ly * snx + lx);
+        int r = (int)atomicAdd(&sm.tile_cnt[q], 1u);
+        if (r == 0) sm.list[atomicAdd(&sm.n_list, 1u)] = (unsigned short)q;
+        q_k[it] = q;
+        r_k[it] = r;
+      } else {
+        // outside the shared sub-window: exact int128 atomics straight to HBM
+        touch_cell(P, C, flat, 1u);
+#pragma unroll
+        for (int c = 0; c < 5; ++c)
+          atomic_add_i128(P.tab_sum + ((i64)c * P.G + flat) * 2, f32_to_fixed(o[c], FX_STATE));
+      }
+    }
+    __syncthreads();
+    // ---- phase 2: segment offsets (exclusive scan of counts in list order) ----
+    const int nl = (int)sm.n_list;
+    {
+      int base = t * 4, loc[4], sum = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        int idx = base + e;
+        loc[e] = (idx < nl) ? (int)sm.tile_cnt[sm.list[idx]] : 0;
+        sum += loc[e];
+      }
+      int inc = sum;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        int o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+      }
+      if (lane == 31) sm.scan_tmp[warp] = inc;
+      __syncthreads();
+      int woff = 0;
+      for (int w = 0; w < warp; ++w) woff += sm.scan_tmp[w];
+      int run = woff + inc - sum;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        int idx = base + e;
+        if (idx < nl) sm.tile_start[sm.list[idx]] = (u32)run;
+        run += loc[e];
+      }
+      if (t == S1_THREADS - 1) sm.n_in = (u32)run;
+    }
+    __syncthreads();
+    // ---- phase 3: scatter the in-window particles into cell-sorted order ----
+#pragma unroll
+    for (int it = 0; it < S1_IPT; ++it) {
+      if (q_k[it] < 0) continue;
+      int pos = (int)sm.tile_start[q_k[it]] + r_k[it];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) sm.pay[c][pos] = o_k[it][c];
+      sm.pay_q[pos] = (unsigned short)q_k[it];
+    }
+    __syncthreads();
+    // ---- phase 4: warp segmented scans over sorted runs -> int128 accumulators ----
+    const int nin = (int)sm.n_in;
+    for (int base = warp * 32; base < nin; base += S1_THREADS) {
+      int pos = base + lane;
+      bool valid = pos < nin;
+      int q = valid ? (int)sm.pay_q[pos] : -1 - lane;
+      long long v[5] = {0, 0, 0, 0, 0};
+      if (valid) {
+        i64 ix = sx0 + q % snx, iy = sy0 + q / snx;
+        bool ok;
+        float rx = cell_ref32(g.ox, g.lx, ix, ok), ry = cell_ref32(g.oy, g.ly, iy, ok);
+        delta_fixed(sm.pay[0][pos], rx, v[0]);
+        delta_fixed(sm.pay[1][pos], ry, v[1]);
+#pragma unroll
+        for (int c = 2; c < 5; ++c) v[c] = __float2ll_rn(__fmul_rn(sm.pay[c][pos], 1099511627776.0f));
+      }
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        int qo = __shfl_up_sync(0xffffffffu, q, d);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+          long long o = __shfl_up_sync(0xffffffffu, v[c], d);
+          if (lane >= d && qo == q) v[c] += o;
+        }
+      }
+      int qn = __shfl_down_sync(0xffffffffu, q, 1);
+      bool tail = valid && (lane == 31 || qn != q);
+      if (tail) {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) smem_add_i128(&sm.acc_lo[c][q], &sm.acc_hi[c][q], v[c]);
+      }
+    }
+    // ---- phase 5: counts; reset the tile state ----
+    for (int e = t; e < nl; e += S1_THREADS) {
+      int q = sm.list[e];
+      sm.acc_cnt[q] += sm.tile_cnt[q];
+      sm.tile_cnt[q] = 0;
+    }
+    __syncthreads();
+    if (t == 0) sm.n_list = 0;
+    __syncthreads();
+  }
+  // ---- flush the CTA's sub-window into the HBM table (exact int128) ----
+  for (int q = t; q < subn; q += S1_THREADS) {
+    u32 cnt = sm.acc_cnt[q];
+    if (!cnt) continue;
+    i64 ix = sx0 + q % snx, iy = sy0 + q / snx;
+    u32 flat = (u32)(iy * g.ncols + ix);
+    touch_cell(P, C, flat, cnt);
+    bool ok;
+    float ref[2] = {cell_ref32(g.ox, g.lx, ix, ok), cell_ref32(g.oy, g.ly, iy, ok)};
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      i128 s = (i128)(((u128)sm.acc_hi[c][q] << 64) | (u128)sm.acc_lo[c][q]);
+      if (c < 2) s += (i128)cnt * f32_to_fixed(ref[c], FX_STATE);
+      atomic_add_i128(P.tab_sum + ((i64)c * P.G + flat) * 2, s);
+    }
+  }
+  if (bad) set_flag(C, PCS_FLAG_NONFINITE);
+}
+
+// ===========================================================================
+// pcSIR bins (one CTA): dummies, likelihood per occupied cell (one warp per
+// cell, pixels across lanes), normaliser, per-cell weights, estimate, ESS,
+// resampling decision. Zeroes the consumed table cells.
+// ===========================================================================
+constexpr int BINS_BLOCK = 1024;
+constexpr int BINS_MAXM = 8192;              // occupied cells handled by the fused bins kernel
+constexpr int STAGE_PIX = 12288;             // staged frame tile (48 KB)
+constexpr size_t BINS_SMEM = BINS_MAXM * sizeof(double) + STAGE_PIX * sizeof(float);
+
+struct BinsScratch {  // global scratch for the dummies of the occupied cells
+  float* dx;
+  float* dy;
+  float* di;
+};
+
+template <int MAXS>
+__global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScratch Sd) {
+  TrackCtl* C = P.ctl;
+  extern __shared__ __align__(16) unsigned char bins_raw[];
+  double* s_ll = reinterpret_cast<double*>(bins_raw);
+  float* s_pix = reinterpret_cast<float*>(bins_raw + BINS_MAXM * sizeof(double));
+  __shared__ i128 s_red[BINS_BLOCK / 32];
+  __shared__ long long s_max;
+  __shared__ unsigned s_wmin, s_wmax;
+  __shared__ int s_box[4];
+  __shared__ double s_Sf;
+  const int t = threadIdx.x;
+  const i64 k = C->k;
+  const i64 ko = k - C->k_out;
+  const u32 nocc = C->n_occ;
+  if ((C->flags & PCS_FLAG_CAPACITY) || nocc > (u32)BINS_MAXM) {
+    if (t == 0) {
+      set_flag(C, PCS_FLAG_CAPACITY);
+      C->do_resample = 0;
+      C->out_occ[ko] = -1;
+      reset_frame(C);
+      C->k = k + 1;
+    }
+    return;
+  }
+  const int M = (int)nocc;
+  const float* frame = C->frames + (k - C->k_frames) * P.H * P.W;
+  if (t == 0) {
+    s_max = LLONG_MIN;
+    s_wmin = 0xFFFFFFFFu;
+    s_wmax = 0u;
+    s_box[0] = INT_MAX; s_box[1] = INT_MIN; s_box[2] = INT_MAX; s_box[3] = INT_MIN;
+  }
+  __syncthreads();
+  // 1) dummies (exact means, binning.py:157-172) and the union of their windows
+  int bx0 = INT_MAX, bx1 = INT_MIN, by0 = INT_MAX, by1 = INT_MIN;
+  for (int b = t; b < M; b += BINS_BLOCK) {
+    u32 cell = P.occ[b];
+    u32 cnt = P.tab_cnt[cell];
+    float d[5];
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      double num = i128_to_f64_rn(load_i128(P.tab_sum + ((i64)c * P.G + cell) * 2));
+      d[c] = __double2float_rn(scalbn(__ddiv_rn(num, (double)cnt), -FX_STATE));
+    }
+    if (P.placement == 1) {  // cell centre (binning.py:168-171)
+      i64 ix = (i64)cell % P.grid.ncols, iy = (i64)cell / P.grid.ncols;
+      d[0] = __double2float_rn(__dadd_rn(P.grid.ox, __dmul_rn((double)ix + 0.5, P.grid.lx)));
+      d[1] = __double2float_rn(__dadd_rn(P.grid.oy, __dmul_rn((double)iy + 0.5, P.grid.ly)));
+    }
+    Sd.dx[b] = d[0];
+    Sd.dy[b] = d[1];
+    Sd.di[b] = d[4];
+    if (d[0] == d[0] && d[1] == d[1]) {
+      int xlo, xhi, ylo, yhi;
+      window_of(d[0], d[1], P.spot, P.H, P.W, xlo, xhi, ylo, yhi);
+      bx0 = min(bx0, xlo); bx1 = max(bx1, xhi); by0 = min(by0, ylo); by1 = max(by1, yhi);
+    }
+  }
+  atomicMin(&s_box[0], bx0); atomicMax(&s_box[1], bx1);
+  atomicMin(&s_box[2], by0); atomicMax(&s_box[3], by1);
+  __syncthreads();
+  // 2) stage the frame region covering every window in shared memory
+  PixView pv = frame_view(frame, P.H, P.W);
+  {
+    int x0 = s_box[0], y0 = s_box[2];
+    i64 wx = (i64)s_box[1] - x0 + 1, wy = (i64)s_box[3] - y0 + 1;
+    if (s_box[1] >= s_box[0] && wx * wy <= STAGE_PIX) {
+      for (int p = t; p < (int)(wx * wy); p += BINS_BLOCK) {
+        int yy = p / (int)wx, xx = p % (int)wx;
+        s_pix[p] = __ldg(frame + (i64)(y0 + yy) * P.W + (x0 + xx));
+      }
+      pv.base = s_pix;
+      pv.pitch = wx;
+      pv.x0 = x0;
+      pv.y0 = y0;
+    }
+  }
+  __syncthreads();
+  // 3) likelihood once per occupied cell (binning.py:189)
+  long long lmax = LLONG_MIN;
+  for (int b = t; b < M; b += BINS_BLOCK) {
+    double ll = loglik_dispatch<MAXS>(pv, Sd.dx[b], Sd.dy[b], Sd.di[b], P.spot);
+    s_ll[b] = ll;
+    lmax = max(lmax, (long long)f64_to_ordered(ll));
+  }
+  atomicMax(&s_max, lmax);
+  __syncthreads();
+  const double m = ordered_to_f64((i64)s_max);
+  const bool bad_m = !(m == m) || m == INFINITY;
+  const bool degenerate = (m == -INFINITY);
+  // 4) normaliser S = sum_b cnt_b * round(exp(ll_b - m) * 2^95)
+  i128 acc = 0;
+  for (int b = t; b < M; b += BINS_BLOCK) {
+    u32 cnt = P.tab_cnt[P.occ[b]];
+    acc += (i128)cnt * f64_to_fixed(exp(__dsub_rn(s_ll[b], m)), FX_S);
+  }
+  i128 Sfix = block_sum_i128<BINS_BLOCK>(acc, s_red);
+  if (t == 0) s_Sf = scalbn(i128_to_f64_rn(Sfix), -FX_S);
+  __syncthreads();
+  const double Sf = s_Sf;
+  // 5) weights per cell (broadcast table), estimate, ESS; zero consumed cells
+  i128 e[6] = {0, 0, 0, 0, 0, 0};
+  for (int b = t; b < M; b += BINS_BLOCK) {
+    u32 cell = P.occ[b];
+    u32 cnt = P.tab_cnt[cell];
+    float w = normalised_weight(s_ll[b], m, Sf);
+    P.wtab[cell] = w;
+    atomicMin(&s_wmin, __float_as_uint(w));
+    atomicMax(&s_wmax, __float_as_uint(w));
+    i128 wq = f32_to_fixed(w, FX_WQ);
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      u64* p = P.tab_sum + ((i64)c * P.G + cell) * 2;
+      e[c] += wq * load_i128(p);
+      p[0] = 0;
+      p[1] = 0;
+    }
+    e[5] += (i128)cnt * f64_to_fixed((double)w * (double)w, FX_W2);
+    P.tab_cnt[cell] = 0;
+  }
+  double est[5];
+  double w2f = 0;
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    i128 tot = block_sum_i128<BINS_BLOCK>(e[c], s_red);
+    if (t == 0) {
+      if (c < 5) est[c] = scalbn(i128_to_f64_rn(tot), -(FX_WQ + FX_STATE));
+      else w2f = scalbn(i128_to_f64_rn(tot), -FX_W2);
+    }
+  }
+  if (t == 0) {
+    double ess = 1.0 / w2f;
+    bool flag_bad = degenerate || bad_m;
+    if (degenerate) set_flag(C, PCS_FLAG_DEGENERATE);
+    if (bad_m) set_flag(C, PCS_FLAG_NONFINITE);
+    for (int c = 0; c < 5; ++c) C->out_est[ko * 5 + c] = est[c];
+    C->out_ess[ko] = ess;
+    int res = (!flag_bad && ess < (double)P.n) ? 1 : 0;   // threshold_fraction = 1.0
+    // no resampling with unequal weights -> non-uniform prior next frame:
+    // only the general path carries per-particle prior weights
+    if (!res && !flag_bad && s_wmin != s_wmax) set_flag(C, PCS_FLAG_CAPACITY);
+    C->out_res[ko] = (unsigned char)res;
+    C->out_occ[ko] = M;
+    C->evals += M;
+    C->do_resample = res;
+    C->m = m;
+    C->Sf = Sf;
+    C->u = philox_resample_u(P.seed, P.frame0 + (u32)k);
+    if (!flag_bad) {
+      C->center[0] = est[0];
+      C->center[1] = est[1];
+    }
+    reset_frame(C);
+    C->k = k + 1;   // last reader of k in this frame
+  }
+}
+
+// ===========================================================================
+// Single-pass exact-prefix systematic resampling: decoupled look-back over
+// tiles (dynamic tile tickets guarantee forward progress; the tile status
+// carries a frame tag so nothing is reset between frames).
+// KIND 1: weight = wtab[pslot[i]] (pcSIR), KIND 2: from ll[i], m, Sf (SIR).
+// ===========================================================================
+__device__ __forceinline__ void st_release_u32(u32* p, u32 v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ u32 ld_acquire_u32(const u32* p) {
+  u32 v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_emit(TrackParams P) {
+  __shared__ float wsh[SCAN_TILE];
+  __shared__ u128 wtot[SCAN_BLOCK / 32];
+  __shared__ u128 s_excl;
+  __shared__ unsigned long long s_ticket;
+  TrackCtl* C = P.ctl;
+  const i64 n = P.n, nt = P.ntiles;
+  if (threadIdx.x == 0) s_ticket = atomicAdd(&C->tile_ctr, 1ull);
+  __syncthreads();
+  const unsigned long long ticket = s_ticket;
+  const i64 tile = (i64)(ticket % (unsigned long long)nt);
+  const u32 tag = (u32)(ticket / (unsigned long long)nt) & 0x3FFFFFFFu;
+  const int do_res = C->do_resample;
+  const i64 base = tile * SCAN_TILE;
+  if (!do_res) {   // identity ancestors, weights stay uniform (all equal)
+    for (int q = 0; q < SCAN_ITEMS; ++q) {
+      i64 i = base + (i64)q * SCAN_BLOCK + threadIdx.x;
+      if (i < n) P.anc[i] = (int)i;
+    }
+    return;
+  }
+  const double m = C->m, Sf = C->Sf, u = C->u;
+#pragma unroll 4
+  for (int q = 0; q < SCAN_ITEMS; ++q) {
+    i64 i = base + (i64)q * SCAN_BLOCK + threadIdx.x;
+    float w = 0.0f;
+    if (i < n) w = (KIND == 1) ? P.wtab[P.pslot[i]] : normalised_weight(P.ll[i], m, Sf);
+    wsh[q * SCAN_BLOCK + threadIdx.x] = w;
+  }
+  __syncthreads();
+  u128 loc[SCAN_ITEMS];
+  u128 tsum = 0;
+#pragma unroll
+  for (int q = 0; q < SCAN_ITEMS; ++q) {
+    tsum += cdf_fixed(wsh[threadIdx.x * SCAN_ITEMS + q]);
+    loc[q] = tsum;
+  }
+  const int l = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  u128 inc = tsum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    u128 o = shfl_up_u128(inc, d);
+    if (l >= d) inc += o;
+  }
+  if (l == 31) wtot[wi] = inc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    u128 agg = 0;
+    for (int w = 0; w < SCAN_BLOCK / 32; ++w) agg += wtot[w];
+    u128 excl = 0;
+    if (tile == 0) {
+      P.tile_inc[0] = agg;
+      __threadfence();
+      st_release_u32(P.tile_status + 0, (tag << 2) | 2u);
+    } else {
+      P.tile_agg[tile] = agg;
+      __threadfence();
+      st_release_u32(P.tile_status + tile, (tag << 2) | 1u);
+      i64 p = tile - 1;
+      while (true) {
+        u32 s;
+        do {
+          s = ld_acquire_u32(P.tile_status + p);
+        } while ((s >> 2) != tag || (s & 3u) == 0u);
+        if ((s & 3u) == 2u) {
+          excl += *((volatile u128*)(P.tile_inc + p));
+          break;
+        }
+        excl += *((volatile u128*)(P.tile_agg + p));
+        --p;
+      }
+      P.tile_inc[tile] = excl + agg;
+      __threadfence();
+      st_release_u32(P.tile_status + tile, (tag << 2) | 2u);
+    }
+    s_excl = excl;
+  }
+  __syncthreads();
+  u128 woff = 0;
+  for (int w = 0; w < wi; ++w) woff += wtot[w];
+  u128 excl = s_excl + woff + (inc - tsum);
+  const i64 i0 = base + (i64)threadIdx.x * SCAN_ITEMS;
+  if (i0 >= n) return;
+  i64 j = (i0 == 0) ? 0 : first_slot_at_or_above(cdf_round(excl), u, n);
+#pragma unroll
+  for (int q = 0; q < SCAN_ITEMS; ++q) {
+    i64 i = i0 + q;
+    if (i >= n) break;
+    i64 jend = (i == n - 1) ? n : first_slot_at_or_above(cdf_round(excl + loc[q]), u, n);
+    for (; j < jend; ++j) P.anc[j] = (int)i;
+  }
+}
+
+constexpr size_t S1_SMEM = sizeof(S1Smem);
+
+}  // namespace pcs

@@ -7,8 +7,10 @@
 //
 // Precision contract: per-pixel prediction in float32, each
 // squared residual r*r added EXACTLY into a float64 accumulator (r is float32,
-// so r*r is exact in float64), log-likelihood returned in float64. The
-// remaining error is the float32 rounding of the predicted pixel value.
+// so r*r is exact in float64) in row-major window order, log-likelihood
+// returned in float64. Pixels come through a PixView: the frame in HBM or a
+// staged shared-memory tile of it — same values, same arithmetic, same order,
+// so both sources give bit-identical results.
 #pragma once
 #include "pcs_common.cuh"
 
@@ -24,6 +26,28 @@ struct Spot {
   float erf_scale;     // sigma*sqrt(pi/2)  (model 1)
   float inv_sqrt2s;    // 1/(sqrt(2) sigma) (model 1)
 };
+
+// frame (H x W) view; pixel (x, y) lives at base[(y - y0) * pitch + (x - x0)]
+struct PixView {
+  const float* base;
+  i64 pitch;
+  int x0, y0;
+  i64 H, W;
+  __device__ __forceinline__ const float* row(int y, int x) const {
+    return base + (i64)(y - y0) * pitch + (x - x0);
+  }
+};
+
+__device__ __forceinline__ PixView frame_view(const float* pix, i64 H, i64 W) {
+  PixView v;
+  v.base = pix;
+  v.pitch = W;
+  v.x0 = 0;
+  v.y0 = 0;
+  v.H = H;
+  v.W = W;
+  return v;
+}
 
 __device__ __forceinline__ void window_axis(double p, int hw, i64 extent, int& lo, int& hi) {
   // cx = floor(p + 0.5); lo = clamp(cx - hw, 0, extent-1); hi = clamp(cx + hw, 0, extent-1)
@@ -41,15 +65,16 @@ __device__ __forceinline__ double nan_ll() { return __longlong_as_double(0x7ff80
 // ---- Gaussian windowed SSD (CANONICAL hot-path arithmetic) ----------------
 //   gx[i] = expf(-(d*d) * inv2s2), d = RN32(xi - x)        (fp32)
 //   pred  = fmaf(I0*gx[i], gy[j], bg); r = p - pred         (fp32)
-//   ssd   = sum fma((double)r, (double)r, ssd)              (fp64, exact terms)
+//   ssd   = sum fma((double)r, (double)r, ssd)              (fp64, exact terms,
+//                                                            row-major order)
 //   ll    = -ssd * inv_2sxi2                                (fp64)
 template <int MAXS>
-__device__ __forceinline__ double loglik_gauss(const float* __restrict__ pix, i64 H, i64 W, float x,
-                                               float y, float i0, const Spot& sp) {
+__device__ __forceinline__ double loglik_gauss(const PixView& pv, float x, float y, float i0,
+                                               const Spot& sp) {
   if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
   int xlo, xhi, ylo, yhi;
-  window_axis((double)x, sp.hw, W, xlo, xhi);
-  window_axis((double)y, sp.hw, H, ylo, yhi);
+  window_axis((double)x, sp.hw, pv.W, xlo, xhi);
+  window_axis((double)y, sp.hw, pv.H, ylo, yhi);
   int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
   float ag[MAXS];
 #pragma unroll
@@ -60,18 +85,21 @@ __device__ __forceinline__ double loglik_gauss(const float* __restrict__ pix, i6
     }
   }
   double ssd = 0.0;
-  const float* row = pix + (i64)ylo * W + xlo;
   for (int j = 0; j < ny; ++j) {
+    const float* row = pv.row(ylo + j, xlo);
     float d = __double2float_rn((double)(ylo + j) - (double)y);
     float gy = expf(-(d * d) * sp.inv2s2);
+    float pr[MAXS];
+#pragma unroll
+    for (int i = 0; i < MAXS; ++i)
+      if (i < nx) pr[i] = row[i];
 #pragma unroll
     for (int i = 0; i < MAXS; ++i) {
       if (i < nx) {
-        float r = __ldg(row + i) - fmaf(ag[i], gy, sp.bg);
+        float r = pr[i] - fmaf(ag[i], gy, sp.bg);
         ssd = fma((double)r, (double)r, ssd);
       }
     }
-    row += W;
   }
   return -ssd * sp.inv_2sxi2;
 }
@@ -106,12 +134,12 @@ __device__ __forceinline__ double poisson_term(float z, float t, float bg) {
 }
 
 template <int MAXS>
-__device__ __forceinline__ double loglik_poisson(const float* __restrict__ pix, i64 H, i64 W,
-                                                 float x, float y, float i0, const Spot& sp) {
+__device__ __forceinline__ double loglik_poisson(const PixView& pv, float x, float y, float i0,
+                                                 const Spot& sp) {
   if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
   int xlo, xhi, ylo, yhi;
-  window_axis((double)x, sp.hw, W, xlo, xhi);
-  window_axis((double)y, sp.hw, H, ylo, yhi);
+  window_axis((double)x, sp.hw, pv.W, xlo, xhi);
+  window_axis((double)y, sp.hw, pv.H, ylo, yhi);
   int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
   float ex[MAXS];
   const float inv_bg = 1.0f / sp.bg;
@@ -123,81 +151,85 @@ __device__ __forceinline__ double loglik_poisson(const float* __restrict__ pix, 
     }
   }
   double ll = 0.0;
-  const float* row = pix + (i64)ylo * W + xlo;
   for (int j = 0; j < ny; ++j) {
+    const float* row = pv.row(ylo + j, xlo);
     float ey = psf_axis(__double2float_rn((double)(ylo + j) - (double)y), sp);
 #pragma unroll
     for (int i = 0; i < MAXS; ++i)
-      if (i < nx) ll += poisson_term(__ldg(row + i), ex[i] * ey, sp.bg);
-    row += W;
+      if (i < nx) ll += poisson_term(row[i], ex[i] * ey, sp.bg);
   }
   return ll;
 }
 
 template <int MAXS>
-__device__ __forceinline__ double loglik_any(const float* __restrict__ pix, i64 H, i64 W, float x,
-                                             float y, float i0, const Spot& sp) {
-  if (sp.model == 0) return loglik_gauss<MAXS>(pix, H, W, x, y, i0, sp);
-  return loglik_poisson<MAXS>(pix, H, W, x, y, i0, sp);
+__device__ __forceinline__ double loglik_any(const PixView& pv, float x, float y, float i0,
+                                             const Spot& sp) {
+  if (sp.model == 0) return loglik_gauss<MAXS>(pv, x, y, i0, sp);
+  return loglik_poisson<MAXS>(pv, x, y, i0, sp);
 }
 
 // Generic window (any halfwidth): gx/gy recomputed per pixel; the per-pixel
 // expressions and the accumulation order are identical to the MAXS forms, so
 // results are bit-identical for any window size.
-__device__ __forceinline__ double loglik_gauss_generic(const float* __restrict__ pix, i64 H, i64 W,
-                                                       float x, float y, float i0,
-                                                       const Spot& sp) {
+__device__ __forceinline__ double loglik_gauss_generic(const PixView& pv, float x, float y,
+                                                       float i0, const Spot& sp) {
   if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
   int xlo, xhi, ylo, yhi;
-  window_axis((double)x, sp.hw, W, xlo, xhi);
-  window_axis((double)y, sp.hw, H, ylo, yhi);
+  window_axis((double)x, sp.hw, pv.W, xlo, xhi);
+  window_axis((double)y, sp.hw, pv.H, ylo, yhi);
   double ssd = 0.0;
   for (int yy = ylo; yy <= yhi; ++yy) {
     float d = __double2float_rn((double)yy - (double)y);
     float gy = expf(-(d * d) * sp.inv2s2);
-    const float* row = pix + (i64)yy * W;
+    const float* row = pv.row(yy, xlo);
     for (int xx = xlo; xx <= xhi; ++xx) {
       float dx = __double2float_rn((double)xx - (double)x);
       float ag = i0 * expf(-(dx * dx) * sp.inv2s2);
-      float r = __ldg(row + xx) - fmaf(ag, gy, sp.bg);
+      float r = row[xx - xlo] - fmaf(ag, gy, sp.bg);
       ssd = fma((double)r, (double)r, ssd);
     }
   }
   return -ssd * sp.inv_2sxi2;
 }
 
-__device__ __forceinline__ double loglik_poisson_generic(const float* __restrict__ pix, i64 H,
-                                                         i64 W, float x, float y, float i0,
-                                                         const Spot& sp) {
+__device__ __forceinline__ double loglik_poisson_generic(const PixView& pv, float x, float y,
+                                                         float i0, const Spot& sp) {
   if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
   int xlo, xhi, ylo, yhi;
-  window_axis((double)x, sp.hw, W, xlo, xhi);
-  window_axis((double)y, sp.hw, H, ylo, yhi);
+  window_axis((double)x, sp.hw, pv.W, xlo, xhi);
+  window_axis((double)y, sp.hw, pv.H, ylo, yhi);
   const float inv_bg = 1.0f / sp.bg;
   double ll = 0.0;
   for (int yy = ylo; yy <= yhi; ++yy) {
     float ey = psf_axis(__double2float_rn((double)yy - (double)y), sp);
-    const float* row = pix + (i64)yy * W;
+    const float* row = pv.row(yy, xlo);
     for (int xx = xlo; xx <= xhi; ++xx) {
       float exi = i0 * psf_axis(__double2float_rn((double)xx - (double)x), sp) * inv_bg;
-      ll += poisson_term(__ldg(row + xx), exi * ey, sp.bg);
+      ll += poisson_term(row[xx - xlo], exi * ey, sp.bg);
     }
   }
   return ll;
 }
 
-__device__ __forceinline__ double loglik_generic(const float* __restrict__ pix, i64 H, i64 W,
-                                                 float x, float y, float i0, const Spot& sp) {
-  return (sp.model == 0) ? loglik_gauss_generic(pix, H, W, x, y, i0, sp)
-                         : loglik_poisson_generic(pix, H, W, x, y, i0, sp);
+__device__ __forceinline__ double loglik_generic(const PixView& pv, float x, float y, float i0,
+                                                 const Spot& sp) {
+  return (sp.model == 0) ? loglik_gauss_generic(pv, x, y, i0, sp)
+                         : loglik_poisson_generic(pv, x, y, i0, sp);
 }
 
 // dispatch: MAXS > 0 -> register-resident window, MAXS == 0 -> generic
 template <int MAXS>
-__device__ __forceinline__ double loglik_dispatch(const float* __restrict__ pix, i64 H, i64 W,
-                                                  float x, float y, float i0, const Spot& sp) {
-  if constexpr (MAXS > 0) return loglik_any<MAXS>(pix, H, W, x, y, i0, sp);
-  else return loglik_generic(pix, H, W, x, y, i0, sp);
+__device__ __forceinline__ double loglik_dispatch(const PixView& pv, float x, float y, float i0,
+                                                  const Spot& sp) {
+  if constexpr (MAXS > 0) return loglik_any<MAXS>(pv, x, y, i0, sp);
+  else return loglik_generic(pv, x, y, i0, sp);
+}
+
+// window bounds of a state (for staging decisions)
+__device__ __forceinline__ void window_of(float x, float y, const Spot& sp, i64 H, i64 W, int& xlo,
+                                          int& xhi, int& ylo, int& yhi) {
+  window_axis((double)x, sp.hw, W, xlo, xhi);
+  window_axis((double)y, sp.hw, H, ylo, yhi);
 }
 
 template <int MAXS>
@@ -206,8 +238,9 @@ __global__ void __launch_bounds__(256) k_loglik(const float* __restrict__ pix, i
                                                 const float* __restrict__ ys,
                                                 const float* __restrict__ is, i64 n, Spot sp,
                                                 double* __restrict__ out) {
+  const PixView pv = frame_view(pix, H, W);
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
-    out[i] = loglik_dispatch<MAXS>(pix, H, W, __ldg(xs + i), __ldg(ys + i), __ldg(is + i), sp);
+    out[i] = loglik_dispatch<MAXS>(pv, __ldg(xs + i), __ldg(ys + i), __ldg(is + i), sp);
 }
 
 // ---- float64 drop-in operator: spot_window_ssd (_speedups.pyx:42-83) ------
