@@ -55,13 +55,15 @@ static double u01_double(uint32_t a, uint32_t b) {
   return ((double)(a >> 5) * 67108864.0 + (double)(b >> 6)) * (1.0 / 9007199254740992.0);
 }
 
-/* float64 Box–Muller on the same 24-bit uniforms the device uses */
+/* float64 Box–Muller on the same 24-bit uniforms the device uses:
+ * r = sqrt(-2 ln u1), angle 2 pi (u2 - 1/2) */
 static void bm64(uint32_t a, uint32_t b, double* z0, double* z1) {
   double u1 = ((double)(a >> 8) + 0.5) * 5.9604644775390625e-8;
   double u2 = (double)(b >> 8) * 5.9604644775390625e-8;
   double r = sqrt(-2.0 * log(u1));
-  *z0 = r * cos(2.0 * M_PI * u2);
-  *z1 = r * sin(2.0 * M_PI * u2);
+  double th = 2.0 * M_PI * (u2 - 0.5);
+  *z0 = r * cos(th);
+  *z1 = r * sin(th);
 }
 
 /* the N x 5 standard normals of one propagation (state.py:125), out[c*n+i] */

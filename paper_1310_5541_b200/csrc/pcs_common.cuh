@@ -234,13 +234,16 @@ __host__ __device__ __forceinline__ double u01_double(u32 a, u32 b) {
   return ((double)(a >> 5) * 67108864.0 + (double)(b >> 6)) * (1.0 / 9007199254740992.0);
 }
 
-// Box–Muller pair in fp32 (logf / sincospif: full-precision libdevice paths).
+// Box–Muller pair in fp32 on the SFU: r = sqrt(-2 ln u1) (MUFU.LG2),
+// (z0, z1) = r (cos, sin)(2 pi (u2 - 1/2)) (MUFU.SIN/COS on [-pi, pi), where
+// the approximations are accurate to ~2^-21 absolute). The normals are
+// defined by this function; the oracle replays them (pcs_philox_normals).
 __device__ __forceinline__ void box_muller(u32 a, u32 b, float& z0, float& z1) {
   float u1 = u01_open(a);
   float u2 = u01_closed_open(b);
-  float r = sqrtf(-2.0f * logf(u1));
+  float r = sqrtf(-2.0f * __logf(u1));
   float s, c;
-  sincospif(2.0f * u2, &s, &c);
+  __sincosf(6.28318530717958647692f * (u2 - 0.5f), &s, &c);
   z0 = r * c;
   z1 = r * s;
 }

@@ -217,15 +217,27 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
     // ---- phase 1: gather + propagate + cell; rank within the tile's cell ----
     int q_k[S1_IPT], r_k[S1_IPT];
     float o_k[S1_IPT][5];
+    // issue every gather before any arithmetic (memory-level parallelism)
+    int src_k[S1_IPT];
+#pragma unroll
+    for (int it = 0; it < S1_IPT; ++it) {
+      i64 j = tile * S1_TILE + (i64)it * S1_THREADS + t;
+      src_k[it] = (j < n) ? __ldg(P.anc + j) : 0;
+    }
+#pragma unroll
+    for (int it = 0; it < S1_IPT; ++it) {
+      i64 j = tile * S1_TILE + (i64)it * S1_THREADS + t;
+#pragma unroll
+      for (int c = 0; c < 5; ++c) o_k[it][c] = (j < n) ? __ldg(sin + c * ld + src_k[it]) : 0.0f;
+    }
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {
       q_k[it] = -1;
       i64 j = tile * S1_TILE + (i64)it * S1_THREADS + t;
       if (j >= n) continue;
-      i64 src = (i64)__ldg(P.anc + j);
       float s[5], z[5];
 #pragma unroll
-      for (int c = 0; c < 5; ++c) s[c] = __ldg(sin + c * ld + src);
+      for (int c = 0; c < 5; ++c) s[c] = o_k[it][c];
       philox_normals5(P.seed, P.frame0 + (u32)k, (u64)j, z);
       propagate_one(s, z, P.dyn, o_k[it]);
 #pragma unroll
@@ -384,6 +396,7 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   double* s_ll = reinterpret_cast<double*>(bins_raw);
   float* s_pix = reinterpret_cast<float*>(bins_raw + BINS_MAXM * sizeof(double));
   __shared__ i128 s_red[BINS_BLOCK / 32];
+  __shared__ i128 s_red6[BINS_BLOCK / 32 * 6];
   __shared__ long long s_max;
   __shared__ unsigned s_wmin, s_wmax;
   __shared__ int s_box[4];
@@ -456,12 +469,17 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     }
   }
   __syncthreads();
-  // 3) likelihood once per occupied cell (binning.py:189)
+  // 3) likelihood once per occupied cell (binning.py:189): one warp per cell
   long long lmax = LLONG_MIN;
-  for (int b = t; b < M; b += BINS_BLOCK) {
-    double ll = loglik_dispatch<MAXS>(pv, Sd.dx[b], Sd.dy[b], Sd.di[b], P.spot);
-    s_ll[b] = ll;
-    lmax = max(lmax, (long long)f64_to_ordered(ll));
+  {
+    const int lane = t & 31, warp = t >> 5;
+    for (int b = warp; b < M; b += BINS_BLOCK / 32) {
+      double ll = loglik_warp(pv, Sd.dx[b], Sd.dy[b], Sd.di[b], P.spot, lane);
+      if (lane == 0) {
+        s_ll[b] = ll;
+        lmax = max(lmax, (long long)f64_to_ordered(ll));
+      }
+    }
   }
   atomicMax(&s_max, lmax);
   __syncthreads();
@@ -500,15 +518,11 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   }
   double est[5];
   double w2f = 0;
-#pragma unroll
-  for (int c = 0; c < 6; ++c) {
-    i128 tot = block_sum_i128<BINS_BLOCK>(e[c], s_red);
-    if (t == 0) {
-      if (c < 5) est[c] = scalbn(i128_to_f64_rn(tot), -(FX_WQ + FX_STATE));
-      else w2f = scalbn(i128_to_f64_rn(tot), -FX_W2);
-    }
-  }
+  block_sum_i128_k<BINS_BLOCK, 6>(e, s_red6);
   if (t == 0) {
+#pragma unroll
+    for (int c = 0; c < 5; ++c) est[c] = scalbn(i128_to_f64_rn(e[c]), -(FX_WQ + FX_STATE));
+    w2f = scalbn(i128_to_f64_rn(e[5]), -FX_W2);
     double ess = 1.0 / w2f;
     bool flag_bad = degenerate || bad_m;
     if (degenerate) set_flag(C, PCS_FLAG_DEGENERATE);
@@ -597,36 +611,57 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_emit(TrackParams P) {
   }
   if (l == 31) wtot[wi] = inc;
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (wi == 0) {
+    // tile aggregate; publish it, then warp-parallel look-back over 32
+    // predecessors at a time (closest inclusive prefix ends the walk)
     u128 agg = 0;
     for (int w = 0; w < SCAN_BLOCK / 32; ++w) agg += wtot[w];
-    u128 excl = 0;
-    if (tile == 0) {
-      P.tile_inc[0] = agg;
-      __threadfence();
-      st_release_u32(P.tile_status + 0, (tag << 2) | 2u);
-    } else {
-      P.tile_agg[tile] = agg;
-      __threadfence();
-      st_release_u32(P.tile_status + tile, (tag << 2) | 1u);
-      i64 p = tile - 1;
-      while (true) {
-        u32 s;
-        do {
-          s = ld_acquire_u32(P.tile_status + p);
-        } while ((s >> 2) != tag || (s & 3u) == 0u);
-        if ((s & 3u) == 2u) {
-          excl += *((volatile u128*)(P.tile_inc + p));
-          break;
-        }
-        excl += *((volatile u128*)(P.tile_agg + p));
-        --p;
+    if (l == 0) {
+      if (tile == 0) {
+        P.tile_inc[0] = agg;
+        __threadfence();
+        st_release_u32(P.tile_status + 0, (tag << 2) | 2u);
+      } else {
+        P.tile_agg[tile] = agg;
+        __threadfence();
+        st_release_u32(P.tile_status + tile, (tag << 2) | 1u);
       }
-      P.tile_inc[tile] = excl + agg;
-      __threadfence();
-      st_release_u32(P.tile_status + tile, (tag << 2) | 2u);
     }
-    s_excl = excl;
+    u128 excl = 0;
+    if (tile > 0) {
+      i64 pbase = tile - 1;
+      while (true) {
+        i64 p = pbase - l;
+        u32 s = 0;
+        if (p >= 0) {
+          do {
+            s = ld_acquire_u32(P.tile_status + p);
+          } while ((s >> 2) != tag || (s & 3u) == 0u);
+        }
+        bool incl = (p >= 0) && ((s & 3u) == 2u);
+        unsigned ball = __ballot_sync(0xffffffffu, incl);
+        int f = ball ? (__ffs(ball) - 1) : 32;
+        u128 v = 0;
+        if (p >= 0 && l <= f)
+          v = (l == f) ? *((volatile u128*)(P.tile_inc + p)) : *((volatile u128*)(P.tile_agg + p));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          u64 lo = (u64)v, hi = (u64)(v >> 64);
+          u64 olo = __shfl_xor_sync(0xffffffffu, lo, o);
+          u64 ohi = __shfl_xor_sync(0xffffffffu, hi, o);
+          v += ((u128)ohi << 64) | (u128)olo;
+        }
+        excl += v;
+        if (ball) break;
+        pbase -= 32;
+      }
+      if (l == 0) {
+        P.tile_inc[tile] = excl + agg;
+        __threadfence();
+        st_release_u32(P.tile_status + tile, (tag << 2) | 2u);
+      }
+    }
+    if (l == 0) s_excl = excl;
   }
   __syncthreads();
   u128 woff = 0;

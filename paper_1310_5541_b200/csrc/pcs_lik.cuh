@@ -65,9 +65,12 @@ __device__ __forceinline__ double nan_ll() { return __longlong_as_double(0x7ff80
 // ---- Gaussian windowed SSD (CANONICAL hot-path arithmetic) ----------------
 //   gx[i] = expf(-(d*d) * inv2s2), d = RN32(xi - x)        (fp32)
 //   pred  = fmaf(I0*gx[i], gy[j], bg); r = p - pred         (fp32)
-//   ssd   = sum fma((double)r, (double)r, ssd)              (fp64, exact terms,
-//                                                            row-major order)
+//   row_j = sum_i fma((double)r, (double)r, row_j)          (fp64, exact terms,
+//                                                            column order)
+//   ssd   = sum_j row_j                                     (fp64, row order)
 //   ll    = -ssd * inv_2sxi2                                (fp64)
+// The per-row partials let a warp evaluate one window with one lane per row
+// (k_pc_bins) and still match the per-thread loop bit for bit.
 template <int MAXS>
 __device__ __forceinline__ double loglik_gauss(const PixView& pv, float x, float y, float i0,
                                                const Spot& sp) {
@@ -93,13 +96,15 @@ __device__ __forceinline__ double loglik_gauss(const PixView& pv, float x, float
 #pragma unroll
     for (int i = 0; i < MAXS; ++i)
       if (i < nx) pr[i] = row[i];
+    double racc = 0.0;
 #pragma unroll
     for (int i = 0; i < MAXS; ++i) {
       if (i < nx) {
         float r = pr[i] - fmaf(ag[i], gy, sp.bg);
-        ssd = fma((double)r, (double)r, ssd);
+        racc = fma((double)r, (double)r, racc);
       }
     }
+    ssd += racc;
   }
   return -ssd * sp.inv_2sxi2;
 }
@@ -154,9 +159,11 @@ __device__ __forceinline__ double loglik_poisson(const PixView& pv, float x, flo
   for (int j = 0; j < ny; ++j) {
     const float* row = pv.row(ylo + j, xlo);
     float ey = psf_axis(__double2float_rn((double)(ylo + j) - (double)y), sp);
+    double racc = 0.0;
 #pragma unroll
     for (int i = 0; i < MAXS; ++i)
-      if (i < nx) ll += poisson_term(row[i], ex[i] * ey, sp.bg);
+      if (i < nx) racc += poisson_term(row[i], ex[i] * ey, sp.bg);
+    ll += racc;
   }
   return ll;
 }
@@ -182,12 +189,14 @@ __device__ __forceinline__ double loglik_gauss_generic(const PixView& pv, float 
     float d = __double2float_rn((double)yy - (double)y);
     float gy = expf(-(d * d) * sp.inv2s2);
     const float* row = pv.row(yy, xlo);
+    double racc = 0.0;
     for (int xx = xlo; xx <= xhi; ++xx) {
       float dx = __double2float_rn((double)xx - (double)x);
       float ag = i0 * expf(-(dx * dx) * sp.inv2s2);
       float r = row[xx - xlo] - fmaf(ag, gy, sp.bg);
-      ssd = fma((double)r, (double)r, ssd);
+      racc = fma((double)r, (double)r, racc);
     }
+    ssd += racc;
   }
   return -ssd * sp.inv_2sxi2;
 }
@@ -203,10 +212,12 @@ __device__ __forceinline__ double loglik_poisson_generic(const PixView& pv, floa
   for (int yy = ylo; yy <= yhi; ++yy) {
     float ey = psf_axis(__double2float_rn((double)yy - (double)y), sp);
     const float* row = pv.row(yy, xlo);
+    double racc = 0.0;
     for (int xx = xlo; xx <= xhi; ++xx) {
       float exi = i0 * psf_axis(__double2float_rn((double)xx - (double)x), sp) * inv_bg;
-      ll += poisson_term(row[xx - xlo], exi * ey, sp.bg);
+      racc += poisson_term(row[xx - xlo], exi * ey, sp.bg);
     }
+    ll += racc;
   }
   return ll;
 }
@@ -223,6 +234,48 @@ __device__ __forceinline__ double loglik_dispatch(const PixView& pv, float x, fl
                                                   const Spot& sp) {
   if constexpr (MAXS > 0) return loglik_any<MAXS>(pv, x, y, i0, sp);
   else return loglik_generic(pv, x, y, i0, sp);
+}
+
+// Warp-cooperative evaluation of one window: lane i owns column factor i,
+// lane j owns row j; row sums are accumulated in the same column order and
+// added in the same row order as the per-thread loops above, so the result is
+// bit-identical. All lanes return the value. Windows wider than 32 fall back
+// to the per-thread generic loop on every lane.
+__device__ __forceinline__ double loglik_warp(const PixView& pv, float x, float y, float i0,
+                                              const Spot& sp, int lane) {
+  if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
+  int xlo, xhi, ylo, yhi;
+  window_axis((double)x, sp.hw, pv.W, xlo, xhi);
+  window_axis((double)y, sp.hw, pv.H, ylo, yhi);
+  const int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
+  if (nx > 32 || ny > 32) return loglik_generic(pv, x, y, i0, sp);
+  const bool gauss = (sp.model == 0);
+  const float inv_bg = 1.0f / sp.bg;
+  float colf = 0.0f, rowf = 0.0f;
+  if (lane < nx) {
+    float d = __double2float_rn((double)(xlo + lane) - (double)x);
+    colf = gauss ? i0 * expf(-(d * d) * sp.inv2s2) : i0 * psf_axis(d, sp) * inv_bg;
+  }
+  if (lane < ny) {
+    float d = __double2float_rn((double)(ylo + lane) - (double)y);
+    rowf = gauss ? expf(-(d * d) * sp.inv2s2) : psf_axis(d, sp);
+  }
+  const float* row = pv.row(ylo + min(lane, ny - 1), xlo);
+  double racc = 0.0;
+  for (int i = 0; i < nx; ++i) {
+    float ci = __shfl_sync(0xffffffffu, colf, i);
+    if (lane < ny) {
+      if (gauss) {
+        float r = row[i] - fmaf(ci, rowf, sp.bg);
+        racc = fma((double)r, (double)r, racc);
+      } else {
+        racc += poisson_term(row[i], ci * rowf, sp.bg);
+      }
+    }
+  }
+  double tot = 0.0;
+  for (int j = 0; j < ny; ++j) tot += __shfl_sync(0xffffffffu, racc, j);
+  return gauss ? -tot * sp.inv_2sxi2 : tot;
 }
 
 // window bounds of a state (for staging decisions)

@@ -32,6 +32,28 @@ __device__ __forceinline__ i128 block_sum_i128(i128 v, i128* sh /*[BLOCK/32]*/) 
   return t;  // valid in thread 0
 }
 
+// K sums with one barrier pair; results valid in thread 0
+template <int BLOCK, int K>
+__device__ __forceinline__ void block_sum_i128_k(i128 (&v)[K], i128* sh /*[BLOCK/32*K]*/) {
+#pragma unroll
+  for (int c = 0; c < K; ++c) v[c] = warp_sum_i128(v[c]);
+  int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) sh[w * K + c] = v[c];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      i128 t = 0;
+      for (int q = 0; q < BLOCK / 32; ++q) t += sh[q * K + c];
+      v[c] = t;
+    }
+  }
+}
+
 __device__ __forceinline__ double warp_max_f64(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
