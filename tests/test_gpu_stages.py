@@ -31,10 +31,11 @@ def test_device_normals_match_philox_restatement(cuda):
     for frame, n, off in ((0, 10000, 0), (7, 3000, 2 ** 33 + 5)):
         dev = state.device_normals(seed, frame, n, offset=off).double().cpu().numpy()
         ref = orc.propagate_normals(seed, frame, n, offset=off)
-        # same Philox words; float32 Box-Muller (logf/sqrtf/sincospif) vs float64
-        assert np.max(np.abs(dev - ref)) < 2e-5
-        assert np.max(np.abs(dev - ref) / np.maximum(1.0, np.abs(ref))) < 1e-5
-        assert np.median(np.abs(dev - ref)) < 1e-7
+        # same Philox words; float32 SFU Box-Muller (__logf/__sincosf, ~2^-21
+        # absolute) vs the float64 restatement
+        assert np.max(np.abs(dev - ref)) < 1e-4
+        assert np.max(np.abs(dev - ref) / np.maximum(1.0, np.abs(ref))) < 2e-5
+        assert np.median(np.abs(dev - ref)) < 5e-7
 
 
 def test_device_normals_law(cuda):
