@@ -28,6 +28,7 @@ constexpr int S1_THREADS = 512;
 constexpr int S1_IPT = 4;
 constexpr int S1_TILE = S1_THREADS * S1_IPT;   // 2048 particles per tile
 constexpr int S1_WARPS = S1_THREADS / 32;
+constexpr int S1_RUN = 8;                      // sorted particles summed per thread
 constexpr int SUBW = 1536;                     // shared-memory sub-window cells
 constexpr i64 TABLE_MAX = 1ll << 28;           // dense full-grid table (cells)
 constexpr int MAXM = 16384;                    // occupied cells per frame (fused)
@@ -126,6 +127,21 @@ __device__ __forceinline__ void reset_frame(TrackCtl* c) {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ i64 cell_axis_fast(float p, double origin, double cell, double inv,
                                               i64 n) {
+  // float32 estimate first: accepted when its fractional part is farther from
+  // an integer than its error bound (|p|+|o|)|1/l| 2^-20 + |t| 2^-20
+  {
+    float o32 = (float)origin, inv32 = (float)inv;
+    float t32 = (p - o32) * inv32;
+    float f32 = floorf(t32);
+    float fr32 = t32 - f32;
+    float margin = ((fabsf(p) + fabsf(o32)) * fabsf(inv32) + fabsf(t32) + 1.0f) *
+                   9.5367431640625e-07f;
+    if (fr32 > margin && fr32 < 1.0f - margin) {
+      if (!(f32 >= 0.0f)) return 0;
+      if ((double)f32 > (double)(n - 1)) return n - 1;
+      return (i64)f32;
+    }
+  }
   double d = __dsub_rn((double)p, origin);
   double t = __dmul_rn(d, inv);
   double f = floor(t);
@@ -312,36 +328,38 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
       sm.pay_q[pos] = (unsigned short)q_k[it];
     }
     __syncthreads();
-    // ---- phase 4: warp segmented scans over sorted runs -> int128 accumulators ----
+    // ---- phase 4: each thread sums a window of S1_RUN sorted particles in
+    //      order, flushing a partial into the int128 accumulators whenever the
+    //      cell changes (exactness of v - ref was verified in phase 1) ----
     const int nin = (int)sm.n_in;
-    for (int base = warp * 32; base < nin; base += S1_THREADS) {
-      int pos = base + lane;
-      bool valid = pos < nin;
-      int q = valid ? (int)sm.pay_q[pos] : -1 - lane;
+    for (int w0 = t * S1_RUN; w0 < nin; w0 += S1_THREADS * S1_RUN) {
+      const int w1 = min(nin, w0 + S1_RUN);
+      int cq = -1;
+      float rx = 0.f, ry = 0.f;
       long long v[5] = {0, 0, 0, 0, 0};
-      if (valid) {
-        i64 ix = sx0 + q % snx, iy = sy0 + q / snx;
-        bool ok;
-        float rx = cell_ref32(g.ox, g.lx, ix, ok), ry = cell_ref32(g.oy, g.ly, iy, ok);
-        delta_fixed(sm.pay[0][pos], rx, v[0]);
-        delta_fixed(sm.pay[1][pos], ry, v[1]);
+      for (int pos = w0; pos < w1; ++pos) {
+        int q = sm.pay_q[pos];
+        if (q != cq) {
+          if (cq >= 0) {
 #pragma unroll
-        for (int c = 2; c < 5; ++c) v[c] = __float2ll_rn(__fmul_rn(sm.pay[c][pos], 1099511627776.0f));
-      }
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        int qo = __shfl_up_sync(0xffffffffu, q, d);
-#pragma unroll
-        for (int c = 0; c < 5; ++c) {
-          long long o = __shfl_up_sync(0xffffffffu, v[c], d);
-          if (lane >= d && qo == q) v[c] += o;
+            for (int c = 0; c < 5; ++c) {
+              smem_add_i128(&sm.acc_lo[c][cq], &sm.acc_hi[c][cq], v[c]);
+              v[c] = 0;
+            }
+          }
+          cq = q;
+          bool ok;
+          rx = cell_ref32(g.ox, g.lx, sx0 + q % snx, ok);
+          ry = cell_ref32(g.oy, g.ly, sy0 + q / snx, ok);
         }
-      }
-      int qn = __shfl_down_sync(0xffffffffu, q, 1);
-      bool tail = valid && (lane == 31 || qn != q);
-      if (tail) {
+        v[0] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[0][pos], rx), 1099511627776.0f));
+        v[1] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[1][pos], ry), 1099511627776.0f));
 #pragma unroll
-        for (int c = 0; c < 5; ++c) smem_add_i128(&sm.acc_lo[c][q], &sm.acc_hi[c][q], v[c]);
+        for (int c = 2; c < 5; ++c) v[c] += __float2ll_rn(__fmul_rn(sm.pay[c][pos], 1099511627776.0f));
+      }
+      if (cq >= 0) {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) smem_add_i128(&sm.acc_lo[c][cq], &sm.acc_hi[c][cq], v[c]);
       }
     }
     // ---- phase 5: counts; reset the tile state ----
@@ -381,7 +399,9 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
 constexpr int BINS_BLOCK = 1024;
 constexpr int BINS_MAXM = 8192;              // occupied cells handled by the fused bins kernel
 constexpr int STAGE_PIX = 12288;             // staged frame tile (48 KB)
-constexpr size_t BINS_SMEM = BINS_MAXM * sizeof(double) + STAGE_PIX * sizeof(float);
+constexpr int ROWBUF = 4096;                 // (cell, row) partials per chunk (32 KB)
+constexpr size_t BINS_SMEM =
+    BINS_MAXM * sizeof(double) + STAGE_PIX * sizeof(float) + ROWBUF * sizeof(double);
 
 struct BinsScratch {  // global scratch for the dummies of the occupied cells
   float* dx;
@@ -395,6 +415,8 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   extern __shared__ __align__(16) unsigned char bins_raw[];
   double* s_ll = reinterpret_cast<double*>(bins_raw);
   float* s_pix = reinterpret_cast<float*>(bins_raw + BINS_MAXM * sizeof(double));
+  double* s_row = reinterpret_cast<double*>(bins_raw + BINS_MAXM * sizeof(double) +
+                                            STAGE_PIX * sizeof(float));
   __shared__ i128 s_red[BINS_BLOCK / 32];
   __shared__ i128 s_red6[BINS_BLOCK / 32 * 6];
   __shared__ long long s_max;
@@ -469,16 +491,44 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     }
   }
   __syncthreads();
-  // 3) likelihood once per occupied cell (binning.py:189): one warp per cell
+  // 3) likelihood once per occupied cell (binning.py:189): one thread per
+  //    (cell, window row) computes the row partial; then one thread per cell
+  //    adds its rows in row order (= the canonical per-thread loop)
   long long lmax = LLONG_MIN;
   {
-    const int lane = t & 31, warp = t >> 5;
-    for (int b = warp; b < M; b += BINS_BLOCK / 32) {
-      double ll = loglik_warp(pv, Sd.dx[b], Sd.dy[b], Sd.di[b], P.spot, lane);
-      if (lane == 0) {
+    const int S = 2 * P.spot.hw + 1;
+    const int C = ROWBUF / S;   // cells per chunk
+    for (int b0 = 0; b0 < M; b0 += C) {
+      const int nb = min(C, M - b0);
+      for (int it = t; it < nb * S; it += BINS_BLOCK) {
+        int b = b0 + it / S, j = it % S;
+        float x = Sd.dx[b], y = Sd.dy[b], i0 = Sd.di[b];
+        double part = 0.0;
+        if (x == x && y == y && i0 == i0) {
+          int xlo, xhi, ylo, yhi;
+          window_of(x, y, P.spot, P.H, P.W, xlo, xhi, ylo, yhi);
+          if (j <= yhi - ylo) part = loglik_row(pv, x, y, i0, P.spot, xlo, xhi - xlo + 1, ylo + j);
+        }
+        s_row[it] = part;
+      }
+      __syncthreads();
+      for (int bb = t; bb < nb; bb += BINS_BLOCK) {
+        int b = b0 + bb;
+        float x = Sd.dx[b], y = Sd.dy[b], i0 = Sd.di[b];
+        double ll;
+        if (!(x == x) || !(y == y) || !(i0 == i0)) {
+          ll = nan_ll();
+        } else {
+          int xlo, xhi, ylo, yhi;
+          window_of(x, y, P.spot, P.H, P.W, xlo, xhi, ylo, yhi);
+          double tot = 0.0;
+          for (int j = 0; j <= yhi - ylo; ++j) tot += s_row[bb * S + j];
+          ll = (P.spot.model == 0) ? -tot * P.spot.inv_2sxi2 : tot;
+        }
         s_ll[b] = ll;
         lmax = max(lmax, (long long)f64_to_ordered(ll));
       }
+      __syncthreads();
     }
   }
   atomicMax(&s_max, lmax);

@@ -278,6 +278,31 @@ __device__ __forceinline__ double loglik_warp(const PixView& pv, float x, float 
   return gauss ? -tot * sp.inv_2sxi2 : tot;
 }
 
+// One row of one window: the float64 partial row_j of the canonical form
+// (column order), computed by one thread. Summing the rows of a window in row
+// order reproduces loglik_gauss / loglik_poisson bit for bit.
+__device__ __forceinline__ double loglik_row(const PixView& pv, float x, float y, float i0,
+                                             const Spot& sp, int xlo, int nx, int yy) {
+  const bool gauss = (sp.model == 0);
+  const float inv_bg = 1.0f / sp.bg;
+  float d = __double2float_rn((double)yy - (double)y);
+  float rowf = gauss ? expf(-(d * d) * sp.inv2s2) : psf_axis(d, sp);
+  const float* row = pv.row(yy, xlo);
+  double racc = 0.0;
+  for (int i = 0; i < nx; ++i) {
+    float dx = __double2float_rn((double)(xlo + i) - (double)x);
+    if (gauss) {
+      float ag = i0 * expf(-(dx * dx) * sp.inv2s2);
+      float r = row[i] - fmaf(ag, rowf, sp.bg);
+      racc = fma((double)r, (double)r, racc);
+    } else {
+      float ex = i0 * psf_axis(dx, sp) * inv_bg;
+      racc += poisson_term(row[i], ex * rowf, sp.bg);
+    }
+  }
+  return racc;
+}
+
 // window bounds of a state (for staging decisions)
 __device__ __forceinline__ void window_of(float x, float y, const Spot& sp, i64 H, i64 W, int& xlo,
                                           int& xhi, int& ylo, int& yhi) {
