@@ -210,6 +210,8 @@ int pcs_track_steps_timed(pcs_ctx* ctx, const float* frames, int64_t k0, int64_t
                           double* ess, uint8_t* resampled, int64_t* occupied, double* kernel_ms,
                           int32_t max_kernels, void* stream);
 const char* pcs_track_kernel_name(pcs_ctx* ctx, int32_t i);
+/* phase timestamps (globaltimer ns) recorded by the fused bins kernel */
+int pcs_track_debug(pcs_ctx* ctx, int64_t* out16, void* stream);
 /* kernel launches per fused step (for gpu_launches accounting) */
 int pcs_track_launches_per_step(pcs_ctx* ctx);
 /* export the current particle states / last ancestors of a running track */

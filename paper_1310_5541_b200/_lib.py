@@ -115,6 +115,7 @@ _SIGNATURES = [
                                         c_void_p, c_void_p, c_void_p, c_int32, c_void_p]),
     ("pcs_track_kernel_name", c_char_p, [c_void_p, c_int32]),
     ("pcs_track_launches_per_step", c_int32, [c_void_p]),
+    ("pcs_track_debug", c_int32, [c_void_p, c_void_p, c_void_p]),
     ("pcs_track_states", c_int32, [c_void_p, P(c_void_p), P(c_int64)]),
 ]
 

@@ -898,6 +898,16 @@ int pcs_track(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, const float* frames, int
 
 int pcs_track_launches_per_step(pcs_ctx* ctx) { return ctx ? ctx->tr.launches : 0; }
 
+int pcs_track_debug(pcs_ctx* ctx, int64_t* out16, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && out16, "bad arguments");
+  cudaStream_t st = S(stream);
+  TrackCtl h;
+  PCS_CUDA_TRY(cudaMemcpyAsync(&h, ctx->tr.P.ctl, sizeof(h), cudaMemcpyDeviceToHost, st));
+  PCS_CUDA_TRY(cudaStreamSynchronize(st));
+  for (int i = 0; i < 16; ++i) out16[i] = h.dbg[i];
+  return PCS_OK;
+}
+
 int pcs_track_states(pcs_ctx* ctx, float** states, int64_t* ld) {
   PCS_CHECK_ARG(ctx && ctx->tr.active && states && ld, "bad arguments");
   // frame k reads buf[k&1] and writes buf[(k+1)&1]

@@ -75,6 +75,7 @@ struct TrackCtl {
   int first_bad;
   i64 evals;
   double center[2];          // previous estimate (shared-memory sub-window centre)
+  long long dbg[16];         // phase timestamps (globaltimer ns) of the bins kernel
   unsigned long long tile_ctr;  // decoupled look-back: monotone tile ticket counter
 };
 
@@ -397,6 +398,14 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
 // resampling decision. Zeroes the consumed table cells.
 // ===========================================================================
 constexpr int BINS_BLOCK = 1024;
+#define PCS_PROBE(i)                                                                  \
+  do {                                                                                \
+    if (threadIdx.x == 0) {                                                           \
+      unsigned long long _g;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_g));                          \
+      C->dbg[i] = (long long)_g;                                                      \
+    }                                                                                 \
+  } while (0)
 constexpr int BINS_MAXM = 8192;              // occupied cells handled by the fused bins kernel
 constexpr int STAGE_PIX = 12288;             // staged frame tile (48 KB)
 constexpr int ROWBUF = 4096;                 // (cell, row) partials per chunk (32 KB)
@@ -439,6 +448,7 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   }
   const int M = (int)nocc;
   const float* frame = C->frames + (k - C->k_frames) * P.H * P.W;
+  PCS_PROBE(0);
   if (t == 0) {
     s_max = LLONG_MIN;
     s_wmin = 0xFFFFFFFFu;
@@ -474,6 +484,7 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   atomicMin(&s_box[0], bx0); atomicMax(&s_box[1], bx1);
   atomicMin(&s_box[2], by0); atomicMax(&s_box[3], by1);
   __syncthreads();
+  PCS_PROBE(1);
   // 2) stage the frame region covering every window in shared memory
   PixView pv = frame_view(frame, P.H, P.W);
   {
@@ -491,6 +502,7 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     }
   }
   __syncthreads();
+  PCS_PROBE(2);
   // 3) likelihood once per occupied cell (binning.py:189): one thread per
   //    (cell, window row) computes the row partial; then one thread per cell
   //    adds its rows in row order (= the canonical per-thread loop)
@@ -536,6 +548,7 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   const double m = ordered_to_f64((i64)s_max);
   const bool bad_m = !(m == m) || m == INFINITY;
   const bool degenerate = (m == -INFINITY);
+  PCS_PROBE(3);
   // 4) normaliser S = sum_b cnt_b * round(exp(ll_b - m) * 2^95)
   i128 acc = 0;
   for (int b = t; b < M; b += BINS_BLOCK) {
@@ -546,6 +559,7 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   if (t == 0) s_Sf = scalbn(i128_to_f64_rn(Sfix), -FX_S);
   __syncthreads();
   const double Sf = s_Sf;
+  PCS_PROBE(4);
   // 5) weights per cell (broadcast table), estimate, ESS; zero consumed cells
   i128 e[6] = {0, 0, 0, 0, 0, 0};
   for (int b = t; b < M; b += BINS_BLOCK) {
@@ -568,7 +582,9 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   }
   double est[5];
   double w2f = 0;
+  PCS_PROBE(5);
   block_sum_i128_k<BINS_BLOCK, 6>(e, s_red6);
+  PCS_PROBE(6);
   if (t == 0) {
 #pragma unroll
     for (int c = 0; c < 5; ++c) est[c] = scalbn(i128_to_f64_rn(e[c]), -(FX_WQ + FX_STATE));
@@ -597,6 +613,7 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     reset_frame(C);
     C->k = k + 1;   // last reader of k in this frame
   }
+  PCS_PROBE(7);
 }
 
 // ===========================================================================
