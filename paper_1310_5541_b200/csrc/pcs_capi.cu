@@ -693,6 +693,18 @@ static int set_attrs() {
                                     (int)BINS_SMEM));
   PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<15>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)BINS_SMEM));
+  // one shared-memory carveout for every kernel of the frame: consecutive
+  // kernels with different carveouts force an SM reconfiguration between them
+  const void* fns[] = {(const void*)k_pc_step1,        (const void*)k_pc_bins<0>,
+                       (const void*)k_pc_bins<9>,       (const void*)k_pc_bins<11>,
+                       (const void*)k_pc_bins<15>,      (const void*)k_scan_emit<1>,
+                       (const void*)k_scan_emit<2>,     (const void*)k_sir_propagate_lik<0>,
+                       (const void*)k_sir_propagate_lik<9>, (const void*)k_sir_propagate_lik<11>,
+                       (const void*)k_sir_propagate_lik<15>, (const void*)k_sir_sum,
+                       (const void*)k_sir_stats,        (const void*)k_sir_finalize};
+  for (const void* f : fns)
+    PCS_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                      (int)cudaSharedmemCarveoutMaxShared));
   g_attr_done = true;
   return PCS_OK;
 }

@@ -28,7 +28,7 @@ constexpr int S1_THREADS = 512;
 constexpr int S1_IPT = 4;
 constexpr int S1_TILE = S1_THREADS * S1_IPT;   // 2048 particles per tile
 constexpr int S1_WARPS = S1_THREADS / 32;
-constexpr int S1_RUN = 8;                      // sorted particles summed per thread
+constexpr int S1_SMALL = 16;                   // runs up to this length are owned by one lane
 constexpr int SUBW = 1536;                     // shared-memory sub-window cells
 constexpr i64 TABLE_MAX = 1ll << 28;           // dense full-grid table (cells)
 constexpr int MAXM = 16384;                    // occupied cells per frame (fused)
@@ -42,6 +42,7 @@ struct S1Smem {
   float pay[5][S1_TILE];
   unsigned short pay_q[S1_TILE];
   unsigned short list[S1_TILE];
+  u32 lcnt[S1_TILE];      // count of list entry e (immutable within phase 4)
   u32 n_list;
   u32 n_in;
   int scan_tmp[S1_WARPS];
@@ -192,6 +193,17 @@ __device__ __forceinline__ void smem_add_i128(unsigned long long* lo, unsigned l
   if (vhi) atomicAdd(hi, vhi);
 }
 
+// exclusive (single-owner) int128 read-modify-write in shared memory
+__device__ __forceinline__ void smem_rmw_i128(unsigned long long* lo, unsigned long long* hi,
+                                              long long v) {
+  unsigned long long vlo = (unsigned long long)v;
+  unsigned long long vhi = (v < 0) ? ~0ull : 0ull;
+  unsigned long long old = *lo;
+  unsigned long long nlo = old + vlo;
+  *lo = nlo;
+  *hi += vhi + (nlo < old ? 1ull : 0ull);
+}
+
 // ===========================================================================
 // pcSIR step 1
 // ===========================================================================
@@ -313,7 +325,10 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         int idx = base + e;
-        if (idx < nl) sm.tile_start[sm.list[idx]] = (u32)run;
+        if (idx < nl) {
+          sm.tile_start[sm.list[idx]] = (u32)run;
+          sm.lcnt[idx] = (u32)loc[e];
+        }
         run += loc[e];
       }
       if (t == S1_THREADS - 1) sm.n_in = (u32)run;
@@ -329,45 +344,55 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
       sm.pay_q[pos] = (unsigned short)q_k[it];
     }
     __syncthreads();
-    // ---- phase 4: each thread sums a window of S1_RUN sorted particles in
-    //      order, flushing a partial into the int128 accumulators whenever the
-    //      cell changes (exactness of v - ref was verified in phase 1) ----
-    const int nin = (int)sm.n_in;
-    for (int w0 = t * S1_RUN; w0 < nin; w0 += S1_THREADS * S1_RUN) {
-      const int w1 = min(nin, w0 + S1_RUN);
-      int cq = -1;
-      float rx = 0.f, ry = 0.f;
+    // ---- phase 4: each occupied cell of the tile has exactly one owner that
+    //      sums its sorted run and updates the int128 accumulators with a plain
+    //      read-modify-write (no atomics): runs of <= S1_SMALL particles are
+    //      owned by one lane, longer runs by a whole warp (exactness of v - ref
+    //      was verified in phase 1) ----
+    for (int e = t; e < nl; e += S1_THREADS) {
+      const int cnt = (int)sm.lcnt[e];
+      if (cnt > S1_SMALL) continue;
+      const int q = sm.list[e], st = (int)sm.tile_start[q];
+      bool ok;
+      const float rx = cell_ref32(g.ox, g.lx, sx0 + q % snx, ok);
+      const float ry = cell_ref32(g.oy, g.ly, sy0 + q / snx, ok);
       long long v[5] = {0, 0, 0, 0, 0};
-      for (int pos = w0; pos < w1; ++pos) {
-        int q = sm.pay_q[pos];
-        if (q != cq) {
-          if (cq >= 0) {
-#pragma unroll
-            for (int c = 0; c < 5; ++c) {
-              smem_add_i128(&sm.acc_lo[c][cq], &sm.acc_hi[c][cq], v[c]);
-              v[c] = 0;
-            }
-          }
-          cq = q;
-          bool ok;
-          rx = cell_ref32(g.ox, g.lx, sx0 + q % snx, ok);
-          ry = cell_ref32(g.oy, g.ly, sy0 + q / snx, ok);
-        }
+      for (int pos = st; pos < st + cnt; ++pos) {
         v[0] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[0][pos], rx), 1099511627776.0f));
         v[1] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[1][pos], ry), 1099511627776.0f));
 #pragma unroll
         for (int c = 2; c < 5; ++c) v[c] += __float2ll_rn(__fmul_rn(sm.pay[c][pos], 1099511627776.0f));
       }
-      if (cq >= 0) {
 #pragma unroll
-        for (int c = 0; c < 5; ++c) smem_add_i128(&sm.acc_lo[c][cq], &sm.acc_hi[c][cq], v[c]);
-      }
-    }
-    // ---- phase 5: counts; reset the tile state ----
-    for (int e = t; e < nl; e += S1_THREADS) {
-      int q = sm.list[e];
-      sm.acc_cnt[q] += sm.tile_cnt[q];
+      for (int c = 0; c < 5; ++c) smem_rmw_i128(&sm.acc_lo[c][q], &sm.acc_hi[c][q], v[c]);
+      sm.acc_cnt[q] += (u32)cnt;
       sm.tile_cnt[q] = 0;
+    }
+    for (int e = warp; e < nl; e += S1_WARPS) {
+      const int cnt = (int)sm.lcnt[e];
+      if (cnt <= S1_SMALL) continue;
+      const int q = sm.list[e], st = (int)sm.tile_start[q];
+      bool ok;
+      const float rx = cell_ref32(g.ox, g.lx, sx0 + q % snx, ok);
+      const float ry = cell_ref32(g.oy, g.ly, sy0 + q / snx, ok);
+      long long v[5] = {0, 0, 0, 0, 0};
+      for (int pos = st + lane; pos < st + cnt; pos += 32) {
+        v[0] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[0][pos], rx), 1099511627776.0f));
+        v[1] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[1][pos], ry), 1099511627776.0f));
+#pragma unroll
+        for (int c = 2; c < 5; ++c) v[c] += __float2ll_rn(__fmul_rn(sm.pay[c][pos], 1099511627776.0f));
+      }
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) smem_rmw_i128(&sm.acc_lo[c][q], &sm.acc_hi[c][q], v[c]);
+        sm.acc_cnt[q] += (u32)cnt;
+        sm.tile_cnt[q] = 0;
+      }
     }
     __syncthreads();
     if (t == 0) sm.n_list = 0;
