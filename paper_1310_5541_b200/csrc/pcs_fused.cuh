@@ -446,6 +446,7 @@ struct BinsScratch {  // global scratch for the dummies of the occupied cells
 template <int MAXS>
 __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScratch Sd) {
   TrackCtl* C = P.ctl;
+  PCS_PROBE(8);
   extern __shared__ __align__(16) unsigned char bins_raw[];
   double* s_ll = reinterpret_cast<double*>(bins_raw);
   float* s_pix = reinterpret_cast<float*>(bins_raw + BINS_MAXM * sizeof(double));
@@ -639,6 +640,8 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     C->k = k + 1;   // last reader of k in this frame
   }
   PCS_PROBE(7);
+  __syncthreads();
+  PCS_PROBE(9);
 }
 
 // ===========================================================================

@@ -34,4 +34,5 @@ for f in range(k):
     dbg = (ctypes.c_int64 * 16)()
     _lib.check(_lib.lib().pcs_track_debug(_lib.ctx(), dbg, st))
     t = np.array(dbg[:8], dtype=np.int64)
-    print(f"frame {f} occ={int(occ[f])} phase ns:", np.diff(t).tolist(), "total", t[7] - t[0])
+    print(f"frame {f} occ={int(occ[f])} phase ns:", np.diff(t).tolist(), "total", t[7] - t[0],
+          "entry->p0", t[0] - dbg[8], "p7->exit", dbg[9] - t[7])
