@@ -217,6 +217,29 @@ int pcs_track_launches_per_step(pcs_ctx* ctx);
 /* export the current particle states / last ancestors of a running track */
 int pcs_track_states(pcs_ctx* ctx, float** states, int64_t* ld);
 
+/* ---- particle-sharded giant filter (config 5, new; no reference code).
+ * One rank's side of each phase; the host exchanges between the calls:
+ * step1 -> all-reduce(bbox MIN/MAX) -> export(window limbs) ->
+ * all-reduce(limbs SUM) -> import_bins -> scan -> all-gather(rank totals) ->
+ * emit(prefix, slot_lo) -> gather per destination -> all-to-all -> set_states
+ * (or advance when the frame did not resample). Limbs: per cell
+ * [count, 5 x (three 42-bit limbs of the int128 sum)] as int64. */
+int pcs_shard_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t height, int64_t width,
+                    int64_t index_offset, int64_t n_global, int64_t slot_capacity, void* stream);
+int pcs_shard_step1(pcs_ctx* ctx, const float* frame, int64_t k, double* est, double* ess,
+                    uint8_t* resampled, int64_t* occupied, int64_t* bbox5_out, void* stream);
+int pcs_shard_export(pcs_ctx* ctx, int64_t x0, int64_t y0, int64_t nx, int64_t ny,
+                     int64_t* limbs, void* stream);
+int pcs_shard_import_bins(pcs_ctx* ctx, int64_t x0, int64_t y0, int64_t nx, int64_t ny,
+                          const int64_t* limbs, void* stream);
+int pcs_shard_scan(pcs_ctx* ctx, uint64_t* total_lo, uint64_t* total_hi, int32_t* do_resample,
+                   void* stream);
+int pcs_shard_emit(pcs_ctx* ctx, uint64_t prefix_lo, uint64_t prefix_hi, int64_t slot_lo,
+                   int32_t** ancestors, void* stream);
+int pcs_shard_gather(pcs_ctx* ctx, int64_t first, int64_t count, float* out, void* stream);
+int pcs_shard_set_states(pcs_ctx* ctx, const float* states, void* stream);
+int pcs_shard_advance(pcs_ctx* ctx, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

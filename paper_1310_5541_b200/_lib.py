@@ -117,6 +117,19 @@ _SIGNATURES = [
     ("pcs_track_launches_per_step", c_int32, [c_void_p]),
     ("pcs_track_debug", c_int32, [c_void_p, c_void_p, c_void_p]),
     ("pcs_track_states", c_int32, [c_void_p, P(c_void_p), P(c_int64)]),
+    ("pcs_shard_begin", c_int32, [c_void_p, P(PcsTrackCfg), c_int64, c_int64, c_int64, c_int64,
+                                  c_int64, c_void_p]),
+    ("pcs_shard_step1", c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
+                                  c_void_p, P(c_int64), c_void_p]),
+    ("pcs_shard_export", c_int32, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_void_p,
+                                   c_void_p]),
+    ("pcs_shard_import_bins", c_int32, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_void_p,
+                                        c_void_p]),
+    ("pcs_shard_scan", c_int32, [c_void_p, P(c_uint64), P(c_uint64), P(c_int32), c_void_p]),
+    ("pcs_shard_emit", c_int32, [c_void_p, c_uint64, c_uint64, c_int64, P(c_void_p), c_void_p]),
+    ("pcs_shard_gather", c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+    ("pcs_shard_set_states", c_int32, [c_void_p, c_void_p, c_void_p]),
+    ("pcs_shard_advance", c_int32, [c_void_p, c_void_p]),
 ]
 
 EXPORTED_SYMBOLS = [name for name, _, _ in _SIGNATURES]

@@ -17,6 +17,7 @@
 #include "pcs_common.cuh"
 #include "pcs_lik.cuh"
 #include "pcs_state.cuh"
+#include "pcs_shard.cuh"
 #include "pcs_track.cuh"
 #include "pcs_weights.cuh"
 
@@ -100,6 +101,8 @@ enum Slot {
   SL_TR_CTL,
   SL_TR_TILES,
   SL_TR_PRE,
+  SL_SHARD_ANC,
+  SL_SHARD_BOX,
   SL_COUNT
 };
 
@@ -748,9 +751,15 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   P.seed = cfg->seed;
   P.frame0 = cfg->frame0;
   P.placement = cfg->placement;
+  P.idx_off = 0;
+  P.n_global = n;
+  P.slot_lo = 0;
+  P.slot_cap = n;
+  P.scan_mode = 0;
   PCS_SCRATCH(SL_TR_BUF0, 5 * ld * sizeof(float), P.buf0);
   PCS_SCRATCH(SL_TR_BUF1, 5 * ld * sizeof(float), P.buf1);
   PCS_SCRATCH(SL_TR_ANC, ld * sizeof(int), P.anc);
+  P.anc_out = P.anc;
   PCS_SCRATCH(SL_TR_CTL, sizeof(TrackCtl), P.ctl);
   P.ntiles = ceil_div(n, SCAN_TILE);
   PCS_SCRATCH(SL_TR_TILES, P.ntiles * (2 * sizeof(u128) + sizeof(u32)) + 64, P.tile_agg);
@@ -909,6 +918,154 @@ int pcs_track(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, const float* frames, int
 }
 
 int pcs_track_launches_per_step(pcs_ctx* ctx) { return ctx ? ctx->tr.launches : 0; }
+
+// ---------------------------------------------------------------------------
+// particle-sharded giant filter (config 5): one rank's side of each phase
+// ---------------------------------------------------------------------------
+int pcs_shard_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t W,
+                    int64_t idx_off, int64_t n_global, int64_t slot_cap, void* stream) {
+  PCS_CHECK_ARG(ctx && cfg && cfg->method == 1, "sharded filter is pcSIR only");
+  PCS_CHECK_ARG(idx_off >= 0 && n_global >= idx_off + cfg->n_particles, "bad shard range");
+  pcs_track_cfg_t c = *cfg;
+  c.use_graph = 0;
+  int r = pcs_track_begin(ctx, &c, H, W, stream);
+  if (r) return r;
+  TrackState& T = ctx->tr;
+  TrackParams& P = T.P;
+  P.idx_off = idx_off;
+  P.n_global = n_global;
+  P.slot_cap = slot_cap;
+  PCS_SCRATCH(SL_SHARD_ANC, slot_cap * sizeof(int), P.anc_out);
+  // the initial cloud uses the global particle index as the Philox counter
+  pcs_init_t init = cfg->init;
+  r = pcs_init_particles(&init, cfg->seed, idx_off, P.n, P.buf0, P.ld, stream);
+  if (r) return r;
+  return PCS_OK;
+}
+
+int pcs_shard_step1(pcs_ctx* ctx, const float* frame, int64_t k, double* est, double* ess,
+                    uint8_t* res, int64_t* occ, int64_t* bbox5_out, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && frame && bbox5_out, "bad arguments");
+  PCS_CHECK_ARG(k == ctx->tr.k, "frames must be stepped in order");
+  cudaStream_t st = S(stream);
+  TrackState& T = ctx->tr;
+  i64* dbox;
+  PCS_SCRATCH(SL_SHARD_BOX, 8 * sizeof(i64), dbox);
+  k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frame, k, k, est, ess, res, (i64*)occ);
+  k_pc_step1<<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(T.P);
+  k_shard_bbox<<<1, 1024, 0, st>>>(T.P, dbox);
+  PCS_LAUNCH_CHECK();
+  PCS_CUDA_TRY(cudaMemcpyAsync(bbox5_out, dbox, 5 * sizeof(i64), cudaMemcpyDeviceToHost, st));
+  PCS_CUDA_TRY(cudaStreamSynchronize(st));
+  return PCS_OK;
+}
+
+int pcs_shard_export(pcs_ctx* ctx, int64_t x0, int64_t y0, int64_t nx, int64_t ny, int64_t* limbs,
+                     void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && limbs && nx >= 1 && ny >= 1, "bad arguments");
+  k_shard_export<<<grid_for(nx * ny, 256, ctx->sms), 256, 0, S(stream)>>>(ctx->tr.P, x0, y0, nx,
+                                                                           ny, (i64*)limbs);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+int pcs_shard_import_bins(pcs_ctx* ctx, int64_t x0, int64_t y0, int64_t nx, int64_t ny,
+                          const int64_t* limbs, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && limbs, "bad arguments");
+  cudaStream_t st = S(stream);
+  TrackState& T = ctx->tr;
+  k_shard_import<<<grid_for(nx * ny, 256, ctx->sms), 256, 0, st>>>(T.P, x0, y0, nx, ny,
+                                                                  (const i64*)limbs);
+  switch (T.maxs) {
+    case 9: k_pc_bins<9><<<1, BINS_BLOCK, BINS_SMEM, st>>>(T.P, T.bins); break;
+    case 11: k_pc_bins<11><<<1, BINS_BLOCK, BINS_SMEM, st>>>(T.P, T.bins); break;
+    case 15: k_pc_bins<15><<<1, BINS_BLOCK, BINS_SMEM, st>>>(T.P, T.bins); break;
+    default: k_pc_bins<0><<<1, BINS_BLOCK, BINS_SMEM, st>>>(T.P, T.bins);
+  }
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+// rank-local exact prefix; returns the rank total (u128 as lo, hi) and the
+// resampling decision of this frame
+int pcs_shard_scan(pcs_ctx* ctx, uint64_t* total_lo, uint64_t* total_hi, int32_t* do_resample,
+                   void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && total_lo && total_hi && do_resample, "bad arguments");
+  cudaStream_t st = S(stream);
+  TrackState& T = ctx->tr;
+  TrackParams Q = T.P;
+  Q.scan_mode = 1;
+  k_scan_emit<1><<<(unsigned)Q.ntiles, SCAN_BLOCK, 0, st>>>(Q);
+  PCS_LAUNCH_CHECK();
+  u128 tot = 0;
+  TrackCtl h;
+  PCS_CUDA_TRY(cudaMemcpyAsync(&tot, Q.tile_inc + (Q.ntiles - 1), sizeof(u128),
+                               cudaMemcpyDeviceToHost, st));
+  PCS_CUDA_TRY(cudaMemcpyAsync(&h, Q.ctl, sizeof(h), cudaMemcpyDeviceToHost, st));
+  PCS_CUDA_TRY(cudaStreamSynchronize(st));
+  *do_resample = h.do_resample;
+  if (!h.do_resample) tot = 0;
+  *total_lo = (uint64_t)tot;
+  *total_hi = (uint64_t)(tot >> 64);
+  return PCS_OK;
+}
+
+// emit this rank's global slots [slot_lo, slot_lo + count) as local ancestors
+int pcs_shard_emit(pcs_ctx* ctx, uint64_t prefix_lo, uint64_t prefix_hi, int64_t slot_lo,
+                   int32_t** anc_out, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && anc_out, "bad arguments");
+  cudaStream_t st = S(stream);
+  TrackState& T = ctx->tr;
+  k_shard_set_prefix<<<1, 1, 0, st>>>(T.P.ctl, prefix_lo, prefix_hi);
+  TrackParams Q = T.P;
+  Q.scan_mode = 2;
+  Q.slot_lo = slot_lo;
+  k_scan_emit<1><<<(unsigned)Q.ntiles, SCAN_BLOCK, 0, st>>>(Q);
+  PCS_LAUNCH_CHECK();
+  *anc_out = Q.anc_out;
+  return PCS_OK;
+}
+
+// the states to send: out[c*count + q] = current[c][anc_out[first + q]]
+int pcs_shard_gather(pcs_ctx* ctx, int64_t first, int64_t count, float* out, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && out && count >= 0, "bad arguments");
+  if (count == 0) return PCS_OK;
+  TrackState& T = ctx->tr;
+  // step1 of frame k wrote its propagated states into buf[(k+1) & 1]
+  const float* cur = ((T.k + 1) & 1) ? T.P.buf1 : T.P.buf0;
+  k_shard_gather<<<grid_for(count, 256, ctx->sms), 256, 0, S(stream)>>>(cur, T.P.ld,
+                                                                       T.P.anc_out + first, count,
+                                                                       out);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+// no resampling this frame: keep the propagated states, identity ancestors
+int pcs_shard_advance(pcs_ctx* ctx, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active, "bad arguments");
+  TrackState& T = ctx->tr;
+  T.k += 1;
+  k_iota<<<grid_for(T.P.n, 256, ctx->sms), 256, 0, S(stream)>>>(T.P.anc, T.P.n);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+// install the received states (SoA, ld = n_local) as the input of the next
+// frame with identity ancestors
+int pcs_shard_set_states(pcs_ctx* ctx, const float* states, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && states, "bad arguments");
+  cudaStream_t st = S(stream);
+  TrackState& T = ctx->tr;
+  TrackParams& P = T.P;
+  T.k += 1;   // the bins kernel advanced the device frame counter
+  float* dst = (T.k & 1) ? P.buf1 : P.buf0;
+  for (int c = 0; c < 5; ++c)
+    PCS_CUDA_TRY(cudaMemcpyAsync(dst + c * P.ld, states + c * P.n, P.n * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, st));
+  k_iota<<<grid_for(P.n, 256, ctx->sms), 256, 0, st>>>(P.anc, P.n);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
 
 int pcs_track_debug(pcs_ctx* ctx, int64_t* out16, void* stream) {
   PCS_CHECK_ARG(ctx && ctx->tr.active && out16, "bad arguments");

@@ -241,7 +241,8 @@ __host__ __device__ __forceinline__ double u01_double(u32 a, u32 b) {
 __device__ __forceinline__ void box_muller(u32 a, u32 b, float& z0, float& z1) {
   float u1 = u01_open(a);
   float u2 = u01_closed_open(b);
-  float r = sqrtf(-2.0f * __logf(u1));
+  float l2 = -2.0f * __logf(u1);   // >= 0 since u1 < 1 (the SFU log may round to 0 near 1)
+  float r = (l2 > 0.0f) ? l2 * rsqrtf(l2) : 0.0f;   // MUFU.RSQ, not the IEEE sqrt sequence
   float s, c;
   __sincosf(6.28318530717958647692f * (u2 - 0.5f), &s, &c);
   z0 = r * c;

@@ -78,6 +78,7 @@ struct TrackCtl {
   double center[2];          // previous estimate (shared-memory sub-window centre)
   long long dbg[16];         // phase timestamps (globaltimer ns) of the bins kernel
   unsigned long long tile_ctr;  // decoupled look-back: monotone tile ticket counter
+  u64 rank_prefix[2];        // sharded: exact cumulative weight of the preceding ranks
 };
 
 struct TrackParams {
@@ -105,6 +106,13 @@ struct TrackParams {
   u128* tile_agg;            // [ntiles]
   u128* tile_inc;            // [ntiles]
   TrackCtl* ctl;
+  // ---- particle sharding (config 5); single GPU: 0, n, 0, n, anc
+  i64 idx_off;               // global index of local particle 0 (Philox counter)
+  i64 n_global;              // particles over all ranks
+  i64 slot_lo;               // first global output slot emitted by this rank
+  i64 slot_cap;              // capacity of anc_out
+  int* anc_out;              // ancestors (local particle index) for slots slot_lo + k
+  int scan_mode;             // 0 scan+emit, 1 scan only, 2 emit only (rank prefix in ctl)
 };
 
 __device__ __forceinline__ void set_flag(TrackCtl* c, u32 f) {
@@ -267,7 +275,7 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
       float s[5], z[5];
 #pragma unroll
       for (int c = 0; c < 5; ++c) s[c] = o_k[it][c];
-      philox_normals5(P.seed, P.frame0 + (u32)k, (u64)j, z);
+      philox_normals5(P.seed, P.frame0 + (u32)k, (u64)(P.idx_off + j), z);
       propagate_one(s, z, P.dyn, o_k[it]);
 #pragma unroll
       for (int c = 0; c < 5; ++c) sout[c * ld + j] = o_k[it][c];
@@ -659,6 +667,12 @@ __device__ __forceinline__ u32 ld_acquire_u32(const u32* p) {
   return v;
 }
 
+// scan_mode 0: tile ticket + decoupled look-back + emission (single GPU)
+// scan_mode 1: tile ticket + decoupled look-back only (sharded: tile_inc holds
+//              the rank-local inclusive prefixes; the last one is the rank total)
+// scan_mode 2: emission only, excl = rank_prefix + tile_inc[tile-1] (sharded)
+// Emitted slots are global (n_global points), written as local ancestor
+// indices to anc_out[j - slot_lo].
 template <int KIND>
 __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_emit(TrackParams P) {
   __shared__ float wsh[SCAN_TILE];
@@ -667,17 +681,19 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_emit(TrackParams P) {
   __shared__ unsigned long long s_ticket;
   TrackCtl* C = P.ctl;
   const i64 n = P.n, nt = P.ntiles;
-  if (threadIdx.x == 0) s_ticket = atomicAdd(&C->tile_ctr, 1ull);
+  const int mode = P.scan_mode;
+  if (threadIdx.x == 0) s_ticket = (mode == 2) ? 0ull : atomicAdd(&C->tile_ctr, 1ull);
   __syncthreads();
   const unsigned long long ticket = s_ticket;
-  const i64 tile = (i64)(ticket % (unsigned long long)nt);
+  const i64 tile = (mode == 2) ? (i64)blockIdx.x : (i64)(ticket % (unsigned long long)nt);
   const u32 tag = (u32)(ticket / (unsigned long long)nt) & 0x3FFFFFFFu;
   const int do_res = C->do_resample;
   const i64 base = tile * SCAN_TILE;
   if (!do_res) {   // identity ancestors, weights stay uniform (all equal)
+    if (mode == 1) return;
     for (int q = 0; q < SCAN_ITEMS; ++q) {
       i64 i = base + (i64)q * SCAN_BLOCK + threadIdx.x;
-      if (i < n) P.anc[i] = (int)i;
+      if (i < n) P.anc_out[P.idx_off + i - P.slot_lo] = (int)i;
     }
     return;
   }
@@ -707,71 +723,84 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_emit(TrackParams P) {
   if (l == 31) wtot[wi] = inc;
   __syncthreads();
   if (wi == 0) {
-    // tile aggregate; publish it, then warp-parallel look-back over 32
-    // predecessors at a time (closest inclusive prefix ends the walk)
-    u128 agg = 0;
-    for (int w = 0; w < SCAN_BLOCK / 32; ++w) agg += wtot[w];
-    if (l == 0) {
-      if (tile == 0) {
-        P.tile_inc[0] = agg;
-        __threadfence();
-        st_release_u32(P.tile_status + 0, (tag << 2) | 2u);
-      } else {
-        P.tile_agg[tile] = agg;
-        __threadfence();
-        st_release_u32(P.tile_status + tile, (tag << 2) | 1u);
-      }
-    }
     u128 excl = 0;
-    if (tile > 0) {
-      i64 pbase = tile - 1;
-      while (true) {
-        i64 p = pbase - l;
-        u32 s = 0;
-        if (p >= 0) {
-          do {
-            s = ld_acquire_u32(P.tile_status + p);
-          } while ((s >> 2) != tag || (s & 3u) == 0u);
-        }
-        bool incl = (p >= 0) && ((s & 3u) == 2u);
-        unsigned ball = __ballot_sync(0xffffffffu, incl);
-        int f = ball ? (__ffs(ball) - 1) : 32;
-        u128 v = 0;
-        if (p >= 0 && l <= f)
-          v = (l == f) ? *((volatile u128*)(P.tile_inc + p)) : *((volatile u128*)(P.tile_agg + p));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          u64 lo = (u64)v, hi = (u64)(v >> 64);
-          u64 olo = __shfl_xor_sync(0xffffffffu, lo, o);
-          u64 ohi = __shfl_xor_sync(0xffffffffu, hi, o);
-          v += ((u128)ohi << 64) | (u128)olo;
-        }
-        excl += v;
-        if (ball) break;
-        pbase -= 32;
-      }
+    if (mode == 2) {
+      excl = ((u128)C->rank_prefix[1] << 64) | (u128)C->rank_prefix[0];
+      if (tile > 0) excl += P.tile_inc[tile - 1];
+    } else {
+      // tile aggregate; publish it, then warp-parallel look-back over 32
+      // predecessors at a time (closest inclusive prefix ends the walk)
+      u128 agg = 0;
+      for (int w = 0; w < SCAN_BLOCK / 32; ++w) agg += wtot[w];
       if (l == 0) {
-        P.tile_inc[tile] = excl + agg;
-        __threadfence();
-        st_release_u32(P.tile_status + tile, (tag << 2) | 2u);
+        if (tile == 0) {
+          P.tile_inc[0] = agg;
+          __threadfence();
+          st_release_u32(P.tile_status + 0, (tag << 2) | 2u);
+        } else {
+          P.tile_agg[tile] = agg;
+          __threadfence();
+          st_release_u32(P.tile_status + tile, (tag << 2) | 1u);
+        }
+      }
+      if (tile > 0) {
+        i64 pbase = tile - 1;
+        while (true) {
+          i64 p = pbase - l;
+          u32 s = 0;
+          if (p >= 0) {
+            do {
+              s = ld_acquire_u32(P.tile_status + p);
+            } while ((s >> 2) != tag || (s & 3u) == 0u);
+          }
+          bool incl = (p >= 0) && ((s & 3u) == 2u);
+          unsigned ball = __ballot_sync(0xffffffffu, incl);
+          int f = ball ? (__ffs(ball) - 1) : 32;
+          u128 v = 0;
+          if (p >= 0 && l <= f)
+            v = (l == f) ? *((volatile u128*)(P.tile_inc + p)) : *((volatile u128*)(P.tile_agg + p));
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) {
+            u64 lo = (u64)v, hi = (u64)(v >> 64);
+            u64 olo = __shfl_xor_sync(0xffffffffu, lo, o);
+            u64 ohi = __shfl_xor_sync(0xffffffffu, hi, o);
+            v += ((u128)ohi << 64) | (u128)olo;
+          }
+          excl += v;
+          if (ball) break;
+          pbase -= 32;
+        }
+        if (l == 0) {
+          P.tile_inc[tile] = excl + agg;
+          __threadfence();
+          st_release_u32(P.tile_status + tile, (tag << 2) | 2u);
+        }
       }
     }
     if (l == 0) s_excl = excl;
   }
+  if (mode == 1) return;
   __syncthreads();
   u128 woff = 0;
   for (int w = 0; w < wi; ++w) woff += wtot[w];
   u128 excl = s_excl + woff + (inc - tsum);
   const i64 i0 = base + (i64)threadIdx.x * SCAN_ITEMS;
   if (i0 >= n) return;
-  i64 j = (i0 == 0) ? 0 : first_slot_at_or_above(cdf_round(excl), u, n);
+  const i64 ng = P.n_global, off = P.idx_off, lo = P.slot_lo, cap = P.slot_cap;
+  i64 j = (off + i0 == 0) ? 0 : first_slot_at_or_above(cdf_round(excl), u, ng);
+  bool oob = false;
 #pragma unroll
   for (int q = 0; q < SCAN_ITEMS; ++q) {
     i64 i = i0 + q;
     if (i >= n) break;
-    i64 jend = (i == n - 1) ? n : first_slot_at_or_above(cdf_round(excl + loc[q]), u, n);
-    for (; j < jend; ++j) P.anc[j] = (int)i;
+    i64 jend = (off + i == ng - 1) ? ng : first_slot_at_or_above(cdf_round(excl + loc[q]), u, ng);
+    for (; j < jend; ++j) {
+      i64 kk = j - lo;
+      if (kk >= 0 && kk < cap) P.anc_out[kk] = (int)i;
+      else oob = true;
+    }
   }
+  if (oob) set_flag(C, PCS_FLAG_CAPACITY);
 }
 
 constexpr size_t S1_SMEM = sizeof(S1Smem);

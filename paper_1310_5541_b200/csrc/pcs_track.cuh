@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
     float s[5], z[5], o[5];
 #pragma unroll
     for (int c = 0; c < 5; ++c) s[c] = __ldg(sin + c * ld + src);
-    philox_normals5(P.seed, P.frame0 + (u32)k, (u64)j, z);
+    philox_normals5(P.seed, P.frame0 + (u32)k, (u64)(P.idx_off + j), z);
     propagate_one(s, z, P.dyn, o);
 #pragma unroll
     for (int c = 0; c < 5; ++c) sout[c * ld + j] = o[c];
