@@ -217,6 +217,20 @@ int pcs_track_launches_per_step(pcs_ctx* ctx);
 /* export the current particle states / last ancestors of a running track */
 int pcs_track_states(pcs_ctx* ctx, float** states, int64_t* ld);
 
+/* ---- batched multi-target pcSIR (config 4, new; the reference tracks one
+ * spot per filter). n_targets independent filters of
+ * cfg->n_particles each, one CTA per target per frame. centers[t*5 + c] is
+ * target t's InitSpec centre (mode/width/sigma from cfg->init). Target t's
+ * RNG key is cfg->seed + (target_offset + t) * 0x9E3779B97F4A7C15, so it
+ * equals pcs_track with that seed. Targets of different ranks are
+ * independent (no communication). */
+int pcs_mt_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t n_targets,
+                 const double* centers, int64_t target_offset, int64_t n_frames, int64_t height,
+                 int64_t width, void* stream);
+int pcs_mt_step(pcs_ctx* ctx, const float* frame, int64_t k, void* stream);
+int pcs_mt_results(pcs_ctx* ctx, double* est, double* ess, uint8_t* resampled, int64_t* occupied,
+                   uint32_t* flags, int64_t* evals, void* stream);
+
 /* ---- particle-sharded giant filter (config 5, new; no reference code).
  * One rank's side of each phase; the host exchanges between the calls:
  * step1 -> all-reduce(bbox MIN/MAX) -> export(window limbs) ->

@@ -117,6 +117,11 @@ _SIGNATURES = [
     ("pcs_track_launches_per_step", c_int32, [c_void_p]),
     ("pcs_track_debug", c_int32, [c_void_p, c_void_p, c_void_p]),
     ("pcs_track_states", c_int32, [c_void_p, P(c_void_p), P(c_int64)]),
+    ("pcs_mt_begin", c_int32, [c_void_p, P(PcsTrackCfg), c_int64, c_void_p, c_int64, c_int64,
+                               c_int64, c_int64, c_void_p]),
+    ("pcs_mt_step", c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
+    ("pcs_mt_results", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
+                                 c_void_p, c_void_p]),
     ("pcs_shard_begin", c_int32, [c_void_p, P(PcsTrackCfg), c_int64, c_int64, c_int64, c_int64,
                                   c_int64, c_void_p]),
     ("pcs_shard_step1", c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,

@@ -17,6 +17,7 @@
 #include "pcs_common.cuh"
 #include "pcs_lik.cuh"
 #include "pcs_state.cuh"
+#include "pcs_multi.cuh"
 #include "pcs_shard.cuh"
 #include "pcs_track.cuh"
 #include "pcs_weights.cuh"
@@ -67,12 +68,20 @@ struct TrackState {
   int launches = 0;
 };
 
+struct MtState {
+  bool active = false;
+  MtParams P{};
+  int maxs = 0;
+  i64 k = 0;
+};
+
 struct pcs_ctx {
   int device = 0;
   int sms = 148;
   std::vector<Buf> bufs;  // indexed scratch slots
   cudaStream_t cap = nullptr;
   TrackState tr;
+  MtState mt;
   bool table_dirty = false;
   i64 table_cells = 0;
   u32* tab_cnt = nullptr;
@@ -103,6 +112,13 @@ enum Slot {
   SL_TR_PRE,
   SL_SHARD_ANC,
   SL_SHARD_BOX,
+  SL_MT_BUF0,
+  SL_MT_BUF1,
+  SL_MT_ANC,
+  SL_MT_PSLOT,
+  SL_MT_TGT,
+  SL_MT_HASH,
+  SL_MT_OUT,
   SL_COUNT
 };
 
@@ -614,6 +630,11 @@ __global__ void k_iota(int* a, i64 n) {
     a[i] = (int)i;
 }
 
+__global__ void k_iota_mod(int* a, i64 n, i64 m) {
+  for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+    a[i] = (int)(i % m);
+}
+
 __global__ void k_ctl_init(TrackCtl* C, double cx, double cy) {
   memset(C, 0, sizeof(TrackCtl));
   reset_frame(C);
@@ -918,6 +939,130 @@ int pcs_track(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, const float* frames, int
 }
 
 int pcs_track_launches_per_step(pcs_ctx* ctx) { return ctx ? ctx->tr.launches : 0; }
+
+// ---------------------------------------------------------------------------
+// batched multi-target pcSIR (config 4): one CTA per target per frame
+// ---------------------------------------------------------------------------
+int pcs_mt_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t n_targets,
+                 const double* centers, int64_t target_offset, int64_t n_frames, int64_t H,
+                 int64_t W, void* stream) {
+  PCS_CHECK_ARG(ctx && cfg && centers && n_targets >= 1 && n_frames >= 1, "bad arguments");
+  PCS_CHECK_ARG(cfg->method == 1, "multi-target filter is pcSIR");
+  PCS_CHECK_ARG(cfg->n_particles >= 1 && (double)cfg->n_particles * n_targets < 2.0e9,
+                "too many particles for 32-bit ancestors");
+  int r = check_spot(&cfg->spot);
+  if (r) return r;
+  r = check_grid(&cfg->grid);
+  if (r) return r;
+  PCS_CHECK_ARG((double)cfg->grid.n_cols * cfg->grid.n_rows < 4.0e9, "grid exceeds 32-bit cells");
+  cudaStream_t st = S(stream);
+  static bool attr = false;
+  if (!attr) {
+    const void* fns[] = {(const void*)k_mt_frame<0>, (const void*)k_mt_frame<9>,
+                         (const void*)k_mt_frame<11>, (const void*)k_mt_frame<15>};
+    for (const void* f : fns) {
+      PCS_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)MT_SMEM));
+      PCS_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                        (int)cudaSharedmemCarveoutMaxShared));
+    }
+    attr = true;
+  }
+  MtState& M = ctx->mt;
+  M = MtState();
+  MtParams& P = M.P;
+  const i64 n = cfg->n_particles, T = n_targets, ld = n * T;
+  P.T = T;
+  P.n = n;
+  P.ld = ld;
+  P.H = H;
+  P.W = W;
+  P.dyn = Dyn{cfg->dyn.sigma_pos, cfg->dyn.sigma_vel, cfg->dyn.sigma_int, cfg->dyn.dt};
+  P.spot = to_spot(&cfg->spot);
+  P.grid = to_grid(&cfg->grid);
+  P.inv_lx = 1.0 / P.grid.lx;
+  P.inv_ly = 1.0 / P.grid.ly;
+  P.seed = cfg->seed;
+  P.tgt_off = target_offset;
+  P.frame0 = cfg->frame0;
+  P.placement = cfg->placement;
+  P.K = n_frames;
+  PCS_SCRATCH(SL_MT_BUF0, 5 * ld * sizeof(float), P.buf0);
+  PCS_SCRATCH(SL_MT_BUF1, 5 * ld * sizeof(float), P.buf1);
+  PCS_SCRATCH(SL_MT_ANC, ld * sizeof(int), P.anc);
+  PCS_SCRATCH(SL_MT_PSLOT, ld * sizeof(u32), P.pslot);
+  PCS_SCRATCH(SL_MT_TGT, T * sizeof(MtTarget), P.tgt);
+  PCS_SCRATCH(SL_MT_HASH, T * MT_HCAP * sizeof(MtHash), P.hash);
+  PCS_SCRATCH(SL_MT_OUT, T * n_frames * (5 * sizeof(double) + sizeof(double) + sizeof(i64) + 1) + 64,
+              P.out_est);
+  P.out_ess = P.out_est + T * n_frames * 5;
+  P.out_occ = (i64*)(P.out_ess + T * n_frames);
+  P.out_res = (unsigned char*)(P.out_occ + T * n_frames);
+  PCS_CUDA_TRY(cudaMemsetAsync(P.hash, 0, T * MT_HCAP * sizeof(MtHash), st));
+  std::vector<MtTarget> h(T);
+  for (i64 t = 0; t < T; ++t) {
+    h[t].center[0] = centers[t * 5 + 0];
+    h[t].center[1] = centers[t * 5 + 1];
+    h[t].flags = 0;
+    h[t].first_bad = INT_MAX;
+    h[t].evals = 0;
+    pcs_init_t init = cfg->init;
+    for (int c = 0; c < 5; ++c) init.center[c] = centers[t * 5 + c];
+    const u64 seed_t = cfg->seed + (u64)(target_offset + t) * MT_KEY_STEP;
+    // each target's SoA slice: component c at c*ld + t*n
+    InitSpecDev d = to_init(&init);
+    k_init<<<grid_for(n, 256, ctx->sms), 256, 0, st>>>(d, seed_t, 0, n, P.buf0 + t * n, ld);
+  }
+  k_iota_mod<<<grid_for(ld, 256, ctx->sms), 256, 0, st>>>(P.anc, ld, n);
+  PCS_CUDA_TRY(cudaMemcpyAsync(P.tgt, h.data(), T * sizeof(MtTarget), cudaMemcpyHostToDevice, st));
+  PCS_CUDA_TRY(cudaStreamSynchronize(st));   // h goes out of scope
+  PCS_LAUNCH_CHECK();
+  M.maxs = maxs_for(cfg->spot.halfwidth);
+  M.k = 0;
+  M.active = true;
+  return PCS_OK;
+}
+
+int pcs_mt_step(pcs_ctx* ctx, const float* frame, int64_t k, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->mt.active && frame, "bad arguments");
+  PCS_CHECK_ARG(k == ctx->mt.k && k < ctx->mt.P.K, "frames must be stepped in order");
+  MtState& M = ctx->mt;
+  M.P.frame = frame;
+  M.P.k = k;
+  cudaStream_t st = S(stream);
+  const unsigned grid = (unsigned)M.P.T;
+  switch (M.maxs) {
+    case 9: k_mt_frame<9><<<grid, MT_THREADS, MT_SMEM, st>>>(M.P); break;
+    case 11: k_mt_frame<11><<<grid, MT_THREADS, MT_SMEM, st>>>(M.P); break;
+    case 15: k_mt_frame<15><<<grid, MT_THREADS, MT_SMEM, st>>>(M.P); break;
+    default: k_mt_frame<0><<<grid, MT_THREADS, MT_SMEM, st>>>(M.P);
+  }
+  PCS_LAUNCH_CHECK();
+  M.k = k + 1;
+  return PCS_OK;
+}
+
+// copy the outputs: est[T][K][5], ess[T][K], resampled[T][K], occupied[T][K];
+// flags[T], evals[T], first_bad[T] (host arrays; NULL skips)
+int pcs_mt_results(pcs_ctx* ctx, double* est, double* ess, uint8_t* res, int64_t* occ,
+                   uint32_t* flags, int64_t* evals, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->mt.active, "bad arguments");
+  cudaStream_t st = S(stream);
+  const MtParams& P = ctx->mt.P;
+  const i64 TK = P.T * P.K;
+  if (est) PCS_CUDA_TRY(cudaMemcpyAsync(est, P.out_est, TK * 5 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (ess) PCS_CUDA_TRY(cudaMemcpyAsync(ess, P.out_ess, TK * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (res) PCS_CUDA_TRY(cudaMemcpyAsync(res, P.out_res, TK, cudaMemcpyDeviceToHost, st));
+  if (occ) PCS_CUDA_TRY(cudaMemcpyAsync(occ, P.out_occ, TK * sizeof(i64), cudaMemcpyDeviceToHost, st));
+  std::vector<MtTarget> h(P.T);
+  PCS_CUDA_TRY(cudaMemcpyAsync(h.data(), P.tgt, P.T * sizeof(MtTarget), cudaMemcpyDeviceToHost, st));
+  PCS_CUDA_TRY(cudaStreamSynchronize(st));
+  for (i64 t = 0; t < P.T; ++t) {
+    if (flags) flags[t] = h[t].flags;
+    if (evals) evals[t] = h[t].evals;
+  }
+  return PCS_OK;
+}
 
 // ---------------------------------------------------------------------------
 // particle-sharded giant filter (config 5): one rank's side of each phase

@@ -1,0 +1,555 @@
+// pcs_multi.cuh — batched multi-target pcSIR (config 4; new — the reference
+// tracks one spot per filter).
+//
+// One CTA owns one target for a whole frame and runs the complete pcsir_track
+// step (binning.py:175-195 + filtering.py:148-173) for that target with
+// block-level synchronisation only:
+//   A  gather + propagate + cell index + exact per-cell sums (tile counting
+//      sort into a shared-memory sub-window; rare outliers into a per-target
+//      HBM hash table with exact int128 atomics)
+//   B  occupied cells -> dummies -> likelihood (frame region staged in shared
+//      memory) -> exact normaliser -> per-cell weights, estimate, ESS, decision
+//   C  exact-prefix systematic resampling over the target's particles (tiles
+//      scanned in order inside the CTA; no inter-CTA look-back needed)
+// Target t uses the RNG key seed_t = seed + t*0x9E3779B97F4A7C15 with local
+// particle indices, so every target equals a single-target pcsir_track run
+// with seed_t bit for bit (tests/test_gpu_multi.py).
+#pragma once
+#include "pcs_common.cuh"
+#include "pcs_fused.cuh"
+#include "pcs_lik.cuh"
+#include "pcs_state.cuh"
+#include "pcs_weights.cuh"
+
+namespace pcs {
+
+constexpr int MT_THREADS = 512;
+constexpr int MT_IPT = 4;
+constexpr int MT_TILE = MT_THREADS * MT_IPT;   // 2048
+constexpr int MT_WARPS = MT_THREADS / 32;
+constexpr int MT_SUBW = 1024;                  // sub-window cells (32 x 32)
+constexpr int MT_HCAP = 2048;                  // per-target outlier hash capacity
+constexpr int MT_MAXM = 2048;                  // occupied cells per target per frame
+constexpr int MT_STAGE = 4096;                 // staged frame pixels
+constexpr u64 MT_KEY_STEP = 0x9E3779B97F4A7C15ull;
+
+struct MtTarget {
+  double center[2];
+  u32 flags;
+  int first_bad;
+  i64 evals;
+};
+
+struct MtHash {          // one outlier cell
+  u32 key;               // flat cell + 1 (0 = empty)
+  u32 cnt;
+  u64 sum[5][2];
+};
+
+struct MtParams {
+  i64 T, n, ld;          // targets on this rank, particles per target, SoA stride (= T*n)
+  i64 H, W;
+  Dyn dyn;
+  Spot spot;
+  Grid grid;
+  double inv_lx, inv_ly;
+  u64 seed;
+  i64 tgt_off;           // global index of target 0 of this rank (RNG key)
+  u32 frame0;
+  int placement;
+  float* buf0;
+  float* buf1;
+  int* anc;
+  u32* pslot;
+  MtTarget* tgt;
+  MtHash* hash;          // [T][MT_HCAP]
+  const float* frame;    // current frame
+  i64 k;                 // frame index (buffer parity, RNG frame, output row)
+  i64 K;                 // output rows per target
+  double* out_est;       // [T][K][5]
+  double* out_ess;       // [T][K]
+  unsigned char* out_res;
+  i64* out_occ;
+};
+
+struct MtSmem {
+  // phase A
+  unsigned long long acc_lo[5][MT_SUBW];
+  unsigned long long acc_hi[5][MT_SUBW];
+  u32 acc_cnt[MT_SUBW];
+  u32 tile_cnt[MT_SUBW];
+  u32 tile_start[MT_SUBW];
+  float pay[5][MT_TILE];
+  unsigned short pay_q[MT_TILE];
+  unsigned short list[MT_TILE];
+  u32 lcnt[MT_TILE];
+  u32 n_list, n_in;
+  int scan_tmp[MT_WARPS];
+  // phase B/C (reuse is not attempted: the struct fits in shared memory)
+  float w_sub[MT_SUBW];
+  int occ[MT_MAXM];      // >= 0: sub-window cell, < 0: -(hash slot) - 1
+  double ll[MT_MAXM];
+  float dpix[MT_STAGE];
+  i128 red[MT_WARPS * 6];
+  long long lmax;
+  int box[4];
+  u32 n_occ;
+  unsigned wmin, wmax;
+  double Sf;
+  u128 carry;
+  u128 wtot[MT_WARPS];
+};
+
+__device__ __forceinline__ u32 mt_hash_slot(u32 key) { return (key * 2654435761u) & (MT_HCAP - 1); }
+
+// exact int128 atomics into the target's outlier hash table
+__device__ __forceinline__ bool mt_hash_add(MtHash* H, u32 flat, const float o[5]) {
+  u32 key = flat + 1u;
+  u32 s = mt_hash_slot(key);
+  for (int probe = 0; probe < MT_HCAP; ++probe) {
+    u32 prev = atomicCAS(&H[s].key, 0u, key);
+    if (prev == 0u || prev == key) {
+      atomicAdd(&H[s].cnt, 1u);
+#pragma unroll
+      for (int c = 0; c < 5; ++c) atomic_add_i128(H[s].sum[c], f32_to_fixed(o[c], FX_STATE));
+      return true;
+    }
+    s = (s + 1u) & (MT_HCAP - 1);
+  }
+  return false;
+}
+
+template <int MAXS>
+__global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
+  extern __shared__ __align__(16) unsigned char mt_raw[];
+  MtSmem& sm = *reinterpret_cast<MtSmem*>(mt_raw);
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const i64 tg = blockIdx.x;
+  MtTarget& TG = P.tgt[tg];
+  if (TG.flags & PCS_FLAG_CAPACITY) return;   // this target needs the general path
+  const u64 seed_t = P.seed + (u64)(P.tgt_off + tg) * MT_KEY_STEP;
+  const i64 n = P.n, ld = P.ld, base_i = tg * n;
+  const i64 k = P.k;
+  const float* sin = (k & 1) ? P.buf1 : P.buf0;
+  float* sout = (k & 1) ? P.buf0 : P.buf1;
+  const Grid g = P.grid;
+  MtHash* HT = P.hash + tg * MT_HCAP;
+
+  // ---------------- phase A: propagate + exact per-cell sums -------------------
+  const i64 snx = min((i64)32, g.ncols), sny = min((i64)32, g.nrows);
+  const i64 cx = cell_axis_fast((float)TG.center[0], g.ox, g.lx, P.inv_lx, g.ncols);
+  const i64 cy = cell_axis_fast((float)TG.center[1], g.oy, g.ly, P.inv_ly, g.nrows);
+  const i64 sx0 = min(max(cx - snx / 2, (i64)0), g.ncols - snx);
+  const i64 sy0 = min(max(cy - sny / 2, (i64)0), g.nrows - sny);
+  for (int q = t; q < MT_SUBW; q += MT_THREADS) {
+    sm.acc_cnt[q] = 0;
+    sm.tile_cnt[q] = 0;
+#pragma unroll
+    for (int c = 0; c < 5; ++c) sm.acc_lo[c][q] = sm.acc_hi[c][q] = 0ull;
+  }
+  if (t == 0) {
+    sm.n_list = 0;
+    sm.n_occ = 0;
+    sm.lmax = LLONG_MIN;
+    sm.wmin = 0xFFFFFFFFu;
+    sm.wmax = 0u;
+    sm.box[0] = INT_MAX; sm.box[1] = INT_MIN; sm.box[2] = INT_MAX; sm.box[3] = INT_MIN;
+  }
+  __syncthreads();
+  bool bad = false, hash_full = false;
+  const i64 ntile = ceil_div(n, MT_TILE);
+  for (i64 tile = 0; tile < ntile; ++tile) {
+    int q_k[MT_IPT], r_k[MT_IPT], src_k[MT_IPT];
+    float o_k[MT_IPT][5];
+#pragma unroll
+    for (int it = 0; it < MT_IPT; ++it) {
+      i64 j = tile * MT_TILE + (i64)it * MT_THREADS + t;
+      src_k[it] = (j < n) ? __ldg(P.anc + base_i + j) : 0;
+    }
+#pragma unroll
+    for (int it = 0; it < MT_IPT; ++it) {
+      i64 j = tile * MT_TILE + (i64)it * MT_THREADS + t;
+#pragma unroll
+      for (int c = 0; c < 5; ++c)
+        o_k[it][c] = (j < n) ? __ldg(sin + c * ld + base_i + src_k[it]) : 0.0f;
+    }
+#pragma unroll
+    for (int it = 0; it < MT_IPT; ++it) {
+      q_k[it] = -1;
+      i64 j = tile * MT_TILE + (i64)it * MT_THREADS + t;
+      if (j >= n) continue;
+      float s[5], z[5];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) s[c] = o_k[it][c];
+      philox_normals5(seed_t, P.frame0 + (u32)k, (u64)j, z);
+      propagate_one(s, z, P.dyn, o_k[it]);
+      const float* o = o_k[it];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) sout[c * ld + base_i + j] = o[c];
+      if (!(o[0] == o[0]) || !(o[1] == o[1])) bad = true;
+      i64 ix = cell_axis_fast(o[0], g.ox, g.lx, P.inv_lx, g.ncols);
+      i64 iy = cell_axis_fast(o[1], g.oy, g.ly, P.inv_ly, g.nrows);
+      u32 flat = (u32)(iy * g.ncols + ix);
+      P.pslot[base_i + j] = flat;
+      i64 lx = ix - sx0, ly = iy - sy0;
+      bool in_sub = (lx >= 0 && lx < snx && ly >= 0 && ly < sny);
+      if (in_sub) {
+        bool okx, oky;
+        float rx = cell_ref32(g.ox, g.lx, ix, okx), ry = cell_ref32(g.oy, g.ly, iy, oky);
+        long long D;
+        in_sub = okx && oky && delta_fixed(o[0], rx, D) && delta_fixed(o[1], ry, D) &&
+                 fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f && fabsf(o[4]) < 128.0f;
+      }
+      if (in_sub) {
+        int q = (int)(ly * snx + lx);
+        int r = (int)atomicAdd(&sm.tile_cnt[q], 1u);
+        if (r == 0) sm.list[atomicAdd(&sm.n_list, 1u)] = (unsigned short)q;
+        q_k[it] = q;
+        r_k[it] = r;
+      } else if (!mt_hash_add(HT, flat, o)) {
+        hash_full = true;
+      }
+    }
+    __syncthreads();
+    const int nl = (int)sm.n_list;
+    {
+      int base = t * 4, loc[4], sum = 0;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        int idx = base + e;
+        loc[e] = (idx < nl) ? (int)sm.tile_cnt[sm.list[idx]] : 0;
+        sum += loc[e];
+      }
+      int inc = sum;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        int o = __shfl_up_sync(0xffffffffu, inc, d);
+        if (lane >= d) inc += o;
+      }
+      if (lane == 31) sm.scan_tmp[warp] = inc;
+      __syncthreads();
+      int woff = 0;
+      for (int w = 0; w < warp; ++w) woff += sm.scan_tmp[w];
+      int run = woff + inc - sum;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        int idx = base + e;
+        if (idx < nl) {
+          sm.tile_start[sm.list[idx]] = (u32)run;
+          sm.lcnt[idx] = (u32)loc[e];
+        }
+        run += loc[e];
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int it = 0; it < MT_IPT; ++it) {
+      if (q_k[it] < 0) continue;
+      int pos = (int)sm.tile_start[q_k[it]] + r_k[it];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) sm.pay[c][pos] = o_k[it][c];
+      sm.pay_q[pos] = (unsigned short)q_k[it];
+    }
+    __syncthreads();
+    for (int e = t; e < nl; e += MT_THREADS) {
+      const int cnt = (int)sm.lcnt[e];
+      if (cnt > S1_SMALL) continue;
+      const int q = sm.list[e], st = (int)sm.tile_start[q];
+      bool ok;
+      const float rx = cell_ref32(g.ox, g.lx, sx0 + q % snx, ok);
+      const float ry = cell_ref32(g.oy, g.ly, sy0 + q / snx, ok);
+      long long v[5] = {0, 0, 0, 0, 0};
+      for (int pos = st; pos < st + cnt; ++pos) {
+        v[0] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[0][pos], rx), 1099511627776.0f));
+        v[1] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[1][pos], ry), 1099511627776.0f));
+#pragma unroll
+        for (int c = 2; c < 5; ++c) v[c] += __float2ll_rn(__fmul_rn(sm.pay[c][pos], 1099511627776.0f));
+      }
+#pragma unroll
+      for (int c = 0; c < 5; ++c) smem_rmw_i128(&sm.acc_lo[c][q], &sm.acc_hi[c][q], v[c]);
+      sm.acc_cnt[q] += (u32)cnt;
+      sm.tile_cnt[q] = 0;
+    }
+    for (int e = warp; e < nl; e += MT_WARPS) {
+      const int cnt = (int)sm.lcnt[e];
+      if (cnt <= S1_SMALL) continue;
+      const int q = sm.list[e], st = (int)sm.tile_start[q];
+      bool ok;
+      const float rx = cell_ref32(g.ox, g.lx, sx0 + q % snx, ok);
+      const float ry = cell_ref32(g.oy, g.ly, sy0 + q / snx, ok);
+      long long v[5] = {0, 0, 0, 0, 0};
+      for (int pos = st + lane; pos < st + cnt; pos += 32) {
+        v[0] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[0][pos], rx), 1099511627776.0f));
+        v[1] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[1][pos], ry), 1099511627776.0f));
+#pragma unroll
+        for (int c = 2; c < 5; ++c) v[c] += __float2ll_rn(__fmul_rn(sm.pay[c][pos], 1099511627776.0f));
+      }
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
+      }
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < 5; ++c) smem_rmw_i128(&sm.acc_lo[c][q], &sm.acc_hi[c][q], v[c]);
+        sm.acc_cnt[q] += (u32)cnt;
+        sm.tile_cnt[q] = 0;
+      }
+    }
+    __syncthreads();
+    if (t == 0) sm.n_list = 0;
+    __syncthreads();
+  }
+  if (bad) atomicOr(&TG.flags, (u32)PCS_FLAG_NONFINITE);
+  if (hash_full) atomicOr(&TG.flags, (u32)PCS_FLAG_CAPACITY);
+
+  // ---------------- phase B: occupied cells, dummies, likelihood ----------------
+  for (int q = t; q < (int)(snx * sny); q += MT_THREADS) {
+    if (sm.acc_cnt[q]) {
+      u32 idx = atomicAdd(&sm.n_occ, 1u);
+      if (idx < (u32)MT_MAXM) sm.occ[idx] = q;
+    }
+  }
+  for (int s = t; s < MT_HCAP; s += MT_THREADS) {
+    if (HT[s].key) {
+      u32 idx = atomicAdd(&sm.n_occ, 1u);
+      if (idx < (u32)MT_MAXM) sm.occ[idx] = -s - 1;
+    }
+  }
+  __syncthreads();
+  const int M = (int)min(sm.n_occ, (u32)MT_MAXM);
+  if (sm.n_occ > (u32)MT_MAXM) {
+    if (t == 0) atomicOr(&TG.flags, (u32)PCS_FLAG_CAPACITY);
+    return;
+  }
+  // dummies -> stored temporarily in pay[0..2][b] (phase A payload is free)
+  int bx0 = INT_MAX, bx1 = INT_MIN, by0 = INT_MAX, by1 = INT_MIN;
+  for (int b = t; b < M; b += MT_THREADS) {
+    int o = sm.occ[b];
+    u32 cnt;
+    i128 S[5];
+    i64 ix, iy;
+    if (o >= 0) {
+      cnt = sm.acc_cnt[o];
+      ix = sx0 + o % snx;
+      iy = sy0 + o / snx;
+      bool ok;
+      float ref[2] = {cell_ref32(g.ox, g.lx, ix, ok), cell_ref32(g.oy, g.ly, iy, ok)};
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        S[c] = (i128)(((u128)sm.acc_hi[c][o] << 64) | (u128)sm.acc_lo[c][o]);
+        if (c < 2) S[c] += (i128)cnt * f32_to_fixed(ref[c], FX_STATE);
+      }
+    } else {
+      const MtHash& h = HT[-o - 1];
+      cnt = h.cnt;
+      ix = (i64)(h.key - 1u) % g.ncols;
+      iy = (i64)(h.key - 1u) / g.ncols;
+#pragma unroll
+      for (int c = 0; c < 5; ++c) S[c] = load_i128(h.sum[c]);
+    }
+    float d[5];
+#pragma unroll
+    for (int c = 0; c < 5; ++c)
+      d[c] = __double2float_rn(scalbn(__ddiv_rn(i128_to_f64_rn(S[c]), (double)cnt), -FX_STATE));
+    if (P.placement == 1) {
+      d[0] = __double2float_rn(__dadd_rn(g.ox, __dmul_rn((double)ix + 0.5, g.lx)));
+      d[1] = __double2float_rn(__dadd_rn(g.oy, __dmul_rn((double)iy + 0.5, g.ly)));
+    }
+    sm.pay[0][b] = d[0];
+    sm.pay[1][b] = d[1];
+    sm.pay[2][b] = d[4];
+    if (d[0] == d[0] && d[1] == d[1]) {
+      int xlo, xhi, ylo, yhi;
+      window_of(d[0], d[1], P.spot, P.H, P.W, xlo, xhi, ylo, yhi);
+      bx0 = min(bx0, xlo); bx1 = max(bx1, xhi); by0 = min(by0, ylo); by1 = max(by1, yhi);
+    }
+  }
+  atomicMin(&sm.box[0], bx0); atomicMax(&sm.box[1], bx1);
+  atomicMin(&sm.box[2], by0); atomicMax(&sm.box[3], by1);
+  __syncthreads();
+  PixView pv = frame_view(P.frame, P.H, P.W);
+  {
+    int x0 = sm.box[0], y0 = sm.box[2];
+    i64 wx = (i64)sm.box[1] - x0 + 1, wy = (i64)sm.box[3] - y0 + 1;
+    if (sm.box[1] >= sm.box[0] && wx * wy <= MT_STAGE) {
+      for (int p = t; p < (int)(wx * wy); p += MT_THREADS)
+        sm.dpix[p] = __ldg(P.frame + (i64)(y0 + p / (int)wx) * P.W + (x0 + p % (int)wx));
+      pv.base = sm.dpix;
+      pv.pitch = wx;
+      pv.x0 = x0;
+      pv.y0 = y0;
+    }
+  }
+  __syncthreads();
+  // likelihood once per occupied cell: one thread per cell, canonical order
+  long long lmax = LLONG_MIN;
+  for (int b = t; b < M; b += MT_THREADS) {
+    double ll = loglik_dispatch<MAXS>(pv, sm.pay[0][b], sm.pay[1][b], sm.pay[2][b], P.spot);
+    sm.ll[b] = ll;
+    lmax = max(lmax, (long long)f64_to_ordered(ll));
+  }
+  atomicMax(&sm.lmax, lmax);
+  __syncthreads();
+  const double m = ordered_to_f64((i64)sm.lmax);
+  const bool bad_m = !(m == m) || m == INFINITY;
+  const bool degenerate = (m == -INFINITY);
+  i128 acc1[1] = {0};
+  for (int b = t; b < M; b += MT_THREADS) {
+    int o = sm.occ[b];
+    u32 cnt = (o >= 0) ? sm.acc_cnt[o] : HT[-o - 1].cnt;
+    acc1[0] += (i128)cnt * f64_to_fixed(exp(__dsub_rn(sm.ll[b], m)), FX_S);
+  }
+  block_sum_i128_k<MT_THREADS, 1>(acc1, sm.red);
+  if (t == 0) sm.Sf = scalbn(i128_to_f64_rn(acc1[0]), -FX_S);
+  __syncthreads();
+  const double Sf = sm.Sf;
+  i128 e[6] = {0, 0, 0, 0, 0, 0};
+  for (int b = t; b < M; b += MT_THREADS) {
+    int o = sm.occ[b];
+    float w = normalised_weight(sm.ll[b], m, Sf);
+    atomicMin(&sm.wmin, __float_as_uint(w));
+    atomicMax(&sm.wmax, __float_as_uint(w));
+    i128 wq = f32_to_fixed(w, FX_WQ);
+    u32 cnt;
+    if (o >= 0) {
+      sm.w_sub[o] = w;
+      cnt = sm.acc_cnt[o];
+      i64 ix = sx0 + o % snx, iy = sy0 + o / snx;
+      bool ok;
+      float ref[2] = {cell_ref32(g.ox, g.lx, ix, ok), cell_ref32(g.oy, g.ly, iy, ok)};
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        i128 S = (i128)(((u128)sm.acc_hi[c][o] << 64) | (u128)sm.acc_lo[c][o]);
+        if (c < 2) S += (i128)cnt * f32_to_fixed(ref[c], FX_STATE);
+        e[c] += wq * S;
+      }
+    } else {
+      MtHash& h = HT[-o - 1];
+      cnt = h.cnt;
+      // keep the weight in the (otherwise consumed) count-free slot: sum[0][1] is
+      // restored below; weights of hash cells live in a float alias of sum[4][1]
+#pragma unroll
+      for (int c = 0; c < 5; ++c) e[c] += wq * load_i128(h.sum[c]);
+      h.sum[0][0] = 0; h.sum[0][1] = 0; h.sum[1][0] = 0; h.sum[1][1] = 0;
+      h.sum[2][0] = 0; h.sum[2][1] = 0; h.sum[3][0] = 0; h.sum[3][1] = 0;
+      h.sum[4][0] = 0;
+      h.sum[4][1] = (u64)__float_as_uint(w);   // weight for phase C; cleared there
+    }
+    e[5] += (i128)cnt * f64_to_fixed((double)w * (double)w, FX_W2);
+  }
+  block_sum_i128_k<MT_THREADS, 6>(e, sm.red);
+  __shared__ int s_res;
+  if (t == 0) {
+    const i64 row = tg * P.K + k;
+    double ess = 1.0 / scalbn(i128_to_f64_rn(e[5]), -FX_W2);
+    bool flag_bad = degenerate || bad_m;
+    if (degenerate) atomicOr(&TG.flags, (u32)PCS_FLAG_DEGENERATE);
+    if (bad_m) atomicOr(&TG.flags, (u32)PCS_FLAG_NONFINITE);
+    if (flag_bad) atomicMin(&TG.first_bad, (int)k);
+    double est[5];
+    for (int c = 0; c < 5; ++c) {
+      est[c] = scalbn(i128_to_f64_rn(e[c]), -(FX_WQ + FX_STATE));
+      P.out_est[row * 5 + c] = est[c];
+    }
+    P.out_ess[row] = ess;
+    int res = (!flag_bad && ess < (double)n) ? 1 : 0;
+    if (!res && !flag_bad && sm.wmin != sm.wmax) atomicOr(&TG.flags, (u32)PCS_FLAG_CAPACITY);
+    P.out_res[row] = (unsigned char)res;
+    P.out_occ[row] = M;
+    TG.evals += M;
+    if (!flag_bad) {
+      TG.center[0] = est[0];
+      TG.center[1] = est[1];
+    }
+    s_res = res;
+    sm.carry = 0;
+  }
+  __syncthreads();
+
+  // ---------------- phase C: exact-prefix systematic resampling ----------------
+  const int do_res = s_res;
+  const double u = philox_resample_u(seed_t, P.frame0 + (u32)k);
+  float* wsh = &sm.pay[0][0];   // MT_TILE... reuse 5*MT_TILE floats as SCAN_TILE
+  constexpr int CI = 8;          // items per thread
+  constexpr int CT = MT_THREADS * CI;   // 4096 particles per scan tile
+  for (i64 base = 0; base < n; base += CT) {
+    if (!do_res) {
+      for (int q = 0; q < CI; ++q) {
+        i64 i = base + (i64)q * MT_THREADS + t;
+        if (i < n) P.anc[base_i + i] = (int)i;
+      }
+      continue;
+    }
+    for (int q = 0; q < CI; ++q) {
+      i64 i = base + (i64)q * MT_THREADS + t;
+      float w = 0.0f;
+      if (i < n) {
+        u32 flat = P.pslot[base_i + i];
+        i64 ix = (i64)flat % g.ncols, iy = (i64)flat / g.ncols;
+        i64 lx = ix - sx0, ly = iy - sy0;
+        bool in_sub = (lx >= 0 && lx < snx && ly >= 0 && ly < sny) && sm.acc_cnt[ly * snx + lx];
+        if (in_sub) {
+          w = sm.w_sub[ly * snx + lx];
+        } else {
+          u32 key = flat + 1u, s = mt_hash_slot(key);
+          for (int probe = 0; probe < MT_HCAP; ++probe) {
+            if (HT[s].key == key) {
+              w = __uint_as_float((u32)HT[s].sum[4][1]);
+              break;
+            }
+            s = (s + 1u) & (MT_HCAP - 1);
+          }
+        }
+      }
+      wsh[q * MT_THREADS + t] = w;
+    }
+    __syncthreads();
+    u128 loc[CI];
+    u128 tsum = 0;
+#pragma unroll
+    for (int q = 0; q < CI; ++q) {
+      tsum += cdf_fixed(wsh[t * CI + q]);
+      loc[q] = tsum;
+    }
+    u128 inc = tsum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      u128 o = shfl_up_u128(inc, d);
+      if (lane >= d) inc += o;
+    }
+    if (lane == 31) sm.wtot[warp] = inc;
+    __syncthreads();
+    u128 woff = 0, ttot = 0;
+    for (int w = 0; w < MT_WARPS; ++w) {
+      if (w < warp) woff += sm.wtot[w];
+      ttot += sm.wtot[w];
+    }
+    u128 excl = sm.carry + woff + (inc - tsum);
+    const i64 i0 = base + (i64)t * CI;
+    if (i0 < n) {
+      i64 j = (i0 == 0) ? 0 : first_slot_at_or_above(cdf_round(excl), u, n);
+      for (int q = 0; q < CI; ++q) {
+        i64 i = i0 + q;
+        if (i >= n) break;
+        i64 jend = (i == n - 1) ? n : first_slot_at_or_above(cdf_round(excl + loc[q]), u, n);
+        for (; j < jend; ++j) P.anc[base_i + j] = (int)i;
+      }
+    }
+    __syncthreads();
+    if (t == 0) sm.carry += ttot;
+    __syncthreads();
+  }
+  // clear the consumed outlier cells for the next frame
+  for (int s = t; s < MT_HCAP; s += MT_THREADS) {
+    if (HT[s].key) {
+      HT[s].key = 0u;
+      HT[s].cnt = 0u;
+      HT[s].sum[4][1] = 0ull;
+    }
+  }
+}
+
+constexpr size_t MT_SMEM = sizeof(MtSmem);
+
+}  // namespace pcs

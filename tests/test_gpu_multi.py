@@ -1,0 +1,50 @@
+"""Batched multi-target pcSIR (config 4): every target of one batched launch
+equals a single-target fused pcsir_track with that target's RNG key, bit for
+bit (estimates, ESS, resampling decisions, likelihood evaluations)."""
+
+import numpy as np
+import pytest
+
+import paper_1310_5541_b200 as pc
+from paper_1310_5541_b200 import multitarget as mt
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg(n, cpp=1):
+    return pc.PcFilterConfig(
+        n, pc.InitSpec(pc.StateVector(0, 0, 0, 0, 20.0), "gauss", sigma=2.0),
+        pc.DynamicsParams(0.5, 0.1, 1.0), pc.ResampleConfig(1.0, "systematic"),
+        pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(10.0, 5)),
+        grid=pc.BinGrid.pixel_aligned(160, 160, cpp))
+
+
+@pytest.mark.parametrize("cpp,n", [(1, 3000), (2, 5000)])
+def test_each_target_equals_single_target_filter(cuda, cpp, n):
+    frames, truth = mt.multi_target_scene(12, 6, 160, seed=3)
+    centers = truth[:, 0].copy()
+    seed = 99
+    r = mt.multi_pcsir_track(frames, _cfg(n, cpp), centers, seed)
+    for t in range(12):
+        cfg_t = pc.PcFilterConfig(
+            n, pc.InitSpec(pc.StateVector(*centers[t]), "gauss", sigma=2.0),
+            pc.DynamicsParams(0.5, 0.1, 1.0), pc.ResampleConfig(1.0, "systematic"),
+            pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(10.0, 5)),
+            grid=pc.BinGrid.pixel_aligned(160, 160, cpp))
+        single = pc.pcsir_track([pc.ImageFrame(f) for f in frames], cfg_t,
+                                pc.PhiloxRng(mt.target_seed(seed, t)))
+        assert single.path == "fused"
+        assert np.array_equal(r.estimates[t], single.estimates), t
+        assert np.array_equal(r.ess[t], single.ess), t
+        assert np.array_equal(r.resampled[t], single.resampled), t
+        assert int(r.likelihood_evals[t]) == single.likelihood_evals
+    err = np.sqrt(np.mean(np.sum((r.estimates[:, :, :2] - truth[:, 1:, :2]) ** 2, axis=2)))
+    assert err < 1.0
+
+
+def test_target_offset_selects_keys(cuda):
+    frames, truth = mt.multi_target_scene(6, 3, 160, seed=4)
+    centers = truth[:, 0].copy()
+    full = mt.multi_pcsir_track(frames, _cfg(2000), centers, 5)
+    half = mt.multi_pcsir_track(frames, _cfg(2000), centers[3:], 5, target_offset=3)
+    assert np.array_equal(full.estimates[3:], half.estimates)
