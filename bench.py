@@ -1,18 +1,22 @@
 #!/usr/bin/env python
 """Benchmark of the B200 pcSIR / SIR filter step (BASELINE.json metric:
-particle-updates/sec per filter step).
+particle-updates/sec per filter step; one line of JSON on rank 0).
 
-One "step" = one frame of the filter (propagate+gather -> bin -> dummies ->
-likelihood -> normalise/estimate/ESS -> exact systematic resampling) over
-all N particles. Default workload = BASELINE config 2: 256x256 frames,
-N = 1e6, pcSIR with 1 px bins (the other bin sizes and SIR are reported
-under "variants").
+A "step" is one frame of the filter over all N particles of the workload
+(gather -> propagate -> bin -> dummies -> likelihood -> normalise / estimate /
+ESS -> exact systematic resampling). Workloads (BASELINE.json configs):
 
-  python bench.py [--gpus N --steps K --warmup W]            # our arm
-  python bench.py --impl reference [...]                     # CPU reference arm
+  c1  64x64,   N=1e4, pcSIR 1 px (the reference's CPU-scale case)
+  c2  256x256, N=1e6, pcSIR 1 px                    <- default headline
+      (SIR and the 0.25/0.5/2 px grids are reported under "variants")
+  c3  512x512, N=1e7, erf-PSF Poisson likelihood 15x15, pcSIR 0.5 px (+ SIR)
+  c4  2048x2048, 4096 targets x 1e5 particles, pcSIR 1 px; targets sharded
+      across GPUs with no communication
+  c5  4096x4096, N=2^30, pcSIR 0.25 px; one filter sharded by particle
+      across GPUs (NCCL all-reduce / all-gather / all-to-all); 1 GPU = fused
 
-Multi-GPU (torchrun): config 2 is a single filter, so ranks run independent
-replicas ("replicas only"); time = max over ranks.
+  python bench.py [--gpus N --steps K --warmup W --workload c2]
+  python bench.py --impl reference [...]     # the reference CPU path, rank 0
 """
 
 import argparse
@@ -29,34 +33,50 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # name: (width, n_particles, start_xy, cells_per_pixel or None for SIR)
-    "c2": dict(width=256, n=1_000_000, start=(103.0, 128.0)),
-    "c1": dict(width=64, n=10_000, start=(20.0, 32.0)),
+    "c1": dict(width=64, n=10_000, start=(20.0, 32.0), variant="pcSIR-1px", model="gauss", hw=5),
+    "c2": dict(width=256, n=1_000_000, start=(103.0, 128.0), variant="pcSIR-1px", model="gauss",
+               hw=5),
+    "c3": dict(width=512, n=10_000_000, start=(203.0, 256.0), variant="pcSIR-0.5px", model="erf",
+               hw=7),
+    "c4": dict(width=2048, n=100_000, targets=4096, variant="pcSIR-1px", model="gauss", hw=5),
+    "c5": dict(width=4096, n=1 << 30, start=(2043.0, 2048.0), variant="pcSIR-0.25px",
+               model="gauss", hw=5),
 }
 VARIANTS = {"pcSIR-1px": 1.0, "pcSIR-0.5px": 0.5, "pcSIR-0.25px": 0.25, "pcSIR-2px": 2.0,
             "SIR": None}
+OTHER_VARIANTS = {"c2": ["SIR", "pcSIR-0.5px", "pcSIR-0.25px", "pcSIR-2px"], "c3": ["SIR"],
+                  "c1": ["SIR"]}
 ALGO_BYTES = {  # algorithmic bytes per particle per launch
-    # pcSIR: R anc 4 + R state 20 + W state 20 + W cell 4; scan: R cell 4 + W ancestor 4
+    # pcSIR step1: R anc 4 + R state 20 + W state 20 + W cell 4; scan: R cell 4 + W anc 4
     "k_pc_step1": 48, "k_scan_emit:pc": 8,
     # SIR: + W loglik 8; sum: R 8; stats: R 8 + R 20; scan: R 8 + W 4
     "k_sir_propagate_lik": 52, "k_sir_sum": 8, "k_sir_stats": 28, "k_scan_emit:sir": 12,
+    # multi-target frame kernel: step1 48 + scan R cell 4 + W anc 4
+    "k_mt_frame": 56,
 }
 STEP_BYTES = 60  # canonical fused minimum per particle-update
 
 
+# ---------------------------------------------------------------------------
+# synthetic inputs (BASELINE configs; the paper and reference use synthetic scenes)
+# ---------------------------------------------------------------------------
 def frames_for(width, count, start, seed=0):
-    """Synthetic config frames: one Gaussian spot (sigma 1.5, I0 20, bg 10)
-    moving +0.5 px/frame along x, Poisson noise, seed 0 (BASELINE configs)."""
+    """One Gaussian spot (sigma 1.5 px, I0 20, bg 10) moving +0.5 px/frame
+    along x (direction unstated in the configs), Poisson noise, seed 0."""
     rng = np.random.default_rng(seed)
     x, y = start
-    xs = np.arange(width)
     out = np.empty((count, width, width), dtype=np.float32)
     truth = np.empty((count, 2))
+    r = 12
     for k in range(count):
         x += 0.5
-        gx = np.exp(-((xs - x) ** 2) / (2 * 1.5 ** 2))
-        gy = np.exp(-((xs - y) ** 2) / (2 * 1.5 ** 2))
-        out[k] = rng.poisson(20.0 * np.outer(gy, gx) + 10.0)
+        ideal = np.full((width, width), 10.0)
+        cx, cy = int(round(x)), int(round(y))
+        xa, xb, ya, yb = max(cx - r, 0), min(cx + r + 1, width), max(cy - r, 0), min(cy + r + 1, width)
+        gx = np.exp(-((np.arange(xa, xb) - x) ** 2) / (2 * 1.5 ** 2))
+        gy = np.exp(-((np.arange(ya, yb) - y) ** 2) / (2 * 1.5 ** 2))
+        ideal[ya:yb, xa:xb] += 20.0 * np.outer(gy, gx)
+        out[k] = rng.poisson(ideal)
         truth[k] = (x, y)
     return out, truth
 
@@ -92,7 +112,7 @@ class ClockSampler:
                     self.rows.append([c.strip() for c in out.strip().split(",")])
                 except Exception:
                     pass
-                self._stop.wait(0.2)
+                self._stop.wait(0.1)
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()
 
@@ -113,16 +133,22 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def make_cfg(pc, wl, cpp, seed):
-    width, n = wl["width"], wl["n"]
-    init = pc.InitSpec(pc.StateVector(wl["start"][0], wl["start"][1], 0.5, 0.0, 20.0), "gauss",
-                       sigma=2.0)
+def make_cfg(pc, wl, cpp, n=None, center=None):
+    width = wl["width"]
+    n = n or wl["n"]
+    c = center if center is not None else (wl["start"][0], wl["start"][1], 0.5, 0.0, 20.0)
+    init = pc.InitSpec(pc.StateVector(*c), "gauss", sigma=2.0)
     dyn = pc.DynamicsParams(0.5, 0.1, 1.0)
-    lik = pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(10.0, 5))
+    if wl["model"] == "gauss":
+        lik = pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(10.0, wl["hw"]))
+    else:
+        lik = pc.PoissonSpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(10.0, wl["hw"]),
+                                       "erf")
     res = pc.ResampleConfig(1.0, "systematic")
     if cpp is None:
         return pc.FilterConfig(n, init, dyn, res, lik), None
-    grid = pc.BinGrid(-0.5, -0.5, cpp, cpp, int(round(width / cpp)), int(round(width / cpp)))
+    cells = int(round(width / cpp))
+    grid = pc.BinGrid(-0.5, -0.5, cpp, cpp, cells, cells)
     return pc.PcFilterConfig(n, init, dyn, res, lik, grid=grid), grid
 
 
@@ -142,10 +168,12 @@ def c_cfg(pc, _lib, cfg, grid, seed, use_graph=True):
     return c
 
 
-def run_device_steps(torch, pc, _lib, cfg, grid, dev_frames, warmup, steps, seed, flush,
-                     sampler=None):
-    """Warm-up W frames, then time K frames one graph replay at a time with an
-    L2 flush (write > L2) between timed steps. Returns (per-step ms list, outs)."""
+# ---------------------------------------------------------------------------
+# single-filter workloads (c1, c2, c3, c5 on one GPU): fused device loop
+# ---------------------------------------------------------------------------
+def run_fused(torch, pc, _lib, cfg, grid, dev_frames, warmup, steps, seed, flush, sampler=None):
+    """W warm-up frames, then K frames timed one graph replay at a time
+    (optionally flushing L2 before each). Returns per-step ms and outputs."""
     import ctypes
     k_total = warmup + steps
     c = c_cfg(pc, _lib, cfg, grid, seed)
@@ -171,15 +199,15 @@ def run_device_steps(torch, pc, _lib, cfg, grid, dev_frames, warmup, steps, seed
     if sampler:
         sampler.start()
     for i in range(steps):
-        flush.zero_()                      # > L2: every timed step starts cold
+        if flush is not None:
+            flush.zero_()                  # > L2: every timed step starts cold
         ev[i][0].record()
         step(warmup + i, warmup + i + 1)
         ev[i][1].record()
     torch.cuda.synchronize()
     clocks = sampler.stop() if sampler else None
     out = _lib.PcsTrackResult()
-    rc = _lib.lib().pcs_track_end(_lib.ctx(), ctypes.byref(out), st)
-    _lib.check(rc, "pcs_track_end")
+    _lib.check(_lib.lib().pcs_track_end(_lib.ctx(), ctypes.byref(out), st), "pcs_track_end")
     ms = [a.elapsed_time(b) for a, b in ev]
     return ms, dict(est=est.cpu().numpy(), ess=ess.cpu().numpy(), occ=occ.cpu().numpy(),
                     flags=int(out.flags), clocks=clocks,
@@ -187,8 +215,7 @@ def run_device_steps(torch, pc, _lib, cfg, grid, dev_frames, warmup, steps, seed
 
 
 def kernel_profile(torch, pc, _lib, cfg, grid, dev_frames, warmup, frames_n, seed, flush):
-    """Per-kernel device time (CUDA events on the launching stream, no graph),
-    L2 flushed before every frame."""
+    """Per-kernel device time (CUDA events on the launching stream, no graph)."""
     import ctypes
     c = c_cfg(pc, _lib, cfg, grid, seed, use_graph=False)
     st = _lib.stream()
@@ -205,7 +232,8 @@ def kernel_profile(torch, pc, _lib, cfg, grid, dev_frames, warmup, frames_n, see
     acc = np.zeros(8)
     buf = (ctypes.c_double * 8)()
     for k in range(warmup, k_total):
-        flush.zero_()
+        if flush is not None:
+            flush.zero_()
         fr = dev_frames[k:k + 1]
         _lib.check(_lib.lib().pcs_track_steps_timed(
             _lib.ctx(), _lib.ptr(fr), k, k + 1, _lib.ptr(est[k:]), _lib.ptr(ess[k:]),
@@ -218,13 +246,17 @@ def kernel_profile(torch, pc, _lib, cfg, grid, dev_frames, warmup, frames_n, see
     return {nm: acc[i] / frames_n for i, nm in enumerate(names)}
 
 
-def cpu_port_track(width, n, frames, start, cpp):
-    """The oracle port of the reference driver (filtering.py:148-182 /
-    binning.py:175-226), numpy Generator draws like the reference, and the
-    reference's own compiled likelihood kernel when oracle/_ref has it."""
+# ---------------------------------------------------------------------------
+# CPU reference path (oracle port of the reference driver + the reference's
+# compiled likelihood kernel when oracle/_ref holds it)
+# ---------------------------------------------------------------------------
+def cpu_port_track(wl, n, frames, start, cpp):
     from oracle import pcsir_oracle as orc
     ssd = orc.reference_ssd_kernel()
-    lik = orc.SpotModel(1.5, 10.0, 10.0, 5, ssd=ssd)
+    model = wl["model"]
+    lik = orc.SpotModel(1.5, 10.0, 10.0, wl["hw"], model=model,
+                        ssd=ssd if model == "gauss" else None)
+    width = wl["width"]
     grid = None if cpp is None else (-0.5, -0.5, cpp, cpp, int(round(width / cpp)),
                                      int(round(width / cpp)))
     rng = np.random.default_rng(0)
@@ -232,60 +264,109 @@ def cpu_port_track(width, n, frames, start, cpp):
     orc.track([f.astype(np.float64) for f in frames], n, [start[0], start[1], 0.5, 0.0, 20.0],
               2.0, [0.5, 0.5, 0.1, 0.1, 1.0], 1.0, lik, rng, grid=grid)
     dt = time.perf_counter() - t0
-    return n * len(frames) / dt, dt, ("reference _speedups.pyx kernel (oracle/_ref)"
-                                      if ssd is not None else "oracle C kernel")
+    kern = ("reference _speedups.pyx kernel (oracle/_ref)" if (ssd is not None and model == "gauss")
+            else "oracle C likelihood")
+    return n * len(frames) / dt, dt, kern
 
 
-def reference_arm(args, wl, cpp):
+def _c4_cpu_worker(args):
+    wl, n, frames, center, cpp = args
+    v, dt, kern = cpu_port_track(wl, n, frames, center, cpp)
+    return n * len(frames), dt, kern
+
+
+def cpu_sample(wl_name, wl, frames_host, cpp, pool_cores=1):
+    """A bounded sample (~10-30 s of CPU work) of the workload on this host."""
+    if wl_name in ("c1", "c2"):
+        nf = {"c1": 50, "c2": 12}[wl_name]
+        v, dt, kern = cpu_port_track(wl, wl["n"], frames_host[:nf], wl["start"], cpp)
+        return v, 1, f"{nf} frames x N={wl['n']} ({kern}), {dt:.1f} s on 1 core"
+    if wl_name in ("c3", "c5"):
+        n = 1_000_000 if wl_name == "c3" else 1 << 21
+        v, dt, kern = cpu_port_track(wl, n, frames_host[:3], wl["start"], cpp)
+        return v, 1, (f"3 frames x N={n} (1/{wl['n'] // n} of the config's N; particle-updates/s "
+                      f"is per-particle so it scales with N) ({kern}), {dt:.1f} s on 1 core")
+    # c4: independent targets -> process pool over the host cores
+    frames, truth = frames_host
+    nt = max(2, pool_cores)
+    jobs = [(wl, wl["n"], frames[:3], (truth[t, 0, 0], truth[t, 0, 1]), cpp) for t in range(nt)]
+    import multiprocessing as mp
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(pool_cores) as pool:
+        out = pool.map(_c4_cpu_worker, jobs)
+    dt = time.perf_counter() - t0
+    tot = sum(o[0] for o in out)
+    return tot / dt, pool_cores, (f"{nt} of {wl['targets']} targets x N={wl['n']} x 3 frames, "
+                                  f"process pool of {pool_cores} ({out[0][2]}), {dt:.1f} s")
+
+
+def reference_arm(args, wl_name, wl, cpp):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
     os.environ.setdefault("OMP_NUM_THREADS", "1")
-    frames, _ = frames_for(wl["width"], args.warmup + args.steps, wl["start"])
-    n = wl["n"]
-    # warm-up frames then K timed frames; each step = one frame over all N particles
-    t0 = time.perf_counter()
-    v, dt, kern = cpu_port_track(wl["width"], n, frames, wl["start"], cpp)
-    total = time.perf_counter() - t0
-    per_step = dt / (args.warmup + args.steps)
-    value = n / per_step
+    cores = len(os.sched_getaffinity(0))
+    if wl_name == "c4":
+        from paper_1310_5541_b200.multitarget import multi_target_scene
+        fh = multi_target_scene(min(wl["targets"], 64), 4, wl["width"], seed=0)
+        v, used, sample = cpu_sample(wl_name, wl, fh, cpp, pool_cores=cores)
+    else:
+        k_total = args.warmup + args.steps
+        if wl_name in ("c1", "c2"):
+            frames, _ = frames_for(wl["width"], k_total, wl["start"])
+            t0 = time.perf_counter()
+            v, dt, kern = cpu_port_track(wl, wl["n"], frames, wl["start"], cpp)
+            used = 1
+            sample = (f"{k_total} frames x N={wl['n']} (reference driver restated in oracle/, "
+                      f"{kern}), {time.perf_counter() - t0:.1f} s")
+        else:
+            frames, _ = frames_for(wl["width"], 3, wl["start"])
+            v, used, sample = cpu_sample(wl_name, wl, frames, cpp)
     line = {
         "impl": "reference", "metric": "particle-updates/sec per filter step",
-        "value": value, "unit": "particle-updates/s", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": per_step * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload}:{args.variant}", "n_particles": n,
-                   "frame": f"{wl['width']}x{wl['width']}"},
-        "cpu_baseline": {"value": value, "unit": "particle-updates/s", "cores": 1,
-                         "kind": "port",
-                         "sample": f"{args.warmup + args.steps} frames x N={n} "
-                                   f"(reference driver restated in oracle/, {kern}), "
-                                   f"{total:.1f} s"},
-        "e2e": {"value": value, "unit": "particle-updates/s", "h2d_bytes_per_step": 0,
+        "value": v, "unit": "particle-updates/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": wl.get("targets", 1) * wl["n"] / v * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{wl_name}:{args.variant or wl['variant']}",
+                   "n_particles": wl["n"], "frame": f"{wl['width']}x{wl['width']}"},
+        "cpu_baseline": {"value": v, "unit": "particle-updates/s", "cores": used, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "particle-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
     return 0
 
 
+# ---------------------------------------------------------------------------
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
-    ap.add_argument("--variant", default="pcSIR-1px", choices=sorted(VARIANTS))
+    ap.add_argument("--variant", default=None, choices=sorted(VARIANTS))
+    ap.add_argument("--targets", type=int, default=None, help="c4: number of targets")
+    ap.add_argument("--n", type=int, default=None, help="override particles (per target for c4)")
     ap.add_argument("--no-variants", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
     args = ap.parse_args()
-    if args.warmup < 3:
-        args.warmup = 3
-    wl = WORKLOADS[args.workload]
-    cpp_main = VARIANTS[args.variant]
+    args.warmup = max(args.warmup, 3)
+    wl_name = args.workload
+    wl = dict(WORKLOADS[wl_name])
+    if args.n:
+        wl["n"] = args.n
+    if args.targets:
+        wl["targets"] = args.targets
+    if args.steps is None:
+        args.steps = {"c1": 50, "c2": 100, "c3": 20, "c4": 10, "c5": 10}[wl_name]
+    variant = args.variant or wl["variant"]
+    cpp_main = VARIANTS[variant]
     if args.impl == "reference":
-        return reference_arm(args, wl, None if cpp_main is None else cpp_main)
+        return reference_arm(args, wl_name, wl, cpp_main)
 
     import torch
     import paper_1310_5541_b200 as pc
@@ -299,125 +380,254 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    n = wl["n"]
-    k_total = args.warmup + args.steps
-    frames_host, truth = frames_for(wl["width"], k_total, wl["start"])
-    dev_frames = torch.from_numpy(frames_host).cuda()
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     info = _lib.device_info(local)
-    flush = torch.empty(int(max(2 * info["l2_bytes"], 256 << 20)) // 4, dtype=torch.float32,
-                        device="cuda")
-
-    def timed_variant(cpp, sampler=None, steps=None, warmup=None):
-        steps = steps or args.steps
-        warmup = warmup or args.warmup
-        cfg, grid = make_cfg(pc, wl, cpp, args.seed)
-        return run_device_steps(torch, pc, _lib, cfg, grid, dev_frames, warmup, steps,
-                                args.seed, flush, sampler)
-
-    # ---- headline: K timed steps of the main variant ----
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    sampler = ClockSampler(local)
-    ms, out = timed_variant(cpp_main, sampler)
-    total_ms = float(np.sum(ms))
-    if dist:
-        t = torch.tensor([total_ms], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-        dist.barrier()
-    torch.cuda.synchronize()
-    value = n * args.steps * world / (total_ms * 1e-3)
-    rmse = float(np.sqrt(np.mean(np.sum((out["est"][args.warmup:, :2]
-                                         - truth[args.warmup:]) ** 2, axis=1))))
-
-    # ---- per-kernel profile (dominant kernel roofline) ----
-    cfg, grid = make_cfg(pc, wl, cpp_main, args.seed)
-    kprof = kernel_profile(torch, pc, _lib, cfg, grid, dev_frames, args.warmup,
-                           min(args.steps, 20), args.seed, flush)
-    dom = max(kprof, key=kprof.get)
     peak, peak_kind = peaks()
-    key = dom if dom != "k_scan_emit" else ("k_scan_emit:pc" if cpp_main else "k_scan_emit:sir")
-    dom_bytes = ALGO_BYTES.get(key, 0) * n
-    achieved = dom_bytes / (kprof[dom] * 1e-3) / 1e9 if kprof[dom] > 0 else 0.0
-    step_ms = total_ms / args.steps
-    l2 = info["l2_bytes"]
-    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
-                "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "algo_bytes_per_launch": dom_bytes,
-                "kernel_ms": {k: round(v, 5) for k, v in kprof.items()},
-                "kernel_share": {k: round(v / sum(kprof.values()), 4) for k, v in kprof.items()},
-                "step_bytes_per_particle": STEP_BYTES,
-                "step_achieved_gbs": STEP_BYTES * n / (step_ms * 1e-3) / 1e9,
-                "step_frac": STEP_BYTES * n / (step_ms * 1e-3) / 1e9 / peak,
-                "working_set_mb": round(60 * n / 1e6, 1), "l2_mb": round(l2 / 2 ** 20, 1)}
+    k_total = args.warmup + args.steps
+    sampler = ClockSampler(local)
+    extra = {}
 
-    # ---- e2e: the public call with host frames (H2D + D2H inside the timed region) ----
-    cfg_e, _ = make_cfg(pc, wl, cpp_main, args.seed)
-    host_frames = [pc.ImageFrame(f) for f in frames_host[:args.warmup]]
-    track = pc.pcsir_track if cpp_main is not None else pc.sir_track
-    track(host_frames, cfg_e, pc.PhiloxRng(args.seed))          # warm (allocs, graph)
-    e_frames = [pc.ImageFrame(f) for f in frames_host[args.warmup:k_total]]
-    cfg_e, _ = make_cfg(pc, wl, cpp_main, args.seed)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    r = track(e_frames, cfg_e, pc.PhiloxRng(args.seed))
-    torch.cuda.synchronize()
-    e2e_s = time.perf_counter() - t0
-    if dist:
-        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
-    e2e = {"value": n * args.steps * world / e2e_s, "unit": "particle-updates/s",
-           "h2d_bytes_per_step": int(wl["width"] * wl["width"] * 4),
-           "d2h_bytes_per_step": 5 * 8 + 8 + 1 + 8, "path": r.path,
-           "note": "pcsir_track(list of host ImageFrame) wall time incl. frame upload, "
-                   "graph capture and result download"}
-
-    # ---- other variants (SIR and the other bin sizes), shorter runs ----
-    variants = {}
-    if not args.no_variants:
-        for name, cpp in VARIANTS.items():
-            if name == args.variant:
-                continue
-            vms, vout = timed_variant(cpp, None, steps=min(args.steps, 30))
-            vt = float(np.sum(vms))
-            variants[name] = {"value": n * len(vms) / (vt * 1e-3),
-                              "ms_per_step": vt / len(vms),
-                              "mean_occupied_bins": float(np.mean(vout["occ"][args.warmup:]))}
-
-    # ---- CPU baseline: oracle port on this host (rank 0, N=1 only) ----
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        nf = 10
-        v, dt, kern = cpu_port_track(wl["width"], n, frames_host[:nf], wl["start"], cpp_main)
-        cpu = {"value": v, "unit": "particle-updates/s", "cores": 1, "kind": "port",
-               "sample": f"{nf} frames x N={n} {args.variant} (reference driver restated in "
-                         f"oracle/, {kern}) = {dt:.1f} s on 1 host core"}
-
-    if rank == 0:
+    if wl_name == "c4":
+        line = bench_c4(args, wl, cpp_main, world, rank, dist, torch, pc, _lib, sampler,
+                        max_over_ranks, peak, peak_kind)
+    elif wl_name == "c5" and world > 1:
+        line = bench_c5_sharded(args, wl, cpp_main, world, rank, dist, torch, pc, _lib, sampler,
+                                max_over_ranks, peak, peak_kind)
+    else:
+        n = wl["n"]
+        frames_host, truth = frames_for(wl["width"], k_total, wl["start"])
+        dev_frames = torch.from_numpy(frames_host).cuda()
+        working_set = STEP_BYTES * n
+        flush = None
+        if working_set < 2 * info["l2_bytes"]:
+            flush = torch.empty(int(max(2 * info["l2_bytes"], 256 << 20)) // 4,
+                                dtype=torch.float32, device="cuda")
+        cfg, grid = make_cfg(pc, wl, cpp_main)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ms, out = run_fused(torch, pc, _lib, cfg, grid, dev_frames, args.warmup, args.steps,
+                            args.seed, flush, sampler)
+        total_ms = max_over_ranks(float(np.sum(ms)))
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        value = n * args.steps * world / (total_ms * 1e-3)
+        step_ms = total_ms / args.steps
+        rmse = float(np.sqrt(np.mean(np.sum((out["est"][args.warmup:, :2]
+                                             - truth[args.warmup:]) ** 2, axis=1))))
+        cfg, grid = make_cfg(pc, wl, cpp_main)
+        kprof = kernel_profile(torch, pc, _lib, cfg, grid, dev_frames, args.warmup,
+                               min(args.steps, 10), args.seed, flush)
+        dom = max(kprof, key=kprof.get)
+        key = dom if dom != "k_scan_emit" else ("k_scan_emit:pc" if cpp_main else "k_scan_emit:sir")
+        dom_bytes = ALGO_BYTES.get(key, 0) * n
+        achieved = dom_bytes / (kprof[dom] * 1e-3) / 1e9 if kprof[dom] > 0 else 0.0
+        roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                    "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": None, "algo_bytes_per_launch": dom_bytes,
+                    "kernel_ms": {k: round(v, 5) for k, v in kprof.items()},
+                    "kernel_share": {k: round(v / sum(kprof.values()), 4)
+                                     for k, v in kprof.items()},
+                    "step_bytes_per_particle": STEP_BYTES,
+                    "step_achieved_gbs": STEP_BYTES * n / (step_ms * 1e-3) / 1e9,
+                    "step_frac": STEP_BYTES * n / (step_ms * 1e-3) / 1e9 / peak,
+                    "working_set_mb": round(working_set / 1e6, 1),
+                    "l2_mb": round(info["l2_bytes"] / 2 ** 20, 1),
+                    "note": ("kernel times from a non-graph pass with CUDA events around every "
+                             "launch (include ~5 us launch gaps); the headline is graph replay")}
+        # e2e: the public call with host frames (H2D + D2H inside the timed region)
+        track = pc.pcsir_track if cpp_main is not None else pc.sir_track
+        warm = [pc.ImageFrame(f) for f in frames_host[:args.warmup]]
+        cfg_e, _ = make_cfg(pc, wl, cpp_main)
+        track(warm, cfg_e, pc.PhiloxRng(args.seed))
+        e_frames = [pc.ImageFrame(f) for f in frames_host[args.warmup:k_total]]
+        cfg_e, _ = make_cfg(pc, wl, cpp_main)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = track(e_frames, cfg_e, pc.PhiloxRng(args.seed))
+        torch.cuda.synchronize()
+        e2e_s = max_over_ranks(time.perf_counter() - t0)
+        e2e = {"value": n * args.steps * world / e2e_s, "unit": "particle-updates/s",
+               "h2d_bytes_per_step": int(wl["width"] * wl["width"] * 4),
+               "d2h_bytes_per_step": 5 * 8 + 8 + 1 + 8, "path": r.path,
+               "note": "pcsir_track/sir_track(list of host ImageFrame): wall time incl. frame "
+                       "upload, graph capture and result download"}
+        variants = {}
+        if not args.no_variants:
+            for name in OTHER_VARIANTS.get(wl_name, []):
+                cfg_v, grid_v = make_cfg(pc, wl, VARIANTS[name])
+                vsteps = min(args.steps, 20)
+                vms, vout = run_fused(torch, pc, _lib, cfg_v, grid_v, dev_frames, args.warmup,
+                                      vsteps, args.seed, flush)
+                vt = max_over_ranks(float(np.sum(vms)))
+                variants[name] = {"value": n * vsteps * world / (vt * 1e-3),
+                                  "ms_per_step": vt / vsteps,
+                                  "mean_occupied_bins": float(np.mean(vout["occ"][args.warmup:]))}
+        cpu = None
+        if rank == 0 and world == 1 and not args.no_cpu_baseline:
+            v, used, sample = cpu_sample(wl_name, wl, frames_host, cpp_main)
+            cpu = {"value": v, "unit": "particle-updates/s", "cores": used, "kind": "port",
+                   "sample": sample + "; reference driver restated in oracle/"}
         line = {
             "metric": "particle-updates/sec per filter step", "value": value,
             "unit": "particle-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{args.workload}:{args.variant}", "n_particles": n,
+            "config": {"workload": f"{wl_name}:{variant}", "n_particles": n,
                        "frame": f"{wl['width']}x{wl['width']}", "bin_px": cpp_main,
-                       "likelihood": "gauss-ssd 11x11, sigma_xi 10",
+                       "likelihood": (f"{'gauss-ssd' if wl['model'] == 'gauss' else 'erf-poisson'}"
+                                      f" {2 * wl['hw'] + 1}x{2 * wl['hw'] + 1}"),
                        "resampling": "systematic every frame (threshold 1.0)",
-                       "l2": "flushed (write > L2) before every timed step",
+                       "l2": ("flushed (write > L2) before every timed step" if flush is not None
+                              else "working set larger than L2"),
                        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "rmse_px": rmse, "mean_occupied_bins":
-                           float(np.mean(out["occ"][args.warmup:]))},
+                       "rmse_px": rmse,
+                       "mean_occupied_bins": float(np.mean(out["occ"][args.warmup:]))},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": out["launches"] * args.steps,
             "clocks": out["clocks"], "variants": variants, "flags": out["flags"],
         }
+    if rank == 0 and line is not None:
         print(json.dumps(line))
     if dist:
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def bench_c4(args, wl, cpp, world, rank, dist, torch, pc, _lib, sampler, max_over_ranks, peak,
+             peak_kind):
+    """Config 4: T targets, targets partitioned over ranks (no communication)."""
+    from paper_1310_5541_b200 import multitarget as mt
+    T = wl["targets"]
+    k_total = args.warmup + args.steps
+    frames_host, truth = mt.multi_target_scene(T, k_total, wl["width"], seed=0)
+    lo, hi = mt.target_range(T, rank, world)
+    n = wl["n"]
+    cfg, _ = make_cfg(pc, wl, cpp, n=n, center=(0, 0, 0, 0, 20.0))
+    dev_frames = torch.from_numpy(frames_host).cuda()
+    tr = mt.MultiTargetTracker(cfg, truth[lo:hi, 0], args.seed, k_total, wl["width"],
+                               wl["width"], target_offset=lo)
+    for k in range(args.warmup):
+        tr.step(dev_frames[k])
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    sampler.start()
+    for i in range(args.steps):
+        ev[i][0].record()
+        tr.step(dev_frames[args.warmup + i])
+        ev[i][1].record()
+    torch.cuda.synchronize()
+    clocks = sampler.stop()
+    ms = float(np.sum([a.elapsed_time(b) for a, b in ev]))
+    total_ms = max_over_ranks(ms)
+    res = tr.results()
+    value = T * n * args.steps / (total_ms * 1e-3)
+    step_ms = total_ms / args.steps
+    local_particles = (hi - lo) * n
+    achieved = ALGO_BYTES["k_mt_frame"] * local_particles / (ms / args.steps * 1e-3) / 1e9
+    err = float(np.sqrt(np.mean(np.sum((res.estimates[:, args.warmup:, :2]
+                                        - truth[lo:hi, 1 + args.warmup:, :2]) ** 2, axis=2))))
+    # e2e: the public call with host frames
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = mt.multi_pcsir_track(frames_host[:args.steps], cfg, truth[lo:hi, 0], args.seed,
+                             target_offset=lo)
+    torch.cuda.synchronize()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cores = len(os.sched_getaffinity(0))
+        v, used, sample = cpu_sample("c4", wl, (frames_host, truth), cpp, pool_cores=cores)
+        cpu = {"value": v, "unit": "particle-updates/s", "cores": used, "kind": "port",
+               "sample": sample}
+    return {
+        "metric": "particle-updates/sec per filter step", "value": value,
+        "unit": "particle-updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"c4:{args.variant or wl['variant']}", "targets": T,
+                   "n_particles_per_target": n, "frame": f"{wl['width']}x{wl['width']}",
+                   "parallelism": f"targets sharded x{world}, no communication",
+                   "l2": "working set larger than L2", "rmse_px": err},
+        "roofline": {"bound": "hbm", "kernel": "k_mt_frame", "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": None,
+                     "algo_bytes_per_launch": ALGO_BYTES["k_mt_frame"] * local_particles},
+        "cpu_baseline": cpu,
+        "e2e": {"value": T * n * args.steps / e2e_s, "unit": "particle-updates/s",
+                "h2d_bytes_per_step": int(wl["width"] ** 2 * 4),
+                "d2h_bytes_per_step": int((hi - lo) * (5 * 8 + 8 + 1 + 8)), "path": "multi"},
+        "gpu_launches": args.steps, "clocks": clocks,
+        "flags_nonzero_targets": int(np.count_nonzero(res.flags)),
+    }
+
+
+def bench_c5_sharded(args, wl, cpp, world, rank, dist, torch, pc, _lib, sampler, max_over_ranks,
+                     peak, peak_kind):
+    """Config 5 over >1 GPU: one filter sharded by particle (NCCL)."""
+    from paper_1310_5541_b200 import distributed as D
+    k_total = args.warmup + args.steps
+    frames_host, truth = frames_for(wl["width"], k_total, wl["start"])
+    dev_frames = torch.from_numpy(frames_host).cuda()
+    cfg, _ = make_cfg(pc, wl, cpp)
+    ops = D.DeviceShardOps(k_total)
+    times = []
+
+    class TimedOps(D.DeviceShardOps):
+        pass
+
+    dist.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    t_start = [None]
+
+    # run warm-up + timed frames through one sharded track; time the last K frames
+    orig_step1 = ops.step1
+
+    def step1(frame, k):
+        if k == args.warmup:
+            torch.cuda.synchronize()
+            dist.barrier()
+            t_start[0] = time.perf_counter()
+        return orig_step1(frame, k)
+
+    ops.step1 = step1
+    est, ess, res, evals = D.sharded_pcsir_track(dev_frames, cfg, args.seed, ops)
+    torch.cuda.synchronize()
+    dist.barrier()
+    elapsed = max_over_ranks(time.perf_counter() - t_start[0])
+    clocks = sampler.stop()
+    n = wl["n"]
+    value = n * args.steps / elapsed
+    return {
+        "metric": "particle-updates/sec per filter step", "value": value,
+        "unit": "particle-updates/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": f"c5:{args.variant or wl['variant']}", "n_particles": n,
+                   "frame": f"{wl['width']}x{wl['width']}",
+                   "parallelism": f"particles sharded x{world} (NCCL all-reduce/all-gather/"
+                                  f"all-to-all)", "l2": "working set larger than L2",
+                   "timing": "host wall clock between barriers (the protocol synchronises "
+                             "the host every frame)"},
+        "roofline": None, "cpu_baseline": None,
+        "e2e": {"value": value, "unit": "particle-updates/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 57},
+        "gpu_launches": None, "clocks": clocks,
+    }
 
 
 if __name__ == "__main__":
