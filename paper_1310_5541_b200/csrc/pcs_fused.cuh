@@ -785,18 +785,55 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_emit(TrackParams P) {
   for (int w = 0; w < wi; ++w) woff += wtot[w];
   u128 excl = s_excl + woff + (inc - tsum);
   const i64 i0 = base + (i64)threadIdx.x * SCAN_ITEMS;
-  if (i0 >= n) return;
   const i64 ng = P.n_global, off = P.idx_off, lo = P.slot_lo, cap = P.slot_cap;
-  i64 j = (off + i0 == 0) ? 0 : first_slot_at_or_above(cdf_round(excl), u, ng);
-  bool oob = false;
+  const double nd = (double)ng, eps = nd * 8.881784197001252e-16;   // n * 2^-50
+  // slot boundaries of this thread's items: j0 = start of item i0, jb[q] = end of item q
+  i64 j0 = 0, jb[SCAN_ITEMS];
+  if (i0 < n) {
+    j0 = (off + i0 == 0) ? 0 : first_slot_fast(cdf_round(excl), u, ng, nd, eps);
 #pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) {
-    i64 i = i0 + q;
-    if (i >= n) break;
-    i64 jend = (off + i == ng - 1) ? ng : first_slot_at_or_above(cdf_round(excl + loc[q]), u, ng);
-    for (; j < jend; ++j) {
+    for (int q = 0; q < SCAN_ITEMS; ++q) {
+      i64 i = i0 + q;
+      jb[q] = (i >= n) ? -1
+              : ((off + i == ng - 1) ? ng : first_slot_fast(cdf_round(excl + loc[q]), u, ng, nd, eps));
+    }
+  }
+  // the tile's slot range: start of its first item .. end of its last item
+  __shared__ long long s_jrange[2];
+  if (threadIdx.x == 0) s_jrange[0] = j0;
+  if (i0 < n && (i0 + SCAN_ITEMS >= min(n, base + (i64)SCAN_TILE))) {
+    i64 last = j0;
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q)
+      if (jb[q] >= 0) last = jb[q];
+    s_jrange[1] = last;
+  }
+  __syncthreads();
+  const i64 tj0 = s_jrange[0], tj1 = s_jrange[1];
+  const bool staged = (tj1 - tj0) <= (i64)SCAN_TILE && (tj1 - tj0) >= 0;
+  int* stage = reinterpret_cast<int*>(wsh);   // the weights are no longer needed
+  bool oob = false;
+  if (i0 < n) {
+    i64 j = j0;
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q) {
+      if (jb[q] < 0) break;
+      for (; j < jb[q]; ++j) {
+        if (staged) {
+          stage[j - tj0] = (int)(i0 + q);
+        } else {
+          i64 kk = j - lo;
+          if (kk >= 0 && kk < cap) P.anc_out[kk] = (int)(i0 + q);
+          else oob = true;
+        }
+      }
+    }
+  }
+  if (staged) {
+    __syncthreads();
+    for (i64 j = tj0 + threadIdx.x; j < tj1; j += SCAN_BLOCK) {
       i64 kk = j - lo;
-      if (kk >= 0 && kk < cap) P.anc_out[kk] = (int)i;
+      if (kk >= 0 && kk < cap) P.anc_out[kk] = stage[j - tj0];
       else oob = true;
     }
   }

@@ -183,7 +183,13 @@ struct WeightSrc {
   }
 };
 
-__device__ __forceinline__ u128 cdf_fixed(float w) { return (u128)f32_to_fixed(w, FX_CDF); }
+__device__ __forceinline__ u128 cdf_fixed(float w) {
+  // fast path (w >= 2^-97, positive): round(w * 2^120) is an exact left shift
+  u32 b = __float_as_uint(w);
+  u32 ef = (b >> 23) & 0xFFu;
+  if (!(b >> 31) && ef >= 30u) return ((u128)((b & 0x7FFFFFu) | 0x800000u)) << (ef - 30u);
+  return (u128)f32_to_fixed(w, FX_CDF);
+}
 
 __device__ __forceinline__ double cdf_round(u128 P) { return scalbn(u128_to_f64_rn(P), -FX_CDF); }
 
@@ -202,6 +208,18 @@ __device__ __forceinline__ i64 first_slot_at_or_above(double c, double u, i64 n)
   while (j > 0 && sys_point(u, j - 1, nd) >= c) --j;
   while (j < n && sys_point(u, j, nd) < c) ++j;
   return j;
+}
+
+// Same result as first_slot_at_or_above without a division unless
+// T = c*n - u is within eps = n*2^-50 of an integer: the points satisfy
+// |p_j - (u+j)/n| <= 2^-52, so away from integers J = ceil(T) exactly.
+__device__ __forceinline__ i64 first_slot_fast(double c, double u, i64 n, double nd,
+                                               double eps) {
+  double t = fma(c, nd, -u);
+  double g = ceil(t);
+  double gap = g - t;
+  if (gap > eps && gap < 1.0 - eps && g > 0.0 && g < nd) return (i64)g;
+  return first_slot_at_or_above(c, u, n);
 }
 
 // pass 1: per-tile sums of W_i (striped, coalesced; integer sums are order-free)
