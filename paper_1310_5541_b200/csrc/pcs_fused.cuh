@@ -24,8 +24,8 @@
 
 namespace pcs {
 
-constexpr int S1_THREADS = 512;
-constexpr int S1_IPT = 4;
+constexpr int S1_THREADS = 1024;               // 32 warps/SM; fits 64 registers
+constexpr int S1_IPT = 2;
 constexpr int S1_TILE = S1_THREADS * S1_IPT;   // 2048 particles per tile
 constexpr int S1_WARPS = S1_THREADS / 32;
 constexpr int S1_SMALL = 16;                   // runs up to this length are owned by one lane
@@ -706,13 +706,9 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_emit(TrackParams P) {
     wsh[q * SCAN_BLOCK + threadIdx.x] = w;
   }
   __syncthreads();
-  u128 loc[SCAN_ITEMS];
   u128 tsum = 0;
 #pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) {
-    tsum += cdf_fixed(wsh[threadIdx.x * SCAN_ITEMS + q]);
-    loc[q] = tsum;
-  }
+  for (int q = 0; q < SCAN_ITEMS; ++q) tsum += cdf_fixed(wsh[threadIdx.x * SCAN_ITEMS + q]);
   const int l = threadIdx.x & 31, wi = threadIdx.x >> 5;
   u128 inc = tsum;
 #pragma unroll
@@ -781,49 +777,44 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_emit(TrackParams P) {
   }
   if (mode == 1) return;
   __syncthreads();
-  u128 woff = 0;
-  for (int w = 0; w < wi; ++w) woff += wtot[w];
-  u128 excl = s_excl + woff + (inc - tsum);
+  u128 woff = 0, tagg = 0;
+  for (int w = 0; w < SCAN_BLOCK / 32; ++w) {
+    if (w < wi) woff += wtot[w];
+    tagg += wtot[w];
+  }
+  const u128 excl = s_excl + woff + (inc - tsum);
   const i64 i0 = base + (i64)threadIdx.x * SCAN_ITEMS;
   const i64 ng = P.n_global, off = P.idx_off, lo = P.slot_lo, cap = P.slot_cap;
   const double nd = (double)ng, eps = nd * 8.881784197001252e-16;   // n * 2^-50
-  // slot boundaries of this thread's items: j0 = start of item i0, jb[q] = end of item q
-  i64 j0 = 0, jb[SCAN_ITEMS];
-  if (i0 < n) {
-    j0 = (off + i0 == 0) ? 0 : first_slot_fast(cdf_round(excl), u, ng, nd, eps);
-#pragma unroll
-    for (int q = 0; q < SCAN_ITEMS; ++q) {
-      i64 i = i0 + q;
-      jb[q] = (i >= n) ? -1
-              : ((off + i == ng - 1) ? ng : first_slot_fast(cdf_round(excl + loc[q]), u, ng, nd, eps));
-    }
-  }
   // the tile's slot range: start of its first item .. end of its last item
   __shared__ long long s_jrange[2];
-  if (threadIdx.x == 0) s_jrange[0] = j0;
-  if (i0 < n && (i0 + SCAN_ITEMS >= min(n, base + (i64)SCAN_TILE))) {
-    i64 last = j0;
-#pragma unroll
-    for (int q = 0; q < SCAN_ITEMS; ++q)
-      if (jb[q] >= 0) last = jb[q];
-    s_jrange[1] = last;
+  __shared__ int stage[SCAN_TILE];
+  if (threadIdx.x == 0) {
+    const i64 tl = min(n, base + (i64)SCAN_TILE) - 1;
+    s_jrange[0] = (off + base == 0) ? 0 : first_slot_fast(cdf_round(s_excl), u, ng, nd, eps);
+    s_jrange[1] = (off + tl == ng - 1) ? ng
+                                       : first_slot_fast(cdf_round(s_excl + tagg), u, ng, nd, eps);
   }
   __syncthreads();
   const i64 tj0 = s_jrange[0], tj1 = s_jrange[1];
   const bool staged = (tj1 - tj0) <= (i64)SCAN_TILE && (tj1 - tj0) >= 0;
-  int* stage = reinterpret_cast<int*>(wsh);   // the weights are no longer needed
   bool oob = false;
   if (i0 < n) {
-    i64 j = j0;
-#pragma unroll
+    // running inclusive prefix recomputed from the staged weights (no
+    // per-item register array)
+    i64 j = (off + i0 == 0) ? 0 : first_slot_fast(cdf_round(excl), u, ng, nd, eps);
+    u128 run = excl;
     for (int q = 0; q < SCAN_ITEMS; ++q) {
-      if (jb[q] < 0) break;
-      for (; j < jb[q]; ++j) {
+      const i64 i = i0 + q;
+      if (i >= n) break;
+      run += cdf_fixed(wsh[threadIdx.x * SCAN_ITEMS + q]);
+      const i64 jend = (off + i == ng - 1) ? ng : first_slot_fast(cdf_round(run), u, ng, nd, eps);
+      for (; j < jend; ++j) {
         if (staged) {
-          stage[j - tj0] = (int)(i0 + q);
+          stage[j - tj0] = (int)i;
         } else {
           i64 kk = j - lo;
-          if (kk >= 0 && kk < cap) P.anc_out[kk] = (int)(i0 + q);
+          if (kk >= 0 && kk < cap) P.anc_out[kk] = (int)i;
           else oob = true;
         }
       }
