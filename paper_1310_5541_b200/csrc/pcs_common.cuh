@@ -72,6 +72,20 @@ __host__ __device__ __forceinline__ double u128_to_f64_rn(u128 v) {
 #endif
 }
 
+// RN64(v) * 2^-s for v < 2^127 and a result in the normal range; same value
+// as scalbn(u128_to_f64_rn(v), -s): the top 64 bits with the discarded low
+// bits OR-ed into bit 0 (a sticky bit below the 11 rounding bits) round
+// exactly like the full 128-bit value, and the power-of-two scale is exact.
+__device__ __forceinline__ double u128_to_f64_rn_scaled(u128 v, int s) {
+  u64 hi = (u64)(v >> 64), lo = (u64)v;
+  if (hi == 0) return __dmul_rn(__ull2double_rn(lo), __longlong_as_double((i64)(1023 - s) << 52));
+  int lz = __clzll((long long)hi);
+  u64 t = lz ? ((hi << lz) | (lo >> (64 - lz))) : hi;
+  u64 rest = lz ? (lo << lz) : lo;
+  t |= (rest != 0ull) ? 1ull : 0ull;
+  return __dmul_rn(__ull2double_rn(t), __longlong_as_double((i64)(1023 + 64 - lz - s) << 52));
+}
+
 __host__ __device__ __forceinline__ double i128_to_f64_rn(i128 v) {
   if (v < 0) return -u128_to_f64_rn((u128)(-v));
   return u128_to_f64_rn((u128)v);

@@ -8,14 +8,10 @@
 //                   (filtering.py:93-100): decoupled look-back scan of the
 //                   fixed-point weights + ancestor emission.
 //
-// Per-cell accumulation without 64-bit shared-memory atomics in the hot loop:
-// each CTA counting-sorts a tile of 2048 particles by cell inside shared
-// memory (one native 32-bit shared atomic per particle gives the rank), then
-// every warp runs a segmented scan over 32 sorted particles at a time and one
-// lane per run adds the run total into the CTA's int128 sub-window
-// accumulators (a handful of uncontended atomics per run instead of one per
-// particle). Integer sums are order-free, so the result is exactly the
-// canonical sum of round(s * 2^40).
+// Per-cell accumulation without 64-bit shared-memory atomics: tile counting
+// sort + warp-segmented run sums + 32-bit digit accumulators (S1Smem).
+// Integer sums are order-free, so the result is exactly the canonical sum of
+// round(s * 2^40).
 #pragma once
 #include "pcs_common.cuh"
 #include "pcs_lik.cuh"
@@ -28,23 +24,36 @@ constexpr int S1_THREADS = 1024;               // 32 warps/SM; fits 64 registers
 constexpr int S1_IPT = 2;
 constexpr int S1_TILE = S1_THREADS * S1_IPT;   // 2048 particles per tile
 constexpr int S1_WARPS = S1_THREADS / 32;
-constexpr int S1_SMALL = 16;                   // runs up to this length are owned by one lane
+constexpr int S1_SMALL = 16;                   // (multi-target kernel) lane-owned run length
 constexpr int SUBW = 1536;                     // shared-memory sub-window cells
+constexpr int S1_PARTS = 15;                   // 5 components x 3 digits (18/18/signed)
+constexpr int S1_E = 4;                        // sorted elements per thread in the run sums
+constexpr int S1_SUM_THREADS = S1_TILE / S1_E; // 512 threads (16 warps) sum the sorted tile
+constexpr int S1_FLUSH_TILES = 256;            // digit accumulators stay in range (see below)
 constexpr i64 TABLE_MAX = 1ll << 28;           // dense full-grid table (cells)
 constexpr int MAXM = 16384;                    // occupied cells per frame (fused)
 
+// Per-tile pipeline (k_pc_step1): each CTA counting-sorts a tile of 2048
+// particles by sub-window cell in shared memory (a native 32-bit shared atomic
+// per particle gives its rank), then 16 warps walk the sorted tile, 4
+// consecutive particles per lane, and a warp-segmented scan joins runs that
+// cross lanes. One lane per (cell, warp) adds the exact run sum S (int64,
+// |S| < 2^54) to three 32-bit digit accumulators: bits 0-17, 18-35 (unsigned)
+// and S >> 36 (signed) with native 32-bit shared atomics. A cell gets <= 16
+// additions per tile, so over S1_FLUSH_TILES tiles the digits stay below 2^30
+// in magnitude; the CTA then folds them into the exact int128 HBM table.
 struct S1Smem {
-  unsigned long long acc_lo[5][SUBW];
-  unsigned long long acc_hi[5][SUBW];
-  u32 acc_cnt[SUBW];
+  u32 dig[S1_PARTS][SUBW];
+  u32 cnt[SUBW];          // particles per cell since the last flush
   u32 tile_cnt[SUBW];
   u32 tile_start[SUBW];
-  float pay[5][S1_TILE];
+  float refx[SUBW];       // cell lower edges of the sub-window (NaN: not usable)
+  float refy[SUBW];
+  float pay[5][S1_TILE];  // sorted tile: x - ref, y - ref, vx, vy, I0 (exact)
   unsigned short pay_q[S1_TILE];
-  unsigned short list[S1_TILE];
-  u32 lcnt[S1_TILE];      // count of list entry e (immutable within phase 4)
-  u32 n_list;
-  u32 n_in;
+  unsigned short list[S1_TILE];   // cells occupied in this tile
+  unsigned short flist[SUBW];     // cells touched since the last flush
+  u32 n_list, n_flist, n_in;
   int scan_tmp[S1_WARPS];
 };
 
@@ -215,6 +224,51 @@ __device__ __forceinline__ void smem_rmw_i128(unsigned long long* lo, unsigned l
 // ===========================================================================
 // pcSIR step 1
 // ===========================================================================
+// v - ref exactly representable (TwoSum error 0) and |v - ref| < 128
+__device__ __forceinline__ bool delta_exact(float v, float ref, float& s) {
+  s = __fsub_rn(v, ref);
+  float bp = __fsub_rn(s, v);
+  float ap = __fsub_rn(s, bp);
+  float err = __fadd_rn(__fsub_rn(v, ap), __fsub_rn(-ref, bp));
+  return err == 0.0f && fabsf(s) < 128.0f;
+}
+
+// add an exact run sum to the three digit accumulators of cell q
+__device__ __forceinline__ void s1_emit(S1Smem& sm, int q, const long long S[5]) {
+#pragma unroll
+  for (int c = 0; c < 5; ++c) {
+    atomicAdd(&sm.dig[3 * c][q], (u32)S[c] & 0x3FFFFu);
+    atomicAdd(&sm.dig[3 * c + 1][q], (u32)(S[c] >> 18) & 0x3FFFFu);
+    atomicAdd(&sm.dig[3 * c + 2][q], (u32)(int)(S[c] >> 36));
+  }
+}
+
+// fold the CTA's digit accumulators into the exact int128 HBM table
+__device__ __forceinline__ void s1_flush(const TrackParams& P, TrackCtl* C, S1Smem& sm, i64 sx0,
+                                         i64 sy0, int snx) {
+  const Grid& g = P.grid;
+  const int nl = (int)sm.n_flist;
+  for (int e = threadIdx.x; e < nl; e += S1_THREADS) {
+    const int q = sm.flist[e];
+    const u32 cnt = sm.cnt[q];
+    const int qx = q % snx, qy = q / snx;
+    const u32 flat = (u32)((sy0 + qy) * g.ncols + (sx0 + qx));
+    touch_cell(P, C, flat, cnt);
+#pragma unroll
+    for (int c = 0; c < 5; ++c) {
+      i128 s = (i128)sm.dig[3 * c][q] + ((i128)sm.dig[3 * c + 1][q] << 18) +
+               ((i128)(int)sm.dig[3 * c + 2][q] << 36);
+      if (c == 0) s += (i128)cnt * f32_to_fixed(sm.refx[qx], FX_STATE);
+      if (c == 1) s += (i128)cnt * f32_to_fixed(sm.refy[qy], FX_STATE);
+      atomic_add_i128(P.tab_sum + ((i64)c * P.G + flat) * 2, s);
+      sm.dig[3 * c][q] = 0;
+      sm.dig[3 * c + 1][q] = 0;
+      sm.dig[3 * c + 2][q] = 0;
+    }
+    sm.cnt[q] = 0;
+  }
+}
+
 __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
   extern __shared__ __align__(16) unsigned char s1_raw[];
   S1Smem& sm = *reinterpret_cast<S1Smem*>(s1_raw);
@@ -238,26 +292,41 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
   if (blockIdx.x == 0 && t == 0) {
     C->sx0 = sx0; C->sy0 = sy0; C->snx = snx; C->sny = sny;
   }
-  const int subn = (int)(snx * sny);
+  const int snxi = (int)snx, snyi = (int)sny;
   for (int q = t; q < SUBW; q += S1_THREADS) {
-    sm.acc_cnt[q] = 0;
+    sm.cnt[q] = 0;
     sm.tile_cnt[q] = 0;
 #pragma unroll
-    for (int c = 0; c < 5; ++c) sm.acc_lo[c][q] = sm.acc_hi[c][q] = 0ull;
+    for (int p = 0; p < S1_PARTS; ++p) sm.dig[p][q] = 0;
   }
-  if (t == 0) sm.n_list = 0;
+  // cell lower edges; NaN marks an edge whose deltas may not be exact
+  for (int q = t; q < snxi; q += S1_THREADS) {
+    bool ok;
+    float r = cell_ref32(g.ox, g.lx, sx0 + q, ok);
+    sm.refx[q] = ok ? r : __int_as_float(0x7fc00000);
+  }
+  for (int q = t; q < snyi; q += S1_THREADS) {
+    bool ok;
+    float r = cell_ref32(g.oy, g.ly, sy0 + q, ok);
+    sm.refy[q] = ok ? r : __int_as_float(0x7fc00000);
+  }
+  if (t == 0) {
+    sm.n_list = 0;
+    sm.n_flist = 0;
+  }
   __syncthreads();
 
+  const u32 frame = P.frame0 + (u32)k;
   bool bad = false;
   const i64 ntile = ceil_div(n, S1_TILE);
+  int since = 0;
   for (i64 tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
     // ---- phase 1: gather + propagate + cell; rank within the tile's cell ----
     int q_k[S1_IPT], r_k[S1_IPT];
     float o_k[S1_IPT][5];
-    // issue every gather before any arithmetic (memory-level parallelism)
     int src_k[S1_IPT];
 #pragma unroll
-    for (int it = 0; it < S1_IPT; ++it) {
+    for (int it = 0; it < S1_IPT; ++it) {   // every gather before any arithmetic
       i64 j = tile * S1_TILE + (i64)it * S1_THREADS + t;
       src_k[it] = (j < n) ? __ldg(P.anc + j) : 0;
     }
@@ -270,36 +339,33 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {
       q_k[it] = -1;
-      i64 j = tile * S1_TILE + (i64)it * S1_THREADS + t;
+      const i64 j = tile * S1_TILE + (i64)it * S1_THREADS + t;
       if (j >= n) continue;
       float s[5], z[5];
 #pragma unroll
       for (int c = 0; c < 5; ++c) s[c] = o_k[it][c];
-      philox_normals5(P.seed, P.frame0 + (u32)k, (u64)(P.idx_off + j), z);
-      propagate_one(s, z, P.dyn, o_k[it]);
+      philox_normals5(P.seed, frame, (u64)(P.idx_off + j), z);
+      float* o = o_k[it];
+      propagate_one(s, z, P.dyn, o);
 #pragma unroll
-      for (int c = 0; c < 5; ++c) sout[c * ld + j] = o_k[it][c];
-      const float* o = o_k[it];
+      for (int c = 0; c < 5; ++c) sout[c * ld + j] = o[c];
       if (!(o[0] == o[0]) || !(o[1] == o[1])) bad = true;
-      i64 ix = cell_axis_fast(o[0], g.ox, g.lx, P.inv_lx, g.ncols);
-      i64 iy = cell_axis_fast(o[1], g.oy, g.ly, P.inv_ly, g.nrows);
-      u32 flat = (u32)(iy * g.ncols + ix);
+      const i64 ix = cell_axis_fast(o[0], g.ox, g.lx, P.inv_lx, g.ncols);
+      const i64 iy = cell_axis_fast(o[1], g.oy, g.ly, P.inv_ly, g.nrows);
+      const u32 flat = (u32)(iy * g.ncols + ix);
       P.pslot[j] = flat;
-      i64 lx = ix - sx0, ly = iy - sy0;
-      bool in_sub = (lx >= 0 && lx < snx && ly >= 0 && ly < sny);
-      if (in_sub) {
-        bool okx, oky;
-        float rx = cell_ref32(g.ox, g.lx, ix, okx), ry = cell_ref32(g.oy, g.ly, iy, oky);
-        long long D;
-        in_sub = okx && oky && delta_fixed(o[0], rx, D) && delta_fixed(o[1], ry, D) &&
-                 fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f && fabsf(o[4]) < 128.0f;
-      }
-      if (in_sub) {
-        int q = (int)(ly * snx + lx);
-        int r = (int)atomicAdd(&sm.tile_cnt[q], 1u);
+      const int lx = (int)(ix - sx0), ly = (int)(iy - sy0);
+      float dx, dy;
+      if (lx >= 0 && lx < snxi && ly >= 0 && ly < snyi && delta_exact(o[0], sm.refx[lx], dx) &&
+          delta_exact(o[1], sm.refy[ly], dy) && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f &&
+          fabsf(o[4]) < 128.0f) {
+        const int q = ly * snxi + lx;
+        const int r = (int)atomicAdd(&sm.tile_cnt[q], 1u);
         if (r == 0) sm.list[atomicAdd(&sm.n_list, 1u)] = (unsigned short)q;
         q_k[it] = q;
         r_k[it] = r;
+        o[0] = dx;
+        o[1] = dy;
       } else {
         // outside the shared sub-window: exact int128 atomics straight to HBM
         touch_cell(P, C, flat, 1u);
@@ -309,17 +375,13 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
       }
     }
     __syncthreads();
-    // ---- phase 2: segment offsets (exclusive scan of counts in list order) ----
-    const int nl = (int)sm.n_list;
+    // ---- phase 2: run offsets (exclusive scan of the tile's cell counts) ----
     {
-      int base = t * 4, loc[4], sum = 0;
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        int idx = base + e;
-        loc[e] = (idx < nl) ? (int)sm.tile_cnt[sm.list[idx]] : 0;
-        sum += loc[e];
-      }
-      int inc = sum;
+      const int nl = (int)sm.n_list;
+      const int e0 = 2 * t;
+      const int c0 = (e0 < nl) ? (int)sm.tile_cnt[sm.list[e0]] : 0;
+      const int c1 = (e0 + 1 < nl) ? (int)sm.tile_cnt[sm.list[e0 + 1]] : 0;
+      int inc = c0 + c1;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         int o = __shfl_up_sync(0xffffffffu, inc, d);
@@ -327,17 +389,24 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
       }
       if (lane == 31) sm.scan_tmp[warp] = inc;
       __syncthreads();
-      int woff = 0;
-      for (int w = 0; w < warp; ++w) woff += sm.scan_tmp[w];
-      int run = woff + inc - sum;
+      if (t == 0) sm.n_list = 0;   // every thread has read n_list
+      int woff = (lane < warp) ? sm.scan_tmp[lane] : 0;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        int idx = base + e;
-        if (idx < nl) {
-          sm.tile_start[sm.list[idx]] = (u32)run;
-          sm.lcnt[idx] = (u32)loc[e];
+      for (int d = 16; d > 0; d >>= 1) woff += __shfl_xor_sync(0xffffffffu, woff, d);
+      int run = woff + inc - c0 - c1;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int e = e0 + h;
+        if (e < nl) {
+          const int q = sm.list[e];
+          const u32 c = (u32)(h ? c1 : c0);
+          sm.tile_start[q] = (u32)run;
+          sm.tile_cnt[q] = 0;
+          const u32 old = sm.cnt[q];
+          sm.cnt[q] = old + c;
+          if (old == 0) sm.flist[atomicAdd(&sm.n_flist, 1u)] = (unsigned short)q;
+          run += (int)c;
         }
-        run += loc[e];
       }
       if (t == S1_THREADS - 1) sm.n_in = (u32)run;
     }
@@ -346,82 +415,89 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {
       if (q_k[it] < 0) continue;
-      int pos = (int)sm.tile_start[q_k[it]] + r_k[it];
+      const int pos = (int)sm.tile_start[q_k[it]] + r_k[it];
 #pragma unroll
       for (int c = 0; c < 5; ++c) sm.pay[c][pos] = o_k[it][c];
       sm.pay_q[pos] = (unsigned short)q_k[it];
     }
     __syncthreads();
-    // ---- phase 4: each occupied cell of the tile has exactly one owner that
-    //      sums its sorted run and updates the int128 accumulators with a plain
-    //      read-modify-write (no atomics): runs of <= S1_SMALL particles are
-    //      owned by one lane, longer runs by a whole warp (exactness of v - ref
-    //      was verified in phase 1) ----
-    for (int e = t; e < nl; e += S1_THREADS) {
-      const int cnt = (int)sm.lcnt[e];
-      if (cnt > S1_SMALL) continue;
-      const int q = sm.list[e], st = (int)sm.tile_start[q];
-      bool ok;
-      const float rx = cell_ref32(g.ox, g.lx, sx0 + q % snx, ok);
-      const float ry = cell_ref32(g.oy, g.ly, sy0 + q / snx, ok);
-      long long v[5] = {0, 0, 0, 0, 0};
-      for (int pos = st; pos < st + cnt; ++pos) {
-        v[0] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[0][pos], rx), 1099511627776.0f));
-        v[1] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[1][pos], ry), 1099511627776.0f));
+    // ---- phase 4: exact run sums over the sorted tile (16 warps, 4
+    //      consecutive particles per lane, warp-segmented scan across lanes) ----
+    if (t < S1_SUM_THREADS) {
+      const int ni = (int)sm.n_in;
+      const int p0 = t * S1_E;
+      int kf = 0xFFFF, kl = 0xFFFF;   // key of the first / last run piece
+      long long hf[5], tl[5];
+      bool split = false;             // a run ends inside this lane
 #pragma unroll
-        for (int c = 2; c < 5; ++c) v[c] += __float2ll_rn(__fmul_rn(sm.pay[c][pos], 1099511627776.0f));
+      for (int c = 0; c < 5; ++c) hf[c] = tl[c] = 0;
+#pragma unroll
+      for (int e = 0; e < S1_E; ++e) {
+        const int p = p0 + e;
+        if (p >= ni) break;
+        const int q = sm.pay_q[p];
+        long long v[5];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) v[c] = __float2ll_rn(__fmul_rn(sm.pay[c][p], 1099511627776.0f));
+        if (e == 0) {
+          kf = kl = q;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) tl[c] = v[c];
+        } else if (q == kl) {
+#pragma unroll
+          for (int c = 0; c < 5; ++c) tl[c] += v[c];
+        } else {
+          if (!split) {
+#pragma unroll
+            for (int c = 0; c < 5; ++c) hf[c] = tl[c];
+            split = true;
+          } else {
+            s1_emit(sm, kl, tl);      // a run entirely inside this lane
+          }
+          kl = q;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) tl[c] = v[c];
+        }
       }
+      // segmented inclusive scan of the last pieces across lanes
+      const int kprev = __shfl_up_sync(0xffffffffu, kl, 1);
+      bool flag = split || lane == 0 || kprev != kl || kl == 0xFFFF;
+      long long inc[5];
 #pragma unroll
-      for (int c = 0; c < 5; ++c) smem_rmw_i128(&sm.acc_lo[c][q], &sm.acc_hi[c][q], v[c]);
-      sm.acc_cnt[q] += (u32)cnt;
-      sm.tile_cnt[q] = 0;
-    }
-    for (int e = warp; e < nl; e += S1_WARPS) {
-      const int cnt = (int)sm.lcnt[e];
-      if (cnt <= S1_SMALL) continue;
-      const int q = sm.list[e], st = (int)sm.tile_start[q];
-      bool ok;
-      const float rx = cell_ref32(g.ox, g.lx, sx0 + q % snx, ok);
-      const float ry = cell_ref32(g.oy, g.ly, sy0 + q / snx, ok);
-      long long v[5] = {0, 0, 0, 0, 0};
-      for (int pos = st + lane; pos < st + cnt; pos += 32) {
-        v[0] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[0][pos], rx), 1099511627776.0f));
-        v[1] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[1][pos], ry), 1099511627776.0f));
+      for (int c = 0; c < 5; ++c) inc[c] = tl[c];
 #pragma unroll
-        for (int c = 2; c < 5; ++c) v[c] += __float2ll_rn(__fmul_rn(sm.pay[c][pos], 1099511627776.0f));
+      for (int d = 1; d < 32; d <<= 1) {
+        const bool of = __shfl_up_sync(0xffffffffu, flag, d);
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+          const long long ov = __shfl_up_sync(0xffffffffu, inc[c], d);
+          if (lane >= d && !flag) inc[c] += ov;
+        }
+        if (lane >= d) flag = flag || of;
       }
+      // carry into the first piece (runs that started in earlier lanes)
+      long long carry[5];
 #pragma unroll
-      for (int c = 0; c < 5; ++c) {
+      for (int c = 0; c < 5; ++c) carry[c] = __shfl_up_sync(0xffffffffu, inc[c], 1);
+      const int knext = __shfl_down_sync(0xffffffffu, kf, 1);
+      if (split) {
+        const bool join = lane > 0 && kprev == kf;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
+        for (int c = 0; c < 5; ++c) hf[c] += join ? carry[c] : 0ll;
+        s1_emit(sm, kf, hf);
       }
-      if (lane == 0) {
-#pragma unroll
-        for (int c = 0; c < 5; ++c) smem_rmw_i128(&sm.acc_lo[c][q], &sm.acc_hi[c][q], v[c]);
-        sm.acc_cnt[q] += (u32)cnt;
-        sm.tile_cnt[q] = 0;
-      }
+      if (kl != 0xFFFF && (lane == 31 || knext != kl)) s1_emit(sm, kl, inc);
     }
     __syncthreads();
-    if (t == 0) sm.n_list = 0;
-    __syncthreads();
-  }
-  // ---- flush the CTA's sub-window into the HBM table (exact int128) ----
-  for (int q = t; q < subn; q += S1_THREADS) {
-    u32 cnt = sm.acc_cnt[q];
-    if (!cnt) continue;
-    i64 ix = sx0 + q % snx, iy = sy0 + q / snx;
-    u32 flat = (u32)(iy * g.ncols + ix);
-    touch_cell(P, C, flat, cnt);
-    bool ok;
-    float ref[2] = {cell_ref32(g.ox, g.lx, ix, ok), cell_ref32(g.oy, g.ly, iy, ok)};
-#pragma unroll
-    for (int c = 0; c < 5; ++c) {
-      i128 s = (i128)(((u128)sm.acc_hi[c][q] << 64) | (u128)sm.acc_lo[c][q]);
-      if (c < 2) s += (i128)cnt * f32_to_fixed(ref[c], FX_STATE);
-      atomic_add_i128(P.tab_sum + ((i64)c * P.G + flat) * 2, s);
+    if (++since == S1_FLUSH_TILES) {
+      since = 0;
+      s1_flush(P, C, sm, sx0, sy0, snxi);
+      __syncthreads();
+      if (t == 0) sm.n_flist = 0;
+      __syncthreads();
     }
   }
+  s1_flush(P, C, sm, sx0, sy0, snxi);
   if (bad) set_flag(C, PCS_FLAG_NONFINITE);
 }
 

@@ -191,7 +191,8 @@ __device__ __forceinline__ u128 cdf_fixed(float w) {
   return (u128)f32_to_fixed(w, FX_CDF);
 }
 
-__device__ __forceinline__ double cdf_round(u128 P) { return scalbn(u128_to_f64_rn(P), -FX_CDF); }
+// P <= 2^121 (sum of normalised weights), so 2^-120 * RN64(P) is normal
+__device__ __forceinline__ double cdf_round(u128 P) { return u128_to_f64_rn_scaled(P, FX_CDF); }
 
 __device__ __forceinline__ double sys_point(double u, i64 j, double nd) {
   return __ddiv_rn(__dadd_rn(u, (double)j), nd);

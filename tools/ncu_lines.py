@@ -10,7 +10,7 @@ import subprocess
 import sys
 import tempfile
 
-rep, kregex, so = sys.argv[1], sys.argv[2], sys.argv[3]
+rep, kregex, so = sys.argv[1], sys.argv[2], os.path.abspath(sys.argv[3])
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name",
                       f"regex:{kregex}", "--print-source", "sass"], capture_output=True,
                      text=True).stdout
@@ -57,5 +57,5 @@ for a, ex, s in data:
     st[l] += s
 tot = sum(agg.values())
 print(f"total warp-instr {tot:.0f}")
-for l, v in agg.most_common(40):
+for l, v in agg.most_common(int(os.environ.get("TOPN", "40"))):
     print(f"{v:12.0f} {100*v/tot:5.1f}%  stall_samples={st[l]:6.0f}  {l}")
