@@ -66,19 +66,27 @@ static void bm64(uint32_t a, uint32_t b, double* z0, double* z1) {
   *z1 = r * sin(th);
 }
 
-/* the N x 5 standard normals of one propagation (state.py:125), out[c*n+i] */
+/* float64 Box–Muller on 22-bit u1 / 20-bit u2 (the propagation normals) */
+static double bm_r22(uint32_t a) { return sqrt(-2.0 * log(((double)a + 0.5) * 2.384185791015625e-07)); }
+static double bm_t20(uint32_t b) { return 2.0 * M_PI * ((double)b * 9.5367431640625e-07 - 0.5); }
+
+/* the N x 5 standard normals of one propagation (state.py:125), out[c*n+i]:
+ * one Philox block (x, y, z, w) per particle, three Box–Muller pairs
+ * (pcs_common.cuh philox_normals5) */
 void orc_propagate_normals(uint64_t seed, uint32_t frame, int64_t off, int64_t n, double* out) {
   for (int64_t i = 0; i < n; ++i) {
     uint64_t idx = (uint64_t)(off + i);
-    uint32_t c0[4] = {(uint32_t)idx, (uint32_t)(idx >> 32), frame, (1u << 4) | 0u};
-    uint32_t c1[4] = {(uint32_t)idx, (uint32_t)(idx >> 32), frame, (1u << 4) | 1u};
-    philox(c0, (uint32_t)seed, (uint32_t)(seed >> 32));
-    philox(c1, (uint32_t)seed, (uint32_t)(seed >> 32));
-    double z[6];
-    bm64(c0[0], c0[1], &z[0], &z[1]);
-    bm64(c0[2], c0[3], &z[2], &z[3]);
-    bm64(c1[0], c1[1], &z[4], &z[5]);
-    for (int c = 0; c < 5; ++c) out[c * n + i] = z[c];
+    uint32_t c[4] = {(uint32_t)idx, (uint32_t)(idx >> 32), frame, (1u << 4) | 0u};
+    philox(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    double r0 = bm_r22(c[0] >> 10), t0 = bm_t20(c[1] >> 12);
+    double r1 = bm_r22(c[2] >> 10), t1 = bm_t20(c[3] >> 12);
+    double r2 = bm_r22(((c[0] & 0x3FFu) << 12) | (c[1] & 0xFFFu));
+    double t2 = bm_t20(((c[2] & 0x3FFu) << 10) | ((c[3] >> 2) & 0x3FFu));
+    out[0 * n + i] = r0 * cos(t0);
+    out[1 * n + i] = r0 * sin(t0);
+    out[2 * n + i] = r1 * cos(t1);
+    out[3 * n + i] = r1 * sin(t1);
+    out[4 * n + i] = r2 * cos(t2);
   }
 }
 

@@ -263,17 +263,40 @@ __device__ __forceinline__ void box_muller(u32 a, u32 b, float& z0, float& z1) {
   z1 = r * s;
 }
 
+// Box–Muller on explicit integer uniforms: u1 = (a + 1/2) 2^-22 (a < 2^22),
+// u2 = b 2^-20 (b < 2^20); same SFU evaluation as box_muller.
+__device__ __forceinline__ float bm_radius22(u32 a) {
+  float u1 = ((float)a + 0.5f) * 2.384185791015625e-07f;
+  float l2 = -2.0f * __logf(u1);
+  return (l2 > 0.0f) ? l2 * rsqrtf(l2) : 0.0f;
+}
+__device__ __forceinline__ float bm_angle20(u32 b) {
+  return 6.28318530717958647692f * ((float)b * 9.5367431640625e-07f - 0.5f);
+}
+
 // The five standard normals used to propagate particle `idx` at `frame`
 // (column order x, y, vx, vy, I0 — matches rng.normal(size=(N,5)) row
-// layout in state.py:125). Exposed through pcs_philox_normals for replay.
+// layout in state.py:125), from ONE Philox4x32-10 block r = (x, y, z, w):
+// three Box–Muller pairs on 22-bit u1 / 20-bit u2 (126 of the 128 bits):
+//   pair 0: u1 = x >> 10, u2 = y >> 12           -> z0, z1
+//   pair 1: u1 = z >> 10, u2 = w >> 12           -> z2, z3
+//   pair 2: u1 = (x & 0x3FF) << 12 | (y & 0xFFF),
+//           u2 = (z & 0x3FF) << 10 | (w >> 2 & 0x3FF) -> z4 (cosine branch)
+// Exposed through pcs_philox_normals for replay; oracle/oracle.c restates it.
 __device__ __forceinline__ void philox_normals5(u64 seed, u32 frame, u64 idx, float z[5]) {
   u32 k0 = (u32)seed, k1 = (u32)(seed >> 32);
-  u32x4 r0 = philox4x32_10({(u32)idx, (u32)(idx >> 32), frame, (TAG_PROPAGATE << 4) | 0u}, k0, k1);
-  u32x4 r1 = philox4x32_10({(u32)idx, (u32)(idx >> 32), frame, (TAG_PROPAGATE << 4) | 1u}, k0, k1);
-  float z5;
-  box_muller(r0.x, r0.y, z[0], z[1]);
-  box_muller(r0.z, r0.w, z[2], z[3]);
-  box_muller(r1.x, r1.y, z[4], z5);
+  u32x4 r = philox4x32_10({(u32)idx, (u32)(idx >> 32), frame, (TAG_PROPAGATE << 4) | 0u}, k0, k1);
+  float s, c, rad;
+  rad = bm_radius22(r.x >> 10);
+  __sincosf(bm_angle20(r.y >> 12), &s, &c);
+  z[0] = rad * c;
+  z[1] = rad * s;
+  rad = bm_radius22(r.z >> 10);
+  __sincosf(bm_angle20(r.w >> 12), &s, &c);
+  z[2] = rad * c;
+  z[3] = rad * s;
+  rad = bm_radius22(((r.x & 0x3FFu) << 12) | (r.y & 0xFFFu));
+  z[4] = rad * __cosf(bm_angle20(((r.z & 0x3FFu) << 10) | ((r.w >> 2) & 0x3FFu)));
 }
 
 // Two standard normals for the initial cloud (InitSpec "gauss", state.py:173)

@@ -43,13 +43,13 @@ constexpr int MAXM = 16384;                    // occupied cells per frame (fuse
 // additions per tile, so over S1_FLUSH_TILES tiles the digits stay below 2^30
 // in magnitude; the CTA then folds them into the exact int128 HBM table.
 struct S1Smem {
+  float pay[5][S1_TILE];   // cell-sorted tile: x - ref, y - ref, vx, vy, I0 (exact)
   u32 dig[S1_PARTS][SUBW];
   u32 cnt[SUBW];          // particles per cell since the last flush
   u32 tile_cnt[SUBW];
-  u32 tile_start[SUBW];
-  float refx[SUBW];       // cell lower edges of the sub-window (NaN: not usable)
-  float refy[SUBW];
-  float pay[5][S1_TILE];  // sorted tile: x - ref, y - ref, vx, vy, I0 (exact)
+  unsigned short tile_start[SUBW];
+  float ref[SUBW + 1];    // cell lower edges: x at [0, snx), y at [snx, snx + sny)
+                          // (NaN: deltas from this edge may not be exact)
   unsigned short pay_q[S1_TILE];
   unsigned short list[S1_TILE];   // cells occupied in this tile
   unsigned short flist[SUBW];     // cells touched since the last flush
@@ -173,6 +173,55 @@ __device__ __forceinline__ i64 cell_axis_fast(float p, double origin, double cel
   return (i64)q;
 }
 
+// Hot-loop form of cell_axis_fast with the per-axis constants hoisted. The
+// float32 estimate t32 = (p - o32) * inv32 is accepted when its fractional
+// part is farther from an integer than the margin
+//   general:            ((|p| + |o32|)|inv32| + |t32| + 1) 2^-20 (cell_axis_fast)
+//   pow2 cell, o32 = o: |t32| 2^-22
+// (with a power-of-two cell and a float32-exact origin the product is exact
+// and the only error is the rounding of p - o32, <= ulp(t32)/2), and only
+// inside [0, min(n-1, 2^24)]; everything else (near-integer quotients,
+// clamping, NaN) takes the float64 path. Same result as cell_axis_fast.
+struct AxisFast {
+  float o32, inv32, mt, ma, mb, fmax;
+  double origin, cell, inv;
+  i64 n;
+};
+
+__device__ __forceinline__ AxisFast make_axis(double origin, double cell, double inv, i64 n) {
+  AxisFast a;
+  a.o32 = (float)origin;
+  a.inv32 = (float)inv;
+  int e;
+  const bool pow2 = frexp(inv, &e) == 0.5 && __dmul_rn(cell, inv) == 1.0 &&
+                    (double)a.inv32 == inv && (double)a.o32 == origin && e > -100 && e < 100;
+  if (pow2) {
+    a.mt = 2.384185791015625e-07f;   // 2^-22
+    a.ma = 0.0f;
+    a.mb = 0.0f;
+  } else {
+    a.mt = 9.5367431640625e-07f;     // 2^-20
+    a.ma = fabsf(a.inv32) * 9.5367431640625e-07f;
+    a.mb = (fabsf(a.o32) * fabsf(a.inv32) + 1.0f) * 9.5367431640625e-07f;
+  }
+  a.fmax = (float)min(n - 1, (i64)(1 << 24));
+  a.origin = origin;
+  a.cell = cell;
+  a.inv = inv;
+  a.n = n;
+  return a;
+}
+
+__device__ __forceinline__ int cell_axis_hot(float p, const AxisFast& a) {
+  const float t32 = __fmul_rn(__fsub_rn(p, a.o32), a.inv32);
+  const float f32 = floorf(t32);
+  const float fr32 = t32 - f32;
+  const float margin = fmaf(fabsf(t32), a.mt, fmaf(fabsf(p), a.ma, a.mb));
+  if (fr32 > margin && fr32 < 1.0f - margin && f32 >= 0.0f && f32 <= a.fmax)
+    return __float2int_rz(f32);
+  return (int)cell_axis_fast(p, a.origin, a.cell, a.inv, a.n);
+}
+
 // cell lower edge as float32 and whether it is an integer multiple of 2^-40
 __device__ __forceinline__ float cell_ref32(double origin, double cell, i64 i, bool& ok) {
   float r = __double2float_rn(__dadd_rn(origin, __dmul_rn((double)i, cell)));
@@ -258,8 +307,8 @@ __device__ __forceinline__ void s1_flush(const TrackParams& P, TrackCtl* C, S1Sm
     for (int c = 0; c < 5; ++c) {
       i128 s = (i128)sm.dig[3 * c][q] + ((i128)sm.dig[3 * c + 1][q] << 18) +
                ((i128)(int)sm.dig[3 * c + 2][q] << 36);
-      if (c == 0) s += (i128)cnt * f32_to_fixed(sm.refx[qx], FX_STATE);
-      if (c == 1) s += (i128)cnt * f32_to_fixed(sm.refy[qy], FX_STATE);
+      if (c == 0) s += (i128)cnt * f32_to_fixed(sm.ref[qx], FX_STATE);
+      if (c == 1) s += (i128)cnt * f32_to_fixed(sm.ref[snx + qy], FX_STATE);
       atomic_add_i128(P.tab_sum + ((i64)c * P.G + flat) * 2, s);
       sm.dig[3 * c][q] = 0;
       sm.dig[3 * c + 1][q] = 0;
@@ -280,6 +329,8 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
   float* sout = (k & 1) ? P.buf0 : P.buf1;
   const Grid g = P.grid;
   const i64 n = P.n, ld = P.ld;
+  const i64 ntile = ceil_div(n, S1_TILE);
+  const i64 tstep = gridDim.x;
 
   // sub-window (identical in every CTA): centred on the previous estimate
   i64 snx = min((i64)39, g.ncols), sny = min((i64)39, g.nrows);
@@ -300,39 +351,39 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
     for (int p = 0; p < S1_PARTS; ++p) sm.dig[p][q] = 0;
   }
   // cell lower edges; NaN marks an edge whose deltas may not be exact
-  for (int q = t; q < snxi; q += S1_THREADS) {
+  for (int q = t; q < snxi + snyi; q += S1_THREADS) {
     bool ok;
-    float r = cell_ref32(g.ox, g.lx, sx0 + q, ok);
-    sm.refx[q] = ok ? r : __int_as_float(0x7fc00000);
-  }
-  for (int q = t; q < snyi; q += S1_THREADS) {
-    bool ok;
-    float r = cell_ref32(g.oy, g.ly, sy0 + q, ok);
-    sm.refy[q] = ok ? r : __int_as_float(0x7fc00000);
+    float r = (q < snxi) ? cell_ref32(g.ox, g.lx, sx0 + q, ok)
+                         : cell_ref32(g.oy, g.ly, sy0 + (q - snxi), ok);
+    sm.ref[q] = ok ? r : __int_as_float(0x7fc00000);
   }
   if (t == 0) {
     sm.n_list = 0;
     sm.n_flist = 0;
   }
+  const float* refy = sm.ref + snxi;
   __syncthreads();
 
   const u32 frame = P.frame0 + (u32)k;
+  const AxisFast axx = make_axis(g.ox, g.lx, P.inv_lx, g.ncols);
+  const AxisFast axy = make_axis(g.oy, g.ly, P.inv_ly, g.nrows);
+  const u32 ncols32 = (u32)g.ncols;
+  const int sx0i = (int)sx0, sy0i = (int)sy0;
   bool bad = false;
-  const i64 ntile = ceil_div(n, S1_TILE);
   int since = 0;
-  for (i64 tile = blockIdx.x; tile < ntile; tile += gridDim.x) {
+  for (i64 tile = blockIdx.x; tile < ntile; tile += tstep) {
     // ---- phase 1: gather + propagate + cell; rank within the tile's cell ----
     int q_k[S1_IPT], r_k[S1_IPT];
     float o_k[S1_IPT][5];
     int src_k[S1_IPT];
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {   // every gather before any arithmetic
-      i64 j = tile * S1_TILE + (i64)it * S1_THREADS + t;
+      const i64 j = tile * S1_TILE + (i64)it * S1_THREADS + t;
       src_k[it] = (j < n) ? __ldg(P.anc + j) : 0;
     }
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {
-      i64 j = tile * S1_TILE + (i64)it * S1_THREADS + t;
+      const i64 j = tile * S1_TILE + (i64)it * S1_THREADS + t;
 #pragma unroll
       for (int c = 0; c < 5; ++c) o_k[it][c] = (j < n) ? __ldg(sin + c * ld + src_k[it]) : 0.0f;
     }
@@ -350,14 +401,14 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
 #pragma unroll
       for (int c = 0; c < 5; ++c) sout[c * ld + j] = o[c];
       if (!(o[0] == o[0]) || !(o[1] == o[1])) bad = true;
-      const i64 ix = cell_axis_fast(o[0], g.ox, g.lx, P.inv_lx, g.ncols);
-      const i64 iy = cell_axis_fast(o[1], g.oy, g.ly, P.inv_ly, g.nrows);
-      const u32 flat = (u32)(iy * g.ncols + ix);
+      const int ix = cell_axis_hot(o[0], axx);
+      const int iy = cell_axis_hot(o[1], axy);
+      const u32 flat = (u32)iy * ncols32 + (u32)ix;   // G <= 2^28
       P.pslot[j] = flat;
-      const int lx = (int)(ix - sx0), ly = (int)(iy - sy0);
+      const int lx = ix - sx0i, ly = iy - sy0i;
       float dx, dy;
-      if (lx >= 0 && lx < snxi && ly >= 0 && ly < snyi && delta_exact(o[0], sm.refx[lx], dx) &&
-          delta_exact(o[1], sm.refy[ly], dy) && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f &&
+      if ((u32)lx < (u32)snxi && (u32)ly < (u32)snyi && delta_exact(o[0], sm.ref[lx], dx) &&
+          delta_exact(o[1], refy[ly], dy) && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f &&
           fabsf(o[4]) < 128.0f) {
         const int q = ly * snxi + lx;
         const int r = (int)atomicAdd(&sm.tile_cnt[q], 1u);
@@ -400,7 +451,7 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
         if (e < nl) {
           const int q = sm.list[e];
           const u32 c = (u32)(h ? c1 : c0);
-          sm.tile_start[q] = (u32)run;
+          sm.tile_start[q] = (unsigned short)run;
           sm.tile_cnt[q] = 0;
           const u32 old = sm.cnt[q];
           sm.cnt[q] = old + c;
@@ -412,12 +463,13 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
     }
     __syncthreads();
     // ---- phase 3: scatter the in-window particles into cell-sorted order ----
+    float (*pay)[S1_TILE] = sm.pay;
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {
       if (q_k[it] < 0) continue;
       const int pos = (int)sm.tile_start[q_k[it]] + r_k[it];
 #pragma unroll
-      for (int c = 0; c < 5; ++c) sm.pay[c][pos] = o_k[it][c];
+      for (int c = 0; c < 5; ++c) pay[c][pos] = o_k[it][c];
       sm.pay_q[pos] = (unsigned short)q_k[it];
     }
     __syncthreads();
@@ -438,7 +490,7 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
         const int q = sm.pay_q[p];
         long long v[5];
 #pragma unroll
-        for (int c = 0; c < 5; ++c) v[c] = __float2ll_rn(__fmul_rn(sm.pay[c][p], 1099511627776.0f));
+        for (int c = 0; c < 5; ++c) v[c] = __float2ll_rn(__fmul_rn(pay[c][p], 1099511627776.0f));
         if (e == 0) {
           kf = kl = q;
 #pragma unroll

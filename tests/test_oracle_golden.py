@@ -21,11 +21,19 @@ def test_philox_known_answers(seed, ctr, want):
 
 
 def test_normals_law():
+    # five normals per particle from one Philox block (three Box-Muller pairs,
+    # the third one built from the leftover low bits): each column N(0, 1),
+    # columns uncorrelated
     z = orc.propagate_normals(5, 0, 200_000)
     assert abs(z.mean()) < 0.005
     assert abs(z.std() - 1.0) < 0.005
     import scipy.stats
-    assert scipy.stats.kstest(z[0], "norm").pvalue > 1e-3
+    for c in range(5):
+        assert abs(z[c].std() - 1.0) < 0.01
+        assert scipy.stats.kstest(z[c], "norm").pvalue > 1e-3
+    cc = np.corrcoef(z)
+    assert np.max(np.abs(cc - np.eye(5))) < 0.01
+    assert np.max(np.abs(z)) < 5.7   # 22-bit u1: |z| <= sqrt(-2 ln 2^-23)
 
 
 # --- likelihood operator (_speedups.pyx / kernels.py) --------------------------
