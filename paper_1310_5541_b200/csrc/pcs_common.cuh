@@ -264,14 +264,26 @@ __device__ __forceinline__ void box_muller(u32 a, u32 b, float& z0, float& z1) {
 }
 
 // Box–Muller on explicit integer uniforms: u1 = (a + 1/2) 2^-22 (a < 2^22),
-// u2 = b 2^-20 (b < 2^20); same SFU evaluation as box_muller.
+// u2 = b 2^-20 (b < 2^20). Flush-to-zero SFU forms (the arguments are never
+// subnormal): r = l2 * rsqrt(l2), l2 = lg2(u1) * (-2 ln 2); the angle
+// 2 pi b 2^-20 - pi is one FMA.
+__device__ __forceinline__ float lg2_ftz(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ float bm_radius22(u32 a) {
-  float u1 = ((float)a + 0.5f) * 2.384185791015625e-07f;
-  float l2 = -2.0f * __logf(u1);
-  return (l2 > 0.0f) ? l2 * rsqrtf(l2) : 0.0f;
+  const float u1 = fmaf((float)a, 2.384185791015625e-07f, 1.1920928955078125e-07f);
+  const float l2 = lg2_ftz(u1) * -1.38629436111989061883f;   // -2 ln 2
+  return (l2 > 0.0f) ? l2 * rsqrt_ftz(l2) : 0.0f;
 }
 __device__ __forceinline__ float bm_angle20(u32 b) {
-  return 6.28318530717958647692f * ((float)b * 9.5367431640625e-07f - 0.5f);
+  return fmaf((float)b, 5.9921124526782e-06f, -3.14159265358979323846f);   // 2 pi 2^-20
 }
 
 // The five standard normals used to propagate particle `idx` at `frame`

@@ -43,7 +43,9 @@ constexpr int MAXM = 16384;                    // occupied cells per frame (fuse
 // additions per tile, so over S1_FLUSH_TILES tiles the digits stay below 2^30
 // in magnitude; the CTA then folds them into the exact int128 HBM table.
 struct S1Smem {
-  float pay[5][S1_TILE];   // cell-sorted tile: x - ref, y - ref, vx, vy, I0 (exact)
+  float pay[5][S1_TILE];   // cell-sorted tile, lane-major for phase 4 (sorted
+                           // position p at (p % S1_E) * S1_SUM_THREADS + p / S1_E):
+                           // x - ref, y - ref, vx, vy, I0 (exact)
   u32 dig[S1_PARTS][SUBW];
   u32 cnt[SUBW];          // particles per cell since the last flush
   u32 tile_cnt[SUBW];
@@ -468,9 +470,10 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
     for (int it = 0; it < S1_IPT; ++it) {
       if (q_k[it] < 0) continue;
       const int pos = (int)sm.tile_start[q_k[it]] + r_k[it];
+      const int idx = (pos % S1_E) * S1_SUM_THREADS + pos / S1_E;
 #pragma unroll
-      for (int c = 0; c < 5; ++c) pay[c][pos] = o_k[it][c];
-      sm.pay_q[pos] = (unsigned short)q_k[it];
+      for (int c = 0; c < 5; ++c) pay[c][idx] = o_k[it][c];
+      sm.pay_q[idx] = (unsigned short)q_k[it];
     }
     __syncthreads();
     // ---- phase 4: exact run sums over the sorted tile (16 warps, 4
@@ -487,10 +490,11 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
       for (int e = 0; e < S1_E; ++e) {
         const int p = p0 + e;
         if (p >= ni) break;
-        const int q = sm.pay_q[p];
+        const int idx = e * S1_SUM_THREADS + t;   // conflict-free (lane-major)
+        const int q = sm.pay_q[idx];
         long long v[5];
 #pragma unroll
-        for (int c = 0; c < 5; ++c) v[c] = __float2ll_rn(__fmul_rn(pay[c][p], 1099511627776.0f));
+        for (int c = 0; c < 5; ++c) v[c] = __float2ll_rn(__fmul_rn(pay[c][idx], 1099511627776.0f));
         if (e == 0) {
           kf = kl = q;
 #pragma unroll
