@@ -48,9 +48,9 @@ OTHER_VARIANTS = {"c2": ["SIR", "pcSIR-0.5px", "pcSIR-0.25px", "pcSIR-2px"], "c3
                   "c1": ["SIR"]}
 ALGO_BYTES = {  # algorithmic bytes per particle per launch
     # pcSIR step1: R anc 4 + R state 20 + W state 20 + W cell 4; scan: R cell 4 + W anc 4
-    "k_pc_step1": 48, "k_scan_emit:pc": 8,
+    "k_pc_step1": 48, "k_sys_resample:pc": 8,
     # SIR: + W loglik 8; sum: R 8; stats: R 8 + R 20; scan: R 8 + W 4
-    "k_sir_propagate_lik": 52, "k_sir_sum": 8, "k_sir_stats": 28, "k_scan_emit:sir": 12,
+    "k_sir_propagate_lik": 52, "k_sir_sum": 8, "k_sir_stats": 28, "k_sys_resample:sir": 12,
     # multi-target frame kernel: step1 48 + scan R cell 4 + W anc 4
     "k_mt_frame": 56,
 }
@@ -427,7 +427,7 @@ def main():
         kprof = kernel_profile(torch, pc, _lib, cfg, grid, dev_frames, args.warmup,
                                min(args.steps, 10), args.seed, flush)
         dom = max(kprof, key=kprof.get)
-        key = dom if dom != "k_scan_emit" else ("k_scan_emit:pc" if cpp_main else "k_scan_emit:sir")
+        key = dom if dom != "k_sys_resample" else ("k_sys_resample:pc" if cpp_main else "k_sys_resample:sir")
         dom_bytes = ALGO_BYTES.get(key, 0) * n
         achieved = dom_bytes / (kprof[dom] * 1e-3) / 1e9 if kprof[dom] > 0 else 0.0
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,

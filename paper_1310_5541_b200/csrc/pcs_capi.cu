@@ -60,6 +60,7 @@ struct TrackState {
   TrackParams P{};
   BinsScratch bins{};
   int s1_grid = 0;
+  int rs_grid = 0;       // k_sys_resample CTAs (all co-resident)
   int prop_grid = 0;
   int maxs = 0;
   i64 k = 0;             // host mirror of the frame counter
@@ -654,9 +655,9 @@ __global__ void k_ctl_io(TrackCtl* C, const float* frames, i64 kf, i64 ko, doubl
   C->out_occ = occ;
 }
 
-static const char* kPcNames[] = {"k_pc_step1", "k_pc_bins", "k_scan_emit"};
+static const char* kPcNames[] = {"k_pc_step1", "k_pc_bins", "k_sys_resample"};
 static const char* kSirNames[] = {"k_sir_propagate_lik", "k_sir_sum", "k_sir_stats",
-                                  "k_sir_finalize", "k_scan_emit"};
+                                  "k_sir_finalize", "k_sys_resample"};
 
 // Enqueue one frame. If evs is non-null, evs[i] is recorded before launch i
 // and evs[launches] after the last one (per-kernel CUDA-event timing).
@@ -679,7 +680,7 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
       default: k_pc_bins<0><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P, T.bins);
     }
     mark();
-    k_scan_emit<1><<<(unsigned)P.ntiles, SCAN_BLOCK, 0, st>>>(P);
+    k_sys_resample<1><<<T.rs_grid, SCAN_BLOCK, 0, st>>>(P);
   } else {
     mark();
     switch (T.maxs) {
@@ -695,7 +696,7 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
     mark();
     k_sir_finalize<<<1, 1, 0, st>>>(P);
     mark();
-    k_scan_emit<2><<<(unsigned)P.ntiles, SCAN_BLOCK, 0, st>>>(P);
+    k_sys_resample<2><<<T.rs_grid, SCAN_BLOCK, 0, st>>>(P);
   }
   if (evs) cudaEventRecord(evs[q], st);
   PCS_LAUNCH_CHECK();
@@ -725,7 +726,8 @@ static int set_attrs() {
                        (const void*)k_scan_emit<2>,     (const void*)k_sir_propagate_lik<0>,
                        (const void*)k_sir_propagate_lik<9>, (const void*)k_sir_propagate_lik<11>,
                        (const void*)k_sir_propagate_lik<15>, (const void*)k_sir_sum,
-                       (const void*)k_sir_stats,        (const void*)k_sir_finalize};
+                       (const void*)k_sir_stats,        (const void*)k_sir_finalize,
+                       (const void*)k_sys_resample<1>,  (const void*)k_sys_resample<2>};
   for (const void* f : fns)
     PCS_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                       (int)cudaSharedmemCarveoutMaxShared));
@@ -786,6 +788,7 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   PCS_SCRATCH(SL_TR_TILES, P.ntiles * (2 * sizeof(u128) + sizeof(u32)) + 64, P.tile_agg);
   P.tile_inc = P.tile_agg + P.ntiles;
   P.tile_status = (u32*)(P.tile_inc + P.ntiles);
+  P.cta_agg = P.tile_agg;   // k_sys_resample: rs_grid <= ntiles aggregates
   PCS_CUDA_TRY(cudaMemsetAsync(P.tile_status, 0, P.ntiles * sizeof(u32), st));
   if (cfg->method == 0) {
     PCS_SCRATCH(SL_TR_LL, ld * sizeof(double), P.ll);
@@ -804,7 +807,8 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
       ctx->table_cells = 0;
       PCS_CUDA_TRY(cudaMalloc(&ctx->tab_cnt, P.G * sizeof(u32)));
       PCS_CUDA_TRY(cudaMalloc(&ctx->tab_sum, 5 * P.G * 2 * sizeof(u64)));
-      PCS_CUDA_TRY(cudaMalloc(&ctx->wtab, P.G * sizeof(float)));
+      // float weights, then the 16-byte exact weights (wfix)
+      PCS_CUDA_TRY(cudaMalloc(&ctx->wtab, ceil_div(P.G, 4) * 16 + P.G * sizeof(u128)));
       ctx->table_cells = P.G;
       ctx->table_dirty = true;
     }
@@ -817,6 +821,7 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
     P.tab_cnt = ctx->tab_cnt;
     P.tab_sum = ctx->tab_sum;
     P.wtab = ctx->wtab;
+    P.wfix = (u128*)(ctx->wtab + ceil_div(P.G, 4) * 4);
     P.occ = ctx->occ;
     float* sd = (float*)(ctx->occ + MAXM);
     T.bins.dx = sd;
@@ -826,6 +831,15 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   T.maxs = maxs_for(cfg->spot.halfwidth);
   T.prop_grid = grid_for(n, 256, ctx->sms, 8);
   T.s1_grid = (int)std::min<i64>(ctx->sms, ceil_div(n, S1_TILE));
+  {
+    // k_sys_resample has a grid barrier: every CTA must be co-resident
+    int per_sm = 0;
+    if (cfg->method == 1)
+      PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sys_resample<1>, SCAN_BLOCK, 0));
+    else
+      PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sys_resample<2>, SCAN_BLOCK, 0));
+    T.rs_grid = (int)std::min<i64>((i64)ctx->sms * std::max(per_sm, 1), P.ntiles);
+  }
   // initial cloud (state.py:164-175) and identity ancestors
   pcs_init_t init = cfg->init;
   r = pcs_init_particles(&init, cfg->seed, 0, n, P.buf0, ld, stream);

@@ -90,6 +90,7 @@ struct TrackCtl {
   long long dbg[16];         // phase timestamps (globaltimer ns) of the bins kernel
   unsigned long long tile_ctr;  // decoupled look-back: monotone tile ticket counter
   u64 rank_prefix[2];        // sharded: exact cumulative weight of the preceding ranks
+  u32 gbar_cnt, gbar_gen;    // grid barrier of k_sys_resample
 };
 
 struct TrackParams {
@@ -110,6 +111,7 @@ struct TrackParams {
   u32* tab_cnt;              // [G]
   u64* tab_sum;              // [5][G][2]
   float* wtab;               // [G]
+  u128* wfix;                // [G] exact cdf weight round(wtab * 2^120) (k_sys_resample)
   u32* occ;                  // [MAXM]
   i64 G;                     // table cells (= n_cols * n_rows)
   i64 ntiles;                // scan tiles
@@ -124,6 +126,7 @@ struct TrackParams {
   i64 slot_cap;              // capacity of anc_out
   int* anc_out;              // ancestors (local particle index) for slots slot_lo + k
   int scan_mode;             // 0 scan+emit, 1 scan only, 2 emit only (rank prefix in ctl)
+  u128* cta_agg;             // k_sys_resample: per-CTA exact weight totals
 };
 
 __device__ __forceinline__ void set_flag(TrackCtl* c, u32 f) {
@@ -733,6 +736,7 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     u32 cnt = P.tab_cnt[cell];
     float w = normalised_weight(s_ll[b], m, Sf);
     P.wtab[cell] = w;
+    P.wfix[cell] = cdf_fixed(w);
     atomicMin(&s_wmin, __float_as_uint(w));
     atomicMax(&s_wmax, __float_as_uint(w));
     i128 wq = f32_to_fixed(w, FX_WQ);
@@ -805,9 +809,13 @@ __device__ __forceinline__ u32 ld_acquire_u32(const u32* p) {
 // scan_mode 2: emission only, excl = rank_prefix + tile_inc[tile-1] (sharded)
 // Emitted slots are global (n_global points), written as local ancestor
 // indices to anc_out[j - slot_lo].
+// weights staged with one pad word per SCAN_ITEMS so that thread t's items
+// (t * SCAN_ITEMS + q) are read conflict-free
+__device__ __forceinline__ int wpad(int k) { return k + k / SCAN_ITEMS; }
+
 template <int KIND>
-__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_emit(TrackParams P) {
-  __shared__ float wsh[SCAN_TILE];
+__global__ void __launch_bounds__(SCAN_BLOCK, 4) k_scan_emit(TrackParams P) {
+  __shared__ float wsh[SCAN_TILE + SCAN_TILE / SCAN_ITEMS];
   __shared__ u128 wtot[SCAN_BLOCK / 32];
   __shared__ u128 s_excl;
   __shared__ unsigned long long s_ticket;
@@ -835,12 +843,12 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_emit(TrackParams P) {
     i64 i = base + (i64)q * SCAN_BLOCK + threadIdx.x;
     float w = 0.0f;
     if (i < n) w = (KIND == 1) ? P.wtab[P.pslot[i]] : normalised_weight(P.ll[i], m, Sf);
-    wsh[q * SCAN_BLOCK + threadIdx.x] = w;
+    wsh[wpad(q * SCAN_BLOCK + threadIdx.x)] = w;
   }
   __syncthreads();
   u128 tsum = 0;
 #pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) tsum += cdf_fixed(wsh[threadIdx.x * SCAN_ITEMS + q]);
+  for (int q = 0; q < SCAN_ITEMS; ++q) tsum += cdf_fixed(wsh[wpad(threadIdx.x * SCAN_ITEMS + q)]);
   const int l = threadIdx.x & 31, wi = threadIdx.x >> 5;
   u128 inc = tsum;
 #pragma unroll
@@ -920,7 +928,8 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_emit(TrackParams P) {
   const double nd = (double)ng, eps = nd * 8.881784197001252e-16;   // n * 2^-50
   // the tile's slot range: start of its first item .. end of its last item
   __shared__ long long s_jrange[2];
-  __shared__ int stage[SCAN_TILE];
+  __shared__ int stage[SCAN_TILE + SCAN_TILE / SCAN_ITEMS];
+  __shared__ int s_wmax[SCAN_BLOCK / 32];
   if (threadIdx.x == 0) {
     const i64 tl = min(n, base + (i64)SCAN_TILE) - 1;
     s_jrange[0] = (off + base == 0) ? 0 : first_slot_fast(cdf_round(s_excl), u, ng, nd, eps);
@@ -929,36 +938,316 @@ __global__ void __launch_bounds__(SCAN_BLOCK) k_scan_emit(TrackParams P) {
   }
   __syncthreads();
   const i64 tj0 = s_jrange[0], tj1 = s_jrange[1];
-  const bool staged = (tj1 - tj0) <= (i64)SCAN_TILE && (tj1 - tj0) >= 0;
-  bool oob = false;
-  if (i0 < n) {
-    // running inclusive prefix recomputed from the staged weights (no
-    // per-item register array)
-    i64 j = (off + i0 == 0) ? 0 : first_slot_fast(cdf_round(excl), u, ng, nd, eps);
+  // 1) per item: its first slot relative to tj0 if it receives any slot
+  //    (the run head), else INT_MAX; stored in place of the item's weight
+  int* hp = reinterpret_cast<int*>(wsh);
+  {
+    const int k0 = (int)threadIdx.x * SCAN_ITEMS;
+    int jr = 0;
+    if (i0 < n) jr = (int)(((off + i0 == 0) ? 0 : first_slot_fast(cdf_round(excl), u, ng, nd, eps)) - tj0);
     u128 run = excl;
     for (int q = 0; q < SCAN_ITEMS; ++q) {
       const i64 i = i0 + q;
-      if (i >= n) break;
-      run += cdf_fixed(wsh[threadIdx.x * SCAN_ITEMS + q]);
-      const i64 jend = (off + i == ng - 1) ? ng : first_slot_fast(cdf_round(run), u, ng, nd, eps);
-      for (; j < jend; ++j) {
-        if (staged) {
-          stage[j - tj0] = (int)i;
-        } else {
-          i64 kk = j - lo;
-          if (kk >= 0 && kk < cap) P.anc_out[kk] = (int)i;
-          else oob = true;
-        }
+      int h = INT_MAX;
+      if (i < n) {
+        run += cdf_fixed(wsh[wpad(k0 + q)]);
+        const int jend =
+            (int)(((off + i == ng - 1) ? ng : first_slot_fast(cdf_round(run), u, ng, nd, eps)) - tj0);
+        if (jend > jr) h = jr;
+        jr = jend;
       }
+      hp[wpad(k0 + q)] = h;
     }
   }
-  if (staged) {
+  __syncthreads();
+  // 2) the tile's slots in chunks of SCAN_TILE: mark the run heads, block
+  //    max-scan (ancestor of a slot = last head at or before it), write out
+  //    coalesced
+  bool oob = false;
+  const i64 m_slots = tj1 - tj0;
+  const int lane_s = threadIdx.x & 31, warp_s = threadIdx.x >> 5;
+  int carry = -1;
+  for (i64 c0 = 0; c0 < m_slots; c0 += SCAN_TILE) {
+    const int k0 = (int)threadIdx.x * SCAN_ITEMS;
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q) stage[wpad(k0 + q)] = -1;
     __syncthreads();
-    for (i64 j = tj0 + threadIdx.x; j < tj1; j += SCAN_BLOCK) {
-      i64 kk = j - lo;
-      if (kk >= 0 && kk < cap) P.anc_out[kk] = stage[j - tj0];
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q) {
+      const int h = hp[wpad(k0 + q)];
+      if ((i64)h >= c0 && (i64)h < c0 + SCAN_TILE) stage[wpad((int)((i64)h - c0))] = k0 + q;
+    }
+    __syncthreads();
+    int tmax = -1;
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q) tmax = max(tmax, stage[wpad(k0 + q)]);
+    int incl = tmax;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane_s >= d) incl = max(incl, o);
+    }
+    if (lane_s == 31) s_wmax[warp_s] = incl;
+    int excl_l = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane_s == 0) excl_l = -1;
+    __syncthreads();
+    int prev = carry, total = carry;
+#pragma unroll
+    for (int w = 0; w < SCAN_BLOCK / 32; ++w) {
+      if (w < warp_s) prev = max(prev, s_wmax[w]);
+      total = max(total, s_wmax[w]);
+    }
+    int runm = max(prev, excl_l);
+#pragma unroll
+    for (int q = 0; q < SCAN_ITEMS; ++q) {
+      runm = max(runm, stage[wpad(k0 + q)]);
+      stage[wpad(k0 + q)] = runm;
+    }
+    __syncthreads();
+    const int cm = (int)min((i64)SCAN_TILE, m_slots - c0);
+    for (int k = threadIdx.x; k < cm; k += SCAN_BLOCK) {
+      const i64 kk = tj0 + c0 + k - lo;
+      if (kk >= 0 && kk < cap) P.anc_out[kk] = (int)(base + stage[wpad(k)]);
       else oob = true;
     }
+    carry = total;
+    __syncthreads();
+  }
+  if (oob) set_flag(C, PCS_FLAG_CAPACITY);
+}
+
+// ===========================================================================
+// Persistent reduce-then-scan systematic resampling (single GPU, scan_mode 0).
+// Each CTA owns a contiguous range of tiles. Pass 1 sums the exact
+// fixed-point weights of its range; after ONE grid-wide barrier every CTA
+// adds up the aggregates of the CTAs before it (its exact exclusive prefix);
+// pass 2 re-reads its range tile by tile, emits each item's slots and writes
+// the ancestors coalesced. No per-tile look-back chain: the serial latency is
+// one barrier per frame instead of one L2 round trip per 32 predecessor tiles.
+// Requires every CTA to be co-resident (grid = SMs x occupancy, set by the
+// host from the occupancy calculator).
+// ===========================================================================
+constexpr int RS_MIN_BLOCKS = 3;
+
+__device__ __forceinline__ void grid_barrier(TrackCtl* C, int nblocks) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const u32 gen = ld_acquire_u32(&C->gbar_gen);
+    __threadfence();
+    if (atomicAdd(&C->gbar_cnt, 1u) == (u32)nblocks - 1u) {
+      C->gbar_cnt = 0;
+      __threadfence();
+      st_release_u32(&C->gbar_gen, gen + 1u);
+    } else {
+      while (ld_acquire_u32(&C->gbar_gen) == gen) __nanosleep(64);
+    }
+  }
+  __syncthreads();
+}
+
+// exact fixed-point weight of staged item k: KIND 1 stages the cell id and
+// reads the per-cell table, KIND 2 stages the float weight
+template <int KIND>
+__device__ __forceinline__ u128 rs_weight(const TrackParams& P, const float* wsh, int k) {
+  if (KIND == 1) {
+    const u32 cell = __float_as_uint(wsh[wpad(k)]);
+    return (cell == 0xFFFFFFFFu) ? (u128)0 : P.wfix[cell];
+  }
+  return cdf_fixed(wsh[wpad(k)]);
+}
+
+template <int KIND>
+__device__ __forceinline__ u128 rs_load_tile(const TrackParams& P, i64 tile, float* wsh, double m,
+                                             double Sf) {
+  const i64 base = tile * SCAN_TILE;
+#pragma unroll 4
+  for (int q = 0; q < SCAN_ITEMS; ++q) {
+    const i64 i = base + (i64)q * SCAN_BLOCK + threadIdx.x;
+    float w;
+    if (KIND == 1) w = __uint_as_float((i < P.n) ? P.pslot[i] : 0xFFFFFFFFu);
+    else w = (i < P.n) ? normalised_weight(P.ll[i], m, Sf) : 0.0f;
+    wsh[wpad(q * SCAN_BLOCK + threadIdx.x)] = w;
+  }
+  __syncthreads();
+  u128 tsum = 0;
+#pragma unroll
+  for (int q = 0; q < SCAN_ITEMS; ++q) tsum += rs_weight<KIND>(P, wsh, threadIdx.x * SCAN_ITEMS + q);
+  return tsum;
+}
+
+// first slot at/above the cdf value RN64(Pc) 2^-120 (first_slot_fast(cdf_round(Pc))):
+// float64 estimate from the top 64 bits of Pc, |error| <= n (3 2^-53 + 2^-63)
+// < eps = n 2^-50, exact path otherwise
+__device__ __forceinline__ i64 slot_of_prefix(u128 Pc, double u, i64 ng, double nd, double kappa,
+                                              double eps) {
+  const double t = fma((double)(u64)(Pc >> 57), kappa, -u);
+  const double g = ceil(t);
+  const double gap = g - t;
+  if (gap > eps && gap < 1.0 - eps && g > 0.0 && g < nd) return (i64)g;
+  return first_slot_fast(cdf_round(Pc), u, ng, nd, eps);
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(TrackParams P) {
+  __shared__ float wsh[SCAN_TILE + SCAN_TILE / SCAN_ITEMS];
+  __shared__ int stage[SCAN_TILE + SCAN_TILE / SCAN_ITEMS];
+  __shared__ u128 wtot[SCAN_BLOCK / 32];
+  __shared__ int s_wmax[SCAN_BLOCK / 32];
+  __shared__ long long s_jr[2];
+  TrackCtl* C = P.ctl;
+  const i64 n = P.n, nt = P.ntiles;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const i64 t0 = nt * cta / G, t1 = nt * (cta + 1) / G;
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  if (!C->do_resample) {   // identity ancestors, weights stay uniform (all equal)
+    for (i64 i = t0 * SCAN_TILE + threadIdx.x; i < min(n, t1 * SCAN_TILE); i += SCAN_BLOCK)
+      P.anc_out[P.idx_off + i - P.slot_lo] = (int)i;
+    return;
+  }
+  const double m = C->m, Sf = C->Sf, u = C->u;
+  // ---- pass 1: this CTA's exact total ----
+  u128 acc = 0;
+  for (i64 tile = t0; tile < t1; ++tile) {
+    acc += rs_load_tile<KIND>(P, tile, wsh, m, Sf);
+    __syncthreads();
+  }
+  {
+    u128 v = acc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const u64 lo = (u64)v, hi = (u64)(v >> 64);
+      v += ((u128)__shfl_xor_sync(0xffffffffu, hi, o) << 64) | (u128)__shfl_xor_sync(0xffffffffu, lo, o);
+    }
+    if (lane == 0) wtot[wi] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      u128 tot = 0;
+      for (int w = 0; w < SCAN_BLOCK / 32; ++w) tot += wtot[w];
+      P.cta_agg[cta] = tot;
+      __threadfence();
+    }
+  }
+  grid_barrier(C, G);
+  // ---- exclusive prefix of this CTA: aggregates of the CTAs before it ----
+  u128 pre;
+  {
+    u128 v = 0;
+    for (int k = threadIdx.x; k < cta; k += SCAN_BLOCK) v += *((volatile u128*)(P.cta_agg + k));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const u64 lo = (u64)v, hi = (u64)(v >> 64);
+      v += ((u128)__shfl_xor_sync(0xffffffffu, hi, o) << 64) | (u128)__shfl_xor_sync(0xffffffffu, lo, o);
+    }
+    __syncthreads();
+    if (lane == 0) wtot[wi] = v;
+    __syncthreads();
+    pre = 0;
+    for (int w = 0; w < SCAN_BLOCK / 32; ++w) pre += wtot[w];
+    __syncthreads();
+  }
+  // ---- pass 2: per tile, item prefixes -> run heads -> ancestors ----
+  const i64 ng = P.n_global, off = P.idx_off, lo = P.slot_lo, cap = P.slot_cap;
+  const double nd = (double)ng, eps = nd * 8.881784197001252e-16;   // n * 2^-50
+  const double kappa = nd * 1.0842021724855044e-19;                  // n * 2^-63
+  bool oob = false;
+  int* hp = reinterpret_cast<int*>(wsh);
+  for (i64 tile = t0; tile < t1; ++tile) {
+    const i64 base = tile * SCAN_TILE;
+    const u128 tsum = rs_load_tile<KIND>(P, tile, wsh, m, Sf);
+    u128 inc = tsum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const u128 o = shfl_up_u128(inc, d);
+      if (lane >= d) inc += o;
+    }
+    if (lane == 31) wtot[wi] = inc;
+    __syncthreads();
+    u128 woff = 0, tagg = 0;
+#pragma unroll
+    for (int w = 0; w < SCAN_BLOCK / 32; ++w) {
+      if (w < wi) woff += wtot[w];
+      tagg += wtot[w];
+    }
+    const u128 excl = pre + woff + (inc - tsum);
+    const i64 i0 = base + (i64)threadIdx.x * SCAN_ITEMS;
+    if (threadIdx.x == 0) {
+      const i64 tl = min(n, base + (i64)SCAN_TILE) - 1;
+      s_jr[0] = (off + base == 0) ? 0 : first_slot_fast(cdf_round(pre), u, ng, nd, eps);
+      s_jr[1] = (off + tl == ng - 1) ? ng : first_slot_fast(cdf_round(pre + tagg), u, ng, nd, eps);
+    }
+    __syncthreads();
+    const i64 tj0 = s_jr[0], tj1 = s_jr[1];
+    // run head of every item: its first slot relative to tj0, INT_MAX if none
+    {
+      const int k0 = (int)threadIdx.x * SCAN_ITEMS;
+      int jr = 0;
+      if (i0 < n)
+        jr = (int)(((off + i0 == 0) ? 0 : slot_of_prefix(excl, u, ng, nd, kappa, eps)) - tj0);
+      u128 run = excl;
+      for (int q = 0; q < SCAN_ITEMS; ++q) {
+        const i64 i = i0 + q;
+        int h = INT_MAX;
+        if (i < n) {
+          run += rs_weight<KIND>(P, wsh, k0 + q);
+          const int jend =
+              (int)(((off + i == ng - 1) ? ng : slot_of_prefix(run, u, ng, nd, kappa, eps)) - tj0);
+          if (jend > jr) h = jr;
+          jr = jend;
+        }
+        hp[wpad(k0 + q)] = h;
+      }
+    }
+    __syncthreads();
+    // slots in chunks of SCAN_TILE: heads, block max-scan, coalesced writes
+    const i64 m_slots = tj1 - tj0;
+    int carry = -1;
+    for (i64 c0 = 0; c0 < m_slots; c0 += SCAN_TILE) {
+      const int k0 = (int)threadIdx.x * SCAN_ITEMS;
+#pragma unroll
+      for (int q = 0; q < SCAN_ITEMS; ++q) stage[wpad(k0 + q)] = -1;
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < SCAN_ITEMS; ++q) {
+        const int h = hp[wpad(k0 + q)];
+        if ((i64)h >= c0 && (i64)h < c0 + SCAN_TILE) stage[wpad((int)((i64)h - c0))] = k0 + q;
+      }
+      __syncthreads();
+      int tmax = -1;
+#pragma unroll
+      for (int q = 0; q < SCAN_ITEMS; ++q) tmax = max(tmax, stage[wpad(k0 + q)]);
+      int incl = tmax;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl = max(incl, o);
+      }
+      if (lane == 31) s_wmax[wi] = incl;
+      int excl_l = __shfl_up_sync(0xffffffffu, incl, 1);
+      if (lane == 0) excl_l = -1;
+      __syncthreads();
+      int prev = carry, total = carry;
+#pragma unroll
+      for (int w = 0; w < SCAN_BLOCK / 32; ++w) {
+        if (w < wi) prev = max(prev, s_wmax[w]);
+        total = max(total, s_wmax[w]);
+      }
+      int runm = max(prev, excl_l);
+#pragma unroll
+      for (int q = 0; q < SCAN_ITEMS; ++q) {
+        runm = max(runm, stage[wpad(k0 + q)]);
+        stage[wpad(k0 + q)] = runm;
+      }
+      __syncthreads();
+      const int cm = (int)min((i64)SCAN_TILE, m_slots - c0);
+      for (int k = threadIdx.x; k < cm; k += SCAN_BLOCK) {
+        const i64 kk = tj0 + c0 + k - lo;
+        if (kk >= 0 && kk < cap) P.anc_out[kk] = (int)(base + stage[wpad(k)]);
+        else oob = true;
+      }
+      carry = total;
+      __syncthreads();
+    }
+    pre += tagg;
   }
   if (oob) set_flag(C, PCS_FLAG_CAPACITY);
 }

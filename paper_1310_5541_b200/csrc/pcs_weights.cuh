@@ -183,12 +183,28 @@ struct WeightSrc {
   }
 };
 
+__device__ __noinline__ u128 cdf_fixed_slow(float w) { return (u128)f32_to_fixed(w, FX_CDF); }
+
 __device__ __forceinline__ u128 cdf_fixed(float w) {
-  // fast path (w >= 2^-97, positive): round(w * 2^120) is an exact left shift
-  u32 b = __float_as_uint(w);
-  u32 ef = (b >> 23) & 0xFFu;
-  if (!(b >> 31) && ef >= 30u) return ((u128)((b & 0x7FFFFFu) | 0x800000u)) << (ef - 30u);
-  return (u128)f32_to_fixed(w, FX_CDF);
+  // fast path (2^-97 <= w < 2^98, positive): round(w * 2^120) is an exact
+  // left shift of the 24-bit significand by s = e - 30 (two 64-bit halves)
+  const u32 b = __float_as_uint(w);
+  const u32 ef = (b >> 23) & 0xFFu;
+  if ((b >> 31) || ef < 30u) return cdf_fixed_slow(w);
+  const u64 m = (u64)((b & 0x7FFFFFu) | 0x800000u);
+  const int s = (int)ef - 30;
+  u64 lo, hi;
+  if (s < 40) {          // m << s < 2^64
+    lo = m << s;
+    hi = 0;
+  } else if (s < 64) {
+    lo = m << s;
+    hi = m >> (64 - s);
+  } else {
+    lo = 0;
+    hi = m << (s - 64);
+  }
+  return ((u128)hi << 64) | (u128)lo;
 }
 
 // P <= 2^121 (sum of normalised weights), so 2^-120 * RN64(P) is normal
