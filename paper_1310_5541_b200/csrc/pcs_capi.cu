@@ -680,7 +680,7 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
       default: k_pc_bins<0><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P, T.bins);
     }
     mark();
-    k_sys_resample<1><<<T.rs_grid, SCAN_BLOCK, 0, st>>>(P);
+    k_sys_resample<1><<<T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<1>), st>>>(P);
   } else {
     mark();
     switch (T.maxs) {
@@ -696,7 +696,7 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
     mark();
     k_sir_finalize<<<1, 1, 0, st>>>(P);
     mark();
-    k_sys_resample<2><<<T.rs_grid, SCAN_BLOCK, 0, st>>>(P);
+    k_sys_resample<2><<<T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<2>), st>>>(P);
   }
   if (evs) cudaEventRecord(evs[q], st);
   PCS_LAUNCH_CHECK();
@@ -710,6 +710,10 @@ static int set_attrs() {
   if (g_attr_done) return PCS_OK;
   PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_step1, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)S1_SMEM));
+  PCS_CUDA_TRY(cudaFuncSetAttribute(k_sys_resample<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sizeof(RsSmem<1>)));
+  PCS_CUDA_TRY(cudaFuncSetAttribute(k_sys_resample<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sizeof(RsSmem<2>)));
   PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)BINS_SMEM));
   PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -835,10 +839,12 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
     // k_sys_resample has a grid barrier: every CTA must be co-resident
     int per_sm = 0;
     if (cfg->method == 1)
-      PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sys_resample<1>, SCAN_BLOCK, 0));
+      PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sys_resample<1>, SCAN_BLOCK,
+                                                                 sizeof(RsSmem<1>)));
     else
-      PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sys_resample<2>, SCAN_BLOCK, 0));
-    T.rs_grid = (int)std::min<i64>((i64)ctx->sms * std::max(per_sm, 1), P.ntiles);
+      PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sys_resample<2>, SCAN_BLOCK,
+                                                                 sizeof(RsSmem<2>)));
+    T.rs_grid = (int)std::min<i64>((i64)ctx->sms * std::max(per_sm, 1), ceil_div(n, (i64)RS_TILE));
   }
   // initial cloud (state.py:164-175) and identity ancestors
   pcs_init_t init = cfg->init;

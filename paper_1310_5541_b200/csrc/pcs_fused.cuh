@@ -1017,17 +1017,32 @@ __global__ void __launch_bounds__(SCAN_BLOCK, 4) k_scan_emit(TrackParams P) {
 }
 
 // ===========================================================================
+// first slot at/above the cdf value RN64(Pc) 2^-120 (first_slot_fast(cdf_round(Pc))):
+// float64 estimate from the top 64 bits of Pc, |error| <= n (3 2^-53 + 2^-63)
+// < eps = n 2^-50, exact path otherwise
+__device__ __forceinline__ i64 slot_of_prefix(u128 Pc, double u, i64 ng, double nd, double kappa,
+                                              double eps) {
+  const double t = fma((double)(u64)(Pc >> 57), kappa, -u);
+  const double g = ceil(t);
+  const double gap = g - t;
+  if (gap > eps && gap < 1.0 - eps && g > 0.0 && g < nd) return (i64)g;
+  return first_slot_fast(cdf_round(Pc), u, ng, nd, eps);
+}
+
 // Persistent reduce-then-scan systematic resampling (single GPU, scan_mode 0).
-// Each CTA owns a contiguous range of tiles. Pass 1 sums the exact
-// fixed-point weights of its range; after ONE grid-wide barrier every CTA
-// adds up the aggregates of the CTAs before it (its exact exclusive prefix);
-// pass 2 re-reads its range tile by tile, emits each item's slots and writes
-// the ancestors coalesced. No per-tile look-back chain: the serial latency is
-// one barrier per frame instead of one L2 round trip per 32 predecessor tiles.
-// Requires every CTA to be co-resident (grid = SMs x occupancy, set by the
-// host from the occupancy calculator).
-// ===========================================================================
+// Each CTA owns a contiguous range of tiles (RS_TILE = 3840 particles). Pass
+// 1 sums the exact fixed-point weights of its range; after ONE grid-wide
+// barrier every CTA adds up the aggregates of the CTAs before it (its exact
+// exclusive prefix); pass 2 re-reads its range tile by tile, emits each
+// item's slots and writes the ancestors coalesced. Tiles are streamed into a
+// two-buffer shared-memory ring by TMA bulk copies (cp.async.bulk +
+// mbarrier), so the next tile is in flight while the current one is
+// processed. 15 consecutive items per thread: the stride-15 reads of the
+// dense tile are bank-conflict free. Requires every CTA to be co-resident
+// (grid = SMs x occupancy, set by the host from the occupancy calculator).
 constexpr int RS_MIN_BLOCKS = 3;
+constexpr int RS_ITEMS = 15;
+constexpr int RS_TILE = SCAN_BLOCK * RS_ITEMS;   // 3840
 
 __device__ __forceinline__ void grid_barrier(TrackCtl* C, int nblocks) {
   __syncthreads();
@@ -1045,71 +1060,97 @@ __device__ __forceinline__ void grid_barrier(TrackCtl* C, int nblocks) {
   __syncthreads();
 }
 
-// exact fixed-point weight of staged item k: KIND 1 stages the cell id and
-// reads the per-cell table, KIND 2 stages the float weight
-template <int KIND>
-__device__ __forceinline__ u128 rs_weight(const TrackParams& P, const float* wsh, int k) {
-  if (KIND == 1) {
-    const u32 cell = __float_as_uint(wsh[wpad(k)]);
-    return (cell == 0xFFFFFFFFu) ? (u128)0 : P.wfix[cell];
-  }
-  return cdf_fixed(wsh[wpad(k)]);
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, u32 count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, u32 parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// one thread: arm the barrier with the byte count and start the bulk copy
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, u32 bytes,
+                                            unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
 }
 
-template <int KIND>
-__device__ __forceinline__ u128 rs_load_tile(const TrackParams& P, i64 tile, float* wsh, double m,
-                                             double Sf) {
-  const i64 base = tile * SCAN_TILE;
-#pragma unroll 4
-  for (int q = 0; q < SCAN_ITEMS; ++q) {
-    const i64 i = base + (i64)q * SCAN_BLOCK + threadIdx.x;
-    float w;
-    if (KIND == 1) w = __uint_as_float((i < P.n) ? P.pslot[i] : 0xFFFFFFFFu);
-    else w = (i < P.n) ? normalised_weight(P.ll[i], m, Sf) : 0.0f;
-    wsh[wpad(q * SCAN_BLOCK + threadIdx.x)] = w;
-  }
-  __syncthreads();
-  u128 tsum = 0;
-#pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) tsum += rs_weight<KIND>(P, wsh, threadIdx.x * SCAN_ITEMS + q);
-  return tsum;
-}
+// staged element: KIND 1 the particle's cell id, KIND 2 its log-likelihood
+template <int KIND> struct RsElem { typedef u32 T; };
+template <> struct RsElem<2> { typedef double T; };
 
-// first slot at/above the cdf value RN64(Pc) 2^-120 (first_slot_fast(cdf_round(Pc))):
-// float64 estimate from the top 64 bits of Pc, |error| <= n (3 2^-53 + 2^-63)
-// < eps = n 2^-50, exact path otherwise
-__device__ __forceinline__ i64 slot_of_prefix(u128 Pc, double u, i64 ng, double nd, double kappa,
-                                              double eps) {
-  const double t = fma((double)(u64)(Pc >> 57), kappa, -u);
-  const double g = ceil(t);
-  const double gap = g - t;
-  if (gap > eps && gap < 1.0 - eps && g > 0.0 && g < nd) return (i64)g;
-  return first_slot_fast(cdf_round(Pc), u, ng, nd, eps);
-}
+template <int KIND>
+struct RsSmem {
+  typename RsElem<KIND>::T ring[2][RS_TILE];   // TMA ring (16-byte aligned)
+  int stage[RS_TILE];
+  int hp[RS_TILE];
+  u128 wtot[SCAN_BLOCK / 32];
+  int s_wmax[SCAN_BLOCK / 32];
+  long long s_jr[2];
+  unsigned long long bar[2];
+};
 
 template <int KIND>
 __global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(TrackParams P) {
-  __shared__ float wsh[SCAN_TILE + SCAN_TILE / SCAN_ITEMS];
-  __shared__ int stage[SCAN_TILE + SCAN_TILE / SCAN_ITEMS];
-  __shared__ u128 wtot[SCAN_BLOCK / 32];
-  __shared__ int s_wmax[SCAN_BLOCK / 32];
-  __shared__ long long s_jr[2];
+  typedef typename RsElem<KIND>::T E;
+  extern __shared__ __align__(128) unsigned char rs_raw[];
+  RsSmem<KIND>& sm = *reinterpret_cast<RsSmem<KIND>*>(rs_raw);
+  auto& ring = sm.ring;
+  int* stage = sm.stage;
+  int* hp = sm.hp;
+  u128* wtot = sm.wtot;
+  int* s_wmax = sm.s_wmax;
+  long long* s_jr = sm.s_jr;
+  unsigned long long* bar = sm.bar;
   TrackCtl* C = P.ctl;
-  const i64 n = P.n, nt = P.ntiles;
+  const i64 n = P.n;
+  const i64 nt = ceil_div(n, (i64)RS_TILE);
   const int G = gridDim.x, cta = blockIdx.x;
   const i64 t0 = nt * cta / G, t1 = nt * (cta + 1) / G;
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
   if (!C->do_resample) {   // identity ancestors, weights stay uniform (all equal)
-    for (i64 i = t0 * SCAN_TILE + threadIdx.x; i < min(n, t1 * SCAN_TILE); i += SCAN_BLOCK)
+    for (i64 i = t0 * RS_TILE + threadIdx.x; i < min(n, t1 * RS_TILE); i += SCAN_BLOCK)
       P.anc_out[P.idx_off + i - P.slot_lo] = (int)i;
     return;
   }
   const double m = C->m, Sf = C->Sf, u = C->u;
+  const E* src = (KIND == 1) ? (const E*)(const void*)P.pslot : (const E*)(const void*)P.ll;
+  const int mt = (int)(t1 - t0);      // tiles of this CTA; loads L = 0..2 mt-1 (two passes)
+  auto issue = [&](int L) {           // thread 0 only
+    const i64 tile = t0 + (L % mt);
+    const i64 b0 = tile * RS_TILE;
+    const i64 cnt = min((i64)RS_TILE, n - b0);
+    const u32 bytes = (u32)(((cnt * (i64)sizeof(E)) + 15) & ~(i64)15);
+    tma_load_1d(ring[L & 1], src + b0, bytes, &bar[L & 1]);
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (threadIdx.x == 0 && mt > 0) issue(0);
+  // exact weight of item k of the ring buffer holding tile `b0`
+  auto weight = [&](const E* buf, int k, i64 i) -> u128 {
+    if (i >= n) return 0;
+    if (KIND == 1) return P.wfix[(u32)buf[k]];
+    return cdf_fixed(normalised_weight((double)buf[k], m, Sf));
+  };
   // ---- pass 1: this CTA's exact total ----
   u128 acc = 0;
-  for (i64 tile = t0; tile < t1; ++tile) {
-    acc += rs_load_tile<KIND>(P, tile, wsh, m, Sf);
-    __syncthreads();
+  for (int L = 0; L < mt; ++L) {
+    mbar_wait(&bar[L & 1], (u32)((L >> 1) & 1));
+    if (threadIdx.x == 0 && L + 1 < 2 * mt) issue(L + 1);
+    const E* buf = ring[L & 1];
+    const i64 i0 = (t0 + L) * RS_TILE + (i64)threadIdx.x * RS_ITEMS;
+#pragma unroll 5
+    for (int q = 0; q < RS_ITEMS; ++q) acc += weight(buf, threadIdx.x * RS_ITEMS + q, i0 + q);
+    __syncthreads();   // buffer L & 1 is free for load L + 2
   }
   {
     u128 v = acc;
@@ -1138,7 +1179,6 @@ __global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(Trac
       const u64 lo = (u64)v, hi = (u64)(v >> 64);
       v += ((u128)__shfl_xor_sync(0xffffffffu, hi, o) << 64) | (u128)__shfl_xor_sync(0xffffffffu, lo, o);
     }
-    __syncthreads();
     if (lane == 0) wtot[wi] = v;
     __syncthreads();
     pre = 0;
@@ -1150,10 +1190,16 @@ __global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(Trac
   const double nd = (double)ng, eps = nd * 8.881784197001252e-16;   // n * 2^-50
   const double kappa = nd * 1.0842021724855044e-19;                  // n * 2^-63
   bool oob = false;
-  int* hp = reinterpret_cast<int*>(wsh);
-  for (i64 tile = t0; tile < t1; ++tile) {
-    const i64 base = tile * SCAN_TILE;
-    const u128 tsum = rs_load_tile<KIND>(P, tile, wsh, m, Sf);
+  const int k0 = (int)threadIdx.x * RS_ITEMS;
+  for (int L = mt; L < 2 * mt; ++L) {
+    mbar_wait(&bar[L & 1], (u32)((L >> 1) & 1));
+    if (threadIdx.x == 0 && L + 1 < 2 * mt) issue(L + 1);
+    const E* buf = ring[L & 1];
+    const i64 base = (t0 + (L - mt)) * RS_TILE;
+    const i64 i0 = base + k0;
+    u128 tsum = 0;
+#pragma unroll 5
+    for (int q = 0; q < RS_ITEMS; ++q) tsum += weight(buf, k0 + q, i0 + q);
     u128 inc = tsum;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -1169,9 +1215,8 @@ __global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(Trac
       tagg += wtot[w];
     }
     const u128 excl = pre + woff + (inc - tsum);
-    const i64 i0 = base + (i64)threadIdx.x * SCAN_ITEMS;
     if (threadIdx.x == 0) {
-      const i64 tl = min(n, base + (i64)SCAN_TILE) - 1;
+      const i64 tl = min(n, base + (i64)RS_TILE) - 1;
       s_jr[0] = (off + base == 0) ? 0 : first_slot_fast(cdf_round(pre), u, ng, nd, eps);
       s_jr[1] = (off + tl == ng - 1) ? ng : first_slot_fast(cdf_round(pre + tagg), u, ng, nd, eps);
     }
@@ -1179,42 +1224,38 @@ __global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(Trac
     const i64 tj0 = s_jr[0], tj1 = s_jr[1];
     // run head of every item: its first slot relative to tj0, INT_MAX if none
     {
-      const int k0 = (int)threadIdx.x * SCAN_ITEMS;
       int jr = 0;
-      if (i0 < n)
-        jr = (int)(((off + i0 == 0) ? 0 : slot_of_prefix(excl, u, ng, nd, kappa, eps)) - tj0);
+      if (i0 < n) jr = (int)(((off + i0 == 0) ? 0 : slot_of_prefix(excl, u, ng, nd, kappa, eps)) - tj0);
       u128 run = excl;
-      for (int q = 0; q < SCAN_ITEMS; ++q) {
+      for (int q = 0; q < RS_ITEMS; ++q) {
         const i64 i = i0 + q;
         int h = INT_MAX;
         if (i < n) {
-          run += rs_weight<KIND>(P, wsh, k0 + q);
-          const int jend =
-              (int)(((off + i == ng - 1) ? ng : slot_of_prefix(run, u, ng, nd, kappa, eps)) - tj0);
+          run += weight(buf, k0 + q, i);
+          const int jend = (int)(((off + i == ng - 1) ? ng : slot_of_prefix(run, u, ng, nd, kappa, eps)) - tj0);
           if (jend > jr) h = jr;
           jr = jend;
         }
-        hp[wpad(k0 + q)] = h;
+        hp[k0 + q] = h;
       }
     }
-    __syncthreads();
-    // slots in chunks of SCAN_TILE: heads, block max-scan, coalesced writes
+    __syncthreads();   // every read of ring[L & 1] is done; it is free for load L + 2
+    // slots in chunks of RS_TILE: heads, block max-scan, coalesced writes
     const i64 m_slots = tj1 - tj0;
     int carry = -1;
-    for (i64 c0 = 0; c0 < m_slots; c0 += SCAN_TILE) {
-      const int k0 = (int)threadIdx.x * SCAN_ITEMS;
+    for (i64 c0 = 0; c0 < m_slots; c0 += RS_TILE) {
 #pragma unroll
-      for (int q = 0; q < SCAN_ITEMS; ++q) stage[wpad(k0 + q)] = -1;
+      for (int q = 0; q < RS_ITEMS; ++q) stage[k0 + q] = -1;
       __syncthreads();
 #pragma unroll
-      for (int q = 0; q < SCAN_ITEMS; ++q) {
-        const int h = hp[wpad(k0 + q)];
-        if ((i64)h >= c0 && (i64)h < c0 + SCAN_TILE) stage[wpad((int)((i64)h - c0))] = k0 + q;
+      for (int q = 0; q < RS_ITEMS; ++q) {
+        const int h = hp[k0 + q];
+        if ((i64)h >= c0 && (i64)h < c0 + RS_TILE) stage[(int)((i64)h - c0)] = k0 + q;
       }
       __syncthreads();
       int tmax = -1;
 #pragma unroll
-      for (int q = 0; q < SCAN_ITEMS; ++q) tmax = max(tmax, stage[wpad(k0 + q)]);
+      for (int q = 0; q < RS_ITEMS; ++q) tmax = max(tmax, stage[k0 + q]);
       int incl = tmax;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -1233,15 +1274,15 @@ __global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(Trac
       }
       int runm = max(prev, excl_l);
 #pragma unroll
-      for (int q = 0; q < SCAN_ITEMS; ++q) {
-        runm = max(runm, stage[wpad(k0 + q)]);
-        stage[wpad(k0 + q)] = runm;
+      for (int q = 0; q < RS_ITEMS; ++q) {
+        runm = max(runm, stage[k0 + q]);
+        stage[k0 + q] = runm;
       }
       __syncthreads();
-      const int cm = (int)min((i64)SCAN_TILE, m_slots - c0);
+      const int cm = (int)min((i64)RS_TILE, m_slots - c0);
       for (int k = threadIdx.x; k < cm; k += SCAN_BLOCK) {
         const i64 kk = tj0 + c0 + k - lo;
-        if (kk >= 0 && kk < cap) P.anc_out[kk] = (int)(base + stage[wpad(k)]);
+        if (kk >= 0 && kk < cap) P.anc_out[kk] = (int)(base + stage[k]);
         else oob = true;
       }
       carry = total;
