@@ -816,7 +816,7 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
       ctx->table_cells = P.G;
       ctx->table_dirty = true;
     }
-    if (!ctx->occ) PCS_CUDA_TRY(cudaMalloc(&ctx->occ, MAXM * sizeof(u32) + 3 * BINS_MAXM * sizeof(float)));
+    if (!ctx->occ) PCS_CUDA_TRY(cudaMalloc(&ctx->occ, MAXM * sizeof(u32) + 5 * BINS_MAXM * sizeof(float)));
     if (ctx->table_dirty) {
       PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_cnt, 0, ctx->table_cells * sizeof(u32), st));
       PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_sum, 0, 5 * ctx->table_cells * 2 * sizeof(u64), st));
@@ -831,10 +831,18 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
     T.bins.dx = sd;
     T.bins.dy = sd + BINS_MAXM;
     T.bins.di = sd + 2 * BINS_MAXM;
+    T.bins.cnt = (u32*)(sd + 3 * BINS_MAXM);
+    T.bins.cell = (u32*)(sd + 4 * BINS_MAXM);
   }
   T.maxs = maxs_for(cfg->spot.halfwidth);
   T.prop_grid = grid_for(n, 256, ctx->sms, 8);
   T.s1_grid = (int)std::min<i64>(ctx->sms, ceil_div(n, S1_TILE));
+  {
+    // equal tile counts per CTA: tile = ceil(per_cta / ceil(per_cta / S1_TILE))
+    const i64 per_cta = ceil_div(n, (i64)T.s1_grid);
+    const i64 tpc = ceil_div(per_cta, (i64)S1_TILE);
+    P.s1_tile = (int)std::max<i64>(32, ceil_div(per_cta, tpc));
+  }
   {
     // k_sys_resample has a grid barrier: every CTA must be co-resident
     int per_sm = 0;

@@ -161,6 +161,25 @@ __device__ __forceinline__ void atomic_add_i128(u64* p, i128 v) {
   if (vhi) atomicAdd(p + 1, vhi);
 }
 
+// five int128 atomic adds at p0 + c * stride (c = 0..4): the five low-word
+// atomics are issued back to back (one round trip), then the high words with
+// their carries
+__device__ __forceinline__ void atomic_add_i128_x5(u64* p0, i64 stride, const i128 (&v)[5]) {
+  u64 old[5];
+#pragma unroll
+  for (int c = 0; c < 5; ++c) {
+    const u64 vlo = (u64)v[c];
+    old[c] = vlo ? atomicAdd(p0 + c * stride, vlo) : 0ull;
+  }
+#pragma unroll
+  for (int c = 0; c < 5; ++c) {
+    const u64 vlo = (u64)v[c];
+    u64 vhi = (u64)((u128)v[c] >> 64);
+    if (vlo && old[c] + vlo < old[c]) vhi += 1ull;
+    if (vhi) atomicAdd(p0 + c * stride + 1, vhi);
+  }
+}
+
 __device__ __forceinline__ i128 load_i128(const u64* p) {
   return (i128)(((u128)p[1] << 64) | (u128)p[0]);
 }

@@ -126,6 +126,7 @@ struct TrackParams {
   i64 slot_cap;              // capacity of anc_out
   int* anc_out;              // ancestors (local particle index) for slots slot_lo + k
   int scan_mode;             // 0 scan+emit, 1 scan only, 2 emit only (rank prefix in ctl)
+  int s1_tile;               // k_pc_step1 tile (<= S1_TILE), balanced over its CTAs
   u128* cta_agg;             // k_sys_resample: per-CTA exact weight totals
 };
 
@@ -307,18 +308,19 @@ __device__ __forceinline__ void s1_flush(const TrackParams& P, TrackCtl* C, S1Sm
     const u32 cnt = sm.cnt[q];
     const int qx = q % snx, qy = q / snx;
     const u32 flat = (u32)((sy0 + qy) * g.ncols + (sx0 + qx));
-    touch_cell(P, C, flat, cnt);
+    i128 s[5];
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
-      i128 s = (i128)sm.dig[3 * c][q] + ((i128)sm.dig[3 * c + 1][q] << 18) +
-               ((i128)(int)sm.dig[3 * c + 2][q] << 36);
-      if (c == 0) s += (i128)cnt * f32_to_fixed(sm.ref[qx], FX_STATE);
-      if (c == 1) s += (i128)cnt * f32_to_fixed(sm.ref[snx + qy], FX_STATE);
-      atomic_add_i128(P.tab_sum + ((i64)c * P.G + flat) * 2, s);
+      s[c] = (i128)sm.dig[3 * c][q] + ((i128)sm.dig[3 * c + 1][q] << 18) +
+             ((i128)(int)sm.dig[3 * c + 2][q] << 36);
       sm.dig[3 * c][q] = 0;
       sm.dig[3 * c + 1][q] = 0;
       sm.dig[3 * c + 2][q] = 0;
     }
+    s[0] += (i128)cnt * f32_to_fixed(sm.ref[qx], FX_STATE);
+    s[1] += (i128)cnt * f32_to_fixed(sm.ref[snx + qy], FX_STATE);
+    atomic_add_i128_x5(P.tab_sum + (i64)flat * 2, P.G * 2, s);
+    touch_cell(P, C, flat, cnt);
     sm.cnt[q] = 0;
   }
 }
@@ -334,7 +336,10 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
   float* sout = (k & 1) ? P.buf0 : P.buf1;
   const Grid g = P.grid;
   const i64 n = P.n, ld = P.ld;
-  const i64 ntile = ceil_div(n, S1_TILE);
+  // runtime tile (<= S1_TILE) chosen by the host so that every CTA gets the
+  // same number of tiles (no tail CTA with one extra tile)
+  const int TT = P.s1_tile;
+  const i64 ntile = ceil_div(n, (i64)TT);
   const i64 tstep = gridDim.x;
 
   // sub-window (identical in every CTA): centred on the previous estimate
@@ -383,20 +388,20 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
     int src_k[S1_IPT];
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {   // every gather before any arithmetic
-      const i64 j = tile * S1_TILE + (i64)it * S1_THREADS + t;
-      src_k[it] = (j < n) ? __ldg(P.anc + j) : 0;
+      const int l = it * S1_THREADS + t;
+      const i64 j = tile * TT + l;
+      src_k[it] = (l < TT && j < n) ? __ldg(P.anc + j) : -1;
     }
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {
-      const i64 j = tile * S1_TILE + (i64)it * S1_THREADS + t;
 #pragma unroll
-      for (int c = 0; c < 5; ++c) o_k[it][c] = (j < n) ? __ldg(sin + c * ld + src_k[it]) : 0.0f;
+      for (int c = 0; c < 5; ++c) o_k[it][c] = (src_k[it] >= 0) ? __ldg(sin + c * ld + src_k[it]) : 0.0f;
     }
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {
       q_k[it] = -1;
-      const i64 j = tile * S1_TILE + (i64)it * S1_THREADS + t;
-      if (j >= n) continue;
+      const i64 j = tile * TT + it * S1_THREADS + t;
+      if (src_k[it] < 0) continue;
       float s[5], z[5];
 #pragma unroll
       for (int c = 0; c < 5; ++c) s[c] = o_k[it][c];
@@ -424,10 +429,11 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
         o[1] = dy;
       } else {
         // outside the shared sub-window: exact int128 atomics straight to HBM
-        touch_cell(P, C, flat, 1u);
+        i128 v[5];
 #pragma unroll
-        for (int c = 0; c < 5; ++c)
-          atomic_add_i128(P.tab_sum + ((i64)c * P.G + flat) * 2, f32_to_fixed(o[c], FX_STATE));
+        for (int c = 0; c < 5; ++c) v[c] = f32_to_fixed(o[c], FX_STATE);
+        atomic_add_i128_x5(P.tab_sum + (i64)flat * 2, P.G * 2, v);
+        touch_cell(P, C, flat, 1u);
       }
     }
     __syncthreads();
@@ -561,9 +567,12 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
 }
 
 // ===========================================================================
-// pcSIR bins (one CTA): dummies, likelihood per occupied cell (one warp per
-// cell, pixels across lanes), normaliser, per-cell weights, estimate, ESS,
-// resampling decision. Zeroes the consumed table cells.
+// pcSIR bins (one CTA): dummies, likelihood per occupied cell ((cell, row)
+// parallel), normaliser, per-cell weights, estimate, ESS, resampling
+// decision. Zeroes the consumed table cells. Latency-bound by design (a few
+// hundred cells): everything per cell stays in shared memory, each exact
+// reduction is warp shuffles + one barrier + a warp-parallel final sum, and
+// the control-block reads of the epilogue are issued at kernel entry.
 // ===========================================================================
 constexpr int BINS_BLOCK = 1024;
 #define PCS_PROBE(i)                                                                  \
@@ -575,47 +584,100 @@ constexpr int BINS_BLOCK = 1024;
     }                                                                                 \
   } while (0)
 constexpr int BINS_MAXM = 8192;              // occupied cells handled by the fused bins kernel
-constexpr int STAGE_PIX = 12288;             // staged frame tile (48 KB)
+constexpr int BINS_SM = 4096;                // ... of which kept in shared memory
+constexpr int STAGE_PIX = 11264;             // staged frame tile (44 KB)
 constexpr int ROWBUF = 4096;                 // (cell, row) partials per chunk (32 KB)
-constexpr size_t BINS_SMEM =
-    BINS_MAXM * sizeof(double) + STAGE_PIX * sizeof(float) + ROWBUF * sizeof(double);
+struct BinsSmem {
+  double ll[BINS_MAXM];
+  double row[ROWBUF];
+  float pix[STAGE_PIX];
+  float dx[BINS_SM], dy[BINS_SM], di[BINS_SM];
+  u32 cnt[BINS_SM];
+  u32 cell[BINS_SM];
+  i128 red[BINS_BLOCK / 32 * 6];
+};
+constexpr size_t BINS_SMEM = sizeof(BinsSmem);
 
-struct BinsScratch {  // global scratch for the dummies of the occupied cells
+struct BinsScratch {  // per-cell values of occupied cells b >= BINS_SM (global memory)
   float* dx;
   float* dy;
   float* di;
+  u32* cnt;
+  u32* cell;
 };
+
+// per-cell record b: shared memory for b < BINS_SM, global scratch beyond
+struct BinsView {
+  BinsSmem& sm;
+  const BinsScratch& g;
+  __device__ __forceinline__ float& dx(int b) const { return b < BINS_SM ? sm.dx[b] : g.dx[b]; }
+  __device__ __forceinline__ float& dy(int b) const { return b < BINS_SM ? sm.dy[b] : g.dy[b]; }
+  __device__ __forceinline__ float& di(int b) const { return b < BINS_SM ? sm.di[b] : g.di[b]; }
+  __device__ __forceinline__ u32& cnt(int b) const { return b < BINS_SM ? sm.cnt[b] : g.cnt[b]; }
+  __device__ __forceinline__ u32& cell(int b) const { return b < BINS_SM ? sm.cell[b] : g.cell[b]; }
+};
+
+// K exact sums over the block: warp shuffles, one barrier, then warp 0 sums
+// the 32 warp partials with shuffles; the results are valid in warp 0
+template <int K>
+__device__ __forceinline__ void bins_sum_k(i128 (&v)[K], i128* sh) {
+#pragma unroll
+  for (int c = 0; c < K; ++c) v[c] = warp_sum_i128(v[c]);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) sh[w * K + c] = v[c];
+  }
+  __syncthreads();
+  if (w == 0) {
+#pragma unroll
+    for (int c = 0; c < K; ++c) v[c] = warp_sum_i128((l < BINS_BLOCK / 32) ? sh[l * K + c] : (i128)0);
+  }
+}
 
 template <int MAXS>
 __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScratch Sd) {
   TrackCtl* C = P.ctl;
   PCS_PROBE(8);
   extern __shared__ __align__(16) unsigned char bins_raw[];
-  double* s_ll = reinterpret_cast<double*>(bins_raw);
-  float* s_pix = reinterpret_cast<float*>(bins_raw + BINS_MAXM * sizeof(double));
-  double* s_row = reinterpret_cast<double*>(bins_raw + BINS_MAXM * sizeof(double) +
-                                            STAGE_PIX * sizeof(float));
-  __shared__ i128 s_red[BINS_BLOCK / 32];
-  __shared__ i128 s_red6[BINS_BLOCK / 32 * 6];
+  BinsSmem& sm = *reinterpret_cast<BinsSmem*>(bins_raw);
+  const BinsView V{sm, Sd};
   __shared__ long long s_max;
   __shared__ unsigned s_wmin, s_wmax;
   __shared__ int s_box[4];
   __shared__ double s_Sf;
   const int t = threadIdx.x;
   const i64 k = C->k;
-  const i64 ko = k - C->k_out;
   const u32 nocc = C->n_occ;
   if ((C->flags & PCS_FLAG_CAPACITY) || nocc > (u32)BINS_MAXM) {
     if (t == 0) {
       set_flag(C, PCS_FLAG_CAPACITY);
       C->do_resample = 0;
-      C->out_occ[ko] = -1;
+      C->out_occ[k - C->k_out] = -1;
       reset_frame(C);
       C->k = k + 1;
     }
     return;
   }
   const int M = (int)nocc;
+  // epilogue inputs, read now so that their latency overlaps the work
+  i64 ko = 0;
+  double* out_est = nullptr;
+  double* out_ess = nullptr;
+  unsigned char* out_res = nullptr;
+  i64* out_occ = nullptr;
+  double u_next = 0.0;
+  i64 evals = 0;
+  if (t == 0) {
+    evals = C->evals;
+    ko = k - C->k_out;
+    out_est = C->out_est;
+    out_ess = C->out_ess;
+    out_res = C->out_res;
+    out_occ = C->out_occ;
+    u_next = philox_resample_u(P.seed, P.frame0 + (u32)k);
+  }
   const float* frame = C->frames + (k - C->k_frames) * P.H * P.W;
   PCS_PROBE(0);
   if (t == 0) {
@@ -628,22 +690,24 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   // 1) dummies (exact means, binning.py:157-172) and the union of their windows
   int bx0 = INT_MAX, bx1 = INT_MIN, by0 = INT_MAX, by1 = INT_MIN;
   for (int b = t; b < M; b += BINS_BLOCK) {
-    u32 cell = P.occ[b];
-    u32 cnt = P.tab_cnt[cell];
+    const u32 cell = P.occ[b];
+    const u32 cnt = P.tab_cnt[cell];
     float d[5];
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
-      double num = i128_to_f64_rn(load_i128(P.tab_sum + ((i64)c * P.G + cell) * 2));
+      const double num = i128_to_f64_rn(load_i128(P.tab_sum + ((i64)c * P.G + cell) * 2));
       d[c] = __double2float_rn(scalbn(__ddiv_rn(num, (double)cnt), -FX_STATE));
     }
     if (P.placement == 1) {  // cell centre (binning.py:168-171)
-      i64 ix = (i64)cell % P.grid.ncols, iy = (i64)cell / P.grid.ncols;
+      const i64 ix = (i64)cell % P.grid.ncols, iy = (i64)cell / P.grid.ncols;
       d[0] = __double2float_rn(__dadd_rn(P.grid.ox, __dmul_rn((double)ix + 0.5, P.grid.lx)));
       d[1] = __double2float_rn(__dadd_rn(P.grid.oy, __dmul_rn((double)iy + 0.5, P.grid.ly)));
     }
-    Sd.dx[b] = d[0];
-    Sd.dy[b] = d[1];
-    Sd.di[b] = d[4];
+    V.dx(b) = d[0];
+    V.dy(b) = d[1];
+    V.di(b) = d[4];
+    V.cnt(b) = cnt;
+    V.cell(b) = cell;
     if (d[0] == d[0] && d[1] == d[1]) {
       int xlo, xhi, ylo, yhi;
       window_of(d[0], d[1], P.spot, P.H, P.W, xlo, xhi, ylo, yhi);
@@ -657,14 +721,14 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   // 2) stage the frame region covering every window in shared memory
   PixView pv = frame_view(frame, P.H, P.W);
   {
-    int x0 = s_box[0], y0 = s_box[2];
-    i64 wx = (i64)s_box[1] - x0 + 1, wy = (i64)s_box[3] - y0 + 1;
+    const int x0 = s_box[0], y0 = s_box[2];
+    const i64 wx = (i64)s_box[1] - x0 + 1, wy = (i64)s_box[3] - y0 + 1;
     if (s_box[1] >= s_box[0] && wx * wy <= STAGE_PIX) {
       for (int p = t; p < (int)(wx * wy); p += BINS_BLOCK) {
-        int yy = p / (int)wx, xx = p % (int)wx;
-        s_pix[p] = __ldg(frame + (i64)(y0 + yy) * P.W + (x0 + xx));
+        const int yy = p / (int)wx, xx = p % (int)wx;
+        sm.pix[p] = __ldg(frame + (i64)(y0 + yy) * P.W + (x0 + xx));
       }
-      pv.base = s_pix;
+      pv.base = sm.pix;
       pv.pitch = wx;
       pv.x0 = x0;
       pv.y0 = y0;
@@ -678,24 +742,24 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   long long lmax = LLONG_MIN;
   {
     const int S = 2 * P.spot.hw + 1;
-    const int C = ROWBUF / S;   // cells per chunk
-    for (int b0 = 0; b0 < M; b0 += C) {
-      const int nb = min(C, M - b0);
+    const int CH = ROWBUF / S;   // cells per chunk
+    for (int b0 = 0; b0 < M; b0 += CH) {
+      const int nb = min(CH, M - b0);
       for (int it = t; it < nb * S; it += BINS_BLOCK) {
-        int b = b0 + it / S, j = it % S;
-        float x = Sd.dx[b], y = Sd.dy[b], i0 = Sd.di[b];
+        const int b = b0 + it / S, j = it % S;
+        const float x = V.dx(b), y = V.dy(b), i0 = V.di(b);
         double part = 0.0;
         if (x == x && y == y && i0 == i0) {
           int xlo, xhi, ylo, yhi;
           window_of(x, y, P.spot, P.H, P.W, xlo, xhi, ylo, yhi);
           if (j <= yhi - ylo) part = loglik_row(pv, x, y, i0, P.spot, xlo, xhi - xlo + 1, ylo + j);
         }
-        s_row[it] = part;
+        sm.row[it] = part;
       }
       __syncthreads();
       for (int bb = t; bb < nb; bb += BINS_BLOCK) {
-        int b = b0 + bb;
-        float x = Sd.dx[b], y = Sd.dy[b], i0 = Sd.di[b];
+        const int b = b0 + bb;
+        const float x = V.dx(b), y = V.dy(b), i0 = V.di(b);
         double ll;
         if (!(x == x) || !(y == y) || !(i0 == i0)) {
           ll = nan_ll();
@@ -703,10 +767,10 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
           int xlo, xhi, ylo, yhi;
           window_of(x, y, P.spot, P.H, P.W, xlo, xhi, ylo, yhi);
           double tot = 0.0;
-          for (int j = 0; j <= yhi - ylo; ++j) tot += s_row[bb * S + j];
+          for (int j = 0; j <= yhi - ylo; ++j) tot += sm.row[bb * S + j];
           ll = (P.spot.model == 0) ? -tot * P.spot.inv_2sxi2 : tot;
         }
-        s_ll[b] = ll;
+        sm.ll[b] = ll;
         lmax = max(lmax, (long long)f64_to_ordered(ll));
       }
       __syncthreads();
@@ -719,63 +783,67 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   const bool degenerate = (m == -INFINITY);
   PCS_PROBE(3);
   // 4) normaliser S = sum_b cnt_b * round(exp(ll_b - m) * 2^95)
-  i128 acc = 0;
-  for (int b = t; b < M; b += BINS_BLOCK) {
-    u32 cnt = P.tab_cnt[P.occ[b]];
-    acc += (i128)cnt * f64_to_fixed(exp(__dsub_rn(s_ll[b], m)), FX_S);
+  {
+    i128 acc[1] = {0};
+    for (int b = t; b < M; b += BINS_BLOCK)
+      acc[0] += (i128)V.cnt(b) * f64_to_fixed(exp(__dsub_rn(sm.ll[b], m)), FX_S);
+    bins_sum_k<1>(acc, sm.red);
+    if (t == 0) s_Sf = scalbn(i128_to_f64_rn(acc[0]), -FX_S);
+    __syncthreads();
   }
-  i128 Sfix = block_sum_i128<BINS_BLOCK>(acc, s_red);
-  if (t == 0) s_Sf = scalbn(i128_to_f64_rn(Sfix), -FX_S);
-  __syncthreads();
   const double Sf = s_Sf;
   PCS_PROBE(4);
   // 5) weights per cell (broadcast table), estimate, ESS; zero consumed cells
   i128 e[6] = {0, 0, 0, 0, 0, 0};
-  for (int b = t; b < M; b += BINS_BLOCK) {
-    u32 cell = P.occ[b];
-    u32 cnt = P.tab_cnt[cell];
-    float w = normalised_weight(s_ll[b], m, Sf);
-    P.wtab[cell] = w;
-    P.wfix[cell] = cdf_fixed(w);
-    atomicMin(&s_wmin, __float_as_uint(w));
-    atomicMax(&s_wmax, __float_as_uint(w));
-    i128 wq = f32_to_fixed(w, FX_WQ);
+  {
+    unsigned wmin = 0xFFFFFFFFu, wmax = 0u;
+    for (int b = t; b < M; b += BINS_BLOCK) {
+      const u32 cell = V.cell(b);
+      const u32 cnt = V.cnt(b);
+      const float w = normalised_weight(sm.ll[b], m, Sf);
+      P.wtab[cell] = w;
+      P.wfix[cell] = cdf_fixed(w);
+      wmin = min(wmin, __float_as_uint(w));
+      wmax = max(wmax, __float_as_uint(w));
+      const i128 wq = f32_to_fixed(w, FX_WQ);
 #pragma unroll
-    for (int c = 0; c < 5; ++c) {
-      u64* p = P.tab_sum + ((i64)c * P.G + cell) * 2;
-      e[c] += wq * load_i128(p);
-      p[0] = 0;
-      p[1] = 0;
+      for (int c = 0; c < 5; ++c) {
+        u64* p = P.tab_sum + ((i64)c * P.G + cell) * 2;
+        e[c] += wq * load_i128(p);
+        p[0] = 0;
+        p[1] = 0;
+      }
+      e[5] += (i128)cnt * f64_to_fixed((double)w * (double)w, FX_W2);
+      P.tab_cnt[cell] = 0;
     }
-    e[5] += (i128)cnt * f64_to_fixed((double)w * (double)w, FX_W2);
-    P.tab_cnt[cell] = 0;
+    atomicMin(&s_wmin, wmin);
+    atomicMax(&s_wmax, wmax);
   }
-  double est[5];
-  double w2f = 0;
   PCS_PROBE(5);
-  block_sum_i128_k<BINS_BLOCK, 6>(e, s_red6);
+  bins_sum_k<6>(e, sm.red);
   PCS_PROBE(6);
   if (t == 0) {
+    double est[5];
 #pragma unroll
     for (int c = 0; c < 5; ++c) est[c] = scalbn(i128_to_f64_rn(e[c]), -(FX_WQ + FX_STATE));
-    w2f = scalbn(i128_to_f64_rn(e[5]), -FX_W2);
-    double ess = 1.0 / w2f;
-    bool flag_bad = degenerate || bad_m;
+    const double w2f = scalbn(i128_to_f64_rn(e[5]), -FX_W2);
+    const double ess = 1.0 / w2f;
+    const bool flag_bad = degenerate || bad_m;
     if (degenerate) set_flag(C, PCS_FLAG_DEGENERATE);
     if (bad_m) set_flag(C, PCS_FLAG_NONFINITE);
-    for (int c = 0; c < 5; ++c) C->out_est[ko * 5 + c] = est[c];
-    C->out_ess[ko] = ess;
-    int res = (!flag_bad && ess < (double)P.n) ? 1 : 0;   // threshold_fraction = 1.0
+    for (int c = 0; c < 5; ++c) out_est[ko * 5 + c] = est[c];
+    out_ess[ko] = ess;
+    const int res = (!flag_bad && ess < (double)P.n) ? 1 : 0;   // threshold_fraction = 1.0
     // no resampling with unequal weights -> non-uniform prior next frame:
     // only the general path carries per-particle prior weights
     if (!res && !flag_bad && s_wmin != s_wmax) set_flag(C, PCS_FLAG_CAPACITY);
-    C->out_res[ko] = (unsigned char)res;
-    C->out_occ[ko] = M;
-    C->evals += M;
+    out_res[ko] = (unsigned char)res;
+    out_occ[ko] = M;
+    C->evals = evals + M;
     C->do_resample = res;
     C->m = m;
     C->Sf = Sf;
-    C->u = philox_resample_u(P.seed, P.frame0 + (u32)k);
+    C->u = u_next;
     if (!flag_bad) {
       C->center[0] = est[0];
       C->center[1] = est[1];
