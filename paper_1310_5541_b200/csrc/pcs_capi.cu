@@ -655,6 +655,27 @@ __global__ void k_ctl_io(TrackCtl* C, const float* frames, i64 kf, i64 ko, doubl
   C->out_occ = occ;
 }
 
+// launch with the programmatic-stream-serialization attribute (PDL): the
+// kernel may be scheduled before its predecessor in the stream has drained;
+// it calls griddepcontrol.wait before consuming the predecessor's results
+extern "C++" {
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+}  // extern "C++"
+
 static const char* kPcNames[] = {"k_pc_step1", "k_pc_bins", "k_sys_resample"};
 static const char* kSirNames[] = {"k_sir_propagate_lik", "k_sir_sum", "k_sir_stats",
                                   "k_sir_finalize", "k_sys_resample"};
@@ -674,13 +695,13 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
     k_pc_step1<<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(P);
     mark();
     switch (T.maxs) {
-      case 9: k_pc_bins<9><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P, T.bins); break;
-      case 11: k_pc_bins<11><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P, T.bins); break;
-      case 15: k_pc_bins<15><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P, T.bins); break;
-      default: k_pc_bins<0><<<1, BINS_BLOCK, BINS_SMEM, st>>>(P, T.bins);
+      case 9: launch_pdl(k_pc_bins<9>, 1, BINS_BLOCK, BINS_SMEM, st, P, T.bins); break;
+      case 11: launch_pdl(k_pc_bins<11>, 1, BINS_BLOCK, BINS_SMEM, st, P, T.bins); break;
+      case 15: launch_pdl(k_pc_bins<15>, 1, BINS_BLOCK, BINS_SMEM, st, P, T.bins); break;
+      default: launch_pdl(k_pc_bins<0>, 1, BINS_BLOCK, BINS_SMEM, st, P, T.bins);
     }
     mark();
-    k_sys_resample<1><<<T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<1>), st>>>(P);
+    launch_pdl(k_sys_resample<1>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<1>), st, P);
   } else {
     mark();
     switch (T.maxs) {
@@ -696,7 +717,7 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
     mark();
     k_sir_finalize<<<1, 1, 0, st>>>(P);
     mark();
-    k_sys_resample<2><<<T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<2>), st>>>(P);
+    launch_pdl(k_sys_resample<2>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<2>), st, P);
   }
   if (evs) cudaEventRecord(evs[q], st);
   PCS_LAUNCH_CHECK();

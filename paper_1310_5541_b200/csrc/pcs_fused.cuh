@@ -130,6 +130,15 @@ struct TrackParams {
   u128* cta_agg;             // k_sys_resample: per-CTA exact weight totals
 };
 
+// Programmatic dependent launch: the frame's kernels are launched with the
+// programmatic-serialization attribute, so the next kernel is scheduled while
+// the current one drains; it waits here for the previous grid (complete and
+// visible) before touching its results.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ void set_flag(TrackCtl* c, u32 f) {
   atomicOr(&c->flags, f);
   atomicMin(&c->first_bad, (int)c->k);
@@ -329,6 +338,7 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
   extern __shared__ __align__(16) unsigned char s1_raw[];
   S1Smem& sm = *reinterpret_cast<S1Smem*>(s1_raw);
   TrackCtl* C = P.ctl;
+  pdl_trigger();
   if (C->flags & PCS_FLAG_CAPACITY) return;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   const i64 k = C->k;
@@ -639,6 +649,8 @@ __device__ __forceinline__ void bins_sum_k(i128 (&v)[K], i128* sh) {
 template <int MAXS>
 __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScratch Sd) {
   TrackCtl* C = P.ctl;
+  pdl_wait();
+  pdl_trigger();   // k_sys_resample CTAs may become resident on the other SMs
   PCS_PROBE(8);
   extern __shared__ __align__(16) unsigned char bins_raw[];
   BinsSmem& sm = *reinterpret_cast<BinsSmem*>(bins_raw);
@@ -1176,6 +1188,8 @@ __global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(Trac
   long long* s_jr = sm.s_jr;
   unsigned long long* bar = sm.bar;
   TrackCtl* C = P.ctl;
+  pdl_wait();   // (no early trigger here: the next frame's step 1 must not
+                // take SMs that CTAs of this grid-barrier kernel still need)
   const i64 n = P.n;
   const i64 nt = ceil_div(n, (i64)RS_TILE);
   const int G = gridDim.x, cta = blockIdx.x;

@@ -17,7 +17,8 @@ cpp = float(sys.argv[1]) if len(sys.argv) > 1 else 1.0
 wl = bench.WORKLOADS["c2"]
 frames, _ = bench.frames_for(wl["width"], 8, wl["start"])
 dev = torch.from_numpy(frames).cuda()
-cfg, grid = bench.make_cfg(pc, wl, cpp, 1)
+n = int(sys.argv[2]) if len(sys.argv) > 2 else wl["n"]
+cfg, grid = bench.make_cfg(pc, wl, cpp, n)
 c = bench.c_cfg(pc, _lib, cfg, grid, 1, use_graph=False)
 st = _lib.stream()
 _lib.check(_lib.lib().pcs_track_begin(_lib.ctx(), ctypes.byref(c), 256, 256, st))
