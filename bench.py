@@ -214,6 +214,22 @@ def run_fused(torch, pc, _lib, cfg, grid, dev_frames, warmup, steps, seed, flush
                     launches=int(_lib.lib().pcs_track_launches_per_step(_lib.ctx())))
 
 
+def measured_traffic(wl_name, variant, kernel, n):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` from
+    the committed ncu --set full capture (profiles/traffic.json), scaled to
+    this run's N when the capture used a smaller N; None if not captured."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            tab = json.load(f)
+    except (OSError, ValueError):
+        return None
+    rec = tab.get(f"{wl_name}:{variant}", {}).get(kernel)
+    if not rec:
+        return None
+    return rec["bytes_per_launch"] * n / rec["n"]
+
+
 def kernel_profile(torch, pc, _lib, cfg, grid, dev_frames, warmup, frames_n, seed, flush):
     """Per-kernel device time (CUDA events on the launching stream, no graph)."""
     import ctypes
@@ -432,7 +448,8 @@ def main():
         achieved = dom_bytes / (kprof[dom] * 1e-3) / 1e9 if kprof[dom] > 0 else 0.0
         roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                    "traffic": None, "algo_bytes_per_launch": dom_bytes,
+                    "traffic": measured_traffic(wl_name, variant, dom, n),
+                    "algo_bytes_per_launch": dom_bytes,
                     "kernel_ms": {k: round(v, 5) for k, v in kprof.items()},
                     "kernel_share": {k: round(v / sum(kprof.values()), 4)
                                      for k, v in kprof.items()},
