@@ -159,6 +159,33 @@ def test_fused_sir_equals_general(cuda):
     assert a.likelihood_evals == 2000 * len(frames)
 
 
+@pytest.mark.parametrize("method", ["sir", "pc"])
+def test_fused_resampling_many_tiles_heavy_weights(cuda, method):
+    # 2e5 particles -> 53 resampling tiles on 53 CTAs (grid barrier, exact CTA
+    # prefixes); a sharp likelihood concentrates the weight so some tiles emit
+    # more than one tile of slots (chunked emission)
+    frames, truth, init, dyn = _c1_like(k=5)
+    n = 200_000
+    sharp = pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(1.5, 5))
+    sharp2 = pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(1.5, 5))
+    if method == "sir":
+        a = pc.sir_track(frames, pc.FilterConfig(n, init, dyn, RES, sharp), pc.PhiloxRng(3),
+                         fused=True)
+        b = pc.sir_track(frames, pc.FilterConfig(n, init, dyn, RES, sharp2), pc.PhiloxRng(3),
+                         fused=False)
+    else:
+        g = pc.BinGrid.pixel_aligned(64, 64, 4)
+        a = pc.pcsir_track(frames, pc.PcFilterConfig(n, init, dyn, RES, sharp, grid=g),
+                           pc.PhiloxRng(3), fused=True)
+        b = pc.pcsir_track(frames, pc.PcFilterConfig(n, init, dyn, RES, sharp2, grid=g),
+                           pc.PhiloxRng(3), fused=False)
+    assert a.path == "fused" and b.path == "general"
+    assert np.min(a.ess) < n / 50   # concentrated: some tiles carry many slots
+    assert np.array_equal(a.estimates, b.estimates)
+    assert np.array_equal(a.ess, b.ess)
+    assert np.array_equal(a.resampled, b.resampled)
+
+
 def test_pcsir_tiny_cells_bitidentical_to_sir(cuda):
     # SPEC acceptance #1 / test_binning.py:208-226: 1e-5 px cells (64-bit keys)
     frames, truth, init, dyn = _c1_like(n=500, k=10)
