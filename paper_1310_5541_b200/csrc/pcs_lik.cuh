@@ -60,6 +60,26 @@ __device__ __forceinline__ void window_axis(double p, int hw, i64 extent, int& l
   hi = (int)h;
 }
 
+// float32 forms for float32 positions (bit-identical to the float64 forms):
+// * pixel offset RN32(i - p), |i| < 2^24: the float64 difference is exact and
+//   IEEE float subtraction is correctly rounded, so this equals
+//   __double2float_rn(double(i) - double(p));
+// * window_axis: for |p| < 2^23, p + 0.5f is exact unless it crosses into the
+//   next binade, where the rounding cannot cross an integer, so
+//   floorf(p + 0.5f) == floor((double)p + 0.5); other p use the float64 form.
+__device__ __forceinline__ float pix_off(int i, float p) { return __fsub_rn((float)i, p); }
+
+__device__ __forceinline__ void window_axis_f(float p, int hw, i64 extent, int& lo, int& hi) {
+  if (fabsf(p) < 8388608.0f) {
+    const int c = (int)floorf(__fadd_rn(p, 0.5f));
+    const int e1 = (int)(extent - 1);
+    lo = min(max(c - hw, 0), e1);
+    hi = min(max(c + hw, 0), e1);
+  } else {
+    window_axis((double)p, hw, extent, lo, hi);
+  }
+}
+
 __device__ __forceinline__ double nan_ll() { return __longlong_as_double(0x7ff8000000000000ll); }
 
 // ---- Gaussian windowed SSD (CANONICAL hot-path arithmetic) ----------------
@@ -76,21 +96,21 @@ __device__ __forceinline__ double loglik_gauss(const PixView& pv, float x, float
                                                const Spot& sp) {
   if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
   int xlo, xhi, ylo, yhi;
-  window_axis((double)x, sp.hw, pv.W, xlo, xhi);
-  window_axis((double)y, sp.hw, pv.H, ylo, yhi);
+  window_axis_f(x, sp.hw, pv.W, xlo, xhi);
+  window_axis_f(y, sp.hw, pv.H, ylo, yhi);
   int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
   float ag[MAXS];
 #pragma unroll
   for (int i = 0; i < MAXS; ++i) {
     if (i < nx) {
-      float d = __double2float_rn((double)(xlo + i) - (double)x);
+      float d = pix_off(xlo + i, x);
       ag[i] = i0 * expf(-(d * d) * sp.inv2s2);
     }
   }
   double ssd = 0.0;
   for (int j = 0; j < ny; ++j) {
     const float* row = pv.row(ylo + j, xlo);
-    float d = __double2float_rn((double)(ylo + j) - (double)y);
+    float d = pix_off(ylo + j, y);
     float gy = expf(-(d * d) * sp.inv2s2);
     float pr[MAXS];
 #pragma unroll
@@ -143,22 +163,22 @@ __device__ __forceinline__ double loglik_poisson(const PixView& pv, float x, flo
                                                  const Spot& sp) {
   if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
   int xlo, xhi, ylo, yhi;
-  window_axis((double)x, sp.hw, pv.W, xlo, xhi);
-  window_axis((double)y, sp.hw, pv.H, ylo, yhi);
+  window_axis_f(x, sp.hw, pv.W, xlo, xhi);
+  window_axis_f(y, sp.hw, pv.H, ylo, yhi);
   int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
   float ex[MAXS];
   const float inv_bg = 1.0f / sp.bg;
 #pragma unroll
   for (int i = 0; i < MAXS; ++i) {
     if (i < nx) {
-      float d = __double2float_rn((double)(xlo + i) - (double)x);
+      float d = pix_off(xlo + i, x);
       ex[i] = i0 * psf_axis(d, sp) * inv_bg;   // mu/bg along x (times Ey later)
     }
   }
   double ll = 0.0;
   for (int j = 0; j < ny; ++j) {
     const float* row = pv.row(ylo + j, xlo);
-    float ey = psf_axis(__double2float_rn((double)(ylo + j) - (double)y), sp);
+    float ey = psf_axis(pix_off(ylo + j, y), sp);
     double racc = 0.0;
 #pragma unroll
     for (int i = 0; i < MAXS; ++i)
@@ -182,16 +202,16 @@ __device__ __forceinline__ double loglik_gauss_generic(const PixView& pv, float 
                                                        float i0, const Spot& sp) {
   if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
   int xlo, xhi, ylo, yhi;
-  window_axis((double)x, sp.hw, pv.W, xlo, xhi);
-  window_axis((double)y, sp.hw, pv.H, ylo, yhi);
+  window_axis_f(x, sp.hw, pv.W, xlo, xhi);
+  window_axis_f(y, sp.hw, pv.H, ylo, yhi);
   double ssd = 0.0;
   for (int yy = ylo; yy <= yhi; ++yy) {
-    float d = __double2float_rn((double)yy - (double)y);
+    float d = pix_off(yy, y);
     float gy = expf(-(d * d) * sp.inv2s2);
     const float* row = pv.row(yy, xlo);
     double racc = 0.0;
     for (int xx = xlo; xx <= xhi; ++xx) {
-      float dx = __double2float_rn((double)xx - (double)x);
+      float dx = pix_off(xx, x);
       float ag = i0 * expf(-(dx * dx) * sp.inv2s2);
       float r = row[xx - xlo] - fmaf(ag, gy, sp.bg);
       racc = fma((double)r, (double)r, racc);
@@ -205,16 +225,16 @@ __device__ __forceinline__ double loglik_poisson_generic(const PixView& pv, floa
                                                          float i0, const Spot& sp) {
   if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
   int xlo, xhi, ylo, yhi;
-  window_axis((double)x, sp.hw, pv.W, xlo, xhi);
-  window_axis((double)y, sp.hw, pv.H, ylo, yhi);
+  window_axis_f(x, sp.hw, pv.W, xlo, xhi);
+  window_axis_f(y, sp.hw, pv.H, ylo, yhi);
   const float inv_bg = 1.0f / sp.bg;
   double ll = 0.0;
   for (int yy = ylo; yy <= yhi; ++yy) {
-    float ey = psf_axis(__double2float_rn((double)yy - (double)y), sp);
+    float ey = psf_axis(pix_off(yy, y), sp);
     const float* row = pv.row(yy, xlo);
     double racc = 0.0;
     for (int xx = xlo; xx <= xhi; ++xx) {
-      float exi = i0 * psf_axis(__double2float_rn((double)xx - (double)x), sp) * inv_bg;
+      float exi = i0 * psf_axis(pix_off(xx, x), sp) * inv_bg;
       racc += poisson_term(row[xx - xlo], exi * ey, sp.bg);
     }
     ll += racc;
@@ -245,19 +265,19 @@ __device__ __forceinline__ double loglik_warp(const PixView& pv, float x, float 
                                               const Spot& sp, int lane) {
   if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
   int xlo, xhi, ylo, yhi;
-  window_axis((double)x, sp.hw, pv.W, xlo, xhi);
-  window_axis((double)y, sp.hw, pv.H, ylo, yhi);
+  window_axis_f(x, sp.hw, pv.W, xlo, xhi);
+  window_axis_f(y, sp.hw, pv.H, ylo, yhi);
   const int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
   if (nx > 32 || ny > 32) return loglik_generic(pv, x, y, i0, sp);
   const bool gauss = (sp.model == 0);
   const float inv_bg = 1.0f / sp.bg;
   float colf = 0.0f, rowf = 0.0f;
   if (lane < nx) {
-    float d = __double2float_rn((double)(xlo + lane) - (double)x);
+    float d = pix_off(xlo + lane, x);
     colf = gauss ? i0 * expf(-(d * d) * sp.inv2s2) : i0 * psf_axis(d, sp) * inv_bg;
   }
   if (lane < ny) {
-    float d = __double2float_rn((double)(ylo + lane) - (double)y);
+    float d = pix_off(ylo + lane, y);
     rowf = gauss ? expf(-(d * d) * sp.inv2s2) : psf_axis(d, sp);
   }
   const float* row = pv.row(ylo + min(lane, ny - 1), xlo);
@@ -285,12 +305,12 @@ __device__ __forceinline__ double loglik_row(const PixView& pv, float x, float y
                                              const Spot& sp, int xlo, int nx, int yy) {
   const bool gauss = (sp.model == 0);
   const float inv_bg = 1.0f / sp.bg;
-  float d = __double2float_rn((double)yy - (double)y);
+  float d = pix_off(yy, y);
   float rowf = gauss ? expf(-(d * d) * sp.inv2s2) : psf_axis(d, sp);
   const float* row = pv.row(yy, xlo);
   double racc = 0.0;
   for (int i = 0; i < nx; ++i) {
-    float dx = __double2float_rn((double)(xlo + i) - (double)x);
+    float dx = pix_off(xlo + i, x);
     if (gauss) {
       float ag = i0 * expf(-(dx * dx) * sp.inv2s2);
       float r = row[i] - fmaf(ag, rowf, sp.bg);
@@ -306,8 +326,8 @@ __device__ __forceinline__ double loglik_row(const PixView& pv, float x, float y
 // window bounds of a state (for staging decisions)
 __device__ __forceinline__ void window_of(float x, float y, const Spot& sp, i64 H, i64 W, int& xlo,
                                           int& xhi, int& ylo, int& yhi) {
-  window_axis((double)x, sp.hw, W, xlo, xhi);
-  window_axis((double)y, sp.hw, H, ylo, yhi);
+  window_axis_f(x, sp.hw, W, xlo, xhi);
+  window_axis_f(y, sp.hw, H, ylo, yhi);
 }
 
 template <int MAXS>

@@ -15,13 +15,32 @@
 
 namespace pcs {
 
+// frame region staged in shared memory by every CTA of the SIR likelihood
+// kernel: SIR_SW x SIR_SW pixels centred on the previous estimate; particles
+// whose window lies inside read it from shared memory, the others from HBM
+// (same pixel values, identical log-likelihoods)
+constexpr int SIR_SW = 64;
+
 template <int MAXS>
 __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
+  __shared__ float stg[SIR_SW * SIR_SW];
   TrackCtl* C = P.ctl;
   const i64 k = C->k;
   const float* sin = (k & 1) ? P.buf1 : P.buf0;
   float* sout = (k & 1) ? P.buf0 : P.buf1;
-  const PixView pv = frame_view(C->frames + (k - C->k_frames) * P.H * P.W, P.H, P.W);
+  const float* frame = C->frames + (k - C->k_frames) * P.H * P.W;
+  const PixView pv = frame_view(frame, P.H, P.W);
+  const int sw = (int)min((i64)SIR_SW, P.W), sh = (int)min((i64)SIR_SW, P.H);
+  const int sx0 = (int)min(max((i64)floor(C->center[0]) - sw / 2, (i64)0), P.W - sw);
+  const int sy0 = (int)min(max((i64)floor(C->center[1]) - sh / 2, (i64)0), P.H - sh);
+  for (int p = threadIdx.x; p < sw * sh; p += blockDim.x)
+    stg[p] = __ldg(frame + (i64)(sy0 + p / sw) * P.W + (sx0 + p % sw));
+  __syncthreads();
+  PixView ps = pv;
+  ps.base = stg;
+  ps.pitch = sw;
+  ps.x0 = sx0;
+  ps.y0 = sy0;
   long long lmax = LLONG_MIN;
   bool bad = false;
   const i64 n = P.n, ld = P.ld;
@@ -34,7 +53,16 @@ __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
     propagate_one(s, z, P.dyn, o);
 #pragma unroll
     for (int c = 0; c < 5; ++c) sout[c * ld + j] = o[c];
-    double ll = loglik_dispatch<MAXS>(pv, o[0], o[1], o[4], P.spot);
+    int xlo, xhi, ylo, yhi;
+    window_axis_f(o[0], P.spot.hw, P.W, xlo, xhi);
+    window_axis_f(o[1], P.spot.hw, P.H, ylo, yhi);
+    const bool inside = xlo >= sx0 && xhi < sx0 + sw && ylo >= sy0 && yhi < sy0 + sh;
+    PixView v = pv;
+    v.base = inside ? ps.base : pv.base;
+    v.pitch = inside ? ps.pitch : pv.pitch;
+    v.x0 = inside ? ps.x0 : 0;
+    v.y0 = inside ? ps.y0 : 0;
+    double ll = loglik_dispatch<MAXS>(v, o[0], o[1], o[4], P.spot);
     P.ll[j] = ll;
     if (!(ll == ll) || ll == INFINITY) bad = true;
     lmax = max(lmax, (long long)f64_to_ordered(ll));
@@ -73,12 +101,18 @@ __global__ void __launch_bounds__(256) k_sir_stats(TrackParams P) {
     float w = normalised_weight(P.ll[i], m, Sf);
     wmin = min(wmin, __float_as_uint(w));
     wmax = max(wmax, __float_as_uint(w));
-    i128 wq = f32_to_fixed(w, FX_WQ);
+    // w <= 1: round(w 2^62) <= 2^62 fits a signed 64-bit value; for
+    // 2^-17 <= |v| < 2^23, round(v 2^40) = v 2^40 exactly and fits as well
+    const long long wq = (long long)f32_to_fixed(w, FX_WQ);
 #pragma unroll
     for (int c = 0; c < 5; ++c) {
-      float v = st[c * ld + i];
+      const float v = st[c * ld + i];
       if (fabsf(v) >= 16777216.0f) range = true;
-      e[c] += wq * f32_to_fixed(v, FX_STATE);
+      const float av = fabsf(v);
+      if (av >= 7.62939453125e-06f && av < 8388608.0f)   // 2^-17 <= |v| < 2^23: exact, < 2^63
+        e[c] += (i128)wq * (i128)__float2ll_rn(__fmul_rn(v, 1099511627776.0f));
+      else
+        e[c] += (i128)wq * f32_to_fixed(v, FX_STATE);
     }
     e[5] += f64_to_fixed((double)w * (double)w, FX_W2);
   }
@@ -110,6 +144,10 @@ __global__ void k_sir_finalize(TrackParams P) {
   for (int c = 0; c < 5; ++c) {
     est[c] = scalbn(i128_to_f64_rn(load_i128(C->est[c])), -(FX_WQ + FX_STATE));
     C->out_est[ko * 5 + c] = est[c];
+  }
+  if (est[0] == est[0] && est[1] == est[1]) {   // staging window of the next frame
+    C->center[0] = est[0];
+    C->center[1] = est[1];
   }
   double ess = 1.0 / scalbn(i128_to_f64_rn(load_i128(C->w2)), -FX_W2);
   C->out_ess[ko] = ess;
