@@ -73,16 +73,16 @@ struct MtParams {
 };
 
 struct MtSmem {
-  // phase A
-  unsigned long long acc_lo[5][MT_SUBW];
-  unsigned long long acc_hi[5][MT_SUBW];
+  // phase A (same tile machinery as k_pc_step1: counting sort, lane-major
+  // sorted tile, warp-segmented run sums into 32-bit digit accumulators)
+  u32 dig[15][MT_SUBW];
   u32 acc_cnt[MT_SUBW];
   u32 tile_cnt[MT_SUBW];
-  u32 tile_start[MT_SUBW];
+  unsigned short tile_start[MT_SUBW];
+  float ref[MT_SUBW + 1];          // sub-window cell edges (x then y; NaN: unusable)
   float pay[5][MT_TILE];
   unsigned short pay_q[MT_TILE];
   unsigned short list[MT_TILE];
-  u32 lcnt[MT_TILE];
   u32 n_list, n_in;
   int scan_tmp[MT_WARPS];
   // phase B/C (reuse is not attempted: the struct fits in shared memory)
@@ -145,8 +145,20 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
     sm.acc_cnt[q] = 0;
     sm.tile_cnt[q] = 0;
 #pragma unroll
-    for (int c = 0; c < 5; ++c) sm.acc_lo[c][q] = sm.acc_hi[c][q] = 0ull;
+    for (int p = 0; p < 15; ++p) sm.dig[p][q] = 0;
   }
+  const int snxi = (int)snx, snyi = (int)sny;
+  for (int q = t; q < snxi + snyi; q += MT_THREADS) {
+    bool ok;
+    float r = (q < snxi) ? cell_ref32(g.ox, g.lx, sx0 + q, ok)
+                         : cell_ref32(g.oy, g.ly, sy0 + (q - snxi), ok);
+    sm.ref[q] = ok ? r : __int_as_float(0x7fc00000);
+  }
+  const float* refy = sm.ref + snxi;
+  const AxisFast axx = make_axis(g.ox, g.lx, P.inv_lx, g.ncols);
+  const AxisFast axy = make_axis(g.oy, g.ly, P.inv_ly, g.nrows);
+  const u32 ncols32 = (u32)g.ncols;
+  const int sx0i = (int)sx0, sy0i = (int)sy0;
   if (t == 0) {
     sm.n_list = 0;
     sm.n_occ = 0;
@@ -187,37 +199,35 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
 #pragma unroll
       for (int c = 0; c < 5; ++c) sout[c * ld + base_i + j] = o[c];
       if (!(o[0] == o[0]) || !(o[1] == o[1])) bad = true;
-      i64 ix = cell_axis_fast(o[0], g.ox, g.lx, P.inv_lx, g.ncols);
-      i64 iy = cell_axis_fast(o[1], g.oy, g.ly, P.inv_ly, g.nrows);
-      u32 flat = (u32)(iy * g.ncols + ix);
+      const int ix = cell_axis_hot(o[0], axx);
+      const int iy = cell_axis_hot(o[1], axy);
+      const u32 flat = (u32)iy * ncols32 + (u32)ix;
       P.pslot[base_i + j] = flat;
-      i64 lx = ix - sx0, ly = iy - sy0;
-      bool in_sub = (lx >= 0 && lx < snx && ly >= 0 && ly < sny);
-      if (in_sub) {
-        bool okx, oky;
-        float rx = cell_ref32(g.ox, g.lx, ix, okx), ry = cell_ref32(g.oy, g.ly, iy, oky);
-        long long D;
-        in_sub = okx && oky && delta_fixed(o[0], rx, D) && delta_fixed(o[1], ry, D) &&
-                 fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f && fabsf(o[4]) < 128.0f;
-      }
-      if (in_sub) {
-        int q = (int)(ly * snx + lx);
-        int r = (int)atomicAdd(&sm.tile_cnt[q], 1u);
+      const int lx = ix - sx0i, ly = iy - sy0i;
+      float dx, dy;
+      if ((u32)lx < (u32)snxi && (u32)ly < (u32)snyi && delta_exact(o[0], sm.ref[lx], dx) &&
+          delta_exact(o[1], refy[ly], dy) && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f &&
+          fabsf(o[4]) < 128.0f) {
+        const int q = ly * snxi + lx;
+        const int r = (int)atomicAdd(&sm.tile_cnt[q], 1u);
         if (r == 0) sm.list[atomicAdd(&sm.n_list, 1u)] = (unsigned short)q;
         q_k[it] = q;
         r_k[it] = r;
+        o_k[it][0] = dx;
+        o_k[it][1] = dy;
       } else if (!mt_hash_add(HT, flat, o)) {
         hash_full = true;
       }
     }
     __syncthreads();
-    const int nl = (int)sm.n_list;
+    // run offsets: exclusive scan of the tile's cell counts (4 entries / thread)
     {
-      int base = t * 4, loc[4], sum = 0;
+      const int nl = (int)sm.n_list;
+      const int e0 = 4 * t;
+      int loc[4], sum = 0;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        int idx = base + e;
-        loc[e] = (idx < nl) ? (int)sm.tile_cnt[sm.list[idx]] : 0;
+        loc[e] = (e0 + e < nl) ? (int)sm.tile_cnt[sm.list[e0 + e]] : 0;
         sum += loc[e];
       }
       int inc = sum;
@@ -228,76 +238,37 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
       }
       if (lane == 31) sm.scan_tmp[warp] = inc;
       __syncthreads();
-      int woff = 0;
-      for (int w = 0; w < warp; ++w) woff += sm.scan_tmp[w];
+      if (t == 0) sm.n_list = 0;   // every thread has read n_list
+      int woff = (lane < warp) ? sm.scan_tmp[lane] : 0;
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) woff += __shfl_xor_sync(0xffffffffu, woff, d);
       int run = woff + inc - sum;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
-        int idx = base + e;
-        if (idx < nl) {
-          sm.tile_start[sm.list[idx]] = (u32)run;
-          sm.lcnt[idx] = (u32)loc[e];
+        if (e0 + e < nl) {
+          const int q = sm.list[e0 + e];
+          sm.tile_start[q] = (unsigned short)run;
+          sm.tile_cnt[q] = 0;
+          sm.acc_cnt[q] += (u32)loc[e];
         }
         run += loc[e];
       }
+      if (t == MT_THREADS - 1) sm.n_in = (u32)run;
     }
     __syncthreads();
+    // scatter into the lane-major sorted tile
 #pragma unroll
     for (int it = 0; it < MT_IPT; ++it) {
       if (q_k[it] < 0) continue;
-      int pos = (int)sm.tile_start[q_k[it]] + r_k[it];
+      const int pos = (int)sm.tile_start[q_k[it]] + r_k[it];
+      const int idx = (pos % MT_IPT) * MT_THREADS + pos / MT_IPT;
 #pragma unroll
-      for (int c = 0; c < 5; ++c) sm.pay[c][pos] = o_k[it][c];
-      sm.pay_q[pos] = (unsigned short)q_k[it];
+      for (int c = 0; c < 5; ++c) sm.pay[c][idx] = o_k[it][c];
+      sm.pay_q[idx] = (unsigned short)q_k[it];
     }
     __syncthreads();
-    for (int e = t; e < nl; e += MT_THREADS) {
-      const int cnt = (int)sm.lcnt[e];
-      if (cnt > S1_SMALL) continue;
-      const int q = sm.list[e], st = (int)sm.tile_start[q];
-      bool ok;
-      const float rx = cell_ref32(g.ox, g.lx, sx0 + q % snx, ok);
-      const float ry = cell_ref32(g.oy, g.ly, sy0 + q / snx, ok);
-      long long v[5] = {0, 0, 0, 0, 0};
-      for (int pos = st; pos < st + cnt; ++pos) {
-        v[0] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[0][pos], rx), 1099511627776.0f));
-        v[1] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[1][pos], ry), 1099511627776.0f));
-#pragma unroll
-        for (int c = 2; c < 5; ++c) v[c] += __float2ll_rn(__fmul_rn(sm.pay[c][pos], 1099511627776.0f));
-      }
-#pragma unroll
-      for (int c = 0; c < 5; ++c) smem_rmw_i128(&sm.acc_lo[c][q], &sm.acc_hi[c][q], v[c]);
-      sm.acc_cnt[q] += (u32)cnt;
-      sm.tile_cnt[q] = 0;
-    }
-    for (int e = warp; e < nl; e += MT_WARPS) {
-      const int cnt = (int)sm.lcnt[e];
-      if (cnt <= S1_SMALL) continue;
-      const int q = sm.list[e], st = (int)sm.tile_start[q];
-      bool ok;
-      const float rx = cell_ref32(g.ox, g.lx, sx0 + q % snx, ok);
-      const float ry = cell_ref32(g.oy, g.ly, sy0 + q / snx, ok);
-      long long v[5] = {0, 0, 0, 0, 0};
-      for (int pos = st + lane; pos < st + cnt; pos += 32) {
-        v[0] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[0][pos], rx), 1099511627776.0f));
-        v[1] += __float2ll_rn(__fmul_rn(__fsub_rn(sm.pay[1][pos], ry), 1099511627776.0f));
-#pragma unroll
-        for (int c = 2; c < 5; ++c) v[c] += __float2ll_rn(__fmul_rn(sm.pay[c][pos], 1099511627776.0f));
-      }
-#pragma unroll
-      for (int c = 0; c < 5; ++c) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v[c] += __shfl_xor_sync(0xffffffffu, v[c], o);
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int c = 0; c < 5; ++c) smem_rmw_i128(&sm.acc_lo[c][q], &sm.acc_hi[c][q], v[c]);
-        sm.acc_cnt[q] += (u32)cnt;
-        sm.tile_cnt[q] = 0;
-      }
-    }
-    __syncthreads();
-    if (t == 0) sm.n_list = 0;
+    tile_run_sums<MT_THREADS, MT_IPT, MT_TILE, MT_SUBW>(sm.pay, sm.pay_q, (int)sm.n_in,
+                                                        &sm.dig[0][0], t);
     __syncthreads();
   }
   if (bad) atomicOr(&TG.flags, (u32)PCS_FLAG_NONFINITE);
@@ -333,13 +304,10 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
       cnt = sm.acc_cnt[o];
       ix = sx0 + o % snx;
       iy = sy0 + o / snx;
-      bool ok;
-      float ref[2] = {cell_ref32(g.ox, g.lx, ix, ok), cell_ref32(g.oy, g.ly, iy, ok)};
 #pragma unroll
-      for (int c = 0; c < 5; ++c) {
-        S[c] = (i128)(((u128)sm.acc_hi[c][o] << 64) | (u128)sm.acc_lo[c][o]);
-        if (c < 2) S[c] += (i128)cnt * f32_to_fixed(ref[c], FX_STATE);
-      }
+      for (int c = 0; c < 5; ++c) S[c] = digits_value<MT_SUBW>(&sm.dig[0][0], c, o);
+      S[0] += (i128)cnt * f32_to_fixed(sm.ref[o % snxi], FX_STATE);
+      S[1] += (i128)cnt * f32_to_fixed(refy[o / snxi], FX_STATE);
     } else {
       const MtHash& h = HT[-o - 1];
       cnt = h.cnt;
@@ -415,13 +383,11 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
     if (o >= 0) {
       sm.w_sub[o] = w;
       cnt = sm.acc_cnt[o];
-      i64 ix = sx0 + o % snx, iy = sy0 + o / snx;
-      bool ok;
-      float ref[2] = {cell_ref32(g.ox, g.lx, ix, ok), cell_ref32(g.oy, g.ly, iy, ok)};
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
-        i128 S = (i128)(((u128)sm.acc_hi[c][o] << 64) | (u128)sm.acc_lo[c][o]);
-        if (c < 2) S += (i128)cnt * f32_to_fixed(ref[c], FX_STATE);
+        i128 S = digits_value<MT_SUBW>(&sm.dig[0][0], c, o);
+        if (c == 0) S += (i128)cnt * f32_to_fixed(sm.ref[o % snxi], FX_STATE);
+        if (c == 1) S += (i128)cnt * f32_to_fixed(refy[o / snxi], FX_STATE);
         e[c] += wq * S;
       }
     } else {
