@@ -87,6 +87,7 @@ struct MtSmem {
   int scan_tmp[MT_WARPS];
   // phase B/C (reuse is not attempted: the struct fits in shared memory)
   float w_sub[MT_SUBW];
+  u128 wfix_sub[MT_SUBW];          // exact cdf weight round(w 2^120) per sub-window cell
   int occ[MT_MAXM];      // >= 0: sub-window cell, < 0: -(hash slot) - 1
   double ll[MT_MAXM];
   float dpix[MT_STAGE];
@@ -202,7 +203,6 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
       const int ix = cell_axis_hot(o[0], axx);
       const int iy = cell_axis_hot(o[1], axy);
       const u32 flat = (u32)iy * ncols32 + (u32)ix;
-      P.pslot[base_i + j] = flat;
       const int lx = ix - sx0i, ly = iy - sy0i;
       float dx, dy;
       if ((u32)lx < (u32)snxi && (u32)ly < (u32)snyi && delta_exact(o[0], sm.ref[lx], dx) &&
@@ -215,8 +215,10 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
         r_k[it] = r;
         o_k[it][0] = dx;
         o_k[it][1] = dy;
-      } else if (!mt_hash_add(HT, flat, o)) {
-        hash_full = true;
+        P.pslot[base_i + j] = (u32)q;                 // phase C: sub-window cell
+      } else {
+        P.pslot[base_i + j] = 0x80000000u | flat;     // phase C: outlier (hash) cell
+        if (!mt_hash_add(HT, flat, o)) hash_full = true;
       }
     }
     __syncthreads();
@@ -382,6 +384,7 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
     u32 cnt;
     if (o >= 0) {
       sm.w_sub[o] = w;
+      sm.wfix_sub[o] = cdf_fixed(w);
       cnt = sm.acc_cnt[o];
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
@@ -434,50 +437,49 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
   __syncthreads();
 
   // ---------------- phase C: exact-prefix systematic resampling ----------------
+  // (k_sys_resample in one CTA: scan tiles of 2560 particles in order, exact
+  // u128 prefixes, first slot per item from the top 64 bits of the prefix,
+  // run heads + block max-scan, coalesced ancestor writes)
   const int do_res = s_res;
   const double u = philox_resample_u(seed_t, P.frame0 + (u32)k);
-  float* wsh = &sm.pay[0][0];   // MT_TILE... reuse 5*MT_TILE floats as SCAN_TILE
-  constexpr int CI = 8;          // items per thread
-  constexpr int CT = MT_THREADS * CI;   // 4096 particles per scan tile
+  constexpr int CI = 5;                  // items per thread (stride-5 reads: conflict-free)
+  constexpr int CT = MT_THREADS * CI;    // 2560 particles per scan tile
+  static_assert(3 * CT * 4 <= 5 * MT_TILE * 4, "phase-C buffers alias the phase-A payload");
+  u32* cells = reinterpret_cast<u32*>(&sm.pay[0][0]);
+  int* hp = reinterpret_cast<int*>(cells + CT);
+  int* stage = hp + CT;
+  const double nd = (double)n, eps = nd * 8.881784197001252e-16;   // n * 2^-50
+  const double kappa = nd * 1.0842021724855044e-19;                  // n * 2^-63
+  // exact weight of a staged particle: sub-window cell table, else the hash
+  auto cellw = [&](u32 code) -> u128 {
+    if (code == 0xFFFFFFFFu) return 0;
+    if (!(code & 0x80000000u)) return sm.wfix_sub[code];
+    const u32 key = (code & 0x7FFFFFFFu) + 1u;
+    u32 s = mt_hash_slot(key);
+    for (int probe = 0; probe < MT_HCAP; ++probe) {
+      if (HT[s].key == key) return cdf_fixed(__uint_as_float((u32)HT[s].sum[4][1]));
+      s = (s + 1u) & (MT_HCAP - 1);
+    }
+    return 0;
+  };
+  u128 pre = 0;
+  const int k0 = t * CI;
   for (i64 base = 0; base < n; base += CT) {
     if (!do_res) {
       for (int q = 0; q < CI; ++q) {
-        i64 i = base + (i64)q * MT_THREADS + t;
+        const i64 i = base + (i64)q * MT_THREADS + t;
         if (i < n) P.anc[base_i + i] = (int)i;
       }
       continue;
     }
     for (int q = 0; q < CI; ++q) {
-      i64 i = base + (i64)q * MT_THREADS + t;
-      float w = 0.0f;
-      if (i < n) {
-        u32 flat = P.pslot[base_i + i];
-        i64 ix = (i64)flat % g.ncols, iy = (i64)flat / g.ncols;
-        i64 lx = ix - sx0, ly = iy - sy0;
-        bool in_sub = (lx >= 0 && lx < snx && ly >= 0 && ly < sny) && sm.acc_cnt[ly * snx + lx];
-        if (in_sub) {
-          w = sm.w_sub[ly * snx + lx];
-        } else {
-          u32 key = flat + 1u, s = mt_hash_slot(key);
-          for (int probe = 0; probe < MT_HCAP; ++probe) {
-            if (HT[s].key == key) {
-              w = __uint_as_float((u32)HT[s].sum[4][1]);
-              break;
-            }
-            s = (s + 1u) & (MT_HCAP - 1);
-          }
-        }
-      }
-      wsh[q * MT_THREADS + t] = w;
+      const i64 i = base + (i64)q * MT_THREADS + t;
+      cells[q * MT_THREADS + t] = (i < n) ? P.pslot[base_i + i] : 0xFFFFFFFFu;
     }
     __syncthreads();
-    u128 loc[CI];
     u128 tsum = 0;
 #pragma unroll
-    for (int q = 0; q < CI; ++q) {
-      tsum += cdf_fixed(wsh[t * CI + q]);
-      loc[q] = tsum;
-    }
+    for (int q = 0; q < CI; ++q) tsum += cellw(cells[k0 + q]);
     u128 inc = tsum;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -486,25 +488,77 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
     }
     if (lane == 31) sm.wtot[warp] = inc;
     __syncthreads();
-    u128 woff = 0, ttot = 0;
+    u128 woff = 0, tagg = 0;
     for (int w = 0; w < MT_WARPS; ++w) {
       if (w < warp) woff += sm.wtot[w];
-      ttot += sm.wtot[w];
+      tagg += sm.wtot[w];
     }
-    u128 excl = sm.carry + woff + (inc - tsum);
-    const i64 i0 = base + (i64)t * CI;
-    if (i0 < n) {
-      i64 j = (i0 == 0) ? 0 : first_slot_at_or_above(cdf_round(excl), u, n);
+    const u128 excl = pre + woff + (inc - tsum);
+    const i64 tl = min(n, base + (i64)CT) - 1;
+    const i64 tj0 = (base == 0) ? 0 : first_slot_fast(cdf_round(pre), u, n, nd, eps);
+    const i64 tj1 = (tl == n - 1) ? n : first_slot_fast(cdf_round(pre + tagg), u, n, nd, eps);
+    const i64 i0 = base + k0;
+    {
+      int jr = 0;
+      if (i0 < n) jr = (int)(((i0 == 0) ? 0 : slot_of_prefix(excl, u, n, nd, kappa, eps)) - tj0);
+      u128 run = excl;
       for (int q = 0; q < CI; ++q) {
-        i64 i = i0 + q;
-        if (i >= n) break;
-        i64 jend = (i == n - 1) ? n : first_slot_at_or_above(cdf_round(excl + loc[q]), u, n);
-        for (; j < jend; ++j) P.anc[base_i + j] = (int)i;
+        const i64 i = i0 + q;
+        int h = INT_MAX;
+        if (i < n) {
+          run += cellw(cells[k0 + q]);
+          const int jend = (int)(((i == n - 1) ? n : slot_of_prefix(run, u, n, nd, kappa, eps)) - tj0);
+          if (jend > jr) h = jr;
+          jr = jend;
+        }
+        hp[k0 + q] = h;
       }
     }
     __syncthreads();
-    if (t == 0) sm.carry += ttot;
-    __syncthreads();
+    const i64 m_slots = tj1 - tj0;
+    int carry = -1;
+    for (i64 c0 = 0; c0 < m_slots; c0 += CT) {
+#pragma unroll
+      for (int q = 0; q < CI; ++q) stage[k0 + q] = -1;
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < CI; ++q) {
+        const int h = hp[k0 + q];
+        if ((i64)h >= c0 && (i64)h < c0 + CT) stage[(int)((i64)h - c0)] = k0 + q;
+      }
+      __syncthreads();
+      int tmax = -1;
+#pragma unroll
+      for (int q = 0; q < CI; ++q) tmax = max(tmax, stage[k0 + q]);
+      int incl = tmax;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl = max(incl, o);
+      }
+      if (lane == 31) sm.scan_tmp[warp] = incl;
+      int excl_l = __shfl_up_sync(0xffffffffu, incl, 1);
+      if (lane == 0) excl_l = -1;
+      __syncthreads();
+      int prev = carry, total = carry;
+      for (int w = 0; w < MT_WARPS; ++w) {
+        if (w < warp) prev = max(prev, sm.scan_tmp[w]);
+        total = max(total, sm.scan_tmp[w]);
+      }
+      int runm = max(prev, excl_l);
+#pragma unroll
+      for (int q = 0; q < CI; ++q) {
+        runm = max(runm, stage[k0 + q]);
+        stage[k0 + q] = runm;
+      }
+      __syncthreads();
+      const int cm = (int)min((i64)CT, m_slots - c0);
+      int* out = P.anc + base_i + tj0 + c0;
+      for (int kk = t; kk < cm; kk += MT_THREADS) out[kk] = (int)(base + stage[kk]);
+      carry = total;
+      __syncthreads();
+    }
+    pre += tagg;
   }
   // clear the consumed outlier cells for the next frame
   for (int s = t; s < MT_HCAP; s += MT_THREADS) {
