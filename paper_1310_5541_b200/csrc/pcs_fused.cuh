@@ -1185,11 +1185,22 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, u32 byte
 template <int KIND> struct RsElem { typedef u32 T; };
 template <> struct RsElem<2> { typedef double T; };
 
+// globaltimer stamps of CTA 0 (dbg[10..14]: start, pass 1 done, barrier
+// entered, barrier left, prefix done) and the end of the last CTA (dbg[15])
+#define RS_PROBE(i)                                                                   \
+  do {                                                                                \
+    if (threadIdx.x == 0 && (blockIdx.x == 0 || ((i) == 4 && blockIdx.x == gridDim.x - 1))) { \
+      unsigned long long _g;                                                          \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(_g));                          \
+      C->dbg[(i) == 4 && blockIdx.x == gridDim.x - 1 ? 15 : 10 + (i)] = (long long)_g; \
+    }                                                                                 \
+  } while (0)
+
 template <int KIND>
 struct RsSmem {
   typename RsElem<KIND>::T ring[2][RS_TILE];   // TMA ring (16-byte aligned)
   int stage[RS_TILE];
-  int hp[RS_TILE];
+  int hp[KIND == 1 ? 1 : RS_TILE];   // run heads (KIND 1: in place of the consumed cell ids)
   u128 wtot[SCAN_BLOCK / 32];
   int s_wmax[SCAN_BLOCK / 32];
   long long s_jr[2];
@@ -1197,13 +1208,13 @@ struct RsSmem {
 };
 
 template <int KIND>
-__global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(TrackParams P) {
+__global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(TrackParams P) {
   typedef typename RsElem<KIND>::T E;
   extern __shared__ __align__(128) unsigned char rs_raw[];
   RsSmem<KIND>& sm = *reinterpret_cast<RsSmem<KIND>*>(rs_raw);
   auto& ring = sm.ring;
   int* stage = sm.stage;
-  int* hp = sm.hp;
+  int* hp_own = sm.hp;
   u128* wtot = sm.wtot;
   int* s_wmax = sm.s_wmax;
   long long* s_jr = sm.s_jr;
@@ -1222,6 +1233,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(Trac
     return;
   }
   const double m = C->m, Sf = C->Sf, u = C->u;
+  RS_PROBE(0);
   const E* src = (KIND == 1) ? (const E*)(const void*)P.pslot : (const E*)(const void*)P.ll;
   const int mt = (int)(t1 - t0);      // tiles of this CTA; loads L = 0..2 mt-1 (two passes)
   auto issue = [&](int L) {           // thread 0 only
@@ -1271,7 +1283,9 @@ __global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(Trac
       __threadfence();
     }
   }
+  RS_PROBE(1);
   grid_barrier(C, G);
+  RS_PROBE(2);
   // ---- exclusive prefix of this CTA: aggregates of the CTAs before it ----
   u128 pre;
   {
@@ -1288,6 +1302,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(Trac
     for (int w = 0; w < SCAN_BLOCK / 32; ++w) pre += wtot[w];
     __syncthreads();
   }
+  RS_PROBE(3);
   // ---- pass 2: per tile, item prefixes -> run heads -> ancestors ----
   const i64 ng = P.n_global, off = P.idx_off, lo = P.slot_lo, cap = P.slot_cap;
   const double nd = (double)ng, eps = nd * 8.881784197001252e-16;   // n * 2^-50
@@ -1298,6 +1313,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(Trac
     mbar_wait(&bar[L & 1], (u32)((L >> 1) & 1));
     if (threadIdx.x == 0 && L + 1 < 2 * mt) issue(L + 1);
     const E* buf = ring[L & 1];
+    int* hp = (KIND == 1) ? reinterpret_cast<int*>(ring[L & 1]) : hp_own;
     const i64 base = (t0 + (L - mt)) * RS_TILE;
     const i64 i0 = base + k0;
     u128 tsum = 0;
@@ -1339,7 +1355,8 @@ __global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(Trac
           if (jend > jr) h = jr;
           jr = jend;
         }
-        hp[k0 + q] = h;
+        hp[k0 + q] = h;            // (KIND 1: over item k0 + q, already read)
+        stage[k0 + q] = -1;        // first chunk's fill
       }
     }
     __syncthreads();   // every read of ring[L & 1] is done; it is free for load L + 2
@@ -1347,9 +1364,11 @@ __global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(Trac
     const i64 m_slots = tj1 - tj0;
     int carry = -1;
     for (i64 c0 = 0; c0 < m_slots; c0 += RS_TILE) {
+      if (c0 > 0) {
 #pragma unroll
-      for (int q = 0; q < RS_ITEMS; ++q) stage[k0 + q] = -1;
-      __syncthreads();
+        for (int q = 0; q < RS_ITEMS; ++q) stage[k0 + q] = -1;
+        __syncthreads();
+      }
 #pragma unroll
       for (int q = 0; q < RS_ITEMS; ++q) {
         const int h = hp[k0 + q];
@@ -1394,6 +1413,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, RS_MIN_BLOCKS) k_sys_resample(Trac
     pre += tagg;
   }
   if (oob) set_flag(C, PCS_FLAG_CAPACITY);
+  RS_PROBE(4);
 }
 
 constexpr size_t S1_SMEM = sizeof(S1Smem);
