@@ -857,7 +857,7 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   }
   T.maxs = maxs_for(cfg->spot.halfwidth);
   T.prop_grid = grid_for(n, 256, ctx->sms, 8);
-  T.s1_grid = (int)std::min<i64>(ctx->sms, ceil_div(n, S1_TILE));
+  T.s1_grid = (int)std::min<i64>((i64)ctx->sms * S1_CTAS_PER_SM, ceil_div(n, S1_TILE));
   {
     // equal tile counts per CTA: tile = ceil(per_cta / ceil(per_cta / S1_TILE))
     const i64 per_cta = ceil_div(n, (i64)T.s1_grid);

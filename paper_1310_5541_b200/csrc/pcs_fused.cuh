@@ -20,22 +20,24 @@
 
 namespace pcs {
 
-constexpr int S1_THREADS = 1024;               // 32 warps/SM; fits 64 registers
+constexpr int S1_THREADS = 512;                // 2 CTAs x 16 warps per SM; 64 registers
+constexpr int S1_CTAS_PER_SM = 2;              // two independent barrier domains per SM
 constexpr int S1_IPT = 2;
-constexpr int S1_TILE = S1_THREADS * S1_IPT;   // 2048 particles per tile
+constexpr int S1_TILE = S1_THREADS * S1_IPT;   // 1024 particles per tile
 constexpr int S1_WARPS = S1_THREADS / 32;
 constexpr int S1_SMALL = 16;                   // (multi-target kernel) lane-owned run length
-constexpr int SUBW = 1536;                     // shared-memory sub-window cells
+constexpr int S1_SIDE = 32;                    // sub-window side (cells)
+constexpr int SUBW = S1_SIDE * S1_SIDE;        // shared-memory sub-window cells
 constexpr int S1_PARTS = 15;                   // 5 components x 3 digits (18/18/signed)
 constexpr int S1_E = 4;                        // sorted elements per thread in the run sums
-constexpr int S1_SUM_THREADS = S1_TILE / S1_E; // 512 threads (16 warps) sum the sorted tile
+constexpr int S1_SUM_THREADS = S1_TILE / S1_E; // 256 threads (8 warps) sum the sorted tile
 constexpr int S1_FLUSH_TILES = 256;            // digit accumulators stay in range (see below)
 constexpr i64 TABLE_MAX = 1ll << 28;           // dense full-grid table (cells)
 constexpr int MAXM = 16384;                    // occupied cells per frame (fused)
 
-// Per-tile pipeline (k_pc_step1): each CTA counting-sorts a tile of 2048
-// particles by sub-window cell in shared memory (a native 32-bit shared atomic
-// per particle gives its rank), then 16 warps walk the sorted tile, 4
+// Per-tile pipeline (k_pc_step1, two CTAs per SM): each CTA counting-sorts a
+// tile of 1024 particles by sub-window cell in shared memory (a native 32-bit
+// shared atomic per particle gives its rank), then 8 warps walk the sorted tile, 4
 // consecutive particles per lane, and a warp-segmented scan joins runs that
 // cross lanes. One lane per (cell, warp) adds the exact run sum S (int64,
 // |S| < 2^54) to three 32-bit digit accumulators: bits 0-17, 18-35 (unsigned)
@@ -419,7 +421,7 @@ __device__ __forceinline__ void s1_flush(const TrackParams& P, TrackCtl* C, S1Sm
   }
 }
 
-__global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
+__global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackParams P) {
   extern __shared__ __align__(16) unsigned char s1_raw[];
   S1Smem& sm = *reinterpret_cast<S1Smem*>(s1_raw);
   TrackCtl* C = P.ctl;
@@ -438,9 +440,9 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
   const i64 tstep = gridDim.x;
 
   // sub-window (identical in every CTA): centred on the previous estimate
-  i64 snx = min((i64)39, g.ncols), sny = min((i64)39, g.nrows);
-  if (snx < 39) sny = min(g.nrows, (i64)(SUBW / snx));
-  if (sny < 39) snx = min(g.ncols, (i64)(SUBW / sny));
+  i64 snx = min((i64)S1_SIDE, g.ncols), sny = min((i64)S1_SIDE, g.nrows);
+  if (snx < S1_SIDE) sny = min(g.nrows, (i64)(SUBW / snx));
+  if (sny < S1_SIDE) snx = min(g.ncols, (i64)(SUBW / sny));
   i64 cx = cell_axis_fast((float)C->center[0], g.ox, g.lx, P.inv_lx, g.ncols);
   i64 cy = cell_axis_fast((float)C->center[1], g.oy, g.ly, P.inv_ly, g.nrows);
   const i64 sx0 = min(max(cx - snx / 2, (i64)0), g.ncols - snx);
@@ -580,7 +582,7 @@ __global__ void __launch_bounds__(S1_THREADS, 1) k_pc_step1(TrackParams P) {
       sm.pay_q[idx] = (unsigned short)q_k[it];
     }
     __syncthreads();
-    // ---- phase 4: exact run sums over the sorted tile (16 warps, 4
+    // ---- phase 4: exact run sums over the sorted tile (8 warps, 4
     //      consecutive particles per lane, warp-segmented scan across lanes) ----
     if (t < S1_SUM_THREADS)
       tile_run_sums<S1_SUM_THREADS, S1_E, S1_TILE, SUBW>(pay, sm.pay_q, (int)sm.n_in, &sm.dig[0][0], t);
