@@ -25,7 +25,6 @@ constexpr int S1_CTAS_PER_SM = 2;              // two independent barrier domain
 constexpr int S1_IPT = 2;
 constexpr int S1_TILE = S1_THREADS * S1_IPT;   // 1024 particles per tile
 constexpr int S1_WARPS = S1_THREADS / 32;
-constexpr int S1_SMALL = 16;                   // (multi-target kernel) lane-owned run length
 constexpr int S1_SIDE = 32;                    // sub-window side (cells)
 constexpr int SUBW = S1_SIDE * S1_SIDE;        // shared-memory sub-window cells
 constexpr int S1_PARTS = 15;                   // 5 components x 3 digits (18/18/signed)
@@ -246,17 +245,6 @@ __device__ __forceinline__ float cell_ref32(double origin, double cell, i64 i, b
   return r;
 }
 
-// D = round(v * 2^40) - round(ref * 2^40) via an exact float32 difference
-// (TwoSum check). Returns false if v - ref is not exact (caller falls back).
-__device__ __forceinline__ bool delta_fixed(float v, float ref, long long& D) {
-  float s = __fsub_rn(v, ref);
-  float bp = __fsub_rn(s, v);
-  float ap = __fsub_rn(s, bp);
-  float err = __fadd_rn(__fsub_rn(v, ap), __fsub_rn(-ref, bp));
-  if (err != 0.0f || !(fabsf(s) < 128.0f)) return false;
-  D = __float2ll_rn(__fmul_rn(s, 1099511627776.0f));  // exact scale by 2^40, RN-even
-  return true;
-}
 
 __device__ __forceinline__ void touch_cell(const TrackParams& P, TrackCtl* C, u32 cell, u32 cnt) {
   u32 old = atomicAdd(P.tab_cnt + cell, cnt);
@@ -266,26 +254,7 @@ __device__ __forceinline__ void touch_cell(const TrackParams& P, TrackCtl* C, u3
   }
 }
 
-// shared-memory int128 accumulate (lo/hi words with carry); deterministic sum
-__device__ __forceinline__ void smem_add_i128(unsigned long long* lo, unsigned long long* hi,
-                                              long long v) {
-  unsigned long long vlo = (unsigned long long)v;
-  unsigned long long vhi = (v < 0) ? ~0ull : 0ull;
-  unsigned long long old = atomicAdd(lo, vlo);
-  if (old + vlo < old) vhi += 1ull;
-  if (vhi) atomicAdd(hi, vhi);
-}
 
-// exclusive (single-owner) int128 read-modify-write in shared memory
-__device__ __forceinline__ void smem_rmw_i128(unsigned long long* lo, unsigned long long* hi,
-                                              long long v) {
-  unsigned long long vlo = (unsigned long long)v;
-  unsigned long long vhi = (v < 0) ? ~0ull : 0ull;
-  unsigned long long old = *lo;
-  unsigned long long nlo = old + vlo;
-  *lo = nlo;
-  *hi += vhi + (nlo < old ? 1ull : 0ull);
-}
 
 // ===========================================================================
 // pcSIR step 1
@@ -1143,7 +1112,6 @@ __device__ __forceinline__ i64 slot_of_prefix(u128 Pc, double u, i64 ng, double 
 // processed. 15 consecutive items per thread: the stride-15 reads of the
 // dense tile are bank-conflict free. Requires every CTA to be co-resident
 // (grid = SMs x occupancy, set by the host from the occupancy calculator).
-constexpr int RS_MIN_BLOCKS = 3;
 constexpr int RS_ITEMS = 15;
 constexpr int RS_TILE = SCAN_BLOCK * RS_ITEMS;   // 3840
 
