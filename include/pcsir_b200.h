@@ -90,6 +90,19 @@ double pcs_philox_resample_u(uint64_t seed, uint32_t frame);
 int pcs_philox_multinomial_points(uint64_t seed, uint32_t frame, int64_t n, double* out,
                                   void* stream);
 
+/* ---- scene synthesis (synthesis.py:124-150: render_clean_frame +
+ * render_sequence, generalised to several spots per frame). spots: device
+ * float64 [n_frames][n_spots][3] = (x, y, I0); out: device float32
+ * [n_frames][height][width]. Ideal frame = i_bg + sum of I0 gx gy over each
+ * spot's +-ceil(window_sigmas * sigma_psf) window (exact order-free fixed-point
+ * sum at 2^-32); noise != 0 draws Poisson(ideal) per pixel from the Philox
+ * stream (seed, pixel, frame0 + k) plus optional Gaussian read noise clamped
+ * at 0. */
+int pcs_render_frames(pcs_ctx* ctx, const double* spots, int64_t n_spots, int64_t n_frames,
+                      int64_t width, int64_t height, double sigma_psf, double i_bg,
+                      double window_sigmas, int noise, double read_noise_std, uint64_t seed,
+                      uint32_t frame0, float* out, void* stream);
+
 /* ---- init_particle_set (state.py:164-175) */
 int pcs_init_particles(const pcs_init_t* init, uint64_t seed, int64_t index_offset, int64_t n,
                        float* states, int64_t ld, void* stream);

@@ -307,6 +307,19 @@ def loglik_poisson(pixels, xs, ys, i0s, sigma_psf, i_bg, halfwidth, model=1):
     return out
 
 
+def render_ideal(spots, width, height, sigma_psf, i_bg):
+    """Ideal frame of several spots (synthesis.py:124-130, render_clean_frame,
+    summed over spots): i_bg + sum_s I0_s outer(gy_s, gx_s), float64 over the
+    whole frame. ``spots``: (S, 3) (x, y, I0)."""
+    out = np.full((height, width), float(i_bg))
+    xs, ys = np.arange(width, dtype=np.float64), np.arange(height, dtype=np.float64)
+    for x, y, i0 in np.asarray(spots, dtype=np.float64).reshape(-1, 3):
+        gx = np.exp(-((xs - x) ** 2) / (2.0 * sigma_psf ** 2))
+        gy = np.exp(-((ys - y) ** 2) / (2.0 * sigma_psf ** 2))
+        out += i0 * np.outer(gy, gx)
+    return out
+
+
 def normalize(weights):
     """filtering.py:75-85."""
     w_max = weights.max()

@@ -81,6 +81,9 @@ _SIGNATURES = [
     ("pcs_philox_init_uniforms", c_int32, [c_uint64, c_int64, c_int64, c_void_p, c_int64, c_void_p]),
     ("pcs_philox_resample_u", c_double, [c_uint64, c_uint32]),
     ("pcs_philox_multinomial_points", c_int32, [c_uint64, c_uint32, c_int64, c_void_p, c_void_p]),
+    ("pcs_render_frames", c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_int64, c_int64,
+                                    c_double, c_double, c_double, c_int32, c_double, c_uint64,
+                                    c_uint32, c_void_p, c_void_p]),
     ("pcs_init_particles", c_int32, [P(PcsInit), c_uint64, c_int64, c_int64, c_void_p, c_int64, c_void_p]),
     ("pcs_propagate", c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, P(PcsDynamics),
                                 c_uint64, c_uint32, c_int64, c_void_p]),

@@ -14,6 +14,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "pcs_bin.cuh"
+#include "pcs_synth.cuh"
 #include "pcs_common.cuh"
 #include "pcs_lik.cuh"
 #include "pcs_state.cuh"
@@ -120,6 +121,7 @@ enum Slot {
   SL_MT_TGT,
   SL_MT_HASH,
   SL_MT_OUT,
+  SL_SYNTH,
   SL_COUNT
 };
 
@@ -212,6 +214,34 @@ extern "C" {
 
 const char* pcs_last_error(void) { return g_last_error.c_str(); }
 int pcs_version(void) { return 10000; }
+
+// ---- scene synthesis (synthesis.py:124-150) ----------------------------------
+int pcs_render_frames(pcs_ctx* ctx, const double* spots, int64_t n_spots, int64_t n_frames,
+                      int64_t width, int64_t height, double sigma_psf, double i_bg,
+                      double window_sigmas, int noise, double read_noise_std, uint64_t seed,
+                      uint32_t frame0, float* out, void* stream) {
+  PCS_CHECK_ARG(ctx && out && n_frames >= 0 && n_spots >= 0 && width > 0 && height > 0,
+                "bad arguments");
+  PCS_CHECK_ARG(n_spots == 0 || spots, "spots is NULL");
+  PCS_CHECK_ARG(sigma_psf > 0 && window_sigmas > 0 && read_noise_std >= 0, "bad psf parameters");
+  cudaStream_t st = S(stream);
+  const i64 npix = width * height;
+  u64* acc = nullptr;
+  PCS_SCRATCH(SL_SYNTH, npix * sizeof(u64), acc);
+  const int r = (int)ceil(window_sigmas * sigma_psf);
+  const double inv2s2 = 1.0 / (2.0 * sigma_psf * sigma_psf);
+  const i64 work = n_spots * (i64)(2 * r + 1) * (2 * r + 1);
+  for (i64 k = 0; k < n_frames; ++k) {
+    PCS_CUDA_TRY(cudaMemsetAsync(acc, 0, npix * sizeof(u64), st));
+    if (work > 0)
+      k_synth_spots<<<grid_for(work, 256, ctx->sms), 256, 0, st>>>(spots + k * n_spots * 3, n_spots,
+                                                                   width, height, inv2s2, r, acc);
+    k_synth_finalize<<<grid_for(npix, 256, ctx->sms), 256, 0, st>>>(
+        acc, npix, i_bg, noise, read_noise_std, seed, frame0 + (u32)k, out + k * npix);
+  }
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
 
 int pcs_device_info(int device, int* sm_count, int64_t* l2_bytes, int* cc_major, int* cc_minor) {
   cudaDeviceProp p;

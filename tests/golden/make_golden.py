@@ -257,6 +257,18 @@ def gen_steps():
     return out
 
 
+def gen_synth():
+    """render_clean_frame (synthesis.py:124-130) of the unmodified reference
+    for states in the interior, at a border and off the frame."""
+    from pcsir import synthesis as rsyn
+    from pcsir.imaging import PsfParams as RPsf
+    cfg = rsyn.SceneConfig(psf=RPsf(1.5, 10.0), snr=4.0, frames=1, width=48, height=40)
+    states = np.array([[20.3, 17.6, 0.0, 0.0, 20.0], [0.4, 39.2, 0.0, 0.0, 35.5],
+                       [47.9, 3.3, 0.0, 0.0, 12.25], [-3.0, 50.0, 0.0, 0.0, 8.0]])
+    frames = np.stack([rsyn.render_clean_frame(s, cfg) for s in states])
+    return {"states": states, "frames": frames, "sigma": 1.5, "bg": 10.0}
+
+
 def main():
     np.savez_compressed(HERE / "ssd.npz", **gen_ssd())
     np.savez_compressed(HERE / "partition.npz", **gen_partition())
@@ -264,6 +276,7 @@ def main():
     np.savez_compressed(HERE / "propagate.npz", **gen_propagate())
     np.savez_compressed(HERE / "steps.npz", **gen_steps())
     np.savez_compressed(HERE / "tracks.npz", **gen_tracks())
+    np.savez_compressed(HERE / "synth.npz", **gen_synth())
     for p in sorted(HERE.glob("*.npz")):
         print(p.name, p.stat().st_size)
     print("reference backend:", rk.active_backend(), "pcsir", pcsir.__version__)

@@ -228,3 +228,12 @@ def test_poisson_models_sane():
     mu = 20.0 * ex * ex
     single = orc.loglik_poisson(np.full((1, 1), 10.0), [0.0], [0.0], [20.0], 1.5, 10.0, 0, 1)[0]
     assert single == pytest.approx(10.0 * math.log1p(mu / 10.0) - mu, rel=1e-12)
+
+
+# --- scene synthesis (synthesis.py:124-130) ------------------------------------
+def test_render_ideal_matches_reference_golden():
+    g = golden("synth")
+    h, w = g["frames"].shape[1:]
+    for s, f in zip(g["states"], g["frames"]):
+        got = orc.render_ideal(s[[0, 1, 4]][None, :], w, h, float(g["sigma"]), float(g["bg"]))
+        np.testing.assert_allclose(got, f, rtol=0, atol=1e-12)
