@@ -86,9 +86,24 @@ __device__ __forceinline__ double u128_to_f64_rn_scaled(u128 v, int s) {
   return __dmul_rn(__ull2double_rn(t), __longlong_as_double((i64)(1023 + 64 - lz - s) << 52));
 }
 
+// RN64(v) * 2^-s for a signed 128-bit v (fast path when the result is a
+// normal number, scalbn otherwise); same value as scalbn(i128_to_f64_rn(v), -s)
+__device__ __forceinline__ double i128_to_f64_scaled(i128 v, int s);
+
 __host__ __device__ __forceinline__ double i128_to_f64_rn(i128 v) {
   if (v < 0) return -u128_to_f64_rn((u128)(-v));
   return u128_to_f64_rn((u128)v);
+}
+
+__device__ __forceinline__ double i128_to_f64_scaled(i128 v, int s) {
+  const bool neg = v < 0;
+  const u128 a = neg ? (u128)(-v) : (u128)v;
+  const u64 hi = (u64)(a >> 64);
+  const int lz = hi ? __clzll((long long)hi) : 64 + __clzll((long long)(u64)a);
+  if (a == 0) return 0.0;
+  if (1023 + 127 - lz - s <= 0) return scalbn(i128_to_f64_rn(v), -s);   // subnormal result
+  const double r = u128_to_f64_rn_scaled(a, s);
+  return neg ? -r : r;
 }
 
 // CANONICAL: round(m * 2^s) for a non-negative integer significand m,

@@ -826,12 +826,21 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   PCS_PROBE(5);
   bins_sum_k<6>(e, sm.red);
   PCS_PROBE(6);
-  if (t == 0) {
-    double est[5];
+  // warp 0 holds the six exact sums in every lane: lane c converts sum c
+  double conv = 0.0;
+  if (t < 32) {
+    const int c = min(t, 5);
+    i128 ec = e[0];
 #pragma unroll
-    for (int c = 0; c < 5; ++c) est[c] = scalbn(i128_to_f64_rn(e[c]), -(FX_WQ + FX_STATE));
-    const double w2f = scalbn(i128_to_f64_rn(e[5]), -FX_W2);
-    const double ess = 1.0 / w2f;
+    for (int q = 1; q < 6; ++q) ec = (c == q) ? e[q] : ec;
+    conv = i128_to_f64_scaled(ec, c < 5 ? FX_WQ + FX_STATE : FX_W2);
+    if (c == 5) conv = 1.0 / conv;   // ESS
+  }
+  double est[5];
+#pragma unroll
+  for (int c = 0; c < 5; ++c) est[c] = __shfl_sync(0xffffffffu, conv, c);
+  const double ess = __shfl_sync(0xffffffffu, conv, 5);
+  if (t == 0) {
     const bool flag_bad = degenerate || bad_m;
     if (degenerate) set_flag(C, PCS_FLAG_DEGENERATE);
     if (bad_m) set_flag(C, PCS_FLAG_NONFINITE);
