@@ -576,7 +576,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
 // reduction is warp shuffles + one barrier + a warp-parallel final sum, and
 // the control-block reads of the epilogue are issued at kernel entry.
 // ===========================================================================
-constexpr int BINS_BLOCK = 1024;
+constexpr int BINS_BLOCK = 512;
 #define PCS_PROBE(i)                                                                  \
   do {                                                                                \
     if (threadIdx.x == 0) {                                                           \
@@ -790,9 +790,13 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   {
     i128 acc[1] = {0};
     for (int b = t; b < M; b += BINS_BLOCK)
-      acc[0] += (i128)V.cnt(b) * f64_to_fixed(exp(__dsub_rn(sm.ll[b], m)), FX_S);
+    {
+      const double ex = exp(__dsub_rn(sm.ll[b], m));
+      sm.ll[b] = ex;   // the weights below reuse exp(ll - m)
+      acc[0] += (i128)V.cnt(b) * f64_to_fixed(ex, FX_S);
+    }
     bins_sum_k<1>(acc, sm.red);
-    if (t == 0) s_Sf = scalbn(i128_to_f64_rn(acc[0]), -FX_S);
+    if (t == 0) s_Sf = i128_to_f64_scaled(acc[0], FX_S);
     __syncthreads();
   }
   const double Sf = s_Sf;
@@ -804,16 +808,20 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     for (int b = t; b < M; b += BINS_BLOCK) {
       const u32 cell = V.cell(b);
       const u32 cnt = V.cnt(b);
-      const float w = normalised_weight(sm.ll[b], m, Sf);
+      // the cell's state sums first: their HBM/L2 latency overlaps the division
+      i128 Ssum[5];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) Ssum[c] = load_i128(P.tab_sum + ((i64)c * P.G + cell) * 2);
+      const float w = __double2float_rn(__ddiv_rn(sm.ll[b], Sf));   // normalised_weight
       P.wtab[cell] = w;
       P.wfix[cell] = cdf_fixed(w);
       wmin = min(wmin, __float_as_uint(w));
       wmax = max(wmax, __float_as_uint(w));
-      const i128 wq = f32_to_fixed(w, FX_WQ);
+      const long long wq = (long long)f32_to_fixed(w, FX_WQ);   // w <= 1: fits 63 bits
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
+        e[c] += (i128)wq * Ssum[c];
         u64* p = P.tab_sum + ((i64)c * P.G + cell) * 2;
-        e[c] += wq * load_i128(p);
         p[0] = 0;
         p[1] = 0;
       }
