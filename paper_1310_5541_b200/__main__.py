@@ -1,4 +1,4 @@
-"""Command line: ``python -m paper_1310_5541_b200 {backends,track}``.
+"""Command line: ``python -m paper_1310_5541_b200 {backends,track,pseudo}``.
 
 ``backends`` times the device likelihood operator on the reference CLI's
 micro-benchmark workloads (cli.py:191-213); ``track`` runs a GPU tracking
@@ -25,6 +25,13 @@ def main(argv=None):
     t.add_argument("--sigma-xi", type=float, default=10.0)
     t.add_argument("--seed", type=int, default=0)
     t.add_argument("--out", default="gpu_tracking_summary.csv")
+    q = sub.add_parser("pseudo", help="GPU pseudo-tracking convergence study -> summary CSV")
+    q.add_argument("--variants", default="SIR,pcSIR-1x1-CoM,pcSIR-2x2-CoM")
+    q.add_argument("--n", default="100,1000,10000")
+    q.add_argument("--reps", type=int, default=100)
+    q.add_argument("--prior", default="uniform3x3")
+    q.add_argument("--seed", type=int, default=0)
+    q.add_argument("--out", default="gpu_pseudo_summary.csv")
     args = ap.parse_args(argv)
 
     from . import experiments as ex
@@ -34,6 +41,20 @@ def main(argv=None):
         return 0
     from .imaging import PsfParams
     from .synthesis import SceneConfig
+    if args.cmd == "pseudo":
+        try:
+            records = ex.run_pseudo_tracking(args.variants.split(","),
+                                             [int(x) for x in args.n.split(",") if x], args.reps,
+                                             prior=args.prior, seed=args.seed)
+        except (ex.ConfigError, ValueError) as e:
+            print(f"error: {e}", file=sys.stderr)
+            return 2
+        rows = ex.summarize(records)
+        for r in rows:
+            print(f"{r.variant:>16s} N={r.n_particles:>8d} rms error={r.rmse_mean:.4f} "
+                  f"evals={r.lik_evals_mean:.0f}")
+        print(f"wrote {ex.write_summary_csv(rows, args.out)}")
+        return 0
     try:
         ns = [int(x) for x in args.n.split(",") if x]
         scene = SceneConfig(PsfParams(1.5, 10.0), frames=args.frames, width=args.size,

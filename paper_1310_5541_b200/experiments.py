@@ -24,12 +24,14 @@ from pathlib import Path
 import numpy as np
 import torch
 
-from .binning import BinGrid, DummyPlacement, PcFilterConfig, pcsir_track
-from .filtering import DegenerateWeightsError, FilterConfig, ResampleConfig, sir_track
-from .imaging import LikelihoodParams, PsfParams, SpotLikelihood
+from .binning import (BinGrid, DummyPlacement, PcFilterConfig, dummy_states_device,
+                      partition_device, pcsir_track)
+from .filtering import (DegenerateWeightsError, FilterConfig, ResampleConfig, _check_not_degenerate,
+                        _evaluate_loglik, _weight_update, normalize, posterior_mean, sir_track)
+from .imaging import ImageFrame, LikelihoodParams, PsfParams, SpotLikelihood
 from .kernels import spot_window_ssd
 from .rng import PhiloxRng
-from .state import DynamicsParams, InitSpec, StateVector
+from .state import DynamicsParams, InitSpec, ParticleSet, StateVector, init_particle_set
 from . import synthesis as syn
 
 VARIANT_LABELS = ("SIR", "pcSIR-1x1-CoM", "pcSIR-1x1-CoC", "pcSIR-2x2-CoM", "pcSIR-2x2-CoC")
@@ -196,6 +198,90 @@ def run_tracking_experiment(variants, n_particles, repetitions, scene=None, sigm
     return records
 
 
+PSEUDO_PRIORS = ("uniform3x3", "uniform5x5", "gauss0.5", "gauss0.8")
+
+
+def parse_prior(label, center: StateVector) -> InitSpec:
+    """'point', 'uniform<w>[x<w>]' or 'gauss<s>' (experiments.py:73-90)."""
+    token = label.strip().lower().replace("(", "").replace(")", "")
+    try:
+        if token == "point":
+            return InitSpec(center, "point")
+        if token.startswith("uniform"):
+            return InitSpec(center, "uniform", width=float(token[7:].split("x")[0]))
+        if token.startswith("gauss"):
+            return InitSpec(center, "gauss", sigma=float(token[5:]))
+    except ValueError:
+        pass
+    raise ConfigError(f"unknown prior {label!r}")
+
+
+def pseudo_weight_once(pset: ParticleSet, frame, lik, spec: VariantSpec, grid=None,
+                       weighted_com=False) -> ParticleSet:
+    """One likelihood weighting of a particle cloud, no dynamics
+    (experiments.py:295-310): SIR weights every particle; pcSIR bins,
+    evaluates the dummies and broadcasts."""
+    if not spec.is_pc:
+        logw = _weight_update(pset, _evaluate_loglik(lik, pset.soa, frame))
+    else:
+        part = partition_device(pset.soa, grid)
+        prior_w = pset.weights_f32().contiguous() if weighted_com else None
+        dummies = dummy_states_device(pset.soa, grid, part, spec.placement, prior_w)
+        logw = _weight_update(pset, _evaluate_loglik(lik, dummies, frame), part.bin_of)
+    _check_not_degenerate(logw)
+    return ParticleSet.from_device(pset.soa, logw=logw, timestep=1)
+
+
+def run_pseudo_tracking(variants, n_particles, repetitions, prior="uniform3x3", scene=None,
+                        sigma_xi=10.0, window_halfwidth=5, i0=20.0, seed=0, weighted_com=False,
+                        progress=None):
+    """Single-frame convergence study (experiments.py:313-359) on the GPU.
+
+    Per (N, repetition): a noise-free spot at a sub-pixel offset from the
+    frame centre (all repetitions of an N rendered in one device call), a
+    fresh cloud from the prior, weighted once through every variant; the
+    record's error is |weighted-mean position - truth|."""
+    scene = scene or syn.SceneConfig(PsfParams(1.5, 10.0), frames=1, width=64, height=64,
+                                     noise=False)
+    specs = [parse_variant(v) for v in variants]
+    ns = list(n_particles)
+    if not ns or any(n < 1 for n in ns) or repetitions < 1:
+        raise ConfigError("n_particles must be nonempty and >= 1, repetitions >= 1")
+    cx, cy = (scene.width - 1) / 2.0, (scene.height - 1) / 2.0
+    parse_prior(prior, StateVector(cx, cy, 0.0, 0.0, i0))
+    records = []
+    for n in ns:
+        offs = np.array([np.random.default_rng(derive_seed(seed, "pseudo", prior, n, r))
+                         .uniform(-0.5, 0.5, size=2) for r in range(repetitions)])
+        spots = np.stack([cx + offs[:, 0], cy + offs[:, 1], np.full(repetitions, i0)], axis=1)
+        frames = syn.render_frames(spots, scene.width, scene.height, scene.psf, noise=False)
+        for rep in range(repetitions):
+            truth = StateVector(spots[rep, 0], spots[rep, 1], 0.0, 0.0, i0)
+            frame = ImageFrame(frames[rep])
+            base = init_particle_set(n, parse_prior(prior, truth),
+                                     PhiloxRng(derive_seed(seed, "cloud", prior, n, rep)))
+            for spec in specs:
+                lik = SpotLikelihood(scene.psf, LikelihoodParams(sigma_xi, window_halfwidth))
+                grid = (BinGrid.pixel_aligned(scene.width, scene.height, spec.cells_per_pixel)
+                        if spec.is_pc else None)
+                torch.cuda.synchronize()
+                start = time.perf_counter()
+                try:
+                    w = normalize(pseudo_weight_once(base, frame, lik, spec, grid, weighted_com))
+                    est = posterior_mean(w)
+                except DegenerateWeightsError:
+                    records.append(RunRecord("pseudo_tracking", spec.label, n, rep, float("nan"),
+                                             time.perf_counter() - start, lik.evals, failed=True))
+                    continue
+                elapsed = time.perf_counter() - start
+                err = float(np.hypot(est[0] - truth.x, est[1] - truth.y))
+                records.append(RunRecord("pseudo_tracking", spec.label, n, rep, err, elapsed,
+                                         lik.evals))
+                if progress is not None:
+                    progress(records[-1])
+    return records
+
+
 def _mean_std(values):
     if not values:
         return float("nan"), float("nan")
@@ -219,6 +305,9 @@ def summarize(records) -> list:
     for variant, n in order:
         recs = [r for r in groups[(variant, n)] if not r.failed]
         rmse_mean, rmse_std = _mean_std([r.rmse for r in recs])
+        if groups[(variant, n)][0].experiment == "pseudo_tracking":   # single-shot errors
+            errs = [r.rmse for r in recs]
+            rmse_mean = math.sqrt(sum(e * e for e in errs) / len(errs)) if errs else float("nan")
         t_mean, t_std = _mean_std([r.wall_time_s for r in recs])
         ev_mean, _ = _mean_std([r.lik_evals for r in recs])
         rows.append(SummaryRow(groups[(variant, n)][0].experiment, variant, n, rmse_mean, rmse_std,

@@ -77,3 +77,32 @@ def test_cli_backends_and_track(cuda, tmp_path, capsys):
                  "--frames", "4", "--size", "64", "--out", str(csv)]) == 0
     assert csv.read_text().startswith(",".join(ex.SUMMARY_COLUMNS))
     assert main(["track", "--variants", "bogus"]) == 2
+
+
+def test_parse_prior_and_pseudo_summary():
+    c = ex.StateVector(1.0, 2.0, 0.0, 0.0, 20.0)
+    assert ex.parse_prior("uniform3x3", c).width == 3.0
+    assert ex.parse_prior("gauss0.8", c).sigma == 0.8
+    assert ex.parse_prior("point", c).mode == "point"
+    with pytest.raises(ex.ConfigError):
+        ex.parse_prior("cauchy1", c)
+    R = ex.RunRecord
+    rows = ex.summarize([R("pseudo_tracking", "SIR", 10, 0, 3.0, 1.0, 10),
+                         R("pseudo_tracking", "SIR", 10, 1, 4.0, 1.0, 10)])
+    assert rows[0].rmse_mean == math.sqrt(12.5)   # RMS of single-shot errors
+
+
+@pytest.mark.gpu
+def test_gpu_pseudo_tracking(cuda):
+    recs = ex.run_pseudo_tracking(["SIR", "pcSIR-1x1-CoM", "pcSIR-2x2-CoC"], [300, 30000], 12,
+                                  prior="uniform3x3", seed=1)
+    assert len(recs) == 2 * 12 * 3 and not any(r.failed for r in recs)
+    rows = {(r.variant, r.n_particles): r for r in ex.summarize(recs)}
+    for v in ("SIR", "pcSIR-1x1-CoM", "pcSIR-2x2-CoC"):
+        assert rows[(v, 30000)].rmse_mean < rows[(v, 300)].rmse_mean
+    # the 1x1 grid cannot resolve sub-pixel offsets better than SIR at large N
+    assert rows[("SIR", 30000)].rmse_mean < 0.1
+    assert rows[("pcSIR-1x1-CoM", 30000)].lik_evals_mean <= 16
+    again = ex.run_pseudo_tracking(["pcSIR-1x1-CoM"], [300], 2, prior="uniform3x3", seed=1)
+    assert [r.rmse for r in again] == [r.rmse for r in recs
+                                       if r.variant == "pcSIR-1x1-CoM" and r.n_particles == 300][:2]
