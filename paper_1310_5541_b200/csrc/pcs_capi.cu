@@ -1,9 +1,12 @@
 // pcs_capi.cu — extern "C" boundary of libpcsir_b200.so (see include/pcsir_b200.h).
 //
 // Host-side launch logic only; all arithmetic lives in the .cuh device code.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <climits>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -122,6 +125,7 @@ enum Slot {
   SL_MT_HASH,
   SL_MT_OUT,
   SL_SYNTH,
+  SL_FMAP,
   SL_COUNT
 };
 
@@ -675,7 +679,8 @@ __global__ void k_ctl_init(TrackCtl* C, double cx, double cy) {
 }
 
 __global__ void k_ctl_io(TrackCtl* C, const float* frames, i64 kf, i64 ko, double* est,
-                         double* ess, unsigned char* res, i64* occ) {
+                         double* ess, unsigned char* res, i64* occ, int fmap_ok = 0) {
+  C->fmap_ok = fmap_ok;
   C->frames = frames;
   C->k_frames = kf;
   C->k_out = ko;
@@ -839,6 +844,7 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   PCS_SCRATCH(SL_TR_ANC, ld * sizeof(int), P.anc);
   P.anc_out = P.anc;
   PCS_SCRATCH(SL_TR_CTL, sizeof(TrackCtl), P.ctl);
+  PCS_SCRATCH(SL_FMAP, 128, P.fmap);
   P.ntiles = ceil_div(n, SCAN_TILE);
   PCS_SCRATCH(SL_TR_TILES, P.ntiles * (2 * sizeof(u128) + sizeof(u32)) + 64, P.tile_agg);
   P.tile_inc = P.tile_agg + P.ntiles;
@@ -929,6 +935,38 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   return PCS_OK;
 }
 
+// TMA descriptor of a batch of frames [K][H][W] float32 (boxes FMAP_BX x
+// FMAP_BY x 1), written to the track's device slot; 0 if unavailable (the
+// kernels then stage with plain loads)
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode_tiled = nullptr;
+static int frame_map(TrackState& T, const float* frames, i64 nframes, cudaStream_t st) {
+  static const bool disabled = getenv("PCS_NO_TMA") != nullptr;
+  if (disabled) return 0;
+  if (!g_encode_tiled) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+      return 0;
+    g_encode_tiled = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  }
+  const i64 W = T.P.W, H = T.P.H;
+  if (!T.P.fmap || nframes < 1 || (W * 4) % 16 || ((uintptr_t)frames) % 16) return 0;
+  CUtensorMap m;
+  cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)nframes};
+  cuuint64_t strides[2] = {(cuuint64_t)(W * 4), (cuuint64_t)(W * H * 4)};
+  cuuint32_t box[3] = {FMAP_BX, FMAP_BY, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  if (g_encode_tiled(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)frames, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return 0;
+  if (cudaMemcpyAsync((void*)T.P.fmap, &m, sizeof(m), cudaMemcpyHostToDevice, st) != cudaSuccess)
+    return 0;
+  return 1;
+}
+
 int pcs_track_steps(pcs_ctx* ctx, const float* frames, int64_t k0, int64_t k1, double* est,
                     double* ess, uint8_t* res, int64_t* occ, void* stream) {
   PCS_CHECK_ARG(ctx && ctx->tr.active, "no active track (call pcs_track_begin)");
@@ -936,7 +974,8 @@ int pcs_track_steps(pcs_ctx* ctx, const float* frames, int64_t k0, int64_t k1, d
   PCS_CHECK_ARG(k0 == ctx->tr.k && k1 >= k0, "frames must be stepped in order");
   cudaStream_t st = S(stream);
   TrackState& T = ctx->tr;
-  k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frames, k0, k0, est, ess, res, (i64*)occ);
+  const int fm = frame_map(T, frames, k1 - k0, st);
+  k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frames, k0, k0, est, ess, res, (i64*)occ, fm);
   PCS_LAUNCH_CHECK();
   for (i64 k = k0; k < k1; ++k) {
     if (T.exec) {
@@ -959,7 +998,8 @@ int pcs_track_steps_timed(pcs_ctx* ctx, const float* frames, int64_t k0, int64_t
   PCS_CHECK_ARG(k0 == ctx->tr.k && k1 >= k0, "frames must be stepped in order");
   cudaStream_t st = S(stream);
   TrackState& T = ctx->tr;
-  k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frames, k0, k0, est, ess, res, (i64*)occ);
+  const int fm = frame_map(T, frames, k1 - k0, st);
+  k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frames, k0, k0, est, ess, res, (i64*)occ, fm);
   PCS_LAUNCH_CHECK();
   const int NE = 8;
   cudaEvent_t evs[NE];

@@ -92,6 +92,7 @@ struct TrackCtl {
   unsigned long long tile_ctr;  // decoupled look-back: monotone tile ticket counter
   u64 rank_prefix[2];        // sharded: exact cumulative weight of the preceding ranks
   u32 gbar_cnt, gbar_gen;    // grid barrier of k_sys_resample
+  int fmap_ok;               // P.fmap describes the current frame batch (TMA staging)
 };
 
 struct TrackParams {
@@ -128,6 +129,8 @@ struct TrackParams {
   int* anc_out;              // ancestors (local particle index) for slots slot_lo + k
   int scan_mode;             // 0 scan+emit, 1 scan only, 2 emit only (rank prefix in ctl)
   int s1_tile;               // k_pc_step1 tile (<= S1_TILE), balanced over its CTAs
+  const void* fmap;          // device CUtensorMap of the frame batch [K][H][W] f32,
+                             // boxes of FMAP_BX x FMAP_BY pixels (TMA staging)
   u128* cta_agg;             // k_sys_resample: per-CTA exact weight totals
 };
 
@@ -576,6 +579,41 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
 // reduction is warp shuffles + one barrier + a warp-parallel final sum, and
 // the control-block reads of the epilogue are issued at kernel entry.
 // ===========================================================================
+// ---- TMA staging of frame regions (cp.async.bulk.tensor.3d + mbarrier) ----
+constexpr int FMAP_BX = 64, FMAP_BY = 16;   // box = 64 x 16 float32 pixels (4 KB)
+
+__device__ __forceinline__ void tma_frame_box(float* dst, const void* fmap, int x, int y, int z,
+                                              unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+      "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"((u32)__cvta_generic_to_shared(dst)),
+      "l"(fmap), "r"(x), "r"(y), "r"(z), "r"((u32)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
+// Stage rows [y0, y0 + 16 nb) x columns [x0, x0 + 64) of frame z into dst
+// (pitch 64; out-of-frame pixels arrive as zeros and are never read; x0 must
+// be a multiple of 4: box origins are 16-byte aligned, tools/tma_probe.cu).
+// One thread arms the mbarrier and issues the nb box copies; every thread waits.
+// issue (thread 0 only)
+__device__ __forceinline__ void tma_stage_issue(float* dst, const void* fmap, int x0, int y0, int z,
+                                                int nb, unsigned long long* bar) {
+  const u32 b = (u32)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
+               "r"((u32)(nb * FMAP_BX * FMAP_BY * 4)) : "memory");
+  for (int j = 0; j < nb; ++j)
+    tma_frame_box(dst + j * FMAP_BX * FMAP_BY, fmap, x0, y0 + j * FMAP_BY, z, bar);
+}
+// wait (every thread; after a barrier that orders it behind the issue)
+__device__ __forceinline__ void tma_stage_wait(unsigned long long* bar) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tTMA_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
+      "@!p bra TMA_WAIT_%=;\n\t}" ::"r"((u32)__cvta_generic_to_shared(bar)) : "memory");
+}
+
 constexpr int BINS_BLOCK = 512;
 #define PCS_PROBE(i)                                                                  \
   do {                                                                                \
@@ -597,6 +635,7 @@ struct BinsSmem {
   u32 cnt[BINS_SM];
   u32 cell[BINS_SM];
   i128 red[BINS_BLOCK / 32 * 6];
+  unsigned long long tma_bar;
 };
 constexpr size_t BINS_SMEM = sizeof(BinsSmem);
 
@@ -644,7 +683,7 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   pdl_wait();
   pdl_trigger();   // k_sys_resample CTAs may become resident on the other SMs
   PCS_PROBE(8);
-  extern __shared__ __align__(16) unsigned char bins_raw[];
+  extern __shared__ __align__(128) unsigned char bins_raw[];
   BinsSmem& sm = *reinterpret_cast<BinsSmem*>(bins_raw);
   const BinsView V{sm, Sd};
   __shared__ long long s_max;
@@ -683,6 +722,18 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     u_next = philox_resample_u(P.seed, P.frame0 + (u32)k);
   }
   const float* frame = C->frames + (k - C->k_frames) * P.H * P.W;
+  // TMA prefetch of a 64 x 64 frame region around the previous estimate into
+  // the staging buffer, in flight while the dummies are computed (used in
+  // step 2 if it covers every likelihood window)
+  const bool tma = C->fmap_ok;
+  int txa = 0, tya = 0;
+  if (tma) {
+    txa = (int)min(max((i64)floor(C->center[0]) - FMAP_BX / 2, (i64)0), max(P.W - FMAP_BX, (i64)0)) & ~3;
+    tya = (int)min(max((i64)floor(C->center[1]) - FMAP_BX / 2, (i64)0), max(P.H - FMAP_BX, (i64)0));
+    if (t == 0)
+      tma_stage_issue(sm.pix, P.fmap, txa, tya, (int)(k - C->k_frames), FMAP_BX / FMAP_BY,
+                      &sm.tma_bar);
+  }
   PCS_PROBE(0);
   if (t == 0) {
     s_max = LLONG_MIN;
@@ -722,12 +773,21 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   atomicMin(&s_box[2], by0); atomicMax(&s_box[3], by1);
   __syncthreads();
   PCS_PROBE(1);
-  // 2) stage the frame region covering every window in shared memory
+  // 2) stage the frame region covering every window in shared memory: TMA
+  //    boxes of 64 x 16 pixels when the region is at most 64 px wide, plain
+  //    loads otherwise
   PixView pv = frame_view(frame, P.H, P.W);
   {
     const int x0 = s_box[0], y0 = s_box[2];
     const i64 wx = (i64)s_box[1] - x0 + 1, wy = (i64)s_box[3] - y0 + 1;
-    if (s_box[1] >= s_box[0] && wx * wy <= STAGE_PIX) {
+    if (tma) tma_stage_wait(&sm.tma_bar);   // (the buffer may be overwritten below)
+    if (s_box[1] >= s_box[0] && tma && x0 >= txa && s_box[1] < txa + FMAP_BX && y0 >= tya &&
+        s_box[3] < tya + FMAP_BX) {
+      pv.base = sm.pix;
+      pv.pitch = FMAP_BX;
+      pv.x0 = txa;
+      pv.y0 = tya;
+    } else if (s_box[1] >= s_box[0] && wx * wy <= STAGE_PIX) {
       for (int p = t; p < (int)(wx * wy); p += BINS_BLOCK) {
         const int yy = p / (int)wx, xx = p % (int)wx;
         sm.pix[p] = __ldg(frame + (i64)(y0 + yy) * P.W + (x0 + xx));
