@@ -23,22 +23,41 @@ constexpr int SIR_SW = 64;
 
 template <int MAXS>
 __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
-  __shared__ float stg[SIR_SW * SIR_SW];
+  __shared__ __align__(128) float stg[SIR_SW * SIR_SW];
+  __shared__ __align__(8) unsigned long long tma_bar;
   TrackCtl* C = P.ctl;
   const i64 k = C->k;
   const float* sin = (k & 1) ? P.buf1 : P.buf0;
   float* sout = (k & 1) ? P.buf0 : P.buf1;
   const float* frame = C->frames + (k - C->k_frames) * P.H * P.W;
   const PixView pv = frame_view(frame, P.H, P.W);
-  const int sw = (int)min((i64)SIR_SW, P.W), sh = (int)min((i64)SIR_SW, P.H);
-  const int sx0 = (int)min(max((i64)floor(C->center[0]) - sw / 2, (i64)0), P.W - sw);
-  const int sy0 = (int)min(max((i64)floor(C->center[1]) - sh / 2, (i64)0), P.H - sh);
-  for (int p = threadIdx.x; p < sw * sh; p += blockDim.x)
-    stg[p] = __ldg(frame + (i64)(sy0 + p / sw) * P.W + (sx0 + p % sw));
-  __syncthreads();
   PixView ps = pv;
+  int sx0, sy0, sw, sh;
+  if (C->fmap_ok) {
+    // 64 x 64 region by TMA (4 boxes of 64 x 16; x origin 16-byte aligned;
+    // pixels beyond the frame arrive as zeros and are never read)
+    sw = SIR_SW;
+    sh = SIR_SW;
+    sx0 = (int)min(max((i64)floor(C->center[0]) - SIR_SW / 2, (i64)0), max(P.W - SIR_SW, (i64)0)) & ~3;
+    sy0 = (int)min(max((i64)floor(C->center[1]) - SIR_SW / 2, (i64)0), max(P.H - SIR_SW, (i64)0));
+    if (threadIdx.x == 0)
+      tma_stage_issue(stg, P.fmap, sx0, sy0, (int)(k - C->k_frames), SIR_SW / FMAP_BY, &tma_bar);
+    __syncthreads();
+    tma_stage_wait(&tma_bar);
+    sw = (int)min((i64)SIR_SW, P.W - sx0);   // valid columns / rows for the inside test
+    sh = (int)min((i64)SIR_SW, P.H - sy0);
+    ps.pitch = SIR_SW;
+  } else {
+    sw = (int)min((i64)SIR_SW, P.W);
+    sh = (int)min((i64)SIR_SW, P.H);
+    sx0 = (int)min(max((i64)floor(C->center[0]) - sw / 2, (i64)0), P.W - sw);
+    sy0 = (int)min(max((i64)floor(C->center[1]) - sh / 2, (i64)0), P.H - sh);
+    for (int p = threadIdx.x; p < sw * sh; p += blockDim.x)
+      stg[p] = __ldg(frame + (i64)(sy0 + p / sw) * P.W + (sx0 + p % sw));
+    __syncthreads();
+    ps.pitch = sw;
+  }
   ps.base = stg;
-  ps.pitch = sw;
   ps.x0 = sx0;
   ps.y0 = sy0;
   long long lmax = LLONG_MIN;
