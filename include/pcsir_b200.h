@@ -196,6 +196,8 @@ typedef struct pcs_track_cfg_t {
   uint64_t seed;
   uint32_t frame0;       /* frame counter offset for the RNG streams */
   int32_t use_graph;     /* capture one frame as a CUDA graph and replay it */
+  double threshold_fraction;  /* resample when ESS < threshold_fraction * N
+                                 (filtering.py:169-170); 0 means 1.0 */
 } pcs_track_cfg_t;
 
 typedef struct pcs_track_result_t {

@@ -126,6 +126,7 @@ enum Slot {
   SL_MT_OUT,
   SL_SYNTH,
   SL_FMAP,
+  SL_TR_WPREV,
   SL_COUNT
 };
 
@@ -851,8 +852,14 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   P.tile_status = (u32*)(P.tile_inc + P.ntiles);
   P.cta_agg = P.tile_agg;   // k_sys_resample: rs_grid <= ntiles aggregates
   PCS_CUDA_TRY(cudaMemsetAsync(P.tile_status, 0, P.ntiles * sizeof(u32), st));
+  {
+    const double frac = cfg->threshold_fraction > 0.0 ? cfg->threshold_fraction : 1.0;
+    PCS_CHECK_ARG(frac <= 1.0, "threshold_fraction must be in (0, 1]");
+    P.thresh = frac * (double)n;   // the reference's threshold_fraction * n_particles
+  }
   if (cfg->method == 0) {
     PCS_SCRATCH(SL_TR_LL, ld * sizeof(double), P.ll);
+    PCS_SCRATCH(SL_TR_WPREV, ld * sizeof(float), P.wprev);
     P.pslot = nullptr;
   } else {
     PCS_SCRATCH(SL_TR_PSLOT, ld * sizeof(u32), P.pslot);

@@ -93,6 +93,8 @@ struct TrackCtl {
   u64 rank_prefix[2];        // sharded: exact cumulative weight of the preceding ranks
   u32 gbar_cnt, gbar_gen;    // grid barrier of k_sys_resample
   int fmap_ok;               // P.fmap describes the current frame batch (TMA staging)
+  int prior_nonuniform;      // SIR: particles carry the prior weights wprev (no resampling
+                             // at the previous frame, weights not all equal)
 };
 
 struct TrackParams {
@@ -129,6 +131,8 @@ struct TrackParams {
   int* anc_out;              // ancestors (local particle index) for slots slot_lo + k
   int scan_mode;             // 0 scan+emit, 1 scan only, 2 emit only (rank prefix in ctl)
   int s1_tile;               // k_pc_step1 tile (<= S1_TILE), balanced over its CTAs
+  double thresh;             // resample when ESS < thresh (= threshold_fraction * N)
+  float* wprev;              // SIR: normalised prior weights when prior_nonuniform
   const void* fmap;          // device CUtensorMap of the frame batch [K][H][W] f32,
                              // boxes of FMAP_BX x FMAP_BY pixels (TMA staging)
   u128* cta_agg;             // k_sys_resample: per-CTA exact weight totals
@@ -914,7 +918,7 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     if (bad_m) set_flag(C, PCS_FLAG_NONFINITE);
     for (int c = 0; c < 5; ++c) out_est[ko * 5 + c] = est[c];
     out_ess[ko] = ess;
-    const int res = (!flag_bad && ess < (double)P.n) ? 1 : 0;   // threshold_fraction = 1.0
+    const int res = (!flag_bad && ess < P.thresh) ? 1 : 0;   // filtering.py:169-170
     // no resampling with unequal weights -> non-uniform prior next frame:
     // only the general path carries per-particle prior weights
     if (!res && !flag_bad && s_wmin != s_wmax) set_flag(C, PCS_FLAG_CAPACITY);
@@ -1274,9 +1278,13 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
   const int G = gridDim.x, cta = blockIdx.x;
   const i64 t0 = nt * cta / G, t1 = nt * (cta + 1) / G;
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  if (!C->do_resample) {   // identity ancestors, weights stay uniform (all equal)
-    for (i64 i = t0 * RS_TILE + threadIdx.x; i < min(n, t1 * RS_TILE); i += SCAN_BLOCK)
+  if (!C->do_resample) {   // identity ancestors; SIR keeps the normalised weights
+    const bool keep = (KIND == 2) && C->prior_nonuniform;
+    const double m = C->m, Sf = C->Sf;
+    for (i64 i = t0 * RS_TILE + threadIdx.x; i < min(n, t1 * RS_TILE); i += SCAN_BLOCK) {
       P.anc_out[P.idx_off + i - P.slot_lo] = (int)i;
+      if (keep) P.wprev[i] = normalised_weight(P.ll[i], m, Sf);
+    }
     return;
   }
   const double m = C->m, Sf = C->Sf, u = C->u;

@@ -82,6 +82,8 @@ __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
     v.x0 = inside ? ps.x0 : 0;
     v.y0 = inside ? ps.y0 : 0;
     double ll = loglik_dispatch<MAXS>(v, o[0], o[1], o[4], P.spot);
+    // log w = log(w_prev) + ll (k_weight_update, binning.py:190-192 / filtering.py:69)
+    if (C->prior_nonuniform) ll = __dadd_rn(log((double)P.wprev[j]), ll);
     P.ll[j] = ll;
     if (!(ll == ll) || ll == INFINITY) bad = true;
     lmax = max(lmax, (long long)f64_to_ordered(ll));
@@ -173,8 +175,10 @@ __global__ void k_sir_finalize(TrackParams P) {
   bool flag_bad = degenerate || bad_m;
   if (degenerate) set_flag(C, PCS_FLAG_DEGENERATE);
   if (bad_m) set_flag(C, PCS_FLAG_NONFINITE);
-  int res = (!flag_bad && ess < (double)P.n) ? 1 : 0;
-  if (!res && !flag_bad && C->wmin_bits != C->wmax_bits) set_flag(C, PCS_FLAG_CAPACITY);
+  int res = (!flag_bad && ess < P.thresh) ? 1 : 0;   // filtering.py:169-170
+  // without resampling the next frame starts from these weights unless they
+  // are all equal (then uniform, as the general driver does)
+  C->prior_nonuniform = (!res && !flag_bad && C->wmin_bits != C->wmax_bits) ? 1 : 0;
   C->out_res[ko] = (unsigned char)res;
   C->out_occ[ko] = P.n;
   C->evals += P.n;

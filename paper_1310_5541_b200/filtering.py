@@ -285,6 +285,7 @@ def fused_track(frames, cfg: FilterConfig, rng, method, grid=None, placement=0, 
     c.seed = prng.seed
     c.frame0 = frame0
     c.use_graph = 1 if use_graph else 0
+    c.threshold_fraction = cfg.resampling.threshold_fraction
     dev = dev_frames.device
     est = torch.empty((k, 5), dtype=torch.float64, device=dev)
     ess = torch.empty(k, dtype=torch.float64, device=dev)
@@ -314,11 +315,19 @@ def _fused_ok(cfg):
             and r.scheme == "systematic" and cfg.n_particles < 2 ** 31 - 1)
 
 
+def _fused_sir_ok(cfg):
+    """The fused SIR loop also runs ESS-threshold resampling (threshold < 1):
+    per-particle prior weights stay on the device between frames."""
+    r = cfg.resampling
+    return (isinstance(cfg.likelihood, _DeviceLikelihood) and r.scheme == "systematic"
+            and cfg.n_particles < 2 ** 31 - 1)
+
+
 def sir_track(frames, cfg: FilterConfig, rng, fused=None) -> TrackResult:
     """Classical SIR: one likelihood evaluation per particle per frame (filtering.py:176-182)."""
     prng = as_philox(rng)
     if fused is None:
-        fused = _fused_ok(cfg)
+        fused = _fused_sir_ok(cfg)
     if fused:
         start = (prng.seed, prng.frame)
         try:

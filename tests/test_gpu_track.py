@@ -186,6 +186,23 @@ def test_fused_resampling_many_tiles_heavy_weights(cuda, method):
     assert np.array_equal(a.resampled, b.resampled)
 
 
+@pytest.mark.parametrize("frac", [0.2, 0.5])
+def test_fused_sir_threshold_resampling_equals_general(cuda, frac):
+    # ESS-threshold resampling on the device (filtering.py:169-170): frames
+    # that do not resample carry their normalised weights into the next
+    # update (log w = log w_prev + ll) without a host round trip
+    frames, truth, init, dyn = _c1_like(n=3000, k=12)
+    res = pc.ResampleConfig(frac, "systematic")
+    a = pc.sir_track(frames, pc.FilterConfig(3000, init, dyn, res, _lik()), pc.PhiloxRng(4))
+    b = pc.sir_track(frames, pc.FilterConfig(3000, init, dyn, res, _lik()), pc.PhiloxRng(4),
+                     fused=False)
+    assert a.path == "fused" and b.path == "general"
+    assert 0 < int(np.sum(a.resampled)) < len(frames)   # both kinds of frames occur
+    assert np.array_equal(a.resampled, b.resampled)
+    assert np.array_equal(a.estimates, b.estimates)
+    assert np.array_equal(a.ess, b.ess)
+
+
 def test_pcsir_tiny_cells_bitidentical_to_sir(cuda):
     # SPEC acceptance #1 / test_binning.py:208-226: 1e-5 px cells (64-bit keys)
     frames, truth, init, dyn = _c1_like(n=500, k=10)
