@@ -1305,21 +1305,22 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
   }
   __syncthreads();
   if (threadIdx.x == 0 && mt > 0) issue(0);
-  // exact weight of item k of the ring buffer holding tile `b0`
-  auto weight = [&](const E* buf, int k, i64 i) -> u128 {
-    if (i >= n) return 0;
+  // exact weight of item k of a ring buffer (nv = valid items of its tile)
+  auto weight = [&](const E* buf, int k, int nv) -> u128 {
+    if (k >= nv) return 0;
     if (KIND == 1) return P.wfix[(u32)buf[k]];
     return cdf_fixed(normalised_weight((double)buf[k], m, Sf));
   };
+  auto tile_items = [&](i64 tile) -> int { return (int)min((i64)RS_TILE, n - tile * RS_TILE); };
   // ---- pass 1: this CTA's exact total ----
   u128 acc = 0;
   for (int L = 0; L < mt; ++L) {
     mbar_wait(&bar[L & 1], (u32)((L >> 1) & 1));
     if (threadIdx.x == 0 && L + 1 < 2 * mt) issue(L + 1);
     const E* buf = ring[L & 1];
-    const i64 i0 = (t0 + L) * RS_TILE + (i64)threadIdx.x * RS_ITEMS;
+    const int nv = tile_items(t0 + L);
 #pragma unroll 5
-    for (int q = 0; q < RS_ITEMS; ++q) acc += weight(buf, threadIdx.x * RS_ITEMS + q, i0 + q);
+    for (int q = 0; q < RS_ITEMS; ++q) acc += weight(buf, threadIdx.x * RS_ITEMS + q, nv);
     __syncthreads();   // buffer L & 1 is free for load L + 2
   }
   {
@@ -1370,10 +1371,13 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
     const E* buf = ring[L & 1];
     int* hp = (KIND == 1) ? reinterpret_cast<int*>(ring[L & 1]) : hp_own;
     const i64 base = (t0 + (L - mt)) * RS_TILE;
-    const i64 i0 = base + k0;
+    const int nv = tile_items(t0 + (L - mt));
+    // local index of the globally last item (its run ends at slot ng), -1 if not here
+    const i64 kl = ng - 1 - off - base;
+    const int klast = (kl >= 0 && kl < nv) ? (int)kl : -1;
     u128 tsum = 0;
 #pragma unroll 5
-    for (int q = 0; q < RS_ITEMS; ++q) tsum += weight(buf, k0 + q, i0 + q);
+    for (int q = 0; q < RS_ITEMS; ++q) tsum += weight(buf, k0 + q, nv);
     u128 inc = tsum;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -1390,35 +1394,34 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
     }
     const u128 excl = pre + woff + (inc - tsum);
     if (threadIdx.x == 0) {
-      const i64 tl = min(n, base + (i64)RS_TILE) - 1;
       s_jr[0] = (off + base == 0) ? 0 : first_slot_fast(cdf_round(pre), u, ng, nd, eps);
-      s_jr[1] = (off + tl == ng - 1) ? ng : first_slot_fast(cdf_round(pre + tagg), u, ng, nd, eps);
+      s_jr[1] = (klast == nv - 1) ? ng : first_slot_fast(cdf_round(pre + tagg), u, ng, nd, eps);
     }
     __syncthreads();
     const i64 tj0 = s_jr[0], tj1 = s_jr[1];
-    // run head of every item: its first slot relative to tj0, INT_MAX if none
+    // run head of every item: its first slot relative to tj0, -1 if none
     {
       int jr = 0;
-      if (i0 < n) jr = (int)(((off + i0 == 0) ? 0 : slot_of_prefix(excl, u, ng, nd, kappa, eps)) - tj0);
+      if (k0 < nv) jr = (int)(((off + base + k0 == 0) ? 0 : slot_of_prefix(excl, u, ng, nd, kappa, eps)) - tj0);
       u128 run = excl;
       for (int q = 0; q < RS_ITEMS; ++q) {
-        const i64 i = i0 + q;
-        int h = INT_MAX;
-        if (i < n) {
-          run += weight(buf, k0 + q, i);
-          const int jend = (int)(((off + i == ng - 1) ? ng : slot_of_prefix(run, u, ng, nd, kappa, eps)) - tj0);
+        const int k = k0 + q;
+        int h = -1;   // no slot
+        if (k < nv) {
+          run += weight(buf, k, nv);
+          const int jend = (k == klast) ? (int)(ng - tj0) : (int)(slot_of_prefix(run, u, ng, nd, kappa, eps) - tj0);
           if (jend > jr) h = jr;
           jr = jend;
         }
-        hp[k0 + q] = h;            // (KIND 1: over item k0 + q, already read)
-        stage[k0 + q] = -1;        // first chunk's fill
+        hp[k] = h;            // (KIND 1: over item k, already read)
+        stage[k] = -1;        // first chunk's fill
       }
     }
     __syncthreads();   // every read of ring[L & 1] is done; it is free for load L + 2
     // slots in chunks of RS_TILE: heads, block max-scan, coalesced writes
-    const i64 m_slots = tj1 - tj0;
+    const int m_slots = (int)(tj1 - tj0);   // <= ng < 2^31
     int carry = -1;
-    for (i64 c0 = 0; c0 < m_slots; c0 += RS_TILE) {
+    for (int c0 = 0; c0 < m_slots; c0 += RS_TILE) {
       if (c0 > 0) {
 #pragma unroll
         for (int q = 0; q < RS_ITEMS; ++q) stage[k0 + q] = -1;
@@ -1426,8 +1429,8 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
       }
 #pragma unroll
       for (int q = 0; q < RS_ITEMS; ++q) {
-        const int h = hp[k0 + q];
-        if ((i64)h >= c0 && (i64)h < c0 + RS_TILE) stage[(int)((i64)h - c0)] = k0 + q;
+        const u32 hr = (u32)(hp[k0 + q] - c0);   // no head: (u32)(-1 - c0) >= 2^31
+        if (hr < (u32)RS_TILE) stage[hr] = k0 + q;
       }
       __syncthreads();
       int tmax = -1;
@@ -1456,11 +1459,18 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
         stage[k0 + q] = runm;
       }
       __syncthreads();
-      const int cm = (int)min((i64)RS_TILE, m_slots - c0);
-      for (int k = threadIdx.x; k < cm; k += SCAN_BLOCK) {
-        const i64 kk = tj0 + c0 + k - lo;
-        if (kk >= 0 && kk < cap) P.anc_out[kk] = (int)(base + stage[k]);
-        else oob = true;
+      const int cm = min(RS_TILE, m_slots - c0);
+      const i64 w0 = tj0 + c0 - lo;   // output position of the chunk's first slot
+      const int ib = (int)base;
+      if (w0 >= 0 && w0 + cm <= cap) {
+        int* dst = P.anc_out + w0;
+        for (int k = threadIdx.x; k < cm; k += SCAN_BLOCK) dst[k] = ib + stage[k];
+      } else {
+        for (int k = threadIdx.x; k < cm; k += SCAN_BLOCK) {
+          const i64 kk = w0 + k;
+          if (kk >= 0 && kk < cap) P.anc_out[kk] = ib + stage[k];
+          else oob = true;
+        }
       }
       carry = total;
       __syncthreads();

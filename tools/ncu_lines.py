@@ -11,8 +11,10 @@ import sys
 import tempfile
 
 rep, kregex, so = sys.argv[1], sys.argv[2], os.path.abspath(sys.argv[3])
+# LAUNCH=k (env): the k-th captured launch of the kernel (1-based)
+skip = ["--launch-skip", str(int(os.environ.get("LAUNCH", "1")) - 1)]
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name",
-                      f"regex:{kregex}", "--print-source", "sass"], capture_output=True,
+                      f"regex:{kregex}", *skip, "--print-source", "sass"], capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[1]
