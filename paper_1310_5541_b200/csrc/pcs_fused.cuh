@@ -1181,6 +1181,27 @@ __device__ __forceinline__ i64 slot_of_prefix(u128 Pc, double u, i64 ng, double 
   if (gap > eps && gap < 1.0 - eps && g > 0.0 && g < nd) return (i64)g;
   return first_slot_fast(cdf_round(Pc), u, ng, nd, eps);
 }
+// the exact path of slot_of_prefix out of line (keeps the unrolled hot loop small)
+__device__ __noinline__ i64 slot_of_prefix_slow(u128 Pc, double u, i64 ng, double nd, double eps) {
+  return first_slot_fast(cdf_round(Pc), u, ng, nd, eps);
+}
+// slot_of_prefix - base as int for a tile whose slots lie in [base, base + 2^31)
+__device__ __forceinline__ int slot_rel(u128 Pc, double u, i64 ng, double nd, double kappa, double eps,
+                                        double based, i64 base) {
+  const double t = fma((double)(u64)(Pc >> 57), kappa, -u);
+  const double g = ceil(t);
+  const double gap = g - t;
+  if (gap > eps && gap < 1.0 - eps && g > 0.0 && g < nd) return __double2int_rz(g - based);
+  return (int)(slot_of_prefix_slow(Pc, u, ng, nd, eps) - base);
+}
+__device__ __forceinline__ void sts_u32(u32 addr, int v) {
+  asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ int lds_u32(u32 addr) {
+  int v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+  return v;
+}
 
 // Persistent reduce-then-scan systematic resampling (single GPU, scan_mode 0).
 // Each CTA owns a contiguous range of tiles (RS_TILE = 3840 particles). Pass
@@ -1401,36 +1422,40 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
     const i64 tj0 = s_jr[0], tj1 = s_jr[1];
     // run head of every item: its first slot relative to tj0, -1 if none
     {
+      const double tj0d = (double)tj0;
       int jr = 0;
-      if (k0 < nv) jr = (int)(((off + base + k0 == 0) ? 0 : slot_of_prefix(excl, u, ng, nd, kappa, eps)) - tj0);
+      if (k0 < nv && off + base + k0 != 0) jr = slot_rel(excl, u, ng, nd, kappa, eps, tj0d, tj0);
       u128 run = excl;
+      const u32 hp_s = smem_u32(hp + k0), st_s = smem_u32(stage + k0);
+#pragma unroll
       for (int q = 0; q < RS_ITEMS; ++q) {
         const int k = k0 + q;
         int h = -1;   // no slot
         if (k < nv) {
           run += weight(buf, k, nv);
-          const int jend = (k == klast) ? (int)(ng - tj0) : (int)(slot_of_prefix(run, u, ng, nd, kappa, eps) - tj0);
+          const int jend = (k == klast) ? (int)(ng - tj0) : slot_rel(run, u, ng, nd, kappa, eps, tj0d, tj0);
           if (jend > jr) h = jr;
           jr = jend;
         }
-        hp[k] = h;            // (KIND 1: over item k, already read)
-        stage[k] = -1;        // first chunk's fill
+        sts_u32(hp_s + 4 * q, h);    // (KIND 1: over item k, already read)
+        sts_u32(st_s + 4 * q, -1);   // first chunk's fill
       }
     }
     __syncthreads();   // every read of ring[L & 1] is done; it is free for load L + 2
     // slots in chunks of RS_TILE: heads, block max-scan, coalesced writes
     const int m_slots = (int)(tj1 - tj0);   // <= ng < 2^31
     int carry = -1;
+    const u32 stage_s = smem_u32(stage), hp_s = smem_u32(hp + k0);
     for (int c0 = 0; c0 < m_slots; c0 += RS_TILE) {
       if (c0 > 0) {
 #pragma unroll
-        for (int q = 0; q < RS_ITEMS; ++q) stage[k0 + q] = -1;
+        for (int q = 0; q < RS_ITEMS; ++q) sts_u32(stage_s + 4 * (k0 + q), -1);
         __syncthreads();
       }
 #pragma unroll
       for (int q = 0; q < RS_ITEMS; ++q) {
-        const u32 hr = (u32)(hp[k0 + q] - c0);   // no head: (u32)(-1 - c0) >= 2^31
-        if (hr < (u32)RS_TILE) stage[hr] = k0 + q;
+        const u32 hr = (u32)(lds_u32(hp_s + 4 * q) - c0);   // no head: (u32)(-1 - c0) >= 2^31
+        if (hr < (u32)RS_TILE) sts_u32(stage_s + 4 * hr, k0 + q);
       }
       __syncthreads();
       int tmax = -1;
@@ -1462,7 +1487,12 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
       const int cm = min(RS_TILE, m_slots - c0);
       const i64 w0 = tj0 + c0 - lo;   // output position of the chunk's first slot
       const int ib = (int)base;
-      if (w0 >= 0 && w0 + cm <= cap) {
+      if (cm == RS_TILE && w0 >= 0 && w0 + cm <= cap) {
+        int* dst = P.anc_out + w0 + threadIdx.x;
+        const u32 src_s = stage_s + 4 * threadIdx.x;
+#pragma unroll
+        for (int q = 0; q < RS_ITEMS; ++q) dst[q * SCAN_BLOCK] = ib + lds_u32(src_s + 4 * q * SCAN_BLOCK);
+      } else if (w0 >= 0 && w0 + cm <= cap) {
         int* dst = P.anc_out + w0;
         for (int k = threadIdx.x; k < cm; k += SCAN_BLOCK) dst[k] = ib + stage[k];
       } else {
