@@ -200,11 +200,14 @@ __device__ __forceinline__ i64 cell_axis_fast(float p, double origin, double cel
 // float32 estimate t32 = (p - o32) * inv32 is accepted when its fractional
 // part is farther from an integer than the margin
 //   general:            ((|p| + |o32|)|inv32| + |t32| + 1) 2^-20 (cell_axis_fast)
-//   pow2 cell, o32 = o: |t32| 2^-22
+//   pow2 cell, o32 = o: 0, i.e. t32 not an integer
 // (with a power-of-two cell and a float32-exact origin the product is exact
-// and the only error is the rounding of p - o32, <= ulp(t32)/2), and only
-// inside [0, min(n-1, 2^24)]; everything else (near-integer quotients,
-// clamping, NaN) takes the float64 path. Same result as cell_axis_fast.
+// and the only error is the round-to-nearest of p - o32; rounding is
+// monotone and the cell edges o + k l are float32 values, so the rounded
+// quotient has the exact quotient's floor unless it lands exactly ON an
+// integer), and only inside [0, min(n-1, 2^24)]; everything else (integer
+// quotients, clamping, NaN) takes the float64 path. Same result as
+// cell_axis_fast.
 struct AxisFast {
   float o32, inv32, mt, ma, mb, fmax;
   double origin, cell, inv;
@@ -219,7 +222,7 @@ __device__ __forceinline__ AxisFast make_axis(double origin, double cell, double
   const bool pow2 = frexp(inv, &e) == 0.5 && __dmul_rn(cell, inv) == 1.0 &&
                     (double)a.inv32 == inv && (double)a.o32 == origin && e > -100 && e < 100;
   if (pow2) {
-    a.mt = 2.384185791015625e-07f;   // 2^-22
+    a.mt = 0.0f;
     a.ma = 0.0f;
     a.mb = 0.0f;
   } else {

@@ -203,6 +203,71 @@ def test_fused_sir_threshold_resampling_equals_general(cuda, frac):
     assert np.array_equal(a.ess, b.ess)
 
 
+def _rounding_edge_positions(cpp, ncols):
+    """Cell edges b and the float32 positions just below them whose float32
+    p - origin rounds ONTO the edge (a float32 cell estimate that trusted
+    them would put them in b's cell; binning.py:61-67 puts them below)."""
+    out, n_bad = [], 0
+    for k in range(1, ncols):
+        b = np.float32(-0.5 + k / cpp)
+        below = []
+        p = b
+        for _ in range(6):
+            p = np.nextafter(p, np.float32(-np.inf))
+            t32 = np.float32(np.float32(p + np.float32(0.5)) * np.float32(cpp))
+            if np.floor(t32) != np.floor((float(p) + 0.5) * cpp):
+                below.append(p)
+        if below:
+            out += [b] + below
+            n_bad += len(below)
+    assert n_bad > 0
+    return np.array(out, dtype=np.float32)
+
+
+@pytest.mark.parametrize("cpp", [1, 2, 4])
+def test_fused_step_cell_edges_exact(cuda, cpp):
+    """binning.py:61-67 cell_indices on positions at and just below cell edges:
+    the fused step's occupied-cell count equals the float64 count."""
+    from paper_1310_5541_b200 import _lib
+    import ctypes
+    xs = _rounding_edge_positions(cpp, 16 * cpp)
+    n = 2 * len(xs)
+    st = np.zeros((n, 5), dtype=np.float32)
+    st[:, 4] = 20.0
+    st[: len(xs), 0], st[: len(xs), 1] = xs, np.float32(7.3)     # edges along x
+    st[len(xs):, 0], st[len(xs):, 1] = np.float32(7.3), xs       # edges along y
+    grid = pc.BinGrid.pixel_aligned(16, 16, cpp)
+    want = len({(int(np.floor((float(x) + 0.5) * cpp)), int(np.floor((float(y) + 0.5) * cpp)))
+                for x, y in st[:, :2]})
+    c = _lib.PcsTrackCfg()
+    c.method, c.placement, c.n_particles = 1, 0, n
+    c.init = pc.InitSpec(pc.StateVector(8, 8, 0, 0, 20.0), "point").to_c()
+    c.dyn = pc.DynamicsParams(0.0, 0.0, 0.0).to_c()   # states stay exactly as written
+    c.spot = _lik().spot_c()
+    c.grid = grid.to_c()
+    c.seed, c.frame0, c.use_graph, c.threshold_fraction = 3, 0, 0, 1.0
+    frame = torch.full((1, 16, 16), 10.0, dtype=torch.float32, device="cuda")
+    ctx, stream = _lib.ctx(), _lib.stream()
+    _lib.check(_lib.lib().pcs_track_begin(ctx, ctypes.byref(c), 16, 16, stream))
+    sp, ld = ctypes.c_void_p(), ctypes.c_int64()
+    _lib.check(_lib.lib().pcs_track_states(ctx, ctypes.byref(sp), ctypes.byref(ld)))
+    buf = torch.zeros((5, ld.value), dtype=torch.float32, device="cuda")
+    buf[:, :n] = torch.from_numpy(np.ascontiguousarray(st.T)).cuda()
+    ident = torch.arange(n, dtype=torch.int32, device="cuda")
+    # overwrite the initial cloud with the crafted states (SoA, stride ld)
+    _lib.check(_lib.lib().pcs_gather(_lib.ptr(buf), sp.value, ld.value, n, _lib.ptr(ident), stream))
+    est = torch.empty((1, 5), dtype=torch.float64, device="cuda")
+    ess = torch.empty(1, dtype=torch.float64, device="cuda")
+    res = torch.empty(1, dtype=torch.uint8, device="cuda")
+    occ = torch.empty(1, dtype=torch.int64, device="cuda")
+    _lib.check(_lib.lib().pcs_track_steps(ctx, _lib.ptr(frame), 0, 1, _lib.ptr(est), _lib.ptr(ess),
+                                          _lib.ptr(res), _lib.ptr(occ), stream))
+    out = _lib.PcsTrackResult()
+    _lib.check(_lib.lib().pcs_track_end(ctx, ctypes.byref(out), stream))
+    torch.cuda.synchronize()
+    assert int(occ[0]) == want
+
+
 def test_pcsir_tiny_cells_bitidentical_to_sir(cuda):
     # SPEC acceptance #1 / test_binning.py:208-226: 1e-5 px cells (64-bit keys)
     frames, truth, init, dyn = _c1_like(n=500, k=10)
