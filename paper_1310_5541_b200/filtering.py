@@ -237,6 +237,8 @@ def _track(frames, cfg: FilterConfig, rng, step_fn):
     ess_log = np.empty(len(frames))
     resampled = np.zeros(len(frames), dtype=bool)
     for k, frame in enumerate(frames):
+        if not isinstance(frame, ImageFrame):   # rows of a (K,H,W) array / tensor
+            frame = ImageFrame(frame)
         try:
             pset = step_fn(pset, frame, prng, frame0 + k)
             pset = normalize(pset)
@@ -254,11 +256,21 @@ def _track(frames, cfg: FilterConfig, rng, step_fn):
 
 
 def _frames_to_device(frames):
-    """Stack frames into one (K,H,W) float32 device tensor (pinned H2D)."""
+    """One (K,H,W) float32 device tensor of the frames. Accepts a list of
+    ImageFrame / 2D arrays, a (K,H,W) array, or a (K,H,W) torch tensor (a
+    pinned float32 host tensor is copied asynchronously on the current
+    stream, which the filter kernels run on)."""
     if isinstance(frames, torch.Tensor):
-        return frames.to(_lib.device(), dtype=torch.float32).contiguous()
-    host = np.stack([np.asarray(f.pixels if isinstance(f, ImageFrame) else f, dtype=np.float32)
-                     for f in frames])
+        t = frames if frames.dtype == torch.float32 else frames.float()
+        t = t.contiguous()
+        if t.is_cuda:
+            return t
+        return t.to(_lib.device(), non_blocking=t.is_pinned())
+    if isinstance(frames, np.ndarray) and frames.ndim == 3:
+        host = np.ascontiguousarray(frames, dtype=np.float32)
+    else:
+        host = np.stack([f.pixels if isinstance(f, ImageFrame) else np.asarray(f) for f in frames],
+                        dtype=np.float32)
     t = torch.from_numpy(host)
     if torch.cuda.is_available():
         t = t.pin_memory()

@@ -89,9 +89,10 @@ class MultiTargetTracker:
 
 def multi_pcsir_track(frames, cfg, centers, seed, target_offset=0):
     """T independent pcSIR filters (config 4) on the device; frames (K,H,W)."""
-    dev_frames = frames if isinstance(frames, torch.Tensor) else torch.from_numpy(
+    t = frames if isinstance(frames, torch.Tensor) else torch.from_numpy(
         np.ascontiguousarray(np.asarray(frames, dtype=np.float32)))
-    dev_frames = dev_frames.to(_lib.device(), dtype=torch.float32).contiguous()
+    t = (t if t.dtype == torch.float32 else t.float()).contiguous()
+    dev_frames = t if t.is_cuda else t.to(_lib.device(), non_blocking=t.is_pinned())
     k, h, w = dev_frames.shape
     tr = MultiTargetTracker(cfg, centers, seed, k, h, w, target_offset)
     for f in range(k):
