@@ -1076,6 +1076,10 @@ int pcs_mt_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t n_targets,
   PCS_CHECK_ARG(cfg->method == 1, "multi-target filter is pcSIR");
   PCS_CHECK_ARG(cfg->n_particles >= 1 && (double)cfg->n_particles * n_targets < 2.0e9,
                 "too many particles for 32-bit ancestors");
+  // a cell gets <= 2 digit additions per warp per tile and the digits are never
+  // flushed inside a frame: <= MT_MAX_TILES tiles keep them exact
+  PCS_CHECK_ARG(cfg->n_particles <= (i64)MT_MAX_TILES * MT_TILE,
+                "too many particles per target for the multi-target kernel");
   int r = check_spot(&cfg->spot);
   if (r) return r;
   r = check_grid(&cfg->grid);

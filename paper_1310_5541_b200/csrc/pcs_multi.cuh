@@ -23,14 +23,25 @@
 
 namespace pcs {
 
+// Two CTAs per SM (<= 64 registers, < 113 KB shared memory each): the
+// sub-window is 24 x 24 cells (a c4 cloud spans a few pixels; cells outside
+// it go to the exact per-target hash), and the phase-A tile, the phase-B
+// cell arrays and the phase-C scan buffers share one union.
 constexpr int MT_THREADS = 512;
-constexpr int MT_IPT = 4;
-constexpr int MT_TILE = MT_THREADS * MT_IPT;   // 2048
+constexpr int MT_IPT = 2;
+constexpr int MT_TILE = MT_THREADS * MT_IPT;   // 1024
 constexpr int MT_WARPS = MT_THREADS / 32;
-constexpr int MT_SUBW = 1024;                  // sub-window cells (32 x 32)
+constexpr int MT_SIDE = 24;
+constexpr int MT_SUBW = MT_SIDE * MT_SIDE;     // sub-window cells (24 x 24)
 constexpr int MT_HCAP = 2048;                  // per-target outlier hash capacity
 constexpr int MT_MAXM = 2048;                  // occupied cells per target per frame
 constexpr int MT_STAGE = 4096;                 // staged frame pixels
+constexpr int MT_CI = 5;                       // phase C: items per thread (stride 5: conflict-free)
+constexpr int MT_CT = MT_THREADS * MT_CI;      // phase C: 2560 particles per scan tile
+// phase A digit accumulators: <= 2 additions per warp per tile and cell, each
+// < 2^18 (unsigned digits) / < 2^17 in magnitude (signed top digit), over at
+// most 256 tiles: 256 * 32 * 2^18 = 2^31 (n <= 262144 particles per target)
+constexpr int MT_MAX_TILES = 256;
 constexpr u64 MT_KEY_STEP = 0x9E3779B97F4A7C15ull;
 
 struct MtTarget {
@@ -78,19 +89,28 @@ struct MtSmem {
   u32 dig[15][MT_SUBW];
   u32 acc_cnt[MT_SUBW];
   u32 tile_cnt[MT_SUBW];
+  u128 wfix_sub[MT_SUBW];          // exact cdf weight round(w 2^120) per sub-window cell
   unsigned short tile_start[MT_SUBW];
-  float ref[MT_SUBW + 1];          // sub-window cell edges (x then y; NaN: unusable)
-  float pay[5][MT_TILE];
-  unsigned short pay_q[MT_TILE];
-  unsigned short list[MT_TILE];
+  float ref[2 * MT_SIDE + 1];      // sub-window cell edges (x then y; NaN: unusable)
+  union {
+    struct {                       // phase A: the cell-sorted tile
+      float pay[5][MT_TILE];
+      unsigned short pay_q[MT_TILE];
+      unsigned short list[MT_TILE];
+    } a;
+    struct {                       // phase B: occupied cells, dummies, staged frame
+      int occ[MT_MAXM];            // >= 0: sub-window cell, < 0: -(hash slot) - 1
+      double ll[MT_MAXM];
+      float dpix[MT_STAGE];
+    } b;
+    struct {                       // phase C: staged cells, run heads, slot stage
+      u32 cells[MT_CT];
+      int hp[MT_CT];
+      int stage[MT_CT];
+    } c;
+  } u;
   u32 n_list, n_in;
   int scan_tmp[MT_WARPS];
-  // phase B/C (reuse is not attempted: the struct fits in shared memory)
-  float w_sub[MT_SUBW];
-  u128 wfix_sub[MT_SUBW];          // exact cdf weight round(w 2^120) per sub-window cell
-  int occ[MT_MAXM];      // >= 0: sub-window cell, < 0: -(hash slot) - 1
-  double ll[MT_MAXM];
-  float dpix[MT_STAGE];
   i128 red[MT_WARPS * 6];
   long long lmax;
   int box[4];
@@ -121,7 +141,7 @@ __device__ __forceinline__ bool mt_hash_add(MtHash* H, u32 flat, const float o[5
 }
 
 template <int MAXS>
-__global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
+__global__ void __launch_bounds__(MT_THREADS, 2) k_mt_frame(MtParams P) {
   extern __shared__ __align__(16) unsigned char mt_raw[];
   MtSmem& sm = *reinterpret_cast<MtSmem*>(mt_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -137,7 +157,7 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
   MtHash* HT = P.hash + tg * MT_HCAP;
 
   // ---------------- phase A: propagate + exact per-cell sums -------------------
-  const i64 snx = min((i64)32, g.ncols), sny = min((i64)32, g.nrows);
+  const i64 snx = min((i64)MT_SIDE, g.ncols), sny = min((i64)MT_SIDE, g.nrows);
   const i64 cx = cell_axis_fast((float)TG.center[0], g.ox, g.lx, P.inv_lx, g.ncols);
   const i64 cy = cell_axis_fast((float)TG.center[1], g.oy, g.ly, P.inv_ly, g.nrows);
   const i64 sx0 = min(max(cx - snx / 2, (i64)0), g.ncols - snx);
@@ -210,7 +230,7 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
           fabsf(o[4]) < 128.0f) {
         const int q = ly * snxi + lx;
         const int r = (int)atomicAdd(&sm.tile_cnt[q], 1u);
-        if (r == 0) sm.list[atomicAdd(&sm.n_list, 1u)] = (unsigned short)q;
+        if (r == 0) sm.u.a.list[atomicAdd(&sm.n_list, 1u)] = (unsigned short)q;
         q_k[it] = q;
         r_k[it] = r;
         o_k[it][0] = dx;
@@ -222,14 +242,14 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
       }
     }
     __syncthreads();
-    // run offsets: exclusive scan of the tile's cell counts (4 entries / thread)
+    // run offsets: exclusive scan of the tile's cell counts (MT_IPT entries / thread)
     {
       const int nl = (int)sm.n_list;
-      const int e0 = 4 * t;
-      int loc[4], sum = 0;
+      const int e0 = MT_IPT * t;
+      int loc[MT_IPT], sum = 0;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        loc[e] = (e0 + e < nl) ? (int)sm.tile_cnt[sm.list[e0 + e]] : 0;
+      for (int e = 0; e < MT_IPT; ++e) {
+        loc[e] = (e0 + e < nl) ? (int)sm.tile_cnt[sm.u.a.list[e0 + e]] : 0;
         sum += loc[e];
       }
       int inc = sum;
@@ -246,9 +266,9 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
       for (int d = 16; d > 0; d >>= 1) woff += __shfl_xor_sync(0xffffffffu, woff, d);
       int run = woff + inc - sum;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
+      for (int e = 0; e < MT_IPT; ++e) {
         if (e0 + e < nl) {
-          const int q = sm.list[e0 + e];
+          const int q = sm.u.a.list[e0 + e];
           sm.tile_start[q] = (unsigned short)run;
           sm.tile_cnt[q] = 0;
           sm.acc_cnt[q] += (u32)loc[e];
@@ -265,11 +285,11 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
       const int pos = (int)sm.tile_start[q_k[it]] + r_k[it];
       const int idx = (pos % MT_IPT) * MT_THREADS + pos / MT_IPT;
 #pragma unroll
-      for (int c = 0; c < 5; ++c) sm.pay[c][idx] = o_k[it][c];
-      sm.pay_q[idx] = (unsigned short)q_k[it];
+      for (int c = 0; c < 5; ++c) sm.u.a.pay[c][idx] = o_k[it][c];
+      sm.u.a.pay_q[idx] = (unsigned short)q_k[it];
     }
     __syncthreads();
-    tile_run_sums<MT_THREADS, MT_IPT, MT_TILE, MT_SUBW>(sm.pay, sm.pay_q, (int)sm.n_in,
+    tile_run_sums<MT_THREADS, MT_IPT, MT_TILE, MT_SUBW>(sm.u.a.pay, sm.u.a.pay_q, (int)sm.n_in,
                                                         &sm.dig[0][0], t);
     __syncthreads();
   }
@@ -280,13 +300,13 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
   for (int q = t; q < (int)(snx * sny); q += MT_THREADS) {
     if (sm.acc_cnt[q]) {
       u32 idx = atomicAdd(&sm.n_occ, 1u);
-      if (idx < (u32)MT_MAXM) sm.occ[idx] = q;
+      if (idx < (u32)MT_MAXM) sm.u.b.occ[idx] = q;
     }
   }
   for (int s = t; s < MT_HCAP; s += MT_THREADS) {
     if (HT[s].key) {
       u32 idx = atomicAdd(&sm.n_occ, 1u);
-      if (idx < (u32)MT_MAXM) sm.occ[idx] = -s - 1;
+      if (idx < (u32)MT_MAXM) sm.u.b.occ[idx] = -s - 1;
     }
   }
   __syncthreads();
@@ -295,43 +315,48 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
     if (t == 0) atomicOr(&TG.flags, (u32)PCS_FLAG_CAPACITY);
     return;
   }
-  // dummies -> stored temporarily in pay[0..2][b] (phase A payload is free)
-  int bx0 = INT_MAX, bx1 = INT_MIN, by0 = INT_MAX, by1 = INT_MIN;
-  for (int b = t; b < M; b += MT_THREADS) {
-    int o = sm.occ[b];
+  // dummy (x, y, I0) of occupied cell b (computed where needed: the cell
+  // arrays stay small enough for two CTAs per SM)
+  auto dummy3 = [&](int b, float& x, float& y, float& i0) {
+    const int o = sm.u.b.occ[b];
     u32 cnt;
-    i128 S[5];
+    i128 S[3];
     i64 ix, iy;
     if (o >= 0) {
       cnt = sm.acc_cnt[o];
       ix = sx0 + o % snx;
       iy = sy0 + o / snx;
-#pragma unroll
-      for (int c = 0; c < 5; ++c) S[c] = digits_value<MT_SUBW>(&sm.dig[0][0], c, o);
-      S[0] += (i128)cnt * f32_to_fixed(sm.ref[o % snxi], FX_STATE);
-      S[1] += (i128)cnt * f32_to_fixed(refy[o / snxi], FX_STATE);
+      S[0] = digits_value<MT_SUBW>(&sm.dig[0][0], 0, o) + (i128)cnt * f32_to_fixed(sm.ref[o % snxi], FX_STATE);
+      S[1] = digits_value<MT_SUBW>(&sm.dig[0][0], 1, o) + (i128)cnt * f32_to_fixed(refy[o / snxi], FX_STATE);
+      S[2] = digits_value<MT_SUBW>(&sm.dig[0][0], 4, o);
     } else {
       const MtHash& h = HT[-o - 1];
       cnt = h.cnt;
       ix = (i64)(h.key - 1u) % g.ncols;
       iy = (i64)(h.key - 1u) / g.ncols;
-#pragma unroll
-      for (int c = 0; c < 5; ++c) S[c] = load_i128(h.sum[c]);
+      S[0] = load_i128(h.sum[0]);
+      S[1] = load_i128(h.sum[1]);
+      S[2] = load_i128(h.sum[4]);
     }
-    float d[5];
+    float d[3];
 #pragma unroll
-    for (int c = 0; c < 5; ++c)
+    for (int c = 0; c < 3; ++c)
       d[c] = __double2float_rn(scalbn(__ddiv_rn(i128_to_f64_rn(S[c]), (double)cnt), -FX_STATE));
     if (P.placement == 1) {
       d[0] = __double2float_rn(__dadd_rn(g.ox, __dmul_rn((double)ix + 0.5, g.lx)));
       d[1] = __double2float_rn(__dadd_rn(g.oy, __dmul_rn((double)iy + 0.5, g.ly)));
     }
-    sm.pay[0][b] = d[0];
-    sm.pay[1][b] = d[1];
-    sm.pay[2][b] = d[4];
-    if (d[0] == d[0] && d[1] == d[1]) {
+    x = d[0];
+    y = d[1];
+    i0 = d[2];
+  };
+  int bx0 = INT_MAX, bx1 = INT_MIN, by0 = INT_MAX, by1 = INT_MIN;
+  for (int b = t; b < M; b += MT_THREADS) {
+    float x, y, i0;
+    dummy3(b, x, y, i0);
+    if (x == x && y == y) {
       int xlo, xhi, ylo, yhi;
-      window_of(d[0], d[1], P.spot, P.H, P.W, xlo, xhi, ylo, yhi);
+      window_of(x, y, P.spot, P.H, P.W, xlo, xhi, ylo, yhi);
       bx0 = min(bx0, xlo); bx1 = max(bx1, xhi); by0 = min(by0, ylo); by1 = max(by1, yhi);
     }
   }
@@ -344,8 +369,8 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
     i64 wx = (i64)sm.box[1] - x0 + 1, wy = (i64)sm.box[3] - y0 + 1;
     if (sm.box[1] >= sm.box[0] && wx * wy <= MT_STAGE) {
       for (int p = t; p < (int)(wx * wy); p += MT_THREADS)
-        sm.dpix[p] = __ldg(P.frame + (i64)(y0 + p / (int)wx) * P.W + (x0 + p % (int)wx));
-      pv.base = sm.dpix;
+        sm.u.b.dpix[p] = __ldg(P.frame + (i64)(y0 + p / (int)wx) * P.W + (x0 + p % (int)wx));
+      pv.base = sm.u.b.dpix;
       pv.pitch = wx;
       pv.x0 = x0;
       pv.y0 = y0;
@@ -355,8 +380,10 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
   // likelihood once per occupied cell: one thread per cell, canonical order
   long long lmax = LLONG_MIN;
   for (int b = t; b < M; b += MT_THREADS) {
-    double ll = loglik_dispatch<MAXS>(pv, sm.pay[0][b], sm.pay[1][b], sm.pay[2][b], P.spot);
-    sm.ll[b] = ll;
+    float x, y, i0;
+    dummy3(b, x, y, i0);
+    double ll = loglik_dispatch<MAXS>(pv, x, y, i0, P.spot);
+    sm.u.b.ll[b] = ll;
     lmax = max(lmax, (long long)f64_to_ordered(ll));
   }
   atomicMax(&sm.lmax, lmax);
@@ -366,9 +393,9 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
   const bool degenerate = (m == -INFINITY);
   i128 acc1[1] = {0};
   for (int b = t; b < M; b += MT_THREADS) {
-    int o = sm.occ[b];
+    int o = sm.u.b.occ[b];
     u32 cnt = (o >= 0) ? sm.acc_cnt[o] : HT[-o - 1].cnt;
-    acc1[0] += (i128)cnt * f64_to_fixed(exp(__dsub_rn(sm.ll[b], m)), FX_S);
+    acc1[0] += (i128)cnt * f64_to_fixed(exp(__dsub_rn(sm.u.b.ll[b], m)), FX_S);
   }
   block_sum_i128_k<MT_THREADS, 1>(acc1, sm.red);
   if (t == 0) sm.Sf = scalbn(i128_to_f64_rn(acc1[0]), -FX_S);
@@ -376,14 +403,13 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
   const double Sf = sm.Sf;
   i128 e[6] = {0, 0, 0, 0, 0, 0};
   for (int b = t; b < M; b += MT_THREADS) {
-    int o = sm.occ[b];
-    float w = normalised_weight(sm.ll[b], m, Sf);
+    int o = sm.u.b.occ[b];
+    float w = normalised_weight(sm.u.b.ll[b], m, Sf);
     atomicMin(&sm.wmin, __float_as_uint(w));
     atomicMax(&sm.wmax, __float_as_uint(w));
     i128 wq = f32_to_fixed(w, FX_WQ);
     u32 cnt;
     if (o >= 0) {
-      sm.w_sub[o] = w;
       sm.wfix_sub[o] = cdf_fixed(w);
       cnt = sm.acc_cnt[o];
 #pragma unroll
@@ -442,12 +468,11 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
   // run heads + block max-scan, coalesced ancestor writes)
   const int do_res = s_res;
   const double u = philox_resample_u(seed_t, P.frame0 + (u32)k);
-  constexpr int CI = 5;                  // items per thread (stride-5 reads: conflict-free)
-  constexpr int CT = MT_THREADS * CI;    // 2560 particles per scan tile
-  static_assert(3 * CT * 4 <= 5 * MT_TILE * 4, "phase-C buffers alias the phase-A payload");
-  u32* cells = reinterpret_cast<u32*>(&sm.pay[0][0]);
-  int* hp = reinterpret_cast<int*>(cells + CT);
-  int* stage = hp + CT;
+  constexpr int CI = MT_CI;
+  constexpr int CT = MT_CT;
+  u32* cells = sm.u.c.cells;
+  int* hp = sm.u.c.hp;
+  int* stage = sm.u.c.stage;
   const double nd = (double)n, eps = nd * 8.881784197001252e-16;   // n * 2^-50
   const double kappa = nd * 1.0842021724855044e-19;                  // n * 2^-63
   // exact weight of a staged particle: sub-window cell table, else the hash
@@ -472,9 +497,10 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
       }
       continue;
     }
+    const int nv = (int)min((i64)CT, n - base);   // items of this scan tile
     for (int q = 0; q < CI; ++q) {
-      const i64 i = base + (i64)q * MT_THREADS + t;
-      cells[q * MT_THREADS + t] = (i < n) ? P.pslot[base_i + i] : 0xFFFFFFFFu;
+      const int idx = q * MT_THREADS + t;
+      cells[idx] = (idx < nv) ? P.pslot[base_i + base + idx] : 0xFFFFFFFFu;
     }
     __syncthreads();
     u128 tsum = 0;
@@ -494,37 +520,39 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
       tagg += sm.wtot[w];
     }
     const u128 excl = pre + woff + (inc - tsum);
-    const i64 tl = min(n, base + (i64)CT) - 1;
+    const bool last_tile = base + CT >= n;
     const i64 tj0 = (base == 0) ? 0 : first_slot_fast(cdf_round(pre), u, n, nd, eps);
-    const i64 tj1 = (tl == n - 1) ? n : first_slot_fast(cdf_round(pre + tagg), u, n, nd, eps);
-    const i64 i0 = base + k0;
+    const i64 tj1 = last_tile ? n : first_slot_fast(cdf_round(pre + tagg), u, n, nd, eps);
+    const int klast = last_tile ? nv - 1 : -1;   // the target's last particle ends at slot n
     {
+      const double tj0d = (double)tj0;
       int jr = 0;
-      if (i0 < n) jr = (int)(((i0 == 0) ? 0 : slot_of_prefix(excl, u, n, nd, kappa, eps)) - tj0);
+      if (k0 < nv && base + k0 != 0) jr = slot_rel(excl, u, n, nd, kappa, eps, tj0d, tj0);
       u128 run = excl;
+#pragma unroll
       for (int q = 0; q < CI; ++q) {
-        const i64 i = i0 + q;
-        int h = INT_MAX;
-        if (i < n) {
-          run += cellw(cells[k0 + q]);
-          const int jend = (int)(((i == n - 1) ? n : slot_of_prefix(run, u, n, nd, kappa, eps)) - tj0);
+        const int kk = k0 + q;
+        int h = -1;   // no slot
+        if (kk < nv) {
+          run += cellw(cells[kk]);
+          const int jend = (kk == klast) ? (int)(n - tj0) : slot_rel(run, u, n, nd, kappa, eps, tj0d, tj0);
           if (jend > jr) h = jr;
           jr = jend;
         }
-        hp[k0 + q] = h;
+        hp[kk] = h;
       }
     }
     __syncthreads();
-    const i64 m_slots = tj1 - tj0;
+    const int m_slots = (int)(tj1 - tj0);   // <= n < 2^31
     int carry = -1;
-    for (i64 c0 = 0; c0 < m_slots; c0 += CT) {
+    for (int c0 = 0; c0 < m_slots; c0 += CT) {
 #pragma unroll
       for (int q = 0; q < CI; ++q) stage[k0 + q] = -1;
       __syncthreads();
 #pragma unroll
       for (int q = 0; q < CI; ++q) {
-        const int h = hp[k0 + q];
-        if ((i64)h >= c0 && (i64)h < c0 + CT) stage[(int)((i64)h - c0)] = k0 + q;
+        const u32 hr = (u32)(hp[k0 + q] - c0);   // no head: (u32)(-1 - c0) >= 2^31
+        if (hr < (u32)CT) stage[hr] = k0 + q;
       }
       __syncthreads();
       int tmax = -1;
@@ -552,9 +580,10 @@ __global__ void __launch_bounds__(MT_THREADS, 1) k_mt_frame(MtParams P) {
         stage[k0 + q] = runm;
       }
       __syncthreads();
-      const int cm = (int)min((i64)CT, m_slots - c0);
+      const int cm = min(CT, m_slots - c0);
       int* out = P.anc + base_i + tj0 + c0;
-      for (int kk = t; kk < cm; kk += MT_THREADS) out[kk] = (int)(base + stage[kk]);
+      const int ib = (int)base;
+      for (int kk = t; kk < cm; kk += MT_THREADS) out[kk] = ib + stage[kk];
       carry = total;
       __syncthreads();
     }
