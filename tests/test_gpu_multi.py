@@ -19,7 +19,8 @@ def _cfg(n, cpp=1):
         grid=pc.BinGrid.pixel_aligned(160, 160, cpp))
 
 
-@pytest.mark.parametrize("cpp,n", [(1, 3000), (2, 5000)])
+@pytest.mark.parametrize("cpp,n", [(1, 3000), (2, 5000), (4, 4000)])   # cpp 4: many cells
+                                                                    # outside the 24x24 window
 def test_each_target_equals_single_target_filter(cuda, cpp, n):
     frames, truth = mt.multi_target_scene(12, 6, 160, seed=3)
     centers = truth[:, 0].copy()
@@ -48,3 +49,27 @@ def test_target_offset_selects_keys(cuda):
     full = mt.multi_pcsir_track(frames, _cfg(2000), centers, 5)
     half = mt.multi_pcsir_track(frames, _cfg(2000), centers[3:], 5, target_offset=3)
     assert np.array_equal(full.estimates[3:], half.estimates)
+
+
+def test_many_tiles_per_target(cuda):
+    # 200000 particles = 196 tiles per target (the digit accumulators are
+    # not flushed inside a frame)
+    frames, truth = mt.multi_target_scene(2, 3, 160, seed=5)
+    centers = truth[:, 0].copy()
+    n = 200_000
+    r = mt.multi_pcsir_track(frames, _cfg(n), centers, 7)
+    for t in range(2):
+        cfg_t = pc.PcFilterConfig(
+            n, pc.InitSpec(pc.StateVector(*centers[t]), "gauss", sigma=2.0),
+            pc.DynamicsParams(0.5, 0.1, 1.0), pc.ResampleConfig(1.0, "systematic"),
+            pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(10.0, 5)),
+            grid=pc.BinGrid.pixel_aligned(160, 160, 1))
+        single = pc.pcsir_track([pc.ImageFrame(f) for f in frames], cfg_t,
+                                pc.PhiloxRng(mt.target_seed(seed=7, t=t)))
+        assert np.array_equal(r.estimates[t], single.estimates), t
+
+
+def test_too_many_particles_per_target_rejected(cuda):
+    frames, truth = mt.multi_target_scene(1, 1, 160, seed=6)
+    with pytest.raises(Exception, match="too many particles per target"):
+        mt.multi_pcsir_track(frames, _cfg(262_145), truth[:, 0].copy(), 1)
