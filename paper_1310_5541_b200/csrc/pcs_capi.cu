@@ -899,7 +899,18 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
     T.bins.cell = (u32*)(sd + 4 * BINS_MAXM);
   }
   T.maxs = maxs_for(cfg->spot.halfwidth);
-  T.prop_grid = grid_for(n, 256, ctx->sms, 8);
+  {
+    // SIR propagate + likelihood: every resident CTA stages the frame region
+    // once and strides over the particles (no later waves re-staging it)
+    const void* f = T.maxs == 9    ? (const void*)k_sir_propagate_lik<9>
+                    : T.maxs == 11 ? (const void*)k_sir_propagate_lik<11>
+                    : T.maxs == 15 ? (const void*)k_sir_propagate_lik<15>
+                                   : (const void*)k_sir_propagate_lik<0>;
+    int per_sm = 1;
+    PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, 256, 0));
+    T.prop_grid = (int)std::min<i64>((i64)grid_for(n, 256, ctx->sms, 8),
+                                     (i64)ctx->sms * std::max(per_sm, 1));
+  }
   T.s1_grid = (int)std::min<i64>((i64)ctx->sms * S1_CTAS_PER_SM, ceil_div(n, S1_TILE));
   {
     // equal tile counts per CTA: tile = ceil(per_cta / ceil(per_cta / S1_TILE))

@@ -615,10 +615,12 @@ __device__ __forceinline__ void tma_stage_issue(float* dst, const void* fmap, in
 }
 // wait (every thread; after a barrier that orders it behind the issue)
 __device__ __forceinline__ void tma_stage_wait(unsigned long long* bar) {
+  // try_wait with a suspend-time hint: waiting warps sleep instead of spinning
+  // on issue slots the co-resident CTA needs
   asm volatile(
       "{\n\t.reg .pred p;\n\tTMA_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n\t"
-      "@!p bra TMA_WAIT_%=;\n\t}" ::"r"((u32)__cvta_generic_to_shared(bar)) : "memory");
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0, %1;\n\t"
+      "@!p bra TMA_WAIT_%=;\n\t}" ::"r"((u32)__cvta_generic_to_shared(bar)), "r"(1000000u) : "memory");
 }
 
 constexpr int BINS_BLOCK = 512;

@@ -91,18 +91,13 @@ __device__ __forceinline__ double nan_ll() { return __longlong_as_double(0x7ff80
 //   ll    = -ssd * inv_2sxi2                                (fp64)
 // The per-row partials let a warp evaluate one window with one lane per row
 // (k_pc_bins) and still match the per-thread loop bit for bit.
-template <int MAXS>
-__device__ __forceinline__ double loglik_gauss(const PixView& pv, float x, float y, float i0,
-                                               const Spot& sp) {
-  if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
-  int xlo, xhi, ylo, yhi;
-  window_axis_f(x, sp.hw, pv.W, xlo, xhi);
-  window_axis_f(y, sp.hw, pv.H, ylo, yhi);
-  int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
+template <int MAXS, bool FULL>
+__device__ __forceinline__ double loglik_gauss_k(const PixView& pv, float x, float y, float i0,
+                                                 const Spot& sp, int xlo, int nx, int ylo, int ny) {
   float ag[MAXS];
 #pragma unroll
   for (int i = 0; i < MAXS; ++i) {
-    if (i < nx) {
+    if (FULL || i < nx) {
       float d = pix_off(xlo + i, x);
       ag[i] = i0 * expf(-(d * d) * sp.inv2s2);
     }
@@ -115,11 +110,11 @@ __device__ __forceinline__ double loglik_gauss(const PixView& pv, float x, float
     float pr[MAXS];
 #pragma unroll
     for (int i = 0; i < MAXS; ++i)
-      if (i < nx) pr[i] = row[i];
+      if (FULL || i < nx) pr[i] = row[i];
     double racc = 0.0;
 #pragma unroll
     for (int i = 0; i < MAXS; ++i) {
-      if (i < nx) {
+      if (FULL || i < nx) {
         float r = pr[i] - fmaf(ag[i], gy, sp.bg);
         racc = fma((double)r, (double)r, racc);
       }
@@ -129,33 +124,142 @@ __device__ __forceinline__ double loglik_gauss(const PixView& pv, float x, float
   return -ssd * sp.inv_2sxi2;
 }
 
+template <int MAXS>
+__device__ __forceinline__ double loglik_gauss(const PixView& pv, float x, float y, float i0,
+                                               const Spot& sp) {
+  if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
+  int xlo, xhi, ylo, yhi;
+  window_axis_f(x, sp.hw, pv.W, xlo, xhi);
+  window_axis_f(y, sp.hw, pv.H, ylo, yhi);
+  const int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
+  if (nx == MAXS) return loglik_gauss_k<MAXS, true>(pv, x, y, i0, sp, xlo, nx, ylo, ny);
+  return loglik_gauss_k<MAXS, false>(pv, x, y, i0, sp, xlo, nx, ylo, ny);
+}
+
 // ---- Poisson log-likelihood ratio vs background (config 3, new) -------------
 //   lambda = bg + I0 Ex(xi) Ey(yi);   ll = sum_window [ z log1p(mu/bg) - mu ],
 //   mu = I0 Ex Ey. Equals the full-frame Poisson log-likelihood minus a
 //   per-frame constant (pixels outside the window have lambda = bg), with
 //   the lgamma(z+1) term dropped.
 // model 1: Ex = integral of exp(-(t-x)^2/2s^2) over the pixel (erf form). The
-//   4x4 sub-pixel supersampled integral telescopes exactly to this, so the
-//   S+1 pixel-boundary erf values are evaluated (minimal form).
+//   4x4 sub-pixel supersampled integral telescopes exactly to this, so only
+//   the S+1 pixel-EDGE values are evaluated: edge e_i = RN32(RN32(i - 1/2) - x),
+//   C_i = erfc(|e_i| / (sqrt2 s)), and the pixel between edges a < b is
+//   erfc(a) - erfc(b) (a >= 0), erfc(-b) - erfc(-a) (b <= 0), 2 - C_a - C_b
+//   (straddling) times s sqrt(pi/2) — accurate in both tails, one erfc per edge.
 // model 2: Ex = 1/4 sum_s exp(-((xi - 3/8 + s/4) - x)^2 / 2s^2) (mid-point 4x4).
-__device__ __forceinline__ float erf_diff(float a, float b) {
-  // erf(b) - erf(a), a < b, accurate in both tails
-  if (a >= 0.0f) return erfcf(a) - erfcf(b);
-  if (b <= 0.0f) return erfcf(-b) - erfcf(-a);
-  return erff(b) - erff(a);
+// Per pixel the term z log1p(t) - t bg (t = mu/bg) is float32 with the
+// log1p_pos below; a row is summed in float32 in column order and the rows
+// in float64 in row order (every evaluation form below follows this order,
+// so they agree bit for bit).
+__device__ __forceinline__ float edge_off(int i, float p) {
+  return __fsub_rn(__fsub_rn((float)i, 0.5f), p);   // (float)i - 1/2 exact for |i| < 2^23
+}
+__device__ __forceinline__ float edge_c(float e, const Spot& sp) {
+  return erfcf(fabsf(e) * sp.inv_sqrt2s);
+}
+__device__ __forceinline__ float erf_pixel(float a, float b, float ca, float cb, const Spot& sp) {
+  float d;
+  if (a >= 0.0f) d = ca - cb;
+  else if (b <= 0.0f) d = cb - ca;
+  else d = (2.0f - ca) - cb;
+  return sp.erf_scale * d;
 }
 
-__device__ __forceinline__ float psf_axis(float d, const Spot& sp) {
-  if (sp.model == 1)
-    return sp.erf_scale * erf_diff((d - 0.5f) * sp.inv_sqrt2s, (d + 0.5f) * sp.inv_sqrt2s);
+__device__ __forceinline__ float psf_axis(float d, const Spot& sp) {   // model 2
   float t0 = d - 0.375f, t1 = d - 0.125f, t2 = d + 0.125f, t3 = d + 0.375f;
   return 0.25f * (expf(-(t0 * t0) * sp.inv2s2) + expf(-(t1 * t1) * sp.inv2s2) +
                   expf(-(t2 * t2) * sp.inv2s2) + expf(-(t3 * t3) * sp.inv2s2));
 }
+// PSF factor of pixel i along one axis (position p)
+__device__ __forceinline__ float psf_pixel(int i, float p, const Spot& sp) {
+  if (sp.model == 1) {
+    const float a = edge_off(i, p), b = edge_off(i + 1, p);
+    return erf_pixel(a, b, edge_c(a, sp), edge_c(b, sp), sp);
+  }
+  return psf_axis(pix_off(i, p), sp);
+}
 
-__device__ __forceinline__ double poisson_term(float z, float t, float bg) {
-  // z log1p(mu/bg) - mu with t = mu/bg, accumulated in float64
-  return (double)fmaf(z, log1pf(t), -t * bg);
+__device__ __forceinline__ float rcp_approx(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// log1p(t) for 0 <= t < 1e30, within ~2 ulp: u = RN(1 + t) = m 2^e (m in
+// [sqrt(1/2), sqrt(2))), log m = 2 atanh(s), s = (m - 1)/(m + 1) (series to
+// s^9), plus the rounding error of 1 + t, (t - (u - 1))/u.
+__device__ __forceinline__ float log1p_pos(float t) {
+  const float u = 1.0f + t;
+  const int ib = __float_as_int(u);
+  const int e = (ib - 0x3f3504f3) >> 23;
+  const float f = __int_as_float(ib - (e << 23)) - 1.0f;           // exact
+  const float s = f * rcp_approx(2.0f + f);
+  const float z = s * s;
+  float q = fmaf(z, 0.22222222f, 0.28571429f);                     // 2/9, 2/7
+  q = fmaf(q, z, 0.4f);
+  q = fmaf(q, z, 0.66666669f);
+  q = fmaf(q, z, 2.0f);
+  const float ef = __int_as_float(0x4B400000 + e) - 12582912.0f;   // (float)e
+  const float lu = fmaf(ef, 0.693145751953125f, fmaf(ef, 1.42860677e-06f, s * q));
+  return fmaf(t - (u - 1.0f), rcp_approx(u), lu);
+}
+
+// FAST: every t = mu/bg of the window is in [0, 1e30) (checked once per
+// evaluation by poisson_fast_ok); otherwise the library log1pf.
+template <bool FAST>
+__device__ __forceinline__ float poisson_term(float z, float t, float bg) {
+  return fmaf(z, FAST ? log1p_pos(t) : log1pf(t), -t * bg);
+}
+__device__ __forceinline__ bool poisson_fast_ok(float i0, const Spot& sp) {
+  // mu/bg <= I0 / bg * max(Ex) max(Ey); max Ex <= 2 s sqrt(pi/2) (model 1), <= 1 (model 2)
+  const float pm = (sp.model == 1) ? 2.0f * sp.erf_scale : 1.0f;
+  return i0 >= 0.0f && (i0 / sp.bg) * pm * pm < 1.0e30f;
+}
+
+// FULL: the window has all MAXS columns (not clamped at the frame edge), so
+// the unrolled column loops carry no per-pixel guard
+template <int MAXS, bool FAST, bool FULL>
+__device__ __forceinline__ double loglik_poisson_k(const PixView& pv, float x, float y, float i0,
+                                                   const Spot& sp, int xlo, int nx, int ylo,
+                                                   int ny) {
+  float ex[MAXS];
+  const float inv_bg = 1.0f / sp.bg;
+  if (sp.model == 1) {
+    float a = edge_off(xlo, x), ca = edge_c(a, sp);
+#pragma unroll
+    for (int i = 0; i < MAXS; ++i) {
+      if (FULL || i < nx) {
+        const float b = edge_off(xlo + i + 1, x), cb = edge_c(b, sp);
+        ex[i] = i0 * erf_pixel(a, b, ca, cb, sp) * inv_bg;   // mu/bg along x (times Ey later)
+        a = b;
+        ca = cb;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < MAXS; ++i)
+      if (FULL || i < nx) ex[i] = i0 * psf_axis(pix_off(xlo + i, x), sp) * inv_bg;
+  }
+  double ll = 0.0;
+  float ya = edge_off(ylo, y), yca = (sp.model == 1) ? edge_c(ya, sp) : 0.0f;
+  for (int j = 0; j < ny; ++j) {
+    const float* row = pv.row(ylo + j, xlo);
+    float ey;
+    if (sp.model == 1) {
+      const float yb = edge_off(ylo + j + 1, y), ycb = edge_c(yb, sp);
+      ey = erf_pixel(ya, yb, yca, ycb, sp);
+      ya = yb;
+      yca = ycb;
+    } else {
+      ey = psf_axis(pix_off(ylo + j, y), sp);
+    }
+    float racc = 0.0f;
+#pragma unroll
+    for (int i = 0; i < MAXS; ++i)
+      if (FULL || i < nx) racc += poisson_term<FAST>(row[i], ex[i] * ey, sp.bg);
+    ll += (double)racc;
+  }
+  return ll;
 }
 
 template <int MAXS>
@@ -165,27 +269,10 @@ __device__ __forceinline__ double loglik_poisson(const PixView& pv, float x, flo
   int xlo, xhi, ylo, yhi;
   window_axis_f(x, sp.hw, pv.W, xlo, xhi);
   window_axis_f(y, sp.hw, pv.H, ylo, yhi);
-  int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
-  float ex[MAXS];
-  const float inv_bg = 1.0f / sp.bg;
-#pragma unroll
-  for (int i = 0; i < MAXS; ++i) {
-    if (i < nx) {
-      float d = pix_off(xlo + i, x);
-      ex[i] = i0 * psf_axis(d, sp) * inv_bg;   // mu/bg along x (times Ey later)
-    }
-  }
-  double ll = 0.0;
-  for (int j = 0; j < ny; ++j) {
-    const float* row = pv.row(ylo + j, xlo);
-    float ey = psf_axis(pix_off(ylo + j, y), sp);
-    double racc = 0.0;
-#pragma unroll
-    for (int i = 0; i < MAXS; ++i)
-      if (i < nx) racc += poisson_term(row[i], ex[i] * ey, sp.bg);
-    ll += racc;
-  }
-  return ll;
+  const int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
+  if (!poisson_fast_ok(i0, sp)) return loglik_poisson_k<MAXS, false, false>(pv, x, y, i0, sp, xlo, nx, ylo, ny);
+  if (nx == MAXS) return loglik_poisson_k<MAXS, true, true>(pv, x, y, i0, sp, xlo, nx, ylo, ny);
+  return loglik_poisson_k<MAXS, true, false>(pv, x, y, i0, sp, xlo, nx, ylo, ny);
 }
 
 template <int MAXS>
@@ -228,16 +315,18 @@ __device__ __forceinline__ double loglik_poisson_generic(const PixView& pv, floa
   window_axis_f(x, sp.hw, pv.W, xlo, xhi);
   window_axis_f(y, sp.hw, pv.H, ylo, yhi);
   const float inv_bg = 1.0f / sp.bg;
+  const bool fast = poisson_fast_ok(i0, sp);
   double ll = 0.0;
   for (int yy = ylo; yy <= yhi; ++yy) {
-    float ey = psf_axis(pix_off(yy, y), sp);
+    float ey = psf_pixel(yy, y, sp);
     const float* row = pv.row(yy, xlo);
-    double racc = 0.0;
+    float racc = 0.0f;
     for (int xx = xlo; xx <= xhi; ++xx) {
-      float exi = i0 * psf_axis(pix_off(xx, x), sp) * inv_bg;
-      racc += poisson_term(row[xx - xlo], exi * ey, sp.bg);
+      float exi = i0 * psf_pixel(xx, x, sp) * inv_bg;
+      racc += fast ? poisson_term<true>(row[xx - xlo], exi * ey, sp.bg)
+                   : poisson_term<false>(row[xx - xlo], exi * ey, sp.bg);
     }
-    ll += racc;
+    ll += (double)racc;
   }
   return ll;
 }
@@ -271,17 +360,19 @@ __device__ __forceinline__ double loglik_warp(const PixView& pv, float x, float 
   if (nx > 32 || ny > 32) return loglik_generic(pv, x, y, i0, sp);
   const bool gauss = (sp.model == 0);
   const float inv_bg = 1.0f / sp.bg;
+  const bool fast = !gauss && poisson_fast_ok(i0, sp);
   float colf = 0.0f, rowf = 0.0f;
   if (lane < nx) {
     float d = pix_off(xlo + lane, x);
-    colf = gauss ? i0 * expf(-(d * d) * sp.inv2s2) : i0 * psf_axis(d, sp) * inv_bg;
+    colf = gauss ? i0 * expf(-(d * d) * sp.inv2s2) : i0 * psf_pixel(xlo + lane, x, sp) * inv_bg;
   }
   if (lane < ny) {
     float d = pix_off(ylo + lane, y);
-    rowf = gauss ? expf(-(d * d) * sp.inv2s2) : psf_axis(d, sp);
+    rowf = gauss ? expf(-(d * d) * sp.inv2s2) : psf_pixel(ylo + lane, y, sp);
   }
   const float* row = pv.row(ylo + min(lane, ny - 1), xlo);
   double racc = 0.0;
+  float racc_f = 0.0f;
   for (int i = 0; i < nx; ++i) {
     float ci = __shfl_sync(0xffffffffu, colf, i);
     if (lane < ny) {
@@ -289,10 +380,12 @@ __device__ __forceinline__ double loglik_warp(const PixView& pv, float x, float 
         float r = row[i] - fmaf(ci, rowf, sp.bg);
         racc = fma((double)r, (double)r, racc);
       } else {
-        racc += poisson_term(row[i], ci * rowf, sp.bg);
+        racc_f += fast ? poisson_term<true>(row[i], ci * rowf, sp.bg)
+                       : poisson_term<false>(row[i], ci * rowf, sp.bg);
       }
     }
   }
+  if (!gauss) racc = (double)racc_f;
   double tot = 0.0;
   for (int j = 0; j < ny; ++j) tot += __shfl_sync(0xffffffffu, racc, j);
   return gauss ? -tot * sp.inv_2sxi2 : tot;
@@ -305,10 +398,12 @@ __device__ __forceinline__ double loglik_row(const PixView& pv, float x, float y
                                              const Spot& sp, int xlo, int nx, int yy) {
   const bool gauss = (sp.model == 0);
   const float inv_bg = 1.0f / sp.bg;
+  const bool fast = !gauss && poisson_fast_ok(i0, sp);
   float d = pix_off(yy, y);
-  float rowf = gauss ? expf(-(d * d) * sp.inv2s2) : psf_axis(d, sp);
+  float rowf = gauss ? expf(-(d * d) * sp.inv2s2) : psf_pixel(yy, y, sp);
   const float* row = pv.row(yy, xlo);
   double racc = 0.0;
+  float racc_f = 0.0f;
   for (int i = 0; i < nx; ++i) {
     float dx = pix_off(xlo + i, x);
     if (gauss) {
@@ -316,11 +411,12 @@ __device__ __forceinline__ double loglik_row(const PixView& pv, float x, float y
       float r = row[i] - fmaf(ag, rowf, sp.bg);
       racc = fma((double)r, (double)r, racc);
     } else {
-      float ex = i0 * psf_axis(dx, sp) * inv_bg;
-      racc += poisson_term(row[i], ex * rowf, sp.bg);
+      float ex = i0 * psf_pixel(xlo + i, x, sp) * inv_bg;
+      racc_f += fast ? poisson_term<true>(row[i], ex * rowf, sp.bg)
+                     : poisson_term<false>(row[i], ex * rowf, sp.bg);
     }
   }
-  return racc;
+  return gauss ? racc : (double)racc_f;
 }
 
 // window bounds of a state (for staging decisions)

@@ -21,6 +21,9 @@ namespace pcs {
 // (same pixel values, identical log-likelihoods)
 constexpr int SIR_SW = 64;
 
+// log of a prior weight, out of line (only frames after a non-resampling frame)
+__device__ __noinline__ double log_prior(float w) { return log((double)w); }
+
 template <int MAXS>
 __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
   __shared__ __align__(128) float stg[SIR_SW * SIR_SW];
@@ -63,6 +66,7 @@ __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
   long long lmax = LLONG_MIN;
   bool bad = false;
   const i64 n = P.n, ld = P.ld;
+  const bool prior = C->prior_nonuniform != 0;
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < n; j += (i64)gridDim.x * blockDim.x) {
     i64 src = (i64)__ldg(P.anc + j);
     float s[5], z[5], o[5];
@@ -83,7 +87,7 @@ __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
     v.y0 = inside ? ps.y0 : 0;
     double ll = loglik_dispatch<MAXS>(v, o[0], o[1], o[4], P.spot);
     // log w = log(w_prev) + ll (k_weight_update, binning.py:190-192 / filtering.py:69)
-    if (C->prior_nonuniform) ll = __dadd_rn(log((double)P.wprev[j]), ll);
+    if (prior) ll = __dadd_rn(log_prior(P.wprev[j]), ll);
     P.ll[j] = ll;
     if (!(ll == ll) || ll == INFINITY) bad = true;
     lmax = max(lmax, (long long)f64_to_ordered(ll));

@@ -143,6 +143,7 @@ def test_poisson_loglik_matches_oracle(cuda):
     xs[:250] = (40.3 + rng.normal(0, 1.5, 250)).astype(np.float32)
     ys[:250] = (38.8 + rng.normal(0, 1.5, 250)).astype(np.float32)
     i0 = rng.uniform(5, 30, n).astype(np.float32)
+    i0[250:270] = -2.0   # negative intensities take the library-log1p form
     soa = torch.from_numpy(np.stack([xs, ys, np.zeros(n, np.float32), np.zeros(n, np.float32),
                                      i0])).cuda()
     for sub, model in (("erf", 1), ("midpoint4", 2)):
