@@ -65,6 +65,7 @@ struct TrackState {
   BinsScratch bins{};
   int s1_grid = 0;
   int rs_grid = 0;       // k_sys_resample CTAs (all co-resident)
+  int rs_small = 0;      // > 0: k_sys_resample_small with this many CTAs instead
   int prop_grid = 0;
   int maxs = 0;
   i64 k = 0;             // host mirror of the frame counter
@@ -737,7 +738,8 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
       default: launch_pdl(k_pc_bins<0>, 1, BINS_BLOCK, BINS_SMEM, st, P, T.bins);
     }
     mark();
-    launch_pdl(k_sys_resample<1>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<1>), st, P);
+    if (T.rs_small) launch_pdl(k_sys_resample_small<1>, T.rs_small, SCAN_BLOCK, 0, st, P);
+    else launch_pdl(k_sys_resample<1>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<1>), st, P);
   } else {
     mark();
     switch (T.maxs) {
@@ -753,7 +755,8 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
     mark();
     k_sir_finalize<<<1, 1, 0, st>>>(P);
     mark();
-    launch_pdl(k_sys_resample<2>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<2>), st, P);
+    if (T.rs_small) launch_pdl(k_sys_resample_small<2>, T.rs_small, SCAN_BLOCK, 0, st, P);
+    else launch_pdl(k_sys_resample<2>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<2>), st, P);
   }
   if (evs) cudaEventRecord(evs[q], st);
   PCS_LAUNCH_CHECK();
@@ -847,10 +850,13 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   PCS_SCRATCH(SL_TR_CTL, sizeof(TrackCtl), P.ctl);
   PCS_SCRATCH(SL_FMAP, 128, P.fmap);
   P.ntiles = ceil_div(n, SCAN_TILE);
-  PCS_SCRATCH(SL_TR_TILES, P.ntiles * (2 * sizeof(u128) + sizeof(u32)) + 64, P.tile_agg);
+  // per-CTA aggregates of the resampler: one per CTA (<= one per RSS_TILE particles)
+  const i64 nagg = std::max<i64>(P.ntiles, ceil_div(n, (i64)RSS_TILE));
+  PCS_SCRATCH(SL_TR_TILES, P.ntiles * (2 * sizeof(u128) + sizeof(u32)) + nagg * sizeof(u128) + 64,
+              P.tile_agg);
   P.tile_inc = P.tile_agg + P.ntiles;
-  P.tile_status = (u32*)(P.tile_inc + P.ntiles);
-  P.cta_agg = P.tile_agg;   // k_sys_resample: rs_grid <= ntiles aggregates
+  P.cta_agg = P.tile_inc + P.ntiles;
+  P.tile_status = (u32*)(P.cta_agg + nagg);
   PCS_CUDA_TRY(cudaMemsetAsync(P.tile_status, 0, P.ntiles * sizeof(u32), st));
   {
     const double frac = cfg->threshold_fraction > 0.0 ? cfg->threshold_fraction : 1.0;
@@ -928,6 +934,17 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
       PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sys_resample<2>, SCAN_BLOCK,
                                                                  sizeof(RsSmem<2>)));
     T.rs_grid = (int)std::min<i64>((i64)ctx->sms * std::max(per_sm, 1), ceil_div(n, (i64)RS_TILE));
+    // small N: one RSS_TILE tile per CTA when all those CTAs are co-resident
+    int per_small = 0;
+    if (cfg->method == 1)
+      PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_small, k_sys_resample_small<1>,
+                                                                 SCAN_BLOCK, 0));
+    else
+      PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_small, k_sys_resample_small<2>,
+                                                                 SCAN_BLOCK, 0));
+    const i64 g_small = ceil_div(n, (i64)RSS_TILE);
+    T.rs_small = (g_small <= (i64)ctx->sms * per_small && getenv("PCS_NO_RS_SMALL") == nullptr)
+                     ? (int)g_small : 0;
   }
   // initial cloud (state.py:164-175) and identity ancestors
   pcs_init_t init = cfg->init;

@@ -1516,6 +1516,183 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
   RS_PROBE(4);
 }
 
+// Small-N form of k_sys_resample (every CTA owns ONE tile of RSS_TILE
+// particles; used when all those CTAs are co-resident, e.g. c1/c2): the tile
+// is staged once, its block scan is done before the grid barrier, and the
+// run heads / emission follow right after the prefix — no second pass over
+// the input. Same exact arithmetic and output as k_sys_resample.
+constexpr int RSS_ITEMS = 7;                        // odd: stride-7 reads are conflict-free
+constexpr int RSS_TILE = SCAN_BLOCK * RSS_ITEMS;    // 1792
+
+template <int KIND>
+struct RssSmem {
+  typename RsElem<KIND>::T items[RSS_TILE];
+  int hp[RSS_TILE];
+  int stage[RSS_TILE];
+  u128 wtot[SCAN_BLOCK / 32];
+  int s_wmax[SCAN_BLOCK / 32];
+  long long s_jr[2];
+};
+
+template <int KIND>
+__global__ void __launch_bounds__(SCAN_BLOCK, 4) k_sys_resample_small(TrackParams P) {
+  typedef typename RsElem<KIND>::T E;
+  __shared__ __align__(16) RssSmem<KIND> sm;
+  TrackCtl* C = P.ctl;
+  pdl_wait();
+  const i64 n = P.n;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const i64 base = (i64)cta * RSS_TILE;
+  const int nv = (int)min((i64)RSS_TILE, n - base);
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  if (!C->do_resample) {   // identity ancestors; SIR keeps the normalised weights
+    const bool keep = (KIND == 2) && C->prior_nonuniform;
+    const double m = C->m, Sf = C->Sf;
+    for (int k = threadIdx.x; k < nv; k += SCAN_BLOCK) {
+      const i64 i = base + k;
+      P.anc_out[P.idx_off + i - P.slot_lo] = (int)i;
+      if (keep) P.wprev[i] = normalised_weight(P.ll[i], m, Sf);
+    }
+    return;
+  }
+  const double m = C->m, Sf = C->Sf, u = C->u;
+  RS_PROBE(0);
+  const E* src = (KIND == 1) ? (const E*)(const void*)P.pslot : (const E*)(const void*)P.ll;
+  for (int k = threadIdx.x; k < nv; k += SCAN_BLOCK) sm.items[k] = src[base + k];
+  __syncthreads();
+  auto weight = [&](int k) -> u128 {
+    if (k >= nv) return 0;
+    if (KIND == 1) return P.wfix[(u32)sm.items[k]];
+    return cdf_fixed(normalised_weight((double)sm.items[k], m, Sf));
+  };
+  const int k0 = (int)threadIdx.x * RSS_ITEMS;
+  u128 tsum = 0;
+#pragma unroll
+  for (int q = 0; q < RSS_ITEMS; ++q) tsum += weight(k0 + q);
+  u128 inc = tsum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u128 o = shfl_up_u128(inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (lane == 31) sm.wtot[wi] = inc;
+  __syncthreads();
+  u128 woff = 0, tagg = 0;
+#pragma unroll
+  for (int w = 0; w < SCAN_BLOCK / 32; ++w) {
+    if (w < wi) woff += sm.wtot[w];
+    tagg += sm.wtot[w];
+  }
+  if (threadIdx.x == 0) {
+    P.cta_agg[cta] = tagg;
+    __threadfence();
+  }
+  RS_PROBE(1);
+  grid_barrier(C, G);
+  RS_PROBE(2);
+  // exclusive prefix of this CTA: aggregates of the CTAs before it
+  u128 pre;
+  {
+    u128 v = 0;
+    for (int k = threadIdx.x; k < cta; k += SCAN_BLOCK) v += *((volatile u128*)(P.cta_agg + k));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const u64 lo = (u64)v, hi = (u64)(v >> 64);
+      v += ((u128)__shfl_xor_sync(0xffffffffu, hi, o) << 64) | (u128)__shfl_xor_sync(0xffffffffu, lo, o);
+    }
+    __syncthreads();   // every thread has read sm.wtot
+    if (lane == 0) sm.wtot[wi] = v;
+    __syncthreads();
+    pre = 0;
+#pragma unroll
+    for (int w = 0; w < SCAN_BLOCK / 32; ++w) pre += sm.wtot[w];
+  }
+  RS_PROBE(3);
+  const i64 ng = P.n_global, off = P.idx_off, lo = P.slot_lo, cap = P.slot_cap;
+  const double nd = (double)ng, eps = nd * 8.881784197001252e-16;   // n * 2^-50
+  const double kappa = nd * 1.0842021724855044e-19;                  // n * 2^-63
+  const i64 kl = ng - 1 - off - base;
+  const int klast = (kl >= 0 && kl < nv) ? (int)kl : -1;
+  if (threadIdx.x == 0) {
+    sm.s_jr[0] = (off + base == 0) ? 0 : first_slot_fast(cdf_round(pre), u, ng, nd, eps);
+    sm.s_jr[1] = (klast == nv - 1) ? ng : first_slot_fast(cdf_round(pre + tagg), u, ng, nd, eps);
+  }
+  __syncthreads();
+  const i64 tj0 = sm.s_jr[0], tj1 = sm.s_jr[1];
+  {
+    const u128 excl = pre + woff + (inc - tsum);
+    const double tj0d = (double)tj0;
+    int jr = 0;
+    if (k0 < nv && off + base + k0 != 0) jr = slot_rel(excl, u, ng, nd, kappa, eps, tj0d, tj0);
+    u128 run = excl;
+#pragma unroll
+    for (int q = 0; q < RSS_ITEMS; ++q) {
+      const int k = k0 + q;
+      int h = -1;   // no slot
+      if (k < nv) {
+        run += weight(k);
+        const int jend = (k == klast) ? (int)(ng - tj0) : slot_rel(run, u, ng, nd, kappa, eps, tj0d, tj0);
+        if (jend > jr) h = jr;
+        jr = jend;
+      }
+      sm.hp[k] = h;
+    }
+  }
+  // slots in chunks of RSS_TILE: heads, block max-scan, coalesced writes
+  bool oob = false;
+  const int m_slots = (int)(tj1 - tj0);
+  int carry = -1;
+  for (int c0 = 0; c0 < m_slots; c0 += RSS_TILE) {
+#pragma unroll
+    for (int q = 0; q < RSS_ITEMS; ++q) sm.stage[k0 + q] = -1;
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < RSS_ITEMS; ++q) {
+      const u32 hr = (u32)(sm.hp[k0 + q] - c0);   // no head: (u32)(-1 - c0) >= 2^31
+      if (hr < (u32)RSS_TILE) sm.stage[hr] = k0 + q;
+    }
+    __syncthreads();
+    int tmax = -1;
+#pragma unroll
+    for (int q = 0; q < RSS_ITEMS; ++q) tmax = max(tmax, sm.stage[k0 + q]);
+    int incl = tmax;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int o = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl = max(incl, o);
+    }
+    if (lane == 31) sm.s_wmax[wi] = incl;
+    int excl_l = __shfl_up_sync(0xffffffffu, incl, 1);
+    if (lane == 0) excl_l = -1;
+    __syncthreads();
+    int prev = carry, total = carry;
+#pragma unroll
+    for (int w = 0; w < SCAN_BLOCK / 32; ++w) {
+      if (w < wi) prev = max(prev, sm.s_wmax[w]);
+      total = max(total, sm.s_wmax[w]);
+    }
+    int runm = max(prev, excl_l);
+#pragma unroll
+    for (int q = 0; q < RSS_ITEMS; ++q) {
+      runm = max(runm, sm.stage[k0 + q]);
+      sm.stage[k0 + q] = runm;
+    }
+    __syncthreads();
+    const int cm = min(RSS_TILE, m_slots - c0);
+    const i64 w0 = tj0 + c0 - lo;
+    const int ib = (int)base;
+    for (int k = threadIdx.x; k < cm; k += SCAN_BLOCK) {
+      const i64 kk = w0 + k;
+      if (kk >= 0 && kk < cap) P.anc_out[kk] = ib + sm.stage[k];
+      else oob = true;
+    }
+    carry = total;
+    __syncthreads();
+  }
+  if (oob) set_flag(C, PCS_FLAG_CAPACITY);
+  RS_PROBE(4);
+}
+
 constexpr size_t S1_SMEM = sizeof(S1Smem);
 
 }  // namespace pcs

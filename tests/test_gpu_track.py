@@ -160,10 +160,14 @@ def test_fused_sir_equals_general(cuda):
 
 
 @pytest.mark.parametrize("method", ["sir", "pc"])
-def test_fused_resampling_many_tiles_heavy_weights(cuda, method):
-    # 2e5 particles -> 53 resampling tiles on 53 CTAs (grid barrier, exact CTA
-    # prefixes); a sharp likelihood concentrates the weight so some tiles emit
+@pytest.mark.parametrize("small", [True, False])
+def test_fused_resampling_many_tiles_heavy_weights(cuda, method, small, monkeypatch):
+    # 2e5 particles -> 112 one-tile CTAs (k_sys_resample_small) or 53 CTAs of
+    # the two-pass k_sys_resample (PCS_NO_RS_SMALL): grid barrier, exact CTA
+    # prefixes; a sharp likelihood concentrates the weight so some tiles emit
     # more than one tile of slots (chunked emission)
+    if not small:
+        monkeypatch.setenv("PCS_NO_RS_SMALL", "1")
     frames, truth, init, dyn = _c1_like(k=5)
     n = 200_000
     sharp = pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(1.5, 5))
