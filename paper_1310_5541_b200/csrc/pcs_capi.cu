@@ -66,6 +66,7 @@ struct TrackState {
   int s1_grid = 0;
   int rs_grid = 0;       // k_sys_resample CTAs (all co-resident)
   int rs_small = 0;      // > 0: k_sys_resample_small with this many CTAs instead
+  int red_grid = 0;      // k_sir_sum / k_sir_stats CTAs
   int prop_grid = 0;
   int maxs = 0;
   i64 k = 0;             // host mirror of the frame counter
@@ -749,9 +750,9 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
       default: k_sir_propagate_lik<0><<<T.prop_grid, 256, 0, st>>>(P);
     }
     mark();
-    k_sir_sum<<<grid_for(P.n, 256, ctx->sms), 256, 0, st>>>(P);
+    k_sir_sum<<<T.red_grid, 256, 0, st>>>(P);
     mark();
-    k_sir_stats<<<grid_for(P.n, 256, ctx->sms), 256, 0, st>>>(P);
+    k_sir_stats<<<T.red_grid, 256, 0, st>>>(P);
     mark();
     k_sir_finalize<<<1, 1, 0, st>>>(P);
     mark();
@@ -905,6 +906,10 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
     T.bins.cell = (u32*)(sd + 4 * BINS_MAXM);
   }
   T.maxs = maxs_for(cfg->spot.halfwidth);
+  // SIR reductions: >= 16 particles per thread (few int128 partials per atomic
+  // target at c2 sizes), 2..8 CTAs per SM
+  T.red_grid = (int)std::min<i64>((i64)ctx->sms * 8,
+                                  std::max<i64>((i64)ctx->sms * 2, ceil_div(n, (i64)256 * 16)));
   {
     // SIR propagate + likelihood: every resident CTA stages the frame region
     // once and strides over the particles (no later waves re-staging it)

@@ -110,7 +110,8 @@ struct TrackParams {
   float* buf0;
   float* buf1;
   int* anc;
-  double* ll;                // SIR: per-particle log-likelihood (float64)
+  double* ll;                // SIR: per-particle log-likelihood (float64); k_sir_sum
+                             // replaces it by exp(ll - max) for the rest of the frame
   u32* pslot;                // pcSIR: flat cell id per particle
   u32* tab_cnt;              // [G]
   u64* tab_sum;              // [5][G][2]
@@ -1000,7 +1001,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, 4) k_scan_emit(TrackParams P) {
   for (int q = 0; q < SCAN_ITEMS; ++q) {
     i64 i = base + (i64)q * SCAN_BLOCK + threadIdx.x;
     float w = 0.0f;
-    if (i < n) w = (KIND == 1) ? P.wtab[P.pslot[i]] : normalised_weight(P.ll[i], m, Sf);
+    if (i < n) w = (KIND == 1) ? P.wtab[P.pslot[i]] : weight_from_ex(P.ll[i], Sf);
     wsh[wpad(q * SCAN_BLOCK + threadIdx.x)] = w;
   }
   __syncthreads();
@@ -1309,7 +1310,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
     const double m = C->m, Sf = C->Sf;
     for (i64 i = t0 * RS_TILE + threadIdx.x; i < min(n, t1 * RS_TILE); i += SCAN_BLOCK) {
       P.anc_out[P.idx_off + i - P.slot_lo] = (int)i;
-      if (keep) P.wprev[i] = normalised_weight(P.ll[i], m, Sf);
+      if (keep) P.wprev[i] = weight_from_ex(P.ll[i], Sf);
     }
     return;
   }
@@ -1335,7 +1336,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
   auto weight = [&](const E* buf, int k, int nv) -> u128 {
     if (k >= nv) return 0;
     if (KIND == 1) return P.wfix[(u32)buf[k]];
-    return cdf_fixed(normalised_weight((double)buf[k], m, Sf));
+    return cdf_fixed(weight_from_ex((double)buf[k], Sf));
   };
   auto tile_items = [&](i64 tile) -> int { return (int)min((i64)RS_TILE, n - tile * RS_TILE); };
   // ---- pass 1: this CTA's exact total ----
@@ -1551,7 +1552,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, 4) k_sys_resample_small(TrackParam
     for (int k = threadIdx.x; k < nv; k += SCAN_BLOCK) {
       const i64 i = base + k;
       P.anc_out[P.idx_off + i - P.slot_lo] = (int)i;
-      if (keep) P.wprev[i] = normalised_weight(P.ll[i], m, Sf);
+      if (keep) P.wprev[i] = weight_from_ex(P.ll[i], Sf);
     }
     return;
   }
@@ -1563,7 +1564,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, 4) k_sys_resample_small(TrackParam
   auto weight = [&](int k) -> u128 {
     if (k >= nv) return 0;
     if (KIND == 1) return P.wfix[(u32)sm.items[k]];
-    return cdf_fixed(normalised_weight((double)sm.items[k], m, Sf));
+    return cdf_fixed(weight_from_ex((double)sm.items[k], Sf));
   };
   const int k0 = (int)threadIdx.x * RSS_ITEMS;
   u128 tsum = 0;

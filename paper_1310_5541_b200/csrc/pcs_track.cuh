@@ -98,14 +98,17 @@ __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
   if (bad) set_flag(C, PCS_FLAG_NONFINITE);
 }
 
-// S = sum round(exp(ll - m) * 2^95)
+// S = sum round(exp(ll - m) * 2^95); leaves exp(ll - m) in P.ll
 __global__ void __launch_bounds__(256) k_sir_sum(TrackParams P) {
   __shared__ i128 sh[8];
   TrackCtl* C = P.ctl;
   const double m = ordered_to_f64(C->max_ll_ord);
   i128 acc = 0;
-  for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < P.n; j += (i64)gridDim.x * blockDim.x)
-    acc += f64_to_fixed(exp(__dsub_rn(P.ll[j], m)), FX_S);
+  for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < P.n; j += (i64)gridDim.x * blockDim.x) {
+    const double ex = exp(__dsub_rn(P.ll[j], m));
+    P.ll[j] = ex;   // from here on P.ll holds exp(ll - m) (one exp per particle per frame)
+    acc += f64_to_fixed(ex, FX_S);
+  }
   i128 t = block_sum_i128<256>(acc, sh);
   if (threadIdx.x == 0) atomic_add_i128(C->S, t);
 }
@@ -123,7 +126,7 @@ __global__ void __launch_bounds__(256) k_sir_stats(TrackParams P) {
   bool range = false;
   unsigned wmin = 0xFFFFFFFFu, wmax = 0u;
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
-    float w = normalised_weight(P.ll[i], m, Sf);
+    float w = weight_from_ex(P.ll[i], Sf);
     wmin = min(wmin, __float_as_uint(w));
     wmax = max(wmax, __float_as_uint(w));
     // w <= 1: round(w 2^62) <= 2^62 fits a signed 64-bit value; for

@@ -127,6 +127,10 @@ __global__ void __launch_bounds__(BLOCK) k_logw_sum(const double* __restrict__ l
 __device__ __forceinline__ float normalised_weight(double logw, double m, double Sf) {
   return __double2float_rn(__ddiv_rn(exp(__dsub_rn(logw, m)), Sf));
 }
+// the same weight from a cached ex = exp(logw - m)
+__device__ __forceinline__ float weight_from_ex(double ex, double Sf) {
+  return __double2float_rn(__ddiv_rn(ex, Sf));
+}
 
 __global__ void k_logw_normalise(const double* __restrict__ logw, i64 n, const NormCtl* ctl,
                                  float* __restrict__ w) {
