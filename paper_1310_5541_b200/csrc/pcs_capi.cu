@@ -716,7 +716,7 @@ static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 
 static const char* kPcNames[] = {"k_pc_step1", "k_pc_bins", "k_sys_resample"};
 static const char* kSirNames[] = {"k_sir_propagate_lik", "k_sir_sum", "k_sir_stats",
-                                  "k_sir_finalize", "k_sys_resample"};
+                                  "k_sys_resample"};
 
 // Enqueue one frame. If evs is non-null, evs[i] is recorded before launch i
 // and evs[launches] after the last one (per-kernel CUDA-event timing).
@@ -752,9 +752,7 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
     mark();
     k_sir_sum<<<T.red_grid, 256, 0, st>>>(P);
     mark();
-    k_sir_stats<<<T.red_grid, 256, 0, st>>>(P);
-    mark();
-    k_sir_finalize<<<1, 1, 0, st>>>(P);
+    k_sir_stats<<<T.red_grid, 256, 0, st>>>(P);   // its last CTA finalises the frame
     mark();
     if (T.rs_small) launch_pdl(k_sys_resample_small<2>, T.rs_small, SCAN_BLOCK, 0, st, P);
     else launch_pdl(k_sys_resample<2>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<2>), st, P);
@@ -791,8 +789,9 @@ static int set_attrs() {
                        (const void*)k_scan_emit<2>,     (const void*)k_sir_propagate_lik<0>,
                        (const void*)k_sir_propagate_lik<9>, (const void*)k_sir_propagate_lik<11>,
                        (const void*)k_sir_propagate_lik<15>, (const void*)k_sir_sum,
-                       (const void*)k_sir_stats,        (const void*)k_sir_finalize,
-                       (const void*)k_sys_resample<1>,  (const void*)k_sys_resample<2>};
+                       (const void*)k_sir_stats,        (const void*)k_sys_resample<1>,
+                       (const void*)k_sys_resample<2>,  (const void*)k_sys_resample_small<1>,
+                       (const void*)k_sys_resample_small<2>};
   for (const void* f : fns)
     PCS_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout,
                                       (int)cudaSharedmemCarveoutMaxShared));
@@ -1069,7 +1068,7 @@ int pcs_track_steps_timed(pcs_ctx* ctx, const float* frames, int64_t k0, int64_t
 const char* pcs_track_kernel_name(pcs_ctx* ctx, int32_t i) {
   if (!ctx) return "";
   if (ctx->tr.cfg.method == 1) return (i >= 0 && i < 3) ? kPcNames[i] : "";
-  return (i >= 0 && i < 5) ? kSirNames[i] : "";
+  return (i >= 0 && i < 4) ? kSirNames[i] : "";
 }
 
 int pcs_track_end(pcs_ctx* ctx, pcs_track_result_t* result, void* stream) {

@@ -92,6 +92,7 @@ struct TrackCtl {
   unsigned long long tile_ctr;  // decoupled look-back: monotone tile ticket counter
   u64 rank_prefix[2];        // sharded: exact cumulative weight of the preceding ranks
   u32 gbar_cnt, gbar_gen;    // grid barrier of k_sys_resample
+  u32 stats_done;            // k_sir_stats CTAs finished (the last one finalises)
   int fmap_ok;               // P.fmap describes the current frame batch (TMA staging)
   int prior_nonuniform;      // SIR: particles carry the prior weights wprev (no resampling
                              // at the previous frame, weights not all equal)

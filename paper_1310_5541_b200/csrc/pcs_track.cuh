@@ -113,6 +113,43 @@ __global__ void __launch_bounds__(256) k_sir_sum(TrackParams P) {
   if (threadIdx.x == 0) atomic_add_i128(C->S, t);
 }
 
+// one thread: frame outputs, resampling decision, frame counter advance
+__device__ __forceinline__ void sir_finalize(const TrackParams& P) {
+  TrackCtl* C = P.ctl;
+  const i64 k = C->k, ko = k - C->k_out;
+  const double mf = ordered_to_f64(C->max_ll_ord);
+  const bool degenerate = (mf == -INFINITY);
+  const bool bad_m = !(mf == mf) || mf == INFINITY;
+  double est[5];
+  for (int c = 0; c < 5; ++c) {
+    est[c] = scalbn(i128_to_f64_rn(load_i128(C->est[c])), -(FX_WQ + FX_STATE));
+    C->out_est[ko * 5 + c] = est[c];
+  }
+  if (est[0] == est[0] && est[1] == est[1]) {   // staging window of the next frame
+    C->center[0] = est[0];
+    C->center[1] = est[1];
+  }
+  double ess = 1.0 / scalbn(i128_to_f64_rn(load_i128(C->w2)), -FX_W2);
+  C->out_ess[ko] = ess;
+  bool flag_bad = degenerate || bad_m;
+  if (degenerate) set_flag(C, PCS_FLAG_DEGENERATE);
+  if (bad_m) set_flag(C, PCS_FLAG_NONFINITE);
+  int res = (!flag_bad && ess < P.thresh) ? 1 : 0;   // filtering.py:169-170
+  // without resampling the next frame starts from these weights unless they
+  // are all equal (then uniform, as the general driver does)
+  C->prior_nonuniform = (!res && !flag_bad && C->wmin_bits != C->wmax_bits) ? 1 : 0;
+  C->out_res[ko] = (unsigned char)res;
+  C->out_occ[ko] = P.n;
+  C->evals += P.n;
+  C->do_resample = res;
+  C->m = mf;
+  C->Sf = scalbn(i128_to_f64_rn(load_i128(C->S)), -FX_S);
+  C->u = philox_resample_u(P.seed, P.frame0 + (u32)k);
+  reset_frame(C);
+  C->k = k + 1;
+}
+
+
 // estimate / ESS numerators and the min/max normalised weight
 __global__ void __launch_bounds__(256) k_sir_stats(TrackParams P) {
   __shared__ i128 sh[8];
@@ -158,43 +195,21 @@ __global__ void __launch_bounds__(256) k_sir_stats(TrackParams P) {
   if ((threadIdx.x & 31) == 0) {
     atomicMin(&C->wmin_bits, wmin);
     atomicMax(&C->wmax_bits, wmax);
+    __threadfence();   // this CTA's atomics are visible before it is counted
   }
-}
-
-// one thread: frame outputs, resampling decision, frame counter advance
-__global__ void k_sir_finalize(TrackParams P) {
-  TrackCtl* C = P.ctl;
-  const i64 k = C->k, ko = k - C->k_out;
-  const double mf = ordered_to_f64(C->max_ll_ord);
-  const bool degenerate = (mf == -INFINITY);
-  const bool bad_m = !(mf == mf) || mf == INFINITY;
-  double est[5];
-  for (int c = 0; c < 5; ++c) {
-    est[c] = scalbn(i128_to_f64_rn(load_i128(C->est[c])), -(FX_WQ + FX_STATE));
-    C->out_est[ko * 5 + c] = est[c];
+  // the last CTA to finish runs the frame's finalisation (no extra launch)
+  __shared__ bool last;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(&C->stats_done, 1u) == gridDim.x - 1;
   }
-  if (est[0] == est[0] && est[1] == est[1]) {   // staging window of the next frame
-    C->center[0] = est[0];
-    C->center[1] = est[1];
+  __syncthreads();
+  if (last && threadIdx.x == 0) {
+    __threadfence();
+    C->stats_done = 0;
+    sir_finalize(P);
   }
-  double ess = 1.0 / scalbn(i128_to_f64_rn(load_i128(C->w2)), -FX_W2);
-  C->out_ess[ko] = ess;
-  bool flag_bad = degenerate || bad_m;
-  if (degenerate) set_flag(C, PCS_FLAG_DEGENERATE);
-  if (bad_m) set_flag(C, PCS_FLAG_NONFINITE);
-  int res = (!flag_bad && ess < P.thresh) ? 1 : 0;   // filtering.py:169-170
-  // without resampling the next frame starts from these weights unless they
-  // are all equal (then uniform, as the general driver does)
-  C->prior_nonuniform = (!res && !flag_bad && C->wmin_bits != C->wmax_bits) ? 1 : 0;
-  C->out_res[ko] = (unsigned char)res;
-  C->out_occ[ko] = P.n;
-  C->evals += P.n;
-  C->do_resample = res;
-  C->m = mf;
-  C->Sf = scalbn(i128_to_f64_rn(load_i128(C->S)), -FX_S);
-  C->u = philox_resample_u(P.seed, P.frame0 + (u32)k);
-  reset_frame(C);
-  C->k = k + 1;
 }
 
 }  // namespace pcs
