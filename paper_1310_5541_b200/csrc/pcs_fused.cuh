@@ -567,15 +567,19 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
     //      consecutive particles per lane, warp-segmented scan across lanes) ----
     if (t < S1_SUM_THREADS)
       tile_run_sums<S1_SUM_THREADS, S1_E, S1_TILE, SUBW>(pay, sm.pay_q, (int)sm.n_in, &sm.dig[0][0], t);
-    __syncthreads();
+    // no barrier here: the other warps start the next tile's gathers while the
+    // summing warps finish (phase 1 touches none of pay / pay_q / n_in, and
+    // the next pay write is two barriers away)
     if (++since == S1_FLUSH_TILES) {
       since = 0;
+      __syncthreads();
       s1_flush(P, C, sm, sx0, sy0, snxi);
       __syncthreads();
       if (t == 0) sm.n_flist = 0;
       __syncthreads();
     }
   }
+  __syncthreads();
   s1_flush(P, C, sm, sx0, sy0, snxi);
   if (bad) set_flag(C, PCS_FLAG_NONFINITE);
 }
