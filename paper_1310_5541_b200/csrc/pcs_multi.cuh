@@ -291,8 +291,9 @@ __global__ void __launch_bounds__(MT_THREADS, 2) k_mt_frame(MtParams P) {
     __syncthreads();
     tile_run_sums<MT_THREADS, MT_IPT, MT_TILE, MT_SUBW>(sm.u.a.pay, sm.u.a.pay_q, (int)sm.n_in,
                                                         &sm.dig[0][0], t);
-    __syncthreads();
+    // no barrier: the next tile's phase 1 touches none of pay / pay_q / n_in
   }
+  __syncthreads();
   if (bad) atomicOr(&TG.flags, (u32)PCS_FLAG_NONFINITE);
   if (hash_full) atomicOr(&TG.flags, (u32)PCS_FLAG_CAPACITY);
 
