@@ -1300,7 +1300,6 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
   int* hp_own = sm.hp;
   u128* wtot = sm.wtot;
   int* s_wmax = sm.s_wmax;
-  long long* s_jr = sm.s_jr;
   unsigned long long* bar = sm.bar;
   TrackCtl* C = P.ctl;
   pdl_wait();   // (no early trigger here: the next frame's step 1 must not
@@ -1397,6 +1396,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
   const double kappa = nd * 1.0842021724855044e-19;                  // n * 2^-63
   bool oob = false;
   const int k0 = (int)threadIdx.x * RS_ITEMS;
+  i64 tj_prev = 0;
   for (int L = mt; L < 2 * mt; ++L) {
     mbar_wait(&bar[L & 1], (u32)((L >> 1) & 1));
     if (threadIdx.x == 0 && L + 1 < 2 * mt) issue(L + 1);
@@ -1425,12 +1425,12 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
       tagg += wtot[w];
     }
     const u128 excl = pre + woff + (inc - tsum);
-    if (threadIdx.x == 0) {
-      s_jr[0] = (off + base == 0) ? 0 : first_slot_fast(cdf_round(pre), u, ng, nd, eps);
-      s_jr[1] = (klast == nv - 1) ? ng : first_slot_fast(cdf_round(pre + tagg), u, ng, nd, eps);
-    }
-    __syncthreads();
-    const i64 tj0 = s_jr[0], tj1 = s_jr[1];
+    // the tile's slot range, computed by every thread (no broadcast barrier);
+    // a tile starts where the previous one ended
+    if (L == mt) tj_prev = (off + base == 0) ? 0 : first_slot_fast(cdf_round(pre), u, ng, nd, eps);
+    const i64 tj0 = tj_prev;
+    const i64 tj1 = (klast == nv - 1) ? ng : first_slot_fast(cdf_round(pre + tagg), u, ng, nd, eps);
+    tj_prev = tj1;
     // run head of every item: its first slot relative to tj0, -1 if none
     {
       const double tj0d = (double)tj0;
@@ -1619,12 +1619,9 @@ __global__ void __launch_bounds__(SCAN_BLOCK, 4) k_sys_resample_small(TrackParam
   const double kappa = nd * 1.0842021724855044e-19;                  // n * 2^-63
   const i64 kl = ng - 1 - off - base;
   const int klast = (kl >= 0 && kl < nv) ? (int)kl : -1;
-  if (threadIdx.x == 0) {
-    sm.s_jr[0] = (off + base == 0) ? 0 : first_slot_fast(cdf_round(pre), u, ng, nd, eps);
-    sm.s_jr[1] = (klast == nv - 1) ? ng : first_slot_fast(cdf_round(pre + tagg), u, ng, nd, eps);
-  }
-  __syncthreads();
-  const i64 tj0 = sm.s_jr[0], tj1 = sm.s_jr[1];
+  // the tile's slot range, computed by every thread (no broadcast barrier)
+  const i64 tj0 = (off + base == 0) ? 0 : first_slot_fast(cdf_round(pre), u, ng, nd, eps);
+  const i64 tj1 = (klast == nv - 1) ? ng : first_slot_fast(cdf_round(pre + tagg), u, ng, nd, eps);
   {
     const u128 excl = pre + woff + (inc - tsum);
     const double tj0d = (double)tj0;
