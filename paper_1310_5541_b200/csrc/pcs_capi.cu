@@ -67,6 +67,8 @@ struct TrackState {
   int rs_grid = 0;       // k_sys_resample CTAs (all co-resident)
   int rs_small = 0;      // > 0: k_sys_resample_small with this many CTAs instead
   int red_grid = 0;      // k_sir_sum / k_sir_stats CTAs
+  bool cond = false;     // pcSIR with threshold resampling (7-launch frame)
+  int rs_grid2 = 0;      // k_sys_resample<2> CTAs in that mode
   int prop_grid = 0;
   int maxs = 0;
   i64 k = 0;             // host mirror of the frame counter
@@ -129,6 +131,7 @@ enum Slot {
   SL_SYNTH,
   SL_FMAP,
   SL_TR_WPREV,
+  SL_TR_LLTAB,
   SL_COUNT
 };
 
@@ -738,9 +741,24 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
       case 15: launch_pdl(k_pc_bins<15>, 1, BINS_BLOCK, BINS_SMEM, st, P, T.bins); break;
       default: launch_pdl(k_pc_bins<0>, 1, BINS_BLOCK, BINS_SMEM, st, P, T.bins);
     }
+    if (T.cond) {
+      // frames whose particles carry prior weights finish per particle (the
+      // kernels of the other mode return at once)
+      mark();
+      k_pc_prior_ll<<<T.red_grid, 256, 0, st>>>(P);
+      mark();
+      k_sir_sum<<<T.red_grid, 256, 0, st>>>(P);
+      mark();
+      k_sir_stats<<<T.red_grid, 256, 0, st>>>(P);
+    }
     mark();
     if (T.rs_small) launch_pdl(k_sys_resample_small<1>, T.rs_small, SCAN_BLOCK, 0, st, P);
     else launch_pdl(k_sys_resample<1>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<1>), st, P);
+    if (T.cond) {
+      mark();
+      if (T.rs_small) launch_pdl(k_sys_resample_small<2>, T.rs_small, SCAN_BLOCK, 0, st, P);
+      else launch_pdl(k_sys_resample<2>, T.rs_grid2, SCAN_BLOCK, sizeof(RsSmem<2>), st, P);
+    }
   } else {
     mark();
     switch (T.maxs) {
@@ -843,6 +861,7 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   P.slot_lo = 0;
   P.slot_cap = n;
   P.scan_mode = 0;
+  P.method = cfg->method;
   PCS_SCRATCH(SL_TR_BUF0, 5 * ld * sizeof(float), P.buf0);
   PCS_SCRATCH(SL_TR_BUF1, 5 * ld * sizeof(float), P.buf1);
   PCS_SCRATCH(SL_TR_ANC, ld * sizeof(int), P.anc);
@@ -870,7 +889,15 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   } else {
     PCS_SCRATCH(SL_TR_PSLOT, ld * sizeof(u32), P.pslot);
     P.ll = nullptr;
+    P.wprev = nullptr;
+    P.lltab = nullptr;
     P.G = cfg->grid.n_cols * cfg->grid.n_rows;
+    T.cond = P.thresh < (double)n;   // threshold resampling: frames may carry prior weights
+    if (T.cond) {
+      PCS_SCRATCH(SL_TR_LL, ld * sizeof(double), P.ll);
+      PCS_SCRATCH(SL_TR_WPREV, ld * sizeof(float), P.wprev);
+      PCS_SCRATCH(SL_TR_LLTAB, P.G * sizeof(double), P.lltab);
+    }
     if (ctx->table_cells < P.G) {
       if (ctx->tab_cnt) cudaFree(ctx->tab_cnt);
       if (ctx->tab_sum) cudaFree(ctx->tab_sum);
@@ -938,14 +965,24 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
       PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sys_resample<2>, SCAN_BLOCK,
                                                                  sizeof(RsSmem<2>)));
     T.rs_grid = (int)std::min<i64>((i64)ctx->sms * std::max(per_sm, 1), ceil_div(n, (i64)RS_TILE));
+    T.rs_grid2 = T.rs_grid;
+    if (T.cond) {   // pcSIR frames with prior weights resample per particle
+      int per2 = 0;
+      PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_sys_resample<2>, SCAN_BLOCK,
+                                                                 sizeof(RsSmem<2>)));
+      T.rs_grid2 = (int)std::min<i64>((i64)ctx->sms * std::max(per2, 1), ceil_div(n, (i64)RS_TILE));
+    }
     // small N: one RSS_TILE tile per CTA when all those CTAs are co-resident
     int per_small = 0;
     if (cfg->method == 1)
       PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_small, k_sys_resample_small<1>,
                                                                  SCAN_BLOCK, 0));
-    else
-      PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_small, k_sys_resample_small<2>,
+    if (cfg->method == 0 || T.cond) {
+      int per2 = 0;
+      PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_sys_resample_small<2>,
                                                                  SCAN_BLOCK, 0));
+      per_small = (cfg->method == 0) ? per2 : std::min(per_small, per2);
+    }
     const i64 g_small = ceil_div(n, (i64)RSS_TILE);
     T.rs_small = (g_small <= (i64)ctx->sms * per_small && getenv("PCS_NO_RS_SMALL") == nullptr)
                      ? (int)g_small : 0;

@@ -94,8 +94,11 @@ struct TrackCtl {
   u32 gbar_cnt, gbar_gen;    // grid barrier of k_sys_resample
   u32 stats_done;            // k_sir_stats CTAs finished (the last one finalises)
   int fmap_ok;               // P.fmap describes the current frame batch (TMA staging)
-  int prior_nonuniform;      // SIR: particles carry the prior weights wprev (no resampling
-                             // at the previous frame, weights not all equal)
+  int prior_nonuniform;      // the NEXT frame starts from the prior weights wprev (no
+                             // resampling at this frame, weights not all equal)
+  int pc_prior;              // pcSIR: THIS frame has prior weights (copied from
+                             // prior_nonuniform by k_pc_step1 at the frame start)
+  i64 frame_occ;             // pcSIR with prior weights: occupied cells of the frame
 };
 
 struct TrackParams {
@@ -134,7 +137,9 @@ struct TrackParams {
   int scan_mode;             // 0 scan+emit, 1 scan only, 2 emit only (rank prefix in ctl)
   int s1_tile;               // k_pc_step1 tile (<= S1_TILE), balanced over its CTAs
   double thresh;             // resample when ESS < thresh (= threshold_fraction * N)
-  float* wprev;              // SIR: normalised prior weights when prior_nonuniform
+  float* wprev;              // normalised prior weights when prior_nonuniform
+  double* lltab;             // pcSIR with prior weights: [G] log-likelihood per cell
+  int method;                // 0 SIR, 1 pcSIR
   const void* fmap;          // device CUtensorMap of the frame batch [K][H][W] f32,
                              // boxes of FMAP_BX x FMAP_BY pixels (TMA staging)
   u128* cta_agg;             // k_sys_resample: per-CTA exact weight totals
@@ -409,6 +414,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
   pdl_trigger();
   if (C->flags & PCS_FLAG_CAPACITY) return;
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  if (blockIdx.x == 0 && t == 0) C->pc_prior = C->prior_nonuniform;   // read after this kernel
   const i64 k = C->k;
   const float* sin = (k & 1) ? P.buf1 : P.buf0;
   float* sout = (k & 1) ? P.buf0 : P.buf1;
@@ -861,6 +867,25 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   const bool bad_m = !(m == m) || m == INFINITY;
   const bool degenerate = (m == -INFINITY);
   PCS_PROBE(3);
+  if (C->pc_prior) {
+    // particles carry prior weights (no resampling at the previous frame):
+    // publish the per-cell log-likelihood; the per-particle weights
+    // log w = log w_prev + ll_cell (binning.py:190-192), normaliser, estimate,
+    // ESS and decision follow in k_pc_prior_ll / k_sir_sum / k_sir_stats
+    for (int b = t; b < M; b += BINS_BLOCK) {
+      const u32 cell = V.cell(b);
+      P.lltab[cell] = sm.ll[b];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        u64* p = P.tab_sum + ((i64)c * P.G + cell) * 2;
+        p[0] = 0;
+        p[1] = 0;
+      }
+      P.tab_cnt[cell] = 0;
+    }
+    if (t == 0) C->frame_occ = M;
+    return;
+  }
   // 4) normaliser S = sum_b cnt_b * round(exp(ll_b - m) * 2^95)
   {
     i128 acc[1] = {0};
@@ -930,9 +955,9 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     for (int c = 0; c < 5; ++c) out_est[ko * 5 + c] = est[c];
     out_ess[ko] = ess;
     const int res = (!flag_bad && ess < P.thresh) ? 1 : 0;   // filtering.py:169-170
-    // no resampling with unequal weights -> non-uniform prior next frame:
-    // only the general path carries per-particle prior weights
-    if (!res && !flag_bad && s_wmin != s_wmax) set_flag(C, PCS_FLAG_CAPACITY);
+    // no resampling with unequal weights -> the next frame starts from these
+    // per-cell weights (k_sys_resample<1> writes them per particle)
+    C->prior_nonuniform = (!res && !flag_bad && s_wmin != s_wmax) ? 1 : 0;
     out_res[ko] = (unsigned char)res;
     out_occ[ko] = M;
     C->evals = evals + M;
@@ -1309,12 +1334,15 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
   const int G = gridDim.x, cta = blockIdx.x;
   const i64 t0 = nt * cta / G, t1 = nt * (cta + 1) / G;
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  if (!C->do_resample) {   // identity ancestors; SIR keeps the normalised weights
-    const bool keep = (KIND == 2) && C->prior_nonuniform;
-    const double m = C->m, Sf = C->Sf;
+  // pcSIR frames with prior weights resample per particle (KIND 2), the others
+  // per cell (KIND 1); both are in the frame's launch sequence
+  if (KIND == 1 ? C->pc_prior != 0 : (P.method == 1 && C->pc_prior == 0)) return;
+  if (!C->do_resample) {   // identity ancestors; the particles keep their weights
+    const bool keep = C->prior_nonuniform;
+    const double Sf = C->Sf;
     for (i64 i = t0 * RS_TILE + threadIdx.x; i < min(n, t1 * RS_TILE); i += SCAN_BLOCK) {
       P.anc_out[P.idx_off + i - P.slot_lo] = (int)i;
-      if (keep) P.wprev[i] = weight_from_ex(P.ll[i], Sf);
+      if (keep) P.wprev[i] = (KIND == 1) ? P.wtab[P.pslot[i]] : weight_from_ex(P.ll[i], Sf);
     }
     return;
   }
@@ -1551,13 +1579,16 @@ __global__ void __launch_bounds__(SCAN_BLOCK, 4) k_sys_resample_small(TrackParam
   const i64 base = (i64)cta * RSS_TILE;
   const int nv = (int)min((i64)RSS_TILE, n - base);
   const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  if (!C->do_resample) {   // identity ancestors; SIR keeps the normalised weights
-    const bool keep = (KIND == 2) && C->prior_nonuniform;
-    const double m = C->m, Sf = C->Sf;
+  // pcSIR frames with prior weights resample per particle (KIND 2), the others
+  // per cell (KIND 1); both are in the frame's launch sequence
+  if (KIND == 1 ? C->pc_prior != 0 : (P.method == 1 && C->pc_prior == 0)) return;
+  if (!C->do_resample) {   // identity ancestors; the particles keep their weights
+    const bool keep = C->prior_nonuniform;
+    const double Sf = C->Sf;
     for (int k = threadIdx.x; k < nv; k += SCAN_BLOCK) {
       const i64 i = base + k;
       P.anc_out[P.idx_off + i - P.slot_lo] = (int)i;
-      if (keep) P.wprev[i] = weight_from_ex(P.ll[i], Sf);
+      if (keep) P.wprev[i] = (KIND == 1) ? P.wtab[P.pslot[i]] : weight_from_ex(P.ll[i], Sf);
     }
     return;
   }

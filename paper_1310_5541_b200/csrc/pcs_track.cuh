@@ -98,10 +98,32 @@ __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
   if (bad) set_flag(C, PCS_FLAG_NONFINITE);
 }
 
+// pcSIR frame whose particles carry prior weights (threshold resampling, no
+// resampling at the previous frame): per-particle log w = log(w_prev) +
+// ll[cell] (binning.py:190-192, filtering.py:69) and its maximum; the SIR
+// kernels below then normalise, estimate and resample per particle.
+__global__ void __launch_bounds__(256) k_pc_prior_ll(TrackParams P) {
+  TrackCtl* C = P.ctl;
+  if (!C->pc_prior) return;
+  long long lmax = LLONG_MIN;
+  bool bad = false;
+  for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < P.n; j += (i64)gridDim.x * blockDim.x) {
+    const double ll = __dadd_rn(log_prior(P.wprev[j]), P.lltab[P.pslot[j]]);
+    P.ll[j] = ll;
+    if (!(ll == ll) || ll == INFINITY) bad = true;
+    lmax = max(lmax, (long long)f64_to_ordered(ll));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+  if ((threadIdx.x & 31) == 0) atomicMax((long long*)&C->max_ll_ord, lmax);
+  if (bad) set_flag(C, PCS_FLAG_NONFINITE);
+}
+
 // S = sum round(exp(ll - m) * 2^95); leaves exp(ll - m) in P.ll
 __global__ void __launch_bounds__(256) k_sir_sum(TrackParams P) {
   __shared__ i128 sh[8];
   TrackCtl* C = P.ctl;
+  if (P.method == 1 && !C->pc_prior) return;   // pcSIR frame with uniform priors
   const double m = ordered_to_f64(C->max_ll_ord);
   i128 acc = 0;
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < P.n; j += (i64)gridDim.x * blockDim.x) {
@@ -139,8 +161,9 @@ __device__ __forceinline__ void sir_finalize(const TrackParams& P) {
   // are all equal (then uniform, as the general driver does)
   C->prior_nonuniform = (!res && !flag_bad && C->wmin_bits != C->wmax_bits) ? 1 : 0;
   C->out_res[ko] = (unsigned char)res;
-  C->out_occ[ko] = P.n;
-  C->evals += P.n;
+  const i64 evals = (P.method == 1) ? C->frame_occ : P.n;   // pcSIR: one per occupied cell
+  C->out_occ[ko] = evals;
+  C->evals += evals;
   C->do_resample = res;
   C->m = mf;
   C->Sf = scalbn(i128_to_f64_rn(load_i128(C->S)), -FX_S);
@@ -154,6 +177,7 @@ __device__ __forceinline__ void sir_finalize(const TrackParams& P) {
 __global__ void __launch_bounds__(256) k_sir_stats(TrackParams P) {
   __shared__ i128 sh[8];
   TrackCtl* C = P.ctl;
+  if (P.method == 1 && !C->pc_prior) return;   // pcSIR frame with uniform priors
   const i64 k = C->k;
   const float* st = (k & 1) ? P.buf0 : P.buf1;
   const double m = ordered_to_f64(C->max_ll_ord);

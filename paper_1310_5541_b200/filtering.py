@@ -322,9 +322,12 @@ def fused_track(frames, cfg: FilterConfig, rng, method, grid=None, placement=0, 
 
 
 def _fused_ok(cfg):
+    """The fused pcSIR loop: device likelihood, systematic resampling (any
+    ESS threshold: frames whose particles carry prior weights finish per
+    particle on the device)."""
     r = cfg.resampling
-    return (isinstance(cfg.likelihood, _DeviceLikelihood) and r.threshold_fraction == 1.0
-            and r.scheme == "systematic" and cfg.n_particles < 2 ** 31 - 1)
+    return (isinstance(cfg.likelihood, _DeviceLikelihood) and r.scheme == "systematic"
+            and cfg.n_particles < 2 ** 31 - 1)
 
 
 def _fused_sir_ok(cfg):

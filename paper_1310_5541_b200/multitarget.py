@@ -46,6 +46,10 @@ class MultiTargetTracker:
     """Device state of T filters; step() advances all of them by one frame."""
 
     def __init__(self, cfg, centers, seed, n_frames, height, width, target_offset=0):
+        r = cfg.resampling
+        if r.threshold_fraction != 1.0 or r.scheme != "systematic":
+            raise ValueError("the multi-target kernel resamples every frame (systematic, "
+                             "threshold_fraction=1.0); run pcsir_track per target otherwise")
         centers = np.ascontiguousarray(np.asarray(centers, dtype=np.float64).reshape(-1, 5))
         self.T = centers.shape[0]
         self.K = n_frames

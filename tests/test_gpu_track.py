@@ -207,6 +207,27 @@ def test_fused_sir_threshold_resampling_equals_general(cuda, frac):
     assert np.array_equal(a.ess, b.ess)
 
 
+@pytest.mark.parametrize("frac,cpp", [(0.2, 1), (0.5, 1), (0.5, 4)])
+def test_fused_pcsir_threshold_resampling_equals_general(cuda, frac, cpp):
+    # ESS-threshold resampling in the fused pcSIR loop: frames after a
+    # non-resampling frame carry per-particle prior weights (log w = log w_prev +
+    # ll[cell], binning.py:190-192) and finish per particle on the device
+    frames, truth, init, dyn = _c1_like(n=3000, k=12)
+    res = pc.ResampleConfig(frac, "systematic")
+    g = pc.BinGrid.pixel_aligned(64, 64, cpp)
+    a = pc.pcsir_track(frames, pc.PcFilterConfig(3000, init, dyn, res, _lik(), grid=g),
+                       pc.PhiloxRng(4))
+    lik_b = _lik()
+    b = pc.pcsir_track(frames, pc.PcFilterConfig(3000, init, dyn, res, lik_b, grid=g),
+                       pc.PhiloxRng(4), fused=False)
+    assert a.path == "fused" and b.path == "general"
+    assert 0 < int(np.sum(a.resampled)) < len(frames)   # both kinds of frames occur
+    assert np.array_equal(a.resampled, b.resampled)
+    assert np.array_equal(a.estimates, b.estimates)
+    assert np.array_equal(a.ess, b.ess)
+    assert a.likelihood_evals == b.likelihood_evals == lik_b.evals
+
+
 def _rounding_edge_positions(cpp, ncols):
     """Cell edges b and the float32 positions just below them whose float32
     p - origin rounds ONTO the edge (a float32 cell estimate that trusted
