@@ -58,6 +58,7 @@ struct S1Smem {
   unsigned short flist[SUBW];     // cells touched since the last flush
   u32 n_list, n_flist, n_in;
   int scan_tmp[S1_WARPS];
+  long long next_tile;
 };
 
 struct TrackCtl {
@@ -93,6 +94,7 @@ struct TrackCtl {
   u64 rank_prefix[2];        // sharded: exact cumulative weight of the preceding ranks
   u32 gbar_cnt, gbar_gen;    // grid barrier of k_sys_resample
   u32 stats_done;            // k_sir_stats CTAs finished (the last one finalises)
+  u32 s1_ticket, s1_done;    // k_pc_step1 dynamic tile tickets (reset by its last CTA)
   int fmap_ok;               // P.fmap describes the current frame batch (TMA staging)
   int prior_nonuniform;      // the NEXT frame starts from the prior weights wprev (no
                              // resampling at this frame, weights not all equal)
@@ -465,7 +467,9 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
   const int sx0i = (int)sx0, sy0i = (int)sy0;
   bool bad = false;
   int since = 0;
-  for (i64 tile = blockIdx.x; tile < ntile; tile += tstep) {
+  // first tile static, then dynamic tickets: CTAs on slower SMs (die / HBM
+  // distance) take fewer tiles instead of finishing last
+  for (i64 tile = blockIdx.x; tile < ntile;) {
     // ---- phase 1: gather + propagate + cell; rank within the tile's cell ----
     int q_k[S1_IPT], r_k[S1_IPT];
     float o_k[S1_IPT][5];
@@ -521,6 +525,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
       }
     }
     __syncthreads();
+    if (t == 0) sm.next_tile = tstep + (long long)atomicAdd(&C->s1_ticket, 1u);
     // ---- phase 2: run offsets (exclusive scan of the tile's cell counts) ----
     {
       const int nl = (int)sm.n_list;
@@ -569,6 +574,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
       sm.pay_q[idx] = (unsigned short)q_k[it];
     }
     __syncthreads();
+    const i64 next_tile = sm.next_tile;   // (written before the phase-2 barriers)
     // ---- phase 4: exact run sums over the sorted tile (8 warps, 4
     //      consecutive particles per lane, warp-segmented scan across lanes) ----
     if (t < S1_SUM_THREADS)
@@ -584,8 +590,13 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
       if (t == 0) sm.n_flist = 0;
       __syncthreads();
     }
+    tile = next_tile;
   }
   __syncthreads();
+  if (t == 0 && atomicAdd(&C->s1_done, 1u) == gridDim.x - 1) {   // every ticket is drawn
+    C->s1_ticket = 0;
+    C->s1_done = 0;
+  }
   s1_flush(P, C, sm, sx0, sy0, snxi);
   if (bad) set_flag(C, PCS_FLAG_NONFINITE);
 }
