@@ -947,6 +947,9 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
     PCS_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, 256, 0));
     T.prop_grid = (int)std::min<i64>((i64)grid_for(n, 256, ctx->sms, 8),
                                      (i64)ctx->sms * std::max(per_sm, 1));
+    // dynamic chunks of 2048 when every CTA gets >= 8 of them; below that a
+    // plain grid stride (c1/c2 sizes: the tickets would not pay)
+    P.sir_chunk = (n >= (i64)T.prop_grid * 8 * 2048) ? 2048 : 0;
   }
   T.s1_grid = (int)std::min<i64>((i64)ctx->sms * S1_CTAS_PER_SM, ceil_div(n, S1_TILE));
   {

@@ -95,6 +95,7 @@ struct TrackCtl {
   u32 gbar_cnt, gbar_gen;    // grid barrier of k_sys_resample
   u32 stats_done;            // k_sir_stats CTAs finished (the last one finalises)
   u32 s1_ticket, s1_done;    // k_pc_step1 dynamic tile tickets (reset by its last CTA)
+  u32 sir_ticket, sir_done;  // k_sir_propagate_lik dynamic chunk tickets
   int fmap_ok;               // P.fmap describes the current frame batch (TMA staging)
   int prior_nonuniform;      // the NEXT frame starts from the prior weights wprev (no
                              // resampling at this frame, weights not all equal)
@@ -142,6 +143,7 @@ struct TrackParams {
   float* wprev;              // normalised prior weights when prior_nonuniform
   double* lltab;             // pcSIR with prior weights: [G] log-likelihood per cell
   int method;                // 0 SIR, 1 pcSIR
+  int sir_chunk;             // k_sir_propagate_lik: particles per dynamic chunk
   const void* fmap;          // device CUtensorMap of the frame batch [K][H][W] f32,
                              // boxes of FMAP_BX x FMAP_BY pixels (TMA staging)
   u128* cta_agg;             // k_sys_resample: per-CTA exact weight totals

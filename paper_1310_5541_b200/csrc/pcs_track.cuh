@@ -67,7 +67,16 @@ __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
   bool bad = false;
   const i64 n = P.n, ld = P.ld;
   const bool prior = C->prior_nonuniform != 0;
-  for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < n; j += (i64)gridDim.x * blockDim.x) {
+  // chunks of SIR_CHUNK particles: the first static, then dynamic tickets (a
+  // CTA on a slower SM takes fewer chunks)
+  // (P.sir_chunk == 0: plain grid stride, chunk = one block, no tickets)
+  __shared__ long long s_next;
+  const bool dyn = P.sir_chunk > 0;
+  const i64 SIR_CHUNK = dyn ? P.sir_chunk : blockDim.x;
+  const i64 nch = ceil_div(n, SIR_CHUNK);
+  for (i64 ch = blockIdx.x; ch < nch;) {
+    if (dyn && threadIdx.x == 0) s_next = gridDim.x + (long long)atomicAdd(&C->sir_ticket, 1u);
+    for (i64 j = ch * SIR_CHUNK + threadIdx.x; j < min(n, (ch + 1) * SIR_CHUNK); j += blockDim.x) {
     i64 src = (i64)__ldg(P.anc + j);
     float s[5], z[5], o[5];
 #pragma unroll
@@ -91,6 +100,18 @@ __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
     P.ll[j] = ll;
     if (!(ll == ll) || ll == INFINITY) bad = true;
     lmax = max(lmax, (long long)f64_to_ordered(ll));
+    }
+    if (dyn) {
+      __syncthreads();
+      ch = s_next;
+      __syncthreads();   // s_next is rewritten at the top of the next chunk
+    } else {
+      ch += gridDim.x;
+    }
+  }
+  if (dyn && threadIdx.x == 0 && atomicAdd(&C->sir_done, 1u) == gridDim.x - 1) {   // all drawn
+    C->sir_ticket = 0;
+    C->sir_done = 0;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
