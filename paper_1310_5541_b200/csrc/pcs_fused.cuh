@@ -783,7 +783,8 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     const u32 cnt = P.tab_cnt[cell];
     float d[5];
 #pragma unroll
-    for (int c = 0; c < 5; ++c) {
+    for (int c = 0; c < 5; ++c) {   // only x, y, I0 enter the likelihood (vx, vy unused)
+      if (c == 2 || c == 3) { d[c] = 0.0f; continue; }
       const double num = i128_to_f64_rn(load_i128(P.tab_sum + ((i64)c * P.G + cell) * 2));
       d[c] = __double2float_rn(scalbn(__ddiv_rn(num, (double)cnt), -FX_STATE));
     }
