@@ -403,3 +403,20 @@ def test_eval_count_is_occupied_cells(cuda):
                        pc.PhiloxRng(1))
     assert r.likelihood_evals == lik.evals
     assert r.likelihood_evals < 10000 * len(frames) / 10
+
+
+@pytest.mark.parametrize("n", [1, 2, 31, 257, 1023, 1025, 1793, 3841])
+def test_fused_equals_general_at_ragged_sizes(cuda, n):
+    # particle counts around warp / tile / resampling-tile boundaries
+    # (32, 1024 step-1 tile, 1792 and 3840 resampler tiles) and N = 1
+    frames, truth, init, dyn = _c1_like(k=4)
+    g = pc.BinGrid.pixel_aligned(64, 64, 2)
+    for fused_fn, cfg_fn in (
+            (pc.pcsir_track, lambda lik: pc.PcFilterConfig(n, init, dyn, RES, lik, grid=g)),
+            (pc.sir_track, lambda lik: pc.FilterConfig(n, init, dyn, RES, lik))):
+        a = fused_fn(frames, cfg_fn(_lik()), pc.PhiloxRng(6), fused=True)
+        b = fused_fn(frames, cfg_fn(_lik()), pc.PhiloxRng(6), fused=False)
+        assert a.path == "fused" and b.path == "general"
+        assert np.array_equal(a.estimates, b.estimates)
+        assert np.array_equal(a.ess, b.ess)
+        assert np.array_equal(a.resampled, b.resampled)
