@@ -495,8 +495,9 @@ def main():
                "h2d_bytes_per_step": int(wl["width"] * wl["width"] * 4),
                "d2h_bytes_per_step": 5 * 8 + 8 + 1 + 8, "path": r.path,
                "note": "pcsir_track/sir_track on a pinned (K,H,W) float32 host tensor: wall "
-                       "time incl. frame upload, particle init, graph capture and result "
-                       "download; median of 3 calls"}
+                       "time incl. frame upload (chunks on a side stream overlapping the "
+                       "filter), particle init, graph capture and result download; median "
+                       "of 3 calls"}
         variants = {}
         if not args.no_variants:
             for name in OTHER_VARIANTS.get(wl_name, []):

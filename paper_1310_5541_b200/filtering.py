@@ -282,7 +282,28 @@ def fused_track(frames, cfg: FilterConfig, rng, method, grid=None, placement=0, 
     or raises CapacityError when the general path is needed."""
     prng = as_philox(rng)
     frame0 = prng.frame
-    dev_frames = _frames_to_device(frames)
+    # a pinned host tensor of >= 8 MB is uploaded in up to 4 chunks on a side
+    # stream, each chunk's frames filtered as soon as it has arrived
+    pipelined = (isinstance(frames, torch.Tensor) and not frames.is_cuda and frames.dim() == 3
+                 and frames.dtype == torch.float32 and frames.is_pinned() and frames.shape[0] >= 2
+                 and frames.numel() * 4 >= (8 << 20))
+    if pipelined:
+        host = frames.contiguous()
+        dev_frames = torch.empty(host.shape, dtype=torch.float32, device=_lib.device())
+        nch = min(4, host.shape[0])
+        bounds = np.linspace(0, host.shape[0], nch + 1).astype(int)
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())   # dev_frames allocated
+        arrived = []
+        with torch.cuda.stream(side):
+            for a, b in zip(bounds[:-1], bounds[1:]):
+                dev_frames[a:b].copy_(host[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(side)
+                arrived.append(ev)
+        dev_frames.record_stream(torch.cuda.current_stream())
+    else:
+        dev_frames = _frames_to_device(frames)
     k, h, w = dev_frames.shape
     lik = cfg.likelihood
     c = _lib.PcsTrackCfg()
@@ -304,10 +325,22 @@ def fused_track(frames, cfg: FilterConfig, rng, method, grid=None, placement=0, 
     res = torch.empty(k, dtype=torch.uint8, device=dev)
     occ = torch.empty(k, dtype=torch.int64, device=dev)
     out = _lib.PcsTrackResult()
-    rc = _lib.lib().pcs_track(_lib.ctx(), ctypes.byref(c), _lib.ptr(dev_frames), k, h, w,
-                              _lib.ptr(est), _lib.ptr(ess), _lib.ptr(res), _lib.ptr(occ),
-                              ctypes.byref(out), _lib.stream())
-    _lib.check(rc, "pcs_track")
+    if pipelined:
+        L, ctx, st = _lib.lib(), _lib.ctx(), _lib.stream()
+        _lib.check(L.pcs_track_begin(ctx, ctypes.byref(c), h, w, st), "pcs_track_begin")
+        for (a, b), ev in zip(zip(bounds[:-1], bounds[1:]), arrived):
+            torch.cuda.current_stream().wait_event(ev)
+            rc = L.pcs_track_steps(ctx, _lib.ptr(dev_frames[a:]), int(a), int(b), _lib.ptr(est[a:]),
+                                   _lib.ptr(ess[a:]), _lib.ptr(res[a:]), _lib.ptr(occ[a:]), st)
+            if rc:
+                L.pcs_track_end(ctx, ctypes.byref(out), st)
+                _lib.check(rc, "pcs_track_steps")
+        _lib.check(L.pcs_track_end(ctx, ctypes.byref(out), st), "pcs_track")
+    else:
+        rc = _lib.lib().pcs_track(_lib.ctx(), ctypes.byref(c), _lib.ptr(dev_frames), k, h, w,
+                                  _lib.ptr(est), _lib.ptr(ess), _lib.ptr(res), _lib.ptr(occ),
+                                  ctypes.byref(out), _lib.stream())
+        _lib.check(rc, "pcs_track")
     if out.flags & _lib.FLAG_NONFINITE:
         raise ValueError("likelihood values must be finite and >= 0")
     if out.flags & _lib.FLAG_DEGENERATE:

@@ -420,3 +420,22 @@ def test_fused_equals_general_at_ragged_sizes(cuda, n):
         assert np.array_equal(a.estimates, b.estimates)
         assert np.array_equal(a.ess, b.ess)
         assert np.array_equal(a.resampled, b.resampled)
+
+
+def test_pinned_host_frames_pipelined_upload(cuda):
+    # a pinned float32 (K,H,W) host tensor is uploaded in chunks on a side
+    # stream and filtered chunk by chunk: same result as device-resident frames
+    from paper_1310_5541_b200 import synthesis as syn
+    dev, truth = syn.spot_scene(9, 512, (203.0, 256.0), seed=2)
+    host = dev.cpu().pin_memory()
+    init = pc.InitSpec(pc.StateVector(203.0, 256.0, 0.5, 0.0, 20.0), "gauss", sigma=2.0)
+    dyn = pc.DynamicsParams(0.5, 0.1, 1.0)
+    g = pc.BinGrid.pixel_aligned(512, 512, 2)
+    for res in (RES, pc.ResampleConfig(0.5, "systematic")):
+        a = pc.pcsir_track(host, pc.PcFilterConfig(20000, init, dyn, res, _lik(), grid=g),
+                           pc.PhiloxRng(3))
+        b = pc.pcsir_track(dev, pc.PcFilterConfig(20000, init, dyn, res, _lik(), grid=g),
+                           pc.PhiloxRng(3))
+        assert a.path == b.path == "fused"
+        assert np.array_equal(a.estimates, b.estimates)
+        assert np.array_equal(a.resampled, b.resampled)
