@@ -30,6 +30,8 @@ namespace pcs {
 constexpr int MT_THREADS = 512;
 constexpr int MT_IPT = 2;
 constexpr int MT_TILE = MT_THREADS * MT_IPT;   // 1024
+constexpr int MT_E = 4;                        // sorted particles per lane in the run sums
+constexpr int MT_SUM_THREADS = MT_TILE / MT_E; // 256
 constexpr int MT_WARPS = MT_THREADS / 32;
 constexpr int MT_SIDE = 24;
 constexpr int MT_SUBW = MT_SIDE * MT_SIDE;     // sub-window cells (24 x 24)
@@ -283,14 +285,15 @@ __global__ void __launch_bounds__(MT_THREADS, 2) k_mt_frame(MtParams P) {
     for (int it = 0; it < MT_IPT; ++it) {
       if (q_k[it] < 0) continue;
       const int pos = (int)sm.tile_start[q_k[it]] + r_k[it];
-      const int idx = (pos % MT_IPT) * MT_THREADS + pos / MT_IPT;
+      const int idx = (pos % MT_E) * MT_SUM_THREADS + pos / MT_E;   // lane-major for the sums
 #pragma unroll
       for (int c = 0; c < 5; ++c) sm.u.a.pay[c][idx] = o_k[it][c];
       sm.u.a.pay_q[idx] = (unsigned short)q_k[it];
     }
     __syncthreads();
-    tile_run_sums<MT_THREADS, MT_IPT, MT_TILE, MT_SUBW>(sm.u.a.pay, sm.u.a.pay_q, (int)sm.n_in,
-                                                        &sm.dig[0][0], t);
+    if (t < MT_SUM_THREADS)   // 8 warps, 4 sorted particles per lane (as in k_pc_step1)
+      tile_run_sums<MT_SUM_THREADS, MT_E, MT_TILE, MT_SUBW>(sm.u.a.pay, sm.u.a.pay_q, (int)sm.n_in,
+                                                            &sm.dig[0][0], t);
     // no barrier: the next tile's phase 1 touches none of pay / pay_q / n_in
   }
   __syncthreads();
