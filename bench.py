@@ -306,7 +306,7 @@ def _c4_cpu_worker(args):
 def cpu_sample(wl_name, wl, frames_host, cpp, pool_cores=1):
     """A bounded sample (~10-30 s of CPU work) of the workload on this host."""
     if wl_name in ("c1", "c2"):
-        nf = {"c1": 50, "c2": 12}[wl_name]
+        nf = {"c1": 50, "c2": 40}[wl_name]   # c2: ~10 s on one core
         v, dt, kern = cpu_port_track(wl, wl["n"], frames_host[:nf], wl["start"], cpp)
         return v, 1, f"{nf} frames x N={wl['n']} ({kern}), {dt:.1f} s on 1 core"
     if wl_name in ("c3", "c5"):
