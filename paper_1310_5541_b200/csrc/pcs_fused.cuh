@@ -43,6 +43,9 @@ constexpr int MAXM = 16384;                    // occupied cells per frame (fuse
 // and S >> 36 (signed) with native 32-bit shared atomics. A cell gets <= 16
 // additions per tile, so over S1_FLUSH_TILES tiles the digits stay below 2^30
 // in magnitude; the CTA then folds them into the exact int128 HBM table.
+// Scheduling: a CTA's first tile is blockIdx.x, later ones come from a
+// ticket counter (CTAs on slower SMs take fewer tiles); the other 8 warps do
+// not wait for the run sums but start gathering the next tile.
 struct S1Smem {
   float pay[5][S1_TILE];   // cell-sorted tile, lane-major for phase 4 (sorted
                            // position p at (p % S1_E) * S1_SUM_THREADS + p / S1_E):
