@@ -180,7 +180,7 @@ int pcs_resample_multinomial(pcs_ctx* ctx, const float* w, int64_t n, const doub
 int pcs_cdf(pcs_ctx* ctx, const float* w, int64_t n, double* cdf, void* stream);
 
 /* ---- fused filter (sir_track filtering.py:176-182 / pcsir_track
- * binning.py:212-226 with ResampleConfig(threshold_fraction=1, systematic)).
+ * binning.py:212-226; any ResampleConfig threshold, systematic or multinomial).
  * frames: K x H x W float32 device. Outputs (device): est[K*5] f64,
  * ess[K] f64, resampled[K] u8, occupied[K] i64 (likelihood evals per frame).
  * method 0 = SIR, 1 = pcSIR. Returns PCS_E_CAPACITY (with flags) when a
@@ -198,6 +198,8 @@ typedef struct pcs_track_cfg_t {
   int32_t use_graph;     /* capture one frame as a CUDA graph and replay it */
   double threshold_fraction;  /* resample when ESS < threshold_fraction * N
                                  (filtering.py:169-170); 0 means 1.0 */
+  int32_t scheme;        /* 0 systematic, 1 multinomial (filtering.py:96-100) */
+  int32_t reserved;
 } pcs_track_cfg_t;
 
 typedef struct pcs_track_result_t {

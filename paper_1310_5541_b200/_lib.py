@@ -61,7 +61,8 @@ class PcsTrackCfg(ctypes.Structure):
     _fields_ = [("method", c_int32), ("placement", c_int32), ("n_particles", c_int64),
                 ("init", PcsInit), ("dyn", PcsDynamics), ("spot", PcsSpot),
                 ("grid", PcsGrid), ("seed", c_uint64), ("frame0", c_uint32),
-                ("use_graph", c_int32), ("threshold_fraction", c_double)]
+                ("use_graph", c_int32), ("threshold_fraction", c_double),
+                ("scheme", c_int32), ("reserved", c_int32)]
 
 
 class PcsTrackResult(ctypes.Structure):

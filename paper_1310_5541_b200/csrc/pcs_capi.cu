@@ -69,6 +69,8 @@ struct TrackState {
   int red_grid = 0;      // k_sir_sum / k_sir_stats CTAs
   bool cond = false;     // pcSIR with threshold resampling (7-launch frame)
   int rs_grid2 = 0;      // k_sys_resample<2> CTAs in that mode
+  static constexpr int MAX_LAUNCHES = 12;
+  const char* names[MAX_LAUNCHES] = {};   // kernel of each launch of a frame
   int prop_grid = 0;
   int maxs = 0;
   i64 k = 0;             // host mirror of the frame counter
@@ -132,6 +134,7 @@ enum Slot {
   SL_FMAP,
   SL_TR_WPREV,
   SL_TR_LLTAB,
+  SL_TR_CDF,
   SL_COUNT
 };
 
@@ -717,9 +720,6 @@ static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 }
 }  // extern "C++"
 
-static const char* kPcNames[] = {"k_pc_step1", "k_pc_bins", "k_sys_resample"};
-static const char* kSirNames[] = {"k_sir_propagate_lik", "k_sir_sum", "k_sir_stats",
-                                  "k_sys_resample"};
 
 // Enqueue one frame. If evs is non-null, evs[i] is recorded before launch i
 // and evs[launches] after the last one (per-kernel CUDA-event timing).
@@ -727,14 +727,15 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
   TrackState& T = ctx->tr;
   TrackParams& P = T.P;
   int q = 0;
-  auto mark = [&]() {
+  auto mark = [&](const char* name) {   // event before launch q; its name for the timings
     if (evs) cudaEventRecord(evs[q], st);
+    if (q < TrackState::MAX_LAUNCHES) T.names[q] = name;
     ++q;
   };
   if (T.cfg.method == 1) {
-    mark();
+    mark("k_pc_step1");
     k_pc_step1<<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(P);
-    mark();
+    mark("k_pc_bins");
     switch (T.maxs) {
       case 9: launch_pdl(k_pc_bins<9>, 1, BINS_BLOCK, BINS_SMEM, st, P, T.bins); break;
       case 11: launch_pdl(k_pc_bins<11>, 1, BINS_BLOCK, BINS_SMEM, st, P, T.bins); break;
@@ -744,36 +745,44 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
     if (T.cond) {
       // frames whose particles carry prior weights finish per particle (the
       // kernels of the other mode return at once)
-      mark();
+      mark("k_pc_prior_ll");
       k_pc_prior_ll<<<T.red_grid, 256, 0, st>>>(P);
-      mark();
+      mark("k_sir_sum");
       k_sir_sum<<<T.red_grid, 256, 0, st>>>(P);
-      mark();
+      mark("k_sir_stats");
       k_sir_stats<<<T.red_grid, 256, 0, st>>>(P);
     }
-    mark();
+    mark("k_sys_resample");
     if (T.rs_small) launch_pdl(k_sys_resample_small<1>, T.rs_small, SCAN_BLOCK, 0, st, P);
     else launch_pdl(k_sys_resample<1>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<1>), st, P);
     if (T.cond) {
-      mark();
+      mark("k_sys_resample:prior");
       if (T.rs_small) launch_pdl(k_sys_resample_small<2>, T.rs_small, SCAN_BLOCK, 0, st, P);
       else launch_pdl(k_sys_resample<2>, T.rs_grid2, SCAN_BLOCK, sizeof(RsSmem<2>), st, P);
     }
+    if (P.multinomial) {
+      mark("k_multinomial_emit");
+      k_multinomial_emit<<<grid_for(P.n, 256, ctx->sms), 256, 0, st>>>(P);
+    }
   } else {
-    mark();
+    mark("k_sir_propagate_lik");
     switch (T.maxs) {
       case 9: k_sir_propagate_lik<9><<<T.prop_grid, 256, 0, st>>>(P); break;
       case 11: k_sir_propagate_lik<11><<<T.prop_grid, 256, 0, st>>>(P); break;
       case 15: k_sir_propagate_lik<15><<<T.prop_grid, 256, 0, st>>>(P); break;
       default: k_sir_propagate_lik<0><<<T.prop_grid, 256, 0, st>>>(P);
     }
-    mark();
+    mark("k_sir_sum");
     k_sir_sum<<<T.red_grid, 256, 0, st>>>(P);
-    mark();
+    mark("k_sir_stats");
     k_sir_stats<<<T.red_grid, 256, 0, st>>>(P);   // its last CTA finalises the frame
-    mark();
+    mark("k_sys_resample");
     if (T.rs_small) launch_pdl(k_sys_resample_small<2>, T.rs_small, SCAN_BLOCK, 0, st, P);
     else launch_pdl(k_sys_resample<2>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<2>), st, P);
+    if (P.multinomial) {
+      mark("k_multinomial_emit");
+      k_multinomial_emit<<<grid_for(P.n, 256, ctx->sms), 256, 0, st>>>(P);
+    }
   }
   if (evs) cudaEventRecord(evs[q], st);
   PCS_LAUNCH_CHECK();
@@ -862,6 +871,10 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   P.slot_cap = n;
   P.scan_mode = 0;
   P.method = cfg->method;
+  PCS_CHECK_ARG(cfg->scheme == 0 || cfg->scheme == 1, "scheme must be 0 (systematic) or 1 (multinomial)");
+  P.multinomial = cfg->scheme;
+  P.cdf = nullptr;
+  if (P.multinomial) PCS_SCRATCH(SL_TR_CDF, ld * sizeof(double), P.cdf);
   PCS_SCRATCH(SL_TR_BUF0, 5 * ld * sizeof(float), P.buf0);
   PCS_SCRATCH(SL_TR_BUF1, 5 * ld * sizeof(float), P.buf1);
   PCS_SCRATCH(SL_TR_ANC, ld * sizeof(int), P.anc);
@@ -1080,7 +1093,7 @@ int pcs_track_steps_timed(pcs_ctx* ctx, const float* frames, int64_t k0, int64_t
   const int fm = frame_map(T, frames, k1 - k0, st);
   k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frames, k0, k0, est, ess, res, (i64*)occ, fm);
   PCS_LAUNCH_CHECK();
-  const int NE = 8;
+  const int NE = TrackState::MAX_LAUNCHES + 1;
   cudaEvent_t evs[NE];
   for (int i = 0; i < NE; ++i) PCS_CUDA_TRY(cudaEventCreate(&evs[i]));
   for (int i = 0; i < max_kernels; ++i) kernel_ms[i] = 0.0;
@@ -1094,7 +1107,7 @@ int pcs_track_steps_timed(pcs_ctx* ctx, const float* frames, int64_t k0, int64_t
       r = PCS_E_CUDA;
       break;
     }
-    for (int q = 0; q < T.launches; ++q) {
+    for (int q = 0; q < std::min(T.launches, (int)max_kernels); ++q) {
       float ms = 0.f;
       cudaEventElapsedTime(&ms, evs[q], evs[q + 1]);
       kernel_ms[q] += ms;
@@ -1106,9 +1119,8 @@ int pcs_track_steps_timed(pcs_ctx* ctx, const float* frames, int64_t k0, int64_t
 }
 
 const char* pcs_track_kernel_name(pcs_ctx* ctx, int32_t i) {
-  if (!ctx) return "";
-  if (ctx->tr.cfg.method == 1) return (i >= 0 && i < 3) ? kPcNames[i] : "";
-  return (i >= 0 && i < 4) ? kSirNames[i] : "";
+  if (!ctx || i < 0 || i >= ctx->tr.launches || i >= TrackState::MAX_LAUNCHES) return "";
+  return ctx->tr.names[i] ? ctx->tr.names[i] : "";
 }
 
 int pcs_track_end(pcs_ctx* ctx, pcs_track_result_t* result, void* stream) {

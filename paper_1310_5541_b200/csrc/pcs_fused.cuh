@@ -99,6 +99,7 @@ struct TrackCtl {
   u32 stats_done;            // k_sir_stats CTAs finished (the last one finalises)
   u32 s1_ticket, s1_done;    // k_pc_step1 dynamic tile tickets (reset by its last CTA)
   u32 sir_ticket, sir_done;  // k_sir_propagate_lik dynamic chunk tickets
+  u32 res_frame;             // RNG frame of this frame's resampling (multinomial points)
   int fmap_ok;               // P.fmap describes the current frame batch (TMA staging)
   int prior_nonuniform;      // the NEXT frame starts from the prior weights wprev (no
                              // resampling at this frame, weights not all equal)
@@ -147,6 +148,8 @@ struct TrackParams {
   double* lltab;             // pcSIR with prior weights: [G] log-likelihood per cell
   int method;                // 0 SIR, 1 pcSIR
   int sir_chunk;             // k_sir_propagate_lik: particles per dynamic chunk
+  int multinomial;           // resampling scheme: the resampler writes the cdf and
+  double* cdf;               // [N] k_multinomial_emit searches it
   const void* fmap;          // device CUtensorMap of the frame batch [K][H][W] f32,
                              // boxes of FMAP_BX x FMAP_BY pixels (TMA staging)
   u128* cta_agg;             // k_sys_resample: per-CTA exact weight totals
@@ -982,6 +985,7 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     C->m = m;
     C->Sf = Sf;
     C->u = u_next;
+    C->res_frame = P.frame0 + (u32)k;
     if (!flag_bad) {
       C->center[0] = est[0];
       C->center[1] = est[1];
@@ -1482,9 +1486,19 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
       int jr = 0;
       if (k0 < nv && off + base + k0 != 0) jr = slot_rel(excl, u, ng, nd, kappa, eps, tj0d, tj0);
       u128 run = excl;
+      if (P.multinomial) {   // the exact cdf per particle (filtering.py:94-95)
+#pragma unroll
+        for (int q = 0; q < RS_ITEMS; ++q) {
+          const int k = k0 + q;
+          if (k < nv) {
+            run += weight(buf, k, nv);
+            P.cdf[base + k] = (k == klast) ? 1.0 : cdf_round(run);
+          }
+        }
+      }
       const u32 hp_s = smem_u32(hp + k0), st_s = smem_u32(stage + k0);
 #pragma unroll
-      for (int q = 0; q < RS_ITEMS; ++q) {
+      for (int q = 0; q < (P.multinomial ? 0 : RS_ITEMS); ++q) {
         const int k = k0 + q;
         int h = -1;   // no slot
         if (k < nv) {
@@ -1499,7 +1513,8 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
     }
     __syncthreads();   // every read of ring[L & 1] is done; it is free for load L + 2
     // slots in chunks of RS_TILE: heads, block max-scan, coalesced writes
-    const int m_slots = (int)(tj1 - tj0);   // <= ng < 2^31
+    // (multinomial: k_multinomial_emit draws the slots)
+    const int m_slots = P.multinomial ? 0 : (int)(tj1 - tj0);   // <= ng < 2^31
     int carry = -1;
     const u32 stage_s = smem_u32(stage), hp_s = smem_u32(hp + k0);
     for (int c0 = 0; c0 < m_slots; c0 += RS_TILE) {
@@ -1676,6 +1691,17 @@ __global__ void __launch_bounds__(SCAN_BLOCK, 4) k_sys_resample_small(TrackParam
     int jr = 0;
     if (k0 < nv && off + base + k0 != 0) jr = slot_rel(excl, u, ng, nd, kappa, eps, tj0d, tj0);
     u128 run = excl;
+    if (P.multinomial) {   // the exact cdf per particle (filtering.py:94-95); no emission
+#pragma unroll
+      for (int q = 0; q < RSS_ITEMS; ++q) {
+        const int k = k0 + q;
+        if (k < nv) {
+          run += weight(k);
+          P.cdf[base + k] = (k == klast) ? 1.0 : cdf_round(run);
+        }
+      }
+      return;
+    }
 #pragma unroll
     for (int q = 0; q < RSS_ITEMS; ++q) {
       const int k = k0 + q;
@@ -1742,6 +1768,28 @@ __global__ void __launch_bounds__(SCAN_BLOCK, 4) k_sys_resample_small(TrackParam
   }
   if (oob) set_flag(C, PCS_FLAG_CAPACITY);
   RS_PROBE(4);
+}
+
+// Multinomial resampling of the fused loops (filtering.py:96-97,100): point
+// j = philox_multinomial_u(seed, frame, j) (the general path's
+// pcs_philox_multinomial_points), ancestor = searchsorted(cdf, p, 'right')
+// over the exact cdf the resampler wrote (N-1 at most).
+__global__ void __launch_bounds__(256) k_multinomial_emit(TrackParams P) {
+  TrackCtl* C = P.ctl;
+  if (!C->do_resample) return;   // the resampler wrote the identity
+  const u32 f = C->res_frame;
+  const i64 n = P.n;
+  const double* __restrict__ cdf = P.cdf;
+  for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < n; j += (i64)gridDim.x * blockDim.x) {
+    const double p = philox_multinomial_u(P.seed, f, (u64)j);
+    i64 lo = 0, hi = n;   // first index with cdf > p
+    while (lo < hi) {
+      const i64 mid = (lo + hi) >> 1;
+      if (__ldg(cdf + mid) <= p) lo = mid + 1;
+      else hi = mid;
+    }
+    P.anc_out[j] = (int)((lo < n) ? lo : n - 1);
+  }
 }
 
 constexpr size_t S1_SMEM = sizeof(S1Smem);

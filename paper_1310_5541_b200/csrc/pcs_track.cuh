@@ -189,6 +189,7 @@ __device__ __forceinline__ void sir_finalize(const TrackParams& P) {
   C->m = mf;
   C->Sf = scalbn(i128_to_f64_rn(load_i128(C->S)), -FX_S);
   C->u = philox_resample_u(P.seed, P.frame0 + (u32)k);
+  C->res_frame = P.frame0 + (u32)k;
   reset_frame(C);
   C->k = k + 1;
 }

@@ -5,12 +5,11 @@ Mirrors ``pcsir.filtering`` (filtering.py:1-182). Two drivers share one set
 of canonical device arithmetic:
 
 * the fused device loop (``pcs_track``: one captured CUDA graph per frame, no
-  host synchronisation) for the built-in likelihoods with
-  ``ResampleConfig(threshold_fraction=1.0, scheme="systematic")`` — the
-  benchmark configurations;
-* the general step-by-step driver (``_track``) for every other setting
-  (ESS-threshold resampling, multinomial, duck-typed likelihoods, grids whose
-  occupied-bin window exceeds the fused capacity).
+  host synchronisation) for the built-in likelihoods, systematic or
+  multinomial resampling at any ESS threshold;
+* the general step-by-step driver (``_track``) for duck-typed likelihoods,
+  grids whose occupied-bin window exceeds the fused capacity, and on request
+  (``fused=False``).
 
 Both produce identical estimates / ESS / resampling decisions.
 """
@@ -319,6 +318,7 @@ def fused_track(frames, cfg: FilterConfig, rng, method, grid=None, placement=0, 
     c.frame0 = frame0
     c.use_graph = 1 if use_graph else 0
     c.threshold_fraction = cfg.resampling.threshold_fraction
+    c.scheme = 1 if cfg.resampling.scheme == "multinomial" else 0
     dev = dev_frames.device
     est = torch.empty((k, 5), dtype=torch.float64, device=dev)
     ess = torch.empty(k, dtype=torch.float64, device=dev)
@@ -355,20 +355,20 @@ def fused_track(frames, cfg: FilterConfig, rng, method, grid=None, placement=0, 
 
 
 def _fused_ok(cfg):
-    """The fused pcSIR loop: device likelihood, systematic resampling (any
-    ESS threshold: frames whose particles carry prior weights finish per
-    particle on the device)."""
+    """The fused pcSIR loop: device likelihood, systematic or multinomial
+    resampling, any ESS threshold (frames whose particles carry prior weights
+    finish per particle on the device)."""
     r = cfg.resampling
-    return (isinstance(cfg.likelihood, _DeviceLikelihood) and r.scheme == "systematic"
-            and cfg.n_particles < 2 ** 31 - 1)
+    return (isinstance(cfg.likelihood, _DeviceLikelihood)
+            and r.scheme in ("systematic", "multinomial") and cfg.n_particles < 2 ** 31 - 1)
 
 
 def _fused_sir_ok(cfg):
     """The fused SIR loop also runs ESS-threshold resampling (threshold < 1):
     per-particle prior weights stay on the device between frames."""
     r = cfg.resampling
-    return (isinstance(cfg.likelihood, _DeviceLikelihood) and r.scheme == "systematic"
-            and cfg.n_particles < 2 ** 31 - 1)
+    return (isinstance(cfg.likelihood, _DeviceLikelihood)
+            and r.scheme in ("systematic", "multinomial") and cfg.n_particles < 2 ** 31 - 1)
 
 
 def sir_track(frames, cfg: FilterConfig, rng, fused=None) -> TrackResult:

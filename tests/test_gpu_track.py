@@ -439,3 +439,30 @@ def test_pinned_host_frames_pipelined_upload(cuda):
         assert a.path == b.path == "fused"
         assert np.array_equal(a.estimates, b.estimates)
         assert np.array_equal(a.resampled, b.resampled)
+
+
+@pytest.mark.parametrize("frac", [1.0, 0.5])
+@pytest.mark.parametrize("method", ["sir", "pc"])
+def test_fused_multinomial_equals_general(cuda, frac, method):
+    # multinomial resampling (filtering.py:96-97,100) in the fused loops: the
+    # resampler writes the exact cdf, k_multinomial_emit searches the frame's
+    # Philox points — bit-identical to the step-by-step driver
+    frames, truth, init, dyn = _c1_like(n=3000, k=10)
+    res = pc.ResampleConfig(frac, "multinomial")
+    g = pc.BinGrid.pixel_aligned(64, 64, 2)
+
+    def run(fused):
+        lik = _lik()
+        if method == "sir":
+            return pc.sir_track(frames, pc.FilterConfig(3000, init, dyn, res, lik),
+                                pc.PhiloxRng(12), fused=fused), lik
+        return pc.pcsir_track(frames, pc.PcFilterConfig(3000, init, dyn, res, lik, grid=g),
+                              pc.PhiloxRng(12), fused=fused), lik
+
+    (a, la), (b, lb) = run(True), run(False)
+    assert a.path == "fused" and b.path == "general"
+    assert np.any(a.resampled)
+    assert np.array_equal(a.resampled, b.resampled)
+    assert np.array_equal(a.estimates, b.estimates)
+    assert np.array_equal(a.ess, b.ess)
+    assert la.evals == lb.evals
