@@ -754,10 +754,12 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
     }
     mark("k_sys_resample");
     if (T.rs_small) launch_pdl(k_sys_resample_small<1>, T.rs_small, SCAN_BLOCK, 0, st, P);
+    else if (P.multinomial) launch_pdl(k_sys_resample<1, true>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<1>), st, P);
     else launch_pdl(k_sys_resample<1>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<1>), st, P);
     if (T.cond) {
       mark("k_sys_resample:prior");
       if (T.rs_small) launch_pdl(k_sys_resample_small<2>, T.rs_small, SCAN_BLOCK, 0, st, P);
+      else if (P.multinomial) launch_pdl(k_sys_resample<2, true>, T.rs_grid2, SCAN_BLOCK, sizeof(RsSmem<2>), st, P);
       else launch_pdl(k_sys_resample<2>, T.rs_grid2, SCAN_BLOCK, sizeof(RsSmem<2>), st, P);
     }
     if (P.multinomial) {
@@ -778,6 +780,7 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
     k_sir_stats<<<T.red_grid, 256, 0, st>>>(P);   // its last CTA finalises the frame
     mark("k_sys_resample");
     if (T.rs_small) launch_pdl(k_sys_resample_small<2>, T.rs_small, SCAN_BLOCK, 0, st, P);
+    else if (P.multinomial) launch_pdl(k_sys_resample<2, true>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<2>), st, P);
     else launch_pdl(k_sys_resample<2>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<2>), st, P);
     if (P.multinomial) {
       mark("k_multinomial_emit");
@@ -799,6 +802,10 @@ static int set_attrs() {
   PCS_CUDA_TRY(cudaFuncSetAttribute(k_sys_resample<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)sizeof(RsSmem<1>)));
   PCS_CUDA_TRY(cudaFuncSetAttribute(k_sys_resample<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sizeof(RsSmem<2>)));
+  PCS_CUDA_TRY(cudaFuncSetAttribute(k_sys_resample<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)sizeof(RsSmem<1>)));
+  PCS_CUDA_TRY(cudaFuncSetAttribute(k_sys_resample<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)sizeof(RsSmem<2>)));
   PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)BINS_SMEM));

@@ -1336,7 +1336,10 @@ struct RsSmem {
   unsigned long long bar[2];
 };
 
-template <int KIND>
+// MULTI: multinomial scheme — write the exact cdf per particle instead of
+// emitting slots (k_multinomial_emit draws them); a separate instantiation so
+// the systematic kernel carries none of it
+template <int KIND, bool MULTI = false>
 __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(TrackParams P) {
   typedef typename RsElem<KIND>::T E;
   extern __shared__ __align__(128) unsigned char rs_raw[];
@@ -1486,7 +1489,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
       int jr = 0;
       if (k0 < nv && off + base + k0 != 0) jr = slot_rel(excl, u, ng, nd, kappa, eps, tj0d, tj0);
       u128 run = excl;
-      if (P.multinomial) {   // the exact cdf per particle (filtering.py:94-95)
+      if (MULTI) {   // the exact cdf per particle (filtering.py:94-95)
 #pragma unroll
         for (int q = 0; q < RS_ITEMS; ++q) {
           const int k = k0 + q;
@@ -1497,24 +1500,26 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
         }
       }
       const u32 hp_s = smem_u32(hp + k0), st_s = smem_u32(stage + k0);
+      if (!MULTI) {
 #pragma unroll
-      for (int q = 0; q < (P.multinomial ? 0 : RS_ITEMS); ++q) {
-        const int k = k0 + q;
-        int h = -1;   // no slot
-        if (k < nv) {
-          run += weight(buf, k, nv);
-          const int jend = (k == klast) ? (int)(ng - tj0) : slot_rel(run, u, ng, nd, kappa, eps, tj0d, tj0);
-          if (jend > jr) h = jr;
-          jr = jend;
+        for (int q = 0; q < RS_ITEMS; ++q) {
+          const int k = k0 + q;
+          int h = -1;   // no slot
+          if (k < nv) {
+            run += weight(buf, k, nv);
+            const int jend = (k == klast) ? (int)(ng - tj0) : slot_rel(run, u, ng, nd, kappa, eps, tj0d, tj0);
+            if (jend > jr) h = jr;
+            jr = jend;
+          }
+          sts_u32(hp_s + 4 * q, h);    // (KIND 1: over item k, already read)
+          sts_u32(st_s + 4 * q, -1);   // first chunk's fill
         }
-        sts_u32(hp_s + 4 * q, h);    // (KIND 1: over item k, already read)
-        sts_u32(st_s + 4 * q, -1);   // first chunk's fill
       }
     }
     __syncthreads();   // every read of ring[L & 1] is done; it is free for load L + 2
     // slots in chunks of RS_TILE: heads, block max-scan, coalesced writes
     // (multinomial: k_multinomial_emit draws the slots)
-    const int m_slots = P.multinomial ? 0 : (int)(tj1 - tj0);   // <= ng < 2^31
+    const int m_slots = MULTI ? 0 : (int)(tj1 - tj0);   // <= ng < 2^31
     int carry = -1;
     const u32 stage_s = smem_u32(stage), hp_s = smem_u32(hp + k0);
     for (int c0 = 0; c0 < m_slots; c0 += RS_TILE) {
