@@ -222,6 +222,10 @@ def sharded_pcsir_track(frames, cfg, seed, ops, group=None, slot_slack=2.0, comm
     replicated: every rank evaluates the same occupied cells). ``cfg`` is a
     PcFilterConfig with the GLOBAL n_particles (divisible by the world size).
     """
+    r_cfg = cfg.resampling
+    if r_cfg.threshold_fraction != 1.0 or r_cfg.scheme != "systematic":
+        raise ValueError("the sharded filter resamples every frame (systematic, "
+                         "threshold_fraction=1.0); use pcsir_track on one GPU otherwise")
     p = dist.get_world_size(group)
     r = dist.get_rank(group)
     n_global = cfg.n_particles

@@ -105,3 +105,15 @@ def test_first_slot_matches_points():
     for c in list(rng.random(200)) + [0.0, 1.0, pts[5], pts[999]]:
         j = D.first_slot(float(c), u, n)
         assert j == int(np.searchsorted(pts, c, side="left"))
+
+
+def test_sharded_filter_rejects_other_resampling():
+    import paper_1310_5541_b200 as pc
+    from paper_1310_5541_b200 import distributed as D
+    init = pc.InitSpec(pc.StateVector(8, 8, 0, 0, 20.0), "gauss", sigma=2.0)
+    lik = pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(10.0, 5))
+    for res in (pc.ResampleConfig(0.5, "systematic"), pc.ResampleConfig(1.0, "multinomial")):
+        cfg = pc.PcFilterConfig(64, init, pc.DynamicsParams(0.5, 0.1, 1.0), res, lik,
+                                grid=pc.BinGrid.pixel_aligned(16, 16, 1))
+        with pytest.raises(ValueError, match="resamples every frame"):
+            D.sharded_pcsir_track(torch.zeros((1, 16, 16)), cfg, 0, ops=None)
