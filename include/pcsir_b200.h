@@ -68,6 +68,10 @@ typedef struct pcs_init_t {
 /* ------------------------------------------------------------------ */
 const char* pcs_last_error(void);
 int pcs_version(void);
+/* sizeof of the public structs, in this order: pcs_grid_t, pcs_dynamics_t,
+ * pcs_spot_t, pcs_init_t, pcs_track_cfg_t, pcs_track_result_t (a binding
+ * checks its layouts against them); returns how many were written. */
+int pcs_abi_struct_sizes(int64_t* out, int32_t n);
 int pcs_device_info(int device, int* sm_count, int64_t* l2_bytes, int* cc_major, int* cc_minor);
 
 int pcs_ctx_create(pcs_ctx** out, int device);

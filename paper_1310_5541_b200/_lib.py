@@ -74,6 +74,7 @@ class PcsTrackResult(ctypes.Structure):
 _SIGNATURES = [
     ("pcs_last_error", c_char_p, []),
     ("pcs_version", c_int32, []),
+    ("pcs_abi_struct_sizes", c_int32, [P(c_int64), c_int32]),
     ("pcs_device_info", c_int32, [c_int32, P(c_int32), P(c_int64), P(c_int32), P(c_int32)]),
     ("pcs_ctx_create", c_int32, [P(c_void_p), c_int32]),
     ("pcs_ctx_destroy", c_int32, [c_void_p]),

@@ -228,6 +228,15 @@ extern "C" {
 const char* pcs_last_error(void) { return g_last_error.c_str(); }
 int pcs_version(void) { return 10000; }
 
+int pcs_abi_struct_sizes(int64_t* out, int32_t n) {
+  const int64_t sz[6] = {(int64_t)sizeof(pcs_grid_t),      (int64_t)sizeof(pcs_dynamics_t),
+                         (int64_t)sizeof(pcs_spot_t),      (int64_t)sizeof(pcs_init_t),
+                         (int64_t)sizeof(pcs_track_cfg_t), (int64_t)sizeof(pcs_track_result_t)};
+  int k = 0;
+  for (; out && k < n && k < 6; ++k) out[k] = sz[k];
+  return k;
+}
+
 // ---- scene synthesis (synthesis.py:124-150) ----------------------------------
 int pcs_render_frames(pcs_ctx* ctx, const double* spots, int64_t n_spots, int64_t n_frames,
                       int64_t width, int64_t height, double sigma_psf, double i_bg,

@@ -72,3 +72,13 @@ def test_invalid_arguments_are_rejected(lib_path):
     rc = L.pcs_loglik(None, 1, 1, None, None, None, 1, ctypes.byref(spot), None, None)
     assert rc == _lib.PCS_E_INVALID
     assert "sigma_psf" in _lib.last_error()
+
+
+def test_ctypes_struct_layouts_match_the_library(lib_path):
+    from paper_1310_5541_b200 import _lib
+    L = _lib.load_library()
+    out = (ctypes.c_int64 * 6)()
+    assert L.pcs_abi_struct_sizes(out, 6) == 6
+    mine = [ctypes.sizeof(t) for t in (_lib.PcsGrid, _lib.PcsDynamics, _lib.PcsSpot,
+                                       _lib.PcsInit, _lib.PcsTrackCfg, _lib.PcsTrackResult)]
+    assert list(out) == mine
