@@ -55,6 +55,16 @@ ALGO_BYTES = {  # algorithmic bytes per particle per launch
     "k_mt_frame": 56,
 }
 STEP_BYTES = 60  # canonical fused minimum per particle-update
+# what bounds the dominant kernel, from the committed ncu captures (profiles/)
+LIMITERS = {
+    "k_pc_step1": ("instruction issue and phase barriers: ~18 warp instructions per particle, "
+                   "54-63 % issue active, DRAM traffic ~= the algorithmic bytes "
+                   "(profiles/r1zd_ncu_summary.txt, r1zd_c5s_ncu_summary.txt)"),
+    "k_sys_resample": ("latency of the two passes and the grid barrier (~4 warp instructions "
+                       "per particle, 30-47 % issue active)"),
+    "k_sir_propagate_lik": "FP32/SFU/XU pipes and latency of the per-pixel likelihood",
+    "k_mt_frame": "instruction issue (step-1 machinery per target, two CTAs per SM)",
+}
 
 
 # ---------------------------------------------------------------------------
@@ -469,6 +479,7 @@ def main():
                     "step_frac": STEP_BYTES * n / (step_ms * 1e-3) / 1e9 / peak,
                     "working_set_mb": round(working_set / 1e6, 1),
                     "l2_mb": round(info["l2_bytes"] / 2 ** 20, 1),
+                    "limiter": LIMITERS.get(dom, ""),
                     "note": ("kernel times from a non-graph pass with CUDA events around every "
                              "launch (include ~5 us launch gaps); the headline is graph replay")}
         # e2e: the public call on host frames (H2D + D2H inside the timed region).
@@ -607,7 +618,8 @@ def bench_c4(args, wl, cpp, world, rank, dist, torch, pc, _lib, sampler, max_ove
                    "parallelism": f"targets sharded x{world}, no communication",
                    "l2": "working set larger than L2", "rmse_px": err,
                    "median_err_px": err_median, "lost_target_frac": lost},
-        "roofline": {"bound": "hbm", "kernel": "k_mt_frame", "achieved": achieved, "peak": peak,
+        "roofline": {"bound": "hbm", "kernel": "k_mt_frame", "limiter": LIMITERS["k_mt_frame"],
+                     "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": None,
                      "algo_bytes_per_launch": ALGO_BYTES["k_mt_frame"] * local_particles},
