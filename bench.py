@@ -7,13 +7,20 @@ A "step" is one frame of the filter over all N particles of the workload
 ESS -> exact systematic resampling). Workloads (BASELINE.json configs):
 
   c1  64x64,   N=1e4, pcSIR 1 px (the reference's CPU-scale case)
-  c2  256x256, N=1e6, pcSIR 1 px                    <- default headline
+  c2  256x256, N=1e6, pcSIR 1 px
       (SIR and the 0.25/0.5/2 px grids are reported under "variants")
   c3  512x512, N=1e7, erf-PSF Poisson likelihood 15x15, pcSIR 0.5 px (+ SIR)
   c4  2048x2048, 4096 targets x 1e5 particles, pcSIR 1 px; targets sharded
       across GPUs with no communication
   c5  4096x4096, N=2^30, pcSIR 0.25 px; one filter sharded by particle
       across GPUs (NCCL all-reduce / all-gather / all-to-all); 1 GPU = fused
+                                                    <- default headline: the
+      largest BASELINE.json config that fits one B200 (20 GiB of states)
+
+The default line also carries "likelihood_roofline": the per-particle SIR
+likelihood kernel measured at c3 (erf-PSF Poisson 15x15, N=1e7) and c2
+(Gaussian SSD 11x11, N=1e6) against the FP32 / SFU pipe bound of SURVEY
+§8(d)'s minimal operation counts.
 
   python bench.py [--gpus N --steps K --warmup W --workload c2]
   python bench.py --impl reference [...]     # the reference CPU path, rank 0
@@ -55,6 +62,18 @@ ALGO_BYTES = {  # algorithmic bytes per particle per launch
     "k_mt_frame": 56,
 }
 STEP_BYTES = 60  # canonical fused minimum per particle-update
+L2_BYTES = 132_644_864   # B200 L2 (126.5 MiB): decides the L2 flush, same rule in both arms
+# Minimal likelihood operation counts per evaluation (separable
+# forms): FP32 FLOPs and SFU (MUFU) operations; redundant non-separable
+# arithmetic does not count.
+#   Gaussian SSD S x S: 2S exp (MUFU) + ~4 FLOP each, S amp*gx hoists, 5 S^2
+#   erf-PSF Poisson S x S: 2(S+1) erf edges (~20 FLOP each, no MUFU) + per pixel
+#   one lg2 (MUFU) and ~6 FLOP
+def lik_min_ops(model, hw):
+    S = 2 * hw + 1
+    if model == "gauss":
+        return {"flop": 2 * S * 4 + S + 5 * S * S, "mufu": 2 * S}
+    return {"flop": 2 * (S + 1) * 20 + 6 * S * S, "mufu": S * S}
 # what bounds the dominant kernel, from the committed ncu captures (profiles/)
 LIMITERS = {
     "k_pc_step1": ("instruction issue and phase barriers: ~18 warp instructions per particle, "
@@ -153,6 +172,39 @@ class ClockSampler:
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
                 "samples": len(self.rows)}
+
+
+def bench_config(wl_name, wl, variant, world):
+    """The workload-defining config dict, identical in both arms (results
+    such as RMSE go under "quality", not here)."""
+    cpp = VARIANTS[variant]
+    n = wl["n"]
+    if wl_name == "c4":
+        return {"workload": f"c4:{variant}", "targets": wl["targets"],
+                "n_particles_per_target": n, "frame": f"{wl['width']}x{wl['width']}",
+                "frames": "4096 Gaussian spots (uniform positions, v~N(0,1), I0~U[10,40]), "
+                          "bg 10, Poisson, seed 0",
+                "bin_px": cpp, "likelihood": "gauss-ssd 11x11",
+                "resampling": "systematic every frame (threshold 1.0)",
+                "parallelism": f"targets sharded x{world}, no communication",
+                "l2": "working set larger than L2"}
+    working_set = STEP_BYTES * n
+    lik = (f"{'gauss-ssd' if wl['model'] == 'gauss' else 'erf-poisson'}"
+           f" {2 * wl['hw'] + 1}x{2 * wl['hw'] + 1}")
+    if wl_name == "c5":
+        par = (f"particles sharded x{world} (NCCL all-reduce / all-gather / all-to-all)"
+               if world > 1 else "single GPU (one filter, fused device loop)")
+    else:
+        par = f"replicas x{world}" if world > 1 else "single GPU"
+    return {"workload": f"{wl_name}:{variant}", "n_particles": n,
+            "frame": f"{wl['width']}x{wl['width']}",
+            "frames": "one Gaussian spot (sigma 1.5 px, I0 20, bg 10), +0.5 px/frame, Poisson, "
+                      "seed 0",
+            "bin_px": cpp, "likelihood": lik,
+            "resampling": "systematic every frame (threshold 1.0)",
+            "l2": ("flushed (write > L2) before every timed step" if working_set < 2 * L2_BYTES
+                   else "working set larger than L2"),
+            "parallelism": par}
 
 
 def make_cfg(pc, wl, cpp, n=None, center=None):
@@ -284,6 +336,48 @@ def kernel_profile(torch, pc, _lib, cfg, grid, dev_frames, warmup, frames_n, see
     return {nm: acc[i] / frames_n for i, nm in enumerate(names)}
 
 
+def likelihood_roofline(torch, pc, _lib, info, args, clock_mhz):
+    """FP32 / SFU roofline of the per-particle likelihood kernel
+    (k_sir_propagate_lik, one evaluation per particle): c3's erf-PSF Poisson
+    15x15 at N=1e7 and c2's Gaussian SSD 11x11 at N=1e6, CUDA events around
+    each launch (kernel_profile). Achieved = minimal operation count (SURVEY
+    §8(d), lik_min_ops) x N / kernel time; peaks from the SM count and the SM
+    clock sampled during the timed region: FP32 = SMs x 128 lanes x 2 FLOP x f,
+    SFU = SMs x 16 MUFU x f. The kernel also gathers, draws and propagates (52 B
+    per particle of HBM traffic), which the count leaves out."""
+    f = (clock_mhz or 1965.0) * 1e6
+    sms = info["sm_count"]
+    peak_fp32 = sms * 128 * 2 * f
+    peak_sfu = sms * 16 * f
+    out = {}
+    for wl_name in ("c3", "c2"):
+        wl = dict(WORKLOADS[wl_name])
+        frames_n = 4
+        dev_frames, _, _, _ = scene(wl_name, wl, args.warmup + frames_n, torch)
+        cfg, grid = make_cfg(pc, wl, None)
+        prof = kernel_profile(torch, pc, _lib, cfg, grid, dev_frames, args.warmup, frames_n,
+                              args.seed, None)
+        ms = prof.get("k_sir_propagate_lik")
+        ops = lik_min_ops(wl["model"], wl["hw"])
+        n = wl["n"]
+        t = ms * 1e-3
+        flop_s, mufu_s = ops["flop"] * n / t, ops["mufu"] * n / t
+        t_bound = max(ops["flop"] * n / peak_fp32, ops["mufu"] * n / peak_sfu)
+        out[f"{wl_name}:SIR"] = {
+            "bound": "fp32/sfu", "kernel": "k_sir_propagate_lik", "kernel_ms": round(ms, 5),
+            "likelihood": ("erf-poisson 15x15" if wl["model"] != "gauss" else "gauss-ssd 11x11"),
+            "n_evals": n, "min_flop_per_eval": ops["flop"], "min_mufu_per_eval": ops["mufu"],
+            "achieved_tflops": flop_s / 1e12, "peak_fp32_tflops": peak_fp32 / 1e12,
+            "fp32_frac": flop_s / peak_fp32,
+            "achieved_mufu_per_s": mufu_s, "peak_mufu_per_s": peak_sfu, "sfu_frac": mufu_s / peak_sfu,
+            "frac": t_bound / t, "limiter": "sfu" if ops["mufu"] / peak_sfu >= ops["flop"] / peak_fp32
+            else "fp32",
+            "clock_mhz": f / 1e6, "peak_kind": "SMs x lanes x clock (sampled)"}
+        del dev_frames
+        torch.cuda.empty_cache()
+    return out
+
+
 # ---------------------------------------------------------------------------
 # CPU reference path (oracle port of the reference driver + the reference's
 # compiled likelihood kernel when oracle/_ref holds it)
@@ -338,6 +432,12 @@ def cpu_sample(wl_name, wl, frames_host, cpp, pool_cores=1):
                                   f"process pool of {pool_cores} ({out[0][2]}), {dt:.1f} s")
 
 
+def scaling_of(wl_name):
+    """c4 / c5 fix the total work (targets / particles) as GPUs are added;
+    c1-c3 run one filter per GPU (replicas)."""
+    return "strong" if wl_name in ("c4", "c5") else "weak"
+
+
 def reference_arm(args, wl_name, wl, cpp):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
@@ -364,10 +464,10 @@ def reference_arm(args, wl_name, wl, cpp):
         "impl": "reference", "metric": "particle-updates/sec per filter step",
         "value": v, "unit": "particle-updates/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": wl.get("targets", 1) * wl["n"] / v * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": scaling_of(wl_name), "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": f"{wl_name}:{args.variant or wl['variant']}",
-                   "n_particles": wl["n"], "frame": f"{wl['width']}x{wl['width']}"},
+        "config": bench_config(wl_name, wl, args.variant or wl["variant"], args.gpus),
         "cpu_baseline": {"value": v, "unit": "particle-updates/s", "cores": used, "kind": "port",
                          "sample": sample},
         "e2e": {"value": v, "unit": "particle-updates/s", "h2d_bytes_per_step": 0,
@@ -384,7 +484,7 @@ def main():
     ap.add_argument("--steps", type=int, default=None)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c5", choices=sorted(WORKLOADS))
     ap.add_argument("--variant", default=None, choices=sorted(VARIANTS))
     ap.add_argument("--targets", type=int, default=None, help="c4: number of targets")
     ap.add_argument("--n", type=int, default=None, help="override particles (per target for c4)")
@@ -520,6 +620,12 @@ def main():
                 variants[name] = {"value": n * vsteps * world / (vt * 1e-3),
                                   "ms_per_step": vt / vsteps,
                                   "mean_occupied_bins": float(np.mean(vout["occ"][args.warmup:]))}
+        lik_roof = None
+        if wl_name == "c5" and not args.no_variants:
+            del dev_frames
+            torch.cuda.empty_cache()
+            lik_roof = likelihood_roofline(torch, pc, _lib, info, args,
+                                           (out["clocks"] or {}).get("sm_mhz"))
         cpu = None
         if rank == 0 and world == 1 and not args.no_cpu_baseline:
             v, used, sample = cpu_sample(wl_name, wl, frames_host, cpp_main)
@@ -529,19 +635,13 @@ def main():
             "metric": "particle-updates/sec per filter step", "value": value,
             "unit": "particle-updates/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{wl_name}:{variant}", "n_particles": n,
-                       "frame": f"{wl['width']}x{wl['width']}", "frames": frames_src,
-                       "bin_px": cpp_main,
-                       "likelihood": (f"{'gauss-ssd' if wl['model'] == 'gauss' else 'erf-poisson'}"
-                                      f" {2 * wl['hw'] + 1}x{2 * wl['hw'] + 1}"),
-                       "resampling": "systematic every frame (threshold 1.0)",
-                       "l2": ("flushed (write > L2) before every timed step" if flush is not None
-                              else "working set larger than L2"),
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
-                       "rmse_px": rmse,
-                       "mean_occupied_bins": float(np.mean(out["occ"][args.warmup:]))},
-            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "scaling": scaling_of(wl_name), "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": bench_config(wl_name, wl, variant, world),
+            "quality": {"rmse_px": rmse, "frames_source": frames_src,
+                        "mean_occupied_bins": float(np.mean(out["occ"][args.warmup:]))},
+            "roofline": roofline, "likelihood_roofline": lik_roof, "cpu_baseline": cpu,
+            "e2e": e2e,
             "gpu_launches": out["launches"] * args.steps,
             "clocks": out["clocks"], "variants": variants, "flags": out["flags"],
         }
@@ -612,12 +712,8 @@ def bench_c4(args, wl, cpp, world, rank, dist, torch, pc, _lib, sampler, max_ove
         "unit": "particle-updates/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": step_ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"c4:{args.variant or wl['variant']}", "targets": T,
-                   "n_particles_per_target": n, "frame": f"{wl['width']}x{wl['width']}",
-                   "frames": "GPU Poisson synthesis (pcs_render_frames), seed 0",
-                   "parallelism": f"targets sharded x{world}, no communication",
-                   "l2": "working set larger than L2", "rmse_px": err,
-                   "median_err_px": err_median, "lost_target_frac": lost},
+        "config": bench_config("c4", wl, args.variant or wl["variant"], world),
+        "quality": {"rmse_px": err, "median_err_px": err_median, "lost_target_frac": lost},
         "roofline": {"bound": "hbm", "kernel": "k_mt_frame", "limiter": LIMITERS["k_mt_frame"],
                      "achieved": achieved, "peak": peak,
                      "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
@@ -674,12 +770,9 @@ def bench_c5_sharded(args, wl, cpp, world, rank, dist, torch, pc, _lib, sampler,
         "warmup": args.warmup, "ms_per_step": elapsed / args.steps * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": f"c5:{args.variant or wl['variant']}", "n_particles": n,
-                   "frame": f"{wl['width']}x{wl['width']}",
-                   "parallelism": f"particles sharded x{world} (NCCL all-reduce/all-gather/"
-                                  f"all-to-all)", "l2": "working set larger than L2",
-                   "timing": "host wall clock between barriers (the protocol synchronises "
-                             "the host every frame)"},
+        "config": bench_config("c5", wl, args.variant or wl["variant"], world),
+        "timing": "host wall clock between barriers (the protocol synchronises the host every "
+                  "frame)",
         "roofline": None, "cpu_baseline": None,
         "e2e": {"value": value, "unit": "particle-updates/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 57},

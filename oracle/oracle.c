@@ -195,11 +195,41 @@ double orc_u128_to_double(uint64_t lo, uint64_t hi) {
 
 /* ------------------------------------------------------------------ */
 /* propagate_array (state.py:115-127) on float32 states with given     */
-/* float32 normals: float64 arithmetic in numpy's order, rounded to     */
-/* float32. s, z, out: SoA [5][n].                                      */
+/* float32 normals, in the device's CANONICAL float32 form (pcs_state.cuh */
+/* propagate_one): each parameter p split as hi = RN32(p), lo =          */
+/* RN32(p - hi); mul_add(a, p, b) = fma(a, hi, fma(a, lo, b));           */
+/*   x' = mul_add(z0, sp, mul_add(vx, dt, x)); vx' = mul_add(z2, sv, vx);*/
+/*   I0' = max(mul_add(z4, si, I0), 0)                                  */
+/* s, z, out: SoA [5][n]. (The reference's float64 sums, state.py:123-126,*/
+/* agree to ~1 float32 ulp; orc_propagate_f64 below is numpy's order.)  */
 /* ------------------------------------------------------------------ */
+typedef struct { float hi, lo; } split32;
+static split32 split_param(double p) {
+  split32 s;
+  s.hi = (float)p;
+  s.lo = (float)(p - (double)s.hi);
+  return s;
+}
+static float mul_add(float a, split32 p, float b) { return fmaf(a, p.hi, fmaf(a, p.lo, b)); }
+
 void orc_propagate(const float* s, const float* z, int64_t n, double sp, double sv, double si,
                    double dt, float* out) {
+  const split32 P = split_param(sp), V = split_param(sv), I = split_param(si), T = split_param(dt);
+  for (int64_t i = 0; i < n; ++i) {
+    float x = s[i], y = s[n + i], vx = s[2 * n + i], vy = s[3 * n + i], i0 = s[4 * n + i];
+    out[i] = mul_add(z[i], P, mul_add(vx, T, x));
+    out[n + i] = mul_add(z[n + i], P, mul_add(vy, T, y));
+    out[2 * n + i] = mul_add(z[2 * n + i], V, vx);
+    out[3 * n + i] = mul_add(z[3 * n + i], V, vy);
+    float iv = mul_add(z[4 * n + i], I, i0);
+    out[4 * n + i] = (iv > 0.0f) ? iv : ((iv == iv) ? 0.0f : iv);
+  }
+}
+
+/* numpy's float64 order on the upcast float32 values, rounded once to   */
+/* float32 (what the reference's propagate_array gives on these inputs) */
+void orc_propagate_f64(const float* s, const float* z, int64_t n, double sp, double sv, double si,
+                       double dt, float* out) {
   for (int64_t i = 0; i < n; ++i) {
     double x = s[i], y = s[n + i], vx = s[2 * n + i], vy = s[3 * n + i], i0 = s[4 * n + i];
     double x1 = x + vx * dt;

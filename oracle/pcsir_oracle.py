@@ -64,6 +64,7 @@ def lib():
             "orc_fixed_f32": (None, [dp, i64, ctypes.c_int, dp]),
             "orc_u128_to_double": (d, [u64, u64]),
             "orc_propagate": (None, [dp, dp, i64, d, d, d, d, dp]),
+            "orc_propagate_f64": (None, [dp, dp, i64, d, d, d, d, dp]),
             "orc_spot_window_ssd": (None, [dp, i64, i64, dp, dp, dp, i64, d, d, i64, dp]),
             "orc_poisson_loglik": (None, [dp, i64, i64, dp, dp, dp, i64, d, d, i64, ctypes.c_int, dp]),
             "orc_cdf_exact": (None, [dp, i64, dp]),
@@ -406,12 +407,24 @@ def estimate_ess_exact(soa32, w32):
 
 
 def propagate_f32(soa32, z32, sigma_pos, sigma_vel, sigma_int, dt):
-    """state.py:115-127 on float32 inputs with float32 normals, float64
-    arithmetic in numpy's order, rounded to float32 (bit-exact target)."""
+    """state.py:115-127 in the device's canonical float32 form (one rounding
+    per fused multiply-add, float32 parameters; oracle.c orc_propagate) —
+    the bit-exact target of the device propagation."""
     s = _c(soa32, np.float32)
     z = _c(z32, np.float32)
     out = np.empty_like(s)
     lib().orc_propagate(_p(s), _p(z), s.shape[1], sigma_pos, sigma_vel, sigma_int, dt, _p(out))
+    return out
+
+
+def propagate_f64_order(soa32, z32, sigma_pos, sigma_vel, sigma_int, dt):
+    """state.py:115-127 on the upcast float32 inputs in numpy's float64
+    order, rounded once to float32 (the reference's values on these inputs)."""
+    s = _c(soa32, np.float32)
+    z = _c(z32, np.float32)
+    out = np.empty_like(s)
+    lib().orc_propagate_f64(_p(s), _p(z), s.shape[1], sigma_pos, sigma_vel, sigma_int, dt,
+                            _p(out))
     return out
 
 

@@ -121,6 +121,7 @@ _SIGNATURES = [
     ("pcs_track_kernel_name", c_char_p, [c_void_p, c_int32]),
     ("pcs_track_launches_per_step", c_int32, [c_void_p]),
     ("pcs_track_debug", c_int32, [c_void_p, c_void_p, c_void_p]),
+    ("pcs_track_info", c_int32, [c_void_p, c_void_p, c_int32, c_void_p]),
     ("pcs_track_states", c_int32, [c_void_p, P(c_void_p), P(c_int64)]),
     ("pcs_mt_begin", c_int32, [c_void_p, P(PcsTrackCfg), c_int64, c_void_p, c_int64, c_int64,
                                c_int64, c_int64, c_void_p]),
@@ -237,6 +238,18 @@ def device_info(index=0):
     check(lib().pcs_device_info(index, ctypes.byref(sm), ctypes.byref(l2), ctypes.byref(ma),
                                 ctypes.byref(mi)), "pcs_device_info")
     return {"sm_count": sm.value, "l2_bytes": l2.value, "cc": (ma.value, mi.value)}
+
+
+TRACK_INFO_KEYS = ("s1_ctas", "s1_tile", "s1_tiles_per_cta", "rs_ctas", "rs_tiles_per_cta",
+                   "sir_chunk", "s1_mid_flushes", "max_occupied", "bins_smem_cells",
+                   "s1_flush_tiles", "sir_ctas", "launches_per_frame")
+
+
+def track_info():
+    """pcs_track_info of the context's current / last fused track as a dict."""
+    buf = (ctypes.c_int64 * 16)()
+    check(lib().pcs_track_info(ctx(), buf, 16, stream()), "pcs_track_info")
+    return {k: int(buf[i]) for i, k in enumerate(TRACK_INFO_KEYS)}
 
 
 def loaded_library_path():

@@ -247,7 +247,9 @@ def pcsir_track(frames, cfg: PcFilterConfig, rng, fused=None) -> TrackResult:
     """
     prng = as_philox(rng)
     if fused is None:
-        fused = _fused_ok(cfg) and not cfg.weighted_com
+        fused = _fused_ok(cfg)
+    if cfg.weighted_com:
+        fused = False   # weighted centre of mass (binning.py:160-165) runs the general path
     if fused:
         start = (prng.seed, prng.frame)
         try:

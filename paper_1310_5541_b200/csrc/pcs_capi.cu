@@ -391,12 +391,12 @@ int pcs_propagate(const float* sin, float* sout, int64_t ld, int64_t n, const in
   PCS_CHECK_ARG(dyn->sigma_pos >= 0 && dyn->sigma_vel >= 0 && dyn->sigma_int >= 0,
                 "noise magnitudes must be >= 0");
   PCS_CHECK_ARG(dyn->dt > 0, "dt must be > 0");
-  Dyn d{dyn->sigma_pos, dyn->sigma_vel, dyn->sigma_int, dyn->dt};
+  Dyn d = make_dyn(dyn->sigma_pos, dyn->sigma_vel, dyn->sigma_int, dyn->dt);
   int g = grid_for(n, 256, 148);
   if (anc)
-    k_propagate<true><<<g, 256, 0, S(stream)>>>(sin, sout, ld, n, anc, d, seed, frame, off);
+    k_propagate<true><<<g, 256, 0, S(stream)>>>(sin, sout, ld, n, anc, d, philox_key(seed), frame, off);
   else
-    k_propagate<false><<<g, 256, 0, S(stream)>>>(sin, sout, ld, n, nullptr, d, seed, frame, off);
+    k_propagate<false><<<g, 256, 0, S(stream)>>>(sin, sout, ld, n, nullptr, d, philox_key(seed), frame, off);
   PCS_LAUNCH_CHECK();
   return PCS_OK;
 }
@@ -406,7 +406,7 @@ int pcs_propagate_given(const float* sin, float* sout, int64_t ld, int64_t n, co
                         void* stream) {
   PCS_CHECK_ARG(sin && sout && dyn && normals && n >= 1 && ld >= n && ldz >= n, "bad arguments");
   PCS_CHECK_ARG(sin != sout, "in-place propagate is not supported");
-  Dyn d{dyn->sigma_pos, dyn->sigma_vel, dyn->sigma_int, dyn->dt};
+  Dyn d = make_dyn(dyn->sigma_pos, dyn->sigma_vel, dyn->sigma_int, dyn->dt);
   k_propagate_given<<<grid_for(n, 256, 148), 256, 0, S(stream)>>>(sin, sout, ld, n, anc, d,
                                                                    normals, ldz);
   PCS_LAUNCH_CHECK();
@@ -696,8 +696,9 @@ __global__ void k_ctl_init(TrackCtl* C, double cx, double cy) {
   C->center[1] = cy;
 }
 
-__global__ void k_ctl_io(TrackCtl* C, const float* frames, i64 kf, i64 ko, double* est,
+__global__ void k_ctl_io(TrackCtl* C, const float* frames, i64 kf, i64 ko, i64 kend, double* est,
                          double* ess, unsigned char* res, i64* occ, int fmap_ok = 0) {
+  C->k_end = kend;
   C->fmap_ok = fmap_ok;
   C->frames = frames;
   C->k_frames = kf;
@@ -873,12 +874,13 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   P.ld = ld;
   P.H = H;
   P.W = W;
-  P.dyn = Dyn{cfg->dyn.sigma_pos, cfg->dyn.sigma_vel, cfg->dyn.sigma_int, cfg->dyn.dt};
+  P.dyn = make_dyn(cfg->dyn.sigma_pos, cfg->dyn.sigma_vel, cfg->dyn.sigma_int, cfg->dyn.dt);
   P.spot = to_spot(&cfg->spot);
   P.grid = cfg->method == 1 ? to_grid(&cfg->grid) : Grid{0, 0, 1, 1, 1, 1};
   P.inv_lx = 1.0 / P.grid.lx;
   P.inv_ly = 1.0 / P.grid.ly;
   P.seed = cfg->seed;
+  P.pk = philox_key(cfg->seed);
   P.frame0 = cfg->frame0;
   P.placement = cfg->placement;
   P.idx_off = 0;
@@ -1083,7 +1085,7 @@ int pcs_track_steps(pcs_ctx* ctx, const float* frames, int64_t k0, int64_t k1, d
   cudaStream_t st = S(stream);
   TrackState& T = ctx->tr;
   const int fm = frame_map(T, frames, k1 - k0, st);
-  k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frames, k0, k0, est, ess, res, (i64*)occ, fm);
+  k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frames, k0, k0, k1, est, ess, res, (i64*)occ, fm);
   PCS_LAUNCH_CHECK();
   for (i64 k = k0; k < k1; ++k) {
     if (T.exec) {
@@ -1107,7 +1109,7 @@ int pcs_track_steps_timed(pcs_ctx* ctx, const float* frames, int64_t k0, int64_t
   cudaStream_t st = S(stream);
   TrackState& T = ctx->tr;
   const int fm = frame_map(T, frames, k1 - k0, st);
-  k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frames, k0, k0, est, ess, res, (i64*)occ, fm);
+  k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frames, k0, k0, k1, est, ess, res, (i64*)occ, fm);
   PCS_LAUNCH_CHECK();
   const int NE = TrackState::MAX_LAUNCHES + 1;
   cudaEvent_t evs[NE];
@@ -1207,7 +1209,7 @@ int pcs_mt_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t n_targets,
   P.ld = ld;
   P.H = H;
   P.W = W;
-  P.dyn = Dyn{cfg->dyn.sigma_pos, cfg->dyn.sigma_vel, cfg->dyn.sigma_int, cfg->dyn.dt};
+  P.dyn = make_dyn(cfg->dyn.sigma_pos, cfg->dyn.sigma_vel, cfg->dyn.sigma_int, cfg->dyn.dt);
   P.spot = to_spot(&cfg->spot);
   P.grid = to_grid(&cfg->grid);
   P.inv_lx = 1.0 / P.grid.lx;
@@ -1326,7 +1328,7 @@ int pcs_shard_step1(pcs_ctx* ctx, const float* frame, int64_t k, double* est, do
   TrackState& T = ctx->tr;
   i64* dbox;
   PCS_SCRATCH(SL_SHARD_BOX, 8 * sizeof(i64), dbox);
-  k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frame, k, k, est, ess, res, (i64*)occ);
+  k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frame, k, k, k + 1, est, ess, res, (i64*)occ);
   k_pc_step1<<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(T.P);
   k_shard_bbox<<<1, 1024, 0, st>>>(T.P, dbox);
   PCS_LAUNCH_CHECK();
@@ -1449,6 +1451,31 @@ int pcs_track_debug(pcs_ctx* ctx, int64_t* out16, void* stream) {
   PCS_CUDA_TRY(cudaMemcpyAsync(&h, ctx->tr.P.ctl, sizeof(h), cudaMemcpyDeviceToHost, st));
   PCS_CUDA_TRY(cudaStreamSynchronize(st));
   for (int i = 0; i < 16; ++i) out16[i] = h.dbg[i];
+  return PCS_OK;
+}
+
+int pcs_track_info(pcs_ctx* ctx, int64_t* out, int32_t n, void* stream) {
+  PCS_CHECK_ARG(ctx && out && n >= 12, "bad arguments");
+  PCS_CHECK_ARG(ctx->tr.P.ctl, "no track has been started");
+  const TrackState& T = ctx->tr;
+  const TrackParams& P = T.P;
+  cudaStream_t st = S(stream);
+  TrackCtl h;
+  PCS_CUDA_TRY(cudaMemcpyAsync(&h, P.ctl, sizeof(h), cudaMemcpyDeviceToHost, st));
+  PCS_CUDA_TRY(cudaStreamSynchronize(st));
+  for (int i = 0; i < n; ++i) out[i] = 0;
+  out[0] = T.s1_grid;
+  out[1] = P.s1_tile;
+  out[2] = (T.s1_grid > 0 && P.s1_tile > 0) ? ceil_div(ceil_div(P.n, (i64)P.s1_tile), (i64)T.s1_grid) : 0;
+  out[3] = T.rs_small ? T.rs_small : T.rs_grid;
+  out[4] = T.rs_small ? 1 : (T.rs_grid > 0 ? ceil_div(ceil_div(P.n, (i64)RS_TILE), (i64)T.rs_grid) : 0);
+  out[5] = P.sir_chunk;
+  out[6] = h.s1_mid_flush;
+  out[7] = h.max_occ;
+  out[8] = BINS_SM;
+  out[9] = S1_FLUSH_TILES;
+  out[10] = T.prop_grid;
+  out[11] = T.launches;
   return PCS_OK;
 }
 

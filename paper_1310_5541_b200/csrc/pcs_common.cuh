@@ -261,6 +261,39 @@ __host__ __device__ __forceinline__ u32x4 philox4x32_10(u32x4 c, u32 k0, u32 k1)
   return c;
 }
 
+// Round keys of a seed, (k0 + r W0, k1 + r W1) for r = 0..9. Kernels that
+// take a PhiloxKey as a launch parameter read the keys as constant-bank
+// operands of the xor (no per-thread key schedule); same stream as
+// philox4x32_10(c, (u32)seed, (u32)(seed >> 32)).
+struct PhiloxKey {
+  u32 a[10], b[10];
+};
+__host__ __device__ __forceinline__ PhiloxKey philox_key(u64 seed) {
+  PhiloxKey K;
+  u32 k0 = (u32)seed, k1 = (u32)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    K.a[r] = k0;
+    K.b[r] = k1;
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return K;
+}
+__device__ __forceinline__ u32x4 philox4x32_10k(u32x4 c, const PhiloxKey& K) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const u64 p0 = (u64)0xD2511F53u * c.x;   // one IMAD.WIDE.U32 each
+    const u64 p1 = (u64)0xCD9E8D57u * c.z;
+    u32x4 n;
+    n.x = (u32)(p1 >> 32) ^ c.y ^ K.a[r];
+    n.y = (u32)p1;
+    n.z = (u32)(p0 >> 32) ^ c.w ^ K.b[r];
+    n.w = (u32)p0;
+    c = n;
+  }
+  return c;
+}
+
 // Stream tags (counter word w) — one per consumer so streams never overlap.
 enum : u32 {
   TAG_PROPAGATE = 0x1u,
@@ -329,9 +362,7 @@ __device__ __forceinline__ float bm_angle20(u32 b) {
 //   pair 2: u1 = (x & 0x3FF) << 12 | (y & 0xFFF),
 //           u2 = (z & 0x3FF) << 10 | (w >> 2 & 0x3FF) -> z4 (cosine branch)
 // Exposed through pcs_philox_normals for replay; oracle/oracle.c restates it.
-__device__ __forceinline__ void philox_normals5(u64 seed, u32 frame, u64 idx, float z[5]) {
-  u32 k0 = (u32)seed, k1 = (u32)(seed >> 32);
-  u32x4 r = philox4x32_10({(u32)idx, (u32)(idx >> 32), frame, (TAG_PROPAGATE << 4) | 0u}, k0, k1);
+__device__ __forceinline__ void normals5_from_bits(const u32x4& r, float z[5]) {
   float s, c, rad;
   rad = bm_radius22(r.x >> 10);
   __sincosf(bm_angle20(r.y >> 12), &s, &c);
@@ -343,6 +374,16 @@ __device__ __forceinline__ void philox_normals5(u64 seed, u32 frame, u64 idx, fl
   z[3] = rad * s;
   rad = bm_radius22(((r.x & 0x3FFu) << 12) | (r.y & 0xFFFu));
   z[4] = rad * __cosf(bm_angle20(((r.z & 0x3FFu) << 10) | ((r.w >> 2) & 0x3FFu)));
+}
+__device__ __forceinline__ void philox_normals5(u64 seed, u32 frame, u64 idx, float z[5]) {
+  u32 k0 = (u32)seed, k1 = (u32)(seed >> 32);
+  u32x4 r = philox4x32_10({(u32)idx, (u32)(idx >> 32), frame, (TAG_PROPAGATE << 4) | 0u}, k0, k1);
+  normals5_from_bits(r, z);
+}
+// same normals, round keys from a launch parameter
+__device__ __forceinline__ void philox_normals5k(const PhiloxKey& K, u32 frame, u64 idx, float z[5]) {
+  u32x4 r = philox4x32_10k({(u32)idx, (u32)(idx >> 32), frame, (TAG_PROPAGATE << 4) | 0u}, K);
+  normals5_from_bits(r, z);
 }
 
 // Two standard normals for the initial cloud (InitSpec "gauss", state.py:173)

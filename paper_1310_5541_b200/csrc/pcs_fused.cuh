@@ -106,6 +106,9 @@ struct TrackCtl {
   int pc_prior;              // pcSIR: THIS frame has prior weights (copied from
                              // prior_nonuniform by k_pc_step1 at the frame start)
   i64 frame_occ;             // pcSIR with prior weights: occupied cells of the frame
+  i64 k_end;                 // frame index one past the last output row of this batch
+  u32 s1_mid_flush;          // diagnostics: step-1 mid-loop digit flushes (pcs_track_info)
+  u32 max_occ;               // diagnostics: most occupied cells of a frame
 };
 
 struct TrackParams {
@@ -116,6 +119,7 @@ struct TrackParams {
   Grid grid;
   double inv_lx, inv_ly;
   u64 seed;
+  PhiloxKey pk;              // round keys of seed (constant-bank operands)
   u32 frame0;
   int placement;
   float* buf0;
@@ -501,7 +505,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
       float s[5], z[5];
 #pragma unroll
       for (int c = 0; c < 5; ++c) s[c] = o_k[it][c];
-      philox_normals5(P.seed, frame, (u64)(P.idx_off + j), z);
+      philox_normals5k(P.pk, frame, (u64)(P.idx_off + j), z);
       float* o = o_k[it];
       propagate_one(s, z, P.dyn, o);
 #pragma unroll
@@ -592,6 +596,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
     // the next pay write is two barriers away)
     if (++since == S1_FLUSH_TILES) {
       since = 0;
+      if (t == 0) atomicAdd(&C->s1_mid_flush, 1u);
       __syncthreads();
       s1_flush(P, C, sm, sx0, sy0, snxi);
       __syncthreads();
@@ -733,11 +738,16 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   const int t = threadIdx.x;
   const i64 k = C->k;
   const u32 nocc = C->n_occ;
+  if (t == 0) atomicMax(&C->max_occ, nocc);
   if ((C->flags & PCS_FLAG_CAPACITY) || nocc > (u32)BINS_MAXM) {
     if (t == 0) {
       set_flag(C, PCS_FLAG_CAPACITY);
       C->do_resample = 0;
-      C->out_occ[k - C->k_out] = -1;
+      // no per-particle finish of this frame: the prior-weight kernels
+      // (k_pc_prior_ll, k_sir_sum, k_sir_stats) must not finalise it again
+      C->pc_prior = 0;
+      C->prior_nonuniform = 0;
+      if (k < C->k_end) C->out_occ[k - C->k_out] = -1;
       reset_frame(C);
       C->k = k + 1;
     }
@@ -972,14 +982,19 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     const bool flag_bad = degenerate || bad_m;
     if (degenerate) set_flag(C, PCS_FLAG_DEGENERATE);
     if (bad_m) set_flag(C, PCS_FLAG_NONFINITE);
-    for (int c = 0; c < 5; ++c) out_est[ko * 5 + c] = est[c];
-    out_ess[ko] = ess;
+    const bool row = k < C->k_end;   // (an output row exists for this frame)
+    if (row) {
+      for (int c = 0; c < 5; ++c) out_est[ko * 5 + c] = est[c];
+      out_ess[ko] = ess;
+    }
     const int res = (!flag_bad && ess < P.thresh) ? 1 : 0;   // filtering.py:169-170
     // no resampling with unequal weights -> the next frame starts from these
     // per-cell weights (k_sys_resample<1> writes them per particle)
     C->prior_nonuniform = (!res && !flag_bad && s_wmin != s_wmax) ? 1 : 0;
-    out_res[ko] = (unsigned char)res;
-    out_occ[ko] = M;
+    if (row) {
+      out_res[ko] = (unsigned char)res;
+      out_occ[ko] = M;
+    }
     C->evals = evals + M;
     C->do_resample = res;
     C->m = m;

@@ -8,9 +8,26 @@
 
 namespace pcs {
 
+// propagation parameters as float32 pairs hi + lo (hi = RN32(p), lo =
+// RN32(p - hi)): the products z * p keep ~48 bits of p, so the float32
+// propagation tracks the reference's float64 one to the final rounding even
+// for parameters such as 0.1 that float32 cannot hold
 struct Dyn {
-  double sp, sv, si, dt;
+  float sp, sv, si, dt;          // hi parts
+  float sp_lo, sv_lo, si_lo, dt_lo;
 };
+__host__ __forceinline__ Dyn make_dyn(double sp, double sv, double si, double dt) {
+  Dyn d;
+  d.sp = (float)sp;
+  d.sv = (float)sv;
+  d.si = (float)si;
+  d.dt = (float)dt;
+  d.sp_lo = (float)(sp - (double)d.sp);
+  d.sv_lo = (float)(sv - (double)d.sv);
+  d.si_lo = (float)(si - (double)d.si);
+  d.dt_lo = (float)(dt - (double)d.dt);
+  return d;
+}
 
 // ---- replay: the exact normals pcs_propagate consumes ----------------------
 __global__ void k_philox_normals(u64 seed, u32 frame, i64 off, i64 n, float* __restrict__ out,
@@ -80,36 +97,39 @@ __global__ void k_init(InitSpecDev spec, u64 seed, i64 off, i64 n, float* __rest
 }
 
 // ---- propagate (state.py:115-127), CANONICAL arithmetic --------------------
-//   x'  = RN32( RN( RN(x + RN(vx*dt)) + RN(z0*sp) ) )
-//   vx' = RN32( RN(vx + RN(z2*sv)) )
-//   I0' = max( RN32( RN(I0 + RN(z4*si)) ), 0 )
-// evaluated in float64 on the float32 inputs with FMA contraction disabled,
-// exactly the operation sequence numpy performs on the upcast values.
+// float32 fused multiply-adds, each parameter p split as hi + lo (Dyn):
+//   mul_add(a, p, b) = fma(a, p.hi, fma(a, p.lo, b))
+//   x'  = mul_add(z0, sp, mul_add(vx, dt, x))     (old velocity, state.py:123-125)
+//   vx' = mul_add(z2, sv, vx)
+//   I0' = max(mul_add(z4, si, I0), 0)             (state.py:126; NaN propagates)
+// The reference evaluates the same sums in float64 on float64 states; on
+// the same float32 inputs the two agree to ~1 float32 ulp of the result
+// (tests/test_gpu_stages.py). oracle.c orc_propagate restates this form
+// bit-for-bit.
+__device__ __forceinline__ float mul_add_split(float a, float hi, float lo, float b) {
+  return __fmaf_rn(a, hi, __fmaf_rn(a, lo, b));
+}
 __device__ __forceinline__ void propagate_one(const float in[5], const float z[5], const Dyn& d,
                                               float out[5]) {
-  double x = (double)in[0], y = (double)in[1], vx = (double)in[2], vy = (double)in[3],
-         i0 = (double)in[4];
-  double x1 = __dadd_rn(x, __dmul_rn(vx, d.dt));
-  double y1 = __dadd_rn(y, __dmul_rn(vy, d.dt));
-  out[0] = __double2float_rn(__dadd_rn(x1, __dmul_rn((double)z[0], d.sp)));
-  out[1] = __double2float_rn(__dadd_rn(y1, __dmul_rn((double)z[1], d.sp)));
-  out[2] = __double2float_rn(__dadd_rn(vx, __dmul_rn((double)z[2], d.sv)));
-  out[3] = __double2float_rn(__dadd_rn(vy, __dmul_rn((double)z[3], d.sv)));
-  float iv = __double2float_rn(__dadd_rn(i0, __dmul_rn((double)z[4], d.si)));
+  out[0] = mul_add_split(z[0], d.sp, d.sp_lo, mul_add_split(in[2], d.dt, d.dt_lo, in[0]));
+  out[1] = mul_add_split(z[1], d.sp, d.sp_lo, mul_add_split(in[3], d.dt, d.dt_lo, in[1]));
+  out[2] = mul_add_split(z[2], d.sv, d.sv_lo, in[2]);
+  out[3] = mul_add_split(z[3], d.sv, d.sv_lo, in[3]);
+  const float iv = mul_add_split(z[4], d.si, d.si_lo, in[4]);
   out[4] = (iv > 0.0f) ? iv : ((iv == iv) ? 0.0f : iv);   // np.maximum(., 0) (NaN propagates)
 }
 
 template <bool GATHER>
 __global__ void __launch_bounds__(256) k_propagate(const float* __restrict__ sin,
                                                    float* __restrict__ sout, i64 ld, i64 n,
-                                                   const int* __restrict__ anc, Dyn dyn, u64 seed,
-                                                   u32 frame, i64 off) {
+                                                   const int* __restrict__ anc, Dyn dyn,
+                                                   PhiloxKey pk, u32 frame, i64 off) {
   for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
     i64 src = GATHER ? (i64)__ldg(anc + i) : i;
     float s[5], z[5], o[5];
 #pragma unroll
     for (int c = 0; c < 5; ++c) s[c] = __ldg(sin + c * ld + src);
-    philox_normals5(seed, frame, (u64)(off + i), z);
+    philox_normals5k(pk, frame, (u64)(off + i), z);
     propagate_one(s, z, dyn, o);
 #pragma unroll
     for (int c = 0; c < 5; ++c) sout[c * ld + i] = o[c];

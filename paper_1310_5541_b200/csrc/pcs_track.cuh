@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
     float s[5], z[5], o[5];
 #pragma unroll
     for (int c = 0; c < 5; ++c) s[c] = __ldg(sin + c * ld + src);
-    philox_normals5(P.seed, P.frame0 + (u32)k, (u64)(P.idx_off + j), z);
+    philox_normals5k(P.pk, P.frame0 + (u32)k, (u64)(P.idx_off + j), z);
     propagate_one(s, z, P.dyn, o);
 #pragma unroll
     for (int c = 0; c < 5; ++c) sout[c * ld + j] = o[c];
@@ -125,7 +125,7 @@ __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
 // kernels below then normalise, estimate and resample per particle.
 __global__ void __launch_bounds__(256) k_pc_prior_ll(TrackParams P) {
   TrackCtl* C = P.ctl;
-  if (!C->pc_prior) return;
+  if (!C->pc_prior || (C->flags & PCS_FLAG_CAPACITY)) return;
   long long lmax = LLONG_MIN;
   bool bad = false;
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < P.n; j += (i64)gridDim.x * blockDim.x) {
@@ -144,7 +144,8 @@ __global__ void __launch_bounds__(256) k_pc_prior_ll(TrackParams P) {
 __global__ void __launch_bounds__(256) k_sir_sum(TrackParams P) {
   __shared__ i128 sh[8];
   TrackCtl* C = P.ctl;
-  if (P.method == 1 && !C->pc_prior) return;   // pcSIR frame with uniform priors
+  // pcSIR frame with uniform priors, or one the bins kernel could not hold
+  if (P.method == 1 && (!C->pc_prior || (C->flags & PCS_FLAG_CAPACITY))) return;
   const double m = ordered_to_f64(C->max_ll_ord);
   i128 acc = 0;
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < P.n; j += (i64)gridDim.x * blockDim.x) {
@@ -160,20 +161,21 @@ __global__ void __launch_bounds__(256) k_sir_sum(TrackParams P) {
 __device__ __forceinline__ void sir_finalize(const TrackParams& P) {
   TrackCtl* C = P.ctl;
   const i64 k = C->k, ko = k - C->k_out;
+  const bool row = k < C->k_end;   // (an output row exists for this frame)
   const double mf = ordered_to_f64(C->max_ll_ord);
   const bool degenerate = (mf == -INFINITY);
   const bool bad_m = !(mf == mf) || mf == INFINITY;
   double est[5];
   for (int c = 0; c < 5; ++c) {
     est[c] = scalbn(i128_to_f64_rn(load_i128(C->est[c])), -(FX_WQ + FX_STATE));
-    C->out_est[ko * 5 + c] = est[c];
+    if (row) C->out_est[ko * 5 + c] = est[c];
   }
   if (est[0] == est[0] && est[1] == est[1]) {   // staging window of the next frame
     C->center[0] = est[0];
     C->center[1] = est[1];
   }
   double ess = 1.0 / scalbn(i128_to_f64_rn(load_i128(C->w2)), -FX_W2);
-  C->out_ess[ko] = ess;
+  if (row) C->out_ess[ko] = ess;
   bool flag_bad = degenerate || bad_m;
   if (degenerate) set_flag(C, PCS_FLAG_DEGENERATE);
   if (bad_m) set_flag(C, PCS_FLAG_NONFINITE);
@@ -181,9 +183,11 @@ __device__ __forceinline__ void sir_finalize(const TrackParams& P) {
   // without resampling the next frame starts from these weights unless they
   // are all equal (then uniform, as the general driver does)
   C->prior_nonuniform = (!res && !flag_bad && C->wmin_bits != C->wmax_bits) ? 1 : 0;
-  C->out_res[ko] = (unsigned char)res;
   const i64 evals = (P.method == 1) ? C->frame_occ : P.n;   // pcSIR: one per occupied cell
-  C->out_occ[ko] = evals;
+  if (row) {
+    C->out_res[ko] = (unsigned char)res;
+    C->out_occ[ko] = evals;
+  }
   C->evals += evals;
   C->do_resample = res;
   C->m = mf;
@@ -199,7 +203,7 @@ __device__ __forceinline__ void sir_finalize(const TrackParams& P) {
 __global__ void __launch_bounds__(256) k_sir_stats(TrackParams P) {
   __shared__ i128 sh[8];
   TrackCtl* C = P.ctl;
-  if (P.method == 1 && !C->pc_prior) return;   // pcSIR frame with uniform priors
+  if (P.method == 1 && (!C->pc_prior || (C->flags & PCS_FLAG_CAPACITY))) return;
   const i64 k = C->k;
   const float* st = (k & 1) ? P.buf0 : P.buf1;
   const double m = ordered_to_f64(C->max_ll_ord);

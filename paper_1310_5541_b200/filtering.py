@@ -300,7 +300,9 @@ def fused_track(frames, cfg: FilterConfig, rng, method, grid=None, placement=0, 
                 ev = torch.cuda.Event()
                 ev.record(side)
                 arrived.append(ev)
-        dev_frames.record_stream(torch.cuda.current_stream())
+        # the side stream writes dev_frames: keep its memory until those copies
+        # are done even if the filter raises before waiting on them
+        dev_frames.record_stream(side)
     else:
         dev_frames = _frames_to_device(frames)
     k, h, w = dev_frames.shape

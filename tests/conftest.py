@@ -25,6 +25,17 @@ def _ensure_oracle():
 _ensure_oracle()
 
 
+def assert_propagation_close(got, want, s32, z32, dyn):
+    """|got - want| <= 2^-22 x max(|state in|, |state out|, |noise term|,
+    |v dt| for positions): two float32 ulps of the operands' scale."""
+    sig = np.array([dyn[0], dyn[0], dyn[1], dyn[1], dyn[2]])[:, None]
+    scale = np.maximum.reduce([np.abs(s32.astype(np.float64)), np.abs(want),
+                               np.abs(z32.astype(np.float64)) * sig])
+    scale[:2] = np.maximum(scale[:2], np.abs(s32[2:4].astype(np.float64)) * dyn[3])
+    err = np.abs(got.astype(np.float64) - want)
+    assert np.all(err <= 2.0 ** -22 * scale), float(np.max(err / scale))
+
+
 def golden(name):
     return np.load(GOLDEN / f"{name}.npz", allow_pickle=False)
 

@@ -11,7 +11,7 @@ import pytest
 import torch
 
 import paper_1310_5541_b200 as pc
-from conftest import golden, spot_pixels
+from conftest import assert_propagation_close, golden, spot_pixels
 from oracle import pcsir_oracle as orc
 from paper_1310_5541_b200 import _lib, binning, filtering, kernels, state
 
@@ -67,6 +67,9 @@ def test_propagate_bitexact_with_device_normals(cuda):
     want = orc.propagate_f32(host.T, z, 0.5, 0.1, 1.0, 1.0)
     assert np.array_equal(out.cpu().numpy(), want)
     assert out[4].min().item() >= 0.0
+    # and within two float32 ulps of the reference's float64 order
+    ref = orc.propagate_f64_order(host.T, z, 0.5, 0.1, 1.0, 1.0).astype(np.float64)
+    assert_propagation_close(out.cpu().numpy(), ref, host.T, z, (0.5, 0.1, 1.0, 1.0))
 
 
 def test_propagate_golden_replayed_normals(cuda):
@@ -74,7 +77,11 @@ def test_propagate_golden_replayed_normals(cuda):
     d = g["dyn"]
     out = state.propagate_with_normals(g["states"], pc.DynamicsParams(d[0], d[1], d[2], d[3]),
                                        g["normals"].T)
-    assert np.array_equal(out.cpu().numpy(), g["out"].T.astype(np.float32))
+    s32, z32 = g["states"].T.astype(np.float32), g["normals"].T.astype(np.float32)
+    # bit-exact against the canonical float32 form, and close to the
+    # reference's float64 values (reference golden, state.py:115-127)
+    assert np.array_equal(out.cpu().numpy(), orc.propagate_f32(s32, z32, *d))
+    assert_propagation_close(out.cpu().numpy(), g["out"].T, s32, z32, d)
 
 
 def test_init_cloud_matches_oracle(cuda):

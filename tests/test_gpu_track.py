@@ -8,7 +8,7 @@ import pytest
 import torch
 
 import paper_1310_5541_b200 as pc
-from conftest import golden, spot_pixels
+from conftest import assert_propagation_close, golden, spot_pixels
 from oracle import pcsir_oracle as orc
 from paper_1310_5541_b200 import rng as prng_mod
 from paper_1310_5541_b200 import state
@@ -17,7 +17,8 @@ pytestmark = pytest.mark.gpu
 
 W_RTOL = 1e-5
 # The reference propagates in float64 and weights the UNROUNDED states; the
-# device state is float32 (bit-exact to float32(reference)). Position rounding
+# device state is float32 (bit-exact to the canonical float32 form, within
+# two float32 ulps of the reference's values). Position rounding
 # (<= 1e-6 px) moves log L by up to ~|dlogL/dx| * 1e-6, i.e. a few 1e-5 for
 # particles with large residuals — hence the looser tolerance when comparing
 # with the reference's float64-state weights. Stage-wise (oracle on the
@@ -38,6 +39,15 @@ def _oracle_weights(out_states32, prior, frame_pixels, lik_args, bin_map=None):
     return orc.normalize(np.exp(lw - lw.max()))
 
 
+def _check_states(dev_states, g, ref_states):
+    """Propagated states: bit-exact against the canonical float32 form on the
+    reference's replayed draws, within two float32 ulps of the reference."""
+    s32, z32 = g["states"].T.astype(np.float32), g["normals"].T.astype(np.float32)
+    dyn = (0.5, 0.1, 1.0, 1.0)
+    assert np.array_equal(dev_states.T, orc.propagate_f32(s32, z32, *dyn))
+    assert_propagation_close(np.ascontiguousarray(dev_states.T), ref_states.T, s32, z32, dyn)
+
+
 # --- golden single steps (sis_step / pc_sis_step with the reference's draws) ----------
 def test_sis_step_golden(cuda):
     g = golden("steps")
@@ -46,7 +56,7 @@ def test_sis_step_golden(cuda):
     ps = pc.ParticleSet(g["states"], g["weights"])
     out = pc.sis_step(ps, frame, lik, pc.DynamicsParams(0.5, 0.1, 1.0),
                       prng_mod.ReplayNormals(g["normals"]))
-    assert np.array_equal(out.states, g["sis_states"].astype(np.float32))
+    _check_states(out.states, g, g["sis_states"])
     w = pc.normalize(out).weights
     # stage-wise: oracle weighting of the device's float32 states
     want = _oracle_weights(out.states, g["weights"], g["frame"].astype(np.float32).astype(float),
@@ -69,7 +79,7 @@ def test_pc_sis_step_golden(cuda, cpp):
                               prng_mod.ReplayNormals(g["normals"]))
     assert occ == int(g[f"pc{cpp}_occ"])                 # bit-exact occupied-bin count
     assert lik.evals == int(g[f"pc{cpp}_evals"])
-    assert np.array_equal(out.states, g[f"pc{cpp}_states"].astype(np.float32))
+    _check_states(out.states, g, g[f"pc{cpp}_states"])
     w = pc.normalize(out).weights
     # stage-wise: canonical dummies of the device states, oracle likelihood per bin
     st32 = out.states.astype(np.float32)
@@ -466,3 +476,27 @@ def test_fused_multinomial_equals_general(cuda, frac, method):
     assert np.array_equal(a.estimates, b.estimates)
     assert np.array_equal(a.ess, b.ess)
     assert la.evals == lb.evals
+
+
+def test_capacity_fallback_with_prior_weights(cuda):
+    """More occupied cells than the fused bins kernel holds (8192) on a frame
+    whose particles carry prior weights (ESS threshold, no resampling): the
+    fused loop stops cleanly (no second finalisation of the frame, no writes
+    past the output rows) and the driver reruns the track on the general
+    path (binning.py:212-226 semantics either way)."""
+    frames, truth, init, _ = _c1_like(n=50_000, k=14)
+    init = pc.InitSpec(pc.StateVector(20.0, 32.0, 0.5, 0.0, 20.0), "point")
+    dyn = pc.DynamicsParams(0.8, 0.1, 1.0)
+    res = pc.ResampleConfig(0.001, "systematic")
+    grid = pc.BinGrid.pixel_aligned(64, 64, 8)
+    flat = pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(1e4, 5))
+    flat2 = pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(1e4, 5))
+    a = pc.pcsir_track(frames, pc.PcFilterConfig(50_000, init, dyn, res, flat, grid=grid),
+                       pc.PhiloxRng(13), fused=True)
+    b = pc.pcsir_track(frames, pc.PcFilterConfig(50_000, init, dyn, res, flat2, grid=grid),
+                       pc.PhiloxRng(13), fused=False)
+    assert a.path == "general"            # the fused loop hit its capacity and fell back
+    assert not a.resampled[1:].any()      # frames after the first carry prior weights
+    assert np.array_equal(a.estimates, b.estimates)
+    assert np.array_equal(a.ess, b.ess)
+    assert a.likelihood_evals == b.likelihood_evals > 8192

@@ -5,7 +5,7 @@ the reference tests' inline known answers. CPU only."""
 import numpy as np
 import pytest
 
-from conftest import golden
+from conftest import assert_propagation_close, golden
 from oracle import pcsir_oracle as orc
 
 
@@ -165,9 +165,14 @@ def test_propagate_matches_reference():
     noise = np.array([dyn[0], dyn[0], dyn[1], dyn[1], dyn[2]])
     out = orc.propagate_array(g["states"], noise, dyn[3], g["normals"])
     assert np.array_equal(out, g["out"])
-    f32 = orc.propagate_f32(g["states"].T.astype(np.float32), g["normals"].T.astype(np.float32),
-                            *dyn)
-    assert np.array_equal(f32, g["out"].T.astype(np.float32))
+    s32, z32 = g["states"].T.astype(np.float32), g["normals"].T.astype(np.float32)
+    f64o = orc.propagate_f64_order(s32, z32, *dyn)
+    assert np.array_equal(f64o, g["out"].T.astype(np.float32))
+    # the device's canonical float32 form agrees to 2 float32 ulps of the
+    # operand scale (double rounding of x + vx dt; parameters split hi + lo)
+    f32 = orc.propagate_f32(s32, z32, *dyn)
+    assert_propagation_close(f32, g["out"].T, s32, z32, dyn)
+
 
 
 # --- whole filter driver ------------------------------------------------------
