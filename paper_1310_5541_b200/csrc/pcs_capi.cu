@@ -135,6 +135,7 @@ enum Slot {
   SL_TR_WPREV,
   SL_TR_LLTAB,
   SL_TR_CDF,
+  SL_TR_SUB,
   SL_COUNT
 };
 
@@ -950,6 +951,10 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
       PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_sum, 0, 5 * ctx->table_cells * 2 * sizeof(u64), st));
       ctx->table_dirty = false;
     }
+    // compact per-frame tables of the step-1 sub-window cells (pslot codes < SUBW)
+    PCS_SCRATCH(SL_TR_SUB, SUBW * (sizeof(u128) + sizeof(double) + sizeof(float)), P.wsub);
+    P.ltsub = (double*)(P.wsub + SUBW);
+    P.wtsub = (float*)(P.ltsub + SUBW);
     P.tab_cnt = ctx->tab_cnt;
     P.tab_sum = ctx->tab_sum;
     P.wtab = ctx->wtab;

@@ -127,7 +127,7 @@ struct TrackParams {
   int* anc;
   double* ll;                // SIR: per-particle log-likelihood (float64); k_sir_sum
                              // replaces it by exp(ll - max) for the rest of the frame
-  u32* pslot;                // pcSIR: flat cell id per particle
+  u32* pslot;                // pcSIR: cell code per particle (pslot_code below)
   u32* tab_cnt;              // [G]
   u64* tab_sum;              // [5][G][2]
   float* wtab;               // [G]
@@ -150,6 +150,9 @@ struct TrackParams {
   double thresh;             // resample when ESS < thresh (= threshold_fraction * N)
   float* wprev;              // normalised prior weights when prior_nonuniform
   double* lltab;             // pcSIR with prior weights: [G] log-likelihood per cell
+  u128* wsub;                // [SUBW] wfix of the frame's step-1 sub-window cells (by code)
+  double* ltsub;             // [SUBW] lltab of the sub-window cells
+  float* wtsub;              // [SUBW] wtab of the sub-window cells
   int method;                // 0 SIR, 1 pcSIR
   int sir_chunk;             // k_sir_propagate_lik: particles per dynamic chunk
   int multinomial;           // resampling scheme: the resampler writes the cdf and
@@ -158,6 +161,30 @@ struct TrackParams {
                              // boxes of FMAP_BX x FMAP_BY pixels (TMA staging)
   u128* cta_agg;             // k_sys_resample: per-CTA exact weight totals
 };
+
+// pcSIR cell code of a particle (P.pslot): the cell's index q < SUBW in the
+// frame's step-1 sub-window (row-major, snx columns), else SUBW + its flat id.
+// Per-cell tables are read through the code: the sub-window cells from the
+// compact per-frame tables (16 KB for wsub, L1-resident), the others from the
+// full-grid tables.
+__device__ __forceinline__ u128 code_wfix(const TrackParams& P, u32 code) {
+  const u128* p = (code < (u32)SUBW) ? P.wsub + code : P.wfix + (code - (u32)SUBW);
+  return *p;   // one 16-byte load, no branch
+}
+__device__ __forceinline__ float code_wtab(const TrackParams& P, u32 code) {
+  return code < (u32)SUBW ? P.wtsub[code] : P.wtab[code - SUBW];
+}
+__device__ __forceinline__ double code_ll(const TrackParams& P, u32 code) {
+  return code < (u32)SUBW ? P.ltsub[code] : P.lltab[code - SUBW];
+}
+// the sub-window code of flat cell id `cell` (bins kernel), or -1
+__device__ __forceinline__ int sub_code(const TrackParams& P, const TrackCtl* C, u32 cell) {
+  const u32 nc = (u32)P.grid.ncols;
+  const u32 iy = cell / nc, ix = cell - iy * nc;
+  const i64 qx = (i64)ix - C->sx0, qy = (i64)iy - C->sy0;
+  if (qx < 0 || qx >= C->snx || qy < 0 || qy >= C->sny) return -1;
+  return (int)(qy * C->snx + qx);
+}
 
 // Programmatic dependent launch: the frame's kernels are launched with the
 // programmatic-serialization attribute, so the next kernel is scheduled while
@@ -514,10 +541,11 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
       const int ix = cell_axis_hot(o[0], axx);
       const int iy = cell_axis_hot(o[1], axy);
       const u32 flat = (u32)iy * ncols32 + (u32)ix;   // G <= 2^28
-      P.pslot[j] = flat;
       const int lx = ix - sx0i, ly = iy - sy0i;
+      const bool inwin = (u32)lx < (u32)snxi && (u32)ly < (u32)snyi;
+      P.pslot[j] = inwin ? (u32)(ly * snxi + lx) : (u32)SUBW + flat;   // cell code
       float dx, dy;
-      if ((u32)lx < (u32)snxi && (u32)ly < (u32)snyi && delta_exact(o[0], sm.ref[lx], dx) &&
+      if (inwin && delta_exact(o[0], sm.ref[lx], dx) &&
           delta_exact(o[1], refy[ly], dy) && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f &&
           fabsf(o[4]) < 128.0f) {
         const int q = ly * snxi + lx;
@@ -905,6 +933,8 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     for (int b = t; b < M; b += BINS_BLOCK) {
       const u32 cell = V.cell(b);
       P.lltab[cell] = sm.ll[b];
+      const int qs = sub_code(P, C, cell);
+      if (qs >= 0) P.ltsub[qs] = sm.ll[b];
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
         u64* p = P.tab_sum + ((i64)c * P.G + cell) * 2;
@@ -945,6 +975,11 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
       const float w = __double2float_rn(__ddiv_rn(sm.ll[b], Sf));   // normalised_weight
       P.wtab[cell] = w;
       P.wfix[cell] = cdf_fixed(w);
+      const int qs = sub_code(P, C, cell);
+      if (qs >= 0) {
+        P.wtsub[qs] = w;
+        P.wsub[qs] = cdf_fixed(w);
+      }
       wmin = min(wmin, __float_as_uint(w));
       wmax = max(wmax, __float_as_uint(w));
       const long long wq = (long long)f32_to_fixed(w, FX_WQ);   // w <= 1: fits 63 bits
@@ -1067,7 +1102,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, 4) k_scan_emit(TrackParams P) {
   for (int q = 0; q < SCAN_ITEMS; ++q) {
     i64 i = base + (i64)q * SCAN_BLOCK + threadIdx.x;
     float w = 0.0f;
-    if (i < n) w = (KIND == 1) ? P.wtab[P.pslot[i]] : weight_from_ex(P.ll[i], Sf);
+    if (i < n) w = (KIND == 1) ? code_wtab(P, P.pslot[i]) : weight_from_ex(P.ll[i], Sf);
     wsh[wpad(q * SCAN_BLOCK + threadIdx.x)] = w;
   }
   __syncthreads();
@@ -1288,6 +1323,11 @@ __device__ __forceinline__ int lds_u32(u32 addr) {
 // (grid = SMs x occupancy, set by the host from the occupancy calculator).
 constexpr int RS_ITEMS = 15;
 constexpr int RS_TILE = SCAN_BLOCK * RS_ITEMS;   // 3840
+// A tile emits ~RS_TILE slots (+- a few %): the emission stage holds
+// RS_SCAP slots per thread so that one chunk covers almost every tile (odd:
+// the per-thread stride is bank-conflict free)
+constexpr int RS_SCAP = 17;
+constexpr int RS_STAGE = SCAN_BLOCK * RS_SCAP;   // 4352
 
 __device__ __forceinline__ void grid_barrier(TrackCtl* C, int nblocks) {
   __syncthreads();
@@ -1343,7 +1383,7 @@ template <> struct RsElem<2> { typedef double T; };
 template <int KIND>
 struct RsSmem {
   typename RsElem<KIND>::T ring[2][RS_TILE];   // TMA ring (16-byte aligned)
-  int stage[RS_TILE];
+  int stage[RS_STAGE];
   int hp[KIND == 1 ? 1 : RS_TILE];   // run heads (KIND 1: in place of the consumed cell ids)
   u128 wtot[SCAN_BLOCK / 32];
   int s_wmax[SCAN_BLOCK / 32];
@@ -1381,7 +1421,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
     const double Sf = C->Sf;
     for (i64 i = t0 * RS_TILE + threadIdx.x; i < min(n, t1 * RS_TILE); i += SCAN_BLOCK) {
       P.anc_out[P.idx_off + i - P.slot_lo] = (int)i;
-      if (keep) P.wprev[i] = (KIND == 1) ? P.wtab[P.pslot[i]] : weight_from_ex(P.ll[i], Sf);
+      if (keep) P.wprev[i] = (KIND == 1) ? code_wtab(P, P.pslot[i]) : weight_from_ex(P.ll[i], Sf);
     }
     return;
   }
@@ -1406,7 +1446,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
   // exact weight of item k of a ring buffer (nv = valid items of its tile)
   auto weight = [&](const E* buf, int k, int nv) -> u128 {
     if (k >= nv) return 0;
-    if (KIND == 1) return P.wfix[(u32)buf[k]];
+    if (KIND == 1) return code_wfix(P, (u32)buf[k]);
     return cdf_fixed(weight_from_ex((double)buf[k], Sf));
   };
   auto tile_items = [&](i64 tile) -> int { return (int)min((i64)RS_TILE, n - tile * RS_TILE); };
@@ -1514,7 +1554,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
           }
         }
       }
-      const u32 hp_s = smem_u32(hp + k0), st_s = smem_u32(stage + k0);
+      const u32 hp_s = smem_u32(hp + k0);
       if (!MULTI) {
 #pragma unroll
         for (int q = 0; q < RS_ITEMS; ++q) {
@@ -1527,31 +1567,35 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
             jr = jend;
           }
           sts_u32(hp_s + 4 * q, h);    // (KIND 1: over item k, already read)
-          sts_u32(st_s + 4 * q, -1);   // first chunk's fill
         }
+        const u32 st_s = smem_u32(stage + threadIdx.x * RS_SCAP);
+#pragma unroll
+        for (int q = 0; q < RS_SCAP; ++q) sts_u32(st_s + 4 * q, -1);   // first chunk's fill
       }
     }
     __syncthreads();   // every read of ring[L & 1] is done; it is free for load L + 2
-    // slots in chunks of RS_TILE: heads, block max-scan, coalesced writes
-    // (multinomial: k_multinomial_emit draws the slots)
+    // slots in chunks of RS_STAGE (one chunk for almost every tile): heads,
+    // block max-scan, coalesced writes (multinomial: k_multinomial_emit draws
+    // the slots)
     const int m_slots = MULTI ? 0 : (int)(tj1 - tj0);   // <= ng < 2^31
     int carry = -1;
-    const u32 stage_s = smem_u32(stage), hp_s = smem_u32(hp + k0);
-    for (int c0 = 0; c0 < m_slots; c0 += RS_TILE) {
+    const int ks0 = (int)threadIdx.x * RS_SCAP;          // this thread's stage positions
+    const u32 stage_s = smem_u32(stage), hp_s = smem_u32(hp + k0), own_s = smem_u32(stage + ks0);
+    for (int c0 = 0; c0 < m_slots; c0 += RS_STAGE) {
       if (c0 > 0) {
 #pragma unroll
-        for (int q = 0; q < RS_ITEMS; ++q) sts_u32(stage_s + 4 * (k0 + q), -1);
+        for (int q = 0; q < RS_SCAP; ++q) sts_u32(own_s + 4 * q, -1);
         __syncthreads();
       }
 #pragma unroll
       for (int q = 0; q < RS_ITEMS; ++q) {
         const u32 hr = (u32)(lds_u32(hp_s + 4 * q) - c0);   // no head: (u32)(-1 - c0) >= 2^31
-        if (hr < (u32)RS_TILE) sts_u32(stage_s + 4 * hr, k0 + q);
+        if (hr < (u32)RS_STAGE) sts_u32(stage_s + 4 * hr, k0 + q);
       }
       __syncthreads();
       int tmax = -1;
 #pragma unroll
-      for (int q = 0; q < RS_ITEMS; ++q) tmax = max(tmax, stage[k0 + q]);
+      for (int q = 0; q < RS_SCAP; ++q) tmax = max(tmax, lds_u32(own_s + 4 * q));
       int incl = tmax;
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
@@ -1570,22 +1614,22 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
       }
       int runm = max(prev, excl_l);
 #pragma unroll
-      for (int q = 0; q < RS_ITEMS; ++q) {
-        runm = max(runm, stage[k0 + q]);
-        stage[k0 + q] = runm;
+      for (int q = 0; q < RS_SCAP; ++q) {
+        runm = max(runm, lds_u32(own_s + 4 * q));
+        sts_u32(own_s + 4 * q, runm);
       }
       __syncthreads();
-      const int cm = min(RS_TILE, m_slots - c0);
+      const int cm = min(RS_STAGE, m_slots - c0);
       const i64 w0 = tj0 + c0 - lo;   // output position of the chunk's first slot
       const int ib = (int)base;
-      if (cm == RS_TILE && w0 >= 0 && w0 + cm <= cap) {
-        int* dst = P.anc_out + w0 + threadIdx.x;
+      if (w0 >= 0 && w0 + cm <= cap) {   // coalesced: slot t + q * SCAN_BLOCK
+        int* dst = P.anc_out + w0;
         const u32 src_s = stage_s + 4 * threadIdx.x;
 #pragma unroll
-        for (int q = 0; q < RS_ITEMS; ++q) dst[q * SCAN_BLOCK] = ib + lds_u32(src_s + 4 * q * SCAN_BLOCK);
-      } else if (w0 >= 0 && w0 + cm <= cap) {
-        int* dst = P.anc_out + w0;
-        for (int k = threadIdx.x; k < cm; k += SCAN_BLOCK) dst[k] = ib + stage[k];
+        for (int q = 0; q < RS_SCAP; ++q) {
+          const int k = (int)threadIdx.x + q * SCAN_BLOCK;
+          if (k < cm) dst[k] = ib + lds_u32(src_s + 4 * q * SCAN_BLOCK);
+        }
       } else {
         for (int k = threadIdx.x; k < cm; k += SCAN_BLOCK) {
           const i64 kk = w0 + k;
@@ -1640,7 +1684,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, 4) k_sys_resample_small(TrackParam
     for (int k = threadIdx.x; k < nv; k += SCAN_BLOCK) {
       const i64 i = base + k;
       P.anc_out[P.idx_off + i - P.slot_lo] = (int)i;
-      if (keep) P.wprev[i] = (KIND == 1) ? P.wtab[P.pslot[i]] : weight_from_ex(P.ll[i], Sf);
+      if (keep) P.wprev[i] = (KIND == 1) ? code_wtab(P, P.pslot[i]) : weight_from_ex(P.ll[i], Sf);
     }
     return;
   }
@@ -1651,7 +1695,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, 4) k_sys_resample_small(TrackParam
   __syncthreads();
   auto weight = [&](int k) -> u128 {
     if (k >= nv) return 0;
-    if (KIND == 1) return P.wfix[(u32)sm.items[k]];
+    if (KIND == 1) return code_wfix(P, (u32)sm.items[k]);
     return cdf_fixed(weight_from_ex((double)sm.items[k], Sf));
   };
   const int k0 = (int)threadIdx.x * RSS_ITEMS;

@@ -129,7 +129,7 @@ __global__ void __launch_bounds__(256) k_pc_prior_ll(TrackParams P) {
   long long lmax = LLONG_MIN;
   bool bad = false;
   for (i64 j = blockIdx.x * (i64)blockDim.x + threadIdx.x; j < P.n; j += (i64)gridDim.x * blockDim.x) {
-    const double ll = __dadd_rn(log_prior(P.wprev[j]), P.lltab[P.pslot[j]]);
+    const double ll = __dadd_rn(log_prior(P.wprev[j]), code_ll(P, P.pslot[j]));
     P.ll[j] = ll;
     if (!(ll == ll) || ll == INFINITY) bad = true;
     lmax = max(lmax, (long long)f64_to_ordered(ll));

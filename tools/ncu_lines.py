@@ -40,7 +40,7 @@ in_fn = False
 for ln in dis.splitlines():
     m = re.match(r"\s*\.text\.(\S+):", ln)
     if m:
-        in_fn = re.search(kregex, m.group(1)) is not None
+        in_fn = re.search(os.environ.get("SASS_RE", kregex), m.group(1)) is not None
         continue
     if not in_fn:
         continue

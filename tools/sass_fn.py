@@ -2,6 +2,7 @@
 """Print the SASS of one kernel (substring of its mangled name) from a .so:
 usage: sass_fn.py LIB NAME_SUBSTR [--hist]"""
 import collections
+import re
 import subprocess
 import sys
 
@@ -12,7 +13,7 @@ for ln in out.splitlines():
     if "Function :" in ln:
         cur = ln.split("Function :")[1].strip()
         fns[cur] = []
-    elif cur and ln.strip().startswith("/*") and "*/" in ln:
+    elif cur and re.match(r"\s*/\*[0-9a-f]{4,}\*/\s+\S", ln):
         fns[cur].append(ln)
 hit = [f for f in fns if name in f]
 for f in hit:
