@@ -153,6 +153,13 @@ int pcs_partition(pcs_ctx* ctx, const float* states, int64_t ld, int64_t n,
                   void* stream);
 /* dummies[c*ldd + b] (float32) for the m occupied bins. placement 0 = CoM,
  * 1 = cell centre. prior_w (float32, may be NULL) selects weighted CoM. */
+/* make_dummy (binning.py:129-154): the representative state of ONE cell's
+ * members. members: device float64 (n, 5) row-major; weights: device
+ * float64 (n,) or NULL; placement 0 centre of mass, 1 cell centre (bounds =
+ * host x_lo, x_hi, y_lo, y_hi); out: device float64 (5,). Reference
+ * summation orders (np.add.reduceat rows, numpy pairwise weight total). */
+int pcs_make_dummy(const double* members, int64_t n, const double* weights, int32_t placement,
+                   const double* bounds, double* out, void* stream);
 int pcs_dummies(pcs_ctx* ctx, const float* states, int64_t ld, int64_t n, const int32_t* order,
                 const int32_t* bin_of, const int64_t* counts, const uint64_t* unique, int64_t m,
                 const pcs_grid_t* grid, int32_t placement, const float* prior_w,
@@ -203,7 +210,9 @@ typedef struct pcs_track_cfg_t {
   double threshold_fraction;  /* resample when ESS < threshold_fraction * N
                                  (filtering.py:169-170); 0 means 1.0 */
   int32_t scheme;        /* 0 systematic, 1 multinomial (filtering.py:96-100) */
-  int32_t reserved;
+  int32_t weighted_com;  /* pcSIR: 1 = dummies at the prior-weighted centre of mass
+                            (binning.py:160-165,186); fused while the prior weights
+                            are uniform, PCS_E_CAPACITY (general path) otherwise */
 } pcs_track_cfg_t;
 
 typedef struct pcs_track_result_t {

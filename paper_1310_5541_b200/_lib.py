@@ -62,7 +62,7 @@ class PcsTrackCfg(ctypes.Structure):
                 ("init", PcsInit), ("dyn", PcsDynamics), ("spot", PcsSpot),
                 ("grid", PcsGrid), ("seed", c_uint64), ("frame0", c_uint32),
                 ("use_graph", c_int32), ("threshold_fraction", c_double),
-                ("scheme", c_int32), ("reserved", c_int32)]
+                ("scheme", c_int32), ("weighted_com", c_int32)]
 
 
 class PcsTrackResult(ctypes.Structure):
@@ -122,6 +122,8 @@ _SIGNATURES = [
     ("pcs_track_launches_per_step", c_int32, [c_void_p]),
     ("pcs_track_debug", c_int32, [c_void_p, c_void_p, c_void_p]),
     ("pcs_track_info", c_int32, [c_void_p, c_void_p, c_int32, c_void_p]),
+    ("pcs_make_dummy", c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
+                                 c_void_p]),
     ("pcs_track_states", c_int32, [c_void_p, P(c_void_p), P(c_int64)]),
     ("pcs_mt_begin", c_int32, [c_void_p, P(PcsTrackCfg), c_int64, c_void_p, c_int64, c_int64,
                                c_int64, c_int64, c_void_p]),

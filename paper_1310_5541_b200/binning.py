@@ -151,26 +151,29 @@ def assign_bins(pset: ParticleSet, grid: BinGrid) -> BinOccupancy:
 
 
 def make_dummy(members, cell_bounds, placement: DummyPlacement, weights=None) -> StateVector:
-    """Representative state for one cell's member states (binning.py:129-154).
-
-    Single-cell helper on host values (API surface, not on the step); the
-    step computes the same quantity on the device (``_dummy_states``).
-    """
+    """Representative state for one cell's member states (binning.py:129-154),
+    computed on the device (pcs_make_dummy) in float64 with the reference's
+    summation orders: centre of mass = np.add.reduceat mean (single members
+    reproduce themselves bit for bit), weighted by ``weights`` when given;
+    cell centre puts x, y at the middle of ``cell_bounds``."""
     if len(members) == 0:
         raise ValueError("a dummy needs at least one member state")
     rows = np.atleast_2d(np.asarray(
         [m.as_array() if isinstance(m, StateVector) else m for m in members], dtype=np.float64))
+    _lib.require_cuda()
+    dev = _lib.device()
+    r = torch.from_numpy(np.ascontiguousarray(rows)).to(dev)
+    w = None
     if weights is not None:
-        w = np.asarray(weights, dtype=np.float64)
-        mean = (w @ rows) / w.sum()
-    else:
-        mean = np.add.reduceat(rows, [0], axis=0)[0] / rows.shape[0]
-    if placement is DummyPlacement.CELL_CENTER:
-        x_lo, x_hi, y_lo, y_hi = cell_bounds
-        mean = mean.copy()
-        mean[X] = (x_lo + x_hi) / 2.0
-        mean[Y] = (y_lo + y_hi) / 2.0
-    return StateVector.from_array(mean)
+        w = torch.from_numpy(np.ascontiguousarray(np.asarray(weights, dtype=np.float64))).to(dev)
+        if w.numel() != r.shape[0]:
+            raise ValueError("one weight per member is required")
+    out = torch.empty(5, dtype=torch.float64, device=dev)
+    pl = 1 if placement is DummyPlacement.CELL_CENTER else 0
+    b = (ctypes.c_double * 4)(*[float(v) for v in cell_bounds])
+    _lib.check(_lib.lib().pcs_make_dummy(_lib.ptr(r), r.shape[0], _lib.ptr(w), pl, b,
+                                         _lib.ptr(out), _lib.stream()), "pcs_make_dummy")
+    return StateVector.from_array(out.cpu().numpy())
 
 
 def dummy_states_device(soa, grid, part: DevicePartition, placement, prior_w=None):
@@ -248,8 +251,6 @@ def pcsir_track(frames, cfg: PcFilterConfig, rng, fused=None) -> TrackResult:
     prng = as_philox(rng)
     if fused is None:
         fused = _fused_ok(cfg)
-    if cfg.weighted_com:
-        fused = False   # weighted centre of mass (binning.py:160-165) runs the general path
     if fused:
         start = (prng.seed, prng.frame)
         try:

@@ -103,4 +103,81 @@ __global__ void k_dummies(const u64* __restrict__ sums, const i64* __restrict__ 
   }
 }
 
+// ---- make_dummy (binning.py:129-154): one cell's representative state ----
+// float64 members (n, 5) row-major, as the reference. One thread, in the
+// reference's summation orders: the unweighted mean is np.add.reduceat over
+// axis 0 (rows added one after another, then / n); the weight total is
+// numpy's pairwise sum (blocks of 8 partial sums below 128 elements,
+// recursive halving above), the weighted numerator w @ rows is accumulated
+// row by row (BLAS order is implementation-defined; exact for exact data).
+__device__ double np_pairwise_sum(const double* a, i64 n) {
+  // iterative post-order form of numpy's recursive pairwise_sum
+  // (PW_BLOCKSIZE 128, 8 partial sums); ops: 0 = sum a range, 1 = add the
+  // two most recent results (left + right)
+  double vals[64];
+  int op_kind[128];
+  i64 op_lo[128], op_n[128];
+  int top = 0, vp = 0;
+  op_kind[top] = 0; op_lo[top] = 0; op_n[top] = n; ++top;
+  while (top > 0) {
+    --top;
+    const int kind = op_kind[top];
+    const i64 lo = op_lo[top], m = op_n[top];
+    if (kind == 1) {
+      const double r = vals[vp - 1], l = vals[vp - 2];
+      vp -= 2;
+      vals[vp++] = __dadd_rn(l, r);
+      continue;
+    }
+    const double* x = a + lo;
+    if (m < 8) {
+      double res = 0.0;
+      for (i64 i = 0; i < m; ++i) res = __dadd_rn(res, x[i]);
+      vals[vp++] = res;
+    } else if (m <= 128) {
+      double r[8];
+      for (int q = 0; q < 8; ++q) r[q] = x[q];
+      i64 i;
+      for (i = 8; i < m - (m % 8); i += 8)
+        for (int q = 0; q < 8; ++q) r[q] = __dadd_rn(r[q], x[i + q]);
+      double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                             __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+      for (; i < m; ++i) res = __dadd_rn(res, x[i]);
+      vals[vp++] = res;
+    } else {
+      i64 n2 = m / 2;
+      n2 -= n2 % 8;
+      op_kind[top] = 1; op_lo[top] = 0; op_n[top] = 0; ++top;            // then combine
+      op_kind[top] = 0; op_lo[top] = lo + n2; op_n[top] = m - n2; ++top;  // right second
+      op_kind[top] = 0; op_lo[top] = lo; op_n[top] = n2; ++top;           // left first
+    }
+  }
+  return vals[0];
+}
+
+__global__ void k_make_dummy(const double* __restrict__ rows, i64 n, const double* __restrict__ w,
+                             int placement, double x_lo, double x_hi, double y_lo, double y_hi,
+                             double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  double mean[5];
+  if (w) {
+    double num[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+    for (i64 i = 0; i < n; ++i)
+      for (int c = 0; c < 5; ++c) num[c] = __dadd_rn(num[c], __dmul_rn(w[i], rows[i * 5 + c]));
+    const double den = np_pairwise_sum(w, n);
+    for (int c = 0; c < 5; ++c) mean[c] = __ddiv_rn(num[c], den);
+  } else {
+    double acc[5];
+    for (int c = 0; c < 5; ++c) acc[c] = rows[c];
+    for (i64 i = 1; i < n; ++i)
+      for (int c = 0; c < 5; ++c) acc[c] = __dadd_rn(acc[c], rows[i * 5 + c]);
+    for (int c = 0; c < 5; ++c) mean[c] = __ddiv_rn(acc[c], (double)n);
+  }
+  if (placement == 1) {   // cell centre (binning.py:150-153)
+    mean[0] = __ddiv_rn(__dadd_rn(x_lo, x_hi), 2.0);
+    mean[1] = __ddiv_rn(__dadd_rn(y_lo, y_hi), 2.0);
+  }
+  for (int c = 0; c < 5; ++c) out[c] = mean[c];
+}
+
 }  // namespace pcs

@@ -548,6 +548,17 @@ int pcs_dummies(pcs_ctx* ctx, const float* states, int64_t ld, int64_t n, const 
   return PCS_OK;
 }
 
+int pcs_make_dummy(const double* members, int64_t n, const double* weights, int32_t placement,
+                   const double* bounds, double* out, void* stream) {
+  PCS_CHECK_ARG(members && out && bounds, "bad arguments");
+  PCS_CHECK_ARG(n >= 1, "a dummy needs at least one member state");
+  PCS_CHECK_ARG(placement == 0 || placement == 1, "unknown placement");
+  k_make_dummy<<<1, 32, 0, S(stream)>>>(members, n, weights, placement, bounds[0], bounds[1],
+                                        bounds[2], bounds[3], out);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
 // ---------------------------------------------------------------------------
 // weights
 // ---------------------------------------------------------------------------
@@ -884,6 +895,7 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   P.pk = philox_key(cfg->seed);
   P.frame0 = cfg->frame0;
   P.placement = cfg->placement;
+  P.weighted = (cfg->method == 1 && cfg->placement == 0 && cfg->weighted_com) ? 1 : 0;
   P.idx_off = 0;
   P.n_global = n;
   P.slot_lo = 0;

@@ -122,6 +122,7 @@ struct TrackParams {
   PhiloxKey pk;              // round keys of seed (constant-bank operands)
   u32 frame0;
   int placement;
+  int weighted;              // pcSIR weighted centre of mass (uniform prior weights only)
   float* buf0;
   float* buf1;
   int* anc;
@@ -767,7 +768,9 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   const i64 k = C->k;
   const u32 nocc = C->n_occ;
   if (t == 0) atomicMax(&C->max_occ, nocc);
-  if ((C->flags & PCS_FLAG_CAPACITY) || nocc > (u32)BINS_MAXM) {
+  // (weighted centre of mass with non-uniform prior weights needs the
+  // per-particle weighted sums of the general path)
+  if ((C->flags & PCS_FLAG_CAPACITY) || nocc > (u32)BINS_MAXM || (P.weighted && C->pc_prior)) {
     if (t == 0) {
       set_flag(C, PCS_FLAG_CAPACITY);
       C->do_resample = 0;
@@ -820,17 +823,24 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     s_box[0] = INT_MAX; s_box[1] = INT_MIN; s_box[2] = INT_MAX; s_box[3] = INT_MIN;
   }
   __syncthreads();
-  // 1) dummies (exact means, binning.py:157-172) and the union of their windows
+  // 1) dummies (exact means, binning.py:157-172) and the union of their windows;
+  //    weighted centre of mass with the uniform prior weight w0 = RN32(1/N)
+  //    of the general path: RN32(RN64(RN64(wq S) / RN64(wq count)) 2^-40),
+  //    wq = round(w0 2^62) (pcs_bin.cuh k_dummies)
+  const u64 wq0 = P.weighted ? (u64)f32_to_fixed(__double2float_rn(__ddiv_rn(1.0, (double)P.n_global)), FX_WQ)
+                             : 0ull;
   int bx0 = INT_MAX, bx1 = INT_MIN, by0 = INT_MAX, by1 = INT_MIN;
   for (int b = t; b < M; b += BINS_BLOCK) {
     const u32 cell = P.occ[b];
     const u32 cnt = P.tab_cnt[cell];
     float d[5];
+    const double den = P.weighted ? i128_to_f64_rn((i128)wq0 * (i128)cnt) : (double)cnt;
 #pragma unroll
     for (int c = 0; c < 5; ++c) {   // only x, y, I0 enter the likelihood (vx, vy unused)
       if (c == 2 || c == 3) { d[c] = 0.0f; continue; }
-      const double num = i128_to_f64_rn(load_i128(P.tab_sum + ((i64)c * P.G + cell) * 2));
-      d[c] = __double2float_rn(scalbn(__ddiv_rn(num, (double)cnt), -FX_STATE));
+      const i128 S = load_i128(P.tab_sum + ((i64)c * P.G + cell) * 2);
+      const double num = i128_to_f64_rn(P.weighted ? S * (i128)wq0 : S);
+      d[c] = __double2float_rn(scalbn(__ddiv_rn(num, den), -FX_STATE));
     }
     if (P.placement == 1) {  // cell centre (binning.py:168-171)
       const i64 ix = (i64)cell % P.grid.ncols, iy = (i64)cell / P.grid.ncols;

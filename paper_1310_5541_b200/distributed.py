@@ -207,6 +207,21 @@ class DeviceShardOps(ShardOps):
         return float(_lib.lib().pcs_philox_resample_u(seed, frame & 0xFFFFFFFF))
 
 
+def max_over_ranks(value, group=None):
+    """The largest of every rank's ``value`` (a float), e.g. a device-timed
+    duration, so that a multi-GPU throughput is the whole job's units over
+    the slowest rank's time. A one-element all-reduce MAX on the backend's
+    device (CUDA tensor for nccl, CPU tensor for gloo); identity when
+    torch.distributed is not initialised."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return float(value)
+    dev = torch.device("cuda", torch.cuda.current_device()) \
+        if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())
+
+
 def _all_reduce_box(box, group, device):
     t = torch.tensor([-box[0], box[1], -box[2], box[3]], dtype=torch.int64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)

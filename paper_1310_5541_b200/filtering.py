@@ -321,6 +321,7 @@ def fused_track(frames, cfg: FilterConfig, rng, method, grid=None, placement=0, 
     c.use_graph = 1 if use_graph else 0
     c.threshold_fraction = cfg.resampling.threshold_fraction
     c.scheme = 1 if cfg.resampling.scheme == "multinomial" else 0
+    c.weighted_com = 1 if (method == 1 and getattr(cfg, "weighted_com", False)) else 0
     dev = dev_frames.device
     est = torch.empty((k, 5), dtype=torch.float64, device=dev)
     ess = torch.empty(k, dtype=torch.float64, device=dev)

@@ -340,3 +340,42 @@ def test_resample_resets_weights(cuda):
     deg = pc.ParticleSet(np.column_stack([np.arange(3.0), np.zeros((3, 4))]), [1.0, 0.0, 0.0])
     out = pc.resample(deg, pc.ResampleConfig(), pc.PhiloxRng(2))
     assert np.all(out.states[:, 0] == 0.0)
+
+
+# --- make_dummy (binning.py:129-154), device float64 in the reference's orders ------
+def test_make_dummy_known_answers(cuda):
+    # test_binning.py:97-126
+    members = [pc.StateVector(0.2, 0.2, 1.0, -1.0, 10.0), pc.StateVector(0.8, 0.8, 1.0, -1.0, 10.0)]
+    d = pc.make_dummy(members, (0, 1, 0, 1), pc.DummyPlacement.CENTER_OF_MASS)
+    assert d == pc.StateVector(0.5, 0.5, 1.0, -1.0, 10.0)
+    m = pc.StateVector(3.7, -1.2, 0.5, 0.25, 7.5)
+    assert pc.make_dummy([m], (3, 4, -2, -1), pc.DummyPlacement.CENTER_OF_MASS) == m
+    d = pc.make_dummy([pc.StateVector(1.9, 3.1, 2.0, 0.0, 5.0)], (1.0, 2.0, 3.0, 4.0),
+                      pc.DummyPlacement.CELL_CENTER)
+    assert d == pc.StateVector(1.5, 3.5, 2.0, 0.0, 5.0)
+    d = pc.make_dummy([pc.StateVector(0, 0, 0, 0, 0), pc.StateVector(1, 0, 0, 0, 0)], (0, 1, 0, 1),
+                      pc.DummyPlacement.CENTER_OF_MASS, weights=[1.0, 3.0])
+    assert d.x == 0.75
+    with pytest.raises(ValueError):
+        pc.make_dummy([], (0, 1, 0, 1), pc.DummyPlacement.CENTER_OF_MASS)
+
+
+@pytest.mark.parametrize("n", [1, 7, 100, 1000, 5000])
+def test_make_dummy_matches_reference_orders(cuda, n):
+    rng = np.random.default_rng(n)
+    rows = rng.normal(size=(n, 5)) * np.array([50, 50, 1, 1, 10]) + np.array([100, 80, 0, 0, 20])
+    members = [pc.StateVector(*r) for r in rows]
+    d = pc.make_dummy(members, (0, 1, 0, 1), pc.DummyPlacement.CENTER_OF_MASS)
+    # np.add.reduceat over axis 0 / n (binning.py:144-147), bit for bit
+    want = np.add.reduceat(rows, [0], axis=0)[0] / n
+    assert np.array_equal(d.as_array(), want)
+    w = rng.uniform(0.1, 2.0, n)
+    dw = pc.make_dummy(members, (0, 1, 0, 1), pc.DummyPlacement.CENTER_OF_MASS, weights=w)
+    np.testing.assert_allclose(dw.as_array(), (w @ rows) / w.sum(), rtol=1e-13)
+    # the weight total is numpy's pairwise sum bit for bit: unit rows expose it
+    ones = [pc.StateVector(1.0, 1.0, 1.0, 1.0, 1.0)] * n
+    du = pc.make_dummy(ones, (0, 1, 0, 1), pc.DummyPlacement.CENTER_OF_MASS, weights=w)
+    seq = 0.0
+    for v in w:
+        seq += v
+    assert du.x == seq / w.sum()

@@ -500,3 +500,25 @@ def test_capacity_fallback_with_prior_weights(cuda):
     assert np.array_equal(a.estimates, b.estimates)
     assert np.array_equal(a.ess, b.ess)
     assert a.likelihood_evals == b.likelihood_evals > 8192
+
+
+@pytest.mark.parametrize("frac", [1.0, 0.3])
+def test_fused_weighted_com_equals_general(cuda, frac):
+    """pc_sis_step(weighted_com=True) (binning.py:160-165,186) in the fused
+    loop: with uniform prior weights (every frame resampled) the weighted
+    centre of mass is computed in the bins kernel from the exact cell sums;
+    frames whose particles carry unequal prior weights (ESS threshold < 1)
+    hand the track to the general path. Either way == the general driver."""
+    frames, truth, init, dyn = _c1_like(n=3000, k=10)
+    res = pc.ResampleConfig(frac, "systematic")
+    grid = pc.BinGrid.pixel_aligned(64, 64, 2)
+    cfg = pc.PcFilterConfig(3000, init, dyn, res, _lik(), grid=grid, weighted_com=True)
+    a = pc.pcsir_track(frames, cfg, pc.PhiloxRng(8), fused=True)
+    cfg2 = pc.PcFilterConfig(3000, init, dyn, res, _lik(), grid=grid, weighted_com=True)
+    b = pc.pcsir_track(frames, cfg2, pc.PhiloxRng(8), fused=False)
+    assert b.path == "general"
+    if frac == 1.0:
+        assert a.path == "fused"
+    assert np.array_equal(a.estimates, b.estimates)
+    assert np.array_equal(a.ess, b.ess)
+    assert np.array_equal(a.resampled, b.resampled)
