@@ -105,12 +105,13 @@ __global__ void k_dummies(const u64* __restrict__ sums, const i64* __restrict__ 
 
 // ---- make_dummy (binning.py:129-154): one cell's representative state ----
 // float64 members (n, 5) row-major, as the reference. One thread, in the
-// reference's summation orders: the unweighted mean is np.add.reduceat over
-// axis 0 (rows added one after another, then / n); the weight total is
-// numpy's pairwise sum (blocks of 8 partial sums below 128 elements,
-// recursive halving above), the weighted numerator w @ rows is accumulated
-// row by row (BLAS order is implementation-defined; exact for exact data).
-__device__ double np_pairwise_sum(const double* a, i64 n) {
+// reference's summation orders: np.add.reduceat(rows, [0], axis=0) is the
+// first row plus numpy's pairwise sum of the remaining rows per column; the
+// weight total w.sum() is the pairwise sum of w (blocks of 8 partial sums up
+// to 128 elements, recursive halving above); the weighted numerator w @ rows
+// is accumulated row by row (BLAS order is implementation-defined; exact for
+// exact data).
+__device__ double np_pairwise_sum(const double* a, i64 n, i64 stride = 1) {
   // iterative post-order form of numpy's recursive pairwise_sum
   // (PW_BLOCKSIZE 128, 8 partial sums); ops: 0 = sum a range, 1 = add the
   // two most recent results (left + right)
@@ -129,20 +130,20 @@ __device__ double np_pairwise_sum(const double* a, i64 n) {
       vals[vp++] = __dadd_rn(l, r);
       continue;
     }
-    const double* x = a + lo;
+    const double* x = a + lo * stride;
     if (m < 8) {
-      double res = 0.0;
-      for (i64 i = 0; i < m; ++i) res = __dadd_rn(res, x[i]);
+      double res = -0.0;
+      for (i64 i = 0; i < m; ++i) res = __dadd_rn(res, x[i * stride]);
       vals[vp++] = res;
     } else if (m <= 128) {
       double r[8];
-      for (int q = 0; q < 8; ++q) r[q] = x[q];
+      for (int q = 0; q < 8; ++q) r[q] = x[q * stride];
       i64 i;
       for (i = 8; i < m - (m % 8); i += 8)
-        for (int q = 0; q < 8; ++q) r[q] = __dadd_rn(r[q], x[i + q]);
+        for (int q = 0; q < 8; ++q) r[q] = __dadd_rn(r[q], x[(i + q) * stride]);
       double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                              __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-      for (; i < m; ++i) res = __dadd_rn(res, x[i]);
+      for (; i < m; ++i) res = __dadd_rn(res, x[i * stride]);
       vals[vp++] = res;
     } else {
       i64 n2 = m / 2;
@@ -167,11 +168,10 @@ __global__ void k_make_dummy(const double* __restrict__ rows, i64 n, const doubl
     const double den = np_pairwise_sum(w, n);
     for (int c = 0; c < 5; ++c) mean[c] = __ddiv_rn(num[c], den);
   } else {
-    double acc[5];
-    for (int c = 0; c < 5; ++c) acc[c] = rows[c];
-    for (i64 i = 1; i < n; ++i)
-      for (int c = 0; c < 5; ++c) acc[c] = __dadd_rn(acc[c], rows[i * 5 + c]);
-    for (int c = 0; c < 5; ++c) mean[c] = __ddiv_rn(acc[c], (double)n);
+    for (int c = 0; c < 5; ++c) {
+      const double acc = (n == 1) ? rows[c] : __dadd_rn(rows[c], np_pairwise_sum(rows + 5 + c, n - 1, 5));
+      mean[c] = __ddiv_rn(acc, (double)n);
+    }
   }
   if (placement == 1) {   // cell centre (binning.py:150-153)
     mean[0] = __ddiv_rn(__dadd_rn(x_lo, x_hi), 2.0);

@@ -12,9 +12,6 @@
 #include <string>
 #include <vector>
 
-#include <cub/device/device_radix_sort.cuh>
-#include <cub/device/device_run_length_encode.cuh>
-#include <cub/device/device_scan.cuh>
 
 #include "pcs_bin.cuh"
 #include "pcs_synth.cuh"
@@ -23,6 +20,7 @@
 #include "pcs_state.cuh"
 #include "pcs_multi.cuh"
 #include "pcs_shard.cuh"
+#include "pcs_sort.cuh"
 #include "pcs_track.cuh"
 #include "pcs_weights.cuh"
 
@@ -136,6 +134,9 @@ enum Slot {
   SL_TR_LLTAB,
   SL_TR_CDF,
   SL_TR_SUB,
+  SL_SORT_KEYS2,
+  SL_SORT_IDX2,
+  SL_SCAN,
   SL_COUNT
 };
 
@@ -460,6 +461,21 @@ int pcs_loglik(const float* pixels, int64_t H, int64_t W, const float* xs, const
 // ---------------------------------------------------------------------------
 // partition / dummies (general sort path)
 // ---------------------------------------------------------------------------
+// exclusive scan of n int32 in place: block partials, then the block totals
+// scanned recursively (tmp holds every level's totals) and added back
+static int scan_excl_i32(int* a, i64 n, int* tmp, cudaStream_t st) {
+  const i64 nb = ceil_div(n, (i64)SC_BLOCK);
+  k_scan_blocks<<<(unsigned)nb, SC_THREADS, 0, st>>>(a, n, tmp);
+  PCS_LAUNCH_CHECK();
+  if (nb > 1) {
+    int r = scan_excl_i32(tmp, nb, tmp + nb, st);
+    if (r) return r;
+    k_scan_add<<<(unsigned)std::min<i64>(ceil_div(n, (i64)256), 65535), 256, 0, st>>>(a, n, tmp);
+    PCS_LAUNCH_CHECK();
+  }
+  return PCS_OK;
+}
+
 int pcs_partition(pcs_ctx* ctx, const float* states, int64_t ld, int64_t n,
                   const pcs_grid_t* grid, uint64_t* flat, int32_t* order, int32_t* bin_of,
                   uint64_t* unique, int64_t* starts, int64_t* counts, int64_t* m_out,
@@ -471,47 +487,65 @@ int pcs_partition(pcs_ctx* ctx, const float* states, int64_t ld, int64_t n,
   PCS_CHECK_ARG(n >= 1 && n < INT_MAX && ld >= n, "n out of range");
   cudaStream_t st = S(stream);
   Grid g = to_grid(grid);
-  u64* keys_sorted;
-  int* idx;
-  int* head;
-  int* incl;
-  i64* nruns;
+  // hand-written stable LSD radix sort (pcs_sort.cuh) of (flat id, index)
+  // pairs over the bits of the largest flat id, then the run partition
+  u64 *ka, *kb;
+  int *va, *vb, *incl, *scan_tmp;
   u32* flags;
-  PCS_SCRATCH(SL_SORT_KEYS, n * sizeof(u64), keys_sorted);
-  PCS_SCRATCH(SL_SORT_IDX, n * sizeof(int), idx);
-  PCS_SCRATCH(SL_HEAD, n * sizeof(int), head);
-  PCS_SCRATCH(SL_INCL, n * sizeof(int), incl);
-  PCS_SCRATCH(SL_NRUNS, 64, nruns);
+  const i64 ntiles = ceil_div(n, (i64)RS8_TILE);
+  PCS_SCRATCH(SL_SORT_KEYS, n * sizeof(u64), ka);
+  PCS_SCRATCH(SL_SORT_KEYS2, n * sizeof(u64), kb);
+  PCS_SCRATCH(SL_SORT_IDX, n * sizeof(int), va);
+  PCS_SCRATCH(SL_SORT_IDX2, n * sizeof(int), vb);
+  PCS_SCRATCH(SL_INCL, std::max<i64>(n, 256 * ntiles) * sizeof(int), incl);
+  PCS_SCRATCH(SL_SCAN, (ceil_div(std::max<i64>(n, 256 * ntiles), (i64)SC_BLOCK - 1) + 64) * sizeof(int),
+              scan_tmp);
   PCS_SCRATCH(SL_FLAGS, 64, flags);
   PCS_CUDA_TRY(cudaMemsetAsync(flags, 0, 4, st));
-  int gr = grid_for(n, 256, ctx->sms);
-  k_cell_keys<<<gr, 256, 0, st>>>(states, ld, n, g, (u64*)flat, idx, flags);
+  const int gr = grid_for(n, 256, ctx->sms);
+  k_cell_keys<<<gr, 256, 0, st>>>(states, ld, n, g, ka, va, flags);
   PCS_LAUNCH_CHECK();
-  // key bits = bits of (n_cols*n_rows - 1)
-  u64 maxkey = (u64)grid->n_cols * (u64)grid->n_rows - 1ull;
-  int end_bit = maxkey ? 64 - clz64(maxkey) : 1;
-  size_t tb1 = 0, tb2 = 0, tb3 = 0, tb4 = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, tb1, (const u64*)flat, keys_sorted, (const int*)idx,
-                                  (int*)order, (int)n, 0, end_bit, st);
-  cub::DeviceRunLengthEncode::Encode(nullptr, tb2, (const u64*)keys_sorted, (u64*)unique,
-                                     (i64*)counts, nruns, (int)n, st);
-  cub::DeviceScan::ExclusiveSum(nullptr, tb3, (const i64*)counts, (i64*)starts, (int)n, st);
-  cub::DeviceScan::InclusiveSum(nullptr, tb4, (const int*)head, incl, (int)n, st);
-  size_t tb = std::max(std::max(tb1, tb2), std::max(tb3, tb4));
-  void* temp;
-  PCS_SCRATCH(SL_CUB, tb, temp);
-  PCS_CUDA_TRY(cub::DeviceRadixSort::SortPairs(temp, tb1, (const u64*)flat, keys_sorted,
-                                               (const int*)idx, (int*)order, (int)n, 0, end_bit, st));
-  PCS_CUDA_TRY(cub::DeviceRunLengthEncode::Encode(temp, tb2, (const u64*)keys_sorted,
-                                                  (u64*)unique, (i64*)counts, nruns, (int)n, st));
-  i64 m = 0;
-  PCS_CUDA_TRY(cudaMemcpyAsync(&m, nruns, sizeof(i64), cudaMemcpyDeviceToHost, st));
+  const u64 maxkey = (u64)grid->n_cols * (u64)grid->n_rows - 1ull;
+  const int end_bit = maxkey ? 64 - clz64(maxkey) : 1;
+  const int passes = (end_bit + 7) / 8;
+  for (int ps = 0; ps < passes; ++ps) {
+    k_radix_hist<<<(unsigned)ntiles, RS8_THREADS, 0, st>>>(ka, n, 8 * ps, ntiles, incl);
+    PCS_LAUNCH_CHECK();
+    int r = scan_excl_i32(incl, 256 * ntiles, scan_tmp, st);
+    if (r) return r;
+    // the last pass writes the caller's order array directly
+    u64* kd = (ps == passes - 1) ? (u64*)flat : kb;
+    int* vd = (ps == passes - 1) ? (int*)order : vb;
+    k_radix_scatter<<<(unsigned)ntiles, RS8_THREADS, 0, st>>>(ka, va, kd, vd, n, 8 * ps, ntiles,
+                                                              incl);
+    PCS_LAUNCH_CHECK();
+    if (ps < passes - 1) {
+      std::swap(ka, kb);
+      std::swap(va, vb);
+    }
+  }
+  // flat (the caller's array) now holds the sorted keys: rebuild the
+  // per-particle flat ids afterwards (binning.py:105 returns them unsorted)
+  const u64* sorted = (const u64*)flat;
+  u64* sorted_keep = kb;   // copy of the sorted keys (flat is overwritten below)
+  PCS_CUDA_TRY(cudaMemcpyAsync(sorted_keep, sorted, n * sizeof(u64), cudaMemcpyDeviceToDevice, st));
+  k_key_heads<<<gr, 256, 0, st>>>(sorted_keep, n, incl);
+  PCS_LAUNCH_CHECK();
+  int r2 = scan_excl_i32(incl, n, scan_tmp, st);
+  if (r2) return r2;
+  k_runs<<<gr, 256, 0, st>>>(sorted_keep, order, n, incl, (u64*)unique, (i64*)starts, bin_of);
+  PCS_LAUNCH_CHECK();
+  k_cell_keys<<<gr, 256, 0, st>>>(states, ld, n, g, (u64*)flat, va, flags);   // unsorted ids
+  PCS_LAUNCH_CHECK();
+  int last_rank = 0;
+  u64 last2[2] = {0, 0};
+  PCS_CUDA_TRY(cudaMemcpyAsync(&last_rank, incl + (n - 1), sizeof(int), cudaMemcpyDeviceToHost, st));
+  PCS_CUDA_TRY(cudaMemcpyAsync(last2, sorted_keep + (n >= 2 ? n - 2 : 0), (n >= 2 ? 2 : 1) * sizeof(u64),
+                               cudaMemcpyDeviceToHost, st));
   PCS_CUDA_TRY(cudaStreamSynchronize(st));
-  PCS_CUDA_TRY(cub::DeviceScan::ExclusiveSum(temp, tb3, (const i64*)counts, (i64*)starts, (int)m, st));
-  k_run_heads<<<gr, 256, 0, st>>>(keys_sorted, n, head);
-  PCS_LAUNCH_CHECK();
-  PCS_CUDA_TRY(cub::DeviceScan::InclusiveSum(temp, tb4, (const int*)head, incl, (int)n, st));
-  k_scatter_bin_of<<<gr, 256, 0, st>>>(incl, order, n, bin_of);
+  const bool last_head = (n == 1) || (last2[1] != last2[0]);
+  const i64 m = (i64)last_rank + (last_head ? 1 : 0);
+  k_run_counts<<<grid_for(m, 256, ctx->sms), 256, 0, st>>>((const i64*)starts, m, n, (i64*)counts);
   PCS_LAUNCH_CHECK();
   u32 hflags = 0;
   PCS_CUDA_TRY(cudaMemcpyAsync(&hflags, flags, 4, cudaMemcpyDeviceToHost, st));

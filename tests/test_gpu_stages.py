@@ -225,6 +225,31 @@ def test_partition_large_against_oracle(cuda):
         assert np.array_equal(d.cpu().numpy(), orc.dummies_exact(host, bin_of, counts))
 
 
+@pytest.mark.parametrize("cell,n", [(1e-5, 3_000_000), (0.25, 2_500_000), (64.0, 1_000_000)])
+def test_partition_radix_sort_against_numpy(cuda, cell, n):
+    """The hand-written stable LSD radix sort (pcs_sort.cuh) behind the per-step
+    partition: 46-bit keys (1e-5 px cells, 6 passes), 26-bit keys, and a
+    few heavily shared keys (64 px cells: long runs, stability across tiles);
+    order, unique, starts, counts and the per-particle flat ids equal numpy's
+    stable argsort / unique (binning.py:97-112)."""
+    rng = np.random.default_rng(int(n))
+    host = np.stack([rng.uniform(0, 255, n), rng.uniform(0, 255, n), rng.normal(0, 1, n),
+                     rng.normal(0, 1, n), rng.uniform(0, 40, n)]).astype(np.float32)
+    host[:2, : n // 4] = host[:2, :1]          # a quarter of the particles share one cell
+    soa = torch.from_numpy(host).cuda()
+    cells = int(round(256 / cell))
+    grid = pc.BinGrid(-0.5, -0.5, cell, cell, cells, cells)
+    part = binning.partition_device(soa, grid)
+    flat, order, unique, starts, counts = orc.partition(host.T.astype(np.float64), _grid_tuple(grid))
+    assert np.array_equal(part.flat.cpu().numpy().view(np.uint64).astype(np.int64), flat)
+    assert np.array_equal(part.order.cpu().numpy(), order)
+    assert np.array_equal(part.unique.cpu().numpy().view(np.uint64).astype(np.int64), unique)
+    assert np.array_equal(part.starts.cpu().numpy(), starts)
+    assert np.array_equal(part.counts.cpu().numpy(), counts)
+    bin_of = orc.bin_of_from_partition(n, order, counts)
+    assert np.array_equal(part.bin_of.cpu().numpy(), bin_of)
+
+
 # --- weights, estimate, ESS, resampling (filtering.py:75-114) -----------------------------
 @pytest.mark.parametrize("k", ["halves", "zeros", "tiny", "rand1000", "peaked"])
 def test_normalize_golden(cuda, k):
@@ -364,9 +389,11 @@ def test_make_dummy_known_answers(cuda):
 def test_make_dummy_matches_reference_orders(cuda, n):
     rng = np.random.default_rng(n)
     rows = rng.normal(size=(n, 5)) * np.array([50, 50, 1, 1, 10]) + np.array([100, 80, 0, 0, 20])
+    rows[:, 4] = np.abs(rows[:, 4])
     members = [pc.StateVector(*r) for r in rows]
     d = pc.make_dummy(members, (0, 1, 0, 1), pc.DummyPlacement.CENTER_OF_MASS)
-    # np.add.reduceat over axis 0 / n (binning.py:144-147), bit for bit
+    # np.add.reduceat over axis 0 / n (binning.py:144-147), bit for bit (numpy adds the
+    # first row to the pairwise sum of the others, per column)
     want = np.add.reduceat(rows, [0], axis=0)[0] / n
     assert np.array_equal(d.as_array(), want)
     w = rng.uniform(0.1, 2.0, n)
