@@ -153,6 +153,20 @@ int pcs_partition(pcs_ctx* ctx, const float* states, int64_t ld, int64_t n,
                   void* stream);
 /* dummies[c*ldd + b] (float32) for the m occupied bins. placement 0 = CoM,
  * 1 = cell centre. prior_w (float32, may be NULL) selects weighted CoM. */
+/* Mid-point approximation bound study (bounds.py:116-180), built-in fields
+ * in parametric form: kind 0 = a x^2 + b y^2 + c x + d y + e (params a..e),
+ * 1 = sin(x) sin(y), 2 = i0 exp(-((x-x0)^2+(y-y0)^2)/(2 s2)) + i_bg (params
+ * i0, i_bg, x0, y0, s2); params: host double[6].
+ * pcs_bounds_deriv_max: max |f_xx|, max |f_yy| over np.linspace grids
+ *   (derivative_maxima's sampling), out2: host double[2].
+ * pcs_bounds_midpoint: signed mid-point error per cell (row-major n_rows x
+ *   n_cols) by q x q Gauss-Legendre quadrature; edges / nodes / weights /
+ *   cell_err are device float64 arrays. */
+int pcs_bounds_deriv_max(int32_t kind, const double* params, double x_lo, double x_hi, int64_t nx,
+                         double y_lo, double y_hi, int64_t ny, double* out2, void* stream);
+int pcs_bounds_midpoint(int32_t kind, const double* params, const double* x_edges, int64_t n_cols,
+                        const double* y_edges, int64_t n_rows, const double* nodes,
+                        const double* weights, int32_t q, double* cell_err, void* stream);
 /* make_dummy (binning.py:129-154): the representative state of ONE cell's
  * members. members: device float64 (n, 5) row-major; weights: device
  * float64 (n,) or NULL; placement 0 centre of mass, 1 cell centre (bounds =

@@ -122,6 +122,10 @@ _SIGNATURES = [
     ("pcs_track_launches_per_step", c_int32, [c_void_p]),
     ("pcs_track_debug", c_int32, [c_void_p, c_void_p, c_void_p]),
     ("pcs_track_info", c_int32, [c_void_p, c_void_p, c_int32, c_void_p]),
+    ("pcs_bounds_deriv_max", c_int32, [c_int32, c_void_p, c_double, c_double, c_int64, c_double,
+                                       c_double, c_int64, c_void_p, c_void_p]),
+    ("pcs_bounds_midpoint", c_int32, [c_int32, c_void_p, c_void_p, c_int64, c_void_p, c_int64,
+                                      c_void_p, c_void_p, c_int32, c_void_p, c_void_p]),
     ("pcs_make_dummy", c_int32, [c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                  c_void_p]),
     ("pcs_track_states", c_int32, [c_void_p, P(c_void_p), P(c_int64)]),

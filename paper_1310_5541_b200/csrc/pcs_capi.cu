@@ -21,6 +21,7 @@
 #include "pcs_multi.cuh"
 #include "pcs_shard.cuh"
 #include "pcs_sort.cuh"
+#include "pcs_bounds.cuh"
 #include "pcs_track.cuh"
 #include "pcs_weights.cuh"
 
@@ -578,6 +579,49 @@ int pcs_dummies(pcs_ctx* ctx, const float* states, int64_t ld, int64_t n, const 
   PCS_LAUNCH_CHECK();
   k_dummies<<<grid_for(m, 256, ctx->sms), 256, 0, st>>>(sums, (const i64*)counts, (const u64*)unique, m, to_grid(grid),
                                                          placement, prior_w ? 1 : 0, dummies, ldd);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+static int to_field(int32_t kind, const double* params, FieldDev* F) {
+  PCS_CHECK_ARG(params && kind >= 0 && kind <= 2, "field kind must be 0 (polynomial), 1 (sinsin) or 2 (gaussian)");
+  F->kind = kind;
+  for (int i = 0; i < 6; ++i) F->p[i] = params[i];
+  if (kind == 2) PCS_CHECK_ARG(params[4] > 0.0, "gaussian field needs sigma^2 > 0");
+  return PCS_OK;
+}
+
+int pcs_bounds_deriv_max(int32_t kind, const double* params, double x_lo, double x_hi, int64_t nx,
+                         double y_lo, double y_hi, int64_t ny, double* out2, void* stream) {
+  FieldDev F;
+  int r = to_field(kind, params, &F);
+  if (r) return r;
+  PCS_CHECK_ARG(out2 && nx >= 1 && ny >= 1, "bad arguments");
+  unsigned long long* d;
+  cudaStream_t st = S(stream);
+  PCS_CUDA_TRY(cudaMallocAsync((void**)&d, 16, st));
+  PCS_CUDA_TRY(cudaMemsetAsync(d, 0, 16, st));
+  k_deriv_max<<<grid_for(nx * ny, 256, 148, 8), 256, 0, st>>>(F, x_lo, x_hi, nx, y_lo, y_hi, ny, d);
+  PCS_LAUNCH_CHECK();
+  unsigned long long h[2];
+  PCS_CUDA_TRY(cudaMemcpyAsync(h, d, 16, cudaMemcpyDeviceToHost, st));
+  PCS_CUDA_TRY(cudaFreeAsync(d, st));
+  PCS_CUDA_TRY(cudaStreamSynchronize(st));
+  memcpy(out2, h, 16);
+  return PCS_OK;
+}
+
+int pcs_bounds_midpoint(int32_t kind, const double* params, const double* x_edges, int64_t n_cols,
+                        const double* y_edges, int64_t n_rows, const double* nodes,
+                        const double* weights, int32_t q, double* cell_err, void* stream) {
+  FieldDev F;
+  int r = to_field(kind, params, &F);
+  if (r) return r;
+  PCS_CHECK_ARG(x_edges && y_edges && nodes && weights && cell_err && n_cols >= 1 && n_rows >= 1 &&
+                q >= 1, "bad arguments");
+  const i64 cells = n_cols * n_rows;
+  k_midpoint_error<<<(unsigned)std::min<i64>(ceil_div(cells, (i64)8), 148 * 64), 256, 0, S(stream)>>>(
+      F, x_edges, n_cols, y_edges, n_rows, nodes, weights, q, cell_err);
   PCS_LAUNCH_CHECK();
   return PCS_OK;
 }

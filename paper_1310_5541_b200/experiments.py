@@ -354,3 +354,35 @@ def likelihood_benchmark(repeats=5, seed=0, report=print):
         out[label] = n / best
         report(f"{label:>18s} {'cuda':>9s}: {n / best:12.0f} evals/s")
     return out
+
+
+# ---------------------------------------------------------------------------
+# appendix bound study (experiments.py:362-388) on the device
+# ---------------------------------------------------------------------------
+BOUND_CELL_SIZES = (1.0, 0.5, 0.25, 0.125)
+BOUND_DOMAINS = {
+    "quadratic": (0.0, 4.0, 0.0, 4.0),
+    "gaussian": (-4.0, 4.0, -4.0, 4.0),
+    "sinsin": (0.0, 4.0, 0.0, 4.0),
+}
+
+
+def run_bounds_study(cell_sizes=BOUND_CELL_SIZES, fields=None) -> dict:
+    """True mid-point approximation error versus both bounds:
+    {field name: [(cell size, true error, rect bound, square bound)]} for
+    uniform square partitions of each field's standard domain."""
+    from .bounds import DomainPartition, builtin_fields, midpoint_error, rect_bound, square_bound
+    fields = fields if fields is not None else builtin_fields()
+    results = {}
+    for name, fld in fields.items():
+        domain = BOUND_DOMAINS[name]
+        rows = []
+        for l in cell_sizes:
+            n_cols = int(round((domain[1] - domain[0]) / l))
+            n_rows = int(round((domain[3] - domain[2]) / l))
+            part = DomainPartition.uniform(domain, n_cols, n_rows)
+            rows.append((l, midpoint_error(fld, part), rect_bound(fld, part),
+                         square_bound(fld, l, domain)))
+        results[name] = rows
+    return results
+

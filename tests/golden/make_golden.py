@@ -269,7 +269,44 @@ def gen_synth():
     return {"states": states, "frames": frames, "sigma": 1.5, "bg": 10.0}
 
 
+def gen_bounds():
+    """bounds.py:121-180 and experiments.py:370-388 on the reference."""
+    from pcsir import bounds as rbd
+    from pcsir import experiments as rex
+    out = {}
+    fields = {"quadratic": rbd.quadratic_field(), "linear": rbd.linear_field(),
+              "sinsin": rbd.sinsin_field(), "gaussian": rbd.gaussian_spot_field(),
+              "gauss2": rbd.gaussian_spot_field(1.5, 20.0, 10.0, (0.3, -0.2))}
+    domains = {"quadratic": (0.0, 4.0, 0.0, 4.0), "linear": (0.0, 1.0, 0.0, 1.0),
+               "sinsin": (0.0, np.pi, 0.0, np.pi), "gaussian": (-4.0, 4.0, -4.0, 4.0),
+               "gauss2": (-3.0, 5.0, -4.0, 2.0)}
+    rng = np.random.default_rng(5)
+    for name, fld in fields.items():
+        dom = domains[name]
+        for cells in ((4, 4), (7, 3), (16, 16), (33, 20)):
+            part = rbd.DomainPartition.uniform(dom, *cells)
+            key = f"{name}_{cells[0]}x{cells[1]}"
+            out[f"{key}_dmax"] = np.array(rbd.derivative_maxima(fld, part))
+            out[f"{key}_rect"] = np.array(rbd.rect_bound(fld, part))
+            out[f"{key}_mid64"] = np.array(rbd.midpoint_error(fld, part))
+            out[f"{key}_mid16"] = np.array(rbd.midpoint_error(fld, part, quad_points=16))
+        xe = np.sort(np.concatenate(([dom[0], dom[1]], rng.uniform(dom[0], dom[1], 9))))
+        ye = np.sort(np.concatenate(([dom[2], dom[3]], rng.uniform(dom[2], dom[3], 6))))
+        part = rbd.DomainPartition(xe, ye)
+        out[f"{name}_irr_x"], out[f"{name}_irr_y"] = xe, ye
+        out[f"{name}_irr_dmax"] = np.array(rbd.derivative_maxima(fld, part))
+        out[f"{name}_irr_rect"] = np.array(rbd.rect_bound(fld, part))
+        out[f"{name}_irr_mid64"] = np.array(rbd.midpoint_error(fld, part))
+    for name, rows in rex.run_bounds_study().items():
+        out[f"study_{name}"] = np.array(rows)
+    return out
+
+
 def main():
+    if len(sys.argv) > 1:   # regenerate the named fixtures only
+        for name in sys.argv[1:]:
+            np.savez_compressed(HERE / f"{name}.npz", **globals()[f"gen_{name}"]())
+        return
     np.savez_compressed(HERE / "ssd.npz", **gen_ssd())
     np.savez_compressed(HERE / "partition.npz", **gen_partition())
     np.savez_compressed(HERE / "filtering.npz", **gen_filtering())

@@ -114,3 +114,17 @@ def test_product_path_fails_loudly_without_gpu():
         pc.init_particle_set(10, pc.InitSpec(pc.StateVector(0, 0, 0, 0, 1)), 0)
     with pytest.raises(RuntimeError, match="CUDA"):
         kernels.spot_window_ssd(np.zeros((4, 4)), np.zeros(1), np.zeros(1), np.zeros(1), 1.0, 0, 1)
+
+
+def test_bounds_partition_host_semantics():
+    # test_bounds.py:131-144 (partition validation / geometry, host only)
+    from paper_1310_5541_b200 import bounds as bd
+    with pytest.raises(ValueError):
+        bd.DomainPartition(np.array([0.0, 0.0, 1.0]), np.array([0.0, 1.0]))
+    with pytest.raises(ValueError):
+        bd.DomainPartition(np.array([0.0]), np.array([0.0, 1.0]))
+    part = bd.DomainPartition(np.array([0.0, 1.0, 3.0]), np.array([0.0, 2.0]))
+    assert part.n_cells == 2
+    assert np.array_equal(part.cell_widths, [1.0, 2.0])
+    assert np.array_equal(part.cell_heights, [2.0])
+    assert part.domain == (0.0, 3.0, 0.0, 2.0)
