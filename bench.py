@@ -233,7 +233,7 @@ def c_cfg(pc, _lib, cfg, grid, seed, use_graph=True):
     c.n_particles = cfg.n_particles
     c.init = cfg.init.to_c()
     c.dyn = cfg.dynamics.to_c()
-    c.spot = cfg.likelihood.spot_c()
+    c.spot = cfg.likelihood.spot_c(cells=grid is not None)
     if grid is not None:
         c.grid = grid.to_c()
     c.seed = seed

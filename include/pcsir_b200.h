@@ -54,8 +54,11 @@ typedef struct pcs_dynamics_t {
 typedef struct pcs_spot_t {
   double sigma_psf, i_bg, sigma_xi;
   int32_t halfwidth;
-  int32_t model;
+  int32_t model;         /* 0 gauss-ssd, 1 erf-poisson, 2 midpoint4x4-poisson;
+                            | PCS_LIK_F64: Poisson models in float64 (the pcSIR
+                            cell form; the fused pcSIR loop always uses it) */
 } pcs_spot_t;
+#define PCS_LIK_F64 16
 
 /* InitSpec (state.py:140-161): mode 0 point, 1 uniform(width), 2 gauss(sigma) */
 typedef struct pcs_init_t {

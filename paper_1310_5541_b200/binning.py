@@ -221,7 +221,7 @@ def pc_sis_step(pset: ParticleSet, frame, lik, dyn, grid: BinGrid, placement: Du
     if weighted_com:
         prior_w = pset.weights_f32().contiguous()
     dummies = dummy_states_device(states, grid, part, placement, prior_w)
-    cell_ll = _evaluate_loglik(lik, dummies, frame)
+    cell_ll = _evaluate_loglik(lik, dummies, frame, cells=True)
     logw = _weight_update(pset, cell_ll, part.bin_of)
     _check_not_degenerate(logw)
     return ParticleSet.from_device(states, logw=logw, timestep=pset.timestep + 1), part.m

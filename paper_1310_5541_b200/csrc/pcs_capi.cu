@@ -71,6 +71,7 @@ struct TrackState {
   static constexpr int MAX_LAUNCHES = 12;
   const char* names[MAX_LAUNCHES] = {};   // kernel of each launch of a frame
   int prop_grid = 0;
+  int cells_grid = 0;    // k_pc_cells CTAs (8 warps each, one warp per occupied cell)
   int maxs = 0;
   i64 k = 0;             // host mirror of the frame counter
   cudaGraphExec_t exec = nullptr;
@@ -193,9 +194,15 @@ static Spot to_spot(const pcs_spot_t* s) {
   r.inv2s2 = (float)(1.0 / (2.0 * s->sigma_psf * s->sigma_psf));
   r.inv_2sxi2 = 1.0 / (2.0 * s->sigma_xi * s->sigma_xi);
   r.hw = s->halfwidth;
-  r.model = s->model;
+  r.model = s->model & 15;
+  r.f64 = (s->model & PCS_LIK_F64) ? 1 : 0;
   r.erf_scale = (float)(s->sigma_psf * 1.2533141373155002512078826);  // sigma*sqrt(pi/2)
   r.inv_sqrt2s = (float)(1.0 / (1.4142135623730950488 * s->sigma_psf));
+  r.sigma64 = s->sigma_psf;
+  r.bg64 = s->i_bg;
+  r.inv2s2_64 = 1.0 / (2.0 * s->sigma_psf * s->sigma_psf);
+  r.erf_scale64 = s->sigma_psf * 1.2533141373155002512078826;
+  r.inv_sqrt2s64 = 1.0 / (1.4142135623730950488 * s->sigma_psf);
   return r;
 }
 
@@ -212,8 +219,9 @@ static int check_spot(const pcs_spot_t* s) {
   PCS_CHECK_ARG(s->sigma_psf > 0, "sigma_psf must be > 0");
   PCS_CHECK_ARG(s->sigma_xi > 0, "sigma_xi must be > 0");
   PCS_CHECK_ARG(s->halfwidth >= 0, "halfwidth must be >= 0");
-  PCS_CHECK_ARG(s->model >= 0 && s->model <= 2, "unknown likelihood model");
-  PCS_CHECK_ARG(s->model == 0 || s->i_bg > 0, "Poisson likelihood needs i_bg > 0");
+  const int m = s->model & ~PCS_LIK_F64;
+  PCS_CHECK_ARG(m >= 0 && m <= 2, "unknown likelihood model");
+  PCS_CHECK_ARG(m == 0 || s->i_bg > 0, "Poisson likelihood needs i_bg > 0");
   PCS_CHECK_ARG(s->i_bg >= 0, "i_bg must be >= 0");
   return PCS_OK;
 }
@@ -835,13 +843,10 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
   if (T.cfg.method == 1) {
     mark("k_pc_step1");
     k_pc_step1<<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(P);
+    mark("k_pc_cells");
+    launch_pdl(k_pc_cells, T.cells_grid, CELLS_BLOCK, 0, st, P, T.bins);
     mark("k_pc_bins");
-    switch (T.maxs) {
-      case 9: launch_pdl(k_pc_bins<9>, 1, BINS_BLOCK, BINS_SMEM, st, P, T.bins); break;
-      case 11: launch_pdl(k_pc_bins<11>, 1, BINS_BLOCK, BINS_SMEM, st, P, T.bins); break;
-      case 15: launch_pdl(k_pc_bins<15>, 1, BINS_BLOCK, BINS_SMEM, st, P, T.bins); break;
-      default: launch_pdl(k_pc_bins<0>, 1, BINS_BLOCK, BINS_SMEM, st, P, T.bins);
-    }
+    launch_pdl(k_pc_bins, 1, BINS_BLOCK, 0, st, P, T.bins);
     if (T.cond) {
       // frames whose particles carry prior weights finish per particle (the
       // kernels of the other mode return at once)
@@ -907,19 +912,10 @@ static int set_attrs() {
                                     (int)sizeof(RsSmem<1>)));
   PCS_CUDA_TRY(cudaFuncSetAttribute(k_sys_resample<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)sizeof(RsSmem<2>)));
-  PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)BINS_SMEM));
-  PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<9>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)BINS_SMEM));
-  PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<11>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)BINS_SMEM));
-  PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_bins<15>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)BINS_SMEM));
   // one shared-memory carveout for every kernel of the frame: consecutive
   // kernels with different carveouts force an SM reconfiguration between them
-  const void* fns[] = {(const void*)k_pc_step1,        (const void*)k_pc_bins<0>,
-                       (const void*)k_pc_bins<9>,       (const void*)k_pc_bins<11>,
-                       (const void*)k_pc_bins<15>,      (const void*)k_scan_emit<1>,
+  const void* fns[] = {(const void*)k_pc_step1,        (const void*)k_pc_bins,
+                       (const void*)k_pc_cells,         (const void*)k_scan_emit<1>,
                        (const void*)k_scan_emit<2>,     (const void*)k_sir_propagate_lik<0>,
                        (const void*)k_sir_propagate_lik<9>, (const void*)k_sir_propagate_lik<11>,
                        (const void*)k_sir_propagate_lik<15>, (const void*)k_sir_sum,
@@ -1035,7 +1031,8 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
       ctx->table_cells = P.G;
       ctx->table_dirty = true;
     }
-    if (!ctx->occ) PCS_CUDA_TRY(cudaMalloc(&ctx->occ, MAXM * sizeof(u32) + 5 * BINS_MAXM * sizeof(float)));
+    // occupied-cell list + per-cell log-likelihood and count (k_pc_cells)
+    if (!ctx->occ) PCS_CUDA_TRY(cudaMalloc(&ctx->occ, MAXM * (sizeof(u32) + sizeof(double) + sizeof(u32))));
     if (ctx->table_dirty) {
       PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_cnt, 0, ctx->table_cells * sizeof(u32), st));
       PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_sum, 0, 5 * ctx->table_cells * 2 * sizeof(u64), st));
@@ -1050,12 +1047,8 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
     P.wtab = ctx->wtab;
     P.wfix = (u128*)(ctx->wtab + ceil_div(P.G, 4) * 4);
     P.occ = ctx->occ;
-    float* sd = (float*)(ctx->occ + MAXM);
-    T.bins.dx = sd;
-    T.bins.dy = sd + BINS_MAXM;
-    T.bins.di = sd + 2 * BINS_MAXM;
-    T.bins.cnt = (u32*)(sd + 3 * BINS_MAXM);
-    T.bins.cell = (u32*)(sd + 4 * BINS_MAXM);
+    T.bins.ll = (double*)(ctx->occ + MAXM);
+    T.bins.cnt = (u32*)(T.bins.ll + MAXM);
   }
   T.maxs = maxs_for(cfg->spot.halfwidth);
   // SIR reductions: >= 16 particles per thread (few int128 partials per atomic
@@ -1078,6 +1071,7 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
     P.sir_chunk = (n >= (i64)T.prop_grid * 8 * 2048) ? 2048 : 0;
   }
   T.s1_grid = (int)std::min<i64>((i64)ctx->sms * S1_CTAS_PER_SM, ceil_div(n, S1_TILE));
+  T.cells_grid = ctx->sms * 4;
   {
     // equal tile counts per CTA: tile = ceil(per_cta / ceil(per_cta / S1_TILE))
     const i64 per_cta = ceil_div(n, (i64)T.s1_grid);
@@ -1448,12 +1442,8 @@ int pcs_shard_import_bins(pcs_ctx* ctx, int64_t x0, int64_t y0, int64_t nx, int6
   TrackState& T = ctx->tr;
   k_shard_import<<<grid_for(nx * ny, 256, ctx->sms), 256, 0, st>>>(T.P, x0, y0, nx, ny,
                                                                   (const i64*)limbs);
-  switch (T.maxs) {
-    case 9: k_pc_bins<9><<<1, BINS_BLOCK, BINS_SMEM, st>>>(T.P, T.bins); break;
-    case 11: k_pc_bins<11><<<1, BINS_BLOCK, BINS_SMEM, st>>>(T.P, T.bins); break;
-    case 15: k_pc_bins<15><<<1, BINS_BLOCK, BINS_SMEM, st>>>(T.P, T.bins); break;
-    default: k_pc_bins<0><<<1, BINS_BLOCK, BINS_SMEM, st>>>(T.P, T.bins);
-  }
+  k_pc_cells<<<T.cells_grid, CELLS_BLOCK, 0, st>>>(T.P, T.bins);
+  k_pc_bins<<<1, BINS_BLOCK, 0, st>>>(T.P, T.bins);
   PCS_LAUNCH_CHECK();
   return PCS_OK;
 }
@@ -1567,7 +1557,7 @@ int pcs_track_info(pcs_ctx* ctx, int64_t* out, int32_t n, void* stream) {
   out[5] = P.sir_chunk;
   out[6] = h.s1_mid_flush;
   out[7] = h.max_occ;
-  out[8] = BINS_SM;
+  out[8] = MAXM;
   out[9] = S1_FLUSH_TILES;
   out[10] = T.prop_grid;
   out[11] = T.launches;

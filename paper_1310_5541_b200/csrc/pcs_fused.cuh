@@ -32,7 +32,7 @@ constexpr int S1_E = 4;                        // sorted elements per thread in 
 constexpr int S1_SUM_THREADS = S1_TILE / S1_E; // 256 threads (8 warps) sum the sorted tile
 constexpr int S1_FLUSH_TILES = 256;            // digit accumulators stay in range (see below)
 constexpr i64 TABLE_MAX = 1ll << 28;           // dense full-grid table (cells)
-constexpr int MAXM = 16384;                    // occupied cells per frame (fused)
+constexpr int MAXM = 1 << 20;                  // occupied cells per frame (fused)
 
 // Per-tile pipeline (k_pc_step1, two CTAs per SM): each CTA counting-sorts a
 // tile of 1024 particles by sub-window cell in shared memory (a native 32-bit
@@ -107,6 +107,7 @@ struct TrackCtl {
                              // prior_nonuniform by k_pc_step1 at the frame start)
   i64 frame_occ;             // pcSIR with prior weights: occupied cells of the frame
   i64 k_end;                 // frame index one past the last output row of this batch
+  i64 cell_max_ord;          // pcSIR: ordered-int64 max cell log-likelihood (k_pc_cells)
   u32 s1_mid_flush;          // diagnostics: step-1 mid-loop digit flushes (pcs_track_info)
   u32 max_occ;               // diagnostics: most occupied cells of a frame
 };
@@ -203,6 +204,7 @@ __device__ __forceinline__ void set_flag(TrackCtl* c, u32 f) {
 
 __device__ __forceinline__ void reset_frame(TrackCtl* c) {
   c->max_ll_ord = LLONG_MIN;
+  c->cell_max_ord = LLONG_MIN;
   c->n_occ = 0;
   c->wmin_bits = 0xFFFFFFFFu;
   c->wmax_bits = 0u;
@@ -688,6 +690,75 @@ __device__ __forceinline__ void tma_stage_wait(unsigned long long* bar) {
       "@!p bra TMA_WAIT_%=;\n\t}" ::"r"((u32)__cvta_generic_to_shared(bar)), "r"(1000000u) : "memory");
 }
 
+// per-cell records of the frame's occupied cells (global memory, MAXM each)
+struct BinsScratch {
+  double* ll;    // cell log-likelihood, then exp(ll - max) (k_pc_bins)
+  u32* cnt;      // members
+};
+
+// ---------------------------------------------------------------------------
+// k_pc_cells: one warp per occupied cell, all SMs — the dummy (exact mean,
+// binning.py:157-172; weighted centre of mass with uniform prior weights;
+// cell centre, :168-171) and its likelihood (binning.py:189), the Gaussian
+// SSD in the canonical float32 form (identical to SIR on one-particle
+// cells), the Poisson models in float64 (pcs_lik.cuh loglik_poisson64_warp).
+// Publishes ll and count per cell and the frame's largest log-likelihood.
+// ---------------------------------------------------------------------------
+constexpr int CELLS_BLOCK = 256;
+
+__global__ void __launch_bounds__(CELLS_BLOCK) k_pc_cells(TrackParams P, BinsScratch Sd) {
+  TrackCtl* C = P.ctl;
+  pdl_wait();
+  pdl_trigger();   // the bins kernel may be scheduled
+  const u32 nocc = C->n_occ;
+  if ((C->flags & PCS_FLAG_CAPACITY) || nocc > (u32)MAXM) return;   // (k_pc_bins reports it)
+  const int M = (int)nocc;
+  const int lane = threadIdx.x & 31;
+  const i64 k = C->k;
+  const float* frame = C->frames + (k - C->k_frames) * P.H * P.W;
+  const PixView pv = frame_view(frame, P.H, P.W);
+  const bool f64 = P.spot.model != 0 && P.spot.f64;
+  const u64 wq0 = P.weighted ? (u64)f32_to_fixed(__double2float_rn(__ddiv_rn(1.0, (double)P.n_global)), FX_WQ)
+                             : 0ull;
+  long long lmax = LLONG_MIN;
+  const int nw = gridDim.x * (CELLS_BLOCK / 32);
+  for (int b = blockIdx.x * (CELLS_BLOCK / 32) + (threadIdx.x >> 5); b < M; b += nw) {
+    const u32 cell = P.occ[b];
+    const u32 cnt = P.tab_cnt[cell];
+    // dummy x, y, I0 (vx, vy do not enter the likelihood); weighted centre
+    // of mass with the general path's uniform prior weight w0 = RN32(1/N):
+    // RN32(RN64(RN64(wq S) / RN64(wq count)) 2^-40), wq = round(w0 2^62)
+    const double den = P.weighted ? i128_to_f64_rn((i128)wq0 * (i128)cnt) : (double)cnt;
+    float d[3];
+#pragma unroll
+    for (int q = 0; q < 3; ++q) {
+      const int c = (q == 2) ? 4 : q;
+      const i128 S = load_i128(P.tab_sum + ((i64)c * P.G + cell) * 2);
+      const double num = i128_to_f64_rn(P.weighted ? S * (i128)wq0 : S);
+      d[q] = __double2float_rn(scalbn(__ddiv_rn(num, den), -FX_STATE));
+    }
+    if (P.placement == 1) {   // cell centre (binning.py:168-171)
+      const i64 ix = (i64)cell % P.grid.ncols, iy = (i64)cell / P.grid.ncols;
+      d[0] = __double2float_rn(__dadd_rn(P.grid.ox, __dmul_rn((double)ix + 0.5, P.grid.lx)));
+      d[1] = __double2float_rn(__dadd_rn(P.grid.oy, __dmul_rn((double)iy + 0.5, P.grid.ly)));
+    }
+    double ll;
+    if (f64) {
+      ll = loglik_poisson64_warp(pv, d[0], d[1], d[2], P.spot, lane);
+    } else {
+      ll = loglik_warp(pv, d[0], d[1], d[2], P.spot, lane);
+    }
+    if (lane == 0) {
+      Sd.ll[b] = ll;
+      Sd.cnt[b] = cnt;
+      lmax = max(lmax, (long long)f64_to_ordered(ll));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lmax = max(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+  if (lane == 0 && lmax != LLONG_MIN) atomicMax((long long*)&C->cell_max_ord, lmax);
+}
+
 constexpr int BINS_BLOCK = 512;
 #define PCS_PROBE(i)                                                                  \
   do {                                                                                \
@@ -697,40 +768,6 @@ constexpr int BINS_BLOCK = 512;
       C->dbg[i] = (long long)_g;                                                      \
     }                                                                                 \
   } while (0)
-constexpr int BINS_MAXM = 8192;              // occupied cells handled by the fused bins kernel
-constexpr int BINS_SM = 4096;                // ... of which kept in shared memory
-constexpr int STAGE_PIX = 11264;             // staged frame tile (44 KB)
-constexpr int ROWBUF = 4096;                 // (cell, row) partials per chunk (32 KB)
-struct BinsSmem {
-  double ll[BINS_MAXM];
-  double row[ROWBUF];
-  float pix[STAGE_PIX];
-  float dx[BINS_SM], dy[BINS_SM], di[BINS_SM];
-  u32 cnt[BINS_SM];
-  u32 cell[BINS_SM];
-  i128 red[BINS_BLOCK / 32 * 6];
-  unsigned long long tma_bar;
-};
-constexpr size_t BINS_SMEM = sizeof(BinsSmem);
-
-struct BinsScratch {  // per-cell values of occupied cells b >= BINS_SM (global memory)
-  float* dx;
-  float* dy;
-  float* di;
-  u32* cnt;
-  u32* cell;
-};
-
-// per-cell record b: shared memory for b < BINS_SM, global scratch beyond
-struct BinsView {
-  BinsSmem& sm;
-  const BinsScratch& g;
-  __device__ __forceinline__ float& dx(int b) const { return b < BINS_SM ? sm.dx[b] : g.dx[b]; }
-  __device__ __forceinline__ float& dy(int b) const { return b < BINS_SM ? sm.dy[b] : g.dy[b]; }
-  __device__ __forceinline__ float& di(int b) const { return b < BINS_SM ? sm.di[b] : g.di[b]; }
-  __device__ __forceinline__ u32& cnt(int b) const { return b < BINS_SM ? sm.cnt[b] : g.cnt[b]; }
-  __device__ __forceinline__ u32& cell(int b) const { return b < BINS_SM ? sm.cell[b] : g.cell[b]; }
-};
 
 // K exact sums over the block: warp shuffles, one barrier, then warp 0 sums
 // the 32 warp partials with shuffles; the results are valid in warp 0
@@ -751,18 +788,19 @@ __device__ __forceinline__ void bins_sum_k(i128 (&v)[K], i128* sh) {
   }
 }
 
-template <int MAXS>
+// ---------------------------------------------------------------------------
+// k_pc_bins (one CTA): from the per-cell log-likelihoods of k_pc_cells the
+// exact normaliser, per-cell weights (broadcast tables for the resampler),
+// estimate, ESS and the resampling decision (filtering.py:75-114,169-170);
+// zeroes the consumed table cells. Any number of occupied cells up to MAXM.
+// ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScratch Sd) {
   TrackCtl* C = P.ctl;
   pdl_wait();
   pdl_trigger();   // k_sys_resample CTAs may become resident on the other SMs
   PCS_PROBE(8);
-  extern __shared__ __align__(128) unsigned char bins_raw[];
-  BinsSmem& sm = *reinterpret_cast<BinsSmem*>(bins_raw);
-  const BinsView V{sm, Sd};
-  __shared__ long long s_max;
+  __shared__ i128 red[BINS_BLOCK / 32 * 6];
   __shared__ unsigned s_wmin, s_wmax;
-  __shared__ int s_box[4];
   __shared__ double s_Sf;
   const int t = threadIdx.x;
   const i64 k = C->k;
@@ -770,7 +808,7 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   if (t == 0) atomicMax(&C->max_occ, nocc);
   // (weighted centre of mass with non-uniform prior weights needs the
   // per-particle weighted sums of the general path)
-  if ((C->flags & PCS_FLAG_CAPACITY) || nocc > (u32)BINS_MAXM || (P.weighted && C->pc_prior)) {
+  if ((C->flags & PCS_FLAG_CAPACITY) || nocc > (u32)MAXM || (P.weighted && C->pc_prior)) {
     if (t == 0) {
       set_flag(C, PCS_FLAG_CAPACITY);
       C->do_resample = 0;
@@ -801,137 +839,10 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     out_res = C->out_res;
     out_occ = C->out_occ;
     u_next = philox_resample_u(P.seed, P.frame0 + (u32)k);
-  }
-  const float* frame = C->frames + (k - C->k_frames) * P.H * P.W;
-  // TMA prefetch of a 64 x 64 frame region around the previous estimate into
-  // the staging buffer, in flight while the dummies are computed (used in
-  // step 2 if it covers every likelihood window)
-  const bool tma = C->fmap_ok;
-  int txa = 0, tya = 0;
-  if (tma) {
-    txa = (int)min(max((i64)floor(C->center[0]) - FMAP_BX / 2, (i64)0), max(P.W - FMAP_BX, (i64)0)) & ~3;
-    tya = (int)min(max((i64)floor(C->center[1]) - FMAP_BX / 2, (i64)0), max(P.H - FMAP_BX, (i64)0));
-    if (t == 0)
-      tma_stage_issue(sm.pix, P.fmap, txa, tya, (int)(k - C->k_frames), FMAP_BX / FMAP_BY,
-                      &sm.tma_bar);
-  }
-  PCS_PROBE(0);
-  if (t == 0) {
-    s_max = LLONG_MIN;
     s_wmin = 0xFFFFFFFFu;
     s_wmax = 0u;
-    s_box[0] = INT_MAX; s_box[1] = INT_MIN; s_box[2] = INT_MAX; s_box[3] = INT_MIN;
   }
-  __syncthreads();
-  // 1) dummies (exact means, binning.py:157-172) and the union of their windows;
-  //    weighted centre of mass with the uniform prior weight w0 = RN32(1/N)
-  //    of the general path: RN32(RN64(RN64(wq S) / RN64(wq count)) 2^-40),
-  //    wq = round(w0 2^62) (pcs_bin.cuh k_dummies)
-  const u64 wq0 = P.weighted ? (u64)f32_to_fixed(__double2float_rn(__ddiv_rn(1.0, (double)P.n_global)), FX_WQ)
-                             : 0ull;
-  int bx0 = INT_MAX, bx1 = INT_MIN, by0 = INT_MAX, by1 = INT_MIN;
-  for (int b = t; b < M; b += BINS_BLOCK) {
-    const u32 cell = P.occ[b];
-    const u32 cnt = P.tab_cnt[cell];
-    float d[5];
-    const double den = P.weighted ? i128_to_f64_rn((i128)wq0 * (i128)cnt) : (double)cnt;
-#pragma unroll
-    for (int c = 0; c < 5; ++c) {   // only x, y, I0 enter the likelihood (vx, vy unused)
-      if (c == 2 || c == 3) { d[c] = 0.0f; continue; }
-      const i128 S = load_i128(P.tab_sum + ((i64)c * P.G + cell) * 2);
-      const double num = i128_to_f64_rn(P.weighted ? S * (i128)wq0 : S);
-      d[c] = __double2float_rn(scalbn(__ddiv_rn(num, den), -FX_STATE));
-    }
-    if (P.placement == 1) {  // cell centre (binning.py:168-171)
-      const i64 ix = (i64)cell % P.grid.ncols, iy = (i64)cell / P.grid.ncols;
-      d[0] = __double2float_rn(__dadd_rn(P.grid.ox, __dmul_rn((double)ix + 0.5, P.grid.lx)));
-      d[1] = __double2float_rn(__dadd_rn(P.grid.oy, __dmul_rn((double)iy + 0.5, P.grid.ly)));
-    }
-    V.dx(b) = d[0];
-    V.dy(b) = d[1];
-    V.di(b) = d[4];
-    V.cnt(b) = cnt;
-    V.cell(b) = cell;
-    if (d[0] == d[0] && d[1] == d[1]) {
-      int xlo, xhi, ylo, yhi;
-      window_of(d[0], d[1], P.spot, P.H, P.W, xlo, xhi, ylo, yhi);
-      bx0 = min(bx0, xlo); bx1 = max(bx1, xhi); by0 = min(by0, ylo); by1 = max(by1, yhi);
-    }
-  }
-  atomicMin(&s_box[0], bx0); atomicMax(&s_box[1], bx1);
-  atomicMin(&s_box[2], by0); atomicMax(&s_box[3], by1);
-  __syncthreads();
-  PCS_PROBE(1);
-  // 2) stage the frame region covering every window in shared memory: TMA
-  //    boxes of 64 x 16 pixels when the region is at most 64 px wide, plain
-  //    loads otherwise
-  PixView pv = frame_view(frame, P.H, P.W);
-  {
-    const int x0 = s_box[0], y0 = s_box[2];
-    const i64 wx = (i64)s_box[1] - x0 + 1, wy = (i64)s_box[3] - y0 + 1;
-    if (tma) tma_stage_wait(&sm.tma_bar);   // (the buffer may be overwritten below)
-    if (s_box[1] >= s_box[0] && tma && x0 >= txa && s_box[1] < txa + FMAP_BX && y0 >= tya &&
-        s_box[3] < tya + FMAP_BX) {
-      pv.base = sm.pix;
-      pv.pitch = FMAP_BX;
-      pv.x0 = txa;
-      pv.y0 = tya;
-    } else if (s_box[1] >= s_box[0] && wx * wy <= STAGE_PIX) {
-      for (int p = t; p < (int)(wx * wy); p += BINS_BLOCK) {
-        const int yy = p / (int)wx, xx = p % (int)wx;
-        sm.pix[p] = __ldg(frame + (i64)(y0 + yy) * P.W + (x0 + xx));
-      }
-      pv.base = sm.pix;
-      pv.pitch = wx;
-      pv.x0 = x0;
-      pv.y0 = y0;
-    }
-  }
-  __syncthreads();
-  PCS_PROBE(2);
-  // 3) likelihood once per occupied cell (binning.py:189): one thread per
-  //    (cell, window row) computes the row partial; then one thread per cell
-  //    adds its rows in row order (= the canonical per-thread loop)
-  long long lmax = LLONG_MIN;
-  {
-    const int S = 2 * P.spot.hw + 1;
-    const int CH = ROWBUF / S;   // cells per chunk
-    for (int b0 = 0; b0 < M; b0 += CH) {
-      const int nb = min(CH, M - b0);
-      for (int it = t; it < nb * S; it += BINS_BLOCK) {
-        const int b = b0 + it / S, j = it % S;
-        const float x = V.dx(b), y = V.dy(b), i0 = V.di(b);
-        double part = 0.0;
-        if (x == x && y == y && i0 == i0) {
-          int xlo, xhi, ylo, yhi;
-          window_of(x, y, P.spot, P.H, P.W, xlo, xhi, ylo, yhi);
-          if (j <= yhi - ylo) part = loglik_row(pv, x, y, i0, P.spot, xlo, xhi - xlo + 1, ylo + j);
-        }
-        sm.row[it] = part;
-      }
-      __syncthreads();
-      for (int bb = t; bb < nb; bb += BINS_BLOCK) {
-        const int b = b0 + bb;
-        const float x = V.dx(b), y = V.dy(b), i0 = V.di(b);
-        double ll;
-        if (!(x == x) || !(y == y) || !(i0 == i0)) {
-          ll = nan_ll();
-        } else {
-          int xlo, xhi, ylo, yhi;
-          window_of(x, y, P.spot, P.H, P.W, xlo, xhi, ylo, yhi);
-          double tot = 0.0;
-          for (int j = 0; j <= yhi - ylo; ++j) tot += sm.row[bb * S + j];
-          ll = (P.spot.model == 0) ? -tot * P.spot.inv_2sxi2 : tot;
-        }
-        sm.ll[b] = ll;
-        lmax = max(lmax, (long long)f64_to_ordered(ll));
-      }
-      __syncthreads();
-    }
-  }
-  atomicMax(&s_max, lmax);
-  __syncthreads();
-  const double m = ordered_to_f64((i64)s_max);
+  const double m = ordered_to_f64(C->cell_max_ord);
   const bool bad_m = !(m == m) || m == INFINITY;
   const bool degenerate = (m == -INFINITY);
   PCS_PROBE(3);
@@ -941,10 +852,11 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     // log w = log w_prev + ll_cell (binning.py:190-192), normaliser, estimate,
     // ESS and decision follow in k_pc_prior_ll / k_sir_sum / k_sir_stats
     for (int b = t; b < M; b += BINS_BLOCK) {
-      const u32 cell = V.cell(b);
-      P.lltab[cell] = sm.ll[b];
+      const u32 cell = P.occ[b];
+      const double llb = Sd.ll[b];
+      P.lltab[cell] = llb;
       const int qs = sub_code(P, C, cell);
-      if (qs >= 0) P.ltsub[qs] = sm.ll[b];
+      if (qs >= 0) P.ltsub[qs] = llb;
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
         u64* p = P.tab_sum + ((i64)c * P.G + cell) * 2;
@@ -953,36 +865,38 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
       }
       P.tab_cnt[cell] = 0;
     }
-    if (t == 0) C->frame_occ = M;
+    if (t == 0) {
+      C->frame_occ = M;
+      C->cell_max_ord = LLONG_MIN;
+    }
     return;
   }
-  // 4) normaliser S = sum_b cnt_b * round(exp(ll_b - m) * 2^95)
+  // normaliser S = sum_b cnt_b * round(exp(ll_b - m) * 2^95)
   {
     i128 acc[1] = {0};
-    for (int b = t; b < M; b += BINS_BLOCK)
-    {
-      const double ex = exp(__dsub_rn(sm.ll[b], m));
-      sm.ll[b] = ex;   // the weights below reuse exp(ll - m)
-      acc[0] += (i128)V.cnt(b) * f64_to_fixed(ex, FX_S);
+    for (int b = t; b < M; b += BINS_BLOCK) {
+      const double ex = exp(__dsub_rn(Sd.ll[b], m));
+      Sd.ll[b] = ex;   // the weights below reuse exp(ll - m)
+      acc[0] += (i128)Sd.cnt[b] * f64_to_fixed(ex, FX_S);
     }
-    bins_sum_k<1>(acc, sm.red);
+    bins_sum_k<1>(acc, red);
     if (t == 0) s_Sf = i128_to_f64_scaled(acc[0], FX_S);
     __syncthreads();
   }
   const double Sf = s_Sf;
   PCS_PROBE(4);
-  // 5) weights per cell (broadcast table), estimate, ESS; zero consumed cells
+  // weights per cell (broadcast tables), estimate, ESS; zero consumed cells
   i128 e[6] = {0, 0, 0, 0, 0, 0};
   {
     unsigned wmin = 0xFFFFFFFFu, wmax = 0u;
     for (int b = t; b < M; b += BINS_BLOCK) {
-      const u32 cell = V.cell(b);
-      const u32 cnt = V.cnt(b);
-      // the cell's state sums first: their HBM/L2 latency overlaps the division
+      const u32 cell = P.occ[b];
+      const u32 cnt = Sd.cnt[b];
+      // the cell's state sums first: their latency overlaps the division
       i128 Ssum[5];
 #pragma unroll
       for (int c = 0; c < 5; ++c) Ssum[c] = load_i128(P.tab_sum + ((i64)c * P.G + cell) * 2);
-      const float w = __double2float_rn(__ddiv_rn(sm.ll[b], Sf));   // normalised_weight
+      const float w = __double2float_rn(__ddiv_rn(Sd.ll[b], Sf));   // normalised_weight
       P.wtab[cell] = w;
       P.wfix[cell] = cdf_fixed(w);
       const int qs = sub_code(P, C, cell);
@@ -1007,7 +921,7 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     atomicMax(&s_wmax, wmax);
   }
   PCS_PROBE(5);
-  bins_sum_k<6>(e, sm.red);
+  bins_sum_k<6>(e, red);
   PCS_PROBE(6);
   // warp 0 holds the six exact sums in every lane: lane c converts sum c
   double conv = 0.0;

@@ -25,6 +25,8 @@ struct Spot {
   int model;           // 0 gauss-ssd, 1 erf-poisson, 2 midpoint4x4-poisson
   float erf_scale;     // sigma*sqrt(pi/2)  (model 1)
   float inv_sqrt2s;    // 1/(sqrt(2) sigma) (model 1)
+  int f64;             // Poisson models: 1 = the float64 form (pcSIR cells)
+  double sigma64, bg64, inv2s2_64, erf_scale64, inv_sqrt2s64;   // float64 parameters
 };
 
 // frame (H x W) view; pixel (x, y) lives at base[(y - y0) * pitch + (x - x0)]
@@ -275,10 +277,66 @@ __device__ __forceinline__ double loglik_poisson(const PixView& pv, float x, flo
   return loglik_poisson_k<MAXS, true, false>(pv, x, y, i0, sp, xlo, nx, ylo, ny);
 }
 
+// ---- float64 Poisson form (pcSIR cell likelihoods, any window) -------------
+// The same model and window as above evaluated entirely in float64 (the
+// dummies are float32, exact in float64): edge values C = erfc(|e| / (sqrt2
+// s)) with e = (i - 1/2) - x, pixel integrals by the same sign cases, t =
+// (I0 Ex / bg) Ey, term = z log1p(t) - t bg; a row is summed in column order
+// and the rows in row order. Agrees with the float64 sub-pixel oracle to
+// ~1e-12, i.e. |d log L| <= 1e-5 holds with a wide margin (R19; the
+// per-particle SIR form above trades that for float32 pixel terms).
+__device__ __forceinline__ double edge_c64(double e, const Spot& sp) {
+  return erfc(fabs(e) * sp.inv_sqrt2s64);
+}
+__device__ __forceinline__ double erf_pixel64(double a, double b, double ca, double cb, const Spot& sp) {
+  double d;
+  if (a >= 0.0) d = ca - cb;
+  else if (b <= 0.0) d = cb - ca;
+  else d = (2.0 - ca) - cb;
+  return sp.erf_scale64 * d;
+}
+__device__ __forceinline__ double psf_axis64(double d, const Spot& sp) {   // model 2
+  const double t0 = d - 0.375, t1 = d - 0.125, t2 = d + 0.125, t3 = d + 0.375;
+  return 0.25 * (((exp(-(t0 * t0) * sp.inv2s2_64) + exp(-(t1 * t1) * sp.inv2s2_64)) +
+                  exp(-(t2 * t2) * sp.inv2s2_64)) + exp(-(t3 * t3) * sp.inv2s2_64));
+}
+// PSF factor of pixel i along one axis (position p), float64
+__device__ __forceinline__ double psf_pixel64(int i, double p, const Spot& sp) {
+  if (sp.model == 1) {
+    const double a = ((double)i - 0.5) - p, b = ((double)i + 0.5) - p;
+    return erf_pixel64(a, b, edge_c64(a, sp), edge_c64(b, sp), sp);
+  }
+  return psf_axis64((double)i - p, sp);
+}
+__device__ __forceinline__ double poisson_term64(double z, double t, double bg) {
+  return z * log1p(t) - t * bg;
+}
+__device__ __forceinline__ double loglik_poisson64_generic(const PixView& pv, float x, float y,
+                                                           float i0, const Spot& sp) {
+  if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
+  int xlo, xhi, ylo, yhi;
+  window_axis_f(x, sp.hw, pv.W, xlo, xhi);
+  window_axis_f(y, sp.hw, pv.H, ylo, yhi);
+  const double a0 = (double)i0 / sp.bg64;
+  double ll = 0.0;
+  for (int yy = ylo; yy <= yhi; ++yy) {
+    const double ey = psf_pixel64(yy, (double)y, sp);
+    const float* row = pv.row(yy, xlo);
+    double racc = 0.0;
+    for (int xx = xlo; xx <= xhi; ++xx) {
+      const double ex = a0 * psf_pixel64(xx, (double)x, sp);
+      racc += poisson_term64((double)row[xx - xlo], ex * ey, sp.bg64);
+    }
+    ll += racc;
+  }
+  return ll;
+}
+
 template <int MAXS>
 __device__ __forceinline__ double loglik_any(const PixView& pv, float x, float y, float i0,
                                              const Spot& sp) {
   if (sp.model == 0) return loglik_gauss<MAXS>(pv, x, y, i0, sp);
+  if (sp.f64) return loglik_poisson64_generic(pv, x, y, i0, sp);
   return loglik_poisson<MAXS>(pv, x, y, i0, sp);
 }
 
@@ -333,6 +391,7 @@ __device__ __forceinline__ double loglik_poisson_generic(const PixView& pv, floa
 
 __device__ __forceinline__ double loglik_generic(const PixView& pv, float x, float y, float i0,
                                                  const Spot& sp) {
+  if (sp.model != 0 && sp.f64) return loglik_poisson64_generic(pv, x, y, i0, sp);
   return (sp.model == 0) ? loglik_gauss_generic(pv, x, y, i0, sp)
                          : loglik_poisson_generic(pv, x, y, i0, sp);
 }
@@ -389,6 +448,32 @@ __device__ __forceinline__ double loglik_warp(const PixView& pv, float x, float 
   double tot = 0.0;
   for (int j = 0; j < ny; ++j) tot += __shfl_sync(0xffffffffu, racc, j);
   return gauss ? -tot * sp.inv_2sxi2 : tot;
+}
+
+// Warp-cooperative float64 Poisson window (one window per warp): lane i owns
+// column factor I0 Ex_i / bg, lane j row j; row j is summed in column order
+// by lane j and the rows in row order — bit-identical to
+// loglik_poisson64_generic. All lanes return the value.
+__device__ __forceinline__ double loglik_poisson64_warp(const PixView& pv, float x, float y,
+                                                        float i0, const Spot& sp, int lane) {
+  if (!(x == x) || !(y == y) || !(i0 == i0)) return nan_ll();
+  int xlo, xhi, ylo, yhi;
+  window_axis_f(x, sp.hw, pv.W, xlo, xhi);
+  window_axis_f(y, sp.hw, pv.H, ylo, yhi);
+  const int nx = xhi - xlo + 1, ny = yhi - ylo + 1;
+  if (nx > 32 || ny > 32) return loglik_poisson64_generic(pv, x, y, i0, sp);
+  const double a0 = (double)i0 / sp.bg64;
+  const double colf = (lane < nx) ? a0 * psf_pixel64(xlo + lane, (double)x, sp) : 0.0;
+  const double rowf = (lane < ny) ? psf_pixel64(ylo + lane, (double)y, sp) : 0.0;
+  const float* row = pv.row(ylo + min(lane, ny - 1), xlo);
+  double racc = 0.0;
+  for (int i = 0; i < nx; ++i) {
+    const double ci = __shfl_sync(0xffffffffu, colf, i);
+    if (lane < ny) racc += poisson_term64((double)row[i], ci * rowf, sp.bg64);
+  }
+  double tot = 0.0;
+  for (int j = 0; j < ny; ++j) tot += __shfl_sync(0xffffffffu, racc, j);
+  return tot;
 }
 
 // One row of one window: the float64 partial row_j of the canonical form

@@ -227,7 +227,7 @@ def pseudo_weight_once(pset: ParticleSet, frame, lik, spec: VariantSpec, grid=No
         part = partition_device(pset.soa, grid)
         prior_w = pset.weights_f32().contiguous() if weighted_com else None
         dummies = dummy_states_device(pset.soa, grid, part, spec.placement, prior_w)
-        logw = _weight_update(pset, _evaluate_loglik(lik, dummies, frame), part.bin_of)
+        logw = _weight_update(pset, _evaluate_loglik(lik, dummies, frame, cells=True), part.bin_of)
     _check_not_degenerate(logw)
     return ParticleSet.from_device(pset.soa, logw=logw, timestep=1)
 

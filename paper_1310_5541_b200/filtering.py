@@ -49,7 +49,7 @@ class ResampleConfig:
             raise ValueError(f"unknown resampling scheme {self.scheme!r}")
 
 
-def _evaluate_loglik(lik, soa, frame):
+def _evaluate_loglik(lik, soa, frame, cells=False):
     """Device log-likelihood per state column (filtering.py:48-59).
 
     Built-in likelihoods evaluate on the GPU in float32. A duck-typed object
@@ -57,7 +57,7 @@ def _evaluate_loglik(lik, soa, frame):
     a host float64 copy — conformance only, never the benchmarked path.
     """
     if isinstance(lik, _DeviceLikelihood):
-        return lik.loglik(soa, frame)
+        return lik.loglik(soa, frame, cells=cells)
     host_states = soa.double().t().contiguous().cpu().numpy()
     batch = getattr(lik, "batch", None)
     if batch is not None:
@@ -313,7 +313,7 @@ def fused_track(frames, cfg: FilterConfig, rng, method, grid=None, placement=0, 
     c.n_particles = cfg.n_particles
     c.init = cfg.init.to_c()
     c.dyn = cfg.dynamics.to_c()
-    c.spot = lik.spot_c()
+    c.spot = lik.spot_c(cells=(method == 1))
     if grid is not None:
         c.grid = grid.to_c()
     c.seed = prng.seed

@@ -119,18 +119,21 @@ class _DeviceLikelihood:
 
     model = 0
 
-    def spot_c(self):
+    def spot_c(self, cells=False):
+        """C description; ``cells``: the pcSIR per-cell form (the Poisson
+        models in float64, PCS_LIK_F64 — few evaluations, |d log L| <= 1e-5)."""
+        model = int(self.model) | (_lib.LIK_F64 if (cells and self.model != 0) else 0)
         return _lib.PcsSpot(float(self.psf.sigma_psf), float(self.psf.i_bg),
-                            float(self.params.sigma_xi), int(self.params.window_halfwidth),
-                            int(self.model))
+                            float(self.params.sigma_xi), int(self.params.window_halfwidth), model)
 
-    def loglik(self, soa, frame: ImageFrame, count=True):
-        """Log-likelihood (float64) of each state column of ``soa`` (5,M) float32 device."""
+    def loglik(self, soa, frame: ImageFrame, count=True, cells=False):
+        """Log-likelihood (float64) of each state column of ``soa`` (5,M) float32
+        device; ``cells`` selects the pcSIR per-cell (dummy) form."""
         m = soa.shape[1]
         out = torch.empty(m, dtype=torch.float64, device=soa.device)
         if m:
             pix = frame.device()
-            spot = self.spot_c()
+            spot = self.spot_c(cells)
             soa = soa.contiguous()
             _lib.check(_lib.lib().pcs_loglik(
                 _lib.ptr(pix), pix.shape[0], pix.shape[1], _lib.ptr(soa[X]), _lib.ptr(soa[Y]),

@@ -59,7 +59,7 @@ class MultiTargetTracker:
         c.n_particles = cfg.n_particles
         c.init = cfg.init.to_c()
         c.dyn = cfg.dynamics.to_c()
-        c.spot = cfg.likelihood.spot_c()
+        c.spot = cfg.likelihood.spot_c(cells=True)
         c.grid = cfg.grid.to_c()
         c.seed = seed % (1 << 64)
         c.frame0 = 0

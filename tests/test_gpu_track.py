@@ -479,27 +479,28 @@ def test_fused_multinomial_equals_general(cuda, frac, method):
 
 
 def test_capacity_fallback_with_prior_weights(cuda):
-    """More occupied cells than the fused bins kernel holds (8192) on a frame
+    """More occupied cells than the fused loop holds (MAXM = 2^20) on a frame
     whose particles carry prior weights (ESS threshold, no resampling): the
     fused loop stops cleanly (no second finalisation of the frame, no writes
     past the output rows) and the driver reruns the track on the general
     path (binning.py:212-226 semantics either way)."""
-    frames, truth, init, _ = _c1_like(n=50_000, k=14)
-    init = pc.InitSpec(pc.StateVector(20.0, 32.0, 0.5, 0.0, 20.0), "point")
-    dyn = pc.DynamicsParams(0.8, 0.1, 1.0)
+    n = 1_500_000
+    frames, truth, init, _ = _c1_like(n=n, k=6)
+    init = pc.InitSpec(pc.StateVector(32.0, 32.0, 0.0, 0.0, 20.0), "gauss", sigma=1.0)
+    dyn = pc.DynamicsParams(2.0, 0.1, 1.0)
     res = pc.ResampleConfig(0.001, "systematic")
-    grid = pc.BinGrid.pixel_aligned(64, 64, 8)
+    grid = pc.BinGrid.pixel_aligned(64, 64, 200)          # 0.005 px cells, 1.6e8 cells
     flat = pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(1e4, 5))
     flat2 = pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(1e4, 5))
-    a = pc.pcsir_track(frames, pc.PcFilterConfig(50_000, init, dyn, res, flat, grid=grid),
+    a = pc.pcsir_track(frames, pc.PcFilterConfig(n, init, dyn, res, flat, grid=grid),
                        pc.PhiloxRng(13), fused=True)
-    b = pc.pcsir_track(frames, pc.PcFilterConfig(50_000, init, dyn, res, flat2, grid=grid),
+    b = pc.pcsir_track(frames, pc.PcFilterConfig(n, init, dyn, res, flat2, grid=grid),
                        pc.PhiloxRng(13), fused=False)
     assert a.path == "general"            # the fused loop hit its capacity and fell back
     assert not a.resampled[1:].any()      # frames after the first carry prior weights
     assert np.array_equal(a.estimates, b.estimates)
     assert np.array_equal(a.ess, b.ess)
-    assert a.likelihood_evals == b.likelihood_evals > 8192
+    assert a.likelihood_evals == b.likelihood_evals
 
 
 @pytest.mark.parametrize("frac", [1.0, 0.3])
