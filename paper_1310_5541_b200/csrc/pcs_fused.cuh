@@ -20,7 +20,10 @@
 
 namespace pcs {
 
-constexpr int S1_THREADS = 512;                // 2 CTAs x 16 warps per SM; 64 registers
+#ifndef PCS_S1_THREADS
+#define PCS_S1_THREADS 512
+#endif
+constexpr int S1_THREADS = PCS_S1_THREADS;     // 2 CTAs x 16 warps per SM; 64 registers
 constexpr int S1_CTAS_PER_SM = 2;              // two independent barrier domains per SM
 constexpr int S1_IPT = 2;
 constexpr int S1_TILE = S1_THREADS * S1_IPT;   // 1024 particles per tile
