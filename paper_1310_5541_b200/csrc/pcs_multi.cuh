@@ -143,7 +143,10 @@ __device__ __forceinline__ bool mt_hash_add(MtHash* H, u32 flat, const float o[5
 }
 
 template <int MAXS>
-__global__ void __launch_bounds__(MT_THREADS, 2) k_mt_frame(MtParams P) {
+#ifndef PCS_MT_CTAS
+#define PCS_MT_CTAS 2
+#endif
+__global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P) {
   extern __shared__ __align__(16) unsigned char mt_raw[];
   MtSmem& sm = *reinterpret_cast<MtSmem*>(mt_raw);
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -381,14 +384,23 @@ __global__ void __launch_bounds__(MT_THREADS, 2) k_mt_frame(MtParams P) {
     }
   }
   __syncthreads();
-  // likelihood once per occupied cell: one thread per cell, canonical order
+  // likelihood once per occupied cell: one warp per cell (lane = window row;
+  // the canonical per-thread order, pcs_lik.cuh loglik_warp) — no
+  // register-resident window, so the kernel fits 64 registers without spills
   long long lmax = LLONG_MIN;
-  for (int b = t; b < M; b += MT_THREADS) {
-    float x, y, i0;
-    dummy3(b, x, y, i0);
-    double ll = loglik_dispatch<MAXS>(pv, x, y, i0, P.spot);
-    sm.u.b.ll[b] = ll;
-    lmax = max(lmax, (long long)f64_to_ordered(ll));
+  {
+    const int lane = t & 31;
+    const bool f64 = P.spot.model != 0 && P.spot.f64;
+    for (int b = t >> 5; b < M; b += MT_WARPS) {
+      float x, y, i0;
+      dummy3(b, x, y, i0);
+      const double ll = f64 ? loglik_poisson64_warp(pv, x, y, i0, P.spot, lane)
+                            : loglik_warp(pv, x, y, i0, P.spot, lane);
+      if (lane == 0) {
+        sm.u.b.ll[b] = ll;
+        lmax = max(lmax, (long long)f64_to_ordered(ll));
+      }
+    }
   }
   atomicMax(&sm.lmax, lmax);
   __syncthreads();
