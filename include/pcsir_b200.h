@@ -288,28 +288,31 @@ int pcs_mt_step(pcs_ctx* ctx, const float* frame, int64_t k, void* stream);
 int pcs_mt_results(pcs_ctx* ctx, double* est, double* ess, uint8_t* resampled, int64_t* occupied,
                    uint32_t* flags, int64_t* evals, void* stream);
 
-/* ---- particle-sharded giant filter (config 5, new; no reference code).
- * One rank's side of each phase; the host exchanges between the calls:
- * step1 -> all-reduce(bbox MIN/MAX) -> export(window limbs) ->
- * all-reduce(limbs SUM) -> import_bins -> scan -> all-gather(rank totals) ->
- * emit(prefix, slot_lo) -> gather per destination -> all-to-all -> set_states
- * (or advance when the frame did not resample). Limbs: per cell
- * [count, 5 x (three 42-bit limbs of the int128 sum)] as int64. */
+/* ---- particle-sharded giant filter (config 5, new; pcs_shard.cuh) -------
+ * Rank `rank` of `world` holds global particles [rank n, (rank+1) n)
+ * (n = cfg->n_particles, n_global = world n). Per frame k, stream-ordered,
+ * no host synchronisation, fixed-size collectives between the calls:
+ *   pcs_shard_step1(frame k)      -> box: device int64[5]     (all-reduce MAX)
+ *   pcs_shard_export(box)         -> limbs: device int64[wcap*16] (all-reduce SUM)
+ *   pcs_shard_import_bins(box, limbs)   (identical bins stage on every rank)
+ *   pcs_shard_total()             -> total: device int64[3]   (all-gather -> totals[world*3])
+ *   pcs_shard_emit(totals)        -> send_prev / send_next: device float32[5*bcap+1]
+ *                                    (send to rank-1 / rank+1, receive recv_prev
+ *                                    from rank-1, recv_next from rank+1)
+ *   pcs_shard_unpack(recv_prev, recv_next)
+ * Results (est/ess/resampled/occupied rows) and flags as for pcs_track;
+ * pcs_track_end reads the flags (all-reduce them so every rank raises). */
 int pcs_shard_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t height, int64_t width,
-                    int64_t index_offset, int64_t n_global, int64_t slot_capacity, void* stream);
+                    int32_t rank, int32_t world, int64_t n_global, int64_t wcap, int64_t bcap,
+                    void* stream);
 int pcs_shard_step1(pcs_ctx* ctx, const float* frame, int64_t k, double* est, double* ess,
-                    uint8_t* resampled, int64_t* occupied, int64_t* bbox5_out, void* stream);
-int pcs_shard_export(pcs_ctx* ctx, int64_t x0, int64_t y0, int64_t nx, int64_t ny,
-                     int64_t* limbs, void* stream);
-int pcs_shard_import_bins(pcs_ctx* ctx, int64_t x0, int64_t y0, int64_t nx, int64_t ny,
-                          const int64_t* limbs, void* stream);
-int pcs_shard_scan(pcs_ctx* ctx, uint64_t* total_lo, uint64_t* total_hi, int32_t* do_resample,
+                    uint8_t* resampled, int64_t* occupied, int64_t* box, void* stream);
+int pcs_shard_export(pcs_ctx* ctx, const int64_t* box, int64_t* limbs, void* stream);
+int pcs_shard_import_bins(pcs_ctx* ctx, const int64_t* box, const int64_t* limbs, void* stream);
+int pcs_shard_total(pcs_ctx* ctx, int64_t* total, void* stream);
+int pcs_shard_emit(pcs_ctx* ctx, const int64_t* totals, float* send_prev, float* send_next,
                    void* stream);
-int pcs_shard_emit(pcs_ctx* ctx, uint64_t prefix_lo, uint64_t prefix_hi, int64_t slot_lo,
-                   int32_t** ancestors, void* stream);
-int pcs_shard_gather(pcs_ctx* ctx, int64_t first, int64_t count, float* out, void* stream);
-int pcs_shard_set_states(pcs_ctx* ctx, const float* states, void* stream);
-int pcs_shard_advance(pcs_ctx* ctx, void* stream);
+int pcs_shard_unpack(pcs_ctx* ctx, const float* recv_prev, const float* recv_next, void* stream);
 
 #ifdef __cplusplus
 }

@@ -20,6 +20,7 @@ PCS_E_INVALID = 1
 PCS_E_CUDA = 2
 PCS_E_NOMEM = 3
 PCS_E_CAPACITY = 4
+E_CAPACITY = PCS_E_CAPACITY
 
 FLAG_DEGENERATE = 1
 FLAG_NONFINITE = 2
@@ -134,19 +135,15 @@ _SIGNATURES = [
     ("pcs_mt_step", c_int32, [c_void_p, c_void_p, c_int64, c_void_p]),
     ("pcs_mt_results", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                  c_void_p, c_void_p]),
-    ("pcs_shard_begin", c_int32, [c_void_p, P(PcsTrackCfg), c_int64, c_int64, c_int64, c_int64,
-                                  c_int64, c_void_p]),
+    ("pcs_shard_begin", c_int32, [c_void_p, P(PcsTrackCfg), c_int64, c_int64, c_int32, c_int32,
+                                  c_int64, c_int64, c_int64, c_void_p]),
     ("pcs_shard_step1", c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_void_p, c_void_p,
-                                  c_void_p, P(c_int64), c_void_p]),
-    ("pcs_shard_export", c_int32, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_void_p,
-                                   c_void_p]),
-    ("pcs_shard_import_bins", c_int32, [c_void_p, c_int64, c_int64, c_int64, c_int64, c_void_p,
-                                        c_void_p]),
-    ("pcs_shard_scan", c_int32, [c_void_p, P(c_uint64), P(c_uint64), P(c_int32), c_void_p]),
-    ("pcs_shard_emit", c_int32, [c_void_p, c_uint64, c_uint64, c_int64, P(c_void_p), c_void_p]),
-    ("pcs_shard_gather", c_int32, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
-    ("pcs_shard_set_states", c_int32, [c_void_p, c_void_p, c_void_p]),
-    ("pcs_shard_advance", c_int32, [c_void_p, c_void_p]),
+                                  c_void_p, c_void_p, c_void_p]),
+    ("pcs_shard_export", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("pcs_shard_import_bins", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("pcs_shard_total", c_int32, [c_void_p, c_void_p, c_void_p]),
+    ("pcs_shard_emit", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("pcs_shard_unpack", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
 ]
 
 EXPORTED_SYMBOLS = [name for name, _, _ in _SIGNATURES]
@@ -224,6 +221,14 @@ def ctx():
         check(lib().pcs_ctx_create(ctypes.byref(handle), key), "pcs_ctx_create")
         _ctxs[key] = handle
     return _ctxs[key]
+
+
+def new_ctx():
+    """A further pcs_ctx on the current device (its own scratch and track
+    state), e.g. one per emulated rank of the sharded filter."""
+    handle = c_void_p()
+    check(lib().pcs_ctx_create(ctypes.byref(handle), device().index), "pcs_ctx_create")
+    return handle
 
 
 def stream():

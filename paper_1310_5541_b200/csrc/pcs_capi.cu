@@ -72,6 +72,8 @@ struct TrackState {
   const char* names[MAX_LAUNCHES] = {};   // kernel of each launch of a frame
   int prop_grid = 0;
   int cells_grid = 0;    // k_pc_cells CTAs (8 warps each, one warp per occupied cell)
+  int shard_rank = 0, shard_world = 1;   // sharded filter (pcs_shard_*)
+  i64 shard_wcap = 0, shard_bcap = 0;
   int maxs = 0;
   i64 k = 0;             // host mirror of the frame counter
   cudaGraphExec_t exec = nullptr;
@@ -915,8 +917,7 @@ static int set_attrs() {
   // one shared-memory carveout for every kernel of the frame: consecutive
   // kernels with different carveouts force an SM reconfiguration between them
   const void* fns[] = {(const void*)k_pc_step1,        (const void*)k_pc_bins,
-                       (const void*)k_pc_cells,         (const void*)k_scan_emit<1>,
-                       (const void*)k_scan_emit<2>,     (const void*)k_sir_propagate_lik<0>,
+                       (const void*)k_pc_cells,         (const void*)k_sir_propagate_lik<0>,
                        (const void*)k_sir_propagate_lik<9>, (const void*)k_sir_propagate_lik<11>,
                        (const void*)k_sir_propagate_lik<15>, (const void*)k_sir_sum,
                        (const void*)k_sir_stats,        (const void*)k_sys_resample<1>,
@@ -929,7 +930,17 @@ static int set_attrs() {
   return PCS_OK;
 }
 
+static int track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t W, i64 extra_ld,
+                       void* stream);
+
 int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t W, void* stream) {
+  return track_begin(ctx, cfg, H, W, 0, stream);
+}
+
+// extra_ld: state slots after the n particles (the sharded filter's received
+// boundary states)
+static int track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t W, i64 extra_ld,
+                       void* stream) {
   PCS_CHECK_ARG(ctx && cfg, "bad arguments");
   PCS_CHECK_ARG(cfg->method == 0 || cfg->method == 1, "method must be 0 (SIR) or 1 (pcSIR)");
   PCS_CHECK_ARG(cfg->n_particles >= 1 && cfg->n_particles < INT_MAX, "n_particles out of range");
@@ -954,7 +965,7 @@ int pcs_track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   T = TrackState();
   T.cfg = *cfg;
   const i64 n = cfg->n_particles;
-  const i64 ld = ceil_div(n, 32) * 32;
+  const i64 ld = ceil_div(n + extra_ld, 32) * 32;
   TrackParams& P = T.P;
   P.n = n;
   P.ld = ld;
@@ -1388,144 +1399,106 @@ int pcs_mt_results(pcs_ctx* ctx, double* est, double* ess, uint8_t* res, int64_t
 // ---------------------------------------------------------------------------
 // particle-sharded giant filter (config 5): one rank's side of each phase
 // ---------------------------------------------------------------------------
-int pcs_shard_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t W,
-                    int64_t idx_off, int64_t n_global, int64_t slot_cap, void* stream) {
+int pcs_shard_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t W, int32_t rank,
+                    int32_t world, int64_t n_global, int64_t wcap, int64_t bcap, void* stream) {
   PCS_CHECK_ARG(ctx && cfg && cfg->method == 1, "sharded filter is pcSIR only");
-  PCS_CHECK_ARG(idx_off >= 0 && n_global >= idx_off + cfg->n_particles, "bad shard range");
+  PCS_CHECK_ARG(world >= 1 && rank >= 0 && rank < world, "bad rank / world");
+  PCS_CHECK_ARG(n_global == (int64_t)world * cfg->n_particles, "n_global must be world x n_local");
+  PCS_CHECK_ARG(wcap >= 1 && bcap >= 1 && bcap <= cfg->n_particles, "bad exchange capacities");
+  PCS_CHECK_ARG(cfg->threshold_fraction == 0.0 || cfg->threshold_fraction == 1.0,
+                "the sharded filter resamples every frame (threshold 1.0)");
+  PCS_CHECK_ARG(cfg->scheme == 0, "the sharded filter resamples systematically");
   pcs_track_cfg_t c = *cfg;
   c.use_graph = 0;
-  int r = pcs_track_begin(ctx, &c, H, W, stream);
+  int r = track_begin(ctx, &c, H, W, 2 * bcap, stream);
   if (r) return r;
   TrackState& T = ctx->tr;
   TrackParams& P = T.P;
-  P.idx_off = idx_off;
+  P.idx_off = (i64)rank * cfg->n_particles;
   P.n_global = n_global;
-  P.slot_cap = slot_cap;
-  PCS_SCRATCH(SL_SHARD_ANC, slot_cap * sizeof(int), P.anc_out);
+  P.slot_cap = cfg->n_particles + 2 * bcap;
+  PCS_SCRATCH(SL_SHARD_ANC, P.slot_cap * sizeof(int), P.anc_out);
+  T.shard_rank = rank;
+  T.shard_world = world;
+  T.shard_wcap = wcap;
+  T.shard_bcap = bcap;
   // the initial cloud uses the global particle index as the Philox counter
   pcs_init_t init = cfg->init;
-  r = pcs_init_particles(&init, cfg->seed, idx_off, P.n, P.buf0, P.ld, stream);
+  r = pcs_init_particles(&init, cfg->seed, P.idx_off, P.n, P.buf0, P.ld, stream);
   if (r) return r;
   return PCS_OK;
 }
 
 int pcs_shard_step1(pcs_ctx* ctx, const float* frame, int64_t k, double* est, double* ess,
-                    uint8_t* res, int64_t* occ, int64_t* bbox5_out, void* stream) {
-  PCS_CHECK_ARG(ctx && ctx->tr.active && frame && bbox5_out, "bad arguments");
+                    uint8_t* res, int64_t* occ, int64_t* box, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && frame && box, "bad arguments");
   PCS_CHECK_ARG(k == ctx->tr.k, "frames must be stepped in order");
   cudaStream_t st = S(stream);
   TrackState& T = ctx->tr;
-  i64* dbox;
-  PCS_SCRATCH(SL_SHARD_BOX, 8 * sizeof(i64), dbox);
   k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frame, k, k, k + 1, est, ess, res, (i64*)occ);
   k_pc_step1<<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(T.P);
-  k_shard_bbox<<<1, 1024, 0, st>>>(T.P, dbox);
-  PCS_LAUNCH_CHECK();
-  PCS_CUDA_TRY(cudaMemcpyAsync(bbox5_out, dbox, 5 * sizeof(i64), cudaMemcpyDeviceToHost, st));
-  PCS_CUDA_TRY(cudaStreamSynchronize(st));
-  return PCS_OK;
-}
-
-int pcs_shard_export(pcs_ctx* ctx, int64_t x0, int64_t y0, int64_t nx, int64_t ny, int64_t* limbs,
-                     void* stream) {
-  PCS_CHECK_ARG(ctx && ctx->tr.active && limbs && nx >= 1 && ny >= 1, "bad arguments");
-  k_shard_export<<<grid_for(nx * ny, 256, ctx->sms), 256, 0, S(stream)>>>(ctx->tr.P, x0, y0, nx,
-                                                                           ny, (i64*)limbs);
+  k_shard_bbox<<<1, 1024, 0, st>>>(T.P, (i64*)box);
   PCS_LAUNCH_CHECK();
   return PCS_OK;
 }
 
-int pcs_shard_import_bins(pcs_ctx* ctx, int64_t x0, int64_t y0, int64_t nx, int64_t ny,
-                          const int64_t* limbs, void* stream) {
-  PCS_CHECK_ARG(ctx && ctx->tr.active && limbs, "bad arguments");
+int pcs_shard_export(pcs_ctx* ctx, const int64_t* box, int64_t* limbs, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && box && limbs, "bad arguments");
+  const TrackState& T = ctx->tr;
+  k_shard_export<<<grid_for(T.shard_wcap, 256, ctx->sms), 256, 0, S(stream)>>>(
+      T.P, (const i64*)box, T.shard_wcap, (i64*)limbs);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+int pcs_shard_import_bins(pcs_ctx* ctx, const int64_t* box, const int64_t* limbs, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && box && limbs, "bad arguments");
   cudaStream_t st = S(stream);
   TrackState& T = ctx->tr;
-  k_shard_import<<<grid_for(nx * ny, 256, ctx->sms), 256, 0, st>>>(T.P, x0, y0, nx, ny,
-                                                                  (const i64*)limbs);
+  k_shard_import<<<grid_for(T.shard_wcap, 256, ctx->sms), 256, 0, st>>>(
+      T.P, (const i64*)box, T.shard_wcap, (const i64*)limbs);
   k_pc_cells<<<T.cells_grid, CELLS_BLOCK, 0, st>>>(T.P, T.bins);
   k_pc_bins<<<1, BINS_BLOCK, 0, st>>>(T.P, T.bins);
   PCS_LAUNCH_CHECK();
   return PCS_OK;
 }
 
-// rank-local exact prefix; returns the rank total (u128 as lo, hi) and the
-// resampling decision of this frame
-int pcs_shard_scan(pcs_ctx* ctx, uint64_t* total_lo, uint64_t* total_hi, int32_t* do_resample,
-                   void* stream) {
-  PCS_CHECK_ARG(ctx && ctx->tr.active && total_lo && total_hi && do_resample, "bad arguments");
+int pcs_shard_total(pcs_ctx* ctx, int64_t* total, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && total, "bad arguments");
   cudaStream_t st = S(stream);
   TrackState& T = ctx->tr;
   TrackParams Q = T.P;
   Q.scan_mode = 1;
-  k_scan_emit<1><<<(unsigned)Q.ntiles, SCAN_BLOCK, 0, st>>>(Q);
+  launch_pdl(k_sys_resample<1>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<1>), st, Q);
+  k_shard_total<<<1, 32, 0, st>>>(Q, T.rs_grid, (i64*)total);
   PCS_LAUNCH_CHECK();
-  u128 tot = 0;
-  TrackCtl h;
-  PCS_CUDA_TRY(cudaMemcpyAsync(&tot, Q.tile_inc + (Q.ntiles - 1), sizeof(u128),
-                               cudaMemcpyDeviceToHost, st));
-  PCS_CUDA_TRY(cudaMemcpyAsync(&h, Q.ctl, sizeof(h), cudaMemcpyDeviceToHost, st));
-  PCS_CUDA_TRY(cudaStreamSynchronize(st));
-  *do_resample = h.do_resample;
-  if (!h.do_resample) tot = 0;
-  *total_lo = (uint64_t)tot;
-  *total_hi = (uint64_t)(tot >> 64);
   return PCS_OK;
 }
 
-// emit this rank's global slots [slot_lo, slot_lo + count) as local ancestors
-int pcs_shard_emit(pcs_ctx* ctx, uint64_t prefix_lo, uint64_t prefix_hi, int64_t slot_lo,
-                   int32_t** anc_out, void* stream) {
-  PCS_CHECK_ARG(ctx && ctx->tr.active && anc_out, "bad arguments");
+int pcs_shard_emit(pcs_ctx* ctx, const int64_t* totals, float* send_prev, float* send_next,
+                   void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && totals && send_prev && send_next, "bad arguments");
   cudaStream_t st = S(stream);
   TrackState& T = ctx->tr;
-  k_shard_set_prefix<<<1, 1, 0, st>>>(T.P.ctl, prefix_lo, prefix_hi);
+  k_shard_ranges<<<1, 32, 0, st>>>(T.P, (const i64*)totals, T.shard_rank, T.shard_world,
+                                   T.shard_bcap);
   TrackParams Q = T.P;
   Q.scan_mode = 2;
-  Q.slot_lo = slot_lo;
-  k_scan_emit<1><<<(unsigned)Q.ntiles, SCAN_BLOCK, 0, st>>>(Q);
-  PCS_LAUNCH_CHECK();
-  *anc_out = Q.anc_out;
-  return PCS_OK;
-}
-
-// the states to send: out[c*count + q] = current[c][anc_out[first + q]]
-int pcs_shard_gather(pcs_ctx* ctx, int64_t first, int64_t count, float* out, void* stream) {
-  PCS_CHECK_ARG(ctx && ctx->tr.active && out && count >= 0, "bad arguments");
-  if (count == 0) return PCS_OK;
-  TrackState& T = ctx->tr;
-  // step1 of frame k wrote its propagated states into buf[(k+1) & 1]
-  const float* cur = ((T.k + 1) & 1) ? T.P.buf1 : T.P.buf0;
-  k_shard_gather<<<grid_for(count, 256, ctx->sms), 256, 0, S(stream)>>>(cur, T.P.ld,
-                                                                       T.P.anc_out + first, count,
-                                                                       out);
+  launch_pdl(k_sys_resample<1>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<1>), st, Q);
+  k_shard_pack<<<grid_for(T.P.n, 256, ctx->sms), 256, 0, st>>>(T.P, T.shard_rank, send_prev,
+                                                              send_next, T.shard_bcap);
   PCS_LAUNCH_CHECK();
   return PCS_OK;
 }
 
-// no resampling this frame: keep the propagated states, identity ancestors
-int pcs_shard_advance(pcs_ctx* ctx, void* stream) {
-  PCS_CHECK_ARG(ctx && ctx->tr.active, "bad arguments");
-  TrackState& T = ctx->tr;
-  T.k += 1;
-  k_iota<<<grid_for(T.P.n, 256, ctx->sms), 256, 0, S(stream)>>>(T.P.anc, T.P.n);
-  PCS_LAUNCH_CHECK();
-  return PCS_OK;
-}
-
-// install the received states (SoA, ld = n_local) as the input of the next
-// frame with identity ancestors
-int pcs_shard_set_states(pcs_ctx* ctx, const float* states, void* stream) {
-  PCS_CHECK_ARG(ctx && ctx->tr.active && states, "bad arguments");
+int pcs_shard_unpack(pcs_ctx* ctx, const float* recv_prev, const float* recv_next, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && recv_prev && recv_next, "bad arguments");
   cudaStream_t st = S(stream);
   TrackState& T = ctx->tr;
-  TrackParams& P = T.P;
-  T.k += 1;   // the bins kernel advanced the device frame counter
-  float* dst = (T.k & 1) ? P.buf1 : P.buf0;
-  for (int c = 0; c < 5; ++c)
-    PCS_CUDA_TRY(cudaMemcpyAsync(dst + c * P.ld, states + c * P.n, P.n * sizeof(float),
-                                 cudaMemcpyDeviceToDevice, st));
-  k_iota<<<grid_for(P.n, 256, ctx->sms), 256, 0, st>>>(P.anc, P.n);
+  k_shard_unpack<<<grid_for(T.shard_bcap, 256, ctx->sms), 256, 0, st>>>(T.P, recv_prev, recv_next,
+                                                                        T.shard_bcap);
   PCS_LAUNCH_CHECK();
+  T.k += 1;
   return PCS_OK;
 }
 

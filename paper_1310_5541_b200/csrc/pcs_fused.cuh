@@ -4,9 +4,9 @@
 //                   (state.py:115-127) + cell index (binning.py:61-67,105) +
 //                   exact per-cell sums for the dummies (binning.py:157-172)
 //                   in ONE pass over the particle states.
-//   k_scan_emit     single-pass exact-prefix systematic resampling
-//                   (filtering.py:93-100): decoupled look-back scan of the
-//                   fixed-point weights + ancestor emission.
+//   k_pc_cells / k_pc_bins   per-cell dummies + likelihoods, then the
+//                   normaliser / weights / estimate / ESS / decision
+//   k_sys_resample  exact-prefix systematic resampling (filtering.py:93-100)
 //
 // Per-cell accumulation without 64-bit shared-memory atomics: tile counting
 // sort + warp-segmented run sums + 32-bit digit accumulators (S1Smem).
@@ -98,6 +98,9 @@ struct TrackCtl {
   long long dbg[16];         // phase timestamps (globaltimer ns) of the bins kernel
   unsigned long long tile_ctr;  // decoupled look-back: monotone tile ticket counter
   u64 rank_prefix[2];        // sharded: exact cumulative weight of the preceding ranks
+  i64 shard_lo, shard_hi;    // sharded: this rank's emitted global slots [lo, hi)
+  i64 shard_send[2];         // sharded: slots sent to rank r-1 / r+1 this frame
+  i64 shard_recv[2];         // sharded: slots received from rank r-1 / r+1
   u32 gbar_cnt, gbar_gen;    // grid barrier of k_sys_resample
   u32 stats_done;            // k_sir_stats CTAs finished (the last one finalises)
   u32 s1_ticket, s1_done;    // k_pc_step1 dynamic tile tickets (reset by its last CTA)
@@ -150,7 +153,8 @@ struct TrackParams {
   i64 slot_lo;               // first global output slot emitted by this rank
   i64 slot_cap;              // capacity of anc_out
   int* anc_out;              // ancestors (local particle index) for slots slot_lo + k
-  int scan_mode;             // 0 scan+emit, 1 scan only, 2 emit only (rank prefix in ctl)
+  int scan_mode;             // k_sys_resample: 0 both passes, 1 pass 1 only, 2 pass 2 only
+                             // (sharded: rank prefix and first slot in ctl)
   int s1_tile;               // k_pc_step1 tile (<= S1_TILE), balanced over its CTAs
   double thresh;             // resample when ESS < thresh (= threshold_fraction * N)
   float* wprev;              // normalised prior weights when prior_nonuniform
@@ -990,219 +994,6 @@ __device__ __forceinline__ u32 ld_acquire_u32(const u32* p) {
   return v;
 }
 
-// scan_mode 0: tile ticket + decoupled look-back + emission (single GPU)
-// scan_mode 1: tile ticket + decoupled look-back only (sharded: tile_inc holds
-//              the rank-local inclusive prefixes; the last one is the rank total)
-// scan_mode 2: emission only, excl = rank_prefix + tile_inc[tile-1] (sharded)
-// Emitted slots are global (n_global points), written as local ancestor
-// indices to anc_out[j - slot_lo].
-// weights staged with one pad word per SCAN_ITEMS so that thread t's items
-// (t * SCAN_ITEMS + q) are read conflict-free
-__device__ __forceinline__ int wpad(int k) { return k + k / SCAN_ITEMS; }
-
-template <int KIND>
-__global__ void __launch_bounds__(SCAN_BLOCK, 4) k_scan_emit(TrackParams P) {
-  __shared__ float wsh[SCAN_TILE + SCAN_TILE / SCAN_ITEMS];
-  __shared__ u128 wtot[SCAN_BLOCK / 32];
-  __shared__ u128 s_excl;
-  __shared__ unsigned long long s_ticket;
-  TrackCtl* C = P.ctl;
-  const i64 n = P.n, nt = P.ntiles;
-  const int mode = P.scan_mode;
-  if (threadIdx.x == 0) s_ticket = (mode == 2) ? 0ull : atomicAdd(&C->tile_ctr, 1ull);
-  __syncthreads();
-  const unsigned long long ticket = s_ticket;
-  const i64 tile = (mode == 2) ? (i64)blockIdx.x : (i64)(ticket % (unsigned long long)nt);
-  const u32 tag = (u32)(ticket / (unsigned long long)nt) & 0x3FFFFFFFu;
-  const int do_res = C->do_resample;
-  const i64 base = tile * SCAN_TILE;
-  if (!do_res) {   // identity ancestors, weights stay uniform (all equal)
-    if (mode == 1) return;
-    for (int q = 0; q < SCAN_ITEMS; ++q) {
-      i64 i = base + (i64)q * SCAN_BLOCK + threadIdx.x;
-      if (i < n) P.anc_out[P.idx_off + i - P.slot_lo] = (int)i;
-    }
-    return;
-  }
-  const double m = C->m, Sf = C->Sf, u = C->u;
-#pragma unroll 4
-  for (int q = 0; q < SCAN_ITEMS; ++q) {
-    i64 i = base + (i64)q * SCAN_BLOCK + threadIdx.x;
-    float w = 0.0f;
-    if (i < n) w = (KIND == 1) ? code_wtab(P, P.pslot[i]) : weight_from_ex(P.ll[i], Sf);
-    wsh[wpad(q * SCAN_BLOCK + threadIdx.x)] = w;
-  }
-  __syncthreads();
-  u128 tsum = 0;
-#pragma unroll
-  for (int q = 0; q < SCAN_ITEMS; ++q) tsum += cdf_fixed(wsh[wpad(threadIdx.x * SCAN_ITEMS + q)]);
-  const int l = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  u128 inc = tsum;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    u128 o = shfl_up_u128(inc, d);
-    if (l >= d) inc += o;
-  }
-  if (l == 31) wtot[wi] = inc;
-  __syncthreads();
-  if (wi == 0) {
-    u128 excl = 0;
-    if (mode == 2) {
-      excl = ((u128)C->rank_prefix[1] << 64) | (u128)C->rank_prefix[0];
-      if (tile > 0) excl += P.tile_inc[tile - 1];
-    } else {
-      // tile aggregate; publish it, then warp-parallel look-back over 32
-      // predecessors at a time (closest inclusive prefix ends the walk)
-      u128 agg = 0;
-      for (int w = 0; w < SCAN_BLOCK / 32; ++w) agg += wtot[w];
-      if (l == 0) {
-        if (tile == 0) {
-          P.tile_inc[0] = agg;
-          __threadfence();
-          st_release_u32(P.tile_status + 0, (tag << 2) | 2u);
-        } else {
-          P.tile_agg[tile] = agg;
-          __threadfence();
-          st_release_u32(P.tile_status + tile, (tag << 2) | 1u);
-        }
-      }
-      if (tile > 0) {
-        i64 pbase = tile - 1;
-        while (true) {
-          i64 p = pbase - l;
-          u32 s = 0;
-          if (p >= 0) {
-            do {
-              s = ld_acquire_u32(P.tile_status + p);
-            } while ((s >> 2) != tag || (s & 3u) == 0u);
-          }
-          bool incl = (p >= 0) && ((s & 3u) == 2u);
-          unsigned ball = __ballot_sync(0xffffffffu, incl);
-          int f = ball ? (__ffs(ball) - 1) : 32;
-          u128 v = 0;
-          if (p >= 0 && l <= f)
-            v = (l == f) ? *((volatile u128*)(P.tile_inc + p)) : *((volatile u128*)(P.tile_agg + p));
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            u64 lo = (u64)v, hi = (u64)(v >> 64);
-            u64 olo = __shfl_xor_sync(0xffffffffu, lo, o);
-            u64 ohi = __shfl_xor_sync(0xffffffffu, hi, o);
-            v += ((u128)ohi << 64) | (u128)olo;
-          }
-          excl += v;
-          if (ball) break;
-          pbase -= 32;
-        }
-        if (l == 0) {
-          P.tile_inc[tile] = excl + agg;
-          __threadfence();
-          st_release_u32(P.tile_status + tile, (tag << 2) | 2u);
-        }
-      }
-    }
-    if (l == 0) s_excl = excl;
-  }
-  if (mode == 1) return;
-  __syncthreads();
-  u128 woff = 0, tagg = 0;
-  for (int w = 0; w < SCAN_BLOCK / 32; ++w) {
-    if (w < wi) woff += wtot[w];
-    tagg += wtot[w];
-  }
-  const u128 excl = s_excl + woff + (inc - tsum);
-  const i64 i0 = base + (i64)threadIdx.x * SCAN_ITEMS;
-  const i64 ng = P.n_global, off = P.idx_off, lo = P.slot_lo, cap = P.slot_cap;
-  const double nd = (double)ng, eps = nd * 8.881784197001252e-16;   // n * 2^-50
-  // the tile's slot range: start of its first item .. end of its last item
-  __shared__ long long s_jrange[2];
-  __shared__ int stage[SCAN_TILE + SCAN_TILE / SCAN_ITEMS];
-  __shared__ int s_wmax[SCAN_BLOCK / 32];
-  if (threadIdx.x == 0) {
-    const i64 tl = min(n, base + (i64)SCAN_TILE) - 1;
-    s_jrange[0] = (off + base == 0) ? 0 : first_slot_fast(cdf_round(s_excl), u, ng, nd, eps);
-    s_jrange[1] = (off + tl == ng - 1) ? ng
-                                       : first_slot_fast(cdf_round(s_excl + tagg), u, ng, nd, eps);
-  }
-  __syncthreads();
-  const i64 tj0 = s_jrange[0], tj1 = s_jrange[1];
-  // 1) per item: its first slot relative to tj0 if it receives any slot
-  //    (the run head), else INT_MAX; stored in place of the item's weight
-  int* hp = reinterpret_cast<int*>(wsh);
-  {
-    const int k0 = (int)threadIdx.x * SCAN_ITEMS;
-    int jr = 0;
-    if (i0 < n) jr = (int)(((off + i0 == 0) ? 0 : first_slot_fast(cdf_round(excl), u, ng, nd, eps)) - tj0);
-    u128 run = excl;
-    for (int q = 0; q < SCAN_ITEMS; ++q) {
-      const i64 i = i0 + q;
-      int h = INT_MAX;
-      if (i < n) {
-        run += cdf_fixed(wsh[wpad(k0 + q)]);
-        const int jend =
-            (int)(((off + i == ng - 1) ? ng : first_slot_fast(cdf_round(run), u, ng, nd, eps)) - tj0);
-        if (jend > jr) h = jr;
-        jr = jend;
-      }
-      hp[wpad(k0 + q)] = h;
-    }
-  }
-  __syncthreads();
-  // 2) the tile's slots in chunks of SCAN_TILE: mark the run heads, block
-  //    max-scan (ancestor of a slot = last head at or before it), write out
-  //    coalesced
-  bool oob = false;
-  const i64 m_slots = tj1 - tj0;
-  const int lane_s = threadIdx.x & 31, warp_s = threadIdx.x >> 5;
-  int carry = -1;
-  for (i64 c0 = 0; c0 < m_slots; c0 += SCAN_TILE) {
-    const int k0 = (int)threadIdx.x * SCAN_ITEMS;
-#pragma unroll
-    for (int q = 0; q < SCAN_ITEMS; ++q) stage[wpad(k0 + q)] = -1;
-    __syncthreads();
-#pragma unroll
-    for (int q = 0; q < SCAN_ITEMS; ++q) {
-      const int h = hp[wpad(k0 + q)];
-      if ((i64)h >= c0 && (i64)h < c0 + SCAN_TILE) stage[wpad((int)((i64)h - c0))] = k0 + q;
-    }
-    __syncthreads();
-    int tmax = -1;
-#pragma unroll
-    for (int q = 0; q < SCAN_ITEMS; ++q) tmax = max(tmax, stage[wpad(k0 + q)]);
-    int incl = tmax;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const int o = __shfl_up_sync(0xffffffffu, incl, d);
-      if (lane_s >= d) incl = max(incl, o);
-    }
-    if (lane_s == 31) s_wmax[warp_s] = incl;
-    int excl_l = __shfl_up_sync(0xffffffffu, incl, 1);
-    if (lane_s == 0) excl_l = -1;
-    __syncthreads();
-    int prev = carry, total = carry;
-#pragma unroll
-    for (int w = 0; w < SCAN_BLOCK / 32; ++w) {
-      if (w < warp_s) prev = max(prev, s_wmax[w]);
-      total = max(total, s_wmax[w]);
-    }
-    int runm = max(prev, excl_l);
-#pragma unroll
-    for (int q = 0; q < SCAN_ITEMS; ++q) {
-      runm = max(runm, stage[wpad(k0 + q)]);
-      stage[wpad(k0 + q)] = runm;
-    }
-    __syncthreads();
-    const int cm = (int)min((i64)SCAN_TILE, m_slots - c0);
-    for (int k = threadIdx.x; k < cm; k += SCAN_BLOCK) {
-      const i64 kk = tj0 + c0 + k - lo;
-      if (kk >= 0 && kk < cap) P.anc_out[kk] = (int)(base + stage[wpad(k)]);
-      else oob = true;
-    }
-    carry = total;
-    __syncthreads();
-  }
-  if (oob) set_flag(C, PCS_FLAG_CAPACITY);
-}
-
 // ===========================================================================
 // first slot at/above the cdf value RN64(Pc) 2^-120 (first_slot_fast(cdf_round(Pc))):
 // float64 estimate from the top 64 bits of Pc, |error| <= n (3 2^-53 + 2^-63)
@@ -1343,7 +1134,12 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
   // pcSIR frames with prior weights resample per particle (KIND 2), the others
   // per cell (KIND 1); both are in the frame's launch sequence
   if (KIND == 1 ? C->pc_prior != 0 : (P.method == 1 && C->pc_prior == 0)) return;
+  // sharded filter (pcs_shard.cuh): mode 1 = pass 1 only (per-CTA totals ->
+  // rank total), mode 2 = pass 2 only, its prefix offset by the exact weight
+  // of the preceding ranks and its slots written from the rank's first slot
+  const int mode = P.scan_mode;
   if (!C->do_resample) {   // identity ancestors; the particles keep their weights
+    if (mode != 0) return;   // (the shard pack kernel installs the identity)
     const bool keep = C->prior_nonuniform;
     const double Sf = C->Sf;
     for (i64 i = t0 * RS_TILE + threadIdx.x; i < min(n, t1 * RS_TILE); i += SCAN_BLOCK) {
@@ -1356,12 +1152,15 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
   RS_PROBE(0);
   const E* src = (KIND == 1) ? (const E*)(const void*)P.pslot : (const E*)(const void*)P.ll;
   const int mt = (int)(t1 - t0);      // tiles of this CTA; loads L = 0..2 mt-1 (two passes)
+  const int L0 = (mode == 2) ? mt : 0, Lend = (mode == 1) ? mt : 2 * mt;
+  // load L (absolute: tile t0 + L % mt) goes to ring buffer / mbarrier
+  // (L - L0) & 1 and completes phase ((L - L0) >> 1) & 1 of that barrier
   auto issue = [&](int L) {           // thread 0 only
     const i64 tile = t0 + (L % mt);
     const i64 b0 = tile * RS_TILE;
     const i64 cnt = min((i64)RS_TILE, n - b0);
     const u32 bytes = (u32)(((cnt * (i64)sizeof(E)) + 15) & ~(i64)15);
-    tma_load_1d(ring[L & 1], src + b0, bytes, &bar[L & 1]);
+    tma_load_1d(ring[(L - L0) & 1], src + b0, bytes, &bar[(L - L0) & 1]);
   };
   if (threadIdx.x == 0) {
     mbar_init(&bar[0], 1);
@@ -1369,7 +1168,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  if (threadIdx.x == 0 && mt > 0) issue(0);
+  if (threadIdx.x == 0 && mt > 0) issue(L0);
   // exact weight of item k of a ring buffer (nv = valid items of its tile)
   auto weight = [&](const E* buf, int k, int nv) -> u128 {
     if (k >= nv) return 0;
@@ -1379,16 +1178,16 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
   auto tile_items = [&](i64 tile) -> int { return (int)min((i64)RS_TILE, n - tile * RS_TILE); };
   // ---- pass 1: this CTA's exact total ----
   u128 acc = 0;
-  for (int L = 0; L < mt; ++L) {
+  for (int L = 0; L < (mode == 2 ? 0 : mt); ++L) {   // (L0 == 0 here)
     mbar_wait(&bar[L & 1], (u32)((L >> 1) & 1));
-    if (threadIdx.x == 0 && L + 1 < 2 * mt) issue(L + 1);
+    if (threadIdx.x == 0 && L + 1 < Lend) issue(L + 1);
     const E* buf = ring[L & 1];
     const int nv = tile_items(t0 + L);
 #pragma unroll 5
     for (int q = 0; q < RS_ITEMS; ++q) acc += weight(buf, threadIdx.x * RS_ITEMS + q, nv);
     __syncthreads();   // buffer L & 1 is free for load L + 2
   }
-  {
+  if (mode != 2) {
     u128 v = acc;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1403,9 +1202,10 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
       P.cta_agg[cta] = tot;
       __threadfence();
     }
+    if (mode == 1) return;   // (k_shard_total adds the CTA totals)
   }
   RS_PROBE(1);
-  grid_barrier(C, G);
+  if (mode == 0) grid_barrier(C, G);   // (mode 2: the totals come from the mode-1 launch)
   RS_PROBE(2);
   // ---- exclusive prefix of this CTA: aggregates of the CTAs before it ----
   u128 pre;
@@ -1421,21 +1221,24 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(
     __syncthreads();
     pre = 0;
     for (int w = 0; w < SCAN_BLOCK / 32; ++w) pre += wtot[w];
+    if (mode == 2) pre += ((u128)C->rank_prefix[1] << 64) | (u128)C->rank_prefix[0];
     __syncthreads();
   }
   RS_PROBE(3);
   // ---- pass 2: per tile, item prefixes -> run heads -> ancestors ----
-  const i64 ng = P.n_global, off = P.idx_off, lo = P.slot_lo, cap = P.slot_cap;
+  const i64 ng = P.n_global, off = P.idx_off, cap = P.slot_cap;
+  const i64 lo = (mode == 2) ? C->shard_lo : P.slot_lo;
   const double nd = (double)ng, eps = nd * 8.881784197001252e-16;   // n * 2^-50
   const double kappa = nd * 1.0842021724855044e-19;                  // n * 2^-63
   bool oob = false;
   const int k0 = (int)threadIdx.x * RS_ITEMS;
   i64 tj_prev = 0;
   for (int L = mt; L < 2 * mt; ++L) {
-    mbar_wait(&bar[L & 1], (u32)((L >> 1) & 1));
-    if (threadIdx.x == 0 && L + 1 < 2 * mt) issue(L + 1);
-    const E* buf = ring[L & 1];
-    int* hp = (KIND == 1) ? reinterpret_cast<int*>(ring[L & 1]) : hp_own;
+    const int LL = L - L0;   // load index in this launch
+    mbar_wait(&bar[LL & 1], (u32)((LL >> 1) & 1));
+    if (threadIdx.x == 0 && L + 1 < Lend) issue(L + 1);
+    const E* buf = ring[LL & 1];
+    int* hp = (KIND == 1) ? reinterpret_cast<int*>(ring[LL & 1]) : hp_own;
     const i64 base = (t0 + (L - mt)) * RS_TILE;
     const int nv = tile_items(t0 + (L - mt));
     // local index of the globally last item (its run ends at slot ng), -1 if not here

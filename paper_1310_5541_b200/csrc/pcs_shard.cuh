@@ -1,17 +1,30 @@
-// pcs_shard.cuh — particle-sharded giant filter (config 5) helpers.
+// pcs_shard.cuh — particle-sharded giant filter (config 5).
 //
-// Each rank holds a contiguous global index range of particles. Per frame:
-//   k_pc_step1 (local, Philox on global indices) -> local exact cell sums
-//   k_shard_bbox         local occupied-cell bounding box  (all-reduce MIN/MAX)
-//   k_shard_export       window cells -> 16 int64 limbs per cell, table zeroed
-//   NCCL all-reduce SUM  (limbs: exact, associative -> P-invariant)
-//   k_shard_import       global sums back into the table + occupied list
-//   k_pc_bins            identical on every rank (same inputs, same code)
-//   k_scan_emit mode 1   rank-local exact prefix; rank totals all-gathered
-//   k_scan_emit mode 2   global slots for this rank's particles
-//   NCCL all-to-all      resampled states to the ranks owning their slots
-// The int128 per-cell sums are carried as three 42-bit limbs so an int64
-// all-reduce over up to 2^21 ranks cannot overflow and the total is exact.
+// Rank r of P holds the global particles [r n, (r+1) n) and owns the output
+// slots [r n, (r+1) n). Per frame, every step stream-ordered with fixed-size
+// collectives and no host synchronisation (graph-capturable):
+//   k_pc_step1 (local; Philox on global indices) -> local exact cell sums
+//   k_shard_bbox       local occupied-cell box       -> box (all-reduce MAX)
+//   k_shard_export     box-window cells -> 16 int64 limbs each, in a fixed
+//                      wcap-cell buffer               -> limbs (all-reduce SUM)
+//   k_shard_import + k_pc_cells + k_pc_bins   identical on every rank
+//   k_sys_resample mode 1 + k_shard_total     exact rank weight total
+//                                                     -> totals (all-gather)
+//   k_shard_ranges     every rank's emitted slot range from the gathered
+//                      totals (monotone systematic ancestors: contiguous)
+//   k_sys_resample mode 2 (rank prefix)       ancestors of this rank's slots
+//   k_shard_pack       own slots keep their ancestors in place; the head /
+//                      tail slots owned by rank r-1 / r+1 are packed
+//                      (states) into fixed bcap-slot buffers -> send/recv
+//   k_shard_unpack     received states appended after the local particles
+//                      (index n + q); their slots point at them
+// Only boundary states move (the weight-share imbalance between ranks, not
+// the whole state); the limb all-reduce is exact and associative, so every
+// result is identical for any P. Capacity checks (window > wcap, a range
+// reaching past a neighbour, boundary > bcap) are evaluated identically on
+// every rank from the same gathered totals, so all ranks raise together.
+// The int128 per-cell sums travel as three 42-bit limbs so an int64
+// all-reduce over up to 2^21 ranks cannot overflow.
 #pragma once
 #include "pcs_common.cuh"
 #include "pcs_fused.cuh"
@@ -20,14 +33,15 @@ namespace pcs {
 
 constexpr int LIMBS_PER_CELL = 16;   // count + 5 components x 3 limbs
 
-__global__ void k_shard_bbox(TrackParams P, i64* out /* ix0, ix1, iy0, iy1, n_occ */) {
+// box = (-ix0, ix1, -iy0, iy1, local occupied cells): MAX-reducible
+__global__ void k_shard_bbox(TrackParams P, i64* out) {
   __shared__ long long s[4];
   TrackCtl* C = P.ctl;
   const u32 m = C->n_occ;
   if (threadIdx.x == 0) {
-    s[0] = LLONG_MAX;
+    s[0] = LLONG_MIN;
     s[1] = LLONG_MIN;
-    s[2] = LLONG_MAX;
+    s[2] = LLONG_MIN;
     s[3] = LLONG_MIN;
   }
   __syncthreads();
@@ -35,9 +49,9 @@ __global__ void k_shard_bbox(TrackParams P, i64* out /* ix0, ix1, iy0, iy1, n_oc
   for (u32 b = threadIdx.x; b < mm; b += blockDim.x) {
     u32 cell = P.occ[b];
     long long ix = (long long)cell % P.grid.ncols, iy = (long long)cell / P.grid.ncols;
-    atomicMin(&s[0], ix);
+    atomicMax(&s[0], -ix);
     atomicMax(&s[1], ix);
-    atomicMin(&s[2], iy);
+    atomicMax(&s[2], -iy);
     atomicMax(&s[3], iy);
   }
   __syncthreads();
@@ -48,10 +62,28 @@ __global__ void k_shard_bbox(TrackParams P, i64* out /* ix0, ix1, iy0, iy1, n_oc
   }
 }
 
-__global__ void k_shard_export(TrackParams P, i64 x0, i64 y0, i64 nx, i64 ny, i64* __restrict__ limbs) {
+// the global window from the reduced box; false (and the capacity flag) if
+// it does not fit the fixed limb buffer
+__device__ __forceinline__ bool shard_window(const i64* box, i64 wcap, i64& x0, i64& y0, i64& nx,
+                                             i64& ny) {
+  x0 = -box[0];
+  y0 = -box[2];
+  nx = box[1] - x0 + 1;
+  ny = box[3] - y0 + 1;
+  return nx >= 1 && ny >= 1 && nx * ny <= wcap;
+}
+
+__global__ void k_shard_export(TrackParams P, const i64* __restrict__ box, i64 wcap,
+                               i64* __restrict__ limbs) {
+  i64 x0, y0, nx, ny;
+  const bool ok = shard_window(box, wcap, x0, y0, nx, ny);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    P.ctl->n_occ = 0;   // import rebuilds the list
+    if (!ok) set_flag(P.ctl, PCS_FLAG_CAPACITY);
+  }
+  if (!ok) return;
   const i64 W = nx * ny;
   const u64 M42 = (1ull << 42) - 1ull;
-  if (blockIdx.x == 0 && threadIdx.x == 0) P.ctl->n_occ = 0;   // import rebuilds the list
   for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < W; q += (i64)gridDim.x * blockDim.x) {
     i64 ix = x0 + q % nx, iy = y0 + q / nx;
     i64* L = limbs + q * LIMBS_PER_CELL;
@@ -74,8 +106,10 @@ __global__ void k_shard_export(TrackParams P, i64 x0, i64 y0, i64 nx, i64 ny, i6
   }
 }
 
-__global__ void k_shard_import(TrackParams P, i64 x0, i64 y0, i64 nx, i64 ny,
+__global__ void k_shard_import(TrackParams P, const i64* __restrict__ box, i64 wcap,
                                const i64* __restrict__ limbs) {
+  i64 x0, y0, nx, ny;
+  if (!shard_window(box, wcap, x0, y0, nx, ny)) return;
   const i64 W = nx * ny;
   TrackCtl* C = P.ctl;
   for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < W; q += (i64)gridDim.x * blockDim.x) {
@@ -96,19 +130,145 @@ __global__ void k_shard_import(TrackParams P, i64 x0, i64 y0, i64 nx, i64 ny,
   }
 }
 
-// out[c*count + q] = in[c*ld + anc[q]]
-__global__ void k_shard_gather(const float* __restrict__ sin, i64 ld, const int* __restrict__ anc,
-                               i64 count, float* __restrict__ out) {
-  for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < count; q += (i64)gridDim.x * blockDim.x) {
-    i64 src = anc[q];
+__device__ __forceinline__ void u128_to_limbs(u128 v, i64* out) {
+  const u64 M42 = (1ull << 42) - 1ull;
+  out[0] = (i64)((u64)v & M42);
+  out[1] = (i64)((u64)(v >> 42) & M42);
+  out[2] = (i64)(u64)(v >> 84);
+}
+__device__ __forceinline__ u128 limbs_to_u128(const i64* L) {
+  return (u128)(u64)L[0] + ((u128)(u64)L[1] << 42) + ((u128)(u64)L[2] << 84);
+}
+
+// exact rank weight total = sum of the per-CTA totals of k_sys_resample mode 1
+__global__ void k_shard_total(TrackParams P, int nagg, i64* __restrict__ total) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  u128 t = 0;
+  if (P.ctl->do_resample)
+    for (int c = 0; c < nagg; ++c) t += P.cta_agg[c];
+  u128_to_limbs(t, total);
+}
+
+// every rank's emitted slot range [lo_q, hi_q) from the gathered totals,
+// this rank's prefix / range / boundary counts, and the capacity checks
+// (the same on every rank: same inputs)
+__global__ void k_shard_ranges(TrackParams P, const i64* __restrict__ totals, int rank, int world,
+                               i64 bcap) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  TrackCtl* C = P.ctl;
+  const i64 n = P.n, ng = P.n_global;
+  if (!C->do_resample) {
+    C->rank_prefix[0] = C->rank_prefix[1] = 0;
+    C->shard_lo = (i64)rank * n;
+    C->shard_hi = (i64)(rank + 1) * n;
+    C->shard_send[0] = C->shard_send[1] = 0;
+    C->shard_recv[0] = C->shard_recv[1] = 0;
+    return;
+  }
+  const double u = C->u, nd = (double)ng, eps = nd * 8.881784197001252e-16;
+  u128 pre = 0;
+  i64 lo_q = 0;
+  bool bad = false;
+  i64 lo_r = 0, hi_r = 0, hi_prev = 0, lo_next = ng;
+  for (int q = 0; q < world; ++q) {
+    const u128 tq = limbs_to_u128(totals + 3 * q);
+    const u128 pnext = pre + tq;
+    const i64 hi_q = (q == world - 1) ? ng : first_slot_fast(cdf_round(pnext), u, ng, nd, eps);
+    // ranges reach at most into the neighbouring ranks' slots; boundary
+    // chunks fit the exchange buffers; the range fits the ancestor buffer
+    const i64 own0 = (i64)q * n, own1 = (i64)(q + 1) * n;
+    if (lo_q < own0 - n || hi_q > own1 + n || hi_q - lo_q > P.slot_cap) bad = true;
+    if (max((i64)0, min(hi_q, own0) - lo_q) > bcap || max((i64)0, hi_q - max(lo_q, own1)) > bcap)
+      bad = true;
+    if (q == rank) {
+      C->rank_prefix[0] = (u64)pre;
+      C->rank_prefix[1] = (u64)(pre >> 64);
+      lo_r = lo_q;
+      hi_r = hi_q;
+    }
+    if (q == rank - 1) hi_prev = hi_q;
+    if (q == rank + 1) lo_next = lo_q;
+    pre = pnext;
+    lo_q = hi_q;
+  }
+  const i64 own0 = (i64)rank * n, own1 = (i64)(rank + 1) * n;
+  C->shard_lo = lo_r;
+  C->shard_hi = hi_r;
+  C->shard_send[0] = max((i64)0, min(hi_r, own0) - lo_r);
+  C->shard_send[1] = max((i64)0, hi_r - max(lo_r, own1));
+  C->shard_recv[0] = (rank > 0) ? max((i64)0, hi_prev - own0) : 0;
+  C->shard_recv[1] = (rank < world - 1) ? max((i64)0, own1 - lo_next) : 0;
+  if (bad) set_flag(C, PCS_FLAG_CAPACITY);
+}
+
+// boundary buffers: float32 [5][bcap] + one slot holding the count (int bits)
+__device__ __forceinline__ void put_count(float* buf, i64 bcap, i64 cnt) {
+  buf[5 * bcap] = __int_as_float((int)cnt);
+}
+__device__ __forceinline__ i64 get_count(const float* buf, i64 bcap) {
+  return (i64)__float_as_int(buf[5 * bcap]);
+}
+
+// own slots keep their ancestors (the next frame's gather indices); head /
+// tail slots of the neighbours are packed as states
+__global__ void k_shard_pack(TrackParams P, int rank, float* __restrict__ send_prev,
+                             float* __restrict__ send_next, i64 bcap) {
+  TrackCtl* C = P.ctl;
+  const i64 n = P.n, ld = P.ld;
+  const float* cur = (C->k & 1) ? P.buf1 : P.buf0;   // this frame's propagated states
+  const i64 tid = blockIdx.x * (i64)blockDim.x + threadIdx.x, nthr = (i64)gridDim.x * blockDim.x;
+  const bool cap = (C->flags & PCS_FLAG_CAPACITY) != 0;
+  if (!C->do_resample || cap) {   // identity ancestors, nothing to send
+    for (i64 i = tid; i < n; i += nthr) P.anc[i] = (int)i;
+    if (tid == 0) {
+      put_count(send_prev, bcap, 0);
+      put_count(send_next, bcap, 0);
+    }
+    return;
+  }
+  const i64 lo = C->shard_lo, hi = C->shard_hi;
+  const i64 own0 = (i64)rank * n, own1 = own0 + n;
+  for (i64 s = tid; s < hi - lo; s += nthr) {
+    const i64 j = lo + s;
+    const int src = P.anc_out[s];
+    if (j < own0) {
 #pragma unroll
-    for (int c = 0; c < 5; ++c) out[c * count + q] = __ldg(sin + c * ld + src);
+      for (int c = 0; c < 5; ++c) send_prev[c * bcap + (j - lo)] = cur[c * ld + src];
+    } else if (j >= own1) {
+#pragma unroll
+      for (int c = 0; c < 5; ++c) send_next[c * bcap + (j - own1)] = cur[c * ld + src];
+    } else {
+      P.anc[j - own0] = src;
+    }
+  }
+  if (tid == 0) {
+    put_count(send_prev, bcap, C->shard_send[0]);
+    put_count(send_next, bcap, C->shard_send[1]);
   }
 }
 
-__global__ void k_shard_set_prefix(TrackCtl* C, u64 lo, u64 hi) {
-  C->rank_prefix[0] = lo;
-  C->rank_prefix[1] = hi;
+// the received boundary states go after the local particles (index n + q,
+// n + bcap + q) of the next frame's input; the slots they fill point at them
+__global__ void k_shard_unpack(TrackParams P, const float* __restrict__ recv_prev,
+                               const float* __restrict__ recv_next, i64 bcap) {
+  TrackCtl* C = P.ctl;
+  if (!C->do_resample || (C->flags & PCS_FLAG_CAPACITY)) return;
+  const i64 n = P.n, ld = P.ld;
+  float* cur = (C->k & 1) ? P.buf1 : P.buf0;
+  const i64 cp = C->shard_recv[0], cn = C->shard_recv[1];
+  const i64 tid = blockIdx.x * (i64)blockDim.x + threadIdx.x, nthr = (i64)gridDim.x * blockDim.x;
+  if (tid == 0 && ((cp && get_count(recv_prev, bcap) != cp) || (cn && get_count(recv_next, bcap) != cn)))
+    set_flag(C, PCS_FLAG_CAPACITY);   // (a protocol mismatch; cannot happen with one plan)
+  for (i64 q = tid; q < cp; q += nthr) {
+#pragma unroll
+    for (int c = 0; c < 5; ++c) cur[c * ld + n + q] = recv_prev[c * bcap + q];
+    P.anc[q] = (int)(n + q);
+  }
+  for (i64 q = tid; q < cn; q += nthr) {
+#pragma unroll
+    for (int c = 0; c < 5; ++c) cur[c * ld + n + bcap + q] = recv_next[c * bcap + q];
+    P.anc[n - cn + q] = (int)(n + bcap + q);
+  }
 }
 
 }  // namespace pcs

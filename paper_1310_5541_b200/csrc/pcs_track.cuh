@@ -3,7 +3,7 @@
 // One frame of sir_track (filtering.py:176-182, sis_step :62-72) with
 // ResampleConfig(threshold_fraction=1.0, "systematic"): gather + propagate +
 // per-particle likelihood -> max -> exact normaliser -> exact estimate/ESS ->
-// decision -> single-pass exact-prefix systematic resampling (k_scan_emit).
+// decision -> exact-prefix systematic resampling (k_sys_resample).
 // Canonical arithmetic is shared with pcSIR (pcs_fused.cuh) and with the
 // general path, so pcSIR with one particle per cell equals SIR bit-for-bit.
 #pragma once

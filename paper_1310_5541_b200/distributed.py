@@ -2,23 +2,31 @@
 single-process, SPEC.md:14).
 
 One filter of N particles is split across the ranks of a torch.distributed
-group (one process per GPU, NCCL over NVLink): rank r owns the contiguous
-global index range [r*n, (r+1)*n). Per frame the ranks exchange exactly what
-the algorithm needs and nothing else:
+group (one process per GPU, NCCL over NVLink): rank r holds the global
+particles [r n, (r+1) n) and owns the output slots [r n, (r+1) n). Per frame
+the ranks exchange exactly what the algorithm needs, with fixed-size
+stream-ordered collectives and no host synchronisation (pcs_shard.cuh):
 
-  1. all-reduce MIN/MAX of the local occupied-cell bounding boxes (4 ints);
+  1. all-reduce MAX of the occupied-cell bounding boxes (5 int64);
   2. all-reduce SUM of the per-cell accumulators over that window, carried as
-     int64 limbs of the exact int128 sums — integer addition is associative,
-     so the dummies are bit-identical for every rank count;
-  3. every rank runs the same bins stage (dummies, likelihood per occupied
-     cell, normaliser, estimate, ESS, resampling decision) on the same sums;
-  4. all-gather of the ranks' exact cumulative-weight totals (u128) gives each
-     rank its global cdf offset (distributed systematic resampling);
-  5. all-to-all of the resampled states whose output slot belongs to another
-     rank (monotone ancestors: one contiguous chunk per rank pair).
+     int64 limbs of the exact int128 sums in a fixed wcap-cell buffer —
+     integer addition is associative, so the dummies are bit-identical for
+     every rank count;
+  3. every rank runs the same cell / bins stage (dummies, likelihood per
+     occupied cell, normaliser, estimate, ESS, resampling decision);
+  4. all-gather of the ranks' exact cumulative-weight totals (u128 as three
+     42-bit limbs); every rank derives every rank's slot range on the device
+     (distributed systematic resampling, monotone ancestors);
+  5. each rank emits the ancestors of its own slot range: slots it owns keep
+     their ancestors in place (the next frame gathers them directly); only
+     the boundary slots owned by rank r-1 / r+1 travel, as states, in fixed
+     bcap-slot buffers (grouped send / recv with the two neighbours).
 
 Philox counters use the global particle index, so the random draws — and
 therefore every result — are the same for any number of ranks as for one GPU.
+Capacity limits (window, boundary size) are evaluated identically on every
+rank; all flags are all-reduced at the end so every rank raises the same
+error.
 
 The per-rank compute is behind ``ShardOps``: ``DeviceShardOps`` (the product:
 C-ABI kernels on the rank's GPU) or a CPU stand-in used by the gloo tests.
@@ -86,35 +94,37 @@ def exchange_plan(ranges, n_global, p):
 
 
 class ShardOps:
-    """One rank's compute for the sharded step (see DeviceShardOps)."""
+    """One rank's compute for the sharded step (see DeviceShardOps). Every
+    method returns / takes tensors on the ops' device; nothing synchronises
+    the host until flags() / outputs()."""
 
-    def begin(self, cfg, height, width, idx_off, n_global, slot_cap, seed):
+    def begin(self, cfg, height, width, rank, world, n_global, wcap, bcap, seed):
         raise NotImplementedError
 
     def step1(self, frame, k):
-        """propagate + exact local cell sums; -> (bbox[4] ix0, ix1, iy0, iy1, n_occupied)"""
+        """propagate + exact local cell sums -> box int64[5] (MAX-reducible)"""
         raise NotImplementedError
 
-    def export(self, window):
+    def export(self, box):
+        """window cells of the reduced box -> limbs int64[wcap * 16] (SUM-reducible)"""
         raise NotImplementedError
 
-    def import_bins(self, window, limbs):
+    def import_bins(self, box, limbs):
         raise NotImplementedError
 
-    def scan(self):
-        """-> (exact local cumulative-weight total as int, do_resample)"""
+    def total(self):
+        """-> int64[3]: the rank's exact cumulative weight (42-bit limbs)"""
         raise NotImplementedError
 
-    def emit(self, prefix, slot_lo):
+    def emit(self, totals):
+        """gathered totals int64[world * 3] -> (send_prev, send_next) float32[5 bcap + 1]"""
         raise NotImplementedError
 
-    def gather(self, first, count):
+    def unpack(self, recv_prev, recv_next):
         raise NotImplementedError
 
-    def set_states(self, soa):
-        raise NotImplementedError
-
-    def advance(self):
+    def flags(self):
+        """-> PCS_FLAG_* of this rank (host int; synchronises)"""
         raise NotImplementedError
 
     def outputs(self):
@@ -125,16 +135,21 @@ class ShardOps:
 class DeviceShardOps(ShardOps):
     """Product implementation: the rank's GPU through the C ABI (pcs_shard_*)."""
 
-    def __init__(self, n_frames):
+    def __init__(self, n_frames, ctx=None):
         self.n_frames = n_frames
+        self.ctx = ctx if ctx is not None else _lib.ctx()   # pcs_ctx handle (one per rank)
 
-    def begin(self, cfg, height, width, idx_off, n_global, slot_cap, seed):
+    def begin(self, cfg, height, width, rank, world, n_global, wcap, bcap, seed):
         self.dev = _lib.device()
-        self.n_local = cfg.n_particles
-        self.est = torch.empty((self.n_frames, 5), dtype=torch.float64, device=self.dev)
-        self.ess = torch.empty(self.n_frames, dtype=torch.float64, device=self.dev)
-        self.res = torch.empty(self.n_frames, dtype=torch.uint8, device=self.dev)
-        self.occ = torch.empty(self.n_frames, dtype=torch.int64, device=self.dev)
+        dev = self.dev
+        self.est = torch.empty((self.n_frames, 5), dtype=torch.float64, device=dev)
+        self.ess = torch.empty(self.n_frames, dtype=torch.float64, device=dev)
+        self.res = torch.empty(self.n_frames, dtype=torch.uint8, device=dev)
+        self.occ = torch.empty(self.n_frames, dtype=torch.int64, device=dev)
+        self.box = torch.empty(5, dtype=torch.int64, device=dev)
+        self.limbs = torch.empty(wcap * LIMBS, dtype=torch.int64, device=dev)
+        self.tot = torch.empty(3, dtype=torch.int64, device=dev)
+        self.send = [torch.zeros(5 * bcap + 1, dtype=torch.float32, device=dev) for _ in range(2)]
         c = _lib.PcsTrackCfg()
         c.method = 1
         c.placement = 1 if cfg.placement.value == "coc" else 0
@@ -146,65 +161,54 @@ class DeviceShardOps(ShardOps):
         c.seed = seed
         c.frame0 = 0
         c.use_graph = 0
-        self.cfg_c = c
-        _lib.check(_lib.lib().pcs_shard_begin(_lib.ctx(), ctypes.byref(c), height, width, idx_off,
-                                              n_global, slot_cap, _lib.stream()),
+        c.threshold_fraction = 1.0
+        c.weighted_com = 1 if getattr(cfg, "weighted_com", False) else 0
+        _lib.check(_lib.lib().pcs_shard_begin(self.ctx, ctypes.byref(c), height, width, rank,
+                                              world, n_global, wcap, bcap, _lib.stream()),
                    "pcs_shard_begin")
 
     def step1(self, frame, k):
-        box = (ctypes.c_int64 * 5)()
         _lib.check(_lib.lib().pcs_shard_step1(
-            _lib.ctx(), _lib.ptr(frame), k, _lib.ptr(self.est[k:]), _lib.ptr(self.ess[k:]),
-            _lib.ptr(self.res[k:]), _lib.ptr(self.occ[k:]), box, _lib.stream()), "pcs_shard_step1")
-        if box[4] > 16384:
-            raise _lib.CapacityError("more occupied cells than the fused bins stage holds")
-        return list(box[:4]), int(box[4])
+            self.ctx, _lib.ptr(frame), k, _lib.ptr(self.est[k:]), _lib.ptr(self.ess[k:]),
+            _lib.ptr(self.res[k:]), _lib.ptr(self.occ[k:]), _lib.ptr(self.box), _lib.stream()),
+            "pcs_shard_step1")
+        return self.box
 
-    def export(self, window):
-        x0, y0, nx, ny = window
-        limbs = torch.empty((nx * ny, LIMBS), dtype=torch.int64, device=self.dev)
-        _lib.check(_lib.lib().pcs_shard_export(_lib.ctx(), x0, y0, nx, ny, _lib.ptr(limbs),
+    def export(self, box):
+        _lib.check(_lib.lib().pcs_shard_export(self.ctx, _lib.ptr(box), _lib.ptr(self.limbs),
                                                _lib.stream()), "pcs_shard_export")
-        return limbs
+        return self.limbs
 
-    def import_bins(self, window, limbs):
-        x0, y0, nx, ny = window
-        _lib.check(_lib.lib().pcs_shard_import_bins(_lib.ctx(), x0, y0, nx, ny, _lib.ptr(limbs),
+    def import_bins(self, box, limbs):
+        _lib.check(_lib.lib().pcs_shard_import_bins(self.ctx, _lib.ptr(box), _lib.ptr(limbs),
                                                     _lib.stream()), "pcs_shard_import_bins")
 
-    def scan(self):
-        lo, hi, dr = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_int32()
-        _lib.check(_lib.lib().pcs_shard_scan(_lib.ctx(), ctypes.byref(lo), ctypes.byref(hi),
-                                             ctypes.byref(dr), _lib.stream()), "pcs_shard_scan")
-        return (hi.value << 64) | lo.value, bool(dr.value)
+    def total(self):
+        _lib.check(_lib.lib().pcs_shard_total(self.ctx, _lib.ptr(self.tot), _lib.stream()),
+                   "pcs_shard_total")
+        return self.tot
 
-    def emit(self, prefix, slot_lo):
-        anc = ctypes.c_void_p()
-        _lib.check(_lib.lib().pcs_shard_emit(_lib.ctx(), prefix & (2 ** 64 - 1), prefix >> 64,
-                                             slot_lo, ctypes.byref(anc), _lib.stream()),
+    def emit(self, totals):
+        _lib.check(_lib.lib().pcs_shard_emit(self.ctx, _lib.ptr(totals), _lib.ptr(self.send[0]),
+                                             _lib.ptr(self.send[1]), _lib.stream()),
                    "pcs_shard_emit")
+        return self.send[0], self.send[1]
 
-    def gather(self, first, count):
-        out = torch.empty((5, count), dtype=torch.float32, device=self.dev)
-        _lib.check(_lib.lib().pcs_shard_gather(_lib.ctx(), first, count, _lib.ptr(out),
-                                               _lib.stream()), "pcs_shard_gather")
-        return out
+    def unpack(self, recv_prev, recv_next):
+        _lib.check(_lib.lib().pcs_shard_unpack(self.ctx, _lib.ptr(recv_prev), _lib.ptr(recv_next),
+                                               _lib.stream()), "pcs_shard_unpack")
 
-    def set_states(self, soa):
-        soa = soa.contiguous()
-        _lib.check(_lib.lib().pcs_shard_set_states(_lib.ctx(), _lib.ptr(soa), _lib.stream()),
-                   "pcs_shard_set_states")
-
-    def advance(self):
-        _lib.check(_lib.lib().pcs_shard_advance(_lib.ctx(), _lib.stream()), "pcs_shard_advance")
+    def flags(self):
+        out = _lib.PcsTrackResult()
+        rc = _lib.lib().pcs_track_end(self.ctx, ctypes.byref(out), _lib.stream())
+        if rc not in (0, _lib.E_CAPACITY):
+            _lib.check(rc, "pcs_track_end")
+        return int(out.flags), int(out.first_bad_frame)
 
     def outputs(self):
         torch.cuda.synchronize()
         return (self.est.cpu().numpy(), self.ess.cpu().numpy(),
                 self.res.cpu().numpy().astype(bool), self.occ.cpu().numpy())
-
-    def resample_u(self, seed, frame):
-        return float(_lib.lib().pcs_philox_resample_u(seed, frame & 0xFFFFFFFF))
 
 
 def max_over_ranks(value, group=None):
@@ -222,21 +226,38 @@ def max_over_ranks(value, group=None):
     return float(t.item())
 
 
-def _all_reduce_box(box, group, device):
-    t = torch.tensor([-box[0], box[1], -box[2], box[3]], dtype=torch.int64, device=device)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
-    v = t.tolist()
-    return -v[0], v[1], -v[2], v[3]
+def _exchange(send_prev, send_next, rank, world, group):
+    """Grouped send / receive of the boundary buffers with the two neighbours
+    (fixed sizes; an edge rank's missing neighbour contributes an empty buffer)."""
+    recv_prev = torch.zeros_like(send_prev)
+    recv_next = torch.zeros_like(send_next)
+    ops = []
+    if rank > 0:
+        ops += [dist.P2POp(dist.isend, send_prev, rank - 1, group),
+                dist.P2POp(dist.irecv, recv_prev, rank - 1, group)]
+    if rank < world - 1:
+        ops += [dist.P2POp(dist.isend, send_next, rank + 1, group),
+                dist.P2POp(dist.irecv, recv_next, rank + 1, group)]
+    if ops:
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    return recv_prev, recv_next
 
 
-def sharded_pcsir_track(frames, cfg, seed, ops, group=None, slot_slack=2.0, comm_device=None):
+def _on(t, dev):
+    return t if t.device == dev else t.to(dev)
+
+
+def sharded_pcsir_track(frames, cfg, seed, ops, group=None, wcap=1 << 16, bcap=None,
+                        comm_device=None):
     """Run pcSIR over the ranks of ``group``; every rank returns the same
-    TrackResult-like tuple (estimates, ess, resampled, likelihood_evals).
+    (estimates, ess, resampled, likelihood_evals).
 
     ``frames``: (K,H,W) float32 tensor on the rank's device (the frames are
     replicated: every rank evaluates the same occupied cells). ``cfg`` is a
     PcFilterConfig with the GLOBAL n_particles (divisible by the world size).
-    """
+    ``wcap``: cells of the limb window; ``bcap``: boundary slots exchanged
+    with each neighbour per frame (default n_local / 4)."""
     r_cfg = cfg.resampling
     if r_cfg.threshold_fraction != 1.0 or r_cfg.scheme != "systematic":
         raise ValueError("the sharded filter resamples every frame (systematic, "
@@ -247,49 +268,43 @@ def sharded_pcsir_track(frames, cfg, seed, ops, group=None, slot_slack=2.0, comm
     if n_global % p:
         raise ValueError("n_particles must be divisible by the number of ranks")
     n_local = n_global // p
+    bcap = int(bcap) if bcap else max(1, min(n_local, max(4096, n_local // 4)))
     from dataclasses import replace
     local_cfg = replace(cfg, n_particles=n_local)
     k_frames, h, w = frames.shape
-    slot_cap = int(n_local * slot_slack) + 64
-    ops.begin(local_cfg, h, w, r * n_local, n_global, slot_cap, seed)
+    ops.begin(local_cfg, h, w, r, p, n_global, int(wcap), bcap, seed)
     dev = comm_device if comm_device is not None else (
         torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl"
         else torch.device("cpu"))
     for k in range(k_frames):
-        box, _ = ops.step1(frames[k], k)
-        ix0, ix1, iy0, iy1 = _all_reduce_box(box, group, dev)
-        window = (ix0, iy0, ix1 - ix0 + 1, iy1 - iy0 + 1)
-        limbs = ops.export(window)
-        lt = limbs.to(dev)
-        dist.all_reduce(lt, op=dist.ReduceOp.SUM, group=group)
-        ops.import_bins(window, lt.to(limbs.device))
-        total, do_res = ops.scan()
-        if not do_res:
-            ops.advance()
-            continue
-        tt = torch.tensor([total & (2 ** 62 - 1), total >> 62], dtype=torch.int64, device=dev)
-        gathered = [torch.zeros_like(tt) for _ in range(p)]
-        dist.all_gather(gathered, tt, group=group)
-        totals = [int(g[0].item()) + (int(g[1].item()) << 62) for g in gathered]
-        u = ops.resample_u(seed, k)
-        ranges, prefixes = slot_ranges(totals, u, n_global, True)
-        if ranges[r][1] - ranges[r][0] > slot_cap:
-            raise _lib.CapacityError("a rank emitted more slots than its exchange buffer holds")
-        ops.emit(prefixes[r], ranges[r][0])
-        plan = exchange_plan(ranges, n_global, p)
-        send_chunks, send_sizes = [], []
-        for q in range(p):
-            first, count = plan[r][q]
-            send_sizes.append(count)
-            if count:
-                send_chunks.append(ops.gather(first, count).t().contiguous())
-        recv_sizes = [plan[q][r][1] for q in range(p)]
-        send = (torch.cat(send_chunks) if send_chunks else
-                torch.empty((0, 5), dtype=torch.float32)).to(dev)
-        recv = torch.empty((sum(recv_sizes), 5), dtype=torch.float32, device=dev)
-        dist.all_to_all_single(recv, send, output_split_sizes=recv_sizes,
-                               input_split_sizes=send_sizes, group=group)
-        assert recv.shape[0] == n_local
-        ops.set_states(recv.t().contiguous())
+        box = ops.step1(frames[k], k)
+        bc = _on(box, dev)
+        dist.all_reduce(bc, op=dist.ReduceOp.MAX, group=group)
+        box = _on(bc, box.device)
+        limbs = ops.export(box)
+        lc = _on(limbs, dev)
+        dist.all_reduce(lc, op=dist.ReduceOp.SUM, group=group)
+        ops.import_bins(box, _on(lc, limbs.device))
+        tot = ops.total()
+        parts = [torch.empty_like(_on(tot, dev)) for _ in range(p)]
+        dist.all_gather(parts, _on(tot, dev), group=group)
+        totals = _on(torch.cat(parts), tot.device)
+        send_prev, send_next = ops.emit(totals)
+        rp, rn = _exchange(_on(send_prev, dev), _on(send_next, dev), r, p, group)
+        ops.unpack(_on(rp, send_prev.device), _on(rn, send_next.device))
+    flags, first_bad = ops.flags()
+    ft = torch.tensor([flags, -first_bad if first_bad >= 0 else -(1 << 40)], dtype=torch.int64,
+                      device=dev)
+    dist.all_reduce(ft, op=dist.ReduceOp.MAX, group=group)   # every rank raises the same error
+    flags = int(ft[0].item())
+    if flags & _lib.FLAG_CAPACITY:
+        raise _lib.CapacityError("the sharded filter exceeded its exchange capacity (limb window "
+                                 "or boundary buffer); raise wcap / bcap")
+    if flags & _lib.FLAG_NONFINITE:
+        raise ValueError("likelihood values must be finite and >= 0")
+    if flags & _lib.FLAG_DEGENERATE:
+        from .filtering import DegenerateWeightsError
+        raise DegenerateWeightsError("all importance weights vanished",
+                                     frame_index=int(-ft[1].item()))
     est, ess, res, occ = ops.outputs()
     return est, ess, res, int(np.sum(occ))

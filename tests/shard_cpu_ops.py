@@ -34,24 +34,32 @@ def _round_fixed64(x, F):
 
 
 class CpuShardOps(D.ShardOps):
+    """CPU mirror of DeviceShardOps (pcs_shard.cuh): same buffers (box,
+    fixed-size limbs, 42-bit total limbs, boundary buffers with the count in
+    the last float), same ranges / capacity checks, canonical arithmetic."""
+
     def __init__(self, n_frames, frames, sigma_psf=1.5, bg=10.0, sigma_xi=10.0, hw=5):
         self.n_frames = n_frames
         self.frames = frames
         self.spot = (sigma_psf, bg, hw, sigma_xi)
 
-    def begin(self, cfg, height, width, idx_off, n_global, slot_cap, seed):
+    def begin(self, cfg, height, width, rank, world, n_global, wcap, bcap, seed):
         self.cfg = cfg
         self.n = cfg.n_particles
-        self.idx_off = idx_off
+        self.rank, self.world = rank, world
+        self.idx_off = rank * self.n
         self.n_global = n_global
+        self.wcap, self.bcap = wcap, bcap
         self.seed = seed
+        self.flag = 0
         g = cfg.grid
         self.grid = (g.origin_x, g.origin_y, g.cell_width, g.cell_height, g.n_cols, g.n_rows)
         c = cfg.init.center.as_array()
-        z = orc.init_normals(seed, self.n, offset=idx_off)
-        s = np.tile(c, (self.n, 1)).T.copy()
-        s[0] = c[0] + cfg.init.sigma * z[0]
-        s[1] = c[1] + cfg.init.sigma * z[1]
+        z = orc.init_normals(seed, self.n, offset=self.idx_off)
+        s = np.zeros((5, self.n + 2 * bcap), dtype=np.float64)
+        s[:, :self.n] = np.tile(c, (self.n, 1)).T
+        s[0, :self.n] = c[0] + cfg.init.sigma * z[0]
+        s[1, :self.n] = c[1] + cfg.init.sigma * z[1]
         self.soa = s.astype(np.float32)
         self.anc = np.arange(self.n)
         self.est = np.zeros((self.n_frames, 5))
@@ -78,13 +86,23 @@ class CpuShardOps(D.ShardOps):
                 e[1 + c] += fx[c][i]
         keys = np.array(list(self.table))
         ncol = self.grid[4]
-        return [int((keys % ncol).min()), int((keys % ncol).max()), int((keys // ncol).min()),
-                int((keys // ncol).max())], len(keys)
+        return torch.tensor([-int((keys % ncol).min()), int((keys % ncol).max()),
+                             -int((keys // ncol).min()), int((keys // ncol).max()), len(keys)],
+                            dtype=torch.int64)
 
-    def export(self, window):
-        x0, y0, nx, ny = window
+    def _window(self, box):
+        b = box.tolist()
+        x0, y0 = -b[0], -b[2]
+        nx, ny = b[1] - x0 + 1, b[3] - y0 + 1
+        return x0, y0, nx, ny, nx >= 1 and ny >= 1 and nx * ny <= self.wcap
+
+    def export(self, box):
+        x0, y0, nx, ny, ok = self._window(box)
+        limbs = np.zeros((self.wcap, D.LIMBS), dtype=np.int64)
+        if not ok:
+            self.flag |= 4
+            return torch.from_numpy(limbs.reshape(-1))
         ncol = self.grid[4]
-        limbs = np.zeros((nx * ny, D.LIMBS), dtype=np.int64)
         for f, e in self.table.items():
             q = (f // ncol - y0) * nx + (f % ncol - x0)
             limbs[q, 0] = e[0]
@@ -94,12 +112,15 @@ class CpuShardOps(D.ShardOps):
                 limbs[q, 2 + 3 * c] = (v >> 42) & M42
                 limbs[q, 3 + 3 * c] = v >> 84
         self.table = {}
-        return torch.from_numpy(limbs)
+        return torch.from_numpy(limbs.reshape(-1))
 
-    def import_bins(self, window, limbs):
-        x0, y0, nx, ny = window
+    def import_bins(self, box, limbs):
+        x0, y0, nx, ny, ok = self._window(box)
+        if not ok:
+            self.do_res = False
+            return
         ncol = self.grid[4]
-        L = limbs.numpy()
+        L = limbs.numpy().reshape(self.wcap, D.LIMBS)[: nx * ny]
         cells = {}
         for q in np.flatnonzero(L[:, 0]):
             f = (y0 + q // nx) * ncol + (x0 + q % nx)
@@ -136,37 +157,104 @@ class CpuShardOps(D.ShardOps):
         self.res[k] = self.do_res
         self.occ[k] = len(fl)
 
-    def scan(self):
-        w = np.array([self.wmap[f] for f in self.flat.tolist()], dtype=np.float32)
-        wx = _fixed(w, 120)
-        self.incl = np.cumsum(np.array(wx, dtype=object))
-        return int(self.incl[-1]), bool(self.do_res)
+    def total(self):
+        out = np.zeros(3, dtype=np.int64)
+        if self.do_res:
+            w = np.array([self.wmap[f] for f in self.flat.tolist()], dtype=np.float32)
+            wx = _fixed(w, 120)
+            self.incl = np.cumsum(np.array(wx, dtype=object))
+            t = int(self.incl[-1])
+            out[:] = [t & M42, (t >> 42) & M42, t >> 84]
+        return torch.from_numpy(out)
 
-    def emit(self, prefix, slot_lo):
+    def _buffers(self):
+        return [np.zeros(5 * self.bcap + 1, dtype=np.float32) for _ in range(2)]
+
+    @staticmethod
+    def _set_count(buf, cnt):
+        buf[-1:] = np.array([cnt], dtype=np.int32).view(np.float32)
+
+    def emit(self, totals):
+        bufs = self._buffers()
+        n, r, p, ng, bcap = self.n, self.rank, self.world, self.n_global, self.bcap
+        if not self.do_res or self.flag & 4:
+            self.anc = np.arange(n)
+            self.recv_counts = (0, 0)
+            self.next_soa = self._extended(self.prop)
+            return torch.from_numpy(bufs[0]), torch.from_numpy(bufs[1])
+        T = totals.numpy().reshape(p, 3)
+        tots = [int(T[q, 0]) + (int(T[q, 1]) << 42) + (int(T[q, 2]) << 84) for q in range(p)]
         u = orc.resample_u(self.seed, self.k)
-        anc = []
-        j = 0 if (self.idx_off == 0) else D.first_slot(D.cdf_value(prefix), u, self.n_global)
-        for i in range(self.n):
+        # every rank's range (k_shard_ranges), the same capacity checks
+        lo, pre, ranges, prefixes = 0, 0, [], []
+        for q in range(p):
+            hi = ng if q == p - 1 else D.first_slot(D.cdf_value(pre + tots[q]), u, ng)
+            own0, own1 = q * n, (q + 1) * n
+            if (lo < own0 - n or hi > own1 + n or hi - lo > n + 2 * bcap
+                    or max(0, min(hi, own0) - lo) > bcap or max(0, hi - max(lo, own1)) > bcap):
+                self.flag |= 4
+            ranges.append((lo, hi))
+            prefixes.append(pre)
+            pre += tots[q]
+            lo = hi
+        if self.flag & 4:
+            self.anc = np.arange(n)
+            self.recv_counts = (0, 0)
+            self.next_soa = self._extended(self.prop)
+            return torch.from_numpy(bufs[0]), torch.from_numpy(bufs[1])
+        lo_r, hi_r = ranges[r]
+        # ancestors of slots [lo_r, hi_r) from this rank's exact prefixes
+        anc_out = []
+        j = lo_r
+        for i in range(n):
             gi = self.idx_off + i
-            jend = self.n_global if gi == self.n_global - 1 else D.first_slot(
-                D.cdf_value(prefix + int(self.incl[i])), u, self.n_global)
-            anc.extend([i] * (jend - j))
+            jend = ng if gi == ng - 1 else D.first_slot(
+                D.cdf_value(prefixes[r] + int(self.incl[i])), u, ng)
+            anc_out.extend([i] * (jend - j))
             j = max(j, jend)
-        self.anc_out = np.array(anc, dtype=np.int64)
+        assert len(anc_out) == hi_r - lo_r
+        own0, own1 = r * n, (r + 1) * n
+        anc = np.full(n, -1, dtype=np.int64)
+        sp, sn = 0, 0
+        for s_, src in enumerate(anc_out):
+            jj = lo_r + s_
+            if jj < own0:
+                bufs[0][np.arange(5) * bcap + (jj - lo_r)] = self.prop[:, src]
+                sp += 1
+            elif jj >= own1:
+                bufs[1][np.arange(5) * bcap + (jj - own1)] = self.prop[:, src]
+                sn += 1
+            else:
+                anc[jj - own0] = src
+        self._set_count(bufs[0], sp)
+        self._set_count(bufs[1], sn)
+        self.anc = anc
+        hi_prev = ranges[r - 1][1] if r > 0 else own0
+        lo_next = ranges[r + 1][0] if r < p - 1 else own1
+        self.recv_counts = (max(0, hi_prev - own0), max(0, own1 - lo_next))
+        self.next_soa = self._extended(self.prop)
+        return torch.from_numpy(bufs[0]), torch.from_numpy(bufs[1])
 
-    def gather(self, first, count):
-        return torch.from_numpy(np.ascontiguousarray(self.prop[:, self.anc_out[first:first + count]]))
+    def _extended(self, prop):
+        s = np.zeros((5, self.n + 2 * self.bcap), dtype=np.float32)
+        s[:, :self.n] = prop
+        return s
 
-    def set_states(self, soa):
-        self.soa = soa.numpy().astype(np.float32)
-        self.anc = np.arange(self.n)
+    def unpack(self, recv_prev, recv_next):
+        n, bcap = self.n, self.bcap
+        cp, cn = self.recv_counts
+        rp, rn = recv_prev.numpy(), recv_next.numpy()
+        for q in range(cp):
+            self.next_soa[:, n + q] = rp[np.arange(5) * bcap + q]
+            self.anc[q] = n + q
+        for q in range(cn):
+            self.next_soa[:, n + bcap + q] = rn[np.arange(5) * bcap + q]
+            self.anc[n - cn + q] = n + bcap + q
+        assert (self.anc >= 0).all()
+        self.soa = self.next_soa
 
-    def advance(self):
-        self.soa = self.prop
-        self.anc = np.arange(self.n)
+    def flags(self):
+        return self.flag, -1
 
     def outputs(self):
         return self.est, self.ess, self.res, self.occ
-
-    def resample_u(self, seed, frame):
-        return orc.resample_u(seed, frame)

@@ -38,7 +38,7 @@ def _scene(k=5, width=48, seed=0):
     return np.stack(frames)
 
 
-def _run(rank, world, port, n, cpp, out_dir):
+def _run(rank, world, port, n, cpp, out_dir, bcap=None):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -54,7 +54,14 @@ def _run(rank, world, port, n, cpp, out_dir):
                             pc.DynamicsParams(0.5, 0.1, 1.0), pc.ResampleConfig(1.0, "systematic"),
                             likelihood=object(), grid=pc.BinGrid.pixel_aligned(48, 48, cpp))
     ops = CpuShardOps(len(frames), frames)
-    est, ess, res, evals = D.sharded_pcsir_track(torch.from_numpy(frames), cfg, 1234, ops)
+    try:
+        est, ess, res, evals = D.sharded_pcsir_track(torch.from_numpy(frames), cfg, 1234, ops,
+                                                     wcap=4096, bcap=bcap)
+    except Exception as err:   # every rank must raise the same error
+        np.savez(os.path.join(out_dir, f"err_w{world}_r{rank}.npz"), kind=type(err).__name__)
+        dist.barrier()
+        dist.destroy_process_group()
+        return
     if rank == 0:
         np.savez(os.path.join(out_dir, f"w{world}.npz"), est=est, ess=ess, res=res, evals=evals)
     dist.barrier()
@@ -62,19 +69,32 @@ def _run(rank, world, port, n, cpp, out_dir):
 
 
 @pytest.mark.parametrize("cpp", [1, 2])
-def test_two_ranks_equal_one_rank(tmp_path, cpp):
+def test_ranks_equal_one_rank(tmp_path, cpp):
+    """P = 2 and P = 4 reproduce P = 1 bit for bit: the exact limb all-reduce,
+    the exact rank prefixes and the boundary exchange with the neighbours."""
     n = 1200
-    for world in (1, 2):
+    for world in (1, 2, 4):
         mp.spawn(_run, args=(world, _free_port(), n, cpp, str(tmp_path)), nprocs=world, join=True)
     a = np.load(tmp_path / "w1.npz")
-    b = np.load(tmp_path / "w2.npz")
-    assert np.array_equal(a["est"], b["est"])
-    assert np.array_equal(a["ess"], b["ess"])
-    assert np.array_equal(a["res"], b["res"])
-    assert int(a["evals"]) == int(b["evals"])
+    for world in (2, 4):
+        b = np.load(tmp_path / f"w{world}.npz")
+        assert np.array_equal(a["est"], b["est"])
+        assert np.array_equal(a["ess"], b["ess"])
+        assert np.array_equal(a["res"], b["res"])
+        assert int(a["evals"]) == int(b["evals"])
     assert a["res"].all()
     truth_x = 20.0 + 0.5 * np.arange(1, 6)
     assert np.max(np.abs(a["est"][:, 0] - truth_x)) < 1.0
+
+
+def test_capacity_error_raised_on_every_rank(tmp_path):
+    """A boundary buffer too small for the slots a rank must hand to its
+    neighbour: the check is evaluated identically on every rank (same
+    gathered totals) and the flags are all-reduced, so all ranks raise."""
+    world = 4
+    mp.spawn(_run, args=(world, _free_port(), 1200, 1, str(tmp_path), 1), nprocs=world, join=True)
+    kinds = [str(np.load(tmp_path / f"err_w{world}_r{r}.npz")["kind"]) for r in range(world)]
+    assert kinds == ["CapacityError"] * world
 
 
 def test_slot_ranges_and_plan():
