@@ -1416,6 +1416,7 @@ int pcs_shard_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   TrackParams& P = T.P;
   P.idx_off = (i64)rank * cfg->n_particles;
   P.n_global = n_global;
+  P.thresh = (double)n_global;   // resample when ESS < N (the global particle count)
   P.slot_cap = cfg->n_particles + 2 * bcap;
   PCS_SCRATCH(SL_SHARD_ANC, P.slot_cap * sizeof(int), P.anc_out);
   T.shard_rank = rank;
