@@ -952,7 +952,7 @@ static int track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int6
     if (r) return r;
     PCS_CHECK_ARG(cfg->placement == 0 || cfg->placement == 1, "unknown placement");
     if ((double)cfg->grid.n_cols * (double)cfg->grid.n_rows > (double)TABLE_MAX) {
-      pcs_set_last_error("grid exceeds the fused dense-table capacity (2^28 cells)");
+      pcs_set_last_error("grid exceeds the fused loop's cell ids (2^32 - 1 cells)");
       return PCS_E_CAPACITY;
     }
   }
@@ -1020,33 +1020,27 @@ static int track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int6
     P.ll = nullptr;
     P.wprev = nullptr;
     P.lltab = nullptr;
-    P.G = cfg->grid.n_cols * cfg->grid.n_rows;
+    P.G = HT_CAP;   // per-frame cell table: hashed slots (any grid up to 2^32 - 1 cells)
     T.cond = P.thresh < (double)n;   // threshold resampling: frames may carry prior weights
     if (T.cond) {
       PCS_SCRATCH(SL_TR_LL, ld * sizeof(double), P.ll);
       PCS_SCRATCH(SL_TR_WPREV, ld * sizeof(float), P.wprev);
       PCS_SCRATCH(SL_TR_LLTAB, P.G * sizeof(double), P.lltab);
     }
-    if (ctx->table_cells < P.G) {
-      if (ctx->tab_cnt) cudaFree(ctx->tab_cnt);
-      if (ctx->tab_sum) cudaFree(ctx->tab_sum);
-      if (ctx->wtab) cudaFree(ctx->wtab);
-      ctx->tab_cnt = nullptr;
-      ctx->tab_sum = nullptr;
-      ctx->wtab = nullptr;
-      ctx->table_cells = 0;
-      PCS_CUDA_TRY(cudaMalloc(&ctx->tab_cnt, P.G * sizeof(u32)));
-      PCS_CUDA_TRY(cudaMalloc(&ctx->tab_sum, 5 * P.G * 2 * sizeof(u64)));
-      // float weights, then the 16-byte exact weights (wfix)
-      PCS_CUDA_TRY(cudaMalloc(&ctx->wtab, ceil_div(P.G, 4) * 16 + P.G * sizeof(u128)));
-      ctx->table_cells = P.G;
+    if (!ctx->tab_cnt) {
+      // keys, counts, then the float / exact cdf weights per slot
+      PCS_CUDA_TRY(cudaMalloc(&ctx->tab_cnt, 2 * (size_t)HT_CAP * sizeof(u32)));
+      PCS_CUDA_TRY(cudaMalloc(&ctx->tab_sum, 5 * (size_t)HT_CAP * 2 * sizeof(u64)));
+      PCS_CUDA_TRY(cudaMalloc(&ctx->wtab, (size_t)HT_CAP * (sizeof(float) + sizeof(u128))));
+      ctx->table_cells = HT_CAP;
       ctx->table_dirty = true;
     }
     // occupied-cell list + per-cell log-likelihood and count (k_pc_cells)
     if (!ctx->occ) PCS_CUDA_TRY(cudaMalloc(&ctx->occ, MAXM * (sizeof(u32) + sizeof(double) + sizeof(u32))));
     if (ctx->table_dirty) {
-      PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_cnt, 0, ctx->table_cells * sizeof(u32), st));
-      PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_sum, 0, 5 * ctx->table_cells * 2 * sizeof(u64), st));
+      PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_cnt, 0, (size_t)HT_CAP * sizeof(u32), st));
+      PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_cnt + HT_CAP, 0xFF, (size_t)HT_CAP * sizeof(u32), st));
+      PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_sum, 0, 5 * (size_t)HT_CAP * 2 * sizeof(u64), st));
       ctx->table_dirty = false;
     }
     // compact per-frame tables of the step-1 sub-window cells (pslot codes < SUBW)
@@ -1054,9 +1048,10 @@ static int track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int6
     P.ltsub = (double*)(P.wsub + SUBW);
     P.wtsub = (float*)(P.ltsub + SUBW);
     P.tab_cnt = ctx->tab_cnt;
+    P.hkey = ctx->tab_cnt + HT_CAP;
     P.tab_sum = ctx->tab_sum;
-    P.wtab = ctx->wtab;
-    P.wfix = (u128*)(ctx->wtab + ceil_div(P.G, 4) * 4);
+    P.wfix = (u128*)ctx->wtab;
+    P.wtab = (float*)(P.wfix + HT_CAP);
     P.occ = ctx->occ;
     T.bins.ll = (double*)(ctx->occ + MAXM);
     T.bins.cnt = (u32*)(T.bins.ll + MAXM);
@@ -1448,6 +1443,7 @@ int pcs_shard_export(pcs_ctx* ctx, const int64_t* box, int64_t* limbs, void* str
   const TrackState& T = ctx->tr;
   k_shard_export<<<grid_for(T.shard_wcap, 256, ctx->sms), 256, 0, S(stream)>>>(
       T.P, (const i64*)box, T.shard_wcap, (i64*)limbs);
+  k_shard_reset<<<1, 1024, 0, S(stream)>>>(T.P);
   PCS_LAUNCH_CHECK();
   return PCS_OK;
 }

@@ -34,7 +34,13 @@ constexpr int S1_PARTS = 15;                   // 5 components x 3 digits (18/18
 constexpr int S1_E = 4;                        // sorted elements per thread in the run sums
 constexpr int S1_SUM_THREADS = S1_TILE / S1_E; // 256 threads (8 warps) sum the sorted tile
 constexpr int S1_FLUSH_TILES = 256;            // digit accumulators stay in range (see below)
-constexpr i64 TABLE_MAX = 1ll << 28;           // dense full-grid table (cells)
+constexpr i64 TABLE_MAX = 0xFFFFFFFFll;        // grid cells (flat ids are u32; 2^32 - 1 = empty key)
+// per-frame cell table: open addressing over HT_CAP slots keyed by the flat
+// cell id (2x the occupied-cell capacity MAXM), instead of a dense full-grid
+// table (28 GB at config 5's 16384^2 grid)
+constexpr int HT_BITS = 21;
+constexpr u32 HT_CAP = 1u << HT_BITS;
+constexpr u32 HT_EMPTY = 0xFFFFFFFFu;
 constexpr int MAXM = 1 << 20;                  // occupied cells per frame (fused)
 
 // Per-tile pipeline (k_pc_step1, two CTAs per SM): each CTA counting-sorts a
@@ -136,12 +142,13 @@ struct TrackParams {
   double* ll;                // SIR: per-particle log-likelihood (float64); k_sir_sum
                              // replaces it by exp(ll - max) for the rest of the frame
   u32* pslot;                // pcSIR: cell code per particle (pslot_code below)
-  u32* tab_cnt;              // [G]
+  u32* hkey;                 // [G] flat cell id of each table slot (HT_EMPTY: free)
+  u32* tab_cnt;              // [G]   members per slot
   u64* tab_sum;              // [5][G][2]
   float* wtab;               // [G]
   u128* wfix;                // [G] exact cdf weight round(wtab * 2^120) (k_sys_resample)
   u32* occ;                  // [MAXM]
-  i64 G;                     // table cells (= n_cols * n_rows)
+  i64 G;                     // table slots (HT_CAP)
   i64 ntiles;                // scan tiles
   u32* tile_status;          // [ntiles] (frame tag << 2 | state)
   u128* tile_agg;            // [ntiles]
@@ -314,11 +321,41 @@ __device__ __forceinline__ float cell_ref32(double origin, double cell, i64 i, b
 }
 
 
-__device__ __forceinline__ void touch_cell(const TrackParams& P, TrackCtl* C, u32 cell, u32 cnt) {
-  u32 old = atomicAdd(P.tab_cnt + cell, cnt);
+// table slot of flat cell id `flat` (inserted if absent; HT_EMPTY if the
+// table is full): Fibonacci hash, linear probing; keys only go from empty to
+// a cell id within a frame (the bins kernel clears the occupied slots)
+__device__ __forceinline__ u32 ht_hash(u32 flat) { return (flat * 0x9E3779B1u) >> (32 - HT_BITS); }
+__device__ __forceinline__ u32 ht_insert(const TrackParams& P, u32 flat) {
+  u32 s = ht_hash(flat);
+  for (u32 probe = 0; probe < HT_CAP; ++probe) {
+    const u32 k = __ldcg(P.hkey + s);
+    if (k == flat) return s;
+    if (k == HT_EMPTY) {
+      const u32 old = atomicCAS(P.hkey + s, HT_EMPTY, flat);
+      if (old == HT_EMPTY || old == flat) return s;
+    }
+    s = (s + 1) & (HT_CAP - 1);
+  }
+  return HT_EMPTY;
+}
+__device__ __forceinline__ u32 ht_find(const TrackParams& P, u32 flat) {
+  u32 s = ht_hash(flat);
+  for (u32 probe = 0; probe < HT_CAP; ++probe) {
+    const u32 k = __ldcg(P.hkey + s);
+    if (k == flat) return s;
+    if (k == HT_EMPTY) return HT_EMPTY;
+    s = (s + 1) & (HT_CAP - 1);
+  }
+  return HT_EMPTY;
+}
+
+// add cnt members to table slot `slot`; the first touch appends the slot to
+// the frame's occupied list
+__device__ __forceinline__ void touch_cell(const TrackParams& P, TrackCtl* C, u32 slot, u32 cnt) {
+  u32 old = atomicAdd(P.tab_cnt + slot, cnt);
   if (old == 0) {
     u32 idx = atomicAdd(&C->n_occ, 1u);
-    if (idx < (u32)MAXM) P.occ[idx] = cell;
+    if (idx < (u32)MAXM) P.occ[idx] = slot;
   }
 }
 
@@ -452,8 +489,13 @@ __device__ __forceinline__ void s1_flush(const TrackParams& P, TrackCtl* C, S1Sm
     }
     s[0] += (i128)cnt * f32_to_fixed(sm.ref[qx], FX_STATE);
     s[1] += (i128)cnt * f32_to_fixed(sm.ref[snx + qy], FX_STATE);
-    atomic_add_i128_x5(P.tab_sum + (i64)flat * 2, P.G * 2, s);
-    touch_cell(P, C, flat, cnt);
+    const u32 slot = ht_insert(P, flat);
+    if (slot != HT_EMPTY) {
+      atomic_add_i128_x5(P.tab_sum + (i64)slot * 2, P.G * 2, s);
+      touch_cell(P, C, slot, cnt);
+    } else {
+      set_flag(C, PCS_FLAG_CAPACITY);
+    }
     sm.cnt[q] = 0;
   }
 }
@@ -553,7 +595,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
       const u32 flat = (u32)iy * ncols32 + (u32)ix;   // G <= 2^28
       const int lx = ix - sx0i, ly = iy - sy0i;
       const bool inwin = (u32)lx < (u32)snxi && (u32)ly < (u32)snyi;
-      P.pslot[j] = inwin ? (u32)(ly * snxi + lx) : (u32)SUBW + flat;   // cell code
+      if (inwin) P.pslot[j] = (u32)(ly * snxi + lx);   // cell code (else: below)
       float dx, dy;
       if (inwin && delta_exact(o[0], sm.ref[lx], dx) &&
           delta_exact(o[1], refy[ly], dy) && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f &&
@@ -566,12 +608,19 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
         o[0] = dx;
         o[1] = dy;
       } else {
-        // outside the shared sub-window: exact int128 atomics straight to HBM
+        // outside the shared sub-window: exact int128 atomics straight to the
+        // cell's table slot
         i128 v[5];
 #pragma unroll
         for (int c = 0; c < 5; ++c) v[c] = f32_to_fixed(o[c], FX_STATE);
-        atomic_add_i128_x5(P.tab_sum + (i64)flat * 2, P.G * 2, v);
-        touch_cell(P, C, flat, 1u);
+        const u32 slot = ht_insert(P, flat);
+        if (!inwin) P.pslot[j] = (u32)SUBW + slot;   // cell code of an outside cell
+        if (slot != HT_EMPTY) {
+          atomic_add_i128_x5(P.tab_sum + (i64)slot * 2, P.G * 2, v);
+          touch_cell(P, C, slot, 1u);
+        } else {
+          set_flag(C, PCS_FLAG_CAPACITY);
+        }
       }
     }
     __syncthreads();
@@ -745,7 +794,8 @@ __global__ void __launch_bounds__(CELLS_BLOCK) k_pc_cells(TrackParams P, BinsScr
       d[q] = __double2float_rn(scalbn(__ddiv_rn(num, den), -FX_STATE));
     }
     if (P.placement == 1) {   // cell centre (binning.py:168-171)
-      const i64 ix = (i64)cell % P.grid.ncols, iy = (i64)cell / P.grid.ncols;
+      const u32 flat = P.hkey[cell];
+      const i64 ix = (i64)flat % P.grid.ncols, iy = (i64)flat / P.grid.ncols;
       d[0] = __double2float_rn(__dadd_rn(P.grid.ox, __dmul_rn((double)ix + 0.5, P.grid.lx)));
       d[1] = __double2float_rn(__dadd_rn(P.grid.oy, __dmul_rn((double)iy + 0.5, P.grid.ly)));
     }
@@ -859,11 +909,12 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
     // log w = log w_prev + ll_cell (binning.py:190-192), normaliser, estimate,
     // ESS and decision follow in k_pc_prior_ll / k_sir_sum / k_sir_stats
     for (int b = t; b < M; b += BINS_BLOCK) {
-      const u32 cell = P.occ[b];
+      const u32 cell = P.occ[b];   // (table slot)
       const double llb = Sd.ll[b];
       P.lltab[cell] = llb;
-      const int qs = sub_code(P, C, cell);
+      const int qs = sub_code(P, C, P.hkey[cell]);
       if (qs >= 0) P.ltsub[qs] = llb;
+      P.hkey[cell] = HT_EMPTY;   // (no kernel probes the table until the next frame)
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
         u64* p = P.tab_sum + ((i64)c * P.G + cell) * 2;
@@ -897,8 +948,9 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
   {
     unsigned wmin = 0xFFFFFFFFu, wmax = 0u;
     for (int b = t; b < M; b += BINS_BLOCK) {
-      const u32 cell = P.occ[b];
+      const u32 cell = P.occ[b];   // (table slot)
       const u32 cnt = Sd.cnt[b];
+      const u32 flat = P.hkey[cell];
       // the cell's state sums first: their latency overlaps the division
       i128 Ssum[5];
 #pragma unroll
@@ -906,7 +958,8 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
       const float w = __double2float_rn(__ddiv_rn(Sd.ll[b], Sf));   // normalised_weight
       P.wtab[cell] = w;
       P.wfix[cell] = cdf_fixed(w);
-      const int qs = sub_code(P, C, cell);
+      P.hkey[cell] = HT_EMPTY;   // (no kernel probes the table until the next frame)
+      const int qs = sub_code(P, C, flat);
       if (qs >= 0) {
         P.wtsub[qs] = w;
         P.wsub[qs] = cdf_fixed(w);

@@ -47,7 +47,7 @@ __global__ void k_shard_bbox(TrackParams P, i64* out) {
   __syncthreads();
   const u32 mm = min(m, (u32)MAXM);
   for (u32 b = threadIdx.x; b < mm; b += blockDim.x) {
-    u32 cell = P.occ[b];
+    const u32 cell = P.hkey[P.occ[b]];   // (the occupied list holds table slots)
     long long ix = (long long)cell % P.grid.ncols, iy = (long long)cell / P.grid.ncols;
     atomicMax(&s[0], -ix);
     atomicMax(&s[1], ix);
@@ -77,23 +77,21 @@ __global__ void k_shard_export(TrackParams P, const i64* __restrict__ box, i64 w
                                i64* __restrict__ limbs) {
   i64 x0, y0, nx, ny;
   const bool ok = shard_window(box, wcap, x0, y0, nx, ny);
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    P.ctl->n_occ = 0;   // import rebuilds the list
-    if (!ok) set_flag(P.ctl, PCS_FLAG_CAPACITY);
-  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && !ok) set_flag(P.ctl, PCS_FLAG_CAPACITY);
   if (!ok) return;
   const i64 W = nx * ny;
   const u64 M42 = (1ull << 42) - 1ull;
   for (i64 q = blockIdx.x * (i64)blockDim.x + threadIdx.x; q < W; q += (i64)gridDim.x * blockDim.x) {
     i64 ix = x0 + q % nx, iy = y0 + q / nx;
     i64* L = limbs + q * LIMBS_PER_CELL;
-    u32 flat = (u32)(iy * P.grid.ncols + ix);
-    u32 cnt = P.tab_cnt[flat];
+    const u32 flat = (u32)(iy * P.grid.ncols + ix);
+    const u32 slot = ht_find(P, flat);
+    const u32 cnt = (slot != HT_EMPTY) ? P.tab_cnt[slot] : 0u;
     L[0] = cnt;
     for (int c = 0; c < 5; ++c) {
       i128 v = 0;
       if (cnt) {
-        u64* p = P.tab_sum + ((i64)c * P.G + flat) * 2;
+        u64* p = P.tab_sum + ((i64)c * P.G + slot) * 2;
         v = load_i128(p);
         p[0] = 0;
         p[1] = 0;
@@ -102,8 +100,18 @@ __global__ void k_shard_export(TrackParams P, const i64* __restrict__ box, i64 w
       L[2 + 3 * c] = (i64)((u64)(v >> 42) & M42);
       L[3 + 3 * c] = (i64)(v >> 84);   // arithmetic shift keeps the sign
     }
-    if (cnt) P.tab_cnt[flat] = 0;
+    if (cnt) P.tab_cnt[slot] = 0;
   }
+}
+
+// after the export: free the local table's slots (keys) and empty the
+// occupied list; one CTA (the keys must not change while the export probes)
+__global__ void k_shard_reset(TrackParams P) {
+  TrackCtl* C = P.ctl;
+  const u32 m = min(C->n_occ, (u32)MAXM);
+  for (u32 b = threadIdx.x; b < m; b += blockDim.x) P.hkey[P.occ[b]] = HT_EMPTY;
+  __syncthreads();
+  if (threadIdx.x == 0) C->n_occ = 0;   // import rebuilds the list
 }
 
 __global__ void k_shard_import(TrackParams P, const i64* __restrict__ box, i64 wcap,
@@ -117,16 +125,21 @@ __global__ void k_shard_import(TrackParams P, const i64* __restrict__ box, i64 w
     i64 cnt = L[0];
     if (!cnt) continue;
     i64 ix = x0 + q % nx, iy = y0 + q / nx;
-    u32 flat = (u32)(iy * P.grid.ncols + ix);
-    P.tab_cnt[flat] = (u32)cnt;
+    const u32 flat = (u32)(iy * P.grid.ncols + ix);
+    const u32 slot = ht_insert(P, flat);
+    if (slot == HT_EMPTY) {
+      set_flag(C, PCS_FLAG_CAPACITY);
+      continue;
+    }
+    P.tab_cnt[slot] = (u32)cnt;
     for (int c = 0; c < 5; ++c) {
       i128 v = (i128)L[1 + 3 * c] + ((i128)L[2 + 3 * c] << 42) + ((i128)L[3 + 3 * c] << 84);
-      u64* p = P.tab_sum + ((i64)c * P.G + flat) * 2;
+      u64* p = P.tab_sum + ((i64)c * P.G + slot) * 2;
       p[0] = (u64)v;
       p[1] = (u64)((u128)v >> 64);
     }
     u32 idx = atomicAdd(&C->n_occ, 1u);
-    if (idx < (u32)MAXM) P.occ[idx] = flat;
+    if (idx < (u32)MAXM) P.occ[idx] = slot;
   }
 }
 
