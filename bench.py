@@ -336,6 +336,18 @@ def kernel_profile(torch, pc, _lib, cfg, grid, dev_frames, warmup, frames_n, see
     return {nm: acc[i] / frames_n for i, nm in enumerate(names)}
 
 
+# measured pipe utilisation of k_sir_propagate_lik (ncu --set full, one launch;
+# profiles/r2_sir_likelihood_ncu.txt): % of each pipe's peak while active
+LIK_PIPES = {
+    "c3": {"fma_pct": 49.4, "xu_pct": 39.5, "alu_pct": 25.6, "fp64_pct": 0.26,
+           "issue_active_pct": 69.9, "measured_limiter": "issue / FP32 FMA pipe (one 256-thread "
+           "CTA per SM at 167 registers)"},
+    "c2": {"fma_pct": 24.5, "xu_pct": 53.3, "alu_pct": 25.1, "fp64_pct": 11.2,
+           "issue_active_pct": 58.1, "measured_limiter": "XU (expf + float->double "
+           "conversions of the exact r^2 sums)"},
+}
+
+
 def likelihood_roofline(torch, pc, _lib, info, args, clock_mhz):
     """FP32 / SFU roofline of the per-particle likelihood kernel
     (k_sir_propagate_lik, one evaluation per particle): c3's erf-PSF Poisson
@@ -372,7 +384,9 @@ def likelihood_roofline(torch, pc, _lib, info, args, clock_mhz):
             "achieved_mufu_per_s": mufu_s, "peak_mufu_per_s": peak_sfu, "sfu_frac": mufu_s / peak_sfu,
             "frac": t_bound / t, "limiter": "sfu" if ops["mufu"] / peak_sfu >= ops["flop"] / peak_fp32
             else "fp32",
-            "clock_mhz": f / 1e6, "peak_kind": "SMs x lanes x clock (sampled)"}
+            "clock_mhz": f / 1e6, "peak_kind": "SMs x lanes x clock (sampled)",
+            "ncu_pipes": dict(LIK_PIPES[wl_name],
+                              source="profiles/r2_sir_likelihood_ncu.txt")}
         del dev_frames
         torch.cuda.empty_cache()
     return out

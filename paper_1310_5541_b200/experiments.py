@@ -198,6 +198,59 @@ def run_tracking_experiment(variants, n_particles, repetitions, scene=None, sigm
     return records
 
 
+def run_tracking_on_scenes(scenes, variants, n_particles, psf, sigma_xi, window_halfwidth,
+                           filter_dynamics=DynamicsParams(0.5, 0.5, 0.0), prior="point",
+                           resampling=None, seed=0, experiment="small_object",
+                           weighted_com=False, progress=None):
+    """The reference's sweep (experiments.py:251-292) on given scenes: every
+    variant and N of a repetition runs on the same frames (paired), with the
+    reference harness's filter setup — prior parse_prior(prior, truth initial
+    state), filter dynamics, ``ResampleConfig()`` (threshold 0.5, multinomial)
+    unless ``resampling`` is given, weighted centre of mass optional — on the
+    device filters. ``scenes``: iterable of dicts with ``frames`` (K, H, W),
+    ``positions`` (K, 2) and ``init_state`` (5,) (e.g. the reference's own
+    rendered scenes, tests/golden/experiments.npz). Wall time covers the
+    filtering call only."""
+    specs = [parse_variant(v) for v in variants]
+    res = resampling if resampling is not None else ResampleConfig()
+    records = []
+    for rep, sc in enumerate(scenes):
+        frames = torch.from_numpy(np.ascontiguousarray(np.asarray(sc["frames"], dtype=np.float32)))
+        frames = frames.to(torch.device("cuda"))
+        k, h, w = frames.shape
+        center = StateVector(*np.asarray(sc["init_state"], dtype=np.float64))
+        init = parse_prior(prior, center)
+        truth_xy = np.asarray(sc["positions"], dtype=np.float64)
+        for spec in specs:
+            for n in n_particles:
+                lik = SpotLikelihood(psf, LikelihoodParams(sigma_xi, window_halfwidth))
+                if spec.is_pc:
+                    grid = BinGrid.pixel_aligned(w, h, spec.cells_per_pixel)
+                    cfg = PcFilterConfig(n, init, filter_dynamics, res, lik, grid=grid,
+                                         placement=spec.placement, weighted_com=weighted_com)
+                    track = pcsir_track
+                else:
+                    cfg = FilterConfig(n, init, filter_dynamics, res, lik)
+                    track = sir_track
+                rng_f = PhiloxRng(derive_seed(seed, "filter", spec.label, n, rep))
+                torch.cuda.synchronize()
+                start = time.perf_counter()
+                try:
+                    result = track(frames, cfg, rng_f)
+                except DegenerateWeightsError:
+                    records.append(RunRecord(experiment, spec.label, n, rep, float("nan"),
+                                             time.perf_counter() - start, lik.evals, failed=True))
+                    continue
+                elapsed = time.perf_counter() - start
+                d = result.positions - truth_xy
+                rmse = float(np.sqrt(np.mean(np.sum(d ** 2, axis=1))))
+                records.append(RunRecord(experiment, spec.label, n, rep, rmse, elapsed,
+                                         result.likelihood_evals, trajectory=result.positions))
+                if progress is not None:
+                    progress(records[-1])
+    return records
+
+
 PSEUDO_PRIORS = ("uniform3x3", "uniform5x5", "gauss0.5", "gauss0.8")
 
 

@@ -302,6 +302,54 @@ def gen_bounds():
     return out
 
 
+def gen_experiments():
+    """The reference's tracking sweep (experiments.py:251-292) on a reduced
+    small_object preset, with the scenes it rendered (derive_rng 'scene'
+    streams), so the device harness can run on the same frames."""
+    from dataclasses import replace
+    import types
+    if "matplotlib" not in sys.modules:   # reports.py imports it for plotting only (absent here)
+        mpl = types.ModuleType("matplotlib")
+        mpl.use = lambda *a, **k: None
+        plt = types.ModuleType("matplotlib.pyplot")
+        plt.rcParams = {}
+        mpl.pyplot = plt
+        sys.modules["matplotlib"] = mpl
+        sys.modules["matplotlib.pyplot"] = plt
+    from pcsir import experiments as rex
+    from pcsir import reports as rrep
+    from pcsir import synthesis as rsy
+    cfg = rex.preset("small_object", seed=3)
+    cfg = replace(cfg, n_particles=(2000, 8000), repetitions=8,
+                  scene=replace(cfg.scene, frames=20, width=64, height=64))
+    records = rex.run_tracking_experiment(cfg)
+    rows = rrep.summarize(records)
+    out = {"variants": np.array(cfg.variants), "n_particles": np.array(cfg.n_particles),
+           "sigma_psf": np.array(cfg.scene.psf.sigma_psf), "i_bg": np.array(cfg.scene.psf.i_bg),
+           "sigma_xi": np.array(cfg.sigma_xi), "hw": np.array(cfg.window_halfwidth),
+           "filter_dyn": np.array([cfg.filter_dynamics.sigma_pos, cfg.filter_dynamics.sigma_vel,
+                                   cfg.filter_dynamics.sigma_int, cfg.filter_dynamics.dt]),
+           "prior": np.array(cfg.prior),
+           "summary_columns": np.array(rrep.SUMMARY_COLUMNS)}
+    for rep in range(cfg.repetitions):
+        rng = rex.derive_rng(cfg.seed, "scene", cfg.experiment, rep)
+        truth = rsy.generate_truth(cfg.scene, rng)
+        frames = rsy.render_sequence(truth, cfg.scene, rng)
+        out[f"frames_{rep}"] = np.stack([f.pixels for f in frames]).astype(np.uint16)
+        out[f"positions_{rep}"] = truth.positions
+        out[f"init_{rep}"] = truth.init_state
+    out["rec_variant"] = np.array([r.variant for r in records])
+    out["rec_n"] = np.array([r.n_particles for r in records])
+    out["rec_rmse"] = np.array([r.rmse for r in records])
+    out["rec_evals"] = np.array([r.lik_evals for r in records])
+    out["rec_failed"] = np.array([r.failed for r in records])
+    out["sum_variant"] = np.array([r.variant for r in rows])
+    out["sum_n"] = np.array([r.n_particles for r in rows])
+    out["sum_rmse_mean"] = np.array([r.rmse_mean for r in rows])
+    out["sum_evals_mean"] = np.array([r.lik_evals_mean for r in rows])
+    return out
+
+
 def main():
     if len(sys.argv) > 1:   # regenerate the named fixtures only
         for name in sys.argv[1:]:

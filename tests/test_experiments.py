@@ -106,3 +106,55 @@ def test_gpu_pseudo_tracking(cuda):
     again = ex.run_pseudo_tracking(["pcSIR-1x1-CoM"], [300], 2, prior="uniform3x3", seed=1)
     assert [r.rmse for r in again] == [r.rmse for r in recs
                                        if r.variant == "pcSIR-1x1-CoM" and r.n_particles == 300][:2]
+
+
+# --- the reference's own harness on the same scenes -----------
+def _golden_scenes(g):
+    reps = len([k for k in g.files if k.startswith("frames_")])
+    return [{"frames": g[f"frames_{r}"].astype(np.float32), "positions": g[f"positions_{r}"],
+             "init_state": g[f"init_{r}"]} for r in range(reps)]
+
+
+def test_summary_columns_match_reference():
+    from conftest import golden
+    from paper_1310_5541_b200 import experiments as ex
+    g = golden("experiments")
+    assert tuple(ex.SUMMARY_COLUMNS) == tuple(str(c) for c in g["summary_columns"])
+
+
+@pytest.mark.gpu
+def test_sweep_matches_reference_harness_on_its_scenes(cuda):
+    """The reference's run_tracking_experiment (reduced small_object preset,
+    8 repetitions, N = 2000 / 8000, its default ResampleConfig: ESS threshold
+    0.5, multinomial) against the device harness on the SAME rendered frames
+    (tests/golden/experiments.npz). The RNG streams differ (numpy vs Philox),
+    so the comparison is statistical: SIR evaluation counts equal exactly,
+    pcSIR occupied-cell counts and RMSE agree within sampling error, and the
+    1x1-cell bias of pcSIR over SIR that the reference shows is reproduced."""
+    from conftest import golden
+    import paper_1310_5541_b200 as pc
+    from paper_1310_5541_b200 import experiments as ex
+    g = golden("experiments")
+    d = g["filter_dyn"]
+    recs = ex.run_tracking_on_scenes(
+        _golden_scenes(g), [str(v) for v in g["variants"]], [int(n) for n in g["n_particles"]],
+        pc.PsfParams(float(g["sigma_psf"]), float(g["i_bg"])), float(g["sigma_xi"]), int(g["hw"]),
+        filter_dynamics=pc.DynamicsParams(float(d[0]), float(d[1]), float(d[2]), float(d[3])),
+        prior=str(g["prior"]), seed=3)
+    rows = {(r.variant, r.n_particles): r for r in ex.summarize(recs)}
+    ref = {(str(v), int(n)): (float(e), float(m)) for v, n, e, m in
+           zip(g["sum_variant"], g["sum_n"], g["sum_rmse_mean"], g["sum_evals_mean"])}
+    assert set(rows) == set(ref)
+    assert not any(r.failed for r in recs)
+    k = g["frames_0"].shape[0]
+    for r in recs:
+        if r.variant == "SIR":
+            assert r.lik_evals == r.n_particles * k
+    for key, (rmse_ref, evals_ref) in ref.items():
+        row = rows[key]
+        assert abs(row.rmse_mean - rmse_ref) <= 0.06, (key, row.rmse_mean, rmse_ref)
+        assert abs(row.lik_evals_mean - evals_ref) <= 0.12 * evals_ref, (key, row.lik_evals_mean,
+                                                                         evals_ref)
+    for n in (2000, 8000):   # the 1x1-cell approximation costs accuracy in both
+        assert rows[("pcSIR-1x1-CoM", n)].rmse_mean > rows[("SIR", n)].rmse_mean
+        assert ref[("pcSIR-1x1-CoM", n)][0] > ref[("SIR", n)][0]
