@@ -72,6 +72,7 @@ struct TrackState {
   const char* names[MAX_LAUNCHES] = {};   // kernel of each launch of a frame
   int prop_grid = 0;
   int cells_grid = 0;    // k_pc_cells CTAs (8 warps each, one warp per occupied cell)
+  bool s1_pow2 = false;  // k_pc_step1<true>: power-of-two cells, float32-exact origins
   int shard_rank = 0, shard_world = 1;   // sharded filter (pcs_shard_*)
   i64 shard_wcap = 0, shard_bcap = 0;
   int maxs = 0;
@@ -844,7 +845,8 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
   };
   if (T.cfg.method == 1) {
     mark("k_pc_step1");
-    k_pc_step1<<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(P);
+    if (T.s1_pow2) k_pc_step1<true><<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(P);
+    else k_pc_step1<false><<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(P);
     mark("k_pc_cells");
     launch_pdl(k_pc_cells, T.cells_grid, CELLS_BLOCK, 0, st, P, T.bins);
     mark("k_pc_bins");
@@ -904,7 +906,9 @@ static bool g_attr_done = false;
 
 static int set_attrs() {
   if (g_attr_done) return PCS_OK;
-  PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_step1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_step1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)S1_SMEM));
+  PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_step1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)S1_SMEM));
   PCS_CUDA_TRY(cudaFuncSetAttribute(k_sys_resample<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)sizeof(RsSmem<1>)));
@@ -916,7 +920,8 @@ static int set_attrs() {
                                     (int)sizeof(RsSmem<2>)));
   // one shared-memory carveout for every kernel of the frame: consecutive
   // kernels with different carveouts force an SM reconfiguration between them
-  const void* fns[] = {(const void*)k_pc_step1,        (const void*)k_pc_bins,
+  const void* fns[] = {(const void*)k_pc_step1<true>,  (const void*)k_pc_step1<false>,
+                       (const void*)k_pc_bins,
                        (const void*)k_pc_cells,         (const void*)k_sir_propagate_lik<0>,
                        (const void*)k_sir_propagate_lik<9>, (const void*)k_sir_propagate_lik<11>,
                        (const void*)k_sir_propagate_lik<15>, (const void*)k_sir_sum,
@@ -1078,6 +1083,7 @@ static int track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int6
   }
   T.s1_grid = (int)std::min<i64>((i64)ctx->sms * S1_CTAS_PER_SM, ceil_div(n, S1_TILE));
   T.cells_grid = ctx->sms * 4;
+  T.s1_pow2 = cfg->method == 1 && grid_pow2(P.grid.ox, P.grid.lx, P.grid.oy, P.grid.ly);
   {
     // equal tile counts per CTA: tile = ceil(per_cta / ceil(per_cta / S1_TILE))
     const i64 per_cta = ceil_div(n, (i64)T.s1_grid);
@@ -1432,7 +1438,8 @@ int pcs_shard_step1(pcs_ctx* ctx, const float* frame, int64_t k, double* est, do
   cudaStream_t st = S(stream);
   TrackState& T = ctx->tr;
   k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frame, k, k, k + 1, est, ess, res, (i64*)occ);
-  k_pc_step1<<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(T.P);
+  if (T.s1_pow2) k_pc_step1<true><<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(T.P);
+  else k_pc_step1<false><<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(T.P);
   k_shard_bbox<<<1, 1024, 0, st>>>(T.P, (i64*)box);
   PCS_LAUNCH_CHECK();
   return PCS_OK;

@@ -69,6 +69,7 @@ struct S1Smem {
   unsigned short list[S1_TILE];   // cells occupied in this tile
   unsigned short flist[SUBW];     // cells touched since the last flush
   u32 n_list, n_flist, n_in;
+  int fast_delta;
   int scan_tmp[S1_WARPS];
   long long next_tile;
 };
@@ -303,14 +304,31 @@ __device__ __forceinline__ AxisFast make_axis(double origin, double cell, double
   return a;
 }
 
+// POW2: both axes have power-of-two cells and float32-exact origins (the
+// margins are zero, see make_axis): only an integer quotient is ambiguous
+template <bool POW2>
 __device__ __forceinline__ int cell_axis_hot(float p, const AxisFast& a) {
   const float t32 = __fmul_rn(__fsub_rn(p, a.o32), a.inv32);
   const float f32 = floorf(t32);
   const float fr32 = t32 - f32;
-  const float margin = fmaf(fabsf(t32), a.mt, fmaf(fabsf(p), a.ma, a.mb));
-  if (fr32 > margin && fr32 < 1.0f - margin && f32 >= 0.0f && f32 <= a.fmax)
-    return __float2int_rz(f32);
+  if (POW2) {
+    if (fr32 != 0.0f && f32 >= 0.0f && f32 <= a.fmax) return __float2int_rz(f32);
+  } else {
+    const float margin = fmaf(fabsf(t32), a.mt, fmaf(fabsf(p), a.ma, a.mb));
+    if (fr32 > margin && fr32 < 1.0f - margin && f32 >= 0.0f && f32 <= a.fmax)
+      return __float2int_rz(f32);
+  }
   return (int)cell_axis_fast(p, a.origin, a.cell, a.inv, a.n);
+}
+// host: both axes of the grid take the POW2 form of cell_axis_hot
+__host__ __forceinline__ bool grid_pow2(double origin_x, double lx, double origin_y, double ly) {
+  auto axis = [](double o, double l) {
+    const double inv = 1.0 / l;
+    int e;
+    return std::frexp(inv, &e) == 0.5 && l * inv == 1.0 && (double)(float)inv == inv &&
+           (double)(float)o == o && e > -100 && e < 100;
+  };
+  return axis(origin_x, lx) && axis(origin_y, ly);
 }
 
 // cell lower edge as float32 and whether it is an integer multiple of 2^-40
@@ -500,6 +518,7 @@ __device__ __forceinline__ void s1_flush(const TrackParams& P, TrackCtl* C, S1Sm
   }
 }
 
+template <bool POW2>
 __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackParams P) {
   extern __shared__ __align__(16) unsigned char s1_raw[];
   S1Smem& sm = *reinterpret_cast<S1Smem*>(s1_raw);
@@ -537,12 +556,19 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
 #pragma unroll
     for (int p = 0; p < S1_PARTS; ++p) sm.dig[p][q] = 0;
   }
-  // cell lower edges; NaN marks an edge whose deltas may not be exact
+  // cell lower edges; NaN marks an edge whose deltas may not be exact.
+  // fast_delta: every edge r of the sub-window is >= 2 l (and l < 64), so for
+  // any x of the cell, r/2 <= x <= 2r and x - r is exact (Sterbenz) — no
+  // TwoSum check per particle
+  if (t == 0) sm.fast_delta = (g.lx < 64.0 && g.ly < 64.0) ? 1 : 0;
+  __syncthreads();
   for (int q = t; q < snxi + snyi; q += S1_THREADS) {
     bool ok;
     float r = (q < snxi) ? cell_ref32(g.ox, g.lx, sx0 + q, ok)
                          : cell_ref32(g.oy, g.ly, sy0 + (q - snxi), ok);
     sm.ref[q] = ok ? r : __int_as_float(0x7fc00000);
+    const double l2 = 2.0 * ((q < snxi) ? g.lx : g.ly);
+    if (!ok || !((double)r >= l2)) atomicAnd(&sm.fast_delta, 0);
   }
   if (t == 0) {
     sm.n_list = 0;
@@ -550,6 +576,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
   }
   const float* refy = sm.ref + snxi;
   __syncthreads();
+  const bool fast_delta = sm.fast_delta != 0;
 
   const u32 frame = P.frame0 + (u32)k;
   const AxisFast axx = make_axis(g.ox, g.lx, P.inv_lx, g.ncols);
@@ -565,21 +592,28 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
     int q_k[S1_IPT], r_k[S1_IPT];
     float o_k[S1_IPT][5];
     int src_k[S1_IPT];
+    const i64 j0 = tile * TT;   // (n < 2^31: particle indices fit 32 bits)
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {   // every gather before any arithmetic
       const int l = it * S1_THREADS + t;
-      const i64 j = tile * TT + l;
-      src_k[it] = (l < TT && j < n) ? __ldg(P.anc + j) : -1;
+      const int j = (int)j0 + l;
+      src_k[it] = (l < TT && j < (int)n) ? __ldg(P.anc + j) : -1;
     }
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {
+      // component c of particle src at sin + src + c ld: one wide multiply,
+      // then pointer steps of ld (no per-component 64-bit index products)
+      const float* g = sin + (src_k[it] >= 0 ? src_k[it] : 0);
 #pragma unroll
-      for (int c = 0; c < 5; ++c) o_k[it][c] = (src_k[it] >= 0) ? __ldg(sin + c * ld + src_k[it]) : 0.0f;
+      for (int c = 0; c < 5; ++c) {
+        o_k[it][c] = (src_k[it] >= 0) ? __ldg(g) : 0.0f;
+        g += ld;
+      }
     }
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {
       q_k[it] = -1;
-      const i64 j = tile * TT + it * S1_THREADS + t;
+      const int j = (int)j0 + it * S1_THREADS + t;
       if (src_k[it] < 0) continue;
       float s[5], z[5];
 #pragma unroll
@@ -587,19 +621,33 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
       philox_normals5k(P.pk, frame, (u64)(P.idx_off + j), z);
       float* o = o_k[it];
       propagate_one(s, z, P.dyn, o);
+      {
+        float* d = sout + j;
 #pragma unroll
-      for (int c = 0; c < 5; ++c) sout[c * ld + j] = o[c];
+        for (int c = 0; c < 5; ++c) {
+          *d = o[c];
+          d += ld;
+        }
+      }
       if (!(o[0] == o[0]) || !(o[1] == o[1])) bad = true;
-      const int ix = cell_axis_hot(o[0], axx);
-      const int iy = cell_axis_hot(o[1], axy);
+      const int ix = cell_axis_hot<POW2>(o[0], axx);
+      const int iy = cell_axis_hot<POW2>(o[1], axy);
       const u32 flat = (u32)iy * ncols32 + (u32)ix;   // G <= 2^28
       const int lx = ix - sx0i, ly = iy - sy0i;
       const bool inwin = (u32)lx < (u32)snxi && (u32)ly < (u32)snyi;
       if (inwin) P.pslot[j] = (u32)(ly * snxi + lx);   // cell code (else: below)
       float dx, dy;
-      if (inwin && delta_exact(o[0], sm.ref[lx], dx) &&
-          delta_exact(o[1], refy[ly], dy) && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f &&
-          fabsf(o[4]) < 128.0f) {
+      bool dok = false;
+      if (inwin) {
+        if (fast_delta) {   // (CTA-uniform branch)
+          dx = __fsub_rn(o[0], sm.ref[lx]);
+          dy = __fsub_rn(o[1], refy[ly]);
+          dok = true;
+        } else {
+          dok = delta_exact(o[0], sm.ref[lx], dx) && delta_exact(o[1], refy[ly], dy);
+        }
+      }
+      if (dok && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f && fabsf(o[4]) < 128.0f) {
         const int q = ly * snxi + lx;
         const int r = (int)atomicAdd(&sm.tile_cnt[q], 1u);
         if (r == 0) sm.list[atomicAdd(&sm.n_list, 1u)] = (unsigned short)q;

@@ -225,8 +225,8 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
 #pragma unroll
       for (int c = 0; c < 5; ++c) sout[c * ld + base_i + j] = o[c];
       if (!(o[0] == o[0]) || !(o[1] == o[1])) bad = true;
-      const int ix = cell_axis_hot(o[0], axx);
-      const int iy = cell_axis_hot(o[1], axy);
+      const int ix = cell_axis_hot<false>(o[0], axx);
+      const int iy = cell_axis_hot<false>(o[1], axy);
       const u32 flat = (u32)iy * ncols32 + (u32)ix;
       const int lx = ix - sx0i, ly = iy - sy0i;
       float dx, dy;
