@@ -22,7 +22,7 @@ def main(rep):
         def g(k, default="n/a"):
             return d.get(k, default)
         print(f"== {name}")
-        for k, lab in [("gpu__time_duration.sum", "duration (ns)"),
+        for k, lab in [("gpu__time_duration.sum", "duration (us)"),
                        ("dram__bytes_read.sum", "dram read"),
                        ("dram__bytes_write.sum", "dram write"),
                        ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram %"),
