@@ -332,11 +332,13 @@ __device__ __forceinline__ double loglik_poisson64_generic(const PixView& pv, fl
   return ll;
 }
 
-template <int MAXS>
+// F64OK: the float64 Poisson form may be requested (sp.f64); the per-particle
+// SIR kernel instantiates without it (its code would cost registers there)
+template <int MAXS, bool F64OK = true>
 __device__ __forceinline__ double loglik_any(const PixView& pv, float x, float y, float i0,
                                              const Spot& sp) {
   if (sp.model == 0) return loglik_gauss<MAXS>(pv, x, y, i0, sp);
-  if (sp.f64) return loglik_poisson64_generic(pv, x, y, i0, sp);
+  if (F64OK && sp.f64) return loglik_poisson64_generic(pv, x, y, i0, sp);
   return loglik_poisson<MAXS>(pv, x, y, i0, sp);
 }
 
@@ -397,10 +399,10 @@ __device__ __forceinline__ double loglik_generic(const PixView& pv, float x, flo
 }
 
 // dispatch: MAXS > 0 -> register-resident window, MAXS == 0 -> generic
-template <int MAXS>
+template <int MAXS, bool F64OK = true>
 __device__ __forceinline__ double loglik_dispatch(const PixView& pv, float x, float y, float i0,
                                                   const Spot& sp) {
-  if constexpr (MAXS > 0) return loglik_any<MAXS>(pv, x, y, i0, sp);
+  if constexpr (MAXS > 0) return loglik_any<MAXS, F64OK>(pv, x, y, i0, sp);
   else return loglik_generic(pv, x, y, i0, sp);
 }
 

@@ -24,8 +24,11 @@ constexpr int SIR_SW = 64;
 // log of a prior weight, out of line (only frames after a non-resampling frame)
 __device__ __noinline__ double log_prior(float w) { return log((double)w); }
 
+#ifndef PCS_SIR_MINB
+#define PCS_SIR_MINB 2   // 2 CTAs / SM at 128 registers (1: 200-255 registers, 20-40 % slower)
+#endif
 template <int MAXS>
-__global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
+__global__ void __launch_bounds__(256, PCS_SIR_MINB) k_sir_propagate_lik(TrackParams P) {
   __shared__ __align__(128) float stg[SIR_SW * SIR_SW];
   __shared__ __align__(8) unsigned long long tma_bar;
   TrackCtl* C = P.ctl;
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(256) k_sir_propagate_lik(TrackParams P) {
     v.pitch = inside ? ps.pitch : pv.pitch;
     v.x0 = inside ? ps.x0 : 0;
     v.y0 = inside ? ps.y0 : 0;
-    double ll = loglik_dispatch<MAXS>(v, o[0], o[1], o[4], P.spot);
+    double ll = loglik_dispatch<MAXS, false>(v, o[0], o[1], o[4], P.spot);
     // log w = log(w_prev) + ll (k_weight_update, binning.py:190-192 / filtering.py:69)
     if (prior) ll = __dadd_rn(log_prior(P.wprev[j]), ll);
     P.ll[j] = ll;
