@@ -339,11 +339,11 @@ def kernel_profile(torch, pc, _lib, cfg, grid, dev_frames, warmup, frames_n, see
 # measured pipe utilisation of k_sir_propagate_lik (ncu --set full, one launch;
 # profiles/r2_sir_likelihood_ncu.txt): % of each pipe's peak while active
 LIK_PIPES = {
-    "c3": {"fma_pct": 49.4, "xu_pct": 39.5, "alu_pct": 25.6, "fp64_pct": 0.26,
-           "issue_active_pct": 69.9, "measured_limiter": "issue / FP32 FMA pipe (one 256-thread "
-           "CTA per SM at 167 registers)"},
-    "c2": {"fma_pct": 24.5, "xu_pct": 53.3, "alu_pct": 25.1, "fp64_pct": 11.2,
-           "issue_active_pct": 58.1, "measured_limiter": "XU (expf + float->double "
+    "c3": {"fma_pct": 59.2, "xu_pct": 47.5, "alu_pct": 30.8, "fp64_pct": 0.31,
+           "issue_active_pct": 83.9, "measured_limiter": "FP32 FMA pipe / issue (two 256-thread "
+           "CTAs per SM at 128 registers)"},
+    "c2": {"fma_pct": 24.4, "xu_pct": 53.0, "alu_pct": 25.7, "fp64_pct": 11.2,
+           "issue_active_pct": 57.9, "measured_limiter": "XU (expf + float->double "
            "conversions of the exact r^2 sums)"},
 }
 

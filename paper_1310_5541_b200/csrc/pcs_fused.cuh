@@ -1214,7 +1214,10 @@ struct RsSmem {
 // emitting slots (k_multinomial_emit draws them); a separate instantiation so
 // the systematic kernel carries none of it
 template <int KIND, bool MULTI = false>
-__global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? 4 : 2) k_sys_resample(TrackParams P) {
+#ifndef PCS_RS_MINB
+#define PCS_RS_MINB 4
+#endif
+__global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? PCS_RS_MINB : 2) k_sys_resample(TrackParams P) {
   typedef typename RsElem<KIND>::T E;
   extern __shared__ __align__(128) unsigned char rs_raw[];
   RsSmem<KIND>& sm = *reinterpret_cast<RsSmem<KIND>*>(rs_raw);
