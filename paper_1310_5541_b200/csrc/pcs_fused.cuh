@@ -710,6 +710,15 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
     }
     __syncthreads();
     // ---- phase 3: scatter the in-window particles into cell-sorted order ----
+    // (the next tile is known since phase 2: pull its ancestor indices into L2
+    // now, so its gather starts with an L2 hit instead of a DRAM round trip)
+    if (t < S1_TILE / 32) {
+      const i64 nt = sm.next_tile;
+      if (nt < ntile) {
+        const int* a = P.anc + nt * TT + t * 32;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+      }
+    }
     float (*pay)[S1_TILE] = sm.pay;
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {
