@@ -1139,23 +1139,27 @@ __device__ __forceinline__ int lds_u32(u32 addr) {
 }
 
 // Persistent reduce-then-scan systematic resampling (single GPU, scan_mode 0).
-// Each CTA owns a contiguous range of tiles (RS_TILE = 3840 particles). Pass
+// Each CTA owns a contiguous range of tiles (RS_TILE = 5888 particles). Pass
 // 1 sums the exact fixed-point weights of its range; after ONE grid-wide
 // barrier every CTA adds up the aggregates of the CTAs before it (its exact
 // exclusive prefix); pass 2 re-reads its range tile by tile, emits each
 // item's slots and writes the ancestors coalesced. Tiles are streamed into a
 // two-buffer shared-memory ring by TMA bulk copies (cp.async.bulk +
 // mbarrier), so the next tile is in flight while the current one is
-// processed. 15 consecutive items per thread: the stride-15 reads of the
+// processed. RS_ITEMS (odd) consecutive items per thread: the odd-stride reads of the
 // dense tile are bank-conflict free. Requires every CTA to be co-resident
 // (grid = SMs x occupancy, set by the host from the occupancy calculator).
-constexpr int RS_ITEMS = 15;
-constexpr int RS_TILE = SCAN_BLOCK * RS_ITEMS;   // 3840
+#ifndef PCS_RS_ITEMS
+#define PCS_RS_ITEMS 23   // 5888-particle tiles, 3 CTAs / SM (profiles/r2_variants.md)
+#define PCS_RS_SCAP 25
+#endif
+constexpr int RS_ITEMS = PCS_RS_ITEMS;
+constexpr int RS_TILE = SCAN_BLOCK * RS_ITEMS;   // 5888
 // A tile emits ~RS_TILE slots (+- a few %): the emission stage holds
 // RS_SCAP slots per thread so that one chunk covers almost every tile (odd:
 // the per-thread stride is bank-conflict free)
-constexpr int RS_SCAP = 17;
-constexpr int RS_STAGE = SCAN_BLOCK * RS_SCAP;   // 4352
+constexpr int RS_SCAP = PCS_RS_SCAP;
+constexpr int RS_STAGE = SCAN_BLOCK * RS_SCAP;   // 6400
 
 __device__ __forceinline__ void grid_barrier(TrackCtl* C, int nblocks) {
   __syncthreads();
@@ -1224,7 +1228,7 @@ struct RsSmem {
 // the systematic kernel carries none of it
 template <int KIND, bool MULTI = false>
 #ifndef PCS_RS_MINB
-#define PCS_RS_MINB 4
+#define PCS_RS_MINB 3
 #endif
 __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? PCS_RS_MINB : 2) k_sys_resample(TrackParams P) {
   typedef typename RsElem<KIND>::T E;
