@@ -133,6 +133,9 @@ enum Slot {
   SL_MT_TGT,
   SL_MT_HASH,
   SL_MT_OUT,
+  SL_MT_WPREV,
+  SL_MT_LL,
+  SL_MT_CDF,
   SL_SYNTH,
   SL_FMAP,
   SL_TR_WPREV,
@@ -1291,8 +1294,10 @@ int pcs_mt_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t n_targets,
   cudaStream_t st = S(stream);
   static bool attr = false;
   if (!attr) {
-    const void* fns[] = {(const void*)k_mt_frame<0>, (const void*)k_mt_frame<9>,
-                         (const void*)k_mt_frame<11>, (const void*)k_mt_frame<15>};
+    const void* fns[] = {(const void*)k_mt_frame<0, false>, (const void*)k_mt_frame<9, false>,
+                         (const void*)k_mt_frame<11, false>, (const void*)k_mt_frame<15, false>,
+                         (const void*)k_mt_frame<0, true>, (const void*)k_mt_frame<9, true>,
+                         (const void*)k_mt_frame<11, true>, (const void*)k_mt_frame<15, true>};
     for (const void* f : fns) {
       PCS_CUDA_TRY(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)MT_SMEM));
@@ -1320,6 +1325,20 @@ int pcs_mt_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t n_targets,
   P.frame0 = cfg->frame0;
   P.placement = cfg->placement;
   P.K = n_frames;
+  PCS_CHECK_ARG(cfg->scheme == 0 || cfg->scheme == 1, "scheme must be 0 (systematic) or 1 (multinomial)");
+  PCS_CHECK_ARG(!cfg->weighted_com, "the multi-target kernel places dummies at the unweighted centre of mass");
+  const double frac = cfg->threshold_fraction > 0.0 ? cfg->threshold_fraction : 1.0;
+  PCS_CHECK_ARG(frac <= 1.0, "threshold_fraction must be in (0, 1]");
+  P.thresh = frac * (double)n;   // the reference's threshold_fraction * n_particles
+  P.multinomial = cfg->scheme;
+  P.wprev = nullptr;
+  P.ll = nullptr;
+  P.cdf = nullptr;
+  if (P.thresh < (double)n) {    // frames may carry prior weights
+    PCS_SCRATCH(SL_MT_WPREV, ld * sizeof(float), P.wprev);
+    PCS_SCRATCH(SL_MT_LL, ld * sizeof(double), P.ll);
+  }
+  if (P.multinomial) PCS_SCRATCH(SL_MT_CDF, ld * sizeof(double), P.cdf);
   PCS_SCRATCH(SL_MT_BUF0, 5 * ld * sizeof(float), P.buf0);
   PCS_SCRATCH(SL_MT_BUF1, 5 * ld * sizeof(float), P.buf1);
   PCS_SCRATCH(SL_MT_ANC, ld * sizeof(int), P.anc);
@@ -1339,6 +1358,8 @@ int pcs_mt_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t n_targets,
     h[t].flags = 0;
     h[t].first_bad = INT_MAX;
     h[t].evals = 0;
+    h[t].prior = 0;
+    h[t].pad = 0;
     pcs_init_t init = cfg->init;
     for (int c = 0; c < 5; ++c) init.center[c] = centers[t * 5 + c];
     const u64 seed_t = cfg->seed + (u64)(target_offset + t) * MT_KEY_STEP;
@@ -1364,12 +1385,17 @@ int pcs_mt_step(pcs_ctx* ctx, const float* frame, int64_t k, void* stream) {
   M.P.k = k;
   cudaStream_t st = S(stream);
   const unsigned grid = (unsigned)M.P.T;
+  const bool gen = M.P.thresh < (double)M.P.n || M.P.multinomial;
+#define PCS_MT_LAUNCH(S)                                                       \
+  (gen ? k_mt_frame<S, true><<<grid, MT_THREADS, MT_SMEM, st>>>(M.P)           \
+       : k_mt_frame<S, false><<<grid, MT_THREADS, MT_SMEM, st>>>(M.P))
   switch (M.maxs) {
-    case 9: k_mt_frame<9><<<grid, MT_THREADS, MT_SMEM, st>>>(M.P); break;
-    case 11: k_mt_frame<11><<<grid, MT_THREADS, MT_SMEM, st>>>(M.P); break;
-    case 15: k_mt_frame<15><<<grid, MT_THREADS, MT_SMEM, st>>>(M.P); break;
-    default: k_mt_frame<0><<<grid, MT_THREADS, MT_SMEM, st>>>(M.P);
+    case 9: PCS_MT_LAUNCH(9); break;
+    case 11: PCS_MT_LAUNCH(11); break;
+    case 15: PCS_MT_LAUNCH(15); break;
+    default: PCS_MT_LAUNCH(0);
   }
+#undef PCS_MT_LAUNCH
   PCS_LAUNCH_CHECK();
   M.k = k + 1;
   return PCS_OK;

@@ -10,7 +10,14 @@
 //   B  occupied cells -> dummies -> likelihood (frame region staged in shared
 //      memory) -> exact normaliser -> per-cell weights, estimate, ESS, decision
 //   C  exact-prefix systematic resampling over the target's particles (tiles
-//      scanned in order inside the CTA; no inter-CTA look-back needed)
+//      scanned in order inside the CTA; no inter-CTA look-back needed), or the
+//      exact cdf and a binary search of the frame's Philox points (multinomial)
+// With ESS-threshold resampling a frame that does not resample hands its
+// normalised weights to the next one (wprev); that frame's weights are then
+// per particle, log w = log w_prev + ll[cell] (binning.py:190-192,
+// filtering.py:69,169-171), and phase B finishes it per particle with the
+// canonical sums of the single-target kernels (k_pc_prior_ll, k_sir_sum,
+// k_sir_stats).
 // Target t uses the RNG key seed_t = seed + t*0x9E3779B97F4A7C15 with local
 // particle indices, so every target equals a single-target pcsir_track run
 // with seed_t bit for bit (tests/test_gpu_multi.py).
@@ -51,6 +58,8 @@ struct MtTarget {
   u32 flags;
   int first_bad;
   i64 evals;
+  int prior;             // this frame's particles carry prior weights (wprev)
+  int pad;
 };
 
 struct MtHash {          // one outlier cell
@@ -79,6 +88,11 @@ struct MtParams {
   const float* frame;    // current frame
   i64 k;                 // frame index (buffer parity, RNG frame, output row)
   i64 K;                 // output rows per target
+  double thresh;         // resample when ESS < thresh (threshold_fraction * n)
+  int multinomial;       // resampling scheme (filtering.py:96-100)
+  float* wprev;          // [T*n] prior weights (threshold < 1; else null)
+  double* ll;            // [T*n] per-particle log w, then exp(log w - m) (prior frames)
+  double* cdf;           // [T*n] exact cdf (multinomial; else null)
   double* out_est;       // [T][K][5]
   double* out_ess;       // [T][K]
   unsigned char* out_res;
@@ -92,6 +106,8 @@ struct MtSmem {
   u32 acc_cnt[MT_SUBW];
   u32 tile_cnt[MT_SUBW];
   u128 wfix_sub[MT_SUBW];          // exact cdf weight round(w 2^120) per sub-window cell
+                                   // (prior frames: the cell log-likelihood, as double)
+  float wsub_f[MT_SUBW];           // normalised weight per sub-window cell (wprev)
   unsigned short tile_start[MT_SUBW];
   float ref[2 * MT_SIDE + 1];      // sub-window cell edges (x then y; NaN: unusable)
   union {
@@ -115,6 +131,7 @@ struct MtSmem {
   int scan_tmp[MT_WARPS];
   i128 red[MT_WARPS * 6];
   long long lmax;
+  long long plmax;                 // prior frames: max per-particle log w
   int box[4];
   u32 n_occ;
   unsigned wmin, wmax;
@@ -124,6 +141,14 @@ struct MtSmem {
 };
 
 __device__ __forceinline__ u32 mt_hash_slot(u32 key) { return (key * 2654435761u) & (MT_HCAP - 1); }
+
+// slot of outlier cell `flat` (present: it holds a particle of this frame)
+__device__ __forceinline__ u32 mt_hash_find(const MtHash* H, u32 flat) {
+  const u32 key = flat + 1u;
+  u32 s = mt_hash_slot(key);
+  for (int probe = 0; probe < MT_HCAP && H[s].key != key; ++probe) s = (s + 1u) & (MT_HCAP - 1);
+  return s;
+}
 
 // exact int128 atomics into the target's outlier hash table
 __device__ __forceinline__ bool mt_hash_add(MtHash* H, u32 flat, const float o[5]) {
@@ -142,7 +167,9 @@ __device__ __forceinline__ bool mt_hash_add(MtHash* H, u32 flat, const float o[5
   return false;
 }
 
-template <int MAXS>
+// GEN: ESS-threshold and / or multinomial resampling compiled in (the
+// every-frame systematic configuration runs the instantiation without them)
+template <int MAXS, bool GEN>
 #ifndef PCS_MT_CTAS
 #define PCS_MT_CTAS 2
 #endif
@@ -153,6 +180,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
   const i64 tg = blockIdx.x;
   MtTarget& TG = P.tgt[tg];
   if (TG.flags & PCS_FLAG_CAPACITY) return;   // this target needs the general path
+  const bool prior = GEN && TG.prior != 0;     // (thread 0 rewrites it in phase B)
   const u64 seed_t = P.seed + (u64)(P.tgt_off + tg) * MT_KEY_STEP;
   const i64 n = P.n, ld = P.ld, base_i = tg * n;
   const i64 k = P.k;
@@ -189,6 +217,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     sm.n_list = 0;
     sm.n_occ = 0;
     sm.lmax = LLONG_MIN;
+    sm.plmax = LLONG_MIN;
     sm.wmin = 0xFFFFFFFFu;
     sm.wmax = 0u;
     sm.box[0] = INT_MAX; sm.box[1] = INT_MIN; sm.box[2] = INT_MAX; sm.box[3] = INT_MIN;
@@ -404,53 +433,116 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
   }
   atomicMax(&sm.lmax, lmax);
   __syncthreads();
-  const double m = ordered_to_f64((i64)sm.lmax);
+  i128 e[6] = {0, 0, 0, 0, 0, 0};
+  double m;
+  if (!prior) {
+    m = ordered_to_f64((i64)sm.lmax);
+    i128 acc1[1] = {0};
+    for (int b = t; b < M; b += MT_THREADS) {
+      int o = sm.u.b.occ[b];
+      u32 cnt = (o >= 0) ? sm.acc_cnt[o] : HT[-o - 1].cnt;
+      acc1[0] += (i128)cnt * f64_to_fixed(exp(__dsub_rn(sm.u.b.ll[b], m)), FX_S);
+    }
+    block_sum_i128_k<MT_THREADS, 1>(acc1, sm.red);
+    if (t == 0) sm.Sf = scalbn(i128_to_f64_rn(acc1[0]), -FX_S);
+    __syncthreads();
+    const double Sf = sm.Sf;
+    for (int b = t; b < M; b += MT_THREADS) {
+      int o = sm.u.b.occ[b];
+      float w = normalised_weight(sm.u.b.ll[b], m, Sf);
+      atomicMin(&sm.wmin, __float_as_uint(w));
+      atomicMax(&sm.wmax, __float_as_uint(w));
+      i128 wq = f32_to_fixed(w, FX_WQ);
+      u32 cnt;
+      if (o >= 0) {
+        sm.wfix_sub[o] = cdf_fixed(w);
+        sm.wsub_f[o] = w;
+        cnt = sm.acc_cnt[o];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) {
+          i128 S = digits_value<MT_SUBW>(&sm.dig[0][0], c, o);
+          if (c == 0) S += (i128)cnt * f32_to_fixed(sm.ref[o % snxi], FX_STATE);
+          if (c == 1) S += (i128)cnt * f32_to_fixed(refy[o / snxi], FX_STATE);
+          e[c] += wq * S;
+        }
+      } else {
+        MtHash& h = HT[-o - 1];
+        cnt = h.cnt;
+        // the sums are consumed: zero them for the next frame; the cell's
+        // weight waits for phase C in sum[4][1] (cleared there)
+#pragma unroll
+        for (int c = 0; c < 5; ++c) e[c] += wq * load_i128(h.sum[c]);
+        h.sum[0][0] = 0; h.sum[0][1] = 0; h.sum[1][0] = 0; h.sum[1][1] = 0;
+        h.sum[2][0] = 0; h.sum[2][1] = 0; h.sum[3][0] = 0; h.sum[3][1] = 0;
+        h.sum[4][0] = 0;
+        h.sum[4][1] = (u64)__float_as_uint(w);
+      }
+      e[5] += (i128)cnt * f64_to_fixed((double)w * (double)w, FX_W2);
+    }
+  } else {
+    // prior weights: the cell log-likelihoods by cell code (sub-window table
+    // aliasing wfix_sub; outlier cells in their hash slot, sums zeroed)
+    double* llsub = reinterpret_cast<double*>(sm.wfix_sub);
+    for (int b = t; b < M; b += MT_THREADS) {
+      const int o = sm.u.b.occ[b];
+      const double llb = sm.u.b.ll[b];
+      if (o >= 0) {
+        llsub[o] = llb;
+      } else {
+        MtHash& h = HT[-o - 1];
+        h.sum[0][0] = 0; h.sum[0][1] = 0; h.sum[1][0] = 0; h.sum[1][1] = 0;
+        h.sum[2][0] = 0; h.sum[2][1] = 0; h.sum[3][0] = 0; h.sum[3][1] = 0;
+        h.sum[4][0] = 0;
+        h.sum[4][1] = (u64)__double_as_longlong(llb);
+      }
+    }
+    __syncthreads();
+    // log w = log w_prev + ll[cell] and its maximum (k_pc_prior_ll)
+    long long pm = LLONG_MIN;
+    bool nf = false;
+    for (i64 j = t; j < n; j += MT_THREADS) {
+      const u32 code = P.pslot[base_i + j];
+      const double llc = (code & 0x80000000u)
+                             ? __longlong_as_double((long long)HT[mt_hash_find(HT, code & 0x7FFFFFFFu)].sum[4][1])
+                             : llsub[code];
+      const double ll = __dadd_rn(log((double)P.wprev[base_i + j]), llc);
+      P.ll[base_i + j] = ll;
+      if (!(ll == ll) || ll == INFINITY) nf = true;
+      pm = max(pm, (long long)f64_to_ordered(ll));
+    }
+    if (nf) atomicOr(&TG.flags, (u32)PCS_FLAG_NONFINITE);
+    atomicMax(&sm.plmax, pm);
+    __syncthreads();
+    m = ordered_to_f64((i64)sm.plmax);
+    // S = sum round(exp(log w - m) 2^95), exp(log w - m) kept per particle (k_sir_sum)
+    i128 acc1[1] = {0};
+    for (i64 j = t; j < n; j += MT_THREADS) {
+      const double ex = exp(__dsub_rn(P.ll[base_i + j], m));
+      P.ll[base_i + j] = ex;
+      acc1[0] += f64_to_fixed(ex, FX_S);
+    }
+    block_sum_i128_k<MT_THREADS, 1>(acc1, sm.red);
+    if (t == 0) sm.Sf = scalbn(i128_to_f64_rn(acc1[0]), -FX_S);
+    __syncthreads();
+    const double Sf = sm.Sf;
+    // estimate / ESS numerators per particle (k_sir_stats)
+    unsigned wmn = 0xFFFFFFFFu, wmx = 0u;
+    for (i64 j = t; j < n; j += MT_THREADS) {
+      const float w = weight_from_ex(P.ll[base_i + j], Sf);
+      wmn = min(wmn, __float_as_uint(w));
+      wmx = max(wmx, __float_as_uint(w));
+      const i128 wq = f32_to_fixed(w, FX_WQ);
+#pragma unroll
+      for (int c = 0; c < 5; ++c) e[c] += wq * f32_to_fixed(sout[c * ld + base_i + j], FX_STATE);
+      e[5] += f64_to_fixed((double)w * (double)w, FX_W2);
+    }
+    atomicMin(&sm.wmin, wmn);
+    atomicMax(&sm.wmax, wmx);
+  }
   const bool bad_m = !(m == m) || m == INFINITY;
   const bool degenerate = (m == -INFINITY);
-  i128 acc1[1] = {0};
-  for (int b = t; b < M; b += MT_THREADS) {
-    int o = sm.u.b.occ[b];
-    u32 cnt = (o >= 0) ? sm.acc_cnt[o] : HT[-o - 1].cnt;
-    acc1[0] += (i128)cnt * f64_to_fixed(exp(__dsub_rn(sm.u.b.ll[b], m)), FX_S);
-  }
-  block_sum_i128_k<MT_THREADS, 1>(acc1, sm.red);
-  if (t == 0) sm.Sf = scalbn(i128_to_f64_rn(acc1[0]), -FX_S);
-  __syncthreads();
-  const double Sf = sm.Sf;
-  i128 e[6] = {0, 0, 0, 0, 0, 0};
-  for (int b = t; b < M; b += MT_THREADS) {
-    int o = sm.u.b.occ[b];
-    float w = normalised_weight(sm.u.b.ll[b], m, Sf);
-    atomicMin(&sm.wmin, __float_as_uint(w));
-    atomicMax(&sm.wmax, __float_as_uint(w));
-    i128 wq = f32_to_fixed(w, FX_WQ);
-    u32 cnt;
-    if (o >= 0) {
-      sm.wfix_sub[o] = cdf_fixed(w);
-      cnt = sm.acc_cnt[o];
-#pragma unroll
-      for (int c = 0; c < 5; ++c) {
-        i128 S = digits_value<MT_SUBW>(&sm.dig[0][0], c, o);
-        if (c == 0) S += (i128)cnt * f32_to_fixed(sm.ref[o % snxi], FX_STATE);
-        if (c == 1) S += (i128)cnt * f32_to_fixed(refy[o / snxi], FX_STATE);
-        e[c] += wq * S;
-      }
-    } else {
-      MtHash& h = HT[-o - 1];
-      cnt = h.cnt;
-      // keep the weight in the (otherwise consumed) count-free slot: sum[0][1] is
-      // restored below; weights of hash cells live in a float alias of sum[4][1]
-#pragma unroll
-      for (int c = 0; c < 5; ++c) e[c] += wq * load_i128(h.sum[c]);
-      h.sum[0][0] = 0; h.sum[0][1] = 0; h.sum[1][0] = 0; h.sum[1][1] = 0;
-      h.sum[2][0] = 0; h.sum[2][1] = 0; h.sum[3][0] = 0; h.sum[3][1] = 0;
-      h.sum[4][0] = 0;
-      h.sum[4][1] = (u64)__float_as_uint(w);   // weight for phase C; cleared there
-    }
-    e[5] += (i128)cnt * f64_to_fixed((double)w * (double)w, FX_W2);
-  }
   block_sum_i128_k<MT_THREADS, 6>(e, sm.red);
-  __shared__ int s_res;
+  __shared__ int s_res, s_keep;
   if (t == 0) {
     const i64 row = tg * P.K + k;
     double ess = 1.0 / scalbn(i128_to_f64_rn(e[5]), -FX_W2);
@@ -464,8 +556,16 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
       P.out_est[row * 5 + c] = est[c];
     }
     P.out_ess[row] = ess;
-    int res = (!flag_bad && ess < (double)n) ? 1 : 0;
-    if (!res && !flag_bad && sm.wmin != sm.wmax) atomicOr(&TG.flags, (u32)PCS_FLAG_CAPACITY);
+    int res = (!flag_bad && ess < P.thresh) ? 1 : 0;   // filtering.py:169-170
+    // without resampling the next frame starts from these weights unless they
+    // are all equal (then uniform, as the single-target loop does)
+    int keep = (!res && !flag_bad && sm.wmin != sm.wmax) ? 1 : 0;
+    if (keep && !P.wprev) {   // (threshold 1: ESS rounded up to n with unequal weights)
+      atomicOr(&TG.flags, (u32)PCS_FLAG_CAPACITY);
+      keep = 0;
+    }
+    TG.prior = keep;
+    s_keep = keep;
     P.out_res[row] = (unsigned char)res;
     P.out_occ[row] = M;
     TG.evals += M;
@@ -478,11 +578,14 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
   }
   __syncthreads();
 
-  // ---------------- phase C: exact-prefix systematic resampling ----------------
+  // ---------------- phase C: exact-prefix resampling ----------------
   // (k_sys_resample in one CTA: scan tiles of 2560 particles in order, exact
   // u128 prefixes, first slot per item from the top 64 bits of the prefix,
-  // run heads + block max-scan, coalesced ancestor writes)
-  const int do_res = s_res;
+  // run heads + block max-scan, coalesced ancestor writes; multinomial: the
+  // exact cdf per particle, then k_multinomial_emit's search)
+  const int do_res = s_res, keep = GEN && s_keep;
+  const bool multi = GEN && P.multinomial != 0;
+  const double Sfr = sm.Sf;
   const double u = philox_resample_u(seed_t, P.frame0 + (u32)k);
   constexpr int CI = MT_CI;
   constexpr int CT = MT_CT;
@@ -503,13 +606,32 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     }
     return 0;
   };
+  // exact weight of item kk of the scan tile at `base` (prior frames: per particle)
+  auto itemw = [&](int kk, i64 base, int nv) -> u128 {
+    if (!prior) return cellw(cells[kk]);
+    return (kk < nv) ? cdf_fixed(weight_from_ex(P.ll[base_i + base + kk], Sfr)) : (u128)0;
+  };
   u128 pre = 0;
   const int k0 = t * CI;
   for (i64 base = 0; base < n; base += CT) {
     if (!do_res) {
       for (int q = 0; q < CI; ++q) {
         const i64 i = base + (i64)q * MT_THREADS + t;
-        if (i < n) P.anc[base_i + i] = (int)i;
+        if (i < n) {
+          P.anc[base_i + i] = (int)i;
+          if (keep) {   // the particles keep their weights (filtering.py:171)
+            float w;
+            if (prior) {
+              w = weight_from_ex(P.ll[base_i + i], Sfr);
+            } else {
+              const u32 code = P.pslot[base_i + i];
+              w = (code & 0x80000000u)
+                      ? __uint_as_float((u32)HT[mt_hash_find(HT, code & 0x7FFFFFFFu)].sum[4][1])
+                      : sm.wsub_f[code];
+            }
+            P.wprev[base_i + i] = w;
+          }
+        }
       }
       continue;
     }
@@ -521,7 +643,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     __syncthreads();
     u128 tsum = 0;
 #pragma unroll
-    for (int q = 0; q < CI; ++q) tsum += cellw(cells[k0 + q]);
+    for (int q = 0; q < CI; ++q) tsum += itemw(k0 + q, base, nv);
     u128 inc = tsum;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -537,9 +659,23 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     }
     const u128 excl = pre + woff + (inc - tsum);
     const bool last_tile = base + CT >= n;
+    const int klast = last_tile ? nv - 1 : -1;   // the target's last particle ends at slot n
+    if (multi) {   // the exact cdf (filtering.py:94-95); the search follows the scan
+      u128 run = excl;
+#pragma unroll
+      for (int q = 0; q < CI; ++q) {
+        const int kk = k0 + q;
+        if (kk < nv) {
+          run += itemw(kk, base, nv);
+          P.cdf[base_i + base + kk] = (kk == klast) ? 1.0 : cdf_round(run);
+        }
+      }
+      pre += tagg;
+      __syncthreads();   // (wtot is rewritten by the next tile)
+      continue;
+    }
     const i64 tj0 = (base == 0) ? 0 : first_slot_fast(cdf_round(pre), u, n, nd, eps);
     const i64 tj1 = last_tile ? n : first_slot_fast(cdf_round(pre + tagg), u, n, nd, eps);
-    const int klast = last_tile ? nv - 1 : -1;   // the target's last particle ends at slot n
     {
       const double tj0d = (double)tj0;
       int jr = 0;
@@ -550,7 +686,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
         const int kk = k0 + q;
         int h = -1;   // no slot
         if (kk < nv) {
-          run += cellw(cells[kk]);
+          run += itemw(kk, base, nv);
           const int jend = (kk == klast) ? (int)(n - tj0) : slot_rel(run, u, n, nd, kappa, eps, tj0d, tj0);
           if (jend > jr) h = jr;
           jr = jend;
@@ -605,7 +741,26 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     }
     pre += tagg;
   }
-  // clear the consumed outlier cells for the next frame
+  if (do_res && multi) {
+    // ancestor j = searchsorted(cdf, p_j, 'right') over the target's exact cdf,
+    // p_j = philox_multinomial_u(seed_t, frame, j) (filtering.py:96-97,100)
+    __syncthreads();   // the cdf writes of every thread are visible
+    const double* cdf = P.cdf + base_i;
+    const u32 f = P.frame0 + (u32)k;
+    for (i64 j = t; j < n; j += MT_THREADS) {
+      const double p = philox_multinomial_u(seed_t, f, (u64)j);
+      i64 lo = 0, hi = n;   // first index with cdf > p
+      while (lo < hi) {
+        const i64 mid = (lo + hi) >> 1;
+        if (cdf[mid] <= p) lo = mid + 1;
+        else hi = mid;
+      }
+      P.anc[base_i + j] = (int)((lo < n) ? lo : n - 1);
+    }
+  }
+  // clear the consumed outlier cells for the next frame (after every thread's
+  // last read of them: the identity path above reads weights without a barrier)
+  __syncthreads();
   for (int s = t; s < MT_HCAP; s += MT_THREADS) {
     if (HT[s].key) {
       HT[s].key = 0u;

@@ -3,7 +3,9 @@ one filter per spot, ``experiments.py:251-292`` loops targets /
 repetitions serially).
 
 ``multi_pcsir_track`` runs T independent pcSIR filters over the same frame
-sequence in one kernel launch per frame (one CTA per target, pcs_mt_*).
+sequence in one kernel launch per frame (one CTA per target, pcs_mt_*), with
+the configuration's ResampleConfig (ESS threshold, systematic or multinomial;
+filtering.py:38-39,96-100,169-171).
 Target t uses the RNG key ``seed + t * 0x9E3779B97F4A7C15`` so it is exactly
 ``pcsir_track(frames, cfg_t, PhiloxRng(seed_t))`` with ``cfg_t`` centred on
 target t. Across GPUs the targets are partitioned ([r*T/P, (r+1)*T/P) on rank
@@ -47,9 +49,9 @@ class MultiTargetTracker:
 
     def __init__(self, cfg, centers, seed, n_frames, height, width, target_offset=0):
         r = cfg.resampling
-        if r.threshold_fraction != 1.0 or r.scheme != "systematic":
-            raise ValueError("the multi-target kernel resamples every frame (systematic, "
-                             "threshold_fraction=1.0); run pcsir_track per target otherwise")
+        if getattr(cfg, "weighted_com", False):
+            raise ValueError("the multi-target kernel places dummies at the unweighted centre "
+                             "of mass; run pcsir_track per target for weighted_com=True")
         centers = np.ascontiguousarray(np.asarray(centers, dtype=np.float64).reshape(-1, 5))
         self.T = centers.shape[0]
         self.K = n_frames
@@ -61,6 +63,8 @@ class MultiTargetTracker:
         c.dyn = cfg.dynamics.to_c()
         c.spot = cfg.likelihood.spot_c(cells=True)
         c.grid = cfg.grid.to_c()
+        c.threshold_fraction = r.threshold_fraction      # filtering.py:169-171
+        c.scheme = 1 if r.scheme == "multinomial" else 0  # filtering.py:96-100
         c.seed = seed % (1 << 64)
         c.frame0 = 0
         c.use_graph = 0

@@ -43,6 +43,49 @@ def test_each_target_equals_single_target_filter(cuda, cpp, n):
     assert err < 1.0
 
 
+@pytest.mark.parametrize("frac,scheme,cpp", [(0.5, "systematic", 1), (0.2, "systematic", 4),
+                                              (1.0, "multinomial", 2), (0.5, "multinomial", 1),
+                                              (0.5, "multinomial", 4)])
+def test_threshold_and_multinomial_equal_single_target(cuda, frac, scheme, cpp):
+    """ResampleConfig other than (1.0, systematic) in the batched kernel: ESS-
+    threshold frames that do not resample hand their weights to the next frame
+    (log w = log w_prev + ll[cell], filtering.py:169-171, binning.py:190-192),
+    and multinomial frames search the exact cdf (filtering.py:96-100). Every
+    target still equals its single-target fused filter bit for bit."""
+    n, T, K = 3000, 10, 8
+    frames, truth = mt.multi_target_scene(T, K, 160, seed=8)
+    centers = truth[:, 0].copy()
+    res = pc.ResampleConfig(frac, scheme)
+    lik = pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(10.0, 5))
+    grid = pc.BinGrid.pixel_aligned(160, 160, cpp)
+    cfg = pc.PcFilterConfig(n, pc.InitSpec(pc.StateVector(0, 0, 0, 0, 20.0), "gauss", sigma=2.0),
+                            pc.DynamicsParams(0.5, 0.1, 1.0), res, lik, grid=grid)
+    r = mt.multi_pcsir_track(frames, cfg, centers, 31)
+    if frac < 1.0:
+        assert 0 < int(r.resampled.sum()) < T * K    # both kinds of frames occur
+    for t in range(T):
+        cfg_t = pc.PcFilterConfig(
+            n, pc.InitSpec(pc.StateVector(*centers[t]), "gauss", sigma=2.0),
+            pc.DynamicsParams(0.5, 0.1, 1.0), res,
+            pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(10.0, 5)), grid=grid)
+        single = pc.pcsir_track([pc.ImageFrame(f) for f in frames], cfg_t,
+                                pc.PhiloxRng(mt.target_seed(31, t)))
+        assert single.path == "fused"
+        assert np.array_equal(r.resampled[t], single.resampled), t
+        assert np.array_equal(r.estimates[t], single.estimates), t
+        assert np.array_equal(r.ess[t], single.ess), t
+        assert int(r.likelihood_evals[t]) == single.likelihood_evals
+
+
+def test_weighted_com_rejected(cuda):
+    frames, truth = mt.multi_target_scene(1, 1, 160, seed=6)
+    cfg = _cfg(1000)
+    cfg = pc.PcFilterConfig(cfg.n_particles, cfg.init, cfg.dynamics, cfg.resampling, cfg.likelihood,
+                            grid=cfg.grid, weighted_com=True)
+    with pytest.raises(ValueError, match="unweighted centre"):
+        mt.multi_pcsir_track(frames, cfg, truth[:, 0].copy(), 1)
+
+
 def test_target_offset_selects_keys(cuda):
     frames, truth = mt.multi_target_scene(6, 3, 160, seed=4)
     centers = truth[:, 0].copy()
