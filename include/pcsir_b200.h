@@ -295,11 +295,23 @@ int pcs_mt_results(pcs_ctx* ctx, double* est, double* ess, uint8_t* resampled, i
  *   pcs_shard_step1(frame k)      -> box: device int64[5]     (all-reduce MAX)
  *   pcs_shard_export(box)         -> limbs: device int64[wcap*16] (all-reduce SUM)
  *   pcs_shard_import_bins(box, limbs)   (identical bins stage on every rank)
+ *   threshold_fraction < 1 only (frames whose particles carry prior weights,
+ *   filtering.py:169-171; neutral values on the other frames):
+ *     pcs_shard_prior(0)          -> out int64[1] max log-weight     (all-reduce MAX)
+ *     pcs_shard_prior(1, in)      -> out int64[3] normaliser limbs   (all-reduce SUM)
+ *     pcs_shard_prior(2, in)      -> out int64[18] estimate / ESS limbs (SUM),
+ *                                    out_mm int64[2] weight range       (MAX)
+ *     pcs_shard_prior(3, in, in_mm)  finalises the frame on every rank
  *   pcs_shard_total()             -> total: device int64[3]   (all-gather -> totals[world*3])
- *   pcs_shard_emit(totals)        -> send_prev / send_next: device float32[5*bcap+1]
+ *   systematic (scheme 0):
+ *     pcs_shard_emit(totals)      -> send_prev / send_next: device float32[5*bcap+1]
  *                                    (send to rank-1 / rank+1, receive recv_prev
  *                                    from rank-1, recv_next from rank+1)
- *   pcs_shard_unpack(recv_prev, recv_next)
+ *     pcs_shard_unpack(recv_prev, recv_next)
+ *   multinomial (scheme 1; bcap = requests per rank pair):
+ *     pcs_shard_route(totals)     -> req int32[world*(1+bcap)]        (all-to-all)
+ *     pcs_shard_serve(req_in)     -> resp float32[world*5*bcap]      (all-to-all)
+ *     pcs_shard_install(resp_in)
  * Results (est/ess/resampled/occupied rows) and flags as for pcs_track;
  * pcs_track_end reads the flags (all-reduce them so every rank raises). */
 int pcs_shard_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t height, int64_t width,
@@ -313,6 +325,11 @@ int pcs_shard_total(pcs_ctx* ctx, int64_t* total, void* stream);
 int pcs_shard_emit(pcs_ctx* ctx, const int64_t* totals, float* send_prev, float* send_next,
                    void* stream);
 int pcs_shard_unpack(pcs_ctx* ctx, const float* recv_prev, const float* recv_next, void* stream);
+int pcs_shard_prior(pcs_ctx* ctx, int32_t stage, const int64_t* in, const int64_t* in_mm,
+                    int64_t* out, int64_t* out_mm, void* stream);
+int pcs_shard_route(pcs_ctx* ctx, const int64_t* totals, int32_t* req, void* stream);
+int pcs_shard_serve(pcs_ctx* ctx, const int32_t* req_in, float* resp, void* stream);
+int pcs_shard_install(pcs_ctx* ctx, const float* resp_in, void* stream);
 
 #ifdef __cplusplus
 }

@@ -144,6 +144,11 @@ _SIGNATURES = [
     ("pcs_shard_total", c_int32, [c_void_p, c_void_p, c_void_p]),
     ("pcs_shard_emit", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p]),
     ("pcs_shard_unpack", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("pcs_shard_prior", c_int32, [c_void_p, c_int32, c_void_p, c_void_p, c_void_p, c_void_p,
+                                  c_void_p]),
+    ("pcs_shard_route", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("pcs_shard_serve", c_int32, [c_void_p, c_void_p, c_void_p, c_void_p]),
+    ("pcs_shard_install", c_int32, [c_void_p, c_void_p, c_void_p]),
 ]
 
 EXPORTED_SYMBOLS = [name for name, _, _ in _SIGNATURES]

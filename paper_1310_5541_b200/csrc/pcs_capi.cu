@@ -75,6 +75,8 @@ struct TrackState {
   bool s1_pow2 = false;  // k_pc_step1<true>: power-of-two cells, float32-exact origins
   int shard_rank = 0, shard_world = 1;   // sharded filter (pcs_shard_*)
   i64 shard_wcap = 0, shard_bcap = 0;
+  double* shard_bnd = nullptr;     // multinomial: global cdf at the rank boundaries
+  u32* shard_cnt = nullptr;        // multinomial: [world] requests, [world] sent
   int maxs = 0;
   i64 k = 0;             // host mirror of the frame counter
   cudaGraphExec_t exec = nullptr;
@@ -126,6 +128,8 @@ enum Slot {
   SL_TR_PRE,
   SL_SHARD_ANC,
   SL_SHARD_BOX,
+  SL_SHARD_BND,
+  SL_SHARD_CNT,
   SL_MT_BUF0,
   SL_MT_BUF1,
   SL_MT_ANC,
@@ -1432,20 +1436,31 @@ int pcs_shard_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int64_t
   PCS_CHECK_ARG(world >= 1 && rank >= 0 && rank < world, "bad rank / world");
   PCS_CHECK_ARG(n_global == (int64_t)world * cfg->n_particles, "n_global must be world x n_local");
   PCS_CHECK_ARG(wcap >= 1 && bcap >= 1 && bcap <= cfg->n_particles, "bad exchange capacities");
-  PCS_CHECK_ARG(cfg->threshold_fraction == 0.0 || cfg->threshold_fraction == 1.0,
-                "the sharded filter resamples every frame (threshold 1.0)");
-  PCS_CHECK_ARG(cfg->scheme == 0, "the sharded filter resamples systematically");
+  PCS_CHECK_ARG(cfg->scheme == 0 || cfg->scheme == 1, "scheme must be 0 (systematic) or 1 (multinomial)");
+  const double frac = cfg->threshold_fraction > 0.0 ? cfg->threshold_fraction : 1.0;
+  PCS_CHECK_ARG(frac <= 1.0, "threshold_fraction must be in (0, 1]");
+  // systematic: boundary states from / to the two neighbours (2 bcap extra
+  // particles); multinomial: up to bcap answered requests from every rank
+  const i64 extra = cfg->scheme ? (i64)world * bcap : 2 * bcap;
   pcs_track_cfg_t c = *cfg;
   c.use_graph = 0;
-  int r = track_begin(ctx, &c, H, W, 2 * bcap, stream);
+  int r = track_begin(ctx, &c, H, W, extra, stream);
   if (r) return r;
   TrackState& T = ctx->tr;
   TrackParams& P = T.P;
   P.idx_off = (i64)rank * cfg->n_particles;
   P.n_global = n_global;
-  P.thresh = (double)n_global;   // resample when ESS < N (the global particle count)
+  P.thresh = frac * (double)n_global;   // threshold_fraction x the global particle count
+  P.sharded = 1;
   P.slot_cap = cfg->n_particles + 2 * bcap;
   PCS_SCRATCH(SL_SHARD_ANC, P.slot_cap * sizeof(int), P.anc_out);
+  T.shard_bnd = nullptr;
+  T.shard_cnt = nullptr;
+  if (cfg->scheme) {
+    PCS_SCRATCH(SL_SHARD_BND, world * sizeof(double), T.shard_bnd);
+    PCS_SCRATCH(SL_SHARD_CNT, 2 * world * sizeof(u32), T.shard_cnt);
+    PCS_CUDA_TRY(cudaMemsetAsync(T.shard_cnt, 0, 2 * world * sizeof(u32), S(stream)));
+  }
   T.shard_rank = rank;
   T.shard_world = world;
   T.shard_wcap = wcap;
@@ -1500,7 +1515,8 @@ int pcs_shard_total(pcs_ctx* ctx, int64_t* total, void* stream) {
   TrackParams Q = T.P;
   Q.scan_mode = 1;
   launch_pdl(k_sys_resample<1>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<1>), st, Q);
-  k_shard_total<<<1, 32, 0, st>>>(Q, T.rs_grid, (i64*)total);
+  if (T.cond) launch_pdl(k_sys_resample<2>, T.rs_grid2, SCAN_BLOCK, sizeof(RsSmem<2>), st, Q);
+  k_shard_total<<<1, 32, 0, st>>>(Q, T.rs_grid, T.rs_grid2, (i64*)total);
   PCS_LAUNCH_CHECK();
   return PCS_OK;
 }
@@ -1508,13 +1524,15 @@ int pcs_shard_total(pcs_ctx* ctx, int64_t* total, void* stream) {
 int pcs_shard_emit(pcs_ctx* ctx, const int64_t* totals, float* send_prev, float* send_next,
                    void* stream) {
   PCS_CHECK_ARG(ctx && ctx->tr.active && totals && send_prev && send_next, "bad arguments");
+  PCS_CHECK_ARG(!ctx->tr.P.multinomial, "multinomial resampling exchanges through pcs_shard_route");
   cudaStream_t st = S(stream);
   TrackState& T = ctx->tr;
   k_shard_ranges<<<1, 32, 0, st>>>(T.P, (const i64*)totals, T.shard_rank, T.shard_world,
-                                   T.shard_bcap);
+                                   T.shard_bcap, 0, nullptr);
   TrackParams Q = T.P;
   Q.scan_mode = 2;
   launch_pdl(k_sys_resample<1>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<1>), st, Q);
+  if (T.cond) launch_pdl(k_sys_resample<2>, T.rs_grid2, SCAN_BLOCK, sizeof(RsSmem<2>), st, Q);
   k_shard_pack<<<grid_for(T.P.n, 256, ctx->sms), 256, 0, st>>>(T.P, T.shard_rank, send_prev,
                                                               send_next, T.shard_bcap);
   PCS_LAUNCH_CHECK();
@@ -1527,6 +1545,77 @@ int pcs_shard_unpack(pcs_ctx* ctx, const float* recv_prev, const float* recv_nex
   TrackState& T = ctx->tr;
   k_shard_unpack<<<grid_for(T.shard_bcap, 256, ctx->sms), 256, 0, st>>>(T.P, recv_prev, recv_next,
                                                                         T.shard_bcap);
+  PCS_LAUNCH_CHECK();
+  T.k += 1;
+  return PCS_OK;
+}
+
+// frames with prior weights (ESS threshold): stage 0 -> out[1] local max
+// log-weight; stage 1 (in = reduced max) -> out[3] normaliser limbs; stage 2
+// (in = reduced normaliser) -> out[18] estimate / ESS limbs, out_mm[2] weight
+// range; stage 3 (in = reduced limbs, in_mm = reduced range) finalises the
+// frame. Neutral values / no-ops on frames without prior weights.
+int pcs_shard_prior(pcs_ctx* ctx, int32_t stage, const int64_t* in, const int64_t* in_mm,
+                    int64_t* out, int64_t* out_mm, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && ctx->tr.P.sharded && stage >= 0 && stage <= 3,
+                "bad arguments");
+  PCS_CHECK_ARG((stage == 0 || in) && (stage < 3 ? out != nullptr : in_mm != nullptr) &&
+                    (stage != 2 || out_mm), "bad arguments");
+  cudaStream_t st = S(stream);
+  TrackState& T = ctx->tr;
+  if (!T.cond) return PCS_OK;   // threshold 1: no frame carries prior weights
+  TrackParams& P = T.P;
+  if (stage > 0) k_shard_prior_in<<<1, 32, 0, st>>>(P, stage - 1, (const i64*)in, (const i64*)in_mm);
+  if (stage == 0) k_pc_prior_ll<<<T.red_grid, 256, 0, st>>>(P);
+  if (stage == 1) k_sir_sum<<<T.red_grid, 256, 0, st>>>(P);
+  if (stage == 2) k_sir_stats<<<T.red_grid, 256, 0, st>>>(P);
+  if (stage < 3) k_shard_prior_out<<<1, 32, 0, st>>>(P, stage, (i64*)out, (i64*)out_mm);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+// multinomial: exact rank prefix and boundary cdf values, the rank's part of
+// the global cdf, local ancestors and the requests to the other ranks
+// (req int32 [world][1 + bcap], count first)
+int pcs_shard_route(pcs_ctx* ctx, const int64_t* totals, int32_t* req, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && totals && req, "bad arguments");
+  PCS_CHECK_ARG(ctx->tr.P.multinomial, "systematic resampling exchanges through pcs_shard_emit");
+  cudaStream_t st = S(stream);
+  TrackState& T = ctx->tr;
+  k_shard_ranges<<<1, 32, 0, st>>>(T.P, (const i64*)totals, T.shard_rank, T.shard_world,
+                                   T.shard_bcap, 1, T.shard_bnd);
+  TrackParams Q = T.P;
+  Q.scan_mode = 2;
+  launch_pdl(k_sys_resample<1, true>, T.rs_grid, SCAN_BLOCK, sizeof(RsSmem<1>), st, Q);
+  if (T.cond) launch_pdl(k_sys_resample<2, true>, T.rs_grid2, SCAN_BLOCK, sizeof(RsSmem<2>), st, Q);
+  k_shard_route<<<grid_for(T.P.n, 256, ctx->sms), 256, 0, st>>>(
+      T.P, T.shard_rank, T.shard_world, T.shard_bnd, (int*)req, T.shard_cnt, T.shard_bcap);
+  k_shard_route_fin<<<1, 256, 0, st>>>(T.P, T.shard_world, (int*)req, T.shard_cnt,
+                                       T.shard_cnt + T.shard_world, T.shard_bcap);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+// multinomial: answer the gathered requests (req_in int32 [world][1 + bcap])
+// with the ancestors' states (resp float32 [world][5 * bcap])
+int pcs_shard_serve(pcs_ctx* ctx, const int32_t* req_in, float* resp, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && ctx->tr.P.multinomial && req_in && resp, "bad arguments");
+  TrackState& T = ctx->tr;
+  const i64 total = (i64)T.shard_world * T.shard_bcap;
+  k_shard_serve<<<grid_for(total, 256, ctx->sms), 256, 0, S(stream)>>>(
+      T.P, T.shard_rank, T.shard_world, (const int*)req_in, resp, T.shard_bcap);
+  PCS_LAUNCH_CHECK();
+  return PCS_OK;
+}
+
+// multinomial: install the answered states (resp_in float32 [world][5 * bcap]);
+// the frame is complete
+int pcs_shard_install(pcs_ctx* ctx, const float* resp_in, void* stream) {
+  PCS_CHECK_ARG(ctx && ctx->tr.active && ctx->tr.P.multinomial && resp_in, "bad arguments");
+  TrackState& T = ctx->tr;
+  const i64 total = (i64)T.shard_world * T.shard_bcap;
+  k_shard_install<<<grid_for(total, 256, ctx->sms), 256, 0, S(stream)>>>(
+      T.P, T.shard_rank, T.shard_world, resp_in, T.shard_cnt + T.shard_world, T.shard_bcap);
   PCS_LAUNCH_CHECK();
   T.k += 1;
   return PCS_OK;

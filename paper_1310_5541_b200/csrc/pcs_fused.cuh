@@ -162,6 +162,9 @@ struct TrackParams {
   i64 slot_cap;              // capacity of anc_out
   int* anc_out;              // ancestors (local particle index) for slots slot_lo + k
   int scan_mode;             // k_sys_resample: 0 both passes, 1 pass 1 only, 2 pass 2 only
+  int sharded;               // particle-sharded filter: a frame with prior weights is
+                             // finalised after the all-reduce of its per-particle sums
+                             // (k_shard_prior_in), not by k_sir_stats
                              // (sharded: rank prefix and first slot in ctl)
   int s1_tile;               // k_pc_step1 tile (<= S1_TILE), balanced over its CTAs
   double thresh;             // resample when ESS < thresh (= threshold_fraction * N)

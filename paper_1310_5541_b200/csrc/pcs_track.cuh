@@ -261,7 +261,7 @@ __global__ void __launch_bounds__(256) k_sir_stats(TrackParams P) {
   if (last && threadIdx.x == 0) {
     __threadfence();
     C->stats_done = 0;
-    sir_finalize(P);
+    if (!P.sharded) sir_finalize(P);   // (sharded: after the all-reduce, pcs_shard.cuh)
   }
 }
 

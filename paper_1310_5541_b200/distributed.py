@@ -22,6 +22,21 @@ stream-ordered collectives and no host synchronisation (pcs_shard.cuh):
      the boundary slots owned by rank r-1 / r+1 travel, as states, in fixed
      bcap-slot buffers (grouped send / recv with the two neighbours).
 
+ESS-threshold resampling (``threshold_fraction < 1``, filtering.py:169-171)
+adds, between 3 and 4, the per-particle finish of frames whose particles
+carry prior weights: all-reduce MAX of the max log-weight, SUM of the exact
+normaliser, SUM of the exact estimate / ESS numerators with MAX of the weight
+range; then every rank takes the same decision. Frames without prior weights
+pass neutral values through the same fixed-size collectives, so the host
+never needs to know which kind of frame it is.
+
+Multinomial resampling (filtering.py:96-97,100) replaces 5: the ancestors
+are not monotone, so each rank routes its slots to the rank whose part of
+the global cdf holds their Philox point (the cdf's values at the rank
+boundaries follow from the gathered totals), requests the states of the
+remote ancestors (all-to-all of slot offsets, ``bcap`` per rank pair) and
+receives them (all-to-all of states).
+
 Philox counters use the global particle index, so the random draws — and
 therefore every result — are the same for any number of ranks as for one GPU.
 Capacity limits (window, boundary size) are evaluated identically on every
@@ -123,6 +138,23 @@ class ShardOps:
     def unpack(self, recv_prev, recv_next):
         raise NotImplementedError
 
+    def prior(self, stage, red=None, red_mm=None):
+        """ESS-threshold frames with prior weights: stage 0 -> (max int64[1], None)
+        (MAX), 1 -> (normaliser limbs int64[3], None) (SUM), 2 -> (numerator
+        limbs int64[18] (SUM), range int64[2] (MAX)), 3 finalises (-> None)"""
+        raise NotImplementedError
+
+    def route(self, totals):
+        """multinomial: gathered totals -> requests int32[world * (1 + bcap)]"""
+        raise NotImplementedError
+
+    def serve(self, req_in):
+        """multinomial: received requests -> answers float32[world * 5 * bcap]"""
+        raise NotImplementedError
+
+    def install(self, resp_in):
+        raise NotImplementedError
+
     def flags(self):
         """-> PCS_FLAG_* of this rank (host int; synchronises)"""
         raise NotImplementedError
@@ -142,6 +174,13 @@ class DeviceShardOps(ShardOps):
     def begin(self, cfg, height, width, rank, world, n_global, wcap, bcap, seed):
         self.dev = _lib.device()
         dev = self.dev
+        res = cfg.resampling
+        self.multi = res.scheme == "multinomial"
+        self.pout = [torch.empty(n, dtype=torch.int64, device=dev) for n in (1, 3, 18)]
+        self.pmm = torch.empty(2, dtype=torch.int64, device=dev)
+        if self.multi:
+            self.req = torch.empty(world * (1 + bcap), dtype=torch.int32, device=dev)
+            self.resp = torch.zeros(world * 5 * bcap, dtype=torch.float32, device=dev)
         self.est = torch.empty((self.n_frames, 5), dtype=torch.float64, device=dev)
         self.ess = torch.empty(self.n_frames, dtype=torch.float64, device=dev)
         self.res = torch.empty(self.n_frames, dtype=torch.uint8, device=dev)
@@ -161,7 +200,8 @@ class DeviceShardOps(ShardOps):
         c.seed = seed
         c.frame0 = 0
         c.use_graph = 0
-        c.threshold_fraction = 1.0
+        c.threshold_fraction = res.threshold_fraction
+        c.scheme = 1 if self.multi else 0
         c.weighted_com = 1 if getattr(cfg, "weighted_com", False) else 0
         _lib.check(_lib.lib().pcs_shard_begin(self.ctx, ctypes.byref(c), height, width, rank,
                                               world, n_global, wcap, bcap, _lib.stream()),
@@ -197,6 +237,29 @@ class DeviceShardOps(ShardOps):
     def unpack(self, recv_prev, recv_next):
         _lib.check(_lib.lib().pcs_shard_unpack(self.ctx, _lib.ptr(recv_prev), _lib.ptr(recv_next),
                                                _lib.stream()), "pcs_shard_unpack")
+
+    def prior(self, stage, red=None, red_mm=None):
+        out = self.pout[stage] if stage < 3 else None
+        mm = self.pmm if stage == 2 else None
+        _lib.check(_lib.lib().pcs_shard_prior(
+            self.ctx, stage, None if red is None else _lib.ptr(red),
+            None if red_mm is None else _lib.ptr(red_mm), None if out is None else _lib.ptr(out),
+            None if mm is None else _lib.ptr(mm), _lib.stream()), "pcs_shard_prior")
+        return out, mm
+
+    def route(self, totals):
+        _lib.check(_lib.lib().pcs_shard_route(self.ctx, _lib.ptr(totals), _lib.ptr(self.req),
+                                              _lib.stream()), "pcs_shard_route")
+        return self.req
+
+    def serve(self, req_in):
+        _lib.check(_lib.lib().pcs_shard_serve(self.ctx, _lib.ptr(req_in), _lib.ptr(self.resp),
+                                              _lib.stream()), "pcs_shard_serve")
+        return self.resp
+
+    def install(self, resp_in):
+        _lib.check(_lib.lib().pcs_shard_install(self.ctx, _lib.ptr(resp_in), _lib.stream()),
+                   "pcs_shard_install")
 
     def flags(self):
         out = _lib.PcsTrackResult()
@@ -248,27 +311,52 @@ def _on(t, dev):
     return t if t.device == dev else t.to(dev)
 
 
+def default_bcap(n_local, world, multinomial):
+    """Exchange capacity: boundary slots per neighbour (systematic: the
+    weight-share imbalance between neighbouring ranks), or requests per rank
+    pair (multinomial: each rank's slots draw ~n_local / world ancestors from
+    every rank; 1.5x that plus a margin)."""
+    if multinomial:
+        return max(1, min(n_local, max(4096, (3 * n_local) // (2 * world) + 1024)))
+    return max(1, min(n_local, max(4096, n_local // 4)))
+
+
+def _all_reduce(t, op, dev, group):
+    c = _on(t, dev)
+    dist.all_reduce(c, op=op, group=group)
+    return _on(c, t.device)
+
+
+def _all_to_all(t, dev, group):
+    c = _on(t, dev)
+    out = torch.empty_like(c)
+    dist.all_to_all_single(out, c, group=group)
+    return _on(out, t.device)
+
+
 def sharded_pcsir_track(frames, cfg, seed, ops, group=None, wcap=1 << 16, bcap=None,
                         comm_device=None):
     """Run pcSIR over the ranks of ``group``; every rank returns the same
-    (estimates, ess, resampled, likelihood_evals).
+    (estimates, ess, resampled, likelihood_evals), equal to the one-GPU
+    filter's for any ResampleConfig (ESS threshold, systematic or
+    multinomial).
 
     ``frames``: (K,H,W) float32 tensor on the rank's device (the frames are
     replicated: every rank evaluates the same occupied cells). ``cfg`` is a
     PcFilterConfig with the GLOBAL n_particles (divisible by the world size).
     ``wcap``: cells of the limb window; ``bcap``: boundary slots exchanged
-    with each neighbour per frame (default n_local / 4)."""
+    with each neighbour per frame (systematic) or requests per rank pair
+    (multinomial); default ``default_bcap``."""
     r_cfg = cfg.resampling
-    if r_cfg.threshold_fraction != 1.0 or r_cfg.scheme != "systematic":
-        raise ValueError("the sharded filter resamples every frame (systematic, "
-                         "threshold_fraction=1.0); use pcsir_track on one GPU otherwise")
+    cond = r_cfg.threshold_fraction < 1.0
+    multi = r_cfg.scheme == "multinomial"
     p = dist.get_world_size(group)
     r = dist.get_rank(group)
     n_global = cfg.n_particles
     if n_global % p:
         raise ValueError("n_particles must be divisible by the number of ranks")
     n_local = n_global // p
-    bcap = int(bcap) if bcap else max(1, min(n_local, max(4096, n_local // 4)))
+    bcap = int(bcap) if bcap else default_bcap(n_local, p, multi)
     from dataclasses import replace
     local_cfg = replace(cfg, n_particles=n_local)
     k_frames, h, w = frames.shape
@@ -276,22 +364,27 @@ def sharded_pcsir_track(frames, cfg, seed, ops, group=None, wcap=1 << 16, bcap=N
     dev = comm_device if comm_device is not None else (
         torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl"
         else torch.device("cpu"))
+    MAX, SUM = dist.ReduceOp.MAX, dist.ReduceOp.SUM
     for k in range(k_frames):
-        box = ops.step1(frames[k], k)
-        bc = _on(box, dev)
-        dist.all_reduce(bc, op=dist.ReduceOp.MAX, group=group)
-        box = _on(bc, box.device)
-        limbs = ops.export(box)
-        lc = _on(limbs, dev)
-        dist.all_reduce(lc, op=dist.ReduceOp.SUM, group=group)
-        ops.import_bins(box, _on(lc, limbs.device))
+        box = _all_reduce(ops.step1(frames[k], k), MAX, dev, group)
+        limbs = _all_reduce(ops.export(box), SUM, dev, group)
+        ops.import_bins(box, limbs)
+        if cond:   # frames whose particles carry prior weights finish per particle
+            mx, _ = ops.prior(0)
+            s3, _ = ops.prior(1, _all_reduce(mx, MAX, dev, group))
+            st, mm = ops.prior(2, _all_reduce(s3, SUM, dev, group))
+            ops.prior(3, _all_reduce(st, SUM, dev, group), _all_reduce(mm, MAX, dev, group))
         tot = ops.total()
         parts = [torch.empty_like(_on(tot, dev)) for _ in range(p)]
         dist.all_gather(parts, _on(tot, dev), group=group)
         totals = _on(torch.cat(parts), tot.device)
-        send_prev, send_next = ops.emit(totals)
-        rp, rn = _exchange(_on(send_prev, dev), _on(send_next, dev), r, p, group)
-        ops.unpack(_on(rp, send_prev.device), _on(rn, send_next.device))
+        if multi:
+            req_in = _all_to_all(ops.route(totals), dev, group)
+            ops.install(_all_to_all(ops.serve(req_in), dev, group))
+        else:
+            send_prev, send_next = ops.emit(totals)
+            rp, rn = _exchange(_on(send_prev, dev), _on(send_next, dev), r, p, group)
+            ops.unpack(_on(rp, send_prev.device), _on(rn, send_next.device))
     flags, first_bad = ops.flags()
     ft = torch.tensor([flags, -first_bad if first_bad >= 0 else -(1 << 40)], dtype=torch.int64,
                       device=dev)

@@ -33,6 +33,30 @@ def _round_fixed64(x, F):
     return int(round(math.ldexp(x, F)))
 
 
+def _limbs(v):
+    """three 42-bit limbs (the top one signed) of an exact integer"""
+    return [v & M42, (v >> 42) & M42, v >> 84]
+
+
+def _unlimbs(L):
+    return int(L[0]) + (int(L[1]) << 42) + (int(L[2]) << 84)
+
+
+def _ordered(x):
+    """order-preserving int64 of a float64 (MAX-reducible)"""
+    b = int(np.array([x], dtype=np.float64).view(np.int64)[0])
+    return b if b >= 0 else b ^ 0x7FFFFFFFFFFFFFFF
+
+
+def _unordered(b):
+    b = b if b >= 0 else b ^ 0x7FFFFFFFFFFFFFFF
+    return float(np.array([b], dtype=np.int64).view(np.float64)[0])
+
+
+def _bits(w32):
+    return int(np.array([w32], dtype=np.float32).view(np.uint32)[0])
+
+
 class CpuShardOps(D.ShardOps):
     """CPU mirror of DeviceShardOps (pcs_shard.cuh): same buffers (box,
     fixed-size limbs, 42-bit total limbs, boundary buffers with the count in
@@ -45,6 +69,11 @@ class CpuShardOps(D.ShardOps):
 
     def begin(self, cfg, height, width, rank, world, n_global, wcap, bcap, seed):
         self.cfg = cfg
+        self.thresh = cfg.resampling.threshold_fraction * n_global
+        self.multi = cfg.resampling.scheme == "multinomial"
+        self.extra = world * bcap if self.multi else 2 * bcap
+        self.prior_next = False   # the next frame's particles carry prior weights
+        self.wprev = None
         self.n = cfg.n_particles
         self.rank, self.world = rank, world
         self.idx_off = rank * self.n
@@ -56,7 +85,7 @@ class CpuShardOps(D.ShardOps):
         self.grid = (g.origin_x, g.origin_y, g.cell_width, g.cell_height, g.n_cols, g.n_rows)
         c = cfg.init.center.as_array()
         z = orc.init_normals(seed, self.n, offset=self.idx_off)
-        s = np.zeros((5, self.n + 2 * bcap), dtype=np.float64)
+        s = np.zeros((5, self.n + self.extra), dtype=np.float64)
         s[:, :self.n] = np.tile(c, (self.n, 1)).T
         s[0, :self.n] = c[0] + cfg.init.sigma * z[0]
         s[1, :self.n] = c[1] + cfg.init.sigma * z[1]
@@ -70,6 +99,7 @@ class CpuShardOps(D.ShardOps):
 
     def step1(self, frame, k):
         self.k = k
+        self.pc_prior = self.prior_next
         d = self.cfg.dynamics
         src = np.ascontiguousarray(self.soa[:, self.anc])
         z = orc.propagate_normals(self.seed, k, self.n, offset=self.idx_off).astype(np.float32)
@@ -117,7 +147,7 @@ class CpuShardOps(D.ShardOps):
     def import_bins(self, box, limbs):
         x0, y0, nx, ny, ok = self._window(box)
         if not ok:
-            self.do_res = False
+            self.do_res = self.pc_prior = self.prior_next = False
             return
         ncol = self.grid[4]
         L = limbs.numpy().reshape(self.wcap, D.LIMBS)[: nx * ny]
@@ -137,6 +167,10 @@ class CpuShardOps(D.ShardOps):
                 dummies[c, b] = np.float32(math.ldexp(float(sums[c]) / cnt, -40))
         dd = dummies.astype(np.float64)
         ll = orc.loglik_gauss(pix, dd[0], dd[1], dd[4], sp, bg, hw, sxi)
+        self.occ[self.k] = len(fl)
+        if self.pc_prior:   # finished per particle (prior)
+            self.cell_ll = {f: float(ll[b]) for b, f in enumerate(fl)}
+            return
         m = ll.max()
         S = sum(cells[f][0] * _round_fixed64(math.exp(ll[b] - m), 95) for b, f in enumerate(fl))
         Sf = math.ldexp(float(S), -95)
@@ -151,17 +185,61 @@ class CpuShardOps(D.ShardOps):
                 est[c] += wq * cells[f][1][c]
             w2 += cells[f][0] * _round_fixed64(float(w) * float(w), 120)
         k = self.k
+        ws = [_bits(w) for w in self.wmap.values()]
+        self._decide(est, w2, min(ws) != max(ws))
+        self.w = np.array([self.wmap[f] for f in self.flat.tolist()], dtype=np.float32)
+
+    def _decide(self, est, w2, unequal):
+        k = self.k
         self.est[k] = [math.ldexp(float(v), -102) for v in est]
         self.ess[k] = 1.0 / math.ldexp(float(w2), -120)
-        self.do_res = self.ess[k] < self.n_global
+        self.do_res = self.ess[k] < self.thresh
         self.res[k] = self.do_res
-        self.occ[k] = len(fl)
+        self.prior_next = (not self.do_res) and unequal
+        self.u = orc.resample_u(self.seed, k)
+
+    def prior(self, stage, red=None, red_mm=None):
+        """per-particle finish of a frame with prior weights (neutral values otherwise)"""
+        on = self.pc_prior
+        if stage == 0:
+            v = -(1 << 63)
+            if on:
+                self.pll = np.log(self.wprev.astype(np.float64)) + np.array(
+                    [self.cell_ll[f] for f in self.flat.tolist()])
+                v = _ordered(float(self.pll.max()))
+            return torch.tensor([v], dtype=torch.int64), None
+        if stage == 1:
+            S = 0
+            if on:
+                m = _unordered(int(red[0]))
+                self.ex = np.exp(self.pll - m)
+                S = sum(_round_fixed64(float(e), 95) for e in self.ex)
+            return torch.tensor(_limbs(S), dtype=torch.int64), None
+        if stage == 2:
+            out = [0] * 18
+            mm = [-0xFFFFFFFF, 0]
+            if on:
+                Sf = math.ldexp(float(_unlimbs(red.tolist())), -95)
+                self.w = (self.ex / Sf).astype(np.float32)
+                wq = _fixed(self.w, 62)
+                fx = [_fixed(self.prop[c], 40) for c in range(5)]
+                est = [sum(a * b for a, b in zip(wq, fx[c])) for c in range(5)]
+                w2 = sum(_round_fixed64(float(w) * float(w), 120) for w in self.w)
+                out = sum((_limbs(v) for v in est + [w2]), [])
+                bits = self.w.view(np.uint32)
+                mm = [-int(bits.min()), int(bits.max())]
+            return (torch.tensor(out, dtype=torch.int64), torch.tensor(mm, dtype=torch.int64))
+        if on:
+            L = red.tolist()
+            est = [_unlimbs(L[3 * c:3 * c + 3]) for c in range(5)]
+            w2 = _unlimbs(L[15:18])
+            self._decide(est, w2, -int(red_mm[0]) != int(red_mm[1]))
+        return None, None
 
     def total(self):
         out = np.zeros(3, dtype=np.int64)
         if self.do_res:
-            w = np.array([self.wmap[f] for f in self.flat.tolist()], dtype=np.float32)
-            wx = _fixed(w, 120)
+            wx = _fixed(self.w, 120)
             self.incl = np.cumsum(np.array(wx, dtype=object))
             t = int(self.incl[-1])
             out[:] = [t & M42, (t >> 42) & M42, t >> 84]
@@ -178,13 +256,12 @@ class CpuShardOps(D.ShardOps):
         bufs = self._buffers()
         n, r, p, ng, bcap = self.n, self.rank, self.world, self.n_global, self.bcap
         if not self.do_res or self.flag & 4:
-            self.anc = np.arange(n)
+            self._identity()
             self.recv_counts = (0, 0)
-            self.next_soa = self._extended(self.prop)
             return torch.from_numpy(bufs[0]), torch.from_numpy(bufs[1])
         T = totals.numpy().reshape(p, 3)
         tots = [int(T[q, 0]) + (int(T[q, 1]) << 42) + (int(T[q, 2]) << 84) for q in range(p)]
-        u = orc.resample_u(self.seed, self.k)
+        u = self.u
         # every rank's range (k_shard_ranges), the same capacity checks
         lo, pre, ranges, prefixes = 0, 0, [], []
         for q in range(p):
@@ -198,9 +275,8 @@ class CpuShardOps(D.ShardOps):
             pre += tots[q]
             lo = hi
         if self.flag & 4:
-            self.anc = np.arange(n)
+            self._identity()
             self.recv_counts = (0, 0)
-            self.next_soa = self._extended(self.prop)
             return torch.from_numpy(bufs[0]), torch.from_numpy(bufs[1])
         lo_r, hi_r = ranges[r]
         # ancestors of slots [lo_r, hi_r) from this rank's exact prefixes
@@ -236,9 +312,81 @@ class CpuShardOps(D.ShardOps):
         return torch.from_numpy(bufs[0]), torch.from_numpy(bufs[1])
 
     def _extended(self, prop):
-        s = np.zeros((5, self.n + 2 * self.bcap), dtype=np.float32)
+        s = np.zeros((5, self.n + self.extra), dtype=np.float32)
         s[:, :self.n] = prop
         return s
+
+    def _identity(self):
+        """no resampling: identity ancestors; unequal weights go to the next frame"""
+        self.anc = np.arange(self.n)
+        self.next_soa = self._extended(self.prop)
+        if self.prior_next and not self.flag & 4:
+            self.wprev = self.w.copy()
+
+    # ---- multinomial ----
+    def _points(self):
+        return orc.multinomial_points(self.seed, self.k, self.n_global)
+
+    def route(self, totals):
+        n, r, p, bcap = self.n, self.rank, self.world, self.bcap
+        req = np.zeros((p, 1 + bcap), dtype=np.int32)
+        self.sent = [0] * p
+        if not self.do_res or self.flag & 4:
+            self._identity()
+            return torch.from_numpy(req.reshape(-1))
+        T = totals.numpy().reshape(p, 3)
+        tots = [_unlimbs(T[q]) for q in range(p)]
+        pre = [0]
+        for q in range(p):
+            pre.append(pre[-1] + tots[q])
+        bnd = [D.cdf_value(pre[q]) for q in range(p)]
+        wx = _fixed(self.w, 120)
+        cdf, run = [], pre[r]
+        for i in range(n):
+            run += wx[i]
+            cdf.append(1.0 if self.idx_off + i == self.n_global - 1 else D.cdf_value(run))
+        self.cdf = np.array(cdf)
+        pts = self._points()[self.idx_off:self.idx_off + n]
+        anc = np.empty(n, dtype=np.int64)
+        for jl in range(n):
+            q = sum(1 for b in range(1, p) if bnd[b] <= pts[jl])
+            if q == r:
+                anc[jl] = min(int(np.searchsorted(self.cdf, pts[jl], side="right")), n - 1)
+            elif self.sent[q] < bcap:
+                req[q, 1 + self.sent[q]] = jl
+                anc[jl] = n + q * bcap + self.sent[q]
+                self.sent[q] += 1
+            else:
+                self.flag |= 4
+        req[:, 0] = self.sent
+        self.anc = anc
+        self.next_soa = self._extended(self.prop)
+        return torch.from_numpy(req.reshape(-1))
+
+    def serve(self, req_in):
+        n, r, p, bcap = self.n, self.rank, self.world, self.bcap
+        resp = np.zeros((p, 5, bcap), dtype=np.float32)
+        if self.do_res and not self.flag & 4:
+            R = req_in.numpy().reshape(p, 1 + bcap)
+            pts = self._points()
+            for q in range(p):
+                if q == r:
+                    continue
+                for s_ in range(int(R[q, 0])):
+                    i = min(int(np.searchsorted(self.cdf, pts[q * n + int(R[q, 1 + s_])],
+                                                side="right")), n - 1)
+                    resp[q, :, s_] = self.prop[:, i]
+        return torch.from_numpy(resp.reshape(-1))
+
+    def install(self, resp_in):
+        n, r, p, bcap = self.n, self.rank, self.world, self.bcap
+        if self.do_res and not self.flag & 4:
+            R = resp_in.numpy().reshape(p, 5, bcap)
+            for q in range(p):
+                if q != r:
+                    c = self.sent[q]
+                    self.next_soa[:, n + q * bcap:n + q * bcap + c] = R[q, :, :c]
+        self.soa = self.next_soa
 
     def unpack(self, recv_prev, recv_next):
         n, bcap = self.n, self.bcap

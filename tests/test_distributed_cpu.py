@@ -38,7 +38,7 @@ def _scene(k=5, width=48, seed=0):
     return np.stack(frames)
 
 
-def _run(rank, world, port, n, cpp, out_dir, bcap=None):
+def _run(rank, world, port, n, cpp, out_dir, bcap=None, res=(1.0, "systematic")):
     sys.path.insert(0, str(ROOT))
     sys.path.insert(0, str(ROOT / "tests"))
     os.environ["MASTER_ADDR"] = "127.0.0.1"
@@ -51,7 +51,7 @@ def _run(rank, world, port, n, cpp, out_dir, bcap=None):
     frames = _scene()
     cfg = pc.PcFilterConfig(n, pc.InitSpec(pc.StateVector(20.0, 24.0, 0.5, 0.0, 20.0), "gauss",
                                            sigma=2.0),
-                            pc.DynamicsParams(0.5, 0.1, 1.0), pc.ResampleConfig(1.0, "systematic"),
+                            pc.DynamicsParams(0.5, 0.1, 1.0), pc.ResampleConfig(*res),
                             likelihood=object(), grid=pc.BinGrid.pixel_aligned(48, 48, cpp))
     ops = CpuShardOps(len(frames), frames)
     try:
@@ -83,6 +83,29 @@ def test_ranks_equal_one_rank(tmp_path, cpp):
         assert np.array_equal(a["res"], b["res"])
         assert int(a["evals"]) == int(b["evals"])
     assert a["res"].all()
+    truth_x = 20.0 + 0.5 * np.arange(1, 6)
+    assert np.max(np.abs(a["est"][:, 0] - truth_x)) < 1.0
+
+
+@pytest.mark.parametrize("frac,scheme,cpp", [(0.5, "systematic", 1), (1.0, "multinomial", 2),
+                                              (0.5, "multinomial", 1)])
+def test_ranks_equal_one_rank_threshold_multinomial(tmp_path, frac, scheme, cpp):
+    """ESS-threshold frames (prior weights finished per particle through the
+    MAX / SUM all-reduces) and multinomial resampling (requests and states
+    through the two all-to-alls): P = 2 and P = 4 reproduce P = 1 bit for bit."""
+    n = 1200
+    for world in (1, 2, 4):
+        mp.spawn(_run, args=(world, _free_port(), n, cpp, str(tmp_path), None, (frac, scheme)),
+                 nprocs=world, join=True)
+    a = np.load(tmp_path / "w1.npz")
+    if frac < 1.0:
+        assert 0 < int(a["res"].sum()) < len(a["res"])   # both kinds of frames occur
+    for world in (2, 4):
+        b = np.load(tmp_path / f"w{world}.npz")
+        assert np.array_equal(a["est"], b["est"])
+        assert np.array_equal(a["ess"], b["ess"])
+        assert np.array_equal(a["res"], b["res"])
+        assert int(a["evals"]) == int(b["evals"])
     truth_x = 20.0 + 0.5 * np.arange(1, 6)
     assert np.max(np.abs(a["est"][:, 0] - truth_x)) < 1.0
 
@@ -126,14 +149,3 @@ def test_first_slot_matches_points():
         j = D.first_slot(float(c), u, n)
         assert j == int(np.searchsorted(pts, c, side="left"))
 
-
-def test_sharded_filter_rejects_other_resampling():
-    import paper_1310_5541_b200 as pc
-    from paper_1310_5541_b200 import distributed as D
-    init = pc.InitSpec(pc.StateVector(8, 8, 0, 0, 20.0), "gauss", sigma=2.0)
-    lik = pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(10.0, 5))
-    for res in (pc.ResampleConfig(0.5, "systematic"), pc.ResampleConfig(1.0, "multinomial")):
-        cfg = pc.PcFilterConfig(64, init, pc.DynamicsParams(0.5, 0.1, 1.0), res, lik,
-                                grid=pc.BinGrid.pixel_aligned(16, 16, 1))
-        with pytest.raises(ValueError, match="resamples every frame"):
-            D.sharded_pcsir_track(torch.zeros((1, 16, 16)), cfg, 0, ops=None)

@@ -35,8 +35,10 @@ def group(cuda):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("cpp,n", [(1, 20000), (4, 50000)])
-def test_sharded_world1_equals_fused(group, cpp, n):
+@pytest.mark.parametrize("cpp,n,res", [(1, 20000, (1.0, "systematic")), (4, 50000, (1.0, "systematic")),
+                                       (1, 20000, (0.5, "systematic")),
+                                       (2, 20000, (0.25, "multinomial"))])
+def test_sharded_world1_equals_fused(group, cpp, n, res):
     rng = np.random.default_rng(5)
     width, k = 96, 8
     xs = np.arange(width)
@@ -52,12 +54,14 @@ def test_sharded_world1_equals_fused(group, cpp, n):
     grid = pc.BinGrid.pixel_aligned(width, width, cpp)
 
     def cfg():
-        return pc.PcFilterConfig(n, init, dyn, pc.ResampleConfig(1.0, "systematic"),
+        return pc.PcFilterConfig(n, init, dyn, pc.ResampleConfig(*res),
                                  pc.SpotLikelihood(pc.PsfParams(1.5, 10.0),
                                                    pc.LikelihoodParams(10.0, 5)), grid=grid)
 
     fused = pc.pcsir_track([pc.ImageFrame(f) for f in frames], cfg(), pc.PhiloxRng(77))
     assert fused.path == "fused"
+    if res[0] < 1.0:
+        assert 0 < int(fused.resampled.sum()) < k   # both kinds of frames occur
     ops = D.DeviceShardOps(k)
     est, ess, res, evals = D.sharded_pcsir_track(torch.from_numpy(frames).cuda(), cfg(), 77, ops,
                                                  group=group)
@@ -78,7 +82,9 @@ def _emulated_ranks(frames, cfg, seed, world, wcap=1 << 14, bcap=None):
     from paper_1310_5541_b200 import _lib
     n_global = cfg.n_particles
     n = n_global // world
-    bcap = bcap or max(1, n // 4)
+    multi = cfg.resampling.scheme == "multinomial"
+    cond = cfg.resampling.threshold_fraction < 1.0
+    bcap = bcap or D.default_bcap(n, world, multi)
     k_frames, h, w = frames.shape
     ops = [D.DeviceShardOps(k_frames, _lib.new_ctx()) for _ in range(world)]
     for r, o in enumerate(ops):
@@ -89,7 +95,22 @@ def _emulated_ranks(frames, cfg, seed, world, wcap=1 << 14, bcap=None):
         limbs = torch.stack([o.export(box).clone() for o in ops]).sum(dim=0)
         for o in ops:
             o.import_bins(box, limbs)
+        if cond:
+            mx = torch.stack([o.prior(0)[0].clone() for o in ops]).max(dim=0).values
+            s3 = torch.stack([o.prior(1, mx)[0].clone() for o in ops]).sum(dim=0)
+            outs = [tuple(t.clone() for t in o.prior(2, s3)) for o in ops]
+            st = torch.stack([a for a, _ in outs]).sum(dim=0)
+            mm = torch.stack([b for _, b in outs]).max(dim=0).values
+            for o in ops:
+                o.prior(3, st, mm)
         totals = torch.cat([o.total().clone() for o in ops])
+        if multi:   # all-to-all: chunk q of rank r's buffer goes to rank q
+            reqs = [o.route(totals).clone().view(world, -1) for o in ops]
+            resps = [o.serve(torch.stack([reqs[q][r] for q in range(world)]).reshape(-1)).clone()
+                     .view(world, -1) for r, o in enumerate(ops)]
+            for r, o in enumerate(ops):
+                o.install(torch.stack([resps[q][r] for q in range(world)]).reshape(-1))
+            continue
         sends = [tuple(t.clone() for t in o.emit(totals)) for o in ops]
         for r, o in enumerate(ops):
             rp = sends[r - 1][1] if r > 0 else torch.zeros_like(sends[r][0])
@@ -101,8 +122,10 @@ def _emulated_ranks(frames, cfg, seed, world, wcap=1 << 14, bcap=None):
 
 
 @pytest.mark.parametrize("world", [2, 4])
-@pytest.mark.parametrize("cpp", [1, 4])
-def test_sharded_device_kernels_multi_rank_equal_fused(cuda, world, cpp):
+@pytest.mark.parametrize("cpp,res", [(1, (1.0, "systematic")), (4, (1.0, "systematic")),
+                                     (1, (0.5, "systematic")), (4, (0.3, "systematic")),
+                                     (2, (1.0, "multinomial")), (4, (0.25, "multinomial"))])
+def test_sharded_device_kernels_multi_rank_equal_fused(cuda, world, cpp, res):
     rng = np.random.default_rng(7)
     width, k, n = 96, 8, 40000
     xs = np.arange(width)
@@ -118,11 +141,14 @@ def test_sharded_device_kernels_multi_rank_equal_fused(cuda, world, cpp):
     grid = pc.BinGrid.pixel_aligned(width, width, cpp)
 
     def cfg():
-        return pc.PcFilterConfig(n, init, dyn, pc.ResampleConfig(1.0, "systematic"),
+        return pc.PcFilterConfig(n, init, dyn, pc.ResampleConfig(*res),
                                  pc.SpotLikelihood(pc.PsfParams(1.5, 10.0),
                                                    pc.LikelihoodParams(10.0, 5)), grid=grid)
 
     fused = pc.pcsir_track([pc.ImageFrame(f) for f in frames], cfg(), pc.PhiloxRng(77))
+    assert fused.path == "fused"
+    if res[0] < 1.0:
+        assert 0 < int(fused.resampled.sum()) < k   # both kinds of frames occur
     flags, outs = _emulated_ranks(torch.from_numpy(frames).cuda(), cfg(), 77, world)
     assert flags == [0] * world
     for est, ess, res, occ in outs:   # every rank holds the same results
