@@ -1042,7 +1042,7 @@ static int track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int6
     if (!ctx->tab_cnt) {
       // keys, counts, then the float / exact cdf weights per slot
       PCS_CUDA_TRY(cudaMalloc(&ctx->tab_cnt, 2 * (size_t)HT_CAP * sizeof(u32)));
-      PCS_CUDA_TRY(cudaMalloc(&ctx->tab_sum, 5 * (size_t)HT_CAP * 2 * sizeof(u64)));
+      PCS_CUDA_TRY(cudaMalloc(&ctx->tab_sum, 5 * (size_t)HT_CAP * (2 + TAB_LIMBS) * sizeof(u64)));
       PCS_CUDA_TRY(cudaMalloc(&ctx->wtab, (size_t)HT_CAP * (sizeof(float) + sizeof(u128))));
       ctx->table_cells = HT_CAP;
       ctx->table_dirty = true;
@@ -1052,7 +1052,7 @@ static int track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int6
     if (ctx->table_dirty) {
       PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_cnt, 0, (size_t)HT_CAP * sizeof(u32), st));
       PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_cnt + HT_CAP, 0xFF, (size_t)HT_CAP * sizeof(u32), st));
-      PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_sum, 0, 5 * (size_t)HT_CAP * 2 * sizeof(u64), st));
+      PCS_CUDA_TRY(cudaMemsetAsync(ctx->tab_sum, 0, 5 * (size_t)HT_CAP * (2 + TAB_LIMBS) * sizeof(u64), st));
       ctx->table_dirty = false;
     }
     // compact per-frame tables of the step-1 sub-window cells (pslot codes < SUBW)
@@ -1062,6 +1062,7 @@ static int track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int6
     P.tab_cnt = ctx->tab_cnt;
     P.hkey = ctx->tab_cnt + HT_CAP;
     P.tab_sum = ctx->tab_sum;
+    P.tab_lim = ctx->tab_sum + 5 * (size_t)HT_CAP * 2;
     P.wfix = (u128*)ctx->wtab;
     P.wtab = (float*)(P.wfix + HT_CAP);
     P.occ = ctx->occ;

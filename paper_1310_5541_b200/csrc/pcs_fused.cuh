@@ -145,7 +145,8 @@ struct TrackParams {
   u32* pslot;                // pcSIR: cell code per particle (pslot_code below)
   u32* hkey;                 // [G] flat cell id of each table slot (HT_EMPTY: free)
   u32* tab_cnt;              // [G]   members per slot
-  u64* tab_sum;              // [5][G][2]
+  u64* tab_sum;              // [5][G][2] exact int128 sums (step-1 flushes, shard import)
+  u64* tab_lim;              // [5][G][3] limb sums (step-1 single particles, tab_add)
   float* wtab;               // [G]
   u128* wfix;                // [G] exact cdf weight round(wtab * 2^120) (k_sys_resample)
   u32* occ;                  // [MAXM]
@@ -346,18 +347,24 @@ __device__ __forceinline__ float cell_ref32(double origin, double cell, i64 i, b
 // table is full): Fibonacci hash, linear probing; keys only go from empty to
 // a cell id within a frame (the bins kernel clears the occupied slots)
 __device__ __forceinline__ u32 ht_hash(u32 flat) { return (flat * 0x9E3779B1u) >> (32 - HT_BITS); }
-__device__ __forceinline__ u32 ht_insert(const TrackParams& P, u32 flat) {
+__device__ __forceinline__ u32 ht_insert(const TrackParams& P, u32 flat, bool& created) {
+  created = false;
   u32 s = ht_hash(flat);
   for (u32 probe = 0; probe < HT_CAP; ++probe) {
     const u32 k = __ldcg(P.hkey + s);
     if (k == flat) return s;
     if (k == HT_EMPTY) {
       const u32 old = atomicCAS(P.hkey + s, HT_EMPTY, flat);
+      created = (old == HT_EMPTY);
       if (old == HT_EMPTY || old == flat) return s;
     }
     s = (s + 1) & (HT_CAP - 1);
   }
   return HT_EMPTY;
+}
+__device__ __forceinline__ u32 ht_insert(const TrackParams& P, u32 flat) {
+  bool created;
+  return ht_insert(P, flat, created);
 }
 __device__ __forceinline__ u32 ht_find(const TrackParams& P, u32 flat) {
   u32 s = ht_hash(flat);
@@ -372,9 +379,59 @@ __device__ __forceinline__ u32 ht_find(const TrackParams& P, u32 flat) {
 
 // add cnt members to table slot `slot`; the first touch appends the slot to
 // the frame's occupied list
-__device__ __forceinline__ void touch_cell(const TrackParams& P, TrackCtl* C, u32 slot, u32 cnt) {
-  u32 old = atomicAdd(P.tab_cnt + slot, cnt);
-  if (old == 0) {
+// A cell's exact sum of component c is tab_sum (int128, added with a carry
+// chain by the step-1 flushes: few, large additions) plus tab_lim: three
+// 64-bit limbs (bits 0-31 and 32-63 unsigned, the rest signed) that single
+// particles outside the sub-window add with fire-and-forget reductions (RED,
+// no return value), so a warp never waits on an L2 round trip per particle.
+// A limb gains < 2^32 per addition and a cell gets < 2^32 additions per
+// frame (n < 2^31), so none wraps.
+constexpr int TAB_LIMBS = 3;
+__device__ __forceinline__ u64* tab_ptr(const TrackParams& P, int c, u32 slot) {
+  return P.tab_lim + ((i64)c * P.G + slot) * TAB_LIMBS;
+}
+__device__ __forceinline__ void tab_add(u64* p, i128 v) {
+  const u128 u = (u128)v;
+  const u64 l0 = (u64)u & 0xFFFFFFFFull, l1 = (u64)(u >> 32) & 0xFFFFFFFFull;
+  const u64 l2 = (u64)(long long)(v >> 64);   // arithmetic shift: the signed rest
+  if (l0) atomicAdd((unsigned long long*)p, l0);
+  if (l1) atomicAdd((unsigned long long*)p + 1, l1);
+  if (l2) atomicAdd((unsigned long long*)p + 2, l2);
+}
+__device__ __forceinline__ void tab_add_x5(const TrackParams& P, u32 slot, const i128 (&v)[5]) {
+#pragma unroll
+  for (int c = 0; c < 5; ++c) tab_add(tab_ptr(P, c, slot), v[c]);
+}
+__device__ __forceinline__ u64* tab_i128(const TrackParams& P, int c, u32 slot) {
+  return P.tab_sum + ((i64)c * P.G + slot) * 2;
+}
+__device__ __forceinline__ i128 tab_load(const TrackParams& P, int c, u32 slot) {
+  const u64* p = tab_ptr(P, c, slot);
+  return load_i128(tab_i128(P, c, slot)) + (i128)p[0] + ((i128)p[1] << 32) +
+         ((i128)(long long)p[2] << 64);
+}
+__device__ __forceinline__ void tab_zero(const TrackParams& P, int c, u32 slot) {
+  u64* p = tab_ptr(P, c, slot);
+  p[0] = 0;
+  p[1] = 0;
+  p[2] = 0;
+  u64* q = tab_i128(P, c, slot);
+  q[0] = 0;
+  q[1] = 0;
+}
+// (the limbs of a stored cell are zero: its previous content was consumed)
+__device__ __forceinline__ void tab_store(const TrackParams& P, int c, u32 slot, i128 v) {
+  u64* q = tab_i128(P, c, slot);
+  q[0] = (u64)v;
+  q[1] = (u64)((u128)v >> 64);
+}
+
+// add cnt members to table slot `slot` (fire-and-forget); the thread whose
+// ht_insert created the key appends the slot to the frame's occupied list
+__device__ __forceinline__ void touch_cell(const TrackParams& P, TrackCtl* C, u32 slot, u32 cnt,
+                                           bool created) {
+  atomicAdd(P.tab_cnt + slot, cnt);
+  if (created) {
     u32 idx = atomicAdd(&C->n_occ, 1u);
     if (idx < (u32)MAXM) P.occ[idx] = slot;
   }
@@ -510,10 +567,11 @@ __device__ __forceinline__ void s1_flush(const TrackParams& P, TrackCtl* C, S1Sm
     }
     s[0] += (i128)cnt * f32_to_fixed(sm.ref[qx], FX_STATE);
     s[1] += (i128)cnt * f32_to_fixed(sm.ref[snx + qy], FX_STATE);
-    const u32 slot = ht_insert(P, flat);
+    bool created;
+    const u32 slot = ht_insert(P, flat, created);
     if (slot != HT_EMPTY) {
       atomic_add_i128_x5(P.tab_sum + (i64)slot * 2, P.G * 2, s);
-      touch_cell(P, C, slot, cnt);
+      touch_cell(P, C, slot, cnt, created);
     } else {
       set_flag(C, PCS_FLAG_CAPACITY);
     }
@@ -522,8 +580,27 @@ __device__ __forceinline__ void s1_flush(const TrackParams& P, TrackCtl* C, S1Sm
 }
 
 template <bool POW2>
+// PCS_S1_PROBE: clock64 split of CTA 0 thread 0 over the tile phases into
+// dbg[10..14] (p1, p2, p3, p4 run sums, flush) and the loop total in dbg[15]
+// (diagnostic builds only, tools/s1_probe.py)
+#ifdef PCS_S1_PROBE
+#define S1_MARK(i)                                                                    \
+  do {                                                                                \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                        \
+      const long long _c = clock64();                                                 \
+      if ((i) >= 0) s1_acc[i] += _c - s1_t;                                           \
+      s1_t = _c;                                                                      \
+    }                                                                                 \
+  } while (0)
+#else
+#define S1_MARK(i) do {} while (0)
+#endif
+
 __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackParams P) {
   extern __shared__ __align__(16) unsigned char s1_raw[];
+#ifdef PCS_S1_PROBE
+  long long s1_acc[5] = {0, 0, 0, 0, 0}, s1_t = 0, s1_t0 = clock64();
+#endif
   S1Smem& sm = *reinterpret_cast<S1Smem*>(s1_raw);
   TrackCtl* C = P.ctl;
   pdl_trigger();
@@ -590,6 +667,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
   int since = 0;
   // first tile static, then dynamic tickets: CTAs on slower SMs (die / HBM
   // distance) take fewer tiles instead of finishing last
+  S1_MARK(-1);
   for (i64 tile = blockIdx.x; tile < ntile;) {
     // ---- phase 1: gather + propagate + cell; rank within the tile's cell ----
     int q_k[S1_IPT], r_k[S1_IPT];
@@ -664,17 +742,19 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
         i128 v[5];
 #pragma unroll
         for (int c = 0; c < 5; ++c) v[c] = f32_to_fixed(o[c], FX_STATE);
-        const u32 slot = ht_insert(P, flat);
+        bool created;
+        const u32 slot = ht_insert(P, flat, created);
         if (!inwin) P.pslot[j] = (u32)SUBW + slot;   // cell code of an outside cell
         if (slot != HT_EMPTY) {
-          atomic_add_i128_x5(P.tab_sum + (i64)slot * 2, P.G * 2, v);
-          touch_cell(P, C, slot, 1u);
+          tab_add_x5(P, slot, v);
+          touch_cell(P, C, slot, 1u, created);
         } else {
           set_flag(C, PCS_FLAG_CAPACITY);
         }
       }
     }
     __syncthreads();
+    S1_MARK(0);
     if (t == 0) sm.next_tile = tstep + (long long)atomicAdd(&C->s1_ticket, 1u);
     // ---- phase 2: run offsets (exclusive scan of the tile's cell counts) ----
     {
@@ -712,6 +792,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
       if (t == S1_THREADS - 1) sm.n_in = (u32)run;
     }
     __syncthreads();
+    S1_MARK(1);
     // ---- phase 3: scatter the in-window particles into cell-sorted order ----
     // (the next tile is known since phase 2: pull its ancestor indices into L2
     // now, so its gather starts with an L2 hit instead of a DRAM round trip)
@@ -733,11 +814,13 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
       sm.pay_q[idx] = (unsigned short)q_k[it];
     }
     __syncthreads();
+    S1_MARK(2);
     const i64 next_tile = sm.next_tile;   // (written before the phase-2 barriers)
     // ---- phase 4: exact run sums over the sorted tile (8 warps, 4
     //      consecutive particles per lane, warp-segmented scan across lanes) ----
     if (t < S1_SUM_THREADS)
       tile_run_sums<S1_SUM_THREADS, S1_E, S1_TILE, SUBW>(pay, sm.pay_q, (int)sm.n_in, &sm.dig[0][0], t);
+    S1_MARK(3);
     // no barrier here: the other warps start the next tile's gathers while the
     // summing warps finish (phase 1 touches none of pay / pay_q / n_in, and
     // the next pay write is two barriers away)
@@ -749,9 +832,16 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
       __syncthreads();
       if (t == 0) sm.n_flist = 0;
       __syncthreads();
+      S1_MARK(4);
     }
     tile = next_tile;
   }
+#ifdef PCS_S1_PROBE
+  if (blockIdx.x == 0 && t == 0) {
+    for (int i = 0; i < 5; ++i) C->dbg[10 + i] = s1_acc[i];
+    C->dbg[15] = clock64() - s1_t0;
+  }
+#endif
   __syncthreads();
   if (t == 0 && atomicAdd(&C->s1_done, 1u) == gridDim.x - 1) {   // every ticket is drawn
     C->s1_ticket = 0;
@@ -845,11 +935,26 @@ __global__ void __launch_bounds__(CELLS_BLOCK) k_pc_cells(TrackParams P, BinsScr
     // of mass with the general path's uniform prior weight w0 = RN32(1/N):
     // RN32(RN64(RN64(wq S) / RN64(wq count)) 2^-40), wq = round(w0 2^62)
     const double den = P.weighted ? i128_to_f64_rn((i128)wq0 * (i128)cnt) : (double)cnt;
+    // fold the cell's limb sums into its int128 sums (lane c: component c), so
+    // the bins kernel reads one exact sum per component
+    i128 Sc = 0;
+    if (lane < 5) {
+      Sc = tab_load(P, lane, cell);
+      u64* q = tab_i128(P, lane, cell);
+      q[0] = (u64)Sc;
+      q[1] = (u64)((u128)Sc >> 64);
+      u64* l = tab_ptr(P, lane, cell);
+      l[0] = 0;
+      l[1] = 0;
+      l[2] = 0;
+    }
     float d[3];
 #pragma unroll
     for (int q = 0; q < 3; ++q) {
       const int c = (q == 2) ? 4 : q;
-      const i128 S = load_i128(P.tab_sum + ((i64)c * P.G + cell) * 2);
+      const u64 lo = __shfl_sync(0xffffffffu, (u64)Sc, c);
+      const u64 hi = __shfl_sync(0xffffffffu, (u64)((u128)Sc >> 64), c);
+      const i128 S = (i128)(((u128)hi << 64) | (u128)lo);
       const double num = i128_to_f64_rn(P.weighted ? S * (i128)wq0 : S);
       d[q] = __double2float_rn(scalbn(__ddiv_rn(num, den), -FX_STATE));
     }
@@ -976,10 +1081,10 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
       if (qs >= 0) P.ltsub[qs] = llb;
       P.hkey[cell] = HT_EMPTY;   // (no kernel probes the table until the next frame)
 #pragma unroll
-      for (int c = 0; c < 5; ++c) {
-        u64* p = P.tab_sum + ((i64)c * P.G + cell) * 2;
-        p[0] = 0;
-        p[1] = 0;
+      for (int c = 0; c < 5; ++c) {   // (the limbs were folded by k_pc_cells)
+        u64* q = tab_i128(P, c, cell);
+        q[0] = 0;
+        q[1] = 0;
       }
       P.tab_cnt[cell] = 0;
     }
@@ -1014,7 +1119,7 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
       // the cell's state sums first: their latency overlaps the division
       i128 Ssum[5];
 #pragma unroll
-      for (int c = 0; c < 5; ++c) Ssum[c] = load_i128(P.tab_sum + ((i64)c * P.G + cell) * 2);
+      for (int c = 0; c < 5; ++c) Ssum[c] = load_i128(tab_i128(P, c, cell));   // (folded by k_pc_cells)
       const float w = __double2float_rn(__ddiv_rn(Sd.ll[b], Sf));   // normalised_weight
       P.wtab[cell] = w;
       P.wfix[cell] = cdf_fixed(w);
@@ -1030,9 +1135,9 @@ __global__ void __launch_bounds__(BINS_BLOCK) k_pc_bins(TrackParams P, BinsScrat
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
         e[c] += (i128)wq * Ssum[c];
-        u64* p = P.tab_sum + ((i64)c * P.G + cell) * 2;
-        p[0] = 0;
-        p[1] = 0;
+        u64* q = tab_i128(P, c, cell);
+        q[0] = 0;
+        q[1] = 0;
       }
       e[5] += (i128)cnt * f64_to_fixed((double)w * (double)w, FX_W2);
       P.tab_cnt[cell] = 0;
@@ -1206,6 +1311,8 @@ template <> struct RsElem<2> { typedef double T; };
 
 // globaltimer stamps of CTA 0 (dbg[10..14]: start, pass 1 done, barrier
 // entered, barrier left, prefix done) and the end of the last CTA (dbg[15])
+// (diagnostic builds only: -DPCS_RS_PROBE, tools/rs_probe_c5.py)
+#ifdef PCS_RS_PROBE
 #define RS_PROBE(i)                                                                   \
   do {                                                                                \
     if (threadIdx.x == 0 && (blockIdx.x == 0 || ((i) == 4 && blockIdx.x == gridDim.x - 1))) { \
@@ -1214,6 +1321,9 @@ template <> struct RsElem<2> { typedef double T; };
       C->dbg[(i) == 4 && blockIdx.x == gridDim.x - 1 ? 15 : 10 + (i)] = (long long)_g; \
     }                                                                                 \
   } while (0)
+#else
+#define RS_PROBE(i) do {} while (0)
+#endif
 
 template <int KIND>
 struct RsSmem {

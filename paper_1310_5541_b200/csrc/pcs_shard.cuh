@@ -106,10 +106,8 @@ __global__ void k_shard_export(TrackParams P, const i64* __restrict__ box, i64 w
     for (int c = 0; c < 5; ++c) {
       i128 v = 0;
       if (cnt) {
-        u64* p = P.tab_sum + ((i64)c * P.G + slot) * 2;
-        v = load_i128(p);
-        p[0] = 0;
-        p[1] = 0;
+        v = tab_load(P, c, slot);
+        tab_zero(P, c, slot);
       }
       L[1 + 3 * c] = (i64)((u64)v & M42);
       L[2 + 3 * c] = (i64)((u64)(v >> 42) & M42);
@@ -148,9 +146,7 @@ __global__ void k_shard_import(TrackParams P, const i64* __restrict__ box, i64 w
     P.tab_cnt[slot] = (u32)cnt;
     for (int c = 0; c < 5; ++c) {
       i128 v = (i128)L[1 + 3 * c] + ((i128)L[2 + 3 * c] << 42) + ((i128)L[3 + 3 * c] << 84);
-      u64* p = P.tab_sum + ((i64)c * P.G + slot) * 2;
-      p[0] = (u64)v;
-      p[1] = (u64)((u128)v >> 64);
+      tab_store(P, c, slot, v);
     }
     u32 idx = atomicAdd(&C->n_occ, 1u);
     if (idx < (u32)MAXM) P.occ[idx] = slot;
