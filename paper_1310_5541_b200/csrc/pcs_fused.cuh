@@ -398,6 +398,22 @@ __device__ __forceinline__ void tab_add(u64* p, i128 v) {
   if (l1) atomicAdd((unsigned long long*)p + 1, l1);
   if (l2) atomicAdd((unsigned long long*)p + 2, l2);
 }
+__device__ __noinline__ void tab_add_slow(u64* p, float v) { tab_add(p, f32_to_fixed(v, FX_STATE)); }
+// round(v 2^40) of one float32 state value into the limbs: for 2^-17 <= |v| <
+// 2^23 (and 0) the product is an exact int64 (no rounding), else the
+// general conversion
+__device__ __forceinline__ void tab_add_f32(u64* p, float v) {
+  const float av = fabsf(v);
+  if (av < 8388608.0f && (av >= 7.62939453125e-06f || av == 0.0f)) {
+    const long long x = __float2ll_rn(__fmul_rn(v, 1099511627776.0f));
+    const u64 l0 = (u64)x & 0xFFFFFFFFull, l1 = ((u64)x >> 32) & 0xFFFFFFFFull;
+    if (l0) atomicAdd((unsigned long long*)p, l0);
+    if (l1) atomicAdd((unsigned long long*)p + 1, l1);
+    if (x < 0) atomicAdd((unsigned long long*)p + 2, ~0ull);   // the signed rest: -1
+  } else {
+    tab_add_slow(p, v);
+  }
+}
 __device__ __forceinline__ void tab_add_x5(const TrackParams& P, u32 slot, const i128 (&v)[5]) {
 #pragma unroll
   for (int c = 0; c < 5; ++c) tab_add(tab_ptr(P, c, slot), v[c]);
@@ -737,16 +753,14 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
         o[0] = dx;
         o[1] = dy;
       } else {
-        // outside the shared sub-window: exact int128 atomics straight to the
-        // cell's table slot
-        i128 v[5];
-#pragma unroll
-        for (int c = 0; c < 5; ++c) v[c] = f32_to_fixed(o[c], FX_STATE);
+        // outside the shared sub-window: exact fire-and-forget limb
+        // reductions straight to the cell's table slot
         bool created;
         const u32 slot = ht_insert(P, flat, created);
         if (!inwin) P.pslot[j] = (u32)SUBW + slot;   // cell code of an outside cell
         if (slot != HT_EMPTY) {
-          tab_add_x5(P, slot, v);
+#pragma unroll
+          for (int c = 0; c < 5; ++c) tab_add_f32(tab_ptr(P, c, slot), o[c]);
           touch_cell(P, C, slot, 1u, created);
         } else {
           set_flag(C, PCS_FLAG_CAPACITY);
