@@ -258,9 +258,9 @@ def device_info(index=0):
 
 LIK_F64 = 16   # pcs_spot_t.model flag: Poisson models in float64 (pcSIR cells)
 
-TRACK_INFO_KEYS = ("s1_ctas", "s1_tile", "s1_tiles_per_cta", "rs_ctas", "rs_tiles_per_cta",
-                   "sir_chunk", "s1_mid_flushes", "max_occupied", "cells_capacity",
-                   "s1_flush_tiles", "sir_ctas", "launches_per_frame")
+TRACK_INFO_KEYS = ("s1_ctas", "s1_tile", "s1_tiles_per_warp", "rs_ctas", "rs_tiles_per_cta",
+                   "sir_chunk", "s1_cell_flushes", "max_occupied", "cells_capacity",
+                   "s1_cell_flush", "sir_ctas", "launches_per_frame")
 
 
 def track_info():

@@ -1089,14 +1089,14 @@ static int track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int6
     // plain grid stride (c1/c2 sizes: the tickets would not pay)
     P.sir_chunk = (n >= (i64)T.prop_grid * 8 * 2048) ? 2048 : 0;
   }
-  T.s1_grid = (int)std::min<i64>((i64)ctx->sms * S1_CTAS_PER_SM, ceil_div(n, S1_TILE));
+  T.s1_grid = (int)std::min<i64>((i64)ctx->sms * S1_CTAS_PER_SM, std::max<i64>(1, ceil_div(n, (i64)S1_THREADS * 4)));
   T.cells_grid = ctx->sms * 4;
   T.s1_pow2 = cfg->method == 1 && grid_pow2(P.grid.ox, P.grid.lx, P.grid.oy, P.grid.ly);
   {
-    // equal tile counts per CTA: tile = ceil(per_cta / ceil(per_cta / S1_TILE))
-    const i64 per_cta = ceil_div(n, (i64)T.s1_grid);
-    const i64 tpc = ceil_div(per_cta, (i64)S1_TILE);
-    P.s1_tile = (int)std::max<i64>(32, ceil_div(per_cta, tpc));
+    // equal tile counts per warp: tile = ceil(per_warp / ceil(per_warp / S1_MAX_WT))
+    const i64 per_warp = ceil_div(n, (i64)T.s1_grid * S1_WARPS);
+    const i64 tpw = ceil_div(per_warp, (i64)S1_MAX_WT);
+    P.s1_tile = (int)std::max<i64>(32, ceil_div(per_warp, tpw));
   }
   {
     // k_sys_resample has a grid barrier: every CTA must be co-resident
@@ -1644,14 +1644,14 @@ int pcs_track_info(pcs_ctx* ctx, int64_t* out, int32_t n, void* stream) {
   for (int i = 0; i < n; ++i) out[i] = 0;
   out[0] = T.s1_grid;
   out[1] = P.s1_tile;
-  out[2] = (T.s1_grid > 0 && P.s1_tile > 0) ? ceil_div(ceil_div(P.n, (i64)P.s1_tile), (i64)T.s1_grid) : 0;
+  out[2] = (T.s1_grid > 0 && P.s1_tile > 0) ? ceil_div(ceil_div(P.n, (i64)P.s1_tile), (i64)T.s1_grid * S1_WARPS) : 0;
   out[3] = T.rs_small ? T.rs_small : T.rs_grid;
   out[4] = T.rs_small ? 1 : (T.rs_grid > 0 ? ceil_div(ceil_div(P.n, (i64)RS_TILE), (i64)T.rs_grid) : 0);
   out[5] = P.sir_chunk;
   out[6] = h.s1_mid_flush;
   out[7] = h.max_occ;
   out[8] = MAXM;
-  out[9] = S1_FLUSH_TILES;
+  out[9] = S1_CELL_FLUSH;
   out[10] = T.prop_grid;
   out[11] = T.launches;
   return PCS_OK;

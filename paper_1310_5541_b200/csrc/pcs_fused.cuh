@@ -8,8 +8,8 @@
 //                   normaliser / weights / estimate / ESS / decision
 //   k_sys_resample  exact-prefix systematic resampling (filtering.py:93-100)
 //
-// Per-cell accumulation without 64-bit shared-memory atomics: tile counting
-// sort + warp-segmented run sums + 32-bit digit accumulators (S1Smem).
+// Per-cell accumulation without 64-bit shared-memory atomics (those are CAS
+// loops on sm_100): 32-bit digit accumulators (S1Smem).
 // Integer sums are order-free, so the result is exactly the canonical sum of
 // round(s * 2^40).
 #pragma once
@@ -24,16 +24,19 @@ namespace pcs {
 #define PCS_S1_THREADS 512
 #endif
 constexpr int S1_THREADS = PCS_S1_THREADS;     // 2 CTAs x 16 warps per SM; 64 registers
-constexpr int S1_CTAS_PER_SM = 2;              // two independent barrier domains per SM
-constexpr int S1_IPT = 2;
-constexpr int S1_TILE = S1_THREADS * S1_IPT;   // 1024 particles per tile
+constexpr int S1_CTAS_PER_SM = 2;
+constexpr int S1_IPT = 2;                      // particles per lane in flight
 constexpr int S1_WARPS = S1_THREADS / 32;
 constexpr int S1_SIDE = 32;                    // sub-window side (cells)
 constexpr int SUBW = S1_SIDE * S1_SIDE;        // shared-memory sub-window cells
-constexpr int S1_PARTS = 15;                   // 5 components x 3 digits (18/18/signed)
-constexpr int S1_E = 4;                        // sorted elements per thread in the run sums
-constexpr int S1_SUM_THREADS = S1_TILE / S1_E; // 256 threads (8 warps) sum the sorted tile
-constexpr int S1_FLUSH_TILES = 256;            // digit accumulators stay in range (see below)
+constexpr int S1_PARTS = 15;                   // 5 components x 3 digits (16/16/signed)
+constexpr int S1_MAX_WT = 2048;                // most particles per warp tile
+// a sub-window cell's digits are flushed (taken by atomic exchange) each
+// time its count crosses a multiple of S1_CELL_FLUSH, so between two flushes
+// a digit gets S1_CELL_FLUSH additions plus those in flight (< 2 per resident
+// thread): < 2^16 additions of < 2^16 (|.| <= 2^15 for the signed digit), no
+// 32-bit accumulator wraps
+constexpr u32 S1_CELL_FLUSH = 16384;
 constexpr i64 TABLE_MAX = 0xFFFFFFFFll;        // grid cells (flat ids are u32; 2^32 - 1 = empty key)
 // per-frame cell table: open addressing over HT_CAP slots keyed by the flat
 // cell id (2x the occupied-cell capacity MAXM), instead of a dense full-grid
@@ -43,35 +46,25 @@ constexpr u32 HT_CAP = 1u << HT_BITS;
 constexpr u32 HT_EMPTY = 0xFFFFFFFFu;
 constexpr int MAXM = 1 << 20;                  // occupied cells per frame (fused)
 
-// Per-tile pipeline (k_pc_step1, two CTAs per SM): each CTA counting-sorts a
-// tile of 1024 particles by sub-window cell in shared memory (a native 32-bit
-// shared atomic per particle gives its rank), then 8 warps walk the sorted tile, 4
-// consecutive particles per lane, and a warp-segmented scan joins runs that
-// cross lanes. One lane per (cell, warp) adds the exact run sum S (int64,
-// |S| < 2^54) to three 32-bit digit accumulators: bits 0-17, 18-35 (unsigned)
-// and S >> 36 (signed) with native 32-bit shared atomics. A cell gets <= 16
-// additions per tile, so over S1_FLUSH_TILES tiles the digits stay below 2^30
-// in magnitude; the CTA then folds them into the exact int128 HBM table.
-// Scheduling: a CTA's first tile is blockIdx.x, later ones come from a
-// ticket counter (CTAs on slower SMs take fewer tiles); the other 8 warps do
-// not wait for the run sums but start gathering the next tile.
+// k_pc_step1 (two 512-thread CTAs per SM): every warp runs its own tiles of
+// particles, 2 per lane at a time — gather, propagate, cell — and adds each
+// particle that lands in the frame's 32x32-cell shared-memory sub-window to
+// that cell's exact fixed-point sums with native 32-bit shared atomics: the
+// int64 value V = round(v 2^40) of each component goes into three 32-bit
+// digit accumulators (bits 0-15, 16-31, V >> 32). There are no CTA barriers
+// inside the particle loop. Integer sums are order-free, so the cell sums are
+// exactly the canonical sums of round(s 2^40); the CTA folds
+// them into the int128 HBM table at the end (s1_flush) and a cell whose count
+// crosses a multiple of S1_CELL_FLUSH is folded on the spot (s1_cell_flush).
+// Particles outside the sub-window add to the table directly (limb
+// reductions).
+constexpr int S1_CHUNK = 32 * S1_IPT;          // particles per warp pipeline step
 struct S1Smem {
-  float pay[5][S1_TILE];   // cell-sorted tile, lane-major for phase 4 (sorted
-                           // position p at (p % S1_E) * S1_SUM_THREADS + p / S1_E):
-                           // x - ref, y - ref, vx, vy, I0 (exact)
   u32 dig[S1_PARTS][SUBW];
-  u32 cnt[SUBW];          // particles per cell since the last flush
-  u32 tile_cnt[SUBW];
-  unsigned short tile_start[SUBW];
+  u32 cnt[SUBW];          // in-window members of each cell (this CTA)
   float ref[SUBW + 1];    // cell lower edges: x at [0, snx), y at [snx, snx + sny)
                           // (NaN: deltas from this edge may not be exact)
-  unsigned short pay_q[S1_TILE];
-  unsigned short list[S1_TILE];   // cells occupied in this tile
-  unsigned short flist[SUBW];     // cells touched since the last flush
-  u32 n_list, n_flist, n_in;
   int fast_delta;
-  int scan_tmp[S1_WARPS];
-  long long next_tile;
 };
 
 struct TrackCtl {
@@ -167,7 +160,7 @@ struct TrackParams {
                              // finalised after the all-reduce of its per-particle sums
                              // (k_shard_prior_in), not by k_sir_stats
                              // (sharded: rank prefix and first slot in ctl)
-  int s1_tile;               // k_pc_step1 tile (<= S1_TILE), balanced over its CTAs
+  int s1_tile;               // k_pc_step1 warp tile (<= S1_MAX_WT), balanced over the warps
   double thresh;             // resample when ESS < thresh (= threshold_fraction * N)
   float* wprev;              // normalised prior weights when prior_nonuniform
   double* lltab;             // pcSIR with prior weights: [G] log-likelihood per cell
@@ -211,6 +204,7 @@ __device__ __forceinline__ int sub_code(const TrackParams& P, const TrackCtl* C,
 // programmatic-serialization attribute, so the next kernel is scheduled while
 // the current one drains; it waits here for the previous grid (complete and
 // visible) before touching its results.
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -562,25 +556,74 @@ __device__ __forceinline__ void tile_run_sums(const float (*pay)[TILE], const un
   if (kl != 0xFFFF && (lane == 31 || knext != kl)) digits_add<STRIDE>(dig, kl, inc);
 }
 
-// fold the CTA's digit accumulators into the exact int128 HBM table
+// table slot of flat cell id `flat` in the hash-key array (ht_insert without
+// the TrackParams, for the out-of-line cell flush)
+__device__ __forceinline__ u32 ht_insert_k(u32* hkey, u32 flat, bool& created) {
+  created = false;
+  u32 s = ht_hash(flat);
+  for (u32 probe = 0; probe < HT_CAP; ++probe) {
+    const u32 k = __ldcg(hkey + s);
+    if (k == flat) return s;
+    if (k == HT_EMPTY) {
+      const u32 old = atomicCAS(hkey + s, HT_EMPTY, flat);
+      created = (old == HT_EMPTY);
+      if (old == HT_EMPTY || old == flat) return s;
+    }
+    s = (s + 1) & (HT_CAP - 1);
+  }
+  return HT_EMPTY;
+}
+
+// the exact int128 value of the three 16/16/signed digit accumulators of
+// component c, cell q (S1Smem.dig)
+__device__ __forceinline__ i128 s1_digits(u32 d0, u32 d1, u32 d2) {
+  return (i128)d0 + ((i128)d1 << 16) + ((i128)(int)d2 << 32);
+}
+
+// Out-of-line partial flush of ONE sub-window cell whose member count just
+// crossed a multiple of S1_CELL_FLUSH: each digit is taken with an atomic
+// exchange (additions racing with it land either in the taken value or in
+// the accumulator, never in both), so no other warp has to stop. The count
+// and the cell-edge offsets stay for the final flush.
+__device__ __noinline__ void s1_cell_flush(u32* dig, int q, u32 flat, u32* hkey, u64* tab_sum, i64 G,
+                                           u32* tab_cnt, u32* occ, TrackCtl* C) {
+  i128 s[5];
+#pragma unroll
+  for (int c = 0; c < 5; ++c) {
+    const u32 d0 = atomicExch(dig + (3 * c) * SUBW + q, 0u);
+    const u32 d1 = atomicExch(dig + (3 * c + 1) * SUBW + q, 0u);
+    const u32 d2 = atomicExch(dig + (3 * c + 2) * SUBW + q, 0u);
+    s[c] = s1_digits(d0, d1, d2);
+  }
+  bool created;
+  const u32 slot = ht_insert_k(hkey, flat, created);
+  if (slot == HT_EMPTY) {
+    set_flag(C, PCS_FLAG_CAPACITY);
+    return;
+  }
+  atomic_add_i128_x5(tab_sum + (i64)slot * 2, G * 2, s);
+  if (created) {
+    const u32 idx = atomicAdd(&C->n_occ, 1u);
+    if (idx < (u32)MAXM) occ[idx] = slot;
+  }
+  (void)tab_cnt;
+  atomicAdd(&C->s1_mid_flush, 1u);
+}
+
+// fold the CTA's accumulators (digits + count + cell-edge offsets) into the
+// exact int128 HBM table (after the CTA's last particle)
 __device__ __forceinline__ void s1_flush(const TrackParams& P, TrackCtl* C, S1Smem& sm, i64 sx0,
-                                         i64 sy0, int snx) {
+                                         i64 sy0, int snx, int sny) {
   const Grid& g = P.grid;
-  const int nl = (int)sm.n_flist;
-  for (int e = threadIdx.x; e < nl; e += S1_THREADS) {
-    const int q = sm.flist[e];
+  for (int q = threadIdx.x; q < snx * sny; q += S1_THREADS) {
     const u32 cnt = sm.cnt[q];
+    if (cnt == 0) continue;
     const int qx = q % snx, qy = q / snx;
     const u32 flat = (u32)((sy0 + qy) * g.ncols + (sx0 + qx));
     i128 s[5];
 #pragma unroll
-    for (int c = 0; c < 5; ++c) {
-      s[c] = (i128)sm.dig[3 * c][q] + ((i128)sm.dig[3 * c + 1][q] << 18) +
-             ((i128)(int)sm.dig[3 * c + 2][q] << 36);
-      sm.dig[3 * c][q] = 0;
-      sm.dig[3 * c + 1][q] = 0;
-      sm.dig[3 * c + 2][q] = 0;
-    }
+    for (int c = 0; c < 5; ++c)
+      s[c] = s1_digits(sm.dig[3 * c][q], sm.dig[3 * c + 1][q], sm.dig[3 * c + 2][q]);
     s[0] += (i128)cnt * f32_to_fixed(sm.ref[qx], FX_STATE);
     s[1] += (i128)cnt * f32_to_fixed(sm.ref[snx + qy], FX_STATE);
     bool created;
@@ -591,32 +634,27 @@ __device__ __forceinline__ void s1_flush(const TrackParams& P, TrackCtl* C, S1Sm
     } else {
       set_flag(C, PCS_FLAG_CAPACITY);
     }
-    sm.cnt[q] = 0;
+  }
+}
+
+// add one in-window particle's exact values (x - ref, y - ref, vx, vy, I0;
+// round(v 2^40) exact, |v| < 128) to cell q: the int64 V splits into bits
+// 0-15, 16-31 (unsigned) and V >> 32 (signed, |.| < 2^15), each added with a
+// native 32-bit shared atomic
+__device__ __forceinline__ void s1_add(u32* dig, int q, const float (&v)[5]) {
+#pragma unroll
+  for (int c = 0; c < 5; ++c) {
+    const long long V = __float2ll_rn(__fmul_rn(v[c], 1099511627776.0f));
+    const u32 lo = (u32)V;
+    atomicAdd(dig + (3 * c) * SUBW + q, lo & 0xFFFFu);
+    atomicAdd(dig + (3 * c + 1) * SUBW + q, lo >> 16);
+    atomicAdd(dig + (3 * c + 2) * SUBW + q, (u32)(V >> 32));
   }
 }
 
 template <bool POW2>
-// PCS_S1_PROBE: clock64 split of CTA 0 thread 0 over the tile phases into
-// dbg[10..14] (p1, p2, p3, p4 run sums, flush) and the loop total in dbg[15]
-// (diagnostic builds only, tools/s1_probe.py)
-#ifdef PCS_S1_PROBE
-#define S1_MARK(i)                                                                    \
-  do {                                                                                \
-    if (blockIdx.x == 0 && threadIdx.x == 0) {                                        \
-      const long long _c = clock64();                                                 \
-      if ((i) >= 0) s1_acc[i] += _c - s1_t;                                           \
-      s1_t = _c;                                                                      \
-    }                                                                                 \
-  } while (0)
-#else
-#define S1_MARK(i) do {} while (0)
-#endif
-
 __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackParams P) {
   extern __shared__ __align__(16) unsigned char s1_raw[];
-#ifdef PCS_S1_PROBE
-  long long s1_acc[5] = {0, 0, 0, 0, 0}, s1_t = 0, s1_t0 = clock64();
-#endif
   S1Smem& sm = *reinterpret_cast<S1Smem*>(s1_raw);
   TrackCtl* C = P.ctl;
   pdl_trigger();
@@ -628,11 +666,6 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
   float* sout = (k & 1) ? P.buf0 : P.buf1;
   const Grid g = P.grid;
   const i64 n = P.n, ld = P.ld;
-  // runtime tile (<= S1_TILE) chosen by the host so that every CTA gets the
-  // same number of tiles (no tail CTA with one extra tile)
-  const int TT = P.s1_tile;
-  const i64 ntile = ceil_div(n, (i64)TT);
-  const i64 tstep = gridDim.x;
 
   // sub-window (identical in every CTA): centred on the previous estimate
   i64 snx = min((i64)S1_SIDE, g.ncols), sny = min((i64)S1_SIDE, g.nrows);
@@ -648,7 +681,6 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
   const int snxi = (int)snx, snyi = (int)sny;
   for (int q = t; q < SUBW; q += S1_THREADS) {
     sm.cnt[q] = 0;
-    sm.tile_cnt[q] = 0;
 #pragma unroll
     for (int p = 0; p < S1_PARTS; ++p) sm.dig[p][q] = 0;
   }
@@ -666,10 +698,6 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
     const double l2 = 2.0 * ((q < snxi) ? g.lx : g.ly);
     if (!ok || !((double)r >= l2)) atomicAnd(&sm.fast_delta, 0);
   }
-  if (t == 0) {
-    sm.n_list = 0;
-    sm.n_flist = 0;
-  }
   const float* refy = sm.ref + snxi;
   __syncthreads();
   const bool fast_delta = sm.fast_delta != 0;
@@ -679,189 +707,105 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
   const AxisFast axy = make_axis(g.oy, g.ly, P.inv_ly, g.nrows);
   const u32 ncols32 = (u32)g.ncols;
   const int sx0i = (int)sx0, sy0i = (int)sy0;
+  u32* dig = &sm.dig[0][0];
   bool bad = false;
-  int since = 0;
-  // first tile static, then dynamic tickets: CTAs on slower SMs (die / HBM
-  // distance) take fewer tiles instead of finishing last
-  S1_MARK(-1);
-  for (i64 tile = blockIdx.x; tile < ntile;) {
-    // ---- phase 1: gather + propagate + cell; rank within the tile's cell ----
-    int q_k[S1_IPT], r_k[S1_IPT];
-    float o_k[S1_IPT][5];
-    int src_k[S1_IPT];
-    const i64 j0 = tile * TT;   // (n < 2^31: particle indices fit 32 bits)
+  // warp tiles of P.s1_tile particles (sized by the host so that every warp
+  // gets the same number); the first is static, later ones come from a
+  // ticket counter drawn one tile ahead (warps on slower SMs take fewer)
+  const int WT = P.s1_tile;
+  const int nwarps = (int)gridDim.x * S1_WARPS;
+  const int ntile = (int)ceil_div(n, (i64)WT);
+  int tile = (int)blockIdx.x * S1_WARPS + warp;
+  while (tile < ntile) {
+    u32 tk = 0;
+    if (lane == 0) tk = atomicAdd(&C->s1_ticket, 1u);
+    const int jt0 = tile * WT;
+    const int jt1 = (int)min((i64)jt0 + WT, n);
+    for (int jb = jt0; jb < jt1; jb += S1_CHUNK) {
+      int src_k[S1_IPT];
+      float o_k[S1_IPT][5];
 #pragma unroll
-    for (int it = 0; it < S1_IPT; ++it) {   // every gather before any arithmetic
-      const int l = it * S1_THREADS + t;
-      const int j = (int)j0 + l;
-      src_k[it] = (l < TT && j < (int)n) ? __ldg(P.anc + j) : -1;
-    }
-#pragma unroll
-    for (int it = 0; it < S1_IPT; ++it) {
-      // component c of particle src at sin + src + c ld: one wide multiply,
-      // then pointer steps of ld (no per-component 64-bit index products)
-      const float* g = sin + (src_k[it] >= 0 ? src_k[it] : 0);
-#pragma unroll
-      for (int c = 0; c < 5; ++c) {
-        o_k[it][c] = (src_k[it] >= 0) ? __ldg(g) : 0.0f;
-        g += ld;
+      for (int it = 0; it < S1_IPT; ++it) {   // every gather before any arithmetic
+        const int j = jb + it * 32 + lane;
+        src_k[it] = (j < jt1) ? __ldg(P.anc + j) : -1;
       }
-    }
 #pragma unroll
-    for (int it = 0; it < S1_IPT; ++it) {
-      q_k[it] = -1;
-      const int j = (int)j0 + it * S1_THREADS + t;
-      if (src_k[it] < 0) continue;
-      float s[5], z[5];
-#pragma unroll
-      for (int c = 0; c < 5; ++c) s[c] = o_k[it][c];
-      philox_normals5k(P.pk, frame, (u64)(P.idx_off + j), z);
-      float* o = o_k[it];
-      propagate_one(s, z, P.dyn, o);
-      {
-        float* d = sout + j;
+      for (int it = 0; it < S1_IPT; ++it) {
+        const float* gp = sin + (src_k[it] >= 0 ? src_k[it] : 0);
 #pragma unroll
         for (int c = 0; c < 5; ++c) {
-          *d = o[c];
-          d += ld;
+          o_k[it][c] = (src_k[it] >= 0) ? __ldg(gp) : 0.0f;
+          gp += ld;
         }
       }
-      if (!(o[0] == o[0]) || !(o[1] == o[1])) bad = true;
-      const int ix = cell_axis_hot<POW2>(o[0], axx);
-      const int iy = cell_axis_hot<POW2>(o[1], axy);
-      const u32 flat = (u32)iy * ncols32 + (u32)ix;   // G <= 2^28
-      const int lx = ix - sx0i, ly = iy - sy0i;
-      const bool inwin = (u32)lx < (u32)snxi && (u32)ly < (u32)snyi;
-      if (inwin) P.pslot[j] = (u32)(ly * snxi + lx);   // cell code (else: below)
-      float dx, dy;
-      bool dok = false;
-      if (inwin) {
-        if (fast_delta) {   // (CTA-uniform branch)
-          dx = __fsub_rn(o[0], sm.ref[lx]);
-          dy = __fsub_rn(o[1], refy[ly]);
-          dok = true;
+#pragma unroll
+      for (int it = 0; it < S1_IPT; ++it) {
+        if (src_k[it] < 0) continue;
+        const int j = jb + it * 32 + lane;
+        float s[5], z[5];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) s[c] = o_k[it][c];
+        philox_normals5k(P.pk, frame, (u64)(P.idx_off + j), z);
+        float* o = o_k[it];
+        propagate_one(s, z, P.dyn, o);
+        {
+          float* d = sout + j;
+#pragma unroll
+          for (int c = 0; c < 5; ++c) {
+            *d = o[c];
+            d += ld;
+          }
+        }
+        if (!(o[0] == o[0]) || !(o[1] == o[1])) bad = true;
+        const int ix = cell_axis_hot<POW2>(o[0], axx);
+        const int iy = cell_axis_hot<POW2>(o[1], axy);
+        const u32 flat = (u32)iy * ncols32 + (u32)ix;   // G <= 2^32 - 1
+        const int lx = ix - sx0i, ly = iy - sy0i;
+        const bool inwin = (u32)lx < (u32)snxi && (u32)ly < (u32)snyi;
+        if (inwin) P.pslot[j] = (u32)(ly * snxi + lx);   // cell code (else: below)
+        float dx, dy;
+        bool dok = false;
+        if (inwin) {
+          if (fast_delta) {   // (CTA-uniform branch)
+            dx = __fsub_rn(o[0], sm.ref[lx]);
+            dy = __fsub_rn(o[1], refy[ly]);
+            dok = true;
+          } else {
+            dok = delta_exact(o[0], sm.ref[lx], dx) && delta_exact(o[1], refy[ly], dy);
+          }
+        }
+        if (dok && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f && fabsf(o[4]) < 128.0f) {
+          const int q = ly * snxi + lx;
+          const u32 old = atomicAdd(&sm.cnt[q], 1u);
+          if (((old + 1u) & (S1_CELL_FLUSH - 1u)) == 0u)
+            s1_cell_flush(dig, q, flat, P.hkey, P.tab_sum, P.G, P.tab_cnt, P.occ, C);
+          o[0] = dx;
+          o[1] = dy;
+          s1_add(dig, q, o_k[it]);
         } else {
-          dok = delta_exact(o[0], sm.ref[lx], dx) && delta_exact(o[1], refy[ly], dy);
-        }
-      }
-      if (dok && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f && fabsf(o[4]) < 128.0f) {
-        const int q = ly * snxi + lx;
-        const int r = (int)atomicAdd(&sm.tile_cnt[q], 1u);
-        if (r == 0) sm.list[atomicAdd(&sm.n_list, 1u)] = (unsigned short)q;
-        q_k[it] = q;
-        r_k[it] = r;
-        o[0] = dx;
-        o[1] = dy;
-      } else {
-        // outside the shared sub-window: exact fire-and-forget limb
-        // reductions straight to the cell's table slot
-        bool created;
-        const u32 slot = ht_insert(P, flat, created);
-        if (!inwin) P.pslot[j] = (u32)SUBW + slot;   // cell code of an outside cell
-        if (slot != HT_EMPTY) {
+          // outside the shared sub-window: exact fire-and-forget limb
+          // reductions straight to the cell's table slot
+          bool created;
+          const u32 slot = ht_insert(P, flat, created);
+          if (!inwin) P.pslot[j] = (u32)SUBW + slot;   // cell code of an outside cell
+          if (slot != HT_EMPTY) {
 #pragma unroll
-          for (int c = 0; c < 5; ++c) tab_add_f32(tab_ptr(P, c, slot), o[c]);
-          touch_cell(P, C, slot, 1u, created);
-        } else {
-          set_flag(C, PCS_FLAG_CAPACITY);
+            for (int c = 0; c < 5; ++c) tab_add_f32(tab_ptr(P, c, slot), o[c]);
+            touch_cell(P, C, slot, 1u, created);
+          } else {
+            set_flag(C, PCS_FLAG_CAPACITY);
+          }
         }
       }
     }
-    __syncthreads();
-    S1_MARK(0);
-    if (t == 0) sm.next_tile = tstep + (long long)atomicAdd(&C->s1_ticket, 1u);
-    // ---- phase 2: run offsets (exclusive scan of the tile's cell counts) ----
-    {
-      const int nl = (int)sm.n_list;
-      const int e0 = 2 * t;
-      const int c0 = (e0 < nl) ? (int)sm.tile_cnt[sm.list[e0]] : 0;
-      const int c1 = (e0 + 1 < nl) ? (int)sm.tile_cnt[sm.list[e0 + 1]] : 0;
-      int inc = c0 + c1;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        int o = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += o;
-      }
-      if (lane == 31) sm.scan_tmp[warp] = inc;
-      __syncthreads();
-      if (t == 0) sm.n_list = 0;   // every thread has read n_list
-      int woff = (lane < warp) ? sm.scan_tmp[lane] : 0;
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) woff += __shfl_xor_sync(0xffffffffu, woff, d);
-      int run = woff + inc - c0 - c1;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int e = e0 + h;
-        if (e < nl) {
-          const int q = sm.list[e];
-          const u32 c = (u32)(h ? c1 : c0);
-          sm.tile_start[q] = (unsigned short)run;
-          sm.tile_cnt[q] = 0;
-          const u32 old = sm.cnt[q];
-          sm.cnt[q] = old + c;
-          if (old == 0) sm.flist[atomicAdd(&sm.n_flist, 1u)] = (unsigned short)q;
-          run += (int)c;
-        }
-      }
-      if (t == S1_THREADS - 1) sm.n_in = (u32)run;
-    }
-    __syncthreads();
-    S1_MARK(1);
-    // ---- phase 3: scatter the in-window particles into cell-sorted order ----
-    // (the next tile is known since phase 2: pull its ancestor indices into L2
-    // now, so its gather starts with an L2 hit instead of a DRAM round trip)
-    if (t < S1_TILE / 32) {
-      const i64 nt = sm.next_tile;
-      if (nt < ntile) {
-        const int* a = P.anc + nt * TT + t * 32;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-      }
-    }
-    float (*pay)[S1_TILE] = sm.pay;
-#pragma unroll
-    for (int it = 0; it < S1_IPT; ++it) {
-      if (q_k[it] < 0) continue;
-      const int pos = (int)sm.tile_start[q_k[it]] + r_k[it];
-      const int idx = (pos % S1_E) * S1_SUM_THREADS + pos / S1_E;
-#pragma unroll
-      for (int c = 0; c < 5; ++c) pay[c][idx] = o_k[it][c];
-      sm.pay_q[idx] = (unsigned short)q_k[it];
-    }
-    __syncthreads();
-    S1_MARK(2);
-    const i64 next_tile = sm.next_tile;   // (written before the phase-2 barriers)
-    // ---- phase 4: exact run sums over the sorted tile (8 warps, 4
-    //      consecutive particles per lane, warp-segmented scan across lanes) ----
-    if (t < S1_SUM_THREADS)
-      tile_run_sums<S1_SUM_THREADS, S1_E, S1_TILE, SUBW>(pay, sm.pay_q, (int)sm.n_in, &sm.dig[0][0], t);
-    S1_MARK(3);
-    // no barrier here: the other warps start the next tile's gathers while the
-    // summing warps finish (phase 1 touches none of pay / pay_q / n_in, and
-    // the next pay write is two barriers away)
-    if (++since == S1_FLUSH_TILES) {
-      since = 0;
-      if (t == 0) atomicAdd(&C->s1_mid_flush, 1u);
-      __syncthreads();
-      s1_flush(P, C, sm, sx0, sy0, snxi);
-      __syncthreads();
-      if (t == 0) sm.n_flist = 0;
-      __syncthreads();
-      S1_MARK(4);
-    }
-    tile = next_tile;
+    tile = nwarps + (int)__shfl_sync(0xffffffffu, tk, 0);
   }
-#ifdef PCS_S1_PROBE
-  if (blockIdx.x == 0 && t == 0) {
-    for (int i = 0; i < 5; ++i) C->dbg[10 + i] = s1_acc[i];
-    C->dbg[15] = clock64() - s1_t0;
-  }
-#endif
   __syncthreads();
   if (t == 0 && atomicAdd(&C->s1_done, 1u) == gridDim.x - 1) {   // every ticket is drawn
     C->s1_ticket = 0;
     C->s1_done = 0;
   }
-  s1_flush(P, C, sm, sx0, sy0, snxi);
+  s1_flush(P, C, sm, sx0, sy0, snxi, snyi);
   if (bad) set_flag(C, PCS_FLAG_NONFINITE);
 }
 
@@ -1299,7 +1243,6 @@ __device__ __forceinline__ void grid_barrier(TrackCtl* C, int nblocks) {
   __syncthreads();
 }
 
-__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, u32 count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }

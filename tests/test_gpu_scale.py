@@ -2,8 +2,8 @@
 loop equals the independent step-by-step device path bit-for-bit, and the
 fused frame's estimate equals the oracle's canonical sums on the fused path's
 own states. At these sizes the code paths that small tests never reach run:
-the step-1 mid-loop digit flush (>= S1_FLUSH_TILES tiles per CTA), the
-resampler's TMA ring past its first two buffers (>= 2 tiles per CTA), the
+the step-1 per-cell digit flush (a cell's count in one CTA crossing
+S1_CELL_FLUSH), several warp tiles per step-1 warp, the resampler's TMA ring past its first two buffers (>= 2 tiles per CTA), the
 per-cell kernel over thousands of occupied cells (> 4096) and the SIR
 likelihood's dynamic chunks — pcs_track_info reports which ran and the tests
 assert it."""
@@ -52,7 +52,7 @@ def _track_states():
 
 def test_c5_shape_fused_equals_general_and_oracle(cuda):
     """Config 5's shape (4096^2 frames, 0.25 px cells on a 16384^2 grid) at
-    N = 2^27: 296 step-1 CTAs x ~440 tiles each (mid-loop flushes), 59
+    N = 2^27: 296 step-1 CTAs, several warp tiles per warp (ticketed), 59
     resampler tiles per CTA, ~5k occupied cells at frame 0."""
     n = 1 << 27
     start = (2043.0, 2048.0)
@@ -68,8 +68,7 @@ def test_c5_shape_fused_equals_general_and_oracle(cuda):
     assert np.array_equal(a.resampled, b.resampled)
     assert a.likelihood_evals == b.likelihood_evals
     # the size-dependent paths ran
-    assert info["s1_tiles_per_cta"] > info["s1_flush_tiles"], info
-    assert info["s1_mid_flushes"] > 0, info
+    assert info["s1_tiles_per_warp"] > 1, info
     assert info["rs_tiles_per_cta"] >= 2, info
     assert info["max_occupied"] > 4096, info        # (more than one CTA's worth of cells)
     assert np.sqrt(np.mean(np.sum((a.positions - truth) ** 2, axis=1))) < 0.5
@@ -117,6 +116,28 @@ def test_c5_shape_frame_estimate_equals_oracle(cuda):
     est, ess = orc.estimate_ess_exact(s32, w.cpu().numpy())
     assert np.array_equal(a.estimates[0], est)
     assert a.ess[0] == ess
+
+
+def test_coarse_cells_per_cell_flush_fused_equals_general(cuda):
+    """16 px cells at N = 2^24: every step-1 CTA adds tens of thousands of
+    particles to the same few sub-window cells, so their digit accumulators
+    are folded on the spot (count crossing S1_CELL_FLUSH, atomic-exchange
+    flush) while other warps keep adding. Fused == general bit for bit."""
+    n = 1 << 24
+    start = (120.0, 128.0)
+    frames, _ = synthesis.spot_scene(3, 256, start, seed=0)
+    init = pc.InitSpec(pc.StateVector(start[0], start[1], 0.5, 0.0, 20.0), "gauss", sigma=2.0)
+    lik = pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(10.0, 5))
+    grid = pc.BinGrid(-0.5, -0.5, 16.0, 16.0, 16, 16)
+    mk = lambda: pc.PcFilterConfig(n, init, DYN, RES, lik, grid=grid)   # noqa: E731
+    a = pc.pcsir_track(frames, mk(), pc.PhiloxRng(3), fused=True)
+    info = _lib.track_info()
+    b = pc.pcsir_track(frames, mk(), pc.PhiloxRng(3), fused=False)
+    assert a.path == "fused" and b.path == "general"
+    assert np.array_equal(a.estimates, b.estimates)
+    assert np.array_equal(a.ess, b.ess)
+    assert np.array_equal(a.resampled, b.resampled)
+    assert info["s1_cell_flushes"] > 0, info
 
 
 @pytest.mark.parametrize("cpp", [None, 0.5])

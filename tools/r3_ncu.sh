@@ -1,0 +1,11 @@
+# ncu --set full of the frame kernels at the c5 shape (N = 2^24) after a plain run
+set -u
+mkdir -p gpurun_out
+TAG=${1:-x}
+KRE=${KRE:-k_pc_step1|k_sys_resample}
+SARGS="--workload c5 --n 16777216 --steps 3 --warmup 3 --no-variants --no-cpu-baseline"
+timeout 600 python bench.py $SARGS > gpurun_out/plain_${TAG}_c5s.log 2>&1 && \
+timeout 1200 ncu --set full --clock-control none --import-source on \
+  -k "regex:$KRE" -s 6 -c 2 \
+  -o gpurun_out/prof_${TAG}_c5s python bench.py $SARGS > gpurun_out/ncu_${TAG}.log 2>&1
+echo ncu_rc=$?
