@@ -574,6 +574,12 @@ __device__ __forceinline__ u32 ht_insert_k(u32* hkey, u32 flat, bool& created) {
   return HT_EMPTY;
 }
 
+// shared-memory slot of sub-window cell q in the per-cell accumulators: a
+// permutation inside each row of 32 cells so that a compact blob of cells
+// (the particle cloud) spreads over all 32 banks instead of one bank per
+// column (bank conflicts of the shared atomics)
+__device__ __forceinline__ int s1_swz(int q) { return (q & ~31) | ((q + 13 * (q >> 5)) & 31); }
+
 // the exact int128 value of the three 16/16/signed digit accumulators of
 // component c, cell q (S1Smem.dig)
 __device__ __forceinline__ i128 s1_digits(u32 d0, u32 d1, u32 d2) {
@@ -616,14 +622,15 @@ __device__ __forceinline__ void s1_flush(const TrackParams& P, TrackCtl* C, S1Sm
                                          i64 sy0, int snx, int sny) {
   const Grid& g = P.grid;
   for (int q = threadIdx.x; q < snx * sny; q += S1_THREADS) {
-    const u32 cnt = sm.cnt[q];
+    const int qs = s1_swz(q);
+    const u32 cnt = sm.cnt[qs];
     if (cnt == 0) continue;
     const int qx = q % snx, qy = q / snx;
     const u32 flat = (u32)((sy0 + qy) * g.ncols + (sx0 + qx));
     i128 s[5];
 #pragma unroll
     for (int c = 0; c < 5; ++c)
-      s[c] = s1_digits(sm.dig[3 * c][q], sm.dig[3 * c + 1][q], sm.dig[3 * c + 2][q]);
+      s[c] = s1_digits(sm.dig[3 * c][qs], sm.dig[3 * c + 1][qs], sm.dig[3 * c + 2][qs]);
     s[0] += (i128)cnt * f32_to_fixed(sm.ref[qx], FX_STATE);
     s[1] += (i128)cnt * f32_to_fixed(sm.ref[snx + qy], FX_STATE);
     bool created;
@@ -775,13 +782,13 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
           }
         }
         if (dok && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f && fabsf(o[4]) < 128.0f) {
-          const int q = ly * snxi + lx;
-          const u32 old = atomicAdd(&sm.cnt[q], 1u);
+          const int qs = s1_swz(ly * snxi + lx);
+          const u32 old = atomicAdd(&sm.cnt[qs], 1u);
           if (((old + 1u) & (S1_CELL_FLUSH - 1u)) == 0u)
-            s1_cell_flush(dig, q, flat, P.hkey, P.tab_sum, P.G, P.tab_cnt, P.occ, C);
+            s1_cell_flush(dig, qs, flat, P.hkey, P.tab_sum, P.G, P.tab_cnt, P.occ, C);
           o[0] = dx;
           o[1] = dy;
-          s1_add(dig, q, o_k[it]);
+          s1_add(dig, qs, o_k[it]);
         } else {
           // outside the shared sub-window: exact fire-and-forget limb
           // reductions straight to the cell's table slot
