@@ -988,6 +988,8 @@ static int track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int6
   P.grid = cfg->method == 1 ? to_grid(&cfg->grid) : Grid{0, 0, 1, 1, 1, 1};
   P.inv_lx = 1.0 / P.grid.lx;
   P.inv_ly = 1.0 / P.grid.ly;
+  P.axx = make_axis(P.grid.ox, P.grid.lx, P.inv_lx, P.grid.ncols);
+  P.axy = make_axis(P.grid.oy, P.grid.ly, P.inv_ly, P.grid.nrows);
   P.seed = cfg->seed;
   P.pk = philox_key(cfg->seed);
   P.frame0 = cfg->frame0;

@@ -118,6 +118,13 @@ struct TrackCtl {
   u32 max_occ;               // diagnostics: most occupied cells of a frame
 };
 
+// cell-index constants of one grid axis (cell_axis_hot below)
+struct AxisFast {
+  float o32, inv32, mt, ma, mb, fmax;
+  double origin, cell, inv;
+  i64 n;
+};
+
 struct TrackParams {
   i64 n, ld;
   i64 H, W;
@@ -125,6 +132,7 @@ struct TrackParams {
   Spot spot;
   Grid grid;
   double inv_lx, inv_ly;
+  AxisFast axx, axy;         // k_pc_step1 cell index constants (make_axis on the host)
   u64 seed;
   PhiloxKey pk;              // round keys of seed (constant-bank operands)
   u32 frame0;
@@ -272,18 +280,18 @@ __device__ __forceinline__ i64 cell_axis_fast(float p, double origin, double cel
 // integer), and only inside [0, min(n-1, 2^24)]; everything else (integer
 // quotients, clamping, NaN) takes the float64 path. Same result as
 // cell_axis_fast.
-struct AxisFast {
-  float o32, inv32, mt, ma, mb, fmax;
-  double origin, cell, inv;
-  i64 n;
-};
 
-__device__ __forceinline__ AxisFast make_axis(double origin, double cell, double inv, i64 n) {
+__host__ __device__ __forceinline__ AxisFast make_axis(double origin, double cell, double inv, i64 n) {
   AxisFast a;
   a.o32 = (float)origin;
   a.inv32 = (float)inv;
   int e;
-  const bool pow2 = frexp(inv, &e) == 0.5 && __dmul_rn(cell, inv) == 1.0 &&
+#ifdef __CUDA_ARCH__
+  const double ci = __dmul_rn(cell, inv);
+#else
+  const double ci = cell * inv;
+#endif
+  const bool pow2 = frexp(inv, &e) == 0.5 && ci == 1.0 &&
                     (double)a.inv32 == inv && (double)a.o32 == origin && e > -100 && e < 100;
   if (pow2) {
     a.mt = 0.0f;
@@ -294,7 +302,7 @@ __device__ __forceinline__ AxisFast make_axis(double origin, double cell, double
     a.ma = fabsf(a.inv32) * 9.5367431640625e-07f;
     a.mb = (fabsf(a.o32) * fabsf(a.inv32) + 1.0f) * 9.5367431640625e-07f;
   }
-  a.fmax = (float)min(n - 1, (i64)(1 << 24));
+  a.fmax = (float)(n - 1 < (i64)(1 << 24) ? n - 1 : (i64)(1 << 24));
   a.origin = origin;
   a.cell = cell;
   a.inv = inv;
@@ -710,102 +718,126 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
   const bool fast_delta = sm.fast_delta != 0;
 
   const u32 frame = P.frame0 + (u32)k;
-  const AxisFast axx = make_axis(g.ox, g.lx, P.inv_lx, g.ncols);
-  const AxisFast axy = make_axis(g.oy, g.ly, P.inv_ly, g.nrows);
+  const AxisFast& axx = P.axx;   // (host-computed: constant-bank operands, no registers)
+  const AxisFast& axy = P.axy;
   const u32 ncols32 = (u32)g.ncols;
   const int sx0i = (int)sx0, sy0i = (int)sy0;
   u32* dig = &sm.dig[0][0];
   bool bad = false;
   // warp tiles of P.s1_tile particles (sized by the host so that every warp
   // gets the same number); the first is static, later ones come from a
-  // ticket counter drawn one tile ahead (warps on slower SMs take fewer)
+  // ticket counter drawn one tile ahead (warps on slower SMs take fewer).
+  // Each warp streams its tiles as chunks of S1_CHUNK particles; the next
+  // chunk's ancestor indices are loaded while the current chunk computes.
   const int WT = P.s1_tile;
   const int nwarps = (int)gridDim.x * S1_WARPS;
   const int ntile = (int)ceil_div(n, (i64)WT);
-  int tile = (int)blockIdx.x * S1_WARPS + warp;
-  while (tile < ntile) {
-    u32 tk = 0;
-    if (lane == 0) tk = atomicAdd(&C->s1_ticket, 1u);
-    const int jt0 = tile * WT;
-    const int jt1 = (int)min((i64)jt0 + WT, n);
-    for (int jb = jt0; jb < jt1; jb += S1_CHUNK) {
-      int src_k[S1_IPT];
-      float o_k[S1_IPT][5];
+  u32 tk = 0;   // (lane 0) the ticket of the tile after the latest one entered
+  if (lane == 0) tk = atomicAdd(&C->s1_ticket, 1u);
+  auto first_chunk = [&](int tl, int& jb, int& je) {
+    if (tl < ntile) {
+      jb = tl * WT;
+      je = (int)min((i64)jb + WT, n);
+    } else {
+      jb = -1;
+      je = 0;
+    }
+  };
+  auto next_chunk = [&](int& jb, int& je) {
+    if (jb < 0) return;
+    jb += S1_CHUNK;
+    if (jb < je) return;
+    const int tl = nwarps + (int)__shfl_sync(0xffffffffu, tk, 0);
+    if (lane == 0 && tl < ntile) tk = atomicAdd(&C->s1_ticket, 1u);
+    first_chunk(tl, jb, je);
+  };
+  auto load_src = [&](int jb, int je, int (&src)[S1_IPT]) {
 #pragma unroll
-      for (int it = 0; it < S1_IPT; ++it) {   // every gather before any arithmetic
-        const int j = jb + it * 32 + lane;
-        src_k[it] = (j < jt1) ? __ldg(P.anc + j) : -1;
+    for (int it = 0; it < S1_IPT; ++it) {
+      const int j = jb + it * 32 + lane;
+      src[it] = (jb >= 0 && j < je) ? __ldg(P.anc + j) : -1;
+    }
+  };
+  int jb0, je0, jb1, je1;
+  first_chunk((int)blockIdx.x * S1_WARPS + warp, jb0, je0);
+  jb1 = jb0; je1 = je0; next_chunk(jb1, je1);
+  int src_k[S1_IPT], src1[S1_IPT];
+  load_src(jb0, je0, src_k);
+  while (jb0 >= 0) {
+    load_src(jb1, je1, src1);   // the next chunk's ancestors (consumed next iteration)
+    float o_k[S1_IPT][5];
+#pragma unroll
+    for (int it = 0; it < S1_IPT; ++it) {
+      const float* gp = sin + (src_k[it] >= 0 ? src_k[it] : 0);
+#pragma unroll
+      for (int c = 0; c < 5; ++c) {
+        o_k[it][c] = (src_k[it] >= 0) ? __ldg(gp) : 0.0f;
+        gp += ld;
       }
+    }
 #pragma unroll
-      for (int it = 0; it < S1_IPT; ++it) {
-        const float* gp = sin + (src_k[it] >= 0 ? src_k[it] : 0);
+    for (int it = 0; it < S1_IPT; ++it) {
+      if (src_k[it] < 0) continue;
+      const int j = jb0 + it * 32 + lane;
+      float s[5], z[5];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) s[c] = o_k[it][c];
+      philox_normals5k(P.pk, frame, (u64)(P.idx_off + j), z);
+      float* o = o_k[it];
+      propagate_one(s, z, P.dyn, o);
+      {
+        float* d = sout + j;
 #pragma unroll
         for (int c = 0; c < 5; ++c) {
-          o_k[it][c] = (src_k[it] >= 0) ? __ldg(gp) : 0.0f;
-          gp += ld;
+          *d = o[c];
+          d += ld;
         }
       }
-#pragma unroll
-      for (int it = 0; it < S1_IPT; ++it) {
-        if (src_k[it] < 0) continue;
-        const int j = jb + it * 32 + lane;
-        float s[5], z[5];
-#pragma unroll
-        for (int c = 0; c < 5; ++c) s[c] = o_k[it][c];
-        philox_normals5k(P.pk, frame, (u64)(P.idx_off + j), z);
-        float* o = o_k[it];
-        propagate_one(s, z, P.dyn, o);
-        {
-          float* d = sout + j;
-#pragma unroll
-          for (int c = 0; c < 5; ++c) {
-            *d = o[c];
-            d += ld;
-          }
-        }
-        if (!(o[0] == o[0]) || !(o[1] == o[1])) bad = true;
-        const int ix = cell_axis_hot<POW2>(o[0], axx);
-        const int iy = cell_axis_hot<POW2>(o[1], axy);
-        const u32 flat = (u32)iy * ncols32 + (u32)ix;   // G <= 2^32 - 1
-        const int lx = ix - sx0i, ly = iy - sy0i;
-        const bool inwin = (u32)lx < (u32)snxi && (u32)ly < (u32)snyi;
-        if (inwin) P.pslot[j] = (u32)(ly * snxi + lx);   // cell code (else: below)
-        float dx, dy;
-        bool dok = false;
-        if (inwin) {
-          if (fast_delta) {   // (CTA-uniform branch)
-            dx = __fsub_rn(o[0], sm.ref[lx]);
-            dy = __fsub_rn(o[1], refy[ly]);
-            dok = true;
-          } else {
-            dok = delta_exact(o[0], sm.ref[lx], dx) && delta_exact(o[1], refy[ly], dy);
-          }
-        }
-        if (dok && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f && fabsf(o[4]) < 128.0f) {
-          const int qs = s1_swz(ly * snxi + lx);
-          const u32 old = atomicAdd(&sm.cnt[qs], 1u);
-          if (((old + 1u) & (S1_CELL_FLUSH - 1u)) == 0u)
-            s1_cell_flush(dig, qs, flat, P.hkey, P.tab_sum, P.G, P.tab_cnt, P.occ, C);
-          o[0] = dx;
-          o[1] = dy;
-          s1_add(dig, qs, o_k[it]);
+      if (!(o[0] == o[0]) || !(o[1] == o[1])) bad = true;
+      const int ix = cell_axis_hot<POW2>(o[0], axx);
+      const int iy = cell_axis_hot<POW2>(o[1], axy);
+      const u32 flat = (u32)iy * ncols32 + (u32)ix;   // G <= 2^32 - 1
+      const int lx = ix - sx0i, ly = iy - sy0i;
+      const bool inwin = (u32)lx < (u32)snxi && (u32)ly < (u32)snyi;
+      if (inwin) P.pslot[j] = (u32)(ly * snxi + lx);   // cell code (else: below)
+      float dx, dy;
+      bool dok = false;
+      if (inwin) {
+        if (fast_delta) {   // (CTA-uniform branch)
+          dx = __fsub_rn(o[0], sm.ref[lx]);
+          dy = __fsub_rn(o[1], refy[ly]);
+          dok = true;
         } else {
-          // outside the shared sub-window: exact fire-and-forget limb
-          // reductions straight to the cell's table slot
-          bool created;
-          const u32 slot = ht_insert(P, flat, created);
-          if (!inwin) P.pslot[j] = (u32)SUBW + slot;   // cell code of an outside cell
-          if (slot != HT_EMPTY) {
+          dok = delta_exact(o[0], sm.ref[lx], dx) && delta_exact(o[1], refy[ly], dy);
+        }
+      }
+      if (dok && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f && fabsf(o[4]) < 128.0f) {
+        const int qs = s1_swz(ly * snxi + lx);
+        const u32 old = atomicAdd(&sm.cnt[qs], 1u);
+        if (((old + 1u) & (S1_CELL_FLUSH - 1u)) == 0u)
+          s1_cell_flush(dig, qs, flat, P.hkey, P.tab_sum, P.G, P.tab_cnt, P.occ, C);
+        o[0] = dx;
+        o[1] = dy;
+        s1_add(dig, qs, o_k[it]);
+      } else {
+        // outside the shared sub-window: exact fire-and-forget limb
+        // reductions straight to the cell's table slot
+        bool created;
+        const u32 slot = ht_insert(P, flat, created);
+        if (!inwin) P.pslot[j] = (u32)SUBW + slot;   // cell code of an outside cell
+        if (slot != HT_EMPTY) {
 #pragma unroll
-            for (int c = 0; c < 5; ++c) tab_add_f32(tab_ptr(P, c, slot), o[c]);
-            touch_cell(P, C, slot, 1u, created);
-          } else {
-            set_flag(C, PCS_FLAG_CAPACITY);
-          }
+          for (int c = 0; c < 5; ++c) tab_add_f32(tab_ptr(P, c, slot), o[c]);
+          touch_cell(P, C, slot, 1u, created);
+        } else {
+          set_flag(C, PCS_FLAG_CAPACITY);
         }
       }
     }
-    tile = nwarps + (int)__shfl_sync(0xffffffffu, tk, 0);
+    jb0 = jb1; je0 = je1;
+#pragma unroll
+    for (int it = 0; it < S1_IPT; ++it) src_k[it] = src1[it];
+    next_chunk(jb1, je1);
   }
   __syncthreads();
   if (t == 0 && atomicAdd(&C->s1_done, 1u) == gridDim.x - 1) {   // every ticket is drawn
