@@ -21,11 +21,20 @@
 namespace pcs {
 
 #ifndef PCS_S1_THREADS
-#define PCS_S1_THREADS 512
+#define PCS_S1_THREADS 256
+#endif
+#ifndef PCS_S1_DEEP
+#define PCS_S1_DEEP 1   // k_pc_step1: the next chunk's states in registers too
 #endif
 constexpr int S1_THREADS = PCS_S1_THREADS;     // 2 CTAs x 16 warps per SM; 64 registers
-constexpr int S1_CTAS_PER_SM = 2;
-constexpr int S1_IPT = 2;                      // particles per lane in flight
+#ifndef PCS_S1_CTAS
+#define PCS_S1_CTAS 2
+#endif
+#ifndef PCS_S1_IPT
+#define PCS_S1_IPT 3
+#endif
+constexpr int S1_CTAS_PER_SM = PCS_S1_CTAS;
+constexpr int S1_IPT = PCS_S1_IPT;             // particles per lane per chunk
 constexpr int S1_WARPS = S1_THREADS / 32;
 constexpr int S1_SIDE = 32;                    // sub-window side (cells)
 constexpr int SUBW = S1_SIDE * S1_SIDE;        // shared-memory sub-window cells
@@ -762,19 +771,37 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
   first_chunk((int)blockIdx.x * S1_WARPS + warp, jb0, je0);
   jb1 = jb0; je1 = je0; next_chunk(jb1, je1);
   int src_k[S1_IPT], src1[S1_IPT];
-  load_src(jb0, je0, src_k);
-  while (jb0 >= 0) {
-    load_src(jb1, je1, src1);   // the next chunk's ancestors (consumed next iteration)
-    float o_k[S1_IPT][5];
+  float o_k[S1_IPT][5];
+  auto load_states = [&](const int (&src)[S1_IPT], float (&o)[S1_IPT][5]) {
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {
-      const float* gp = sin + (src_k[it] >= 0 ? src_k[it] : 0);
+      const float* gp = sin + (src[it] >= 0 ? src[it] : 0);
 #pragma unroll
       for (int c = 0; c < 5; ++c) {
-        o_k[it][c] = (src_k[it] >= 0) ? __ldg(gp) : 0.0f;
+        o[it][c] = (src[it] >= 0) ? __ldg(gp) : 0.0f;
         gp += ld;
       }
     }
+  };
+  load_src(jb0, je0, src_k);
+#if PCS_S1_DEEP
+  load_states(src_k, o_k);
+  load_src(jb1, je1, src1);
+#endif
+  while (jb0 >= 0) {
+#if PCS_S1_DEEP
+    // the next chunk's states (its ancestors arrived during the last chunk)
+    // and the ancestors of the one after move while this chunk computes
+    float o_n[S1_IPT][5];
+    load_states(src1, o_n);
+    int jb2 = jb1, je2 = je1;
+    next_chunk(jb2, je2);
+    int src2[S1_IPT];
+    load_src(jb2, je2, src2);
+#else
+    load_src(jb1, je1, src1);   // the next chunk's ancestors (consumed next iteration)
+    load_states(src_k, o_k);
+#endif
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {
       if (src_k[it] < 0) continue;
@@ -835,9 +862,20 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
       }
     }
     jb0 = jb1; je0 = je1;
+#if PCS_S1_DEEP
+    jb1 = jb2; je1 = je2;
+#pragma unroll
+    for (int it = 0; it < S1_IPT; ++it) {
+      src_k[it] = src1[it];
+      src1[it] = src2[it];
+#pragma unroll
+      for (int c = 0; c < 5; ++c) o_k[it][c] = o_n[it][c];
+    }
+#else
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) src_k[it] = src1[it];
     next_chunk(jb1, je1);
+#endif
   }
   __syncthreads();
   if (t == 0 && atomicAdd(&C->s1_done, 1u) == gridDim.x - 1) {   // every ticket is drawn
