@@ -1294,7 +1294,7 @@ __device__ __forceinline__ int lds_u32(u32 addr) {
 // (grid = SMs x occupancy, set by the host from the occupancy calculator).
 #ifndef PCS_RS_ITEMS
 #define PCS_RS_ITEMS 23   // 5888-particle tiles, 3 CTAs / SM (profiles/r2_variants.md)
-#define PCS_RS_SCAP 25
+#define PCS_RS_SCAP 23
 #endif
 constexpr int RS_ITEMS = PCS_RS_ITEMS;
 constexpr int RS_TILE = SCAN_BLOCK * RS_ITEMS;   // 5888
@@ -1363,6 +1363,7 @@ template <int KIND>
 struct RsSmem {
   typename RsElem<KIND>::T ring[2][RS_TILE];   // TMA ring (16-byte aligned)
   int stage[RS_STAGE];
+  u32 hist[KIND == 1 ? SUBW : 1];   // KIND 1 pass 1: members per sub-window cell (s1_swz order)
   int hp[KIND == 1 ? 1 : RS_TILE];   // run heads (KIND 1: in place of the consumed cell ids)
   u128 wtot[SCAN_BLOCK / 32];
   int s_wmax[SCAN_BLOCK / 32];
@@ -1441,15 +1442,48 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? PCS_RS_MINB : 2) k_sys
   };
   auto tile_items = [&](i64 tile) -> int { return (int)min((i64)RS_TILE, n - tile * RS_TILE); };
   // ---- pass 1: this CTA's exact total ----
+  // KIND 1: a histogram of the sub-window cell codes (one shared atomic per
+  // item, bank-swizzled), folded with the exact cell weights at the end;
+  // codes of cells outside the sub-window add their weight directly
   u128 acc = 0;
-  for (int L = 0; L < (mode == 2 ? 0 : mt); ++L) {   // (L0 == 0 here)
-    mbar_wait(&bar[L & 1], (u32)((L >> 1) & 1));
-    if (threadIdx.x == 0 && L + 1 < Lend) issue(L + 1);
-    const E* buf = ring[L & 1];
-    const int nv = tile_items(t0 + L);
+  if (KIND == 1 && mode != 2) {
+    u32* hist = sm.hist;
+    for (int q = threadIdx.x; q < SUBW; q += SCAN_BLOCK) hist[q] = 0;
+    __syncthreads();
+    for (int L = 0; L < mt; ++L) {
+      mbar_wait(&bar[L & 1], (u32)((L >> 1) & 1));
+      if (threadIdx.x == 0 && L + 1 < Lend) issue(L + 1);
+      const E* buf = ring[L & 1];
+      const int nv = tile_items(t0 + L);
+      const int kb = threadIdx.x * RS_ITEMS;
+      auto item = [&](int k) {
+        const u32 code = (u32)buf[k];
+        if (code < (u32)SUBW) atomicAdd(hist + s1_swz((int)code), 1u);
+        else acc += P.wfix[code - SUBW];
+      };
+      if (nv == RS_TILE) {
+#pragma unroll
+        for (int q = 0; q < RS_ITEMS; ++q) item(kb + q);
+      } else {
+        for (int q = 0; q < RS_ITEMS; ++q)
+          if (kb + q < nv) item(kb + q);
+      }
+      __syncthreads();   // buffer L & 1 is free for load L + 2
+    }
+    for (int q = threadIdx.x; q < SUBW; q += SCAN_BLOCK) {
+      const u32 c = hist[s1_swz(q)];
+      if (c) acc += P.wsub[q] * (u128)c;
+    }
+  } else {
+    for (int L = 0; L < (mode == 2 ? 0 : mt); ++L) {   // (L0 == 0 here)
+      mbar_wait(&bar[L & 1], (u32)((L >> 1) & 1));
+      if (threadIdx.x == 0 && L + 1 < Lend) issue(L + 1);
+      const E* buf = ring[L & 1];
+      const int nv = tile_items(t0 + L);
 #pragma unroll 5
-    for (int q = 0; q < RS_ITEMS; ++q) acc += weight(buf, threadIdx.x * RS_ITEMS + q, nv);
-    __syncthreads();   // buffer L & 1 is free for load L + 2
+      for (int q = 0; q < RS_ITEMS; ++q) acc += weight(buf, threadIdx.x * RS_ITEMS + q, nv);
+      __syncthreads();   // buffer L & 1 is free for load L + 2
+    }
   }
   if (mode != 2) {
     u128 v = acc;
@@ -1508,9 +1542,15 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? PCS_RS_MINB : 2) k_sys
     // local index of the globally last item (its run ends at slot ng), -1 if not here
     const i64 kl = ng - 1 - off - base;
     const int klast = (kl >= 0 && kl < nv) ? (int)kl : -1;
+    const bool full = (nv == RS_TILE);   // (every tile but the last: no per-item bounds)
     u128 tsum = 0;
+    if (full) {
+#pragma unroll
+      for (int q = 0; q < RS_ITEMS; ++q) tsum += weight(buf, k0 + q, RS_TILE + 1);
+    } else {
 #pragma unroll 5
-    for (int q = 0; q < RS_ITEMS; ++q) tsum += weight(buf, k0 + q, nv);
+      for (int q = 0; q < RS_ITEMS; ++q) tsum += weight(buf, k0 + q, nv);
+    }
     u128 inc = tsum;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
@@ -1550,17 +1590,27 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? PCS_RS_MINB : 2) k_sys
       }
       const u32 hp_s = smem_u32(hp + k0);
       if (!MULTI) {
+        if (full && klast < 0) {
 #pragma unroll
-        for (int q = 0; q < RS_ITEMS; ++q) {
-          const int k = k0 + q;
-          int h = -1;   // no slot
-          if (k < nv) {
-            run += weight(buf, k, nv);
-            const int jend = (k == klast) ? (int)(ng - tj0) : slot_rel(run, u, ng, nd, kappa, eps, tj0d, tj0);
-            if (jend > jr) h = jr;
+          for (int q = 0; q < RS_ITEMS; ++q) {
+            run += weight(buf, k0 + q, RS_TILE + 1);
+            const int jend = slot_rel(run, u, ng, nd, kappa, eps, tj0d, tj0);
+            sts_u32(hp_s + 4 * q, (jend > jr) ? jr : -1);   // (KIND 1: over item k, already read)
             jr = jend;
           }
-          sts_u32(hp_s + 4 * q, h);    // (KIND 1: over item k, already read)
+        } else {
+#pragma unroll
+          for (int q = 0; q < RS_ITEMS; ++q) {
+            const int k = k0 + q;
+            int h = -1;   // no slot
+            if (k < nv) {
+              run += weight(buf, k, nv);
+              const int jend = (k == klast) ? (int)(ng - tj0) : slot_rel(run, u, ng, nd, kappa, eps, tj0d, tj0);
+              if (jend > jr) h = jr;
+              jr = jend;
+            }
+            sts_u32(hp_s + 4 * q, h);    // (KIND 1: over item k, already read)
+          }
         }
         const u32 st_s = smem_u32(stage + threadIdx.x * RS_SCAP);
 #pragma unroll
