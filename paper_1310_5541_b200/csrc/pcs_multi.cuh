@@ -47,10 +47,12 @@ constexpr int MT_MAXM = 2048;                  // occupied cells per target per 
 constexpr int MT_STAGE = 4096;                 // staged frame pixels
 constexpr int MT_CI = 5;                       // phase C: items per thread (stride 5: conflict-free)
 constexpr int MT_CT = MT_THREADS * MT_CI;      // phase C: 2560 particles per scan tile
-// phase A digit accumulators: <= 2 additions per warp per tile and cell, each
-// < 2^18 (unsigned digits) / < 2^17 in magnitude (signed top digit), over at
-// most 256 tiles: 256 * 32 * 2^18 = 2^31 (n <= 262144 particles per target)
-constexpr int MT_MAX_TILES = 256;
+// phase A digit accumulators: one addition per particle of each digit of
+// V = round(v 2^40) (|V| < 2^47): bits 0-13, 14-27, 28-41 (< 2^14 each) and
+// V >> 42 (signed, |.| <= 2^5), so n <= 2^18 particles per target keep every
+// 32-bit accumulator in range
+constexpr int MT_MAX_TILES = 256;   // n <= MT_MAX_TILES * MT_TILE = 2^18
+constexpr int MT_DIG = 20;          // 5 components x 4 digits
 constexpr u64 MT_KEY_STEP = 0x9E3779B97F4A7C15ull;
 
 struct MtTarget {
@@ -100,22 +102,16 @@ struct MtParams {
 };
 
 struct MtSmem {
-  // phase A (same tile machinery as k_pc_step1: counting sort, lane-major
-  // sorted tile, warp-segmented run sums into 32-bit digit accumulators)
-  u32 dig[15][MT_SUBW];
+  // phase A (as k_pc_step1: every in-window particle adds its exact values
+  // to the cell's 32-bit digit accumulators with shared atomics; cells at
+  // s1_swz positions to spread a cloud over the banks)
+  u32 dig[MT_DIG][MT_SUBW];
   u32 acc_cnt[MT_SUBW];
-  u32 tile_cnt[MT_SUBW];
   u128 wfix_sub[MT_SUBW];          // exact cdf weight round(w 2^120) per sub-window cell
                                    // (prior frames: the cell log-likelihood, as double)
   float wsub_f[MT_SUBW];           // normalised weight per sub-window cell (wprev)
-  unsigned short tile_start[MT_SUBW];
   float ref[2 * MT_SIDE + 1];      // sub-window cell edges (x then y; NaN: unusable)
   union {
-    struct {                       // phase A: the cell-sorted tile
-      float pay[5][MT_TILE];
-      unsigned short pay_q[MT_TILE];
-      unsigned short list[MT_TILE];
-    } a;
     struct {                       // phase B: occupied cells, dummies, staged frame
       int occ[MT_MAXM];            // >= 0: sub-window cell, < 0: -(hash slot) - 1
       double ll[MT_MAXM];
@@ -127,7 +123,6 @@ struct MtSmem {
       int stage[MT_CT];
     } c;
   } u;
-  u32 n_list, n_in;
   int scan_tmp[MT_WARPS];
   i128 red[MT_WARPS * 6];
   long long lmax;
@@ -167,6 +162,24 @@ __device__ __forceinline__ bool mt_hash_add(MtHash* H, u32 flat, const float o[5
   return false;
 }
 
+// exact int128 value of component c of sub-window cell q (unswizzled index)
+__device__ __forceinline__ i128 mt_digits(const u32 (*dig)[MT_SUBW], int c, int q) {
+  const int qs = s1_swz(q);
+  return (i128)dig[4 * c][qs] + ((i128)dig[4 * c + 1][qs] << 14) + ((i128)dig[4 * c + 2][qs] << 28) +
+         ((i128)(int)dig[4 * c + 3][qs] << 42);
+}
+__device__ __forceinline__ void mt_add(u32 (*dig)[MT_SUBW], int qs, const float (&v)[5]) {
+#pragma unroll
+  for (int c = 0; c < 5; ++c) {
+    const long long V = __float2ll_rn(__fmul_rn(v[c], 1099511627776.0f));
+    const u32 lo = (u32)V;
+    atomicAdd(&dig[4 * c][qs], lo & 0x3FFFu);
+    atomicAdd(&dig[4 * c + 1][qs], (lo >> 14) & 0x3FFFu);
+    atomicAdd(&dig[4 * c + 2][qs], (u32)(V >> 28) & 0x3FFFu);
+    atomicAdd(&dig[4 * c + 3][qs], (u32)(V >> 42));
+  }
+}
+
 // GEN: ESS-threshold and / or multinomial resampling compiled in (the
 // every-frame systematic configuration runs the instantiation without them)
 template <int MAXS, bool GEN>
@@ -197,9 +210,8 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
   const i64 sy0 = min(max(cy - sny / 2, (i64)0), g.nrows - sny);
   for (int q = t; q < MT_SUBW; q += MT_THREADS) {
     sm.acc_cnt[q] = 0;
-    sm.tile_cnt[q] = 0;
 #pragma unroll
-    for (int p = 0; p < 15; ++p) sm.dig[p][q] = 0;
+    for (int p = 0; p < MT_DIG; ++p) sm.dig[p][q] = 0;
   }
   const int snxi = (int)snx, snyi = (int)sny;
   for (int q = t; q < snxi + snyi; q += MT_THREADS) {
@@ -214,7 +226,6 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
   const u32 ncols32 = (u32)g.ncols;
   const int sx0i = (int)sx0, sy0i = (int)sy0;
   if (t == 0) {
-    sm.n_list = 0;
     sm.n_occ = 0;
     sm.lmax = LLONG_MIN;
     sm.plmax = LLONG_MIN;
@@ -226,7 +237,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
   bool bad = false, hash_full = false;
   const i64 ntile = ceil_div(n, MT_TILE);
   for (i64 tile = 0; tile < ntile; ++tile) {
-    int q_k[MT_IPT], r_k[MT_IPT], src_k[MT_IPT];
+    int src_k[MT_IPT];
     float o_k[MT_IPT][5];
 #pragma unroll
     for (int it = 0; it < MT_IPT; ++it) {
@@ -242,7 +253,6 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     }
 #pragma unroll
     for (int it = 0; it < MT_IPT; ++it) {
-      q_k[it] = -1;
       i64 j = tile * MT_TILE + (i64)it * MT_THREADS + t;
       if (j >= n) continue;
       float s[5], z[5];
@@ -263,70 +273,17 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
           delta_exact(o[1], refy[ly], dy) && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f &&
           fabsf(o[4]) < 128.0f) {
         const int q = ly * snxi + lx;
-        const int r = (int)atomicAdd(&sm.tile_cnt[q], 1u);
-        if (r == 0) sm.u.a.list[atomicAdd(&sm.n_list, 1u)] = (unsigned short)q;
-        q_k[it] = q;
-        r_k[it] = r;
+        const int qs = s1_swz(q);
+        atomicAdd(&sm.acc_cnt[qs], 1u);
         o_k[it][0] = dx;
         o_k[it][1] = dy;
+        mt_add(sm.dig, qs, o_k[it]);
         P.pslot[base_i + j] = (u32)q;                 // phase C: sub-window cell
       } else {
         P.pslot[base_i + j] = 0x80000000u | flat;     // phase C: outlier (hash) cell
         if (!mt_hash_add(HT, flat, o)) hash_full = true;
       }
     }
-    __syncthreads();
-    // run offsets: exclusive scan of the tile's cell counts (MT_IPT entries / thread)
-    {
-      const int nl = (int)sm.n_list;
-      const int e0 = MT_IPT * t;
-      int loc[MT_IPT], sum = 0;
-#pragma unroll
-      for (int e = 0; e < MT_IPT; ++e) {
-        loc[e] = (e0 + e < nl) ? (int)sm.tile_cnt[sm.u.a.list[e0 + e]] : 0;
-        sum += loc[e];
-      }
-      int inc = sum;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        int o = __shfl_up_sync(0xffffffffu, inc, d);
-        if (lane >= d) inc += o;
-      }
-      if (lane == 31) sm.scan_tmp[warp] = inc;
-      __syncthreads();
-      if (t == 0) sm.n_list = 0;   // every thread has read n_list
-      int woff = (lane < warp) ? sm.scan_tmp[lane] : 0;
-#pragma unroll
-      for (int d = 16; d > 0; d >>= 1) woff += __shfl_xor_sync(0xffffffffu, woff, d);
-      int run = woff + inc - sum;
-#pragma unroll
-      for (int e = 0; e < MT_IPT; ++e) {
-        if (e0 + e < nl) {
-          const int q = sm.u.a.list[e0 + e];
-          sm.tile_start[q] = (unsigned short)run;
-          sm.tile_cnt[q] = 0;
-          sm.acc_cnt[q] += (u32)loc[e];
-        }
-        run += loc[e];
-      }
-      if (t == MT_THREADS - 1) sm.n_in = (u32)run;
-    }
-    __syncthreads();
-    // scatter into the lane-major sorted tile
-#pragma unroll
-    for (int it = 0; it < MT_IPT; ++it) {
-      if (q_k[it] < 0) continue;
-      const int pos = (int)sm.tile_start[q_k[it]] + r_k[it];
-      const int idx = (pos % MT_E) * MT_SUM_THREADS + pos / MT_E;   // lane-major for the sums
-#pragma unroll
-      for (int c = 0; c < 5; ++c) sm.u.a.pay[c][idx] = o_k[it][c];
-      sm.u.a.pay_q[idx] = (unsigned short)q_k[it];
-    }
-    __syncthreads();
-    if (t < MT_SUM_THREADS)   // 8 warps, 4 sorted particles per lane (as in k_pc_step1)
-      tile_run_sums<MT_SUM_THREADS, MT_E, MT_TILE, MT_SUBW>(sm.u.a.pay, sm.u.a.pay_q, (int)sm.n_in,
-                                                            &sm.dig[0][0], t);
-    // no barrier: the next tile's phase 1 touches none of pay / pay_q / n_in
   }
   __syncthreads();
   if (bad) atomicOr(&TG.flags, (u32)PCS_FLAG_NONFINITE);
@@ -334,7 +291,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
 
   // ---------------- phase B: occupied cells, dummies, likelihood ----------------
   for (int q = t; q < (int)(snx * sny); q += MT_THREADS) {
-    if (sm.acc_cnt[q]) {
+    if (sm.acc_cnt[s1_swz(q)]) {
       u32 idx = atomicAdd(&sm.n_occ, 1u);
       if (idx < (u32)MT_MAXM) sm.u.b.occ[idx] = q;
     }
@@ -359,12 +316,12 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     i128 S[3];
     i64 ix, iy;
     if (o >= 0) {
-      cnt = sm.acc_cnt[o];
+      cnt = sm.acc_cnt[s1_swz(o)];
       ix = sx0 + o % snx;
       iy = sy0 + o / snx;
-      S[0] = digits_value<MT_SUBW>(&sm.dig[0][0], 0, o) + (i128)cnt * f32_to_fixed(sm.ref[o % snxi], FX_STATE);
-      S[1] = digits_value<MT_SUBW>(&sm.dig[0][0], 1, o) + (i128)cnt * f32_to_fixed(refy[o / snxi], FX_STATE);
-      S[2] = digits_value<MT_SUBW>(&sm.dig[0][0], 4, o);
+      S[0] = mt_digits(sm.dig, 0, o) + (i128)cnt * f32_to_fixed(sm.ref[o % snxi], FX_STATE);
+      S[1] = mt_digits(sm.dig, 1, o) + (i128)cnt * f32_to_fixed(refy[o / snxi], FX_STATE);
+      S[2] = mt_digits(sm.dig, 4, o);
     } else {
       const MtHash& h = HT[-o - 1];
       cnt = h.cnt;
@@ -440,7 +397,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     i128 acc1[1] = {0};
     for (int b = t; b < M; b += MT_THREADS) {
       int o = sm.u.b.occ[b];
-      u32 cnt = (o >= 0) ? sm.acc_cnt[o] : HT[-o - 1].cnt;
+      u32 cnt = (o >= 0) ? sm.acc_cnt[s1_swz(o)] : HT[-o - 1].cnt;
       acc1[0] += (i128)cnt * f64_to_fixed(exp(__dsub_rn(sm.u.b.ll[b], m)), FX_S);
     }
     block_sum_i128_k<MT_THREADS, 1>(acc1, sm.red);
@@ -457,10 +414,10 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
       if (o >= 0) {
         sm.wfix_sub[o] = cdf_fixed(w);
         sm.wsub_f[o] = w;
-        cnt = sm.acc_cnt[o];
+        cnt = sm.acc_cnt[s1_swz(o)];
 #pragma unroll
         for (int c = 0; c < 5; ++c) {
-          i128 S = digits_value<MT_SUBW>(&sm.dig[0][0], c, o);
+          i128 S = mt_digits(sm.dig, c, o);
           if (c == 0) S += (i128)cnt * f32_to_fixed(sm.ref[o % snxi], FX_STATE);
           if (c == 1) S += (i128)cnt * f32_to_fixed(refy[o / snxi], FX_STATE);
           e[c] += wq * S;
