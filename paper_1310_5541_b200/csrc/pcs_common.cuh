@@ -218,6 +218,13 @@ __device__ __forceinline__ u128 shfl_up_u128(u128 v, int d) {
   return ((u128)hi << 64) | (u128)lo;
 }
 
+__device__ __forceinline__ u128 shfl_u128(u128 v, int src) {
+  u64 lo = (u64)v, hi = (u64)(v >> 64);
+  lo = __shfl_sync(0xffffffffu, lo, src);
+  hi = __shfl_sync(0xffffffffu, hi, src);
+  return ((u128)hi << 64) | (u128)lo;
+}
+
 // Order-preserving float <-> int mapping for deterministic atomicMax.
 __device__ __forceinline__ int float_to_ordered(float f) {
   int i = __float_as_int(f);

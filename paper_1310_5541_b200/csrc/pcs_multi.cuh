@@ -45,8 +45,8 @@ constexpr int MT_SUBW = MT_SIDE * MT_SIDE;     // sub-window cells (24 x 24)
 constexpr int MT_HCAP = 2048;                  // per-target outlier hash capacity
 constexpr int MT_MAXM = 2048;                  // occupied cells per target per frame
 constexpr int MT_STAGE = 4096;                 // staged frame pixels
-constexpr int MT_CI = 5;                       // phase C: items per thread (stride 5: conflict-free)
-constexpr int MT_CT = MT_THREADS * MT_CI;      // phase C: 2560 particles per scan tile
+constexpr int MT_CI = 9;                       // phase C: items per thread (odd stride: conflict-free)
+constexpr int MT_CT = MT_THREADS * MT_CI;      // phase C: 4608 particles per scan tile
 // phase A digit accumulators: one addition per particle of each digit of
 // V = round(v 2^40) (|V| < 2^47): bits 0-13, 14-27, 28-41 (< 2^14 each) and
 // V >> 42 (signed, |.| <= 2^5), so n <= 2^18 particles per target keep every
@@ -117,9 +117,8 @@ struct MtSmem {
       double ll[MT_MAXM];
       float dpix[MT_STAGE];
     } b;
-    struct {                       // phase C: staged cells, run heads, slot stage
-      u32 cells[MT_CT];
-      int hp[MT_CT];
+    struct {                       // phase C: staged cells (then each item's run head,
+      u32 cells[MT_CT];            // written over the item's consumed cell), slot stage
       int stage[MT_CT];
     } c;
   } u;
@@ -547,7 +546,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
   constexpr int CI = MT_CI;
   constexpr int CT = MT_CT;
   u32* cells = sm.u.c.cells;
-  int* hp = sm.u.c.hp;
+  int* hp = reinterpret_cast<int*>(sm.u.c.cells);   // item k's run head over its cell
   int* stage = sm.u.c.stage;
   const double nd = (double)n, eps = nd * 8.881784197001252e-16;   // n * 2^-50
   const double kappa = nd * 1.0842021724855044e-19;                  // n * 2^-63
@@ -569,6 +568,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     return (kk < nv) ? cdf_fixed(weight_from_ex(P.ll[base_i + base + kk], Sfr)) : (u128)0;
   };
   u128 pre = 0;
+  i64 tj_prev = 0;
   const int k0 = t * CI;
   for (i64 base = 0; base < n; base += CT) {
     if (!do_res) {
@@ -609,10 +609,17 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     }
     if (lane == 31) sm.wtot[warp] = inc;
     __syncthreads();
-    u128 woff = 0, tagg = 0;
-    for (int w = 0; w < MT_WARPS; ++w) {
-      if (w < warp) woff += sm.wtot[w];
-      tagg += sm.wtot[w];
+    u128 woff, tagg;
+    {   // every warp scans the MT_WARPS warp totals with shuffles (no extra barrier)
+      const u128 wv = (lane < MT_WARPS) ? sm.wtot[lane] : (u128)0;
+      u128 wi = wv;
+#pragma unroll
+      for (int d = 1; d < MT_WARPS; d <<= 1) {
+        const u128 o = shfl_up_u128(wi, d);
+        if (lane >= d) wi += o;
+      }
+      woff = shfl_u128(wi - wv, warp);
+      tagg = shfl_u128(wi, MT_WARPS - 1);
     }
     const u128 excl = pre + woff + (inc - tsum);
     const bool last_tile = base + CT >= n;
@@ -631,8 +638,9 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
       __syncthreads();   // (wtot is rewritten by the next tile)
       continue;
     }
-    const i64 tj0 = (base == 0) ? 0 : first_slot_fast(cdf_round(pre), u, n, nd, eps);
+    const i64 tj0 = tj_prev;   // a tile starts where the previous one ended
     const i64 tj1 = last_tile ? n : first_slot_fast(cdf_round(pre + tagg), u, n, nd, eps);
+    tj_prev = tj1;
     {
       const double tj0d = (double)tj0;
       int jr = 0;
