@@ -128,6 +128,7 @@ struct MtSmem {
   long long plmax;                 // prior frames: max per-particle log w
   int box[4];
   u32 n_occ;
+  int fast_delta;
   unsigned wmin, wmax;
   double Sf;
   u128 carry;
@@ -213,11 +214,17 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     for (int p = 0; p < MT_DIG; ++p) sm.dig[p][q] = 0;
   }
   const int snxi = (int)snx, snyi = (int)sny;
+  // fast_delta: every sub-window edge r is >= 2 l (l < 64), so x - r is exact
+  // for every x of the cell (Sterbenz) and needs no TwoSum check (k_pc_step1)
+  if (t == 0) sm.fast_delta = (g.lx < 64.0 && g.ly < 64.0) ? 1 : 0;
+  __syncthreads();
   for (int q = t; q < snxi + snyi; q += MT_THREADS) {
     bool ok;
     float r = (q < snxi) ? cell_ref32(g.ox, g.lx, sx0 + q, ok)
                          : cell_ref32(g.oy, g.ly, sy0 + (q - snxi), ok);
     sm.ref[q] = ok ? r : __int_as_float(0x7fc00000);
+    const double l2 = 2.0 * ((q < snxi) ? g.lx : g.ly);
+    if (!ok || !((double)r >= l2)) atomicAnd(&sm.fast_delta, 0);
   }
   const float* refy = sm.ref + snxi;
   const AxisFast axx = make_axis(g.ox, g.lx, P.inv_lx, g.ncols);
@@ -233,6 +240,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     sm.box[0] = INT_MAX; sm.box[1] = INT_MIN; sm.box[2] = INT_MAX; sm.box[3] = INT_MIN;
   }
   __syncthreads();
+  const bool fast_delta = sm.fast_delta != 0;
   bool bad = false, hash_full = false;
   const i64 ntile = ceil_div(n, MT_TILE);
   for (i64 tile = 0; tile < ntile; ++tile) {
@@ -268,9 +276,17 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
       const u32 flat = (u32)iy * ncols32 + (u32)ix;
       const int lx = ix - sx0i, ly = iy - sy0i;
       float dx, dy;
-      if ((u32)lx < (u32)snxi && (u32)ly < (u32)snyi && delta_exact(o[0], sm.ref[lx], dx) &&
-          delta_exact(o[1], refy[ly], dy) && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f &&
-          fabsf(o[4]) < 128.0f) {
+      bool dok = false;
+      if ((u32)lx < (u32)snxi && (u32)ly < (u32)snyi) {
+        if (fast_delta) {   // (CTA-uniform branch)
+          dx = __fsub_rn(o[0], sm.ref[lx]);
+          dy = __fsub_rn(o[1], refy[ly]);
+          dok = true;
+        } else {
+          dok = delta_exact(o[0], sm.ref[lx], dx) && delta_exact(o[1], refy[ly], dy);
+        }
+      }
+      if (dok && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f && fabsf(o[4]) < 128.0f) {
         const int q = ly * snxi + lx;
         const int qs = s1_swz(q);
         atomicAdd(&sm.acc_cnt[qs], 1u);
