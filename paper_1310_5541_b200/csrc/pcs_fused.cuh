@@ -1294,7 +1294,7 @@ __device__ __forceinline__ int lds_u32(u32 addr) {
 // (grid = SMs x occupancy, set by the host from the occupancy calculator).
 #ifndef PCS_RS_ITEMS
 #define PCS_RS_ITEMS 23   // 5888-particle tiles, 3 CTAs / SM (profiles/r2_variants.md)
-#define PCS_RS_SCAP 23
+#define PCS_RS_SCAP 25
 #endif
 constexpr int RS_ITEMS = PCS_RS_ITEMS;
 constexpr int RS_TILE = SCAN_BLOCK * RS_ITEMS;   // 5888
@@ -1362,8 +1362,7 @@ template <> struct RsElem<2> { typedef double T; };
 template <int KIND>
 struct RsSmem {
   typename RsElem<KIND>::T ring[2][RS_TILE];   // TMA ring (16-byte aligned)
-  int stage[RS_STAGE];
-  u32 hist[KIND == 1 ? SUBW : 1];   // KIND 1 pass 1: members per sub-window cell (s1_swz order)
+  int stage[RS_STAGE];              // (KIND 1 pass 1: the cell-code histogram, SUBW entries)
   int hp[KIND == 1 ? 1 : RS_TILE];   // run heads (KIND 1: in place of the consumed cell ids)
   u128 wtot[SCAN_BLOCK / 32];
   int s_wmax[SCAN_BLOCK / 32];
@@ -1447,7 +1446,8 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? PCS_RS_MINB : 2) k_sys
   // codes of cells outside the sub-window add their weight directly
   u128 acc = 0;
   if (KIND == 1 && mode != 2) {
-    u32* hist = sm.hist;
+    static_assert(RS_STAGE >= SUBW, "the pass-1 histogram lives in the emission stage");
+    u32* hist = reinterpret_cast<u32*>(sm.stage);
     for (int q = threadIdx.x; q < SUBW; q += SCAN_BLOCK) hist[q] = 0;
     __syncthreads();
     for (int L = 0; L < mt; ++L) {
