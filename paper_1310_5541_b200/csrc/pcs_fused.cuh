@@ -74,6 +74,11 @@ struct S1Smem {
   float ref[SUBW + 1];    // cell lower edges: x at [0, snx), y at [snx, snx + sny)
                           // (NaN: deltas from this edge may not be exact)
   int fast_delta;
+  // table pointers for the out-of-line cell flush (read only on that path)
+  u32* fl_hkey;
+  u64* fl_tab_sum;
+  u32* fl_occ;
+  i64 fl_G;
 };
 
 struct TrackCtl {
@@ -609,7 +614,7 @@ __device__ __forceinline__ i128 s1_digits(u32 d0, u32 d1, u32 d2) {
 // the accumulator, never in both), so no other warp has to stop. The count
 // and the cell-edge offsets stay for the final flush.
 __device__ __noinline__ void s1_cell_flush(u32* dig, int q, u32 flat, u32* hkey, u64* tab_sum, i64 G,
-                                           u32* tab_cnt, u32* occ, TrackCtl* C) {
+                                           u32* occ, TrackCtl* C) {
   i128 s[5];
 #pragma unroll
   for (int c = 0; c < 5; ++c) {
@@ -629,7 +634,6 @@ __device__ __noinline__ void s1_cell_flush(u32* dig, int q, u32 flat, u32* hkey,
     const u32 idx = atomicAdd(&C->n_occ, 1u);
     if (idx < (u32)MAXM) occ[idx] = slot;
   }
-  (void)tab_cnt;
   atomicAdd(&C->s1_mid_flush, 1u);
 }
 
@@ -712,7 +716,13 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
   // fast_delta: every edge r of the sub-window is >= 2 l (and l < 64), so for
   // any x of the cell, r/2 <= x <= 2r and x - r is exact (Sterbenz) — no
   // TwoSum check per particle
-  if (t == 0) sm.fast_delta = (g.lx < 64.0 && g.ly < 64.0) ? 1 : 0;
+  if (t == 0) {
+    sm.fast_delta = (g.lx < 64.0 && g.ly < 64.0) ? 1 : 0;
+    sm.fl_hkey = P.hkey;
+    sm.fl_tab_sum = P.tab_sum;
+    sm.fl_occ = P.occ;
+    sm.fl_G = P.G;
+  }
   __syncthreads();
   for (int q = t; q < snxi + snyi; q += S1_THREADS) {
     bool ok;
@@ -772,15 +782,21 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
   jb1 = jb0; je1 = je0; next_chunk(jb1, je1);
   int src_k[S1_IPT], src1[S1_IPT];
   float o_k[S1_IPT][5];
+  // component base pointers (warp-uniform): one 64-bit offset per particle,
+  // no per-component pointer steps; an unused lane loads particle 0
+  const float* sinc[5];
+  float* soutc[5];
+#pragma unroll
+  for (int c = 0; c < 5; ++c) {
+    sinc[c] = sin + c * ld;
+    soutc[c] = sout + c * ld;
+  }
   auto load_states = [&](const int (&src)[S1_IPT], float (&o)[S1_IPT][5]) {
 #pragma unroll
     for (int it = 0; it < S1_IPT; ++it) {
-      const float* gp = sin + (src[it] >= 0 ? src[it] : 0);
+      const u32 sj = (u32)max(src[it], 0);
 #pragma unroll
-      for (int c = 0; c < 5; ++c) {
-        o[it][c] = (src[it] >= 0) ? __ldg(gp) : 0.0f;
-        gp += ld;
-      }
+      for (int c = 0; c < 5; ++c) o[it][c] = __ldg(sinc[c] + sj);
     }
   };
   load_src(jb0, je0, src_k);
@@ -812,14 +828,8 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
       philox_normals5k(P.pk, frame, (u64)(P.idx_off + j), z);
       float* o = o_k[it];
       propagate_one(s, z, P.dyn, o);
-      {
-        float* d = sout + j;
 #pragma unroll
-        for (int c = 0; c < 5; ++c) {
-          *d = o[c];
-          d += ld;
-        }
-      }
+      for (int c = 0; c < 5; ++c) soutc[c][(u32)j] = o[c];
       if (!(o[0] == o[0]) || !(o[1] == o[1])) bad = true;
       const int ix = cell_axis_hot<POW2>(o[0], axx);
       const int iy = cell_axis_hot<POW2>(o[1], axy);
@@ -842,7 +852,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
         const int qs = s1_swz(ly * snxi + lx);
         const u32 old = atomicAdd(&sm.cnt[qs], 1u);
         if (((old + 1u) & (S1_CELL_FLUSH - 1u)) == 0u)
-          s1_cell_flush(dig, qs, flat, P.hkey, P.tab_sum, P.G, P.tab_cnt, P.occ, C);
+          s1_cell_flush(dig, qs, flat, sm.fl_hkey, sm.fl_tab_sum, sm.fl_G, sm.fl_occ, C);
         o[0] = dx;
         o[1] = dy;
         s1_add(dig, qs, o_k[it]);
