@@ -135,6 +135,7 @@ struct TrackCtl {
 // cell-index constants of one grid axis (cell_axis_hot below)
 struct AxisFast {
   float o32, inv32, mt, ma, mb, fmax;
+  u32 imax;              // (u32)fmax
   double origin, cell, inv;
   i64 n;
 };
@@ -317,6 +318,7 @@ __host__ __device__ __forceinline__ AxisFast make_axis(double origin, double cel
     a.mb = (fabsf(a.o32) * fabsf(a.inv32) + 1.0f) * 9.5367431640625e-07f;
   }
   a.fmax = (float)(n - 1 < (i64)(1 << 24) ? n - 1 : (i64)(1 << 24));
+  a.imax = (u32)(n - 1 < (i64)(1 << 24) ? n - 1 : (i64)(1 << 24));
   a.origin = origin;
   a.cell = cell;
   a.inv = inv;
@@ -332,7 +334,10 @@ __device__ __forceinline__ int cell_axis_hot(float p, const AxisFast& a) {
   const float f32 = floorf(t32);
   const float fr32 = t32 - f32;
   if (POW2) {
-    if (fr32 != 0.0f && f32 >= 0.0f && f32 <= a.fmax) return __float2int_rz(f32);
+    // (floor as an integer; an integer quotient or a value outside [0, fmax]
+    // takes the float64 path)
+    const int i = __float2int_rd(t32);
+    if ((float)i != t32 && (u32)i <= a.imax) return i;
   } else {
     const float margin = fmaf(fabsf(t32), a.mt, fmaf(fabsf(p), a.ma, a.mb));
     if (fr32 > margin && fr32 < 1.0f - margin && f32 >= 0.0f && f32 <= a.fmax)
