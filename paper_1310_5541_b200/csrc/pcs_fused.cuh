@@ -834,14 +834,14 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
       float* o = o_k[it];
       propagate_one(s, z, P.dyn, o);
 #pragma unroll
-      for (int c = 0; c < 5; ++c) soutc[c][(u32)j] = o[c];
+      for (int c = 0; c < 5; ++c) __stcs(soutc[c] + (u32)j, o[c]);   // (read next frame: > L2)
       if (!(o[0] == o[0]) || !(o[1] == o[1])) bad = true;
       const int ix = cell_axis_hot<POW2>(o[0], axx);
       const int iy = cell_axis_hot<POW2>(o[1], axy);
       const u32 flat = (u32)iy * ncols32 + (u32)ix;   // G <= 2^32 - 1
       const int lx = ix - sx0i, ly = iy - sy0i;
       const bool inwin = (u32)lx < (u32)snxi && (u32)ly < (u32)snyi;
-      if (inwin) P.pslot[j] = (u32)(ly * snxi + lx);   // cell code (else: below)
+      if (inwin) __stcs(P.pslot + j, (u32)(ly * snxi + lx));   // cell code (else: below)
       float dx, dy;
       bool dok = false;
       if (inwin) {
@@ -866,7 +866,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
         // reductions straight to the cell's table slot
         bool created;
         const u32 slot = ht_insert(P, flat, created);
-        if (!inwin) P.pslot[j] = (u32)SUBW + slot;   // cell code of an outside cell
+        if (!inwin) __stcs(P.pslot + j, (u32)SUBW + slot);   // cell code of an outside cell
         if (slot != HT_EMPTY) {
 #pragma unroll
           for (int c = 0; c < 5; ++c) tab_add_f32(tab_ptr(P, c, slot), o[c]);
@@ -1687,7 +1687,7 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? PCS_RS_MINB : 2) k_sys
 #pragma unroll
         for (int q = 0; q < RS_SCAP; ++q) {
           const int k = (int)threadIdx.x + q * SCAN_BLOCK;
-          if (k < cm) dst[k] = ib + lds_u32(src_s + 4 * q * SCAN_BLOCK);
+          if (k < cm) __stcs(dst + k, ib + lds_u32(src_s + 4 * q * SCAN_BLOCK));   // (evict-first)
         }
       } else {
         for (int k = threadIdx.x; k < cm; k += SCAN_BLOCK) {
