@@ -488,100 +488,6 @@ __device__ __forceinline__ bool delta_exact(float v, float ref, float& s) {
   return err == 0.0f && fabsf(s) < 128.0f;
 }
 
-// add an exact run sum (|S| < 2^55) to the three 32-bit digit accumulators of
-// cell q: bits 0-17 and 18-35 (unsigned) and S >> 36 (signed); dig is
-// [15][STRIDE], component c at rows 3c .. 3c+2
-template <int STRIDE>
-__device__ __forceinline__ void digits_add(u32* dig, int q, const long long S[5]) {
-#pragma unroll
-  for (int c = 0; c < 5; ++c) {
-    atomicAdd(&dig[(3 * c) * STRIDE + q], (u32)S[c] & 0x3FFFFu);
-    atomicAdd(&dig[(3 * c + 1) * STRIDE + q], (u32)(S[c] >> 18) & 0x3FFFFu);
-    atomicAdd(&dig[(3 * c + 2) * STRIDE + q], (u32)(int)(S[c] >> 36));
-  }
-}
-
-// the exact int128 value of digit accumulator (component c, cell q)
-template <int STRIDE>
-__device__ __forceinline__ i128 digits_value(const u32* dig, int c, int q) {
-  return (i128)dig[(3 * c) * STRIDE + q] + ((i128)dig[(3 * c + 1) * STRIDE + q] << 18) +
-         ((i128)(int)dig[(3 * c + 2) * STRIDE + q] << 36);
-}
-
-// Exact per-cell run sums of one cell-sorted tile (NSUM threads, E consecutive
-// sorted particles per lane, stored lane-major: element e of lane t at
-// pay[c][e * NSUM + t]). A warp-segmented scan joins runs that cross lanes;
-// one lane per (cell, warp) adds the run total to the digit accumulators.
-// Values are x - ref, y - ref, vx, vy, I0 with round(v 2^40) exact (checked
-// when the particle entered the tile).
-template <int NSUM, int E, int TILE, int STRIDE>
-__device__ __forceinline__ void tile_run_sums(const float (*pay)[TILE], const unsigned short* pay_q,
-                                              int ni, u32* dig, int t) {
-  const int lane = t & 31;
-  const int p0 = t * E;
-  int kf = 0xFFFF, kl = 0xFFFF;   // key of the first / last run piece
-  long long hf[5], tl[5];
-  bool split = false;             // a run ends inside this lane
-#pragma unroll
-  for (int c = 0; c < 5; ++c) hf[c] = tl[c] = 0;
-#pragma unroll
-  for (int e = 0; e < E; ++e) {
-    const int p = p0 + e;
-    if (p >= ni) break;
-    const int idx = e * NSUM + t;   // conflict-free (lane-major)
-    const int q = pay_q[idx];
-    long long v[5];
-#pragma unroll
-    for (int c = 0; c < 5; ++c) v[c] = __float2ll_rn(__fmul_rn(pay[c][idx], 1099511627776.0f));
-    if (e == 0) {
-      kf = kl = q;
-#pragma unroll
-      for (int c = 0; c < 5; ++c) tl[c] = v[c];
-    } else if (q == kl) {
-#pragma unroll
-      for (int c = 0; c < 5; ++c) tl[c] += v[c];
-    } else {
-      if (!split) {
-#pragma unroll
-        for (int c = 0; c < 5; ++c) hf[c] = tl[c];
-        split = true;
-      } else {
-        digits_add<STRIDE>(dig, kl, tl);   // a run entirely inside this lane
-      }
-      kl = q;
-#pragma unroll
-      for (int c = 0; c < 5; ++c) tl[c] = v[c];
-    }
-  }
-  // segmented inclusive scan of the last pieces across lanes
-  const int kprev = __shfl_up_sync(0xffffffffu, kl, 1);
-  bool flag = split || lane == 0 || kprev != kl || kl == 0xFFFF;
-  long long inc[5];
-#pragma unroll
-  for (int c = 0; c < 5; ++c) inc[c] = tl[c];
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const bool of = __shfl_up_sync(0xffffffffu, flag, d);
-#pragma unroll
-    for (int c = 0; c < 5; ++c) {
-      const long long ov = __shfl_up_sync(0xffffffffu, inc[c], d);
-      if (lane >= d && !flag) inc[c] += ov;
-    }
-    if (lane >= d) flag = flag || of;
-  }
-  // carry into the first piece (runs that started in earlier lanes)
-  long long carry[5];
-#pragma unroll
-  for (int c = 0; c < 5; ++c) carry[c] = __shfl_up_sync(0xffffffffu, inc[c], 1);
-  const int knext = __shfl_down_sync(0xffffffffu, kf, 1);
-  if (split) {
-    const bool join = lane > 0 && kprev == kf;
-#pragma unroll
-    for (int c = 0; c < 5; ++c) hf[c] += join ? carry[c] : 0ll;
-    digits_add<STRIDE>(dig, kf, hf);
-  }
-  if (kl != 0xFFFF && (lane == 31 || knext != kl)) digits_add<STRIDE>(dig, kl, inc);
-}
 
 // table slot of flat cell id `flat` in the hash-key array (ht_insert without
 // the TrackParams, for the out-of-line cell flush)

@@ -37,8 +37,6 @@ namespace pcs {
 constexpr int MT_THREADS = 512;
 constexpr int MT_IPT = 2;
 constexpr int MT_TILE = MT_THREADS * MT_IPT;   // 1024
-constexpr int MT_E = 4;                        // sorted particles per lane in the run sums
-constexpr int MT_SUM_THREADS = MT_TILE / MT_E; // 256
 constexpr int MT_WARPS = MT_THREADS / 32;
 constexpr int MT_SIDE = 24;
 constexpr int MT_SUBW = MT_SIDE * MT_SIDE;     // sub-window cells (24 x 24)
