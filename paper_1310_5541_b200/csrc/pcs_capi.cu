@@ -1327,6 +1327,7 @@ int pcs_mt_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t n_targets,
   P.grid = to_grid(&cfg->grid);
   P.inv_lx = 1.0 / P.grid.lx;
   P.inv_ly = 1.0 / P.grid.ly;
+  P.pow2 = grid_pow2(P.grid.ox, P.grid.lx, P.grid.oy, P.grid.ly) ? 1 : 0;
   P.seed = cfg->seed;
   P.tgt_off = target_offset;
   P.frame0 = cfg->frame0;

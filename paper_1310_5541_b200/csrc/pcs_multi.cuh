@@ -75,6 +75,7 @@ struct MtParams {
   Spot spot;
   Grid grid;
   double inv_lx, inv_ly;
+  int pow2;              // grid_pow2 of the grid (cell_axis_hot<true> applies)
   u64 seed;
   i64 tgt_off;           // global index of target 0 of this rank (RNG key)
   u32 frame0;
@@ -225,6 +226,10 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     if (!ok || !((double)r >= l2)) atomicAnd(&sm.fast_delta, 0);
   }
   const float* refy = sm.ref + snxi;
+  // the target's Philox round keys once per CTA (not per particle)
+  const PhiloxKey pk = philox_key(seed_t);
+  // power-of-two cells and float32-exact origins: the margin-free cell index
+  const bool pow2 = P.pow2 != 0;
   const AxisFast axx = make_axis(g.ox, g.lx, P.inv_lx, g.ncols);
   const AxisFast axy = make_axis(g.oy, g.ly, P.inv_ly, g.nrows);
   const u32 ncols32 = (u32)g.ncols;
@@ -263,14 +268,14 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
       float s[5], z[5];
 #pragma unroll
       for (int c = 0; c < 5; ++c) s[c] = o_k[it][c];
-      philox_normals5(seed_t, P.frame0 + (u32)k, (u64)j, z);
+      philox_normals5k(pk, P.frame0 + (u32)k, (u64)j, z);
       propagate_one(s, z, P.dyn, o_k[it]);
       const float* o = o_k[it];
 #pragma unroll
       for (int c = 0; c < 5; ++c) sout[c * ld + base_i + j] = o[c];
       if (!(o[0] == o[0]) || !(o[1] == o[1])) bad = true;
-      const int ix = cell_axis_hot<false>(o[0], axx);
-      const int iy = cell_axis_hot<false>(o[1], axy);
+      const int ix = pow2 ? cell_axis_hot<true>(o[0], axx) : cell_axis_hot<false>(o[0], axx);
+      const int iy = pow2 ? cell_axis_hot<true>(o[1], axy) : cell_axis_hot<false>(o[1], axy);
       const u32 flat = (u32)iy * ncols32 + (u32)ix;
       const int lx = ix - sx0i, ly = iy - sy0i;
       float dx, dy;
