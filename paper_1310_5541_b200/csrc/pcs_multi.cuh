@@ -65,8 +65,19 @@ struct MtTarget {
 struct MtHash {          // one outlier cell
   u32 key;               // flat cell + 1 (0 = empty)
   u32 cnt;
-  u64 sum[5][2];
+  u64 lim[5][3];         // exact sums as limbs: bits 0-31 and 32-63 (unsigned), the rest
+                         // (signed), added with fire-and-forget reductions (tab_add_f32)
+  u64 stash;             // phase B -> C: the cell's weight (float bits) or, with prior
+                         // weights, its log-likelihood (double bits)
 };
+// exact int128 sum of component c of an outlier cell
+__device__ __forceinline__ i128 mt_hash_sum(const MtHash& h, int c) {
+  return (i128)h.lim[c][0] + ((i128)h.lim[c][1] << 32) + ((i128)(long long)h.lim[c][2] << 64);
+}
+__device__ __forceinline__ void mt_hash_clear(MtHash& h) {
+#pragma unroll
+  for (int c = 0; c < 5; ++c) h.lim[c][0] = h.lim[c][1] = h.lim[c][2] = 0ull;
+}
 
 struct MtParams {
   i64 T, n, ld;          // targets on this rank, particles per target, SoA stride (= T*n)
@@ -144,16 +155,19 @@ __device__ __forceinline__ u32 mt_hash_find(const MtHash* H, u32 flat) {
   return s;
 }
 
-// exact int128 atomics into the target's outlier hash table
+// add a particle to the target's outlier hash table: the key by CAS (a plain
+// load first finds an existing key without an atomic round trip), the count
+// and the exact limbs with fire-and-forget reductions
 __device__ __forceinline__ bool mt_hash_add(MtHash* H, u32 flat, const float o[5]) {
   u32 key = flat + 1u;
   u32 s = mt_hash_slot(key);
   for (int probe = 0; probe < MT_HCAP; ++probe) {
-    u32 prev = atomicCAS(&H[s].key, 0u, key);
+    u32 prev = __ldcg(&H[s].key);
+    if (prev != key) prev = atomicCAS(&H[s].key, 0u, key);
     if (prev == 0u || prev == key) {
       atomicAdd(&H[s].cnt, 1u);
 #pragma unroll
-      for (int c = 0; c < 5; ++c) atomic_add_i128(H[s].sum[c], f32_to_fixed(o[c], FX_STATE));
+      for (int c = 0; c < 5; ++c) tab_add_f32(&H[s].lim[c][0], o[c]);
       return true;
     }
     s = (s + 1u) & (MT_HCAP - 1);
@@ -345,9 +359,9 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
       cnt = h.cnt;
       ix = (i64)(h.key - 1u) % g.ncols;
       iy = (i64)(h.key - 1u) / g.ncols;
-      S[0] = load_i128(h.sum[0]);
-      S[1] = load_i128(h.sum[1]);
-      S[2] = load_i128(h.sum[4]);
+      S[0] = mt_hash_sum(h, 0);
+      S[1] = mt_hash_sum(h, 1);
+      S[2] = mt_hash_sum(h, 4);
     }
     float d[3];
 #pragma unroll
@@ -446,11 +460,9 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
         // the sums are consumed: zero them for the next frame; the cell's
         // weight waits for phase C in sum[4][1] (cleared there)
 #pragma unroll
-        for (int c = 0; c < 5; ++c) e[c] += wq * load_i128(h.sum[c]);
-        h.sum[0][0] = 0; h.sum[0][1] = 0; h.sum[1][0] = 0; h.sum[1][1] = 0;
-        h.sum[2][0] = 0; h.sum[2][1] = 0; h.sum[3][0] = 0; h.sum[3][1] = 0;
-        h.sum[4][0] = 0;
-        h.sum[4][1] = (u64)__float_as_uint(w);
+        for (int c = 0; c < 5; ++c) e[c] += wq * mt_hash_sum(h, c);
+        mt_hash_clear(h);
+        h.stash = (u64)__float_as_uint(w);
       }
       e[5] += (i128)cnt * f64_to_fixed((double)w * (double)w, FX_W2);
     }
@@ -465,10 +477,8 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
         llsub[o] = llb;
       } else {
         MtHash& h = HT[-o - 1];
-        h.sum[0][0] = 0; h.sum[0][1] = 0; h.sum[1][0] = 0; h.sum[1][1] = 0;
-        h.sum[2][0] = 0; h.sum[2][1] = 0; h.sum[3][0] = 0; h.sum[3][1] = 0;
-        h.sum[4][0] = 0;
-        h.sum[4][1] = (u64)__double_as_longlong(llb);
+        mt_hash_clear(h);
+        h.stash = (u64)__double_as_longlong(llb);
       }
     }
     __syncthreads();
@@ -478,7 +488,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     for (i64 j = t; j < n; j += MT_THREADS) {
       const u32 code = P.pslot[base_i + j];
       const double llc = (code & 0x80000000u)
-                             ? __longlong_as_double((long long)HT[mt_hash_find(HT, code & 0x7FFFFFFFu)].sum[4][1])
+                             ? __longlong_as_double((long long)HT[mt_hash_find(HT, code & 0x7FFFFFFFu)].stash)
                              : llsub[code];
       const double ll = __dadd_rn(log((double)P.wprev[base_i + j]), llc);
       P.ll[base_i + j] = ll;
@@ -576,7 +586,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     const u32 key = (code & 0x7FFFFFFFu) + 1u;
     u32 s = mt_hash_slot(key);
     for (int probe = 0; probe < MT_HCAP; ++probe) {
-      if (HT[s].key == key) return cdf_fixed(__uint_as_float((u32)HT[s].sum[4][1]));
+      if (HT[s].key == key) return cdf_fixed(__uint_as_float((u32)HT[s].stash));
       s = (s + 1u) & (MT_HCAP - 1);
     }
     return 0;
@@ -602,7 +612,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
             } else {
               const u32 code = P.pslot[base_i + i];
               w = (code & 0x80000000u)
-                      ? __uint_as_float((u32)HT[mt_hash_find(HT, code & 0x7FFFFFFFu)].sum[4][1])
+                      ? __uint_as_float((u32)HT[mt_hash_find(HT, code & 0x7FFFFFFFu)].stash)
                       : sm.wsub_f[code];
             }
             P.wprev[base_i + i] = w;
@@ -749,7 +759,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     if (HT[s].key) {
       HT[s].key = 0u;
       HT[s].cnt = 0u;
-      HT[s].sum[4][1] = 0ull;
+      HT[s].stash = 0ull;
     }
   }
 }
