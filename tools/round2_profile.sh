@@ -19,7 +19,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 300 --c
 SARGS="--workload c5 --n 16777216 --steps 3 --warmup 3 --no-variants --no-cpu-baseline"
 timeout 600 python bench.py $SARGS > gpurun_out/plain_${TAG}_c5s.log 2>&1 && \
 timeout 1500 ncu --set full --clock-control none --import-source on \
-  -k "regex:k_pc_step1|k_sys_resample|k_pc_cells|k_pc_bins" -s 12 -c 4 \
+  -k "regex:k_pc_step1|k_sys_resample|k_pc_cells|k_pc_bins" -s 24 -c 4 \
   -o gpurun_out/prof_${TAG}_c5s python bench.py $SARGS > gpurun_out/ncu_full_${TAG}.log 2>&1
 echo ncu_rc=$?
 for w in c5 c1 c2 c3 c4 ref; do grep "^{" gpurun_out/bench_${TAG}_$w.log | tail -1 | cut -c1-300; done
