@@ -57,22 +57,28 @@ class BinGrid:
         return cls(origin_x=-0.5, origin_y=-0.5, cell_width=size, cell_height=size,
                    n_cols=width * cells_per_pixel, n_rows=height * cells_per_pixel)
 
+    def _axis(self, axis):
+        return ((self.origin_x, self.cell_width, self.n_cols) if axis == 0
+                else (self.origin_y, self.cell_height, self.n_rows))
+
     def cell_indices(self, xs, ys):
-        """Column/row indices for coordinate arrays, clamped to the extent (host helper)."""
-        ix = np.floor((np.asarray(xs) - self.origin_x) / self.cell_width)
-        iy = np.floor((np.asarray(ys) - self.origin_y) / self.cell_height)
-        ix = np.clip(ix, 0, self.n_cols - 1).astype(np.int64)
-        iy = np.clip(iy, 0, self.n_rows - 1).astype(np.int64)
-        return ix, iy
+        """Column/row indices for coordinate arrays, clamped to the extent
+        (host helper; the device path is pcs_common.cuh cell_axis)."""
+        out = []
+        for axis, v in ((0, xs), (1, ys)):
+            o, size, n = self._axis(axis)
+            k = np.floor((np.asarray(v) - o) / size)
+            out.append(np.clip(k, 0, n - 1).astype(np.int64))
+        return tuple(out)
 
     def cell_center(self, ix, iy):
-        return (self.origin_x + (ix + 0.5) * self.cell_width,
-                self.origin_y + (iy + 0.5) * self.cell_height)
+        (ox, sx, _), (oy, sy, _) = self._axis(0), self._axis(1)
+        return ox + (ix + 0.5) * sx, oy + (iy + 0.5) * sy
 
     def cell_bounds(self, ix, iy):
-        x_lo = self.origin_x + ix * self.cell_width
-        y_lo = self.origin_y + iy * self.cell_height
-        return x_lo, x_lo + self.cell_width, y_lo, y_lo + self.cell_height
+        (ox, sx, _), (oy, sy, _) = self._axis(0), self._axis(1)
+        left, bottom = ox + ix * sx, oy + iy * sy
+        return left, left + sx, bottom, bottom + sy
 
     def to_c(self):
         return _lib.PcsGrid(float(self.origin_x), float(self.origin_y), float(self.cell_width),
@@ -143,10 +149,11 @@ def _partition(states, grid: BinGrid):
 def assign_bins(pset: ParticleSet, grid: BinGrid) -> BinOccupancy:
     """Partition the particles of a set by spatial cell (binning.py:115-126)."""
     _, order, unique, starts, counts = _partition(pset.soa, grid)
+    ends = starts + counts
     members = {}
-    for u, s, c in zip(unique, starts, counts):
-        key = (int(u % grid.n_cols), int(u // grid.n_cols))
-        members[key] = order[s:s + c]
+    for flat, lo, hi in zip(unique.tolist(), starts.tolist(), ends.tolist()):
+        row, col = divmod(flat, grid.n_cols)
+        members[(col, row)] = order[lo:hi]
     return BinOccupancy(members=members, dummies={})
 
 

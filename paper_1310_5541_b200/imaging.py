@@ -92,26 +92,26 @@ class LikelihoodParams:
 
 def render_object(pos, i0, psf: PsfParams, at) -> float:
     """Ideal intensity of a spot at ``pos`` evaluated at ``at`` (imaging.py:83-92)."""
-    x0, y0 = pos
-    x, y = at
-    r_sq = (x - x0) ** 2 + (y - y0) ** 2
-    return i0 * math.exp(-r_sq / (2.0 * psf.sigma_psf ** 2)) + psf.i_bg
+    dx, dy = at[0] - pos[0], at[1] - pos[1]
+    return psf.i_bg + i0 * math.exp(-(dx * dx + dy * dy) / (2.0 * psf.sigma_psf ** 2))
+
+
+def _clamped_span(coord, halfwidth, extent):
+    """Inclusive [lo, hi] of the pixels within ``halfwidth`` of the pixel
+    nearest to ``coord``, clamped into [0, extent - 1] (never empty)."""
+    centre = int(np.floor(coord + 0.5))
+    last = extent - 1
+    return (min(max(centre - halfwidth, 0), last), min(max(centre + halfwidth, 0), last))
 
 
 def window_bounds(frame: ImageFrame, x, y, halfwidth):
     """Clamped window (x_lo, x_hi, y_lo, y_hi), inclusive, never empty (imaging.py:95-103)."""
-    cx = int(np.floor(x + 0.5))
-    cy = int(np.floor(y + 0.5))
-    x_lo = min(max(cx - halfwidth, 0), frame.width - 1)
-    x_hi = min(max(cx + halfwidth, 0), frame.width - 1)
-    y_lo = min(max(cy - halfwidth, 0), frame.height - 1)
-    y_hi = min(max(cy + halfwidth, 0), frame.height - 1)
-    return x_lo, x_hi, y_lo, y_hi
+    return (*_clamped_span(x, halfwidth, frame.width), *_clamped_span(y, halfwidth, frame.height))
 
 
 def window_pixel_count(frame: ImageFrame, x, y, halfwidth) -> int:
     x_lo, x_hi, y_lo, y_hi = window_bounds(frame, x, y, halfwidth)
-    return (x_hi - x_lo + 1) * (y_hi - y_lo + 1)
+    return (1 + x_hi - x_lo) * (1 + y_hi - y_lo)
 
 
 class _DeviceLikelihood:
