@@ -260,14 +260,14 @@ const char* pcs_track_kernel_name(pcs_ctx* ctx, int32_t i);
 /* phase timestamps (globaltimer ns) recorded by the fused bins kernel */
 int pcs_track_debug(pcs_ctx* ctx, int64_t* out16, void* stream);
 /* launch geometry of the fused loop and which of its size-dependent code
- * paths ran (out[n], n >= 12): [0] step-1 CTAs, [1] step-1 tile, [2] step-1
- * tiles per CTA (mean, rounded up), [3] resampler CTAs, [4] resampler tiles
- * per CTA (max; >= 2 runs the TMA ring past its first buffer pair; 1 for the
- * one-tile small form), [5] SIR likelihood chunk (0: grid stride), [6]
- * step-1 mid-loop digit flushes so far (device), [7] most occupied cells of a
- * frame so far (device), [8] bins cells held in shared memory (more spill to
- * global scratch), [9] step-1 tiles between flushes, [10] SIR likelihood
- * CTAs, [11] launches per frame. Synchronises the stream. */
+ * paths ran (out[n], n >= 12): [0] step-1 CTAs, [1] step-1 warp tile
+ * (particles), [2] step-1 warp tiles per warp (mean, rounded up), [3]
+ * resampler CTAs, [4] resampler tiles per CTA (max; >= 2 runs the TMA ring
+ * past its first buffer pair; 1 for the one-tile small form), [5] SIR
+ * likelihood chunk (0: grid stride), [6] step-1 per-cell exchange flushes so
+ * far (device), [7] most occupied cells of a frame so far (device), [8] cells
+ * capacity of the fused loop, [9] step-1 per-cell flush period (members), [10]
+ * SIR likelihood CTAs, [11] launches per frame. Synchronises the stream. */
 int pcs_track_info(pcs_ctx* ctx, int64_t* out, int32_t n, void* stream);
 /* kernel launches per fused step (for gpu_launches accounting) */
 int pcs_track_launches_per_step(pcs_ctx* ctx);

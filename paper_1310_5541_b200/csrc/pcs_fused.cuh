@@ -128,7 +128,7 @@ struct TrackCtl {
   i64 frame_occ;             // pcSIR with prior weights: occupied cells of the frame
   i64 k_end;                 // frame index one past the last output row of this batch
   i64 cell_max_ord;          // pcSIR: ordered-int64 max cell log-likelihood (k_pc_cells)
-  u32 s1_mid_flush;          // diagnostics: step-1 mid-loop digit flushes (pcs_track_info)
+  u32 s1_mid_flush;          // diagnostics: step-1 per-cell exchange flushes (pcs_track_info)
   u32 max_occ;               // diagnostics: most occupied cells of a frame
 };
 

@@ -4,9 +4,9 @@
 // One CTA owns one target for a whole frame and runs the complete pcsir_track
 // step (binning.py:175-195 + filtering.py:148-173) for that target with
 // block-level synchronisation only:
-//   A  gather + propagate + cell index + exact per-cell sums (tile counting
-//      sort into a shared-memory sub-window; rare outliers into a per-target
-//      HBM hash table with exact int128 atomics)
+//   A  gather + propagate + cell index + exact per-cell sums (32-bit shared
+//      atomics into a shared-memory sub-window; outliers into a per-target
+//      HBM hash table with exact limb reductions)
 //   B  occupied cells -> dummies -> likelihood (frame region staged in shared
 //      memory) -> exact normaliser -> per-cell weights, estimate, ESS, decision
 //   C  exact-prefix systematic resampling over the target's particles (tiles
