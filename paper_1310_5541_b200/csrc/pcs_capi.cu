@@ -955,7 +955,9 @@ static int track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int6
                        void* stream) {
   PCS_CHECK_ARG(ctx && cfg, "bad arguments");
   PCS_CHECK_ARG(cfg->method == 0 || cfg->method == 1, "method must be 0 (SIR) or 1 (pcSIR)");
-  PCS_CHECK_ARG(cfg->n_particles >= 1 && cfg->n_particles < INT_MAX, "n_particles out of range");
+  // (32-bit particle indices in the fused kernels, with a chunk of headroom)
+  PCS_CHECK_ARG(cfg->n_particles >= 1 && cfg->n_particles <= (i64)INT_MAX - 4096,
+                "n_particles out of range");
   PCS_CHECK_ARG(H >= 1 && W >= 1, "bad frame shape");
   int r = check_spot(&cfg->spot);
   if (r) return r;
