@@ -55,9 +55,11 @@ constexpr u32 HT_CAP = 1u << HT_BITS;
 constexpr u32 HT_EMPTY = 0xFFFFFFFFu;
 constexpr int MAXM = 1 << 20;                  // occupied cells per frame (fused)
 
-// k_pc_step1 (two 512-thread CTAs per SM): every warp runs its own tiles of
-// particles, 2 per lane at a time — gather, propagate, cell — and adds each
-// particle that lands in the frame's 32x32-cell shared-memory sub-window to
+// k_pc_step1 (two 256-thread CTAs per SM, 3 particles per lane per chunk, the
+// next chunk's ancestors and states loaded while the current one computes):
+// every warp runs its own tiles of particles — gather, propagate, cell — and
+// adds each particle that lands in the frame's 32x32-cell shared-memory
+// sub-window (cells at bank-swizzled slots, s1_swz) to
 // that cell's exact fixed-point sums with native 32-bit shared atomics: the
 // int64 value V = round(v 2^40) of each component goes into three 32-bit
 // digit accumulators (bits 0-15, 16-31, V >> 32). There are no CTA barriers
