@@ -11,18 +11,19 @@ def raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                          text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    return rows[0], rows[2:]
+    return rows[0], rows[1], rows[2:]   # names, units, one row per launch
 
 
 def main(rep):
-    hdr, rows = raw(rep)
+    hdr, units, rows = raw(rep)
+    unit = dict(zip(hdr, units))
     for v in rows:
         d = dict(zip(hdr, v))
         name = d.get("Kernel Name", "?")[:70]
         def g(k, default="n/a"):
             return d.get(k, default)
         print(f"== {name}")
-        for k, lab in [("gpu__time_duration.sum", "duration (us)"),
+        for k, lab in [("gpu__time_duration.sum", "duration"),
                        ("dram__bytes_read.sum", "dram read"),
                        ("dram__bytes_write.sum", "dram write"),
                        ("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "dram %"),
@@ -33,7 +34,7 @@ def main(rep):
                        ("launch__registers_per_thread", "regs"),
                        ("launch__grid_size", "grid"), ("launch__block_size", "block"),
                        ("smsp__inst_executed.sum", "warp instr")]:
-            print(f"   {lab:16s} {g(k)} {hdr and ''}")
+            print(f"   {lab:16s} {g(k)} {unit.get(k, '')}")
         st = []
         for k in hdr:
             if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith(
