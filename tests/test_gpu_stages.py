@@ -141,13 +141,50 @@ def test_likelihood_exact_ones(cuda):
     assert np.isfinite(far) and far > 0
 
 
+def _poisson_term_mass(pix, xs, ys, i0s, sigma, bg, hw, model):
+    """Per evaluation, sum over the window pixels (a superset: +-(hw + 1)
+    around the rounded position, inside the frame) of |z log1p(mu/bg)| + |mu|
+    in float64 — the scale of the float32 SIR form's rounding error bound
+    (DESIGN.md §2)."""
+    from scipy.special import erf
+    h, w = pix.shape
+    offs = np.arange(-hw - 1, hw + 2)
+    out = np.empty(len(xs))
+    for k, (x, y, i0) in enumerate(zip(xs.astype(np.float64), ys.astype(np.float64),
+                                       i0s.astype(np.float64))):
+        px = np.round(x).astype(int) + offs
+        py = np.round(y).astype(int) + offs
+        px, py = px[(px >= 0) & (px < w)], py[(py >= 0) & (py < h)]
+
+        def axis(idx, p):
+            if model == 1:
+                c = np.sqrt(2.0) * sigma
+                return sigma * np.sqrt(np.pi / 2) * (erf((idx + 0.5 - p) / c) - erf((idx - 0.5 - p) / c))
+            sub = idx[:, None] - 0.375 + 0.25 * np.arange(4)[None, :] - p
+            return np.mean(np.exp(-sub ** 2 / (2 * sigma ** 2)), axis=1)
+
+        mu = i0 * np.outer(axis(py, y), axis(px, x))
+        z = pix[np.ix_(py, px)]
+        with np.errstate(invalid="ignore", divide="ignore"):
+            lz = np.where(mu / bg > -1.0, np.abs(z * np.log1p(mu / bg)), np.inf)
+        out[k] = np.sum(lz + np.abs(mu))
+    return out
+
+
+# float32 SIR Poisson form: |d log L| <= C 2^-24 sum_window (|z log1p(t)| + |mu|)
+# (DESIGN.md §2: t = mu/bg to <= 28 ulp, log1p_pos 2 ulp, fma / product 2 ulp,
+# a float32 row of <= 15 terms 14 ulp of its magnitude: 46 -> C = 64)
+SIR_POISSON_C = 64.0
+
+
 def test_poisson_loglik_matches_oracle(cuda):
     """R19 (config 3, builder-defined): the pcSIR per-cell form (float64,
     what the fused and general pcSIR paths evaluate for every dummy) meets
     |d log L| <= 1e-5 absolute against the float64 sub-pixel oracle; the
     per-particle SIR comparison form keeps float32 pixel terms (log L up to
-    ~200 nats; 225 float32 terms of up to ~60 each), measured within
-    4e-5 max(1, |log L|)."""
+    ~200 nats; 225 float32 terms of up to ~60 each) and meets the derived
+    per-window bound C 2^-24 sum |term scale|, which is also
+    within 4e-5 max(1, |log L|)."""
     rng = np.random.default_rng(3)
     pix = rng.poisson(spot_pixels(40.3, 38.8, 20.0, 1.5, 10.0, 96, 96)).astype(np.float64)
     n = 2000
@@ -166,6 +203,9 @@ def test_poisson_loglik_matches_oracle(cuda):
         assert np.max(np.abs(cells - ref)) <= LOGLIK_TOL, np.max(np.abs(cells - ref))
         fast = lik.loglik(soa, pc.ImageFrame(pix)).double().cpu().numpy()
         err = np.abs(fast - ref)
+        bound = SIR_POISSON_C * 2.0 ** -24 * _poisson_term_mass(pix, xs, ys, i0, 1.5, 10.0, 7, model)
+        print(f"R19 SIR {sub}: max |d log L| {err.max():.3g}, max err / bound {np.max(err / bound):.3g}")
+        assert np.all(err <= bound + 1e-12), np.max(err / (bound + 1e-300))
         assert np.max(err / np.maximum(1.0, np.abs(ref))) < 4e-5, np.max(err)
 
 
