@@ -1226,6 +1226,8 @@ constexpr int RS_TILE = SCAN_BLOCK * RS_ITEMS;   // 5888
 // the per-thread stride is bank-conflict free)
 constexpr int RS_SCAP = PCS_RS_SCAP;
 constexpr int RS_STAGE = SCAN_BLOCK * RS_SCAP;   // 6400
+constexpr int RS_KBITS = 13;                     // bits of a tile-local item index
+static_assert(RS_TILE <= (1 << RS_KBITS), "tagged run heads hold the item index in RS_KBITS bits");
 
 __device__ __forceinline__ void grid_barrier(TrackCtl* C, int nblocks) {
   __syncthreads();
@@ -1454,6 +1456,10 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? PCS_RS_MINB : 2) k_sys
   bool oob = false;
   const int k0 = (int)threadIdx.x * RS_ITEMS;
   i64 tj_prev = 0;
+  // nothing left in the stage (pass-1 histogram, an earlier launch) may pass
+  // for a tagged run head (ordered before the first heads by the first
+  // tile's barrier)
+  for (int q = threadIdx.x; q < RS_STAGE; q += SCAN_BLOCK) stage[q] = 0;
   for (int L = mt; L < 2 * mt; ++L) {
     const int LL = L - L0;   // load index in this launch
     mbar_wait(&bar[LL & 1], (u32)((LL >> 1) & 1));
@@ -1495,8 +1501,22 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? PCS_RS_MINB : 2) k_sys
     const i64 tj0 = tj_prev;
     const i64 tj1 = (klast == nv - 1) ? ng : first_slot_fast(cdf_round(pre + tagg), u, ng, nd, eps);
     tj_prev = tj1;
-    // run head of every item: its first slot relative to tj0, -1 if none
+    // A tile whose slots fit one emission chunk (almost every tile) scatters
+    // its run heads straight into the stage, tagged with the tile's ordinal
+    // in the upper bits: a tagged head is larger than anything an earlier
+    // tile left there, so the block max-scan needs no fill, and slot 0 of a
+    // tile always holds a head of this tile. A larger tile takes the chunked
+    // path: run head of every item in hp (its first slot relative to tj0, -1
+    // if none), then fill -> heads -> block max-scan per chunk.
+    const int m_slots = MULTI ? 0 : (int)(tj1 - tj0);   // <= ng < 2^31
+    const int tord = L - mt + 1;                          // 1, 2, ... within this launch
+    const bool direct = !MULTI && m_slots <= RS_STAGE && tord < (1 << (31 - RS_KBITS));   // (CTA-uniform)
     {
+      const u32 emit_s = smem_u32(stage);
+      const int tag = tord << RS_KBITS;
+      auto emit = [&](int j0, int j1, int k) {   // item k owns slots [j0, j1) of the tile
+        if (j1 > j0 && (u32)j0 < (u32)RS_STAGE) sts_u32(emit_s + 4 * j0, tag | k);
+      };
       const double tj0d = (double)tj0;
       int jr = 0;
       if (k0 < nv && off + base + k0 != 0) jr = slot_rel(excl, u, ng, nd, kappa, eps, tj0d, tj0);
@@ -1512,7 +1532,28 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? PCS_RS_MINB : 2) k_sys
         }
       }
       const u32 hp_s = smem_u32(hp + k0);
-      if (!MULTI) {
+      if (direct) {
+        if (full && klast < 0) {
+#pragma unroll
+          for (int q = 0; q < RS_ITEMS; ++q) {
+            run += weight(buf, k0 + q, RS_TILE + 1);
+            const int jend = slot_rel(run, u, ng, nd, kappa, eps, tj0d, tj0);
+            emit(jr, jend, k0 + q);
+            jr = jend;
+          }
+        } else {
+#pragma unroll 1
+          for (int q = 0; q < RS_ITEMS; ++q) {
+            const int k = k0 + q;
+            if (k < nv) {
+              run += weight(buf, k, nv);
+              const int jend = (k == klast) ? (int)(ng - tj0) : slot_rel(run, u, ng, nd, kappa, eps, tj0d, tj0);
+              emit(jr, jend, k);
+              jr = jend;
+            }
+          }
+        }
+      } else if (!MULTI) {
         if (full && klast < 0) {
 #pragma unroll
           for (int q = 0; q < RS_ITEMS; ++q) {
@@ -1544,48 +1585,54 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? PCS_RS_MINB : 2) k_sys
     // slots in chunks of RS_STAGE (one chunk for almost every tile): heads,
     // block max-scan, coalesced writes (multinomial: k_multinomial_emit draws
     // the slots)
-    const int m_slots = MULTI ? 0 : (int)(tj1 - tj0);   // <= ng < 2^31
     int carry = -1;
     const int ks0 = (int)threadIdx.x * RS_SCAP;          // this thread's stage positions
     const u32 stage_s = smem_u32(stage), hp_s = smem_u32(hp + k0), own_s = smem_u32(stage + ks0);
     for (int c0 = 0; c0 < m_slots; c0 += RS_STAGE) {
-      if (c0 > 0) {
+      int total = -1;
+      {
+        if (!direct) {
+          if (c0 > 0) {
 #pragma unroll
-        for (int q = 0; q < RS_SCAP; ++q) sts_u32(own_s + 4 * q, -1);
+            for (int q = 0; q < RS_SCAP; ++q) sts_u32(own_s + 4 * q, -1);
+            __syncthreads();
+          }
+#pragma unroll
+          for (int q = 0; q < RS_ITEMS; ++q) {
+            const u32 hr = (u32)(lds_u32(hp_s + 4 * q) - c0);   // no head: (u32)(-1 - c0) >= 2^31
+            if (hr < (u32)RS_STAGE) sts_u32(stage_s + 4 * hr, k0 + q);
+          }
+          __syncthreads();
+        }
+        int tmax = -1;
+#pragma unroll
+        for (int q = 0; q < RS_SCAP; ++q) tmax = max(tmax, lds_u32(own_s + 4 * q));
+        int incl = tmax;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const int o = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d) incl = max(incl, o);
+        }
+        if (lane == 31) s_wmax[wi] = incl;
+        int excl_l = __shfl_up_sync(0xffffffffu, incl, 1);
+        if (lane == 0) excl_l = -1;
+        __syncthreads();
+        int prev = carry;
+        total = carry;
+#pragma unroll
+        for (int w = 0; w < SCAN_BLOCK / 32; ++w) {
+          if (w < wi) prev = max(prev, s_wmax[w]);
+          total = max(total, s_wmax[w]);
+        }
+        int runm = max(prev, excl_l);
+#pragma unroll
+        for (int q = 0; q < RS_SCAP; ++q) {
+          runm = max(runm, lds_u32(own_s + 4 * q));
+          sts_u32(own_s + 4 * q, runm);
+        }
         __syncthreads();
       }
-#pragma unroll
-      for (int q = 0; q < RS_ITEMS; ++q) {
-        const u32 hr = (u32)(lds_u32(hp_s + 4 * q) - c0);   // no head: (u32)(-1 - c0) >= 2^31
-        if (hr < (u32)RS_STAGE) sts_u32(stage_s + 4 * hr, k0 + q);
-      }
-      __syncthreads();
-      int tmax = -1;
-#pragma unroll
-      for (int q = 0; q < RS_SCAP; ++q) tmax = max(tmax, lds_u32(own_s + 4 * q));
-      int incl = tmax;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const int o = __shfl_up_sync(0xffffffffu, incl, d);
-        if (lane >= d) incl = max(incl, o);
-      }
-      if (lane == 31) s_wmax[wi] = incl;
-      int excl_l = __shfl_up_sync(0xffffffffu, incl, 1);
-      if (lane == 0) excl_l = -1;
-      __syncthreads();
-      int prev = carry, total = carry;
-#pragma unroll
-      for (int w = 0; w < SCAN_BLOCK / 32; ++w) {
-        if (w < wi) prev = max(prev, s_wmax[w]);
-        total = max(total, s_wmax[w]);
-      }
-      int runm = max(prev, excl_l);
-#pragma unroll
-      for (int q = 0; q < RS_SCAP; ++q) {
-        runm = max(runm, lds_u32(own_s + 4 * q));
-        sts_u32(own_s + 4 * q, runm);
-      }
-      __syncthreads();
+      const int kmask = direct ? (1 << RS_KBITS) - 1 : -1;   // (chunked path: plain indices)
       const int cm = min(RS_STAGE, m_slots - c0);
       const i64 w0 = tj0 + c0 - lo;   // output position of the chunk's first slot
       const int ib = (int)base;
@@ -1595,12 +1642,12 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? PCS_RS_MINB : 2) k_sys
 #pragma unroll
         for (int q = 0; q < RS_SCAP; ++q) {
           const int k = (int)threadIdx.x + q * SCAN_BLOCK;
-          if (k < cm) __stcs(dst + k, ib + lds_u32(src_s + 4 * q * SCAN_BLOCK));   // (evict-first)
+          if (k < cm) __stcs(dst + k, ib + (lds_u32(src_s + 4 * q * SCAN_BLOCK) & kmask));   // (evict-first)
         }
       } else {
         for (int k = threadIdx.x; k < cm; k += SCAN_BLOCK) {
           const i64 kk = w0 + k;
-          if (kk >= 0 && kk < cap) P.anc_out[kk] = ib + stage[k];
+          if (kk >= 0 && kk < cap) P.anc_out[kk] = ib + (stage[k] & kmask);
           else oob = true;
         }
       }
