@@ -1047,7 +1047,9 @@ static int track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int6
       // keys, counts, then the float / exact cdf weights per slot
       PCS_CUDA_TRY(cudaMalloc(&ctx->tab_cnt, 2 * (size_t)HT_CAP * sizeof(u32)));
       PCS_CUDA_TRY(cudaMalloc(&ctx->tab_sum, 5 * (size_t)HT_CAP * (2 + TAB_LIMBS) * sizeof(u64)));
-      PCS_CUDA_TRY(cudaMalloc(&ctx->wtab, (size_t)HT_CAP * (sizeof(float) + sizeof(u128))));
+      // (the exact weights of the SUBW sub-window cells sit right in front of the
+      // per-slot ones: a particle's cell code indexes both, code_wfix)
+      PCS_CUDA_TRY(cudaMalloc(&ctx->wtab, (size_t)HT_CAP * (sizeof(float) + sizeof(u128)) + SUBW * sizeof(u128)));
       ctx->table_cells = HT_CAP;
       ctx->table_dirty = true;
     }
@@ -1060,14 +1062,14 @@ static int track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int6
       ctx->table_dirty = false;
     }
     // compact per-frame tables of the step-1 sub-window cells (pslot codes < SUBW)
-    PCS_SCRATCH(SL_TR_SUB, SUBW * (sizeof(u128) + sizeof(double) + sizeof(float)), P.wsub);
-    P.ltsub = (double*)(P.wsub + SUBW);
+    PCS_SCRATCH(SL_TR_SUB, SUBW * (sizeof(double) + sizeof(float)), P.ltsub);
     P.wtsub = (float*)(P.ltsub + SUBW);
+    P.wsub = (u128*)ctx->wtab;
     P.tab_cnt = ctx->tab_cnt;
     P.hkey = ctx->tab_cnt + HT_CAP;
     P.tab_sum = ctx->tab_sum;
     P.tab_lim = ctx->tab_sum + 5 * (size_t)HT_CAP * 2;
-    P.wfix = (u128*)ctx->wtab;
+    P.wfix = P.wsub + SUBW;
     P.wtab = (float*)(P.wfix + HT_CAP);
     P.occ = ctx->occ;
     T.bins.ll = (double*)(ctx->occ + MAXM);

@@ -189,7 +189,7 @@ struct TrackParams {
   double thresh;             // resample when ESS < thresh (= threshold_fraction * N)
   float* wprev;              // normalised prior weights when prior_nonuniform
   double* lltab;             // pcSIR with prior weights: [G] log-likelihood per cell
-  u128* wsub;                // [SUBW] wfix of the frame's step-1 sub-window cells (by code)
+  u128* wsub;                // [SUBW] wfix of the frame's step-1 sub-window cells (by code); == wfix - SUBW
   double* ltsub;             // [SUBW] lltab of the sub-window cells
   float* wtsub;              // [SUBW] wtab of the sub-window cells
   int method;                // 0 SIR, 1 pcSIR
@@ -207,8 +207,7 @@ struct TrackParams {
 // compact per-frame tables (16 KB for wsub, L1-resident), the others from the
 // full-grid tables.
 __device__ __forceinline__ u128 code_wfix(const TrackParams& P, u32 code) {
-  const u128* p = (code < (u32)SUBW) ? P.wsub + code : P.wfix + (code - (u32)SUBW);
-  return *p;   // one 16-byte load, no branch
+  return P.wsub[code];   // wfix == wsub + SUBW (pcs_track_begin): one 16-byte load, no select
 }
 __device__ __forceinline__ float code_wtab(const TrackParams& P, u32 code) {
   return code < (u32)SUBW ? P.wtsub[code] : P.wtab[code - SUBW];
