@@ -1386,8 +1386,34 @@ __global__ void __launch_bounds__(SCAN_BLOCK, KIND == 1 ? PCS_RS_MINB : 2) k_sys
         else acc += P.wfix[code - SUBW];
       };
       if (nv == RS_TILE) {
+        // warp-uniform: any cell outside the sub-window in this thread group's
+        // items (frame 0 of a track: the wide initial cloud)? then their
+        // table weights are fetched by independent predicated loads, not by
+        // a divergent load -> add chain per item
+        u32 codes[RS_ITEMS];
+        bool any_out = false;
 #pragma unroll
-        for (int q = 0; q < RS_ITEMS; ++q) item(kb + q);
+        for (int q = 0; q < RS_ITEMS; ++q) {
+          codes[q] = (u32)buf[kb + q];
+          any_out |= codes[q] >= (u32)SUBW;
+        }
+#pragma unroll
+        for (int q = 0; q < RS_ITEMS; ++q)
+          if (codes[q] < (u32)SUBW) atomicAdd(hist + s1_swz((int)codes[q]), 1u);
+        if (__any_sync(0xffffffffu, any_out)) {
+          constexpr int B = 6;   // loads in flight per thread
+#pragma unroll
+          for (int q0 = 0; q0 < RS_ITEMS; q0 += B) {
+            u128 wq[B];
+#pragma unroll
+            for (int q = 0; q < B; ++q) {
+              wq[q] = 0;
+              if (q0 + q < RS_ITEMS && codes[q0 + q] >= (u32)SUBW) wq[q] = P.wsub[codes[q0 + q]];
+            }
+#pragma unroll
+            for (int q = 0; q < B; ++q) acc += wq[q];
+          }
+        }
       } else {
         for (int q = 0; q < RS_ITEMS; ++q)
           if (kb + q < nv) item(kb + q);
