@@ -1371,7 +1371,7 @@ int pcs_mt_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t n_targets,
     h[t].first_bad = INT_MAX;
     h[t].evals = 0;
     h[t].prior = 0;
-    h[t].pad = 0;
+    h[t].span = 0;
     pcs_init_t init = cfg->init;
     for (int c = 0; c < 5; ++c) init.center[c] = centers[t * 5 + c];
     const u64 seed_t = cfg->seed + (u64)(target_offset + t) * MT_KEY_STEP;

@@ -34,12 +34,19 @@ namespace pcs {
 // sub-window is 24 x 24 cells (a c4 cloud spans a few pixels; cells outside
 // it go to the exact per-target hash), and the phase-A tile, the phase-B
 // cell arrays and the phase-C scan buffers share one union.
-constexpr int MT_THREADS = 512;
+#ifndef PCS_MT_THREADS
+#define PCS_MT_THREADS 512
+#endif
+constexpr int MT_THREADS = PCS_MT_THREADS;
 constexpr int MT_IPT = 2;
 constexpr int MT_TILE = MT_THREADS * MT_IPT;   // 1024
 constexpr int MT_WARPS = MT_THREADS / 32;
 constexpr int MT_SIDE = 24;
 constexpr int MT_SUBW = MT_SIDE * MT_SIDE;     // sub-window cells (24 x 24)
+#ifndef PCS_MT_MARGIN
+#define PCS_MT_MARGIN 3
+#endif
+constexpr int MT_MARGIN = PCS_MT_MARGIN;       // sub-window cells beyond the previous frame's span
 constexpr int MT_HCAP = 2048;                  // per-target outlier hash capacity
 constexpr int MT_MAXM = 2048;                  // occupied cells per target per frame
 constexpr int MT_STAGE = 4096;                 // staged frame pixels
@@ -59,7 +66,7 @@ struct MtTarget {
   int first_bad;
   i64 evals;
   int prior;             // this frame's particles carry prior weights (wprev)
-  int pad;
+  int span;              // extent (cells) of the previous frame's occupied cells, 0 = unknown
 };
 
 struct MtHash {          // one outlier cell
@@ -137,6 +144,7 @@ struct MtSmem {
   long long lmax;
   long long plmax;                 // prior frames: max per-particle log w
   int box[4];
+  int obox[4];                     // occupied cells' bounds relative to the sub-window origin
   u32 n_occ;
   int fast_delta;
   unsigned wmin, wmax;
@@ -216,7 +224,20 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
   MtHash* HT = P.hash + tg * MT_HCAP;
 
   // ---------------- phase A: propagate + exact per-cell sums -------------------
-  const i64 snx = min((i64)MT_SIDE, g.ncols), sny = min((i64)MT_SIDE, g.nrows);
+  // A compact cloud (the previous frame's occupied cells span <= side - 4
+  // cells) gets a smaller sub-window and `rep` replicas of its accumulators
+  // (replica = lane % rep, folded after the particle loop): at 1 px cells a
+  // warp's particles share ~10 cells and their shared atomics would
+  // serialise on those addresses. The sums are exact integers, so the result
+  // does not depend on the choice.
+  int side = MT_SIDE, rep = 1;
+  {
+    const int span = TG.span;
+    if (span > 0 && span + MT_MARGIN <= 6) { side = 6; rep = 16; }
+    else if (span > 0 && span + MT_MARGIN <= 8) { side = 8; rep = 8; }
+    else if (span > 0 && span + MT_MARGIN <= 12) { side = 12; rep = 4; }
+  }
+  const i64 snx = min((i64)side, g.ncols), sny = min((i64)side, g.nrows);
   const i64 cx = cell_axis_fast((float)TG.center[0], g.ox, g.lx, P.inv_lx, g.ncols);
   const i64 cy = cell_axis_fast((float)TG.center[1], g.oy, g.ly, P.inv_ly, g.nrows);
   const i64 sx0 = min(max(cx - snx / 2, (i64)0), g.ncols - snx);
@@ -255,9 +276,12 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     sm.wmin = 0xFFFFFFFFu;
     sm.wmax = 0u;
     sm.box[0] = INT_MAX; sm.box[1] = INT_MIN; sm.box[2] = INT_MAX; sm.box[3] = INT_MIN;
+    sm.obox[0] = INT_MAX; sm.obox[1] = INT_MIN; sm.obox[2] = INT_MAX; sm.obox[3] = INT_MIN;
   }
   __syncthreads();
   const bool fast_delta = sm.fast_delta != 0;
+  const int rstride = snxi * snyi;                  // rep * rstride <= MT_SUBW
+  const int roff = (lane & (rep - 1)) * rstride;    // this lane's replica
   bool bad = false, hash_full = false;
   const i64 ntile = ceil_div(n, MT_TILE);
   for (i64 tile = 0; tile < ntile; ++tile) {
@@ -305,7 +329,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
       }
       if (dok && fabsf(o[2]) < 128.0f && fabsf(o[3]) < 128.0f && fabsf(o[4]) < 128.0f) {
         const int q = ly * snxi + lx;
-        const int qs = s1_swz(q);
+        const int qs = s1_swz(q + roff);
         atomicAdd(&sm.acc_cnt[qs], 1u);
         o_k[it][0] = dx;
         o_k[it][1] = dy;
@@ -320,18 +344,43 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
   __syncthreads();
   if (bad) atomicOr(&TG.flags, (u32)PCS_FLAG_NONFINITE);
   if (hash_full) atomicOr(&TG.flags, (u32)PCS_FLAG_CAPACITY);
+  if (rep > 1) {   // fold the replicas into replica 0 (modulo 2^32, as the atomics)
+    for (int q = t; q < rstride; q += MT_THREADS) {
+      const int q0 = s1_swz(q);
+      for (int r = 1; r < rep; ++r) {
+        const int qi = s1_swz(q + r * rstride);
+        sm.acc_cnt[q0] += sm.acc_cnt[qi];
+#pragma unroll
+        for (int p = 0; p < MT_DIG; ++p) sm.dig[p][q0] += sm.dig[p][qi];
+      }
+    }
+    __syncthreads();
+  }
 
   // ---------------- phase B: occupied cells, dummies, likelihood ----------------
-  for (int q = t; q < (int)(snx * sny); q += MT_THREADS) {
-    if (sm.acc_cnt[s1_swz(q)]) {
-      u32 idx = atomicAdd(&sm.n_occ, 1u);
-      if (idx < (u32)MT_MAXM) sm.u.b.occ[idx] = q;
+  {
+    int ox0 = INT_MAX, ox1 = INT_MIN, oy0 = INT_MAX, oy1 = INT_MIN;
+    for (int q = t; q < (int)(snx * sny); q += MT_THREADS) {
+      if (sm.acc_cnt[s1_swz(q)]) {
+        u32 idx = atomicAdd(&sm.n_occ, 1u);
+        if (idx < (u32)MT_MAXM) sm.u.b.occ[idx] = q;
+        const int lx = q % snxi, ly = q / snxi;
+        ox0 = min(ox0, lx); ox1 = max(ox1, lx); oy0 = min(oy0, ly); oy1 = max(oy1, ly);
+      }
     }
-  }
-  for (int s = t; s < MT_HCAP; s += MT_THREADS) {
-    if (HT[s].key) {
-      u32 idx = atomicAdd(&sm.n_occ, 1u);
-      if (idx < (u32)MT_MAXM) sm.u.b.occ[idx] = -s - 1;
+    for (int s = t; s < MT_HCAP; s += MT_THREADS) {
+      const u32 key = HT[s].key;
+      if (key) {
+        u32 idx = atomicAdd(&sm.n_occ, 1u);
+        if (idx < (u32)MT_MAXM) sm.u.b.occ[idx] = -s - 1;
+        const i64 fl = (i64)(key - 1u);
+        const int lx = (int)(fl % g.ncols - sx0), ly = (int)(fl / g.ncols - sy0);
+        ox0 = min(ox0, lx); ox1 = max(ox1, lx); oy0 = min(oy0, ly); oy1 = max(oy1, ly);
+      }
+    }
+    if (ox0 <= ox1) {
+      atomicMin(&sm.obox[0], ox0); atomicMax(&sm.obox[1], ox1);
+      atomicMin(&sm.obox[2], oy0); atomicMax(&sm.obox[3], oy1);
     }
   }
   __syncthreads();
@@ -550,6 +599,8 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
       keep = 0;
     }
     TG.prior = keep;
+    TG.span = (sm.obox[0] <= sm.obox[1])
+                  ? max(sm.obox[1] - sm.obox[0], sm.obox[3] - sm.obox[2]) + 1 : 0;
     s_keep = keep;
     P.out_res[row] = (unsigned char)res;
     P.out_occ[row] = M;
