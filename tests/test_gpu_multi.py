@@ -116,3 +116,34 @@ def test_too_many_particles_per_target_rejected(cuda):
     frames, truth = mt.multi_target_scene(1, 1, 160, seed=6)
     with pytest.raises(Exception, match="too many particles per target"):
         mt.multi_pcsir_track(frames, _cfg(262_145), truth[:, 0].copy(), 1)
+
+
+@pytest.mark.parametrize("cpp,sigma_pos", [(1, 1.2), (2, 1.5), (1, 2.0)])
+def test_replicated_accumulators_with_outliers_equal_single_target(cuda, cpp, sigma_pos):
+    """Phase A picks a 6/8/12-cell sub-window with 16/8/4 accumulator replicas
+    from the previous frame's occupied span (pcs_multi.cuh). A large process
+    noise makes the resampled (compact) cloud spread past that window every
+    frame, so replicas and hashed outlier cells mix: the exact sums, hence
+    every output, still equal the single-target fused filter bit for bit."""
+    n, T, K = 4000, 6, 6
+    frames, truth = mt.multi_target_scene(T, K, 160, seed=5)
+    centers = truth[:, 0].copy()
+    dyn = pc.DynamicsParams(sigma_pos, 0.1, 1.0)
+    res = pc.ResampleConfig(1.0, "systematic")
+    grid = pc.BinGrid.pixel_aligned(160, 160, cpp)
+
+    def cfg(center):
+        return pc.PcFilterConfig(
+            n, pc.InitSpec(pc.StateVector(*center), "gauss", sigma=2.0), dyn, res,
+            pc.SpotLikelihood(pc.PsfParams(1.5, 10.0), pc.LikelihoodParams(10.0, 5)), grid=grid)
+
+    r = mt.multi_pcsir_track(frames, cfg((0, 0, 0, 0, 20.0)), centers, 17)
+    # wider than the 6 / 8-cell windows a compact posterior selects
+    assert int(r.occupied.max()) > (60 if cpp == 1 else 8)
+    for t in range(T):
+        single = pc.pcsir_track([pc.ImageFrame(f) for f in frames], cfg(centers[t]),
+                                pc.PhiloxRng(mt.target_seed(17, t)))
+        assert single.path == "fused"
+        assert np.array_equal(r.estimates[t], single.estimates), t
+        assert np.array_equal(r.ess[t], single.ess), t
+        assert int(r.likelihood_evals[t]) == single.likelihood_evals
