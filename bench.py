@@ -78,12 +78,13 @@ def lik_min_ops(model, hw):
 LIMITERS = {
     "k_pc_step1": ("instruction issue: ~9.2 warp instructions per particle at 60 % issue active "
                    "(16 warps/SM at 120 registers), Philox + Box-Muller ~2.8 of them; DRAM "
-                   "traffic ~= the algorithmic bytes (profiles/r4_c5s_ncu_summary.txt)"),
+                   "traffic ~= the algorithmic bytes (profiles/r5_c5s_ncu_summary.txt)"),
     "k_sys_resample": ("latency of pass 2 (u128 prefix -> slot -> run head chains, emission "
-                       "stage): ~3.3 warp instructions per particle, 45 % issue active "
-                       "(profiles/r4_c5s_ncu_summary.txt)"),
+                       "stage): ~2.75 warp instructions per particle, 42 % issue active "
+                       "(profiles/r5_c5s_ncu_summary.txt)"),
     "k_sir_propagate_lik": "FP32/SFU/XU pipes and latency of the per-pixel likelihood",
-    "k_mt_frame": "instruction issue (step-1 machinery per target, two CTAs per SM)",
+    "k_mt_frame": ("instruction issue and shared-atomic serialisation (step-1 machinery per "
+                   "target, two CTAs per SM; replicated accumulators for compact clouds)"),
 }
 
 
