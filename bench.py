@@ -430,7 +430,7 @@ def cpu_sample(wl_name, wl, frames_host, cpp, pool_cores=1):
         v, dt, kern = cpu_port_track(wl, wl["n"], frames_host[:nf], wl["start"], cpp)
         return v, 1, f"{nf} frames x N={wl['n']} ({kern}), {dt:.1f} s on 1 core"
     if wl_name in ("c3", "c5"):
-        n = 1_000_000 if wl_name == "c3" else 1 << 21
+        n = 1_000_000 if wl_name == "c3" else 1 << 23   # c5: ~8 s on one core
         v, dt, kern = cpu_port_track(wl, n, frames_host[:3], wl["start"], cpp)
         return v, 1, (f"3 frames x N={n} (1/{wl['n'] // n} of the config's N; particle-updates/s "
                       f"is per-particle so it scales with N) ({kern}), {dt:.1f} s on 1 core")
