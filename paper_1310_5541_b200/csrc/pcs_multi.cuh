@@ -47,6 +47,9 @@ constexpr int MT_SUBW = MT_SIDE * MT_SIDE;     // sub-window cells (24 x 24)
 #define PCS_MT_MARGIN 3
 #endif
 constexpr int MT_MARGIN = PCS_MT_MARGIN;       // sub-window cells beyond the previous frame's span
+#ifndef PCS_MT_PREFETCH
+#define PCS_MT_PREFETCH 1
+#endif
 constexpr int MT_HCAP = 2048;                  // per-target outlier hash capacity
 constexpr int MT_MAXM = 2048;                  // occupied cells per target per frame
 constexpr int MT_STAGE = 4096;                 // staged frame pixels
@@ -291,6 +294,12 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
     for (int it = 0; it < MT_IPT; ++it) {
       i64 j = tile * MT_TILE + (i64)it * MT_THREADS + t;
       src_k[it] = (j < n) ? __ldg(P.anc + base_i + j) : 0;
+#if PCS_MT_PREFETCH
+      // the next tile's ancestor indices on their way to L1 (the gather below
+      // waits on them first)
+      if (lane == 0 && j + MT_TILE < n)
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(P.anc + base_i + j + MT_TILE));
+#endif
     }
 #pragma unroll
     for (int it = 0; it < MT_IPT; ++it) {
