@@ -841,7 +841,9 @@ static void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 
 // Enqueue one frame. If evs is non-null, evs[i] is recorded before launch i
 // and evs[launches] after the last one (per-kernel CUDA-event timing).
-static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullptr) {
+// first: the track's first frame (step 1 queues the particles outside its sub-window)
+static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullptr,
+                         bool first = false) {
   TrackState& T = ctx->tr;
   TrackParams& P = T.P;
   int q = 0;
@@ -852,8 +854,13 @@ static int enqueue_frame(pcs_ctx* ctx, cudaStream_t st, cudaEvent_t* evs = nullp
   };
   if (T.cfg.method == 1) {
     mark("k_pc_step1");
-    if (T.s1_pow2) k_pc_step1<true><<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(P);
-    else k_pc_step1<false><<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(P);
+    if (first) {
+      if (T.s1_pow2) k_pc_step1<true, true><<<T.s1_grid, S1_THREADS, S1_SMEM_Q, st>>>(P);
+      else k_pc_step1<false, true><<<T.s1_grid, S1_THREADS, S1_SMEM_Q, st>>>(P);
+    } else {
+      if (T.s1_pow2) k_pc_step1<true><<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(P);
+      else k_pc_step1<false><<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(P);
+    }
     mark("k_pc_cells");
     launch_pdl(k_pc_cells, T.cells_grid, CELLS_BLOCK, 0, st, P, T.bins);
     mark("k_pc_bins");
@@ -917,6 +924,10 @@ static int set_attrs() {
                                     (int)S1_SMEM));
   PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_step1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)S1_SMEM));
+  PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_step1<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)S1_SMEM_Q));
+  PCS_CUDA_TRY(cudaFuncSetAttribute(k_pc_step1<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)S1_SMEM_Q));
   PCS_CUDA_TRY(cudaFuncSetAttribute(k_sys_resample<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)sizeof(RsSmem<1>)));
   PCS_CUDA_TRY(cudaFuncSetAttribute(k_sys_resample<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -928,6 +939,7 @@ static int set_attrs() {
   // one shared-memory carveout for every kernel of the frame: consecutive
   // kernels with different carveouts force an SM reconfiguration between them
   const void* fns[] = {(const void*)k_pc_step1<true>,  (const void*)k_pc_step1<false>,
+                       (const void*)k_pc_step1<true, true>, (const void*)k_pc_step1<false, true>,
                        (const void*)k_pc_bins,
                        (const void*)k_pc_cells,         (const void*)k_sir_propagate_lik<0>,
                        (const void*)k_sir_propagate_lik<9>, (const void*)k_sir_propagate_lik<11>,
@@ -1203,10 +1215,10 @@ int pcs_track_steps(pcs_ctx* ctx, const float* frames, int64_t k0, int64_t k1, d
   k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frames, k0, k0, k1, est, ess, res, (i64*)occ, fm);
   PCS_LAUNCH_CHECK();
   for (i64 k = k0; k < k1; ++k) {
-    if (T.exec) {
+    if (T.exec && k > 0) {
       PCS_CUDA_TRY(cudaGraphLaunch(T.exec, st));
-    } else {
-      int r = enqueue_frame(ctx, st);
+    } else {   // (the first frame of a track is launched directly: its own step-1 form)
+      int r = enqueue_frame(ctx, st, nullptr, k == 0);
       if (r) return r;
     }
   }
@@ -1232,7 +1244,7 @@ int pcs_track_steps_timed(pcs_ctx* ctx, const float* frames, int64_t k0, int64_t
   for (int i = 0; i < max_kernels; ++i) kernel_ms[i] = 0.0;
   int r = PCS_OK;
   for (i64 k = k0; k < k1 && r == PCS_OK; ++k) {
-    r = enqueue_frame(ctx, st, evs);
+    r = enqueue_frame(ctx, st, evs, k == 0);
     if (r) break;
     cudaError_t e = cudaEventSynchronize(evs[T.launches]);
     if (e != cudaSuccess) {

@@ -70,6 +70,7 @@ constexpr int MAXM = 1 << 20;                  // occupied cells per frame (fuse
 // Particles outside the sub-window add to the table directly (limb
 // reductions).
 constexpr int S1_CHUNK = 32 * S1_IPT;          // particles per warp pipeline step
+constexpr int S1_OQ = 32 + S1_CHUNK;           // queue entries per warp (< 32 left + one chunk)
 struct S1Smem {
   u32 dig[S1_PARTS][SUBW];
   u32 cnt[SUBW];          // in-window members of each cell (this CTA)
@@ -81,6 +82,14 @@ struct S1Smem {
   u64* fl_tab_sum;
   u32* fl_occ;
   i64 fl_G;
+};
+
+// k_pc_step1<., true> only (behind S1Smem in its dynamic shared memory): per-warp
+// queue of particles outside the sub-window (cell; particle index, bit 31:
+// its cell code is already written) and its length
+struct S1Queue {
+  u32 oq[S1_WARPS][S1_OQ][2];
+  u32 oqn[S1_WARPS];
 };
 
 struct TrackCtl {
@@ -592,10 +601,15 @@ __device__ __forceinline__ void s1_add(u32* dig, int q, const float (&v)[5]) {
   }
 }
 
-template <bool POW2>
+// QUEUE: the instantiation for the first frame of a track (the initial cloud
+// is usually wider than the sub-window): particles outside it are queued per
+// warp and handled 32 at a time; the steady-state instantiation handles the
+// few there are on the spot.
+template <bool POW2, bool QUEUE = false>
 __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackParams P) {
   extern __shared__ __align__(16) unsigned char s1_raw[];
   S1Smem& sm = *reinterpret_cast<S1Smem*>(s1_raw);
+  S1Queue& sq = *reinterpret_cast<S1Queue*>(s1_raw + (QUEUE ? sizeof(S1Smem) : 0));   // (QUEUE only)
   TrackCtl* C = P.ctl;
   pdl_trigger();
   if (C->flags & PCS_FLAG_CAPACITY) return;
@@ -628,6 +642,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
   // fast_delta: every edge r of the sub-window is >= 2 l (and l < 64), so for
   // any x of the cell, r/2 <= x <= 2r and x - r is exact (Sterbenz) — no
   // TwoSum check per particle
+  if (QUEUE && t < S1_WARPS) sq.oqn[t] = 0;
   if (t == 0) {
     sm.fast_delta = (g.lx < 64.0 && g.ly < 64.0) ? 1 : 0;
     sm.fl_hkey = P.hkey;
@@ -711,6 +726,58 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
       for (int c = 0; c < 5; ++c) o[it][c] = __ldg(sinc[c] + sj);
     }
   };
+  // queued particles (outside cells): exact fire-and-forget limb reductions
+  // straight to the cell's table slot, one particle per lane; whole batches
+  // of 32 (all of them when `all`), the rest moves to the front of the queue.
+  // The state values are read back from this frame's output (written by this
+  // warp; the warp barrier orders them).
+  // a particle outside the shared sub-window: exact fire-and-forget limb
+  // reductions straight to its cell's table slot (jw: particle index, bit 31
+  // = its cell code is already written)
+  auto outside_cell = [&](u32 flat, u32 jw, const float* v) {
+    bool created;
+    const u32 slot = ht_insert(P, flat, created);
+    if (!(jw & 0x80000000u)) __stcs(P.pslot + (jw & 0x7FFFFFFFu), (u32)SUBW + slot);   // its cell code
+    if (slot != HT_EMPTY) {
+#pragma unroll
+      for (int c = 0; c < 5; ++c) tab_add_f32(tab_ptr(P, c, slot), v[c]);
+      touch_cell(P, C, slot, 1u, created);
+    } else {
+      set_flag(C, PCS_FLAG_CAPACITY);
+    }
+  };
+  constexpr bool use_q = QUEUE;
+  auto drain_outside = [&](bool all) {
+    __syncwarp();
+    const int qn = (int)sq.oqn[warp];
+    if (qn < 32 && !(all && qn > 0)) return;   // (warp-uniform)
+    int done = 0;
+    while (qn - done >= 32 || (all && done < qn)) {
+      if (done + lane < qn) {
+        const u32 flat = sq.oq[warp][done + lane][0], jw = sq.oq[warp][done + lane][1];
+        const u32 pj = jw & 0x7FFFFFFFu;
+        float v[5];
+#pragma unroll
+        for (int c = 0; c < 5; ++c) v[c] = __ldcg(soutc[c] + pj);
+        outside_cell(flat, jw, v);
+      }
+      done += 32;
+    }
+    done = min(done, qn);
+    const int left = qn - done;
+    u32 e0 = 0, e1 = 0;
+    if (lane < left) {
+      e0 = sq.oq[warp][done + lane][0];
+      e1 = sq.oq[warp][done + lane][1];
+    }
+    __syncwarp();
+    if (lane < left) {
+      sq.oq[warp][lane][0] = e0;
+      sq.oq[warp][lane][1] = e1;
+    }
+    if (lane == 0) sq.oqn[warp] = (u32)left;
+    __syncwarp();
+  };
   load_src(jb0, je0, src_k);
 #if PCS_S1_DEEP
   load_states(src_k, o_k);
@@ -769,20 +836,25 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
         o[1] = dy;
         s1_add(dig, qs, o_k[it]);
       } else {
-        // outside the shared sub-window: exact fire-and-forget limb
-        // reductions straight to the cell's table slot
-        bool created;
-        const u32 slot = ht_insert(P, flat, created);
-        if (!inwin) __stcs(P.pslot + j, (u32)SUBW + slot);   // cell code of an outside cell
-        if (slot != HT_EMPTY) {
-#pragma unroll
-          for (int c = 0; c < 5; ++c) tab_add_f32(tab_ptr(P, c, slot), o[c]);
-          touch_cell(P, C, slot, 1u, created);
+        // outside the shared sub-window (frame 0 of a track: ~9 % of the wide
+        // initial cloud), or values beyond the digit range: queued per warp
+        // and handled 32 at a time at the end of the chunk, instead of every
+        // warp iteration running that path for two or three lanes. The
+        // lanes here together reserve their entries (warp-aggregated atomic).
+        if (use_q) {   // (CTA-uniform)
+          const unsigned m = __activemask();
+          const int leader = __ffs(m) - 1;
+          u32 qb = 0;
+          if (lane == leader) qb = atomicAdd(&sq.oqn[warp], (u32)__popc(m));
+          qb = __shfl_sync(m, qb, leader) + (u32)__popc(m & ((1u << lane) - 1u));
+          sq.oq[warp][qb][0] = flat;
+          sq.oq[warp][qb][1] = (u32)j | (inwin ? 0x80000000u : 0u);
         } else {
-          set_flag(C, PCS_FLAG_CAPACITY);
+          outside_cell(flat, (u32)j | (inwin ? 0x80000000u : 0u), o);
         }
       }
     }
+    if (use_q) drain_outside(false);
     jb0 = jb1; je0 = je1;
 #if PCS_S1_DEEP
     jb1 = jb2; je1 = je2;
@@ -799,6 +871,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
     next_chunk(jb1, je1);
 #endif
   }
+  if (use_q) drain_outside(true);
   __syncthreads();
   if (t == 0 && atomicAdd(&C->s1_done, 1u) == gridDim.x - 1) {   // every ticket is drawn
     C->s1_ticket = 0;
@@ -1896,5 +1969,6 @@ __global__ void __launch_bounds__(256) k_multinomial_emit(TrackParams P) {
 }
 
 constexpr size_t S1_SMEM = sizeof(S1Smem);
+constexpr size_t S1_SMEM_Q = sizeof(S1Smem) + sizeof(S1Queue);   // k_pc_step1<., true>
 
 }  // namespace pcs
