@@ -1499,8 +1499,13 @@ int pcs_shard_step1(pcs_ctx* ctx, const float* frame, int64_t k, double* est, do
   cudaStream_t st = S(stream);
   TrackState& T = ctx->tr;
   k_ctl_io<<<1, 1, 0, st>>>(T.P.ctl, frame, k, k, k + 1, est, ess, res, (i64*)occ);
-  if (T.s1_pow2) k_pc_step1<true><<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(T.P);
-  else k_pc_step1<false><<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(T.P);
+  if (k == 0) {   // (the track's first frame: the queued form, as enqueue_frame)
+    if (T.s1_pow2) k_pc_step1<true, true><<<T.s1_grid, S1_THREADS, S1_SMEM_Q, st>>>(T.P);
+    else k_pc_step1<false, true><<<T.s1_grid, S1_THREADS, S1_SMEM_Q, st>>>(T.P);
+  } else {
+    if (T.s1_pow2) k_pc_step1<true><<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(T.P);
+    else k_pc_step1<false><<<T.s1_grid, S1_THREADS, S1_SMEM, st>>>(T.P);
+  }
   k_shard_bbox<<<1, 1024, 0, st>>>(T.P, (i64*)box);
   PCS_LAUNCH_CHECK();
   return PCS_OK;
