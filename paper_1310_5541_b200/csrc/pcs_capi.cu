@@ -1110,6 +1110,10 @@ static int track_begin(pcs_ctx* ctx, const pcs_track_cfg_t* cfg, int64_t H, int6
   T.s1_grid = (int)std::min<i64>((i64)ctx->sms * S1_CTAS_PER_SM, std::max<i64>(1, ceil_div(n, (i64)S1_THREADS * 4)));
   T.cells_grid = ctx->sms * 4;
   T.s1_pow2 = cfg->method == 1 && grid_pow2(P.grid.ox, P.grid.lx, P.grid.oy, P.grid.ly);
+  P.ht_shift = -1;   // bit-slice table hash when the grid has 2^k columns
+  if (getenv("PCS_HT_MULT") == nullptr)
+    for (int b = 0; b < 31; ++b)
+      if (P.grid.ncols == ((i64)1 << b)) P.ht_shift = b;
   {
     // equal tile counts per warp: tile = ceil(per_warp / ceil(per_warp / S1_MAX_WT))
     const i64 per_warp = ceil_div(n, (i64)T.s1_grid * S1_WARPS);

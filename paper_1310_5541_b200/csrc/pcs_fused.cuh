@@ -79,6 +79,7 @@ struct S1Smem {
   int fast_delta;
   // table pointers for the out-of-line cell flush (read only on that path)
   u32* fl_hkey;
+  int fl_shift;
   u64* fl_tab_sum;
   u32* fl_occ;
   i64 fl_G;
@@ -171,6 +172,7 @@ struct TrackParams {
                              // replaces it by exp(ll - max) for the rest of the frame
   u32* pslot;                // pcSIR: cell code per particle (pslot_code below)
   u32* hkey;                 // [G] flat cell id of each table slot (HT_EMPTY: free)
+  int ht_shift;              // log2(columns) when that is a power of two (bit-slice hash), else -1
   u32* tab_cnt;              // [G]   members per slot
   u64* tab_sum;              // [5][G][2] exact int128 sums (step-1 flushes, shard import)
   u64* tab_lim;              // [5][G][3] limb sums (step-1 single particles, tab_add)
@@ -377,10 +379,17 @@ __device__ __forceinline__ float cell_ref32(double origin, double cell, i64 i, b
 // table slot of flat cell id `flat` (inserted if absent; HT_EMPTY if the
 // table is full): Fibonacci hash, linear probing; keys only go from empty to
 // a cell id within a frame (the bins kernel clears the occupied slots)
-__device__ __forceinline__ u32 ht_hash(u32 flat) { return (flat * 0x9E3779B1u) >> (32 - HT_BITS); }
+// (sh >= 0: the grid has 2^sh columns — the slot is a bit slice of (row,
+// column), so the cells of a cloud never collide and neighbouring cells get
+// neighbouring slots: the weight lookups of the particles outside the
+// sub-window, frame 0 of a track, then share sectors and lines)
+__device__ __forceinline__ u32 ht_hash(u32 flat, int sh) {
+  if (sh >= 0) return (((flat >> sh) & ((HT_CAP >> 11) - 1u)) << 11) | (flat & 2047u);
+  return (flat * 0x9E3779B1u) >> (32 - HT_BITS);
+}
 __device__ __forceinline__ u32 ht_insert(const TrackParams& P, u32 flat, bool& created) {
   created = false;
-  u32 s = ht_hash(flat);
+  u32 s = ht_hash(flat, P.ht_shift);
   for (u32 probe = 0; probe < HT_CAP; ++probe) {
     const u32 k = __ldcg(P.hkey + s);
     if (k == flat) return s;
@@ -398,7 +407,7 @@ __device__ __forceinline__ u32 ht_insert(const TrackParams& P, u32 flat) {
   return ht_insert(P, flat, created);
 }
 __device__ __forceinline__ u32 ht_find(const TrackParams& P, u32 flat) {
-  u32 s = ht_hash(flat);
+  u32 s = ht_hash(flat, P.ht_shift);
   for (u32 probe = 0; probe < HT_CAP; ++probe) {
     const u32 k = __ldcg(P.hkey + s);
     if (k == flat) return s;
@@ -501,9 +510,9 @@ __device__ __forceinline__ bool delta_exact(float v, float ref, float& s) {
 
 // table slot of flat cell id `flat` in the hash-key array (ht_insert without
 // the TrackParams, for the out-of-line cell flush)
-__device__ __forceinline__ u32 ht_insert_k(u32* hkey, u32 flat, bool& created) {
+__device__ __forceinline__ u32 ht_insert_k(u32* hkey, u32 flat, int sh, bool& created) {
   created = false;
-  u32 s = ht_hash(flat);
+  u32 s = ht_hash(flat, sh);
   for (u32 probe = 0; probe < HT_CAP; ++probe) {
     const u32 k = __ldcg(hkey + s);
     if (k == flat) return s;
@@ -534,8 +543,8 @@ __device__ __forceinline__ i128 s1_digits(u32 d0, u32 d1, u32 d2) {
 // exchange (additions racing with it land either in the taken value or in
 // the accumulator, never in both), so no other warp has to stop. The count
 // and the cell-edge offsets stay for the final flush.
-__device__ __noinline__ void s1_cell_flush(u32* dig, int q, u32 flat, u32* hkey, u64* tab_sum, i64 G,
-                                           u32* occ, TrackCtl* C) {
+__device__ __noinline__ void s1_cell_flush(u32* dig, int q, u32 flat, u32* hkey, int ht_shift,
+                                           u64* tab_sum, i64 G, u32* occ, TrackCtl* C) {
   i128 s[5];
 #pragma unroll
   for (int c = 0; c < 5; ++c) {
@@ -545,7 +554,7 @@ __device__ __noinline__ void s1_cell_flush(u32* dig, int q, u32 flat, u32* hkey,
     s[c] = s1_digits(d0, d1, d2);
   }
   bool created;
-  const u32 slot = ht_insert_k(hkey, flat, created);
+  const u32 slot = ht_insert_k(hkey, flat, ht_shift, created);
   if (slot == HT_EMPTY) {
     set_flag(C, PCS_FLAG_CAPACITY);
     return;
@@ -646,6 +655,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
   if (t == 0) {
     sm.fast_delta = (g.lx < 64.0 && g.ly < 64.0) ? 1 : 0;
     sm.fl_hkey = P.hkey;
+    sm.fl_shift = P.ht_shift;
     sm.fl_tab_sum = P.tab_sum;
     sm.fl_occ = P.occ;
     sm.fl_G = P.G;
@@ -831,7 +841,7 @@ __global__ void __launch_bounds__(S1_THREADS, S1_CTAS_PER_SM) k_pc_step1(TrackPa
         const int qs = s1_swz(ly * snxi + lx);
         const u32 old = atomicAdd(&sm.cnt[qs], 1u);
         if (((old + 1u) & (S1_CELL_FLUSH - 1u)) == 0u)
-          s1_cell_flush(dig, qs, flat, sm.fl_hkey, sm.fl_tab_sum, sm.fl_G, sm.fl_occ, C);
+          s1_cell_flush(dig, qs, flat, sm.fl_hkey, sm.fl_shift, sm.fl_tab_sum, sm.fl_G, sm.fl_occ, C);
         o[0] = dx;
         o[1] = dy;
         s1_add(dig, qs, o_k[it]);
