@@ -157,6 +157,30 @@ def test_fused_pcsir_equals_general(cuda, cpp, placement):
     assert rmse < 0.75
 
 
+@pytest.mark.parametrize("mult", [False, True])
+def test_fused_pcsir_both_table_hashes(cuda, mult, monkeypatch):
+    # the cell table's slot hash: the bit slice of (row, column) on grids with
+    # 2^k columns, else (or with PCS_HT_MULT) the multiplicative hash with
+    # linear probing. A wide cloud on fine cells puts many cells outside the
+    # step-1 sub-window, so the first frame's queued form, the per-slot tables
+    # and the resampler's lookups all go through it. Same results either way.
+    if mult:
+        monkeypatch.setenv("PCS_HT_MULT", "1")
+    frames, truth, init, dyn = _c1_like(k=4)
+    n = 60_000
+    g = pc.BinGrid(-0.5, -0.5, 0.125, 0.125, 512, 512)   # 64 px / 0.125 px = 2^9 columns
+    a = pc.pcsir_track(frames, pc.PcFilterConfig(n, init, dyn, RES, _lik(), grid=g),
+                       pc.PhiloxRng(6), fused=True)
+    b = pc.pcsir_track(frames, pc.PcFilterConfig(n, init, dyn, RES, _lik(), grid=g),
+                       pc.PhiloxRng(6), fused=False)
+    assert a.path == "fused" and b.path == "general"
+    assert a.likelihood_evals > 4 * 1100     # more occupied cells than the 32 x 32 sub-window
+    assert np.array_equal(a.estimates, b.estimates)
+    assert np.array_equal(a.ess, b.ess)
+    assert np.array_equal(a.resampled, b.resampled)
+    assert a.likelihood_evals == b.likelihood_evals
+
+
 def test_fused_sir_equals_general(cuda):
     frames, truth, init, dyn = _c1_like()
     a = pc.sir_track(frames, pc.FilterConfig(2000, init, dyn, RES, _lik()), pc.PhiloxRng(9),
