@@ -68,7 +68,9 @@ constexpr int MAXM = 1 << 20;                  // occupied cells per frame (fuse
 // them into the int128 HBM table at the end (s1_flush) and a cell whose count
 // crosses a multiple of S1_CELL_FLUSH is folded on the spot (s1_cell_flush).
 // Particles outside the sub-window add to the table directly (limb
-// reductions).
+// reductions) — on the spot in the steady-state instantiation, from a
+// per-warp queue, 32 per batch, in the one the first frame of a track runs
+// (QUEUE; the initial cloud is usually wider than the sub-window).
 constexpr int S1_CHUNK = 32 * S1_IPT;          // particles per warp pipeline step
 constexpr int S1_OQ = 32 + S1_CHUNK;           // queue entries per warp (< 32 left + one chunk)
 struct S1Smem {
