@@ -319,7 +319,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
       propagate_one(s, z, P.dyn, o_k[it]);
       const float* o = o_k[it];
 #pragma unroll
-      for (int c = 0; c < 5; ++c) sout[c * ld + base_i + j] = o[c];
+      for (int c = 0; c < 5; ++c) __stcs(sout + c * ld + base_i + j, o[c]);   // (read next frame: > L2)
       if (!(o[0] == o[0]) || !(o[1] == o[1])) bad = true;
       const int ix = pow2 ? cell_axis_hot<true>(o[0], axx) : cell_axis_hot<false>(o[0], axx);
       const int iy = pow2 ? cell_axis_hot<true>(o[1], axy) : cell_axis_hot<false>(o[1], axy);
@@ -789,7 +789,7 @@ __global__ void __launch_bounds__(MT_THREADS, PCS_MT_CTAS) k_mt_frame(MtParams P
       const int cm = min(CT, m_slots - c0);
       int* out = P.anc + base_i + tj0 + c0;
       const int ib = (int)base;
-      for (int kk = t; kk < cm; kk += MT_THREADS) out[kk] = ib + stage[kk];
+      for (int kk = t; kk < cm; kk += MT_THREADS) __stcs(out + kk, ib + stage[kk]);   // (evict-first)
       carry = total;
       __syncthreads();
     }
