@@ -38,8 +38,11 @@ namespace pcs {
 #define PCS_MT_THREADS 512
 #endif
 constexpr int MT_THREADS = PCS_MT_THREADS;
-constexpr int MT_IPT = 2;
-constexpr int MT_TILE = MT_THREADS * MT_IPT;   // 1024
+#ifndef PCS_MT_IPT
+#define PCS_MT_IPT 1   // (1 / 2 / 3 particles per thread and tile: c4 11.93 / 12.21 / 13.22 ms)
+#endif
+constexpr int MT_IPT = PCS_MT_IPT;
+constexpr int MT_TILE = MT_THREADS * MT_IPT;   // 512
 constexpr int MT_WARPS = MT_THREADS / 32;
 constexpr int MT_SIDE = 24;
 constexpr int MT_SUBW = MT_SIDE * MT_SIDE;     // sub-window cells (24 x 24)
@@ -59,7 +62,7 @@ constexpr int MT_CT = MT_THREADS * MT_CI;      // phase C: 4608 particles per sc
 // V = round(v 2^40) (|V| < 2^47): bits 0-13, 14-27, 28-41 (< 2^14 each) and
 // V >> 42 (signed, |.| <= 2^5), so n <= 2^18 particles per target keep every
 // 32-bit accumulator in range
-constexpr int MT_MAX_TILES = 256;   // n <= MT_MAX_TILES * MT_TILE = 2^18
+constexpr int MT_MAX_TILES = (1 << 18) / MT_TILE;   // n <= MT_MAX_TILES * MT_TILE = 2^18
 constexpr int MT_DIG = 20;          // 5 components x 4 digits
 constexpr u64 MT_KEY_STEP = 0x9E3779B97F4A7C15ull;
 
