@@ -56,8 +56,11 @@ constexpr int MT_MARGIN = PCS_MT_MARGIN;       // sub-window cells beyond the pr
 constexpr int MT_HCAP = 2048;                  // per-target outlier hash capacity
 constexpr int MT_MAXM = 2048;                  // occupied cells per target per frame
 constexpr int MT_STAGE = 4096;                 // staged frame pixels
-constexpr int MT_CI = 9;                       // phase C: items per thread (odd stride: conflict-free)
-constexpr int MT_CT = MT_THREADS * MT_CI;      // phase C: 4608 particles per scan tile
+#ifndef PCS_MT_CI
+#define PCS_MT_CI 11   // (7 / 9 / 11: c4 12.10 / 11.95 / 11.81 ms; 13 would not fit two CTAs per SM)
+#endif
+constexpr int MT_CI = PCS_MT_CI;                       // phase C: items per thread (odd stride: conflict-free)
+constexpr int MT_CT = MT_THREADS * MT_CI;      // phase C: 5632 particles per scan tile
 // phase A digit accumulators: one addition per particle of each digit of
 // V = round(v 2^40) (|V| < 2^47): bits 0-13, 14-27, 28-41 (< 2^14 each) and
 // V >> 42 (signed, |.| <= 2^5), so n <= 2^18 particles per target keep every
